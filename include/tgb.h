@@ -1,0 +1,116 @@
+/* tgb.h — C ABI of the B200-native tengrid hot path.
+ *
+ * Drop-in boundary for the canonical/Tucker Newton-kernel convolution path of
+ * the reference library `tengrid` (/root/reference/proj).  Each entry point
+ * names the reference function it replaces.  All matrices are column-major
+ * (Eigen's default layout: entry (i, j) at p[i + rows * j]) so an
+ * Eigen::MatrixXd::data() pointer can be passed straight through.
+ *
+ * Memory: every call takes `mem` = TGB_MEM_HOST or TGB_MEM_DEVICE and ALL
+ * pointers of that call live in that space.  Host calls stage through the
+ * context's device workspace (host<->device copies are part of the call);
+ * device calls are stream-ordered on the context stream and return without a
+ * device synchronisation unless a result is a host scalar.  Buffers are
+ * caller-allocated and nothing is retained past the call.
+ *
+ * Errors: return code 0 ok, 1 invalid_argument, 2 domain_error, 3 snap error,
+ * 4 numerical error, 5 CUDA/NCCL error; tgb_last_error() gives a per-thread
+ * message.  The C++ wrapper (include/tengrid_b200/tengrid.hpp) rethrows the
+ * reference's exception types (common.hpp:11-25).
+ */
+#ifndef TGB_H
+#define TGB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TGB_OK 0
+#define TGB_INVALID_ARGUMENT 1
+#define TGB_DOMAIN_ERROR 2
+#define TGB_SNAP_ERROR 3
+#define TGB_NUMERICAL_ERROR 4
+#define TGB_CUDA_ERROR 5
+
+#define TGB_MEM_HOST 0
+#define TGB_MEM_DEVICE 1
+
+typedef struct tgb_ctx tgb_ctx;
+
+/* Rank-R canonical tensor sum_k w_k u_k^(1) x u_k^(2) x u_k^(3)
+ * (reference CanonicalTensor3, proj/include/tengrid/tensor.hpp:119-150). */
+typedef struct tgb_cp {
+  int64_t n[3];      /* extent per axis */
+  int64_t rank;      /* R */
+  double* factor[3]; /* n[ax] x R, column-major */
+  double* weight;    /* R */
+} tgb_cp;
+
+/* ---- context -------------------------------------------------------------
+ * One CUDA stream per context (`stream` = a cudaStream_t, or NULL for a
+ * context-owned stream).  Calls are reentrant across contexts. */
+int tgb_ctx_create(int device, void* stream, tgb_ctx** out);
+int tgb_ctx_destroy(tgb_ctx* ctx);
+void* tgb_ctx_stream(tgb_ctx* ctx);
+int tgb_ctx_synchronize(tgb_ctx* ctx);
+const char* tgb_last_error(void);
+/* Kernel launches issued by this context since creation (or the last reset). */
+int64_t tgb_ctx_launch_count(tgb_ctx* ctx);
+void tgb_ctx_reset_launch_count(tgb_ctx* ctx);
+/* Tuning / testing knob: 1D convolutions with n <= direct_max use direct
+ * summation (reference: kFftConvThreshold = 128, fft.hpp:13).  Default 64;
+ * 0 forces the FFT path wherever it exists. */
+int tgb_ctx_set_direct_max(tgb_ctx* ctx, int64_t direct_max);
+
+/* ---- mode convolutions -----------------------------------------------------
+ * replaces tg::conv_central_many (proj/include/tengrid/fft.hpp:30,
+ * proj/src/fft.cpp:97-122): out(:, c) = central_window(conv_full(U(:, c), v)). */
+int tgb_conv_central_many(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out,
+                          int mem);
+
+/* replaces tg::convolve(a, b, h) (tensor.hpp:185-186, tensor.cpp:179-198).
+ * `out` must have rank a.rank * b.rank; column i + a.rank * j of every factor
+ * is h[ax] * conv_central(a_i, b_j); weight = a.w[i] * b.w[j]. */
+int tgb_convolve(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double h[3], tgb_cp* out, int mem);
+
+/* replaces tg::hartree_potential (hf.hpp:34-39, hf.cpp:131-138):
+ * convolve(theta, kernel with weights / (h0 h1 h2), h).  `kernel` must be a
+ * primary-grid kernel tensor (doubled kernels are rejected by the caller). */
+int tgb_hartree_potential(tgb_ctx* ctx, const tgb_cp* theta, const tgb_cp* kernel, const double h[3], tgb_cp* out,
+                          int mem);
+
+/* replaces CanonicalTensor3::value_at (tensor.hpp:135-140) for a batch of
+ * grid points: out[p] = sum_k w_k f0(i_p,k) f1(j_p,k) f2(l_p,k); ijk is
+ * npts x 3 (row-major triples), both in the space given by `mem`. */
+int tgb_value_at(tgb_ctx* ctx, const tgb_cp* t, int64_t npts, const int64_t* ijk, double* out, int mem);
+
+/* ---- assembly --------------------------------------------------------------
+ * replaces tg::scalar_product(CanonicalTensor3, CanonicalTensor3)
+ * (tensor.hpp:173, tensor.cpp:88-98).  Result written to *result (host). */
+int tgb_scalar_product(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, double* result, int mem);
+
+/* replaces tg::coulomb_matrix (hf.hpp:41-44, hf.cpp:140-151):
+ * J_km = h0 h1 h2 <G_k . G_m, V_H> for k <= m, mirrored.  The basis is given
+ * flattened: `basis` holds all primitives of all functions as one CP tensor
+ * (rank = total primitives, weights = contraction coeff * primitive norm),
+ * fn_offset[k] .. fn_offset[k+1]-1 are the primitives of function k
+ * (nb + 1 entries, host memory).  J is nb x nb (space given by `mem`). */
+int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
+                       const double h[3], double* J, int mem);
+
+/* ---- lattice sums ------------------------------------------------------------
+ * replaces the per-axis assembly of tg::lattice_sum_canonical / _tucker /
+ * _composite (lattice.hpp:56-69, lattice.cpp:50-61,116-165):
+ * out(:, q) = sum_{l < L} ref(offsets[l] : offsets[l] + n, q), summed in
+ * lattice-index order l = 0..L-1 (bit-identical to the reference).
+ * ref is (2n) x R; offsets (host memory) come from tg::window_offset. */
+int tgb_lattice_assemble_axis(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets,
+                              int64_t L, double* out, int mem);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TGB_H */

@@ -1,0 +1,13 @@
+"""B200-native hot path of the tengrid Newton-kernel convolution stack
+(arXiv 1504.06289): mode convolutions, J/TEI assembly, rank reduction and
+lattice sums behind the reference's API.  See DESIGN.md."""
+from ._lib import (CudaError, DomainError, InvalidArgument, NumericalError, SnapError, TengridError,
+                   exported_symbols, lib)
+from .tengrid import (AssembledPotential, BasisSet, CanonicalTensor3, Context, DeviceCP, ExpSum, GaussianPrimitive,
+                      Grid3, KernelTensor, LatticeSpec, SeparableBasisFunction, add, conv_central_many,
+                      convolve, coulomb_matrix, default_context, discretize_basis, flatten_basis,
+                      gauss_cell_integral, hadamard, hartree_potential, kernel_tensor, lattice_assemble_axis,
+                      lattice_offsets, lattice_sum_canonical, make_expsum, make_grid, primitive_norm, scalar_product,
+                      scale, snap_to_node, value_at_points, window_offset)
+
+__all__ = [n for n in dir() if not n.startswith("_")]

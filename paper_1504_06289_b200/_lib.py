@@ -1,0 +1,112 @@
+"""ctypes binding of libtgb.so (include/tgb.h, include/tgb_host.h).
+
+The library is loaded from the package directory (built in-tree by
+build.py).  There is no fallback: if libtgb.so is missing or the GPU is not
+an sm_100 device, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+_HERE = Path(__file__).resolve().parent
+LIB_PATH = _HERE / "libtgb.so"
+
+
+class TengridError(Exception):
+    """Base of the mapped reference exception types."""
+
+
+class InvalidArgument(TengridError, ValueError):
+    """std::invalid_argument (tg::require, common.hpp:23-25)."""
+
+
+class DomainError(TengridError, ValueError):
+    """std::domain_error (grid.cpp:25, basis.cpp:22)."""
+
+
+class SnapError(TengridError, RuntimeError):
+    """tg::SnapError (common.hpp:11-15)."""
+
+
+class NumericalError(TengridError, RuntimeError):
+    """tg::NumericalError (common.hpp:17-21)."""
+
+
+class CudaError(TengridError, RuntimeError):
+    """CUDA / NCCL failure inside libtgb."""
+
+
+_CODES = {1: InvalidArgument, 2: DomainError, 3: SnapError, 4: NumericalError, 5: CudaError}
+
+MEM_HOST = 0
+MEM_DEVICE = 1
+
+
+class tgb_cp(C.Structure):
+    _fields_ = [("n", C.c_int64 * 3), ("rank", C.c_int64), ("factor", C.c_void_p * 3), ("weight", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise CudaError(f"libtgb.so not built ({LIB_PATH}); run __graft_entry__.build()")
+        L = C.CDLL(str(LIB_PATH))
+        P, I64, D, I = C.c_void_p, C.c_int64, C.c_double, C.c_int
+        sig = {
+            "tgb_ctx_create": (I, [I, P, C.POINTER(P)]),
+            "tgb_ctx_destroy": (I, [P]),
+            "tgb_ctx_stream": (P, [P]),
+            "tgb_ctx_synchronize": (I, [P]),
+            "tgb_last_error": (C.c_char_p, []),
+            "tgb_ctx_launch_count": (I64, [P]),
+            "tgb_ctx_reset_launch_count": (None, [P]),
+            "tgb_ctx_set_direct_max": (I, [P, I64]),
+            "tgb_conv_central_many": (I, [P, I64, I64, P, P, P, I]),
+            "tgb_convolve": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),
+            "tgb_hartree_potential": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),
+            "tgb_value_at": (I, [P, C.POINTER(tgb_cp), I64, P, P, I]),
+            "tgb_scalar_product": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), C.POINTER(D), I]),
+            "tgb_coulomb_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, P, I]),
+            "tgb_lattice_assemble_axis": (I, [P, I64, I64, P, P, I64, P, I]),
+            "tgb_host_last_error": (C.c_char_p, []),
+            "tgb_mesh_size": (D, [D, I64]),
+            "tgb_snap_to_node": (I, [D, I64, D, C.POINTER(I64)]),
+            "tgb_window_offset": (I, [D, I64, D, C.POINTER(I64)]),
+            "tgb_make_expsum": (I, [I64, D, D, D, P, P, C.POINTER(D), C.POINTER(D)]),
+            "tgb_kernel_factors": (I, [D, I64, I64, P, P, I, P]),
+            "tgb_gauss_cell_integral": (D, [D, D, D]),
+            "tgb_primitive_norm": (I, [D, I, C.POINTER(D)]),
+            "tgb_gaussian_factor": (I, [D, I64, D, D, I, P]),
+        }
+        for name, (res, args) in sig.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def check(rc: int, host: bool = False) -> None:
+    if rc == 0:
+        return
+    msg = (lib().tgb_host_last_error() if host else lib().tgb_last_error()) or b""
+    raise _CODES.get(rc, TengridError)(msg.decode(errors="replace"))
+
+
+EXPORTED_SYMBOLS = None  # filled lazily by exported_symbols()
+
+
+def exported_symbols() -> list[str]:
+    """Every function declared in include/tgb.h and include/tgb_host.h."""
+    import re
+
+    names = []
+    for h in ("tgb.h", "tgb_host.h"):
+        text = (_HERE.parent / "include" / h).read_text()
+        names += re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(tgb_[a-z_0-9]+)\s*\(", text, re.M)
+    return sorted(set(names))

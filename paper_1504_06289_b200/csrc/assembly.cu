@@ -1,0 +1,251 @@
+// Separable assembly kernels on sm_100a:
+//  * scalar products of canonical tensors and the Coulomb matrix J
+//    (reference tensor.cpp:88-98, hf.cpp:140-151): one fused kernel computes,
+//    for a batch of "left" columns p (a single factor column, or the Hadamard
+//    product of two basis columns formed on the fly), the per-axis inner
+//    products with every right column q, multiplies the three axes, weights
+//    by w_q and reduces over the q tile.  Per-q-tile partials are reduced in
+//    a fixed order (deterministic, no atomics).
+//  * lattice window assembly (lattice.cpp:50-61), summed in lattice order so
+//    the result is bit-identical to the reference.
+//  * batched value_at probes (tensor.hpp:135-140).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "tgb_internal.hpp"
+
+namespace tgb {
+
+namespace {
+
+constexpr int TP = 64;   // left columns per CTA
+constexpr int TQ = 64;   // right columns per CTA
+constexpr int TK = 16;   // grid points per smem stage
+constexpr int NTH = 256; // 16 x 16 threads, 4 x 4 micro-tile each
+
+struct SepArgs {
+  int64_t n[3];
+  const double* F[3];   // left factor matrices (n x nf)
+  const double* B[3];   // right factor matrices (n x R_B)
+  const int* i0;        // left column p = F(:, i0[p]) (* F(:, i1[p]) if i1[p] >= 0)
+  const int* i1;
+  const double* wb;     // right weights
+  int P, RB;
+};
+
+__global__ void __launch_bounds__(NTH) sep_inner_kernel(SepArgs a, double* __restrict__ partial) {
+  __shared__ double As[TK][TP + 1];
+  __shared__ double Bs[TK][TQ + 1];
+  const int p0 = blockIdx.x * TP, q0 = blockIdx.y * TQ;
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // ty: p micro-row, tx: q micro-col
+  double prod[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) prod[i][j] = 1.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    const int64_t n = a.n[ax];
+    const double* F = a.F[ax];
+    const double* B = a.B[ax];
+    double acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+    for (int64_t k0 = 0; k0 < n; k0 += TK) {
+      // stage A (TK x TP) and B (TK x TQ); consecutive threads walk the grid index
+      for (int e = threadIdx.x; e < TK * TP; e += NTH) {
+        const int kk = e % TK, pp = e / TK;
+        const int64_t k = k0 + kk;
+        const int p = p0 + pp;
+        double v = 0.0;
+        if (k < n && p < a.P) {
+          const int c0 = a.i0[p], c1 = a.i1[p];
+          v = F[c0 * n + k];
+          if (c1 >= 0) v *= F[c1 * n + k];
+        }
+        As[kk][pp] = v;
+      }
+      for (int e = threadIdx.x; e < TK * TQ; e += NTH) {
+        const int kk = e % TK, qq = e / TK;
+        const int64_t k = k0 + kk;
+        const int q = q0 + qq;
+        Bs[kk][qq] = (k < n && q < a.RB) ? B[static_cast<int64_t>(q) * n + k] : 0.0;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < TK; ++kk) {
+        double av[4], bv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) prod[i][j] *= acc[i][j];
+  }
+  // weighted row sums over this q tile, reduced across the 16 tx lanes
+  __shared__ double red[TP][17];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int q = q0 + tx + 16 * j;
+      if (q < a.RB) s += a.wb[q] * prod[i][j];
+    }
+    red[ty + 16 * i][tx] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < TP) {
+    double s = 0.0;
+    for (int t = 0; t < 16; ++t) s += red[threadIdx.x][t];
+    const int p = p0 + threadIdx.x;
+    if (p < a.P) partial[static_cast<int64_t>(blockIdx.y) * a.P + p] = s;
+  }
+}
+
+__global__ void reduce_tiles_kernel(const double* __restrict__ partial, int ntiles, int P, double* __restrict__ s) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  double acc = 0.0;
+  for (int t = 0; t < ntiles; ++t) acc += partial[static_cast<int64_t>(t) * P + p];
+  s[p] = acc;
+}
+
+// s[p] = sum_q wb[q] prod_ax <left_p^ax, B_q^ax>, returned to the host.
+std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* const F[3], const double* const B[3],
+                              const double* wb, int RB, const std::vector<int>& i0, const std::vector<int>& i1) {
+  const int P = static_cast<int>(i0.size());
+  std::vector<double> s(P, 0.0);
+  if (P == 0 || RB == 0) return s;
+  auto* idx = static_cast<int*>(ctx->ws_misc.get(2 * P * sizeof(int)));
+  TGB_CUDA(cudaMemcpyAsync(idx, i0.data(), P * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  TGB_CUDA(cudaMemcpyAsync(idx + P, i1.data(), P * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  const int ntq = (RB + TQ - 1) / TQ;
+  auto* partial = static_cast<double*>(ctx->ws_misc2.get(static_cast<size_t>(ntq) * P * sizeof(double) + P * sizeof(double)));
+  double* dsum = partial + static_cast<size_t>(ntq) * P;
+  SepArgs a;
+  for (int ax = 0; ax < 3; ++ax) {
+    a.n[ax] = n[ax];
+    a.F[ax] = F[ax];
+    a.B[ax] = B[ax];
+  }
+  a.i0 = idx;
+  a.i1 = idx + P;
+  a.wb = wb;
+  a.P = P;
+  a.RB = RB;
+  dim3 grid((P + TP - 1) / TP, ntq);
+  sep_inner_kernel<<<grid, NTH, 0, ctx->stream>>>(a, partial);
+  TGB_LAUNCHED(ctx);
+  reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(partial, ntq, P, dsum);
+  TGB_LAUNCHED(ctx);
+  TGB_CUDA(cudaMemcpyAsync(s.data(), dsum, P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return s;
+}
+
+__global__ void lattice_kernel(int64_t n, int64_t R, const double* __restrict__ ref, const int64_t* __restrict__ ofs,
+                               int64_t L, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t q = blockIdx.y;
+  if (i >= n) return;
+  const double* col = ref + q * 2 * n + i;
+  double acc = 0.0;
+  for (int64_t l = 0; l < L; ++l) acc += __ldg(col + ofs[l]);
+  out[q * n + i] = acc;
+}
+
+__global__ void value_at_kernel(int64_t n0, int64_t n1, int64_t n2, int64_t R, const double* __restrict__ f0,
+                                const double* __restrict__ f1, const double* __restrict__ f2,
+                                const double* __restrict__ w, int64_t npts, const int64_t* __restrict__ ijk,
+                                double* __restrict__ out) {
+  const int64_t p = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (p >= npts) return;
+  const int64_t i = ijk[3 * p], j = ijk[3 * p + 1], l = ijk[3 * p + 2];
+  double s = 0.0;
+  for (int64_t k = lane; k < R; k += 32) s += w[k] * f0[i + n0 * k] * f1[j + n1 * k] * f2[l + n2 * k];
+  for (int o = 16; o; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+  if (lane == 0) out[p] = s;
+}
+
+}  // namespace
+
+double scalar_product_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b) {
+  if (a.rank == 0 || b.rank == 0) return 0.0;  // tensor.cpp:92
+  std::vector<int> i0(a.rank), i1(a.rank, -1);
+  for (int64_t p = 0; p < a.rank; ++p) i0[p] = static_cast<int>(p);
+  const double* F[3] = {a.factor[0], a.factor[1], a.factor[2]};
+  const double* B[3] = {b.factor[0], b.factor[1], b.factor[2]};
+  std::vector<double> s = sep_inner(ctx, a.n, F, B, b.weight, static_cast<int>(b.rank), i0, i1);
+  std::vector<double> wa(a.rank);
+  TGB_CUDA(cudaMemcpy(wa.data(), a.weight, a.rank * sizeof(double), cudaMemcpyDeviceToHost));
+  double r = 0.0;
+  for (int64_t p = 0; p < a.rank; ++p) r += wa[p] * s[p];
+  return r;
+}
+
+void coulomb_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const tgb_cp& vh,
+                        double vol, double* J) {
+  std::vector<double> wprim(basis.rank);
+  if (basis.rank)
+    TGB_CUDA(cudaMemcpy(wprim.data(), basis.weight, basis.rank * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<int> i0, i1;
+  std::vector<std::pair<int64_t, int64_t>> owner;  // (k, m) per left column
+  for (int64_t k = 0; k < nb; ++k)
+    for (int64_t m = k; m < nb; ++m)
+      for (int64_t pm = fn_offset[m]; pm < fn_offset[m + 1]; ++pm)
+        for (int64_t pk = fn_offset[k]; pk < fn_offset[k + 1]; ++pk) {
+          i0.push_back(static_cast<int>(pk));
+          i1.push_back(static_cast<int>(pm));
+          owner.push_back({k, m});
+        }
+  const double* F[3] = {basis.factor[0], basis.factor[1], basis.factor[2]};
+  const double* B[3] = {vh.factor[0], vh.factor[1], vh.factor[2]};
+  std::vector<double> s;
+  if (vh.rank > 0) s = sep_inner(ctx, basis.n, F, B, vh.weight, static_cast<int>(vh.rank), i0, i1);
+  std::vector<double> acc(nb * nb, 0.0);
+  for (size_t p = 0; p < i0.size(); ++p) {
+    const double w = wprim[i0[p]] * wprim[i1[p]];
+    acc[owner[p].first + nb * owner[p].second] += vh.rank > 0 ? w * s[p] : 0.0;
+  }
+  for (int64_t k = 0; k < nb; ++k)
+    for (int64_t m = k; m < nb; ++m) {
+      J[k + nb * m] = vol * acc[k + nb * m];
+      J[m + nb * k] = J[k + nb * m];
+    }
+}
+
+void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ijk, double* out) {
+  if (npts == 0) return;
+  const int th = 256;
+  const int64_t blocks = (npts + th / 32 - 1) / (th / 32);
+  value_at_kernel<<<static_cast<unsigned>(blocks), th, 0, ctx->stream>>>(t.n[0], t.n[1], t.n[2], t.rank,
+                                                                          t.factor[0], t.factor[1], t.factor[2],
+                                                                          t.weight, npts, ijk, out);
+  TGB_LAUNCHED(ctx);
+}
+
+void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
+                          double* out) {
+  if (n == 0 || R == 0) return;
+  auto* dofs = static_cast<int64_t*>(ctx->ws_misc3.get(std::max<int64_t>(L, 1) * sizeof(int64_t)));
+  if (L) TGB_CUDA(cudaMemcpyAsync(dofs, offsets, L * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+  dim3 grid(static_cast<unsigned>((n + 255) / 256), static_cast<unsigned>(R));
+  lattice_kernel<<<grid, 256, 0, ctx->stream>>>(n, R, ref, dofs, L, out);
+  TGB_LAUNCHED(ctx);
+}
+
+}  // namespace tgb

@@ -1,0 +1,315 @@
+// extern "C" surface of libtgb (include/tgb.h).  Validation mirrors the
+// reference's require() checks so the same inputs fail with the same error
+// class; host-memory calls stage through the context workspace with
+// per-axis copy/compute overlap.
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "tgb_internal.hpp"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TGB_OK;
+  } catch (const tgb::Error& e) {
+    g_last_error = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return TGB_CUDA_ERROR;
+  }
+}
+
+void check_cp(const tgb_cp* t, const char* what) {
+  tgb::require(t != nullptr, std::string(what) + ": null tensor");
+  tgb::require(t->rank >= 0, std::string(what) + ": negative rank");
+  for (int ax = 0; ax < 3; ++ax) {
+    tgb::require(t->n[ax] >= 0, std::string(what) + ": negative extent");
+    tgb::require(t->rank == 0 || t->n[ax] == 0 || t->factor[ax] != nullptr, std::string(what) + ": null factor");
+  }
+  tgb::require(t->rank == 0 || t->weight != nullptr, std::string(what) + ": null weight");
+}
+
+void check_extents(const tgb_cp* a, const tgb_cp* b, const char* what) {
+  for (int ax = 0; ax < 3; ++ax)
+    tgb::require(a->n[ax] == b->n[ax], std::string(what) + ": extent mismatch");
+}
+
+cudaEvent_t ctx_event(tgb_ctx* ctx, size_t i) {
+  while (ctx->events.size() <= i) {
+    cudaEvent_t e;
+    TGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    ctx->events.push_back(e);
+  }
+  return ctx->events[i];
+}
+
+// convolve with optional weight scale on b (hartree_potential)
+void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double h[3], tgb_cp* out, int mem,
+                   double bscale) {
+  check_cp(a, "convolve");
+  check_cp(b, "convolve");
+  check_extents(a, b, "convolve");
+  tgb::require(h && h[0] > 0.0 && h[1] > 0.0 && h[2] > 0.0, "convolve: mesh size must be positive");
+  tgb::require(out != nullptr, "convolve: null output");
+  const int64_t ra = a->rank, rb = b->rank, r = ra * rb;
+  tgb::require(out->rank == r, "convolve: output rank must be a.rank * b.rank");
+  for (int ax = 0; ax < 3; ++ax) tgb::require(out->n[ax] == a->n[ax], "convolve: output extent mismatch");
+  TGB_CUDA(cudaSetDevice(ctx->device));
+  if (mem == TGB_MEM_DEVICE) {
+    tgb::weights_outer(ctx, ra, a->weight, rb, b->weight, bscale, out->weight);
+    for (int ax = 0; ax < 3; ++ax)
+      tgb::convolve_axis(ctx, a->n[ax], ra, a->factor[ax], rb, b->factor[ax], h[ax], out->factor[ax]);
+    return;
+  }
+  tgb::require(mem == TGB_MEM_HOST, "convolve: bad memory space");
+  for (int64_t j = 0; j < rb; ++j) {
+    const double bj = bscale != 1.0 ? b->weight[j] * bscale : b->weight[j];
+    for (int64_t i = 0; i < ra; ++i) out->weight[i + ra * j] = a->weight[i] * bj;
+  }
+  if (r == 0) return;
+  // stage: [a0 a1 a2 b0 b1 b2] inputs, [o0 o1 o2] outputs
+  size_t in_elems = 0, out_elems = 0;
+  for (int ax = 0; ax < 3; ++ax) {
+    in_elems += a->n[ax] * (ra + rb);
+    out_elems += a->n[ax] * r;
+  }
+  auto* din = static_cast<double*>(ctx->ws_in.get(in_elems * sizeof(double)));
+  auto* dout = static_cast<double*>(ctx->ws_out.get(out_elems * sizeof(double)));
+  double *da[3], *db[3], *dout_ax[3];
+  size_t off = 0, ooff = 0;
+  for (int ax = 0; ax < 3; ++ax) {
+    da[ax] = din + off;
+    off += a->n[ax] * ra;
+    db[ax] = din + off;
+    off += a->n[ax] * rb;
+    dout_ax[ax] = dout + ooff;
+    ooff += a->n[ax] * r;
+  }
+  for (int ax = 0; ax < 3; ++ax) {
+    TGB_CUDA(cudaMemcpyAsync(da[ax], a->factor[ax], a->n[ax] * ra * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    TGB_CUDA(cudaMemcpyAsync(db[ax], b->factor[ax], a->n[ax] * rb * sizeof(double), cudaMemcpyHostToDevice,
+                             ctx->stream));
+    tgb::convolve_axis(ctx, a->n[ax], ra, da[ax], rb, db[ax], h[ax], dout_ax[ax]);
+    cudaEvent_t ev = ctx_event(ctx, ax);
+    TGB_CUDA(cudaEventRecord(ev, ctx->stream));
+    TGB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev, 0));
+    TGB_CUDA(cudaMemcpyAsync(out->factor[ax], dout_ax[ax], a->n[ax] * r * sizeof(double), cudaMemcpyDeviceToHost,
+                             ctx->copy_stream));
+  }
+  TGB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// Device copy of a CP tensor (host mode helper); returns device view.
+struct DevCP {
+  tgb_cp t{};
+  std::vector<double*> bufs;
+  DevCP(const tgb_cp* h, bool on_device) {
+    t = *h;
+    if (on_device) return;
+    for (int ax = 0; ax < 3; ++ax) {
+      double* p = nullptr;
+      const size_t bytes = h->n[ax] * h->rank * sizeof(double);
+      if (bytes) {
+        TGB_CUDA(cudaMalloc(&p, bytes));
+        TGB_CUDA(cudaMemcpy(p, h->factor[ax], bytes, cudaMemcpyHostToDevice));
+      }
+      t.factor[ax] = p;
+      bufs.push_back(p);
+    }
+    double* w = nullptr;
+    if (h->rank) {
+      TGB_CUDA(cudaMalloc(&w, h->rank * sizeof(double)));
+      TGB_CUDA(cudaMemcpy(w, h->weight, h->rank * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    t.weight = w;
+    bufs.push_back(w);
+  }
+  ~DevCP() {
+    for (double* p : bufs)
+      if (p) cudaFree(p);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* tgb_last_error(void) { return g_last_error.c_str(); }
+
+int tgb_ctx_create(int device, void* stream, tgb_ctx** out) {
+  return guarded([&] {
+    tgb::require(out != nullptr, "tgb_ctx_create: null output");
+    int ndev = 0;
+    TGB_CUDA(cudaGetDeviceCount(&ndev));
+    tgb::require(device >= 0 && device < ndev, "tgb_ctx_create: no such CUDA device");
+    TGB_CUDA(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    TGB_CUDA(cudaGetDeviceProperties(&prop, device));
+    tgb::require(prop.major == 10, "tgb_ctx_create: libtgb is built for sm_100a (B200) only");
+    auto* c = new tgb_ctx();
+    c->device = device;
+    c->num_sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    if (stream) {
+      c->stream = static_cast<cudaStream_t>(stream);
+    } else {
+      TGB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+      c->own_stream = true;
+    }
+    TGB_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    *out = c;
+  });
+}
+
+int tgb_ctx_destroy(tgb_ctx* ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(ctx->copy_stream);
+    for (auto e : ctx->events) cudaEventDestroy(e);
+    cudaStreamDestroy(ctx->copy_stream);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+void* tgb_ctx_stream(tgb_ctx* ctx) { return ctx ? ctx->stream : nullptr; }
+
+int tgb_ctx_synchronize(tgb_ctx* ctx) {
+  return guarded([&] {
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  });
+}
+
+int64_t tgb_ctx_launch_count(tgb_ctx* ctx) { return ctx ? ctx->launches : 0; }
+void tgb_ctx_reset_launch_count(tgb_ctx* ctx) {
+  if (ctx) ctx->launches = 0;
+}
+
+int tgb_ctx_set_direct_max(tgb_ctx* ctx, int64_t direct_max) {
+  return guarded([&] {
+    tgb::require(direct_max >= 0, "tgb_ctx_set_direct_max: negative threshold");
+    ctx->direct_max = direct_max;
+  });
+}
+
+int tgb_conv_central_many(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out,
+                          int mem) {
+  return guarded([&] {
+    tgb::require(n >= 1, "conv_central_many: empty operand");
+    tgb::require(cols >= 0, "conv_central_many: negative column count");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::conv_central_many_dev(ctx, n, cols, U, v, out);
+      return;
+    }
+    if (cols == 0) return;
+    auto* din = static_cast<double*>(ctx->ws_in.get((cols + 1) * n * sizeof(double)));
+    auto* dout = static_cast<double*>(ctx->ws_out.get(cols * n * sizeof(double)));
+    TGB_CUDA(cudaMemcpyAsync(din, U, cols * n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    TGB_CUDA(cudaMemcpyAsync(din + cols * n, v, n * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    tgb::conv_central_many_dev(ctx, n, cols, din, din + cols * n, dout);
+    TGB_CUDA(cudaMemcpyAsync(out, dout, cols * n * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int tgb_convolve(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double h[3], tgb_cp* out, int mem) {
+  return guarded([&] { convolve_impl(ctx, a, b, h, out, mem, 1.0); });
+}
+
+int tgb_hartree_potential(tgb_ctx* ctx, const tgb_cp* theta, const tgb_cp* kernel, const double h[3], tgb_cp* out,
+                          int mem) {
+  return guarded([&] {
+    tgb::require(h && h[0] > 0.0 && h[1] > 0.0 && h[2] > 0.0, "convolve: mesh size must be positive");
+    const double inv_vol = 1.0 / (h[0] * h[1] * h[2]);  // hf.cpp:136
+    convolve_impl(ctx, theta, kernel, h, out, mem, inv_vol);
+  });
+}
+
+int tgb_value_at(tgb_ctx* ctx, const tgb_cp* t, int64_t npts, const int64_t* ijk, double* out, int mem) {
+  return guarded([&] {
+    check_cp(t, "value_at");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::value_at_dev(ctx, *t, npts, ijk, out);
+      return;
+    }
+    for (int64_t p = 0; p < npts; ++p)
+      for (int ax = 0; ax < 3; ++ax)
+        tgb::require(ijk[3 * p + ax] >= 0 && ijk[3 * p + ax] < t->n[ax], "value_at: index out of range");
+    DevCP d(t, false);
+    auto* dijk = static_cast<int64_t*>(ctx->ws_misc3.get(std::max<int64_t>(1, 3 * npts) * sizeof(int64_t)));
+    auto* dout = static_cast<double*>(ctx->ws_misc2.get(std::max<int64_t>(1, npts) * sizeof(double)));
+    TGB_CUDA(cudaMemcpyAsync(dijk, ijk, 3 * npts * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream));
+    tgb::value_at_dev(ctx, d.t, npts, dijk, dout);
+    TGB_CUDA(cudaMemcpyAsync(out, dout, npts * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int tgb_scalar_product(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, double* result, int mem) {
+  return guarded([&] {
+    check_cp(a, "scalar_product");
+    check_cp(b, "scalar_product");
+    check_extents(a, b, "scalar_product");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCP da(a, mem == TGB_MEM_DEVICE), db(b, mem == TGB_MEM_DEVICE);
+    *result = tgb::scalar_product_dev(ctx, da.t, db.t);
+  });
+}
+
+int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
+                       const double h[3], double* J, int mem) {
+  return guarded([&] {
+    check_cp(basis, "coulomb_matrix");
+    check_cp(vh, "coulomb_matrix");
+    check_extents(basis, vh, "coulomb_matrix");
+    tgb::require(nb >= 0 && fn_offset && fn_offset[0] == 0 && fn_offset[nb] == basis->rank,
+                 "coulomb_matrix: bad basis function offsets");
+    for (int64_t k = 0; k < nb; ++k) tgb::require(fn_offset[k + 1] > fn_offset[k], "coulomb_matrix: empty function");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCP db(basis, mem == TGB_MEM_DEVICE), dv(vh, mem == TGB_MEM_DEVICE);
+    std::vector<double> hj(nb * nb);
+    tgb::coulomb_matrix_dev(ctx, db.t, fn_offset, nb, dv.t, h[0] * h[1] * h[2], hj.data());
+    if (mem == TGB_MEM_DEVICE)
+      TGB_CUDA(cudaMemcpy(J, hj.data(), hj.size() * sizeof(double), cudaMemcpyHostToDevice));
+    else
+      std::memcpy(J, hj.data(), hj.size() * sizeof(double));
+  });
+}
+
+int tgb_lattice_assemble_axis(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets,
+                              int64_t L, double* out, int mem) {
+  return guarded([&] {
+    tgb::require(n >= 1 && R >= 0 && L >= 0, "lattice_assemble: bad sizes");
+    for (int64_t l = 0; l < L; ++l)
+      tgb::require(offsets[l] >= 0 && offsets[l] + n <= 2 * n, "window_offset: window escapes the doubled grid");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::lattice_assemble_dev(ctx, n, R, ref, offsets, L, out);
+      return;
+    }
+    auto* dref = static_cast<double*>(ctx->ws_in.get(std::max<int64_t>(1, 2 * n * R) * sizeof(double)));
+    auto* dout = static_cast<double*>(ctx->ws_out.get(std::max<int64_t>(1, n * R) * sizeof(double)));
+    TGB_CUDA(cudaMemcpyAsync(dref, ref, 2 * n * R * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    tgb::lattice_assemble_dev(ctx, n, R, dref, offsets, L, dout);
+    TGB_CUDA(cudaMemcpyAsync(out, dout, n * R * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,164 @@
+// Host-side input producers of the hot path (untimed, as in the reference):
+// grid geometry, sinc-quadrature Gaussian sums for 1/r and their cell-integral
+// factor columns, and sampled Gaussian basis factors.  Restated from
+// proj/src/grid.cpp:7-38, proj/src/kernel.cpp:71-123,171-203 and
+// proj/src/basis.cpp:8-46 so results are bit-identical to the reference's
+// formulas evaluated with the same libm.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tgb_internal.hpp"
+#include "tgb_host.h"
+
+namespace {
+
+constexpr double kPi = 3.14159265358979323846;
+constexpr double kSqrtPi = 1.7724538509055160273;
+
+thread_local std::string g_host_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TGB_OK;
+  } catch (const tgb::Error& e) {
+    g_host_err = e.what();
+    return e.code;
+  } catch (const std::exception& e) {
+    g_host_err = e.what();
+    return TGB_INVALID_ARGUMENT;
+  }
+}
+
+double coord(double h, int64_t n, int64_t i) { return (static_cast<double>(i) - 0.5 * static_cast<double>(n - 1)) * h; }
+double ref_coord(double h, int64_t n, int64_t j) { return (static_cast<double>(j) - static_cast<double>(n - 1)) * h; }
+
+double cell_integral(double t, double c, double h) {
+  if (t == 0.0) return h;
+  const double xl = c - 0.5 * h, xr = c + 0.5 * h;
+  const double k = kSqrtPi / (2.0 * t);
+  if (xl >= 0.0) return k * (std::erfc(t * xl) - std::erfc(t * xr));  // far-right cell: no cancellation
+  if (xr <= 0.0) return k * (std::erfc(-t * xr) - std::erfc(-t * xl));
+  return k * (std::erf(t * xr) - std::erf(t * xl));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tgb_host_last_error(void) { return g_host_err.c_str(); }
+
+double tgb_mesh_size(double b_half, int64_t n) { return 2.0 * b_half / static_cast<double>(n + 1); }
+
+int tgb_snap_to_node(double b_half, int64_t n, double x, int64_t* node) {
+  return guarded([&] {
+    const double h = tgb_mesh_size(b_half, n);
+    if (std::abs(x) > b_half) throw tgb::Error(TGB_DOMAIN_ERROR, "snap_to_node: point outside the computational box");
+    const int64_t i = static_cast<int64_t>(std::llround(x / h + 0.5 * static_cast<double>(n - 1)));
+    if (i < 0 || i >= n || std::abs(x - coord(h, n, i)) > 0.5 * h * (1.0 + 1e-12))
+      throw tgb::Error(TGB_SNAP_ERROR, "snap_to_node: point farther than h/2 from every node; refine the grid");
+    *node = i;
+  });
+}
+
+int tgb_window_offset(double b_half, int64_t n, double center, int64_t* ofs) {
+  return guarded([&] {
+    int64_t i0 = 0;
+    const int rc = tgb_snap_to_node(b_half, n, center, &i0);
+    if (rc) throw tgb::Error(rc, g_host_err);
+    const int64_t o = (n - 1) - i0;
+    tgb::require(o >= 0 && o + n <= 2 * n, "window_offset: window escapes the doubled grid");
+    *ofs = o;
+  });
+}
+
+int tgb_make_expsum(int64_t m, double c0, double fit_lo, double fit_hi, double* nodes, double* weights,
+                    double* scale_out, double* mesh_out) {
+  return guarded([&] {
+    tgb::require(m >= 1, "make_radial_expsum: need at least one quadrature point");
+    tgb::require(c0 > 0.0, "make_radial_expsum: C0 must be positive");
+    const double mesh = c0 * std::log(static_cast<double>(std::max<int64_t>(m, 2))) / static_cast<double>(m);
+    const int64_t terms = 2 * m + 1;
+    for (int64_t k = -m; k <= m; ++k) {
+      nodes[k + m] = static_cast<double>(k) * mesh;
+      weights[k + m] = 2.0 / kSqrtPi * mesh;  // Newton Laplace weight, t = 0 kept
+    }
+    const double t_max = c0 * std::log(static_cast<double>(std::max<int64_t>(m, 2)));
+    double dlo = 3.0 / t_max, dhi = kPi / (3.0 * mesh);
+    if (dhi < 2.0 * dlo) dhi = 2.0 * dlo;
+    if (fit_lo <= 0.0 || fit_hi <= 0.0) {
+      fit_lo = dlo;
+      fit_hi = dhi;
+    } else {
+      fit_lo = std::max(fit_lo, dlo);
+      fit_hi = std::min(fit_hi, dhi);
+      if (fit_lo >= fit_hi) {
+        fit_lo = dlo;
+        fit_hi = dhi;
+      }
+    }
+    double num = 0.0, den = 0.0;
+    for (int i = 0; i < 200; ++i) {
+      const double r = fit_lo * std::pow(fit_hi / fit_lo, static_cast<double>(i) / 199);
+      double f = 0.0;
+      for (int64_t k = 0; k < terms; ++k) f += weights[k] * std::exp(-nodes[k] * nodes[k] * r * r);
+      num += f * (1.0 / r);
+      den += f * f;
+    }
+    const double sc = den > 0.0 ? num / den : 1.0;
+    for (int64_t k = 0; k < terms; ++k) weights[k] *= sc;
+    *scale_out = sc;
+    *mesh_out = mesh;
+  });
+}
+
+int tgb_kernel_factors(double b_half, int64_t n, int64_t terms, const double* nodes, const double* weights,
+                       int doubled, double* factor) {
+  return guarded([&] {
+    const double h = tgb_mesh_size(b_half, n);
+    const int64_t len = doubled ? 2 * n : n;
+    for (int64_t q = 0; q < terms; ++q) {
+      const double tq = std::abs(nodes[q]);
+      const double aq = std::cbrt(weights[q]);
+      for (int64_t i = 0; i < len; ++i) {
+        const double c = doubled ? ref_coord(h, n, i) : coord(h, n, i);
+        factor[i + len * q] = aq * cell_integral(tq, c, h);
+      }
+    }
+  });
+}
+
+double tgb_gauss_cell_integral(double t, double c, double h) { return cell_integral(t, c, h); }
+
+int tgb_primitive_norm(double alpha, int l, double* out) {
+  return guarded([&] {
+    tgb::require(alpha > 0.0, "primitive_norm: exponent must be positive");
+    const double ns = std::pow(2.0 * alpha / kPi, 0.75);
+    if (l == 0) *out = ns;
+    else if (l == 1) *out = ns * 2.0 * std::sqrt(alpha);
+    else throw tgb::Error(TGB_INVALID_ARGUMENT, "primitive_norm: only s and p supported");
+  });
+}
+
+int tgb_gaussian_factor(double b_half, int64_t n, double center, double alpha, int degree, double* column) {
+  return guarded([&] {
+    if (std::abs(center) > b_half)
+      throw tgb::Error(TGB_DOMAIN_ERROR, "discretize_basis: basis center outside the computational box");
+    tgb::require(degree == 0 || degree == 1, "discretize_basis: per-axis degree must be 0 or 1");
+    tgb::require(alpha > 0.0, "discretize_basis: primitive exponent must be positive");
+    const double h = tgb_mesh_size(b_half, n);
+    for (int64_t i = 0; i < n; ++i) {
+      const double x = coord(h, n, i) - center;
+      double v = std::exp(-alpha * x * x);
+      if (degree == 1) v *= x;
+      column[i] = v;
+    }
+  });
+}
+
+}  // extern "C"

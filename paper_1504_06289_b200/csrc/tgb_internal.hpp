@@ -1,0 +1,94 @@
+// Internal plumbing of libtgb: context, error mapping, device workspace.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tgb.h"
+
+namespace tgb {
+
+// Exceptions carry the C-ABI return code (tgb.h) and map 1:1 to the
+// reference's exception types (common.hpp:11-25).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void require(bool c, const std::string& m) {
+  if (!c) throw Error(TGB_INVALID_ARGUMENT, m);
+}
+
+#define TGB_CUDA(expr)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (expr);                                                                        \
+    if (e_ != cudaSuccess)                                                                          \
+      throw ::tgb::Error(TGB_CUDA_ERROR, std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+#define TGB_LAUNCHED(ctx)                                                                           \
+  do {                                                                                              \
+    cudaError_t e_ = cudaGetLastError();                                                            \
+    if (e_ != cudaSuccess) throw ::tgb::Error(TGB_CUDA_ERROR, std::string("launch: ") + cudaGetErrorString(e_)); \
+    (ctx)->launches++;                                                                              \
+  } while (0)
+
+// Device buffer that only grows.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need > bytes) {
+      if (p) cudaFree(p);
+      p = nullptr;
+      bytes = 0;
+      if (need) {
+        cudaError_t e = cudaMalloc(&p, need);
+        if (e != cudaSuccess) throw Error(TGB_CUDA_ERROR, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+      }
+      bytes = need;
+    }
+    return p;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+struct ConvPlan;  // fftconv.cu
+
+}  // namespace tgb
+
+struct tgb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  bool own_stream = false;
+  int64_t launches = 0;
+  int64_t direct_max = 64;
+  int num_sms = 148;
+  size_t smem_optin = 232448;
+  // workspaces (named so independent stages never alias)
+  tgb::DevBuf ws_spec_a, ws_spec_b, ws_pairs, ws_flags, ws_in, ws_out, ws_misc, ws_misc2, ws_misc3;
+  std::vector<cudaEvent_t> events;
+  std::map<int64_t, std::shared_ptr<tgb::ConvPlan>> plans;
+};
+
+namespace tgb {
+void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t rb, const double* B, double h,
+                   double* out);
+void conv_central_many_dev(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out);
+void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const double* wb, double scale, double* out);
+double scalar_product_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b);
+void coulomb_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const tgb_cp& vh,
+                        double vol, double* J);
+void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ijk, double* out);
+void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
+                          double* out);
+}  // namespace tgb

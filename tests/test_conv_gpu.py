@@ -1,0 +1,160 @@
+"""Parity of the sm_100a mode convolutions with the CPU oracle (restatement of
+proj/src/fft.cpp + tensor.cpp) and with an independent numpy definition.
+Tolerance: 1e-10 relative max-norm (BASELINE.json north_star), per factor
+matrix.  Semantics pinned by the reference tests test_tensor.cpp:24-37,
+122-169, 211-230 and acceptance.cpp:103-127 are re-expressed here."""
+import numpy as np
+import pytest
+
+from conftest import relmax
+from oracle import oracle as O
+from paper_1504_06289_b200 import (CanonicalTensor3, DeviceCP, InvalidArgument, conv_central_many, convolve,
+                                   hartree_potential, value_at_points)
+from paper_1504_06289_b200.inputs import Rng, hartree_case, random_canonical
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+def window_np(u, v):
+    n = len(u)
+    full = np.convolve(u, v)
+    if n % 2:
+        o = (n - 1) // 2
+        return full[o:o + n]
+    o = n // 2 - 1
+    return 0.5 * (full[o:o + n] + full[o + 1:o + 1 + n])
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 16, 17, 31, 64, 65, 100, 127, 128, 129, 200, 513, 1000, 1025, 2048,
+                               2049, 4097, 8193])
+@pytest.mark.parametrize("force_fft", [False, True])
+def test_conv_central_many_matches_oracle(ctx, n, force_fft):
+    rng = Rng(1000 + n)
+    cols = 7
+    U = np.asfortranarray(rng.normal(n * cols).reshape(n, cols, order="F"))
+    v = rng.normal(n)
+    ctx.set_direct_max(0 if force_fft else 64)
+    try:
+        got = conv_central_many(U, v, ctx)
+    finally:
+        ctx.set_direct_max(64)
+    ref = O.conv_central_many(U, v)
+    assert relmax(got, ref) <= TOL
+    ind = np.stack([window_np(U[:, c], v) for c in range(cols)], axis=1)
+    assert relmax(got, ind) <= TOL
+
+
+def test_conv_large_n_gaussians(ctx):
+    # n = 16385 (config 2 extent): smooth, widely ranged Gaussians
+    n = 16385
+    x = (np.arange(n) - 0.5 * (n - 1)) * (20.0 / (n + 1))
+    a = np.array([0.05, 0.7, 5.0, 60.0, 500.0])
+    U = np.asfortranarray(np.exp(-a[None, :] * (x[:, None] - 0.3) ** 2))
+    v = np.exp(-2.0 * x ** 2)
+    got = conv_central_many(U, v, ctx)
+    ref = O.conv_central_many(U, v)
+    assert relmax(got, ref) <= TOL
+
+
+def test_convolve_delta_identity(ctx):
+    # test_tensor.cpp:122-135 — delta kernel with h-scaling removed
+    n, h = 17, 0.25
+    rng = Rng(7)
+    a = random_canonical(rng, (n, n, n), 2)
+    f = [np.zeros((n, 1), order="F") for _ in range(3)]
+    for ax in range(3):
+        f[ax][(n - 1) // 2, 0] = 1.0 / h
+    delta = CanonicalTensor3(f, np.ones(1))
+    c = convolve(a, delta, h, ctx)
+    assert c.rank() == 2
+    np.testing.assert_allclose(c.to_dense(), a.to_dense(), rtol=0, atol=1e-13 * np.abs(a.to_dense()).max())
+
+
+def test_convolve_semantics_random(ctx):
+    # acceptance.cpp:103-127 / test_tensor.cpp:211-230: per-axis extents 4..32,
+    # ranks 0..4, column order i + Ra*j, weights a.w[i]*b.w[j], h per axis.
+    rng = Rng(20240817)
+    for rep in range(40):
+        dims = tuple(int(4 + x) for x in rng.integers(3, 29))
+        ra, rb = (int(x) for x in rng.integers(2, 5))
+        a = random_canonical(rng, dims, ra)
+        b = random_canonical(rng, dims, rb)
+        h = (0.37, 0.5, 0.21)
+        c = convolve(a, b, h, ctx)
+        assert c.rank() == ra * rb
+        oc = O.convolve(O.OCP.from_cp(a), O.OCP.from_cp(b), h)
+        assert np.array_equal(c.weight, oc.weight())
+        for ax in range(3):
+            assert c.factor[ax].shape == (dims[ax], ra * rb)
+            if ra * rb:
+                assert relmax(c.factor[ax], oc.factors()[ax]) <= TOL
+
+
+def test_convolve_errors(ctx):
+    rng = Rng(8)
+    a = random_canonical(rng, (32, 32, 32), 2)
+    with pytest.raises(InvalidArgument):
+        convolve(a, random_canonical(rng, (32, 32, 8), 1), 0.2, ctx)
+    with pytest.raises(InvalidArgument):
+        convolve(a, a, 0.0, ctx)
+    with pytest.raises(InvalidArgument):
+        convolve(a, a, (0.2, -1.0, 0.2), ctx)
+
+
+def test_bitwise_duplicate_kernel_columns(ctx):
+    # +-t sinc nodes give bitwise-identical kernel columns (kernel.cpp:194);
+    # their output columns must be bitwise identical too.
+    case = hartree_case(0, n=257, rank=6)
+    vh = hartree_potential(case.theta, case.kernel, case.grid.h, ctx)
+    ra, rb = case.theta.rank(), case.kernel.rank()
+    for ax in range(3):
+        kf = case.kernel.tensor.factor[ax]
+        for j in range(rb):
+            jm = rb - 1 - j
+            assert np.array_equal(kf[:, j], kf[:, jm])
+            assert np.array_equal(vh.factor[ax][:, j * ra:(j + 1) * ra], vh.factor[ax][:, jm * ra:(jm + 1) * ra])
+
+
+def test_hartree_config0_full(ctx):
+    case = hartree_case(0)
+    vh = hartree_potential(case.theta, case.kernel, case.grid.h, ctx)
+    ovh = O.hartree_potential(O.OCP.from_cp(case.theta), O.OCP.from_cp(case.kernel.tensor), case.grid.h)
+    assert np.array_equal(vh.weight, ovh.weight())
+    of = ovh.factors()
+    for ax in range(3):
+        assert relmax(vh.factor[ax], of[ax]) <= TOL
+    got = value_at_points(vh, case.samples, ctx)
+    ref = O.value_at(ovh, case.samples)
+    assert relmax(got, ref) <= TOL
+
+
+def test_hartree_device_resident_matches_host(ctx):
+    import torch
+
+    case = hartree_case(0, n=1025, rank=12)
+    host = hartree_potential(case.theta, case.kernel, case.grid.h, ctx)
+    dt = DeviceCP.from_host(case.theta)
+    dk = DeviceCP.from_host(case.kernel.tensor)
+    dv = hartree_potential(dt, dk, case.grid.h, ctx)
+    ctx.synchronize()
+    back = dv.to_host()
+    for ax in range(3):
+        assert np.array_equal(back.factor[ax], host.factor[ax])
+    assert np.array_equal(back.weight, host.weight)
+    pts = torch.as_tensor(case.samples[:500]).cuda()
+    got = value_at_points(dv, pts, ctx).cpu().numpy()
+    assert relmax(got, value_at_points(host, case.samples[:500], ctx)) <= 1e-13
+
+
+def test_hartree_config2_columns(ctx):
+    # n = 16385 (config 2 extent) with a slice of the density: every kernel
+    # column, a few density columns, all three axes against the oracle.
+    case = hartree_case(2, rank=500, nsamples=100)
+    keep = [0, 17, 123, 256, 499]
+    theta = CanonicalTensor3([f[:, keep] for f in case.theta.factor], case.theta.weight[keep])
+    vh = hartree_potential(theta, case.kernel, case.grid.h, ctx)
+    ovh = O.hartree_potential(O.OCP.from_cp(theta), O.OCP.from_cp(case.kernel.tensor), case.grid.h)
+    of = ovh.factors()
+    for ax in range(3):
+        assert relmax(vh.factor[ax], of[ax]) <= TOL
