@@ -59,6 +59,12 @@ const char* tgb_last_error(void);
 /* Kernel launches issued by this context since creation (or the last reset). */
 int64_t tgb_ctx_launch_count(tgb_ctx* ctx);
 void tgb_ctx_reset_launch_count(tgb_ctx* ctx);
+/* Live kernel timing for bench.py: when enabled, every launch of the pair
+ * (inverse FFT) convolution kernel is bracketed by CUDA events on the context
+ * stream; tgb_ctx_profile_read synchronises, returns the summed device time
+ * (ms) and launch count since the last read, and resets them. */
+int tgb_ctx_set_profiling(tgb_ctx* ctx, int enabled);
+int tgb_ctx_profile_read(tgb_ctx* ctx, double* total_ms, int64_t* launches);
 /* Tuning / testing knob: 1D convolutions with n <= direct_max use direct
  * summation (reference: kFftConvThreshold = 128, fft.hpp:13).  Default 64;
  * 0 forces the FFT path wherever it exists. */

@@ -66,6 +66,8 @@ def lib() -> C.CDLL:
             "tgb_ctx_launch_count": (I64, [P]),
             "tgb_ctx_reset_launch_count": (None, [P]),
             "tgb_ctx_set_direct_max": (I, [P, I64]),
+            "tgb_ctx_set_profiling": (I, [P, I]),
+            "tgb_ctx_profile_read": (I, [P, C.POINTER(D), C.POINTER(I64)]),
             "tgb_conv_central_many": (I, [P, I64, I64, P, P, P, I]),
             "tgb_convolve": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),
             "tgb_hartree_potential": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),

@@ -179,6 +179,10 @@ int tgb_ctx_destroy(tgb_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
     for (auto e : ctx->events) cudaEventDestroy(e);
+    for (auto& pe : ctx->prof_events) {
+      cudaEventDestroy(pe.first);
+      cudaEventDestroy(pe.second);
+    }
     cudaStreamDestroy(ctx->copy_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -197,6 +201,25 @@ int tgb_ctx_synchronize(tgb_ctx* ctx) {
 int64_t tgb_ctx_launch_count(tgb_ctx* ctx) { return ctx ? ctx->launches : 0; }
 void tgb_ctx_reset_launch_count(tgb_ctx* ctx) {
   if (ctx) ctx->launches = 0;
+}
+
+int tgb_ctx_set_profiling(tgb_ctx* ctx, int enabled) {
+  return guarded([&] { ctx->profiling = enabled != 0; });
+}
+
+int tgb_ctx_profile_read(tgb_ctx* ctx, double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    double tot = 0.0;
+    for (size_t i = 0; i < ctx->prof_used; ++i) {
+      float ms = 0.f;
+      TGB_CUDA(cudaEventElapsedTime(&ms, ctx->prof_events[i].first, ctx->prof_events[i].second));
+      tot += ms;
+    }
+    *total_ms = tot;
+    *launches = static_cast<int64_t>(ctx->prof_used);
+    ctx->prof_used = 0;
+  });
 }
 
 int tgb_ctx_set_direct_max(tgb_ctx* ctx, int64_t direct_max) {

@@ -678,9 +678,11 @@ void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t
     TGB_CUDA(cudaMemcpyAsync(dreps, reps.data(), reps.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
     launch_spectrum(ctx, *pl, A, n, nullptr, static_cast<int>(ra), specA, 0.0);
     launch_spectrum(ctx, *pl, B, n, dreps, static_cast<int>(reps.size()), specB, h);
+    prof_begin(ctx);
     pair_kernel<<<static_cast<unsigned>(work.size()), pl->threads, pl->smem, ctx->stream>>>(pl->a, specA, specB,
                                                                                             dwork, out);
     TGB_LAUNCHED(ctx);
+    prof_end(ctx);
   }
   // (pageable-source cudaMemcpyAsync stages the host vectors before returning)
 }

@@ -77,10 +77,29 @@ struct tgb_ctx {
   // workspaces (named so independent stages never alias)
   tgb::DevBuf ws_spec_a, ws_spec_b, ws_pairs, ws_flags, ws_in, ws_out, ws_misc, ws_misc2, ws_misc3;
   std::vector<cudaEvent_t> events;
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
+  size_t prof_used = 0;
   std::map<int64_t, std::shared_ptr<tgb::ConvPlan>> plans;
 };
 
 namespace tgb {
+// bracket a hot-kernel launch with timing events when profiling is enabled
+inline void prof_begin(tgb_ctx* ctx) {
+  if (!ctx->profiling) return;
+  if (ctx->prof_used == ctx->prof_events.size()) {
+    cudaEvent_t a, b;
+    TGB_CUDA(cudaEventCreate(&a));
+    TGB_CUDA(cudaEventCreate(&b));
+    ctx->prof_events.push_back({a, b});
+  }
+  TGB_CUDA(cudaEventRecord(ctx->prof_events[ctx->prof_used].first, ctx->stream));
+}
+inline void prof_end(tgb_ctx* ctx) {
+  if (!ctx->profiling) return;
+  TGB_CUDA(cudaEventRecord(ctx->prof_events[ctx->prof_used].second, ctx->stream));
+  ctx->prof_used++;
+}
 void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t rb, const double* B, double h,
                    double* out);
 void conv_central_many_dev(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out);

@@ -54,6 +54,15 @@ class Context:
     def set_direct_max(self, n: int) -> None:
         check(lib().tgb_ctx_set_direct_max(self._h, n))
 
+    def set_profiling(self, enabled: bool) -> None:
+        check(lib().tgb_ctx_set_profiling(self._h, int(enabled)))
+
+    def profile_read(self) -> tuple[float, int]:
+        """(summed device ms, launches) of the pair convolution kernel since the last read."""
+        ms, cnt = C.c_double(), C.c_int64()
+        check(lib().tgb_ctx_profile_read(self._h, C.byref(ms), C.byref(cnt)))
+        return ms.value, cnt.value
+
     def close(self) -> None:
         if self._h:
             check(lib().tgb_ctx_destroy(self._h))
