@@ -12,24 +12,32 @@
 //  * Real signals: a length-m real transform is a length-N complex transform
 //    of the even/odd-packed signal plus an O(N) split step.
 //  * Spectra of every density column (A) and every DISTINCT kernel column
-//    (B) are computed once per call (spectrum_kernel); the kernel spectra
-//    carry the window shift, the even-n two-node mean, h and 1/m as one
-//    complex factor, so the per-pair work is: product, split, inverse FFT,
-//    store.  Bitwise-identical kernel columns (the +-t sinc nodes,
-//    kernel.cpp:194) are convolved once and stored to both output columns.
-//  * In-place mixed-radix decimation-in-time in shared memory: spectra are
-//    STORED in the digit-reversed order the DIT passes consume, so no
-//    permutation pass exists anywhere.  The first inverse pass pairs block g
-//    with the block holding the mirrored frequencies N-k, so the real-signal
-//    split happens in registers.
-//  * Twiddles: a two-level table (64 + m/64 entries) in shared memory and
-//    the recurrence w^s inside a butterfly.
+//    (B) are computed once per call (spectrum_kernel).  Bitwise-identical
+//    kernel columns (the +-t sinc nodes, kernel.cpp:194) are convolved once and
+//    stored to both output columns.  Kernel columns that are mirror-symmetric
+//    about the grid centre (every sinc column) have a real spectrum once the
+//    centring phase is removed; that phase cancels the window shift exactly for
+//    odd n and leaves the real filter cos(pi k/m) for even n, so B is stored as
+//    ONE real number per frequency with h/m folded in, and A needs no factor.
+//    Non-symmetric kernel columns take the general complex path.
+//  * Per pair (persistent CTAs): pass 0 reads A (complex) and B straight from
+//    L2 into registers, forms the product, performs the real-signal split by
+//    pairing block g with the block holding the mirrored frequencies N-k, and
+//    the first radix-r0 butterflies; middle passes are in-place mixed-radix
+//    decimation-in-time in shared memory; the last pass writes the windowed
+//    outputs straight from registers to HBM (both mirrored columns).  Spectra
+//    are STORED in the digit-reversed order the DIT passes consume, so no
+//    permutation pass exists anywhere.
+//  * Twiddles: per-pass tables w_{L r}^j indexed by the butterfly's j (read
+//    coalesced through L1/L2) and the recurrence w^s inside a butterfly.
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <functional>
+#include <tuple>
 #include <vector>
 
 #include "tgb_internal.hpp"
@@ -39,15 +47,19 @@ namespace tgb {
 // ------------------------------------------------------------------ plan
 
 constexpr int kMaxPasses = 12;
-constexpr int kMaxThreads = 512;
+constexpr int kMaxThreads = 384;
 
 struct PlanArgs {
-  int n, N, m, P, ofs, even, ntw;
+  int n, N, m, P, ofs, even, npl;
   int r[kMaxPasses];
-  const int* perm;     // stored position -> natural frequency index (N entries)
-  const int* inv;      // natural frequency index -> stored position (N entries)
-  const int* partner;  // first-pass block g -> block holding the mirrored frequencies
-  const double2* tw;   // [0,64): w^e ; [64, 64 + m/64 + 1): w^(64 h)   with w = exp(2 pi i / m)
+  int L[kMaxPasses];
+  const int* perm;       // stored position -> natural frequency index (N entries)
+  const int* inv;        // natural frequency index -> stored position (N entries)
+  const int2* leader;    // first-pass block pairs (g, g2), g <= g2 (npl entries)
+  const double2* twz;    // first pass: w_m^{kk(g)} per block g (N/r0 entries)
+  const double2* cs;     // first pass: w_m^{s N/r0}, s < r0
+  const double2* twp[kMaxPasses];  // pass p >= 1: w_{L_p r_p}^j, j < L_p   (w = exp(+2 pi i / .))
+  const double2* twpost; // forward post-processing: w_m^k, k <= N
 };
 
 struct ConvPlan {
@@ -55,7 +67,7 @@ struct ConvPlan {
   bool direct = false;
   int threads = 0;
   size_t smem = 0;
-  DevBuf perm, inv, partner, tw;
+  DevBuf perm, inv, leader, twz, cs, twp, twpost;
 };
 
 __host__ __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
@@ -67,25 +79,18 @@ static bool five_smooth(int64_t x) {
   return x == 1;
 }
 
-// Fewest passes, then the largest smallest radix; radices sorted descending.
+// Fewest passes; then a first radix of 8..10 (pass 0 holds two blocks in
+// registers); then the largest smallest radix.
 static bool factor_radices(int N, std::vector<int>& best) {
   static const int kR[] = {16, 10, 8, 6, 5, 4, 3, 2};
-  best.clear();
+  std::vector<std::vector<int>> all;
   std::vector<int> cur;
-  bool found = false;
   std::function<void(int, int)> rec = [&](int rem, int maxr) {
-    if (found && cur.size() >= best.size() && !(rem == 1 && cur.size() == best.size())) {
-      if (cur.size() > best.size()) return;
-    }
     if (rem == 1) {
-      if (!found || cur.size() < best.size() ||
-          (cur.size() == best.size() && cur.back() > best.back())) {
-        best = cur;
-        found = true;
-      }
+      all.push_back(cur);
       return;
     }
-    if (cur.size() >= static_cast<size_t>(kMaxPasses)) return;
+    if (cur.size() >= static_cast<size_t>(kMaxPasses) || all.size() > 20000) return;
     for (int r : kR) {
       if (r > maxr || rem % r) continue;
       cur.push_back(r);
@@ -94,12 +99,35 @@ static bool factor_radices(int N, std::vector<int>& best) {
     }
   };
   rec(N, 16);
-  return found;
+  if (all.empty()) return false;
+  auto score = [](const std::vector<int>& v) {
+    int first = 0;
+    for (int r : v)
+      if (r <= 10) {
+        first = r;
+        break;
+      }
+    return std::make_tuple(static_cast<int>(v.size()), first >= 8 ? 0 : (first >= 4 ? 1 : 2), -v.back());
+  };
+  std::stable_sort(all.begin(), all.end(), [&](const auto& x, const auto& y) { return score(x) < score(y); });
+  best = all.front();
+  // pass 0 = largest radix <= 10, the rest descending
+  int idx = -1;
+  for (size_t i = 0; i < best.size(); ++i)
+    if (best[i] <= 10) {
+      idx = static_cast<int>(i);
+      break;
+    }
+  if (idx < 0) return false;
+  if (idx > 0) std::rotate(best.begin(), best.begin() + idx, best.begin() + idx + 1);
+  return true;
 }
 
-static size_t plan_smem(int N, int m) {
-  const int ntw = 64 + m / 64 + 1;
-  return static_cast<size_t>(pidx(N) + 1 + ntw) * sizeof(double2);
+static size_t plan_smem(int N) { return static_cast<size_t>(pidx(N) + 1) * sizeof(double2); }
+
+static double2 unit_root(int64_t e, int64_t m) {
+  const long double ang = 2.0L * 3.141592653589793238462643383279502884L * static_cast<long double>(e) / m;
+  return make_double2(static_cast<double>(cosl(ang)), static_cast<double>(sinl(ang)));
 }
 
 std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
@@ -119,11 +147,16 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
   a.N = static_cast<int>(N);
   a.m = static_cast<int>(2 * N);
   std::vector<int> rad;
-  const bool fits = N < (1 << 24) && plan_smem(a.N, a.m) <= ctx->smem_optin && factor_radices(a.N, rad);
+  const bool fits = N < (1 << 24) && plan_smem(a.N) <= ctx->smem_optin && factor_radices(a.N, rad);
   pl->direct = n <= ctx->direct_max || !fits;
   if (!pl->direct) {
     a.P = static_cast<int>(rad.size());
-    for (int p = 0; p < a.P; ++p) a.r[p] = rad[p];
+    int L = 1;
+    for (int p = 0; p < a.P; ++p) {
+      a.r[p] = rad[p];
+      a.L[p] = L;
+      L *= rad[p];
+    }
     // digit-reversed storage order consumed by in-place DIT passes
     std::vector<int> perm(N), inv(N);
     for (int64_t pos = 0; pos < N; ++pos) {
@@ -137,32 +170,58 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
       perm[pos] = static_cast<int>(k);
       inv[k] = static_cast<int>(pos);
     }
-    const int r0 = rad[0], nblk = a.N / r0, step = a.N / r0;
-    (void)step;
-    std::vector<int> partner(nblk);
+    const int r0 = rad[0], nblk = a.N / r0;
+    std::vector<int2> leaders;
+    std::vector<double2> twz(nblk), cs(r0);
     for (int g = 0; g < nblk; ++g) {
       const int kk = perm[static_cast<size_t>(g) * r0];
-      partner[g] = kk == 0 ? g : inv[nblk - kk] / r0;
+      const int g2 = kk == 0 ? g : inv[nblk - kk] / r0;
+      if (g2 >= g) leaders.push_back(make_int2(g, g2));
+      twz[g] = unit_root(kk, a.m);
     }
-    a.ntw = 64 + a.m / 64 + 1;
-    std::vector<double2> tw(a.ntw);
-    for (int e = 0; e < a.ntw; ++e) {
-      const long double k = e < 64 ? e : 64.0L * (e - 64);
-      const long double ang = 2.0L * 3.141592653589793238462643383279502884L * k / a.m;
-      tw[e] = make_double2(static_cast<double>(cosl(ang)), static_cast<double>(sinl(ang)));
+    for (int s = 0; s < r0; ++s) cs[s] = unit_root(static_cast<int64_t>(s) * nblk, a.m);
+    a.npl = static_cast<int>(leaders.size());
+    std::vector<double2> twp;
+    std::vector<size_t> twp_off(a.P, 0);
+    for (int p = 1; p < a.P; ++p) {
+      twp_off[p] = twp.size();
+      for (int j = 0; j < a.L[p]; ++j) twp.push_back(unit_root(j, static_cast<int64_t>(a.L[p]) * a.r[p]));
     }
+    std::vector<double2> twpost(a.N + 1);
+    for (int k = 0; k <= a.N; ++k) twpost[k] = unit_root(k, a.m);
     auto up = [&](DevBuf& b, const void* src, size_t bytes) {
-      void* p = b.get(bytes);
-      TGB_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
+      void* p = b.get(std::max<size_t>(bytes, 16));
+      if (bytes) TGB_CUDA(cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice));
       return p;
     };
     a.perm = static_cast<const int*>(up(pl->perm, perm.data(), perm.size() * sizeof(int)));
     a.inv = static_cast<const int*>(up(pl->inv, inv.data(), inv.size() * sizeof(int)));
-    a.partner = static_cast<const int*>(up(pl->partner, partner.data(), partner.size() * sizeof(int)));
-    a.tw = static_cast<const double2*>(up(pl->tw, tw.data(), tw.size() * sizeof(double2)));
-    pl->smem = plan_smem(a.N, a.m);
-    int t = ((a.N / 16 + 31) / 32) * 32;
-    pl->threads = std::max(64, std::min(kMaxThreads, t));
+    a.leader = static_cast<const int2*>(up(pl->leader, leaders.data(), leaders.size() * sizeof(int2)));
+    a.twz = static_cast<const double2*>(up(pl->twz, twz.data(), twz.size() * sizeof(double2)));
+    a.cs = static_cast<const double2*>(up(pl->cs, cs.data(), cs.size() * sizeof(double2)));
+    auto* tp = static_cast<const double2*>(up(pl->twp, twp.data(), twp.size() * sizeof(double2)));
+    for (int p = 1; p < a.P; ++p) a.twp[p] = tp + twp_off[p];
+    a.twpost = static_cast<const double2*>(up(pl->twpost, twpost.data(), twpost.size() * sizeof(double2)));
+    pl->smem = plan_smem(a.N);
+    // threads: best butterfly balance over the passes, at least 8 warps when possible
+    double best_eff = -1.0;
+    int best_t = 64;
+    const int tmax = std::min(kMaxThreads, std::max(64, ((a.N / 8 + 31) / 32) * 32));
+    for (int t = std::min(256, tmax); t <= tmax; t += 32) {
+      double useful = 0.0, slots = 0.0;
+      for (int p = 0; p < a.P; ++p) {
+        const double bf = p == 0 ? a.npl : static_cast<double>(a.N) / a.r[p];
+        const double cost = p == 0 ? 2.0 * a.r[p] : a.r[p];
+        useful += bf * cost;
+        slots += std::ceil(bf / t) * t * cost;
+      }
+      const double eff = useful / slots;
+      if (eff > best_eff + 1e-9 || (std::abs(eff - best_eff) <= 1e-9 && t > best_t)) {
+        best_eff = eff;
+        best_t = t;
+      }
+    }
+    pl->threads = best_t;
   }
   ctx->plans[key] = pl;
   return pl;
@@ -176,19 +235,16 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
-// multiply by sigma * i
 template <int S>
-__device__ __forceinline__ double2 mul_si(double2 a) {
+__device__ __forceinline__ double2 mul_si(double2 a) {  // * (S i)
   return S > 0 ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
 }
-// multiply by (c + sigma i s)
 template <int S>
-__device__ __forceinline__ double2 mul_cs(double2 a, double c, double s) {
+__device__ __forceinline__ double2 mul_cs(double2 a, double c, double s) {  // * (c + S i s)
   const double ss = S > 0 ? s : -s;
   return make_double2(a.x * c - a.y * ss, a.x * ss + a.y * c);
 }
-
-__device__ __forceinline__ double2 tw_m(const double2* tw, int e) { return cmul(tw[e & 63], tw[64 + (e >> 6)]); }
+__device__ __forceinline__ double2 ld2(const double2* p) { return __ldg(p); }
 
 // ------------------------------------------------------------------ small DFTs, y_k = sum_s v_s w^(s k), w = exp(S 2 pi i / R)
 
@@ -247,7 +303,6 @@ __device__ __forceinline__ void dft(double2* v) {
   } else if constexpr (R == 5) {
     dft5<S>(v[0], v[1], v[2], v[3], v[4]);
   } else if constexpr (R == 6) {
-    // s = 2 s' + e: E = DFT3(even), O = DFT3(odd); y_k = E_k + w6^k O_k, y_{k+3} = E_k - w6^k O_k
     double2 e0 = v[0], e1 = v[2], e2 = v[4], o0 = v[1], o1 = v[3], o2 = v[5];
     dft3<S>(e0, e1, e2);
     dft3<S>(o0, o1, o2);
@@ -298,19 +353,17 @@ __device__ __forceinline__ void dft(double2* v) {
     constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
 #pragma unroll
     for (int s2 = 0; s2 < 4; ++s2) dft4<S>(v[s2], v[s2 + 4], v[s2 + 8], v[s2 + 12]);
-    // now v[s2 + 4 k1] = B_{s2}[k1]
-    v[5] = mul_cs<S>(v[5], c1, s1);     // s2=1,k1=1: e=1
-    v[9] = mul_cs<S>(v[9], kR2, kR2);   // s2=1,k1=2: e=2
-    v[13] = mul_cs<S>(v[13], s1, c1);   // s2=1,k1=3: e=3
-    v[6] = mul_cs<S>(v[6], kR2, kR2);   // s2=2,k1=1: e=2
-    v[10] = mul_si<S>(v[10]);           // s2=2,k1=2: e=4
-    v[14] = mul_cs<S>(v[14], -kR2, kR2);  // s2=2,k1=3: e=6
-    v[7] = mul_cs<S>(v[7], s1, c1);     // s2=3,k1=1: e=3
-    v[11] = mul_cs<S>(v[11], -kR2, kR2);  // s2=3,k1=2: e=6
-    v[15] = mul_cs<S>(v[15], -c1, -s1);   // s2=3,k1=3: e=9
+    v[5] = mul_cs<S>(v[5], c1, s1);
+    v[9] = mul_cs<S>(v[9], kR2, kR2);
+    v[13] = mul_cs<S>(v[13], s1, c1);
+    v[6] = mul_cs<S>(v[6], kR2, kR2);
+    v[10] = mul_si<S>(v[10]);
+    v[14] = mul_cs<S>(v[14], -kR2, kR2);
+    v[7] = mul_cs<S>(v[7], s1, c1);
+    v[11] = mul_cs<S>(v[11], -kR2, kR2);
+    v[15] = mul_cs<S>(v[15], -c1, -s1);
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1) dft4<S>(v[4 * k1], v[4 * k1 + 1], v[4 * k1 + 2], v[4 * k1 + 3]);
-    // v[4 k1 + k2] = y[k1 + 4 k2]; transpose 4x4 into natural order
     double2 t[16];
 #pragma unroll
     for (int k1 = 0; k1 < 4; ++k1)
@@ -323,27 +376,29 @@ __device__ __forceinline__ void dft(double2* v) {
 
 // ------------------------------------------------------------------ passes
 
-// One in-place DIT pass of radix R and span L over N elements in shared memory.
+// Butterfly input twiddles w^{j s}, s = 1..R-1 (w from the per-pass table).
 template <int R, int S>
-__device__ __forceinline__ void dit_pass(double2* sm, int N, int L, int m, const double2* tw) {
+__device__ __forceinline__ void apply_twiddles(double2* v, double2 w) {
+  if (S < 0) w.y = -w.y;
+  double2 ws = w;
+#pragma unroll
+  for (int s = 1; s < R; ++s) {
+    v[s] = cmul(v[s], ws);
+    if (s + 1 < R) ws = cmul(ws, w);
+  }
+}
+
+// In-place DIT pass of radix R and span L over N elements in shared memory.
+template <int R, int S>
+__device__ __forceinline__ void dit_pass(double2* sm, int N, int L, const double2* __restrict__ twp) {
   const int nbf = N / R;
-  const int tstep = m / (L * R);
   for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
     const int j = bf % L;
     const int base = (bf - j) * R + j;
     double2 v[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) v[s] = sm[pidx(base + s * L)];
-    if (j) {
-      double2 w = tw_m(tw, j * tstep);
-      if (S < 0) w.y = -w.y;
-      double2 ws = w;
-#pragma unroll
-      for (int s = 1; s < R; ++s) {
-        v[s] = cmul(v[s], ws);
-        if (s + 1 < R) ws = cmul(ws, w);
-      }
-    }
+    if (L > 1) apply_twiddles<R, S>(v, ld2(twp + j));
     dft<R, S>(v);
 #pragma unroll
     for (int t = 0; t < R; ++t) sm[pidx(base + t * L)] = v[t];
@@ -351,55 +406,122 @@ __device__ __forceinline__ void dit_pass(double2* sm, int N, int L, int m, const
 }
 
 template <int S>
-__device__ void run_passes(double2* sm, const PlanArgs& pa, const double2* tw, int p0) {
-  int L = 1;
-  for (int p = 0; p < p0; ++p) L *= pa.r[p];
-  for (int p = p0; p < pa.P; ++p) {
-    switch (pa.r[p]) {
-      case 2: dit_pass<2, S>(sm, pa.N, L, pa.m, tw); break;
-      case 3: dit_pass<3, S>(sm, pa.N, L, pa.m, tw); break;
-      case 4: dit_pass<4, S>(sm, pa.N, L, pa.m, tw); break;
-      case 5: dit_pass<5, S>(sm, pa.N, L, pa.m, tw); break;
-      case 6: dit_pass<6, S>(sm, pa.N, L, pa.m, tw); break;
-      case 8: dit_pass<8, S>(sm, pa.N, L, pa.m, tw); break;
-      case 10: dit_pass<10, S>(sm, pa.N, L, pa.m, tw); break;
-      case 16: dit_pass<16, S>(sm, pa.N, L, pa.m, tw); break;
-    }
-    L *= pa.r[p];
-    __syncthreads();
+__device__ __forceinline__ void dit_pass_rt(double2* sm, const PlanArgs& pa, int p) {
+  const double2* tw = pa.twp[p];
+  switch (pa.r[p]) {
+    case 2: dit_pass<2, S>(sm, pa.N, pa.L[p], tw); break;
+    case 3: dit_pass<3, S>(sm, pa.N, pa.L[p], tw); break;
+    case 4: dit_pass<4, S>(sm, pa.N, pa.L[p], tw); break;
+    case 5: dit_pass<5, S>(sm, pa.N, pa.L[p], tw); break;
+    case 6: dit_pass<6, S>(sm, pa.N, pa.L[p], tw); break;
+    case 8: dit_pass<8, S>(sm, pa.N, pa.L[p], tw); break;
+    case 10: dit_pass<10, S>(sm, pa.N, pa.L[p], tw); break;
+    case 16: dit_pass<16, S>(sm, pa.N, pa.L[p], tw); break;
   }
 }
 
-// Z[K] = (P[K] + conj(P[N-K])) + i w_m^K (P[K] - conj(P[N-K]))  — inverse real split
-__device__ __forceinline__ double2 zmake(double2 p, double2 q, int K, const double2* tw) {
+// Last inverse pass: butterflies, then the windowed outputs straight to HBM.
+// z[t] = x[2t] + i x[2t+1]; only t < ceil(n/2) is stored.
+template <int R>
+__device__ __forceinline__ void last_pass_store(const double2* sm, const PlanArgs& pa, double* o0, double* o1,
+                                                bool aligned) {
+  const int N = pa.N, L = pa.L[pa.P - 1], nbf = N / R;
+  const int nz = (pa.n + 1) >> 1;
+  const bool odd_n = pa.n & 1;
+  const double2* tw = pa.twp[pa.P - 1];
+  for (int j = threadIdx.x; j < nbf; j += blockDim.x) {
+    double2 v[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) v[s] = sm[pidx(j + s * L)];
+    if (L > 1) apply_twiddles<R, 1>(v, ld2(tw + j));
+    dft<R, 1>(v);
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+      const int idx = j + t * L;
+      if (idx >= nz) continue;
+      const bool full = !(odd_n && idx == nz - 1);
+      if (aligned && full) {
+        __stcs(reinterpret_cast<double2*>(o0 + 2 * idx), v[t]);
+        if (o1) __stcs(reinterpret_cast<double2*>(o1 + 2 * idx), v[t]);
+      } else {
+        __stcs(o0 + 2 * idx, v[t].x);
+        if (full) __stcs(o0 + 2 * idx + 1, v[t].y);
+        if (o1) {
+          __stcs(o1 + 2 * idx, v[t].x);
+          if (full) __stcs(o1 + 2 * idx + 1, v[t].y);
+        }
+      }
+    }
+  }
+}
+
+// Z[K] = (P[K] + conj(P[N-K])) + i w^K (P[K] - conj(P[N-K]))  — inverse real split
+__device__ __forceinline__ double2 zsplit(double2 p, double2 q, double2 w) {
   const double2 sum = make_double2(p.x + q.x, p.y - q.y);
   const double2 dif = make_double2(p.x - q.x, p.y + q.y);
-  const double2 wd = cmul(tw_m(tw, K), dif);
+  const double2 wd = cmul(w, dif);
   return make_double2(sum.x - wd.y, sum.y + wd.x);
 }
 
-// First inverse pass: real split + radix-R butterflies on paired blocks.
-template <int R>
-__device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa, const double2* tw) {
-  const int N = pa.N, nblk = N / R, step = N / R;
-  for (int g = threadIdx.x; g < nblk; g += blockDim.x) {
-    const int g2 = pa.partner[g];
-    if (g2 < g) continue;
-    const int kk = pa.perm[g * R];
-    double2 a[R];
+// product P = A * B for R consecutive stored positions starting at pos
+template <int R, bool BREAL>
+__device__ __forceinline__ void load_product(double2* v, const double2* __restrict__ A, const void* __restrict__ Bv,
+                                             int pos) {
+  if constexpr (BREAL) {
+    const double* B = static_cast<const double*>(Bv) + pos;
+    double b[R];
 #pragma unroll
-    for (int s = 0; s < R; ++s) a[s] = sm[pidx(g * R + s)];
-    if (kk == 0) {
-      const double2 z0 = zmake(a[0], sm[pidx(N)], 0, tw);
+    for (int s = 0; s < R; ++s) {
+      v[s] = ld2(A + pos + s);
+      b[s] = __ldg(B + s);
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) v[s] = cscale(v[s], b[s]);
+  } else {
+    const double2* B = static_cast<const double2*>(Bv) + pos;
+    double2 b[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      v[s] = ld2(A + pos + s);
+      b[s] = ld2(B + s);
+    }
+#pragma unroll
+    for (int s = 0; s < R; ++s) v[s] = cmul(v[s], b[s]);
+  }
+}
+
+template <bool BREAL>
+__device__ __forceinline__ double2 load_product1(const double2* __restrict__ A, const void* __restrict__ Bv, int pos) {
+  if constexpr (BREAL) return cscale(ld2(A + pos), __ldg(static_cast<const double*>(Bv) + pos));
+  else return cmul(ld2(A + pos), ld2(static_cast<const double2*>(Bv) + pos));
+}
+
+// First inverse pass straight from the spectra in L2: product, real split,
+// radix-R butterflies on the paired blocks, results to shared memory.
+template <int R, bool BREAL>
+__device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa, const double2* __restrict__ A,
+                                               const void* __restrict__ B) {
+  const int N = pa.N;
+  for (int q = threadIdx.x; q < pa.npl; q += blockDim.x) {
+    const int2 gg = __ldg(pa.leader + q);
+    const int g = gg.x, g2 = gg.y;
+    double2 a[R];
+    load_product<R, BREAL>(a, A, B, g * R);
+    const double2 wk = ld2(pa.twz + g);
+    if (g == 0) {
+      // natural frequencies s*N/R; mirror of s is R-s (s=0 mirrors to N)
+      const double2 pn = load_product1<BREAL>(A, B, N);
+      const double2 z0 = zsplit(a[0], pn, make_double2(1.0, 0.0));
 #pragma unroll
       for (int s = 1; 2 * s <= R; ++s) {
+        const double2 ws = ld2(pa.cs + s), wr = ld2(pa.cs + (R - s));
         if (2 * s < R) {
-          const double2 zs = zmake(a[s], a[R - s], s * step, tw);
-          const double2 zr = zmake(a[R - s], a[s], (R - s) * step, tw);
+          const double2 zs = zsplit(a[s], a[R - s], ws);
+          const double2 zr = zsplit(a[R - s], a[s], wr);
           a[s] = zs;
           a[R - s] = zr;
         } else {
-          a[s] = zmake(a[s], a[s], s * step, tw);
+          a[s] = zsplit(a[s], a[s], ws);
         }
       }
       a[0] = z0;
@@ -409,24 +531,28 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa, 
     } else if (g2 == g) {
 #pragma unroll
       for (int s = 0; 2 * s < R - 1; ++s) {
-        const double2 z1 = zmake(a[s], a[R - 1 - s], kk + s * step, tw);
-        const double2 z2 = zmake(a[R - 1 - s], a[s], kk + (R - 1 - s) * step, tw);
+        const double2 w1 = cmul(wk, ld2(pa.cs + s)), w2 = cmul(wk, ld2(pa.cs + (R - 1 - s)));
+        const double2 z1 = zsplit(a[s], a[R - 1 - s], w1);
+        const double2 z2 = zsplit(a[R - 1 - s], a[s], w2);
         a[s] = z1;
         a[R - 1 - s] = z2;
       }
-      if (R & 1) a[(R - 1) / 2] = zmake(a[(R - 1) / 2], a[(R - 1) / 2], kk + ((R - 1) / 2) * step, tw);
+      if (R & 1) {
+        const int s = (R - 1) / 2;
+        a[s] = zsplit(a[s], a[s], cmul(wk, ld2(pa.cs + s)));
+      }
       dft<R, 1>(a);
 #pragma unroll
       for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
     } else {
-      const int kk2 = nblk - kk;
       double2 b[R];
-#pragma unroll
-      for (int s = 0; s < R; ++s) b[s] = sm[pidx(g2 * R + s)];
+      load_product<R, BREAL>(b, A, B, g2 * R);
+      const double2 wk2 = ld2(pa.twz + g2);
 #pragma unroll
       for (int s = 0; s < R; ++s) {
-        const double2 za = zmake(a[s], b[R - 1 - s], kk + s * step, tw);
-        const double2 zb = zmake(b[R - 1 - s], a[s], kk2 + (R - 1 - s) * step, tw);
+        const double2 cs1 = ld2(pa.cs + s), cs2 = ld2(pa.cs + (R - 1 - s));
+        const double2 za = zsplit(a[s], b[R - 1 - s], cmul(wk, cs1));
+        const double2 zb = zsplit(b[R - 1 - s], a[s], cmul(wk2, cs2));
         a[s] = za;
         b[R - 1 - s] = zb;
       }
@@ -441,22 +567,17 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa, 
   }
 }
 
-__device__ __forceinline__ void load_twiddles(double2* dst, const PlanArgs& pa) {
-  for (int i = threadIdx.x; i < pa.ntw; i += blockDim.x) dst[i] = pa.tw[i];
-}
-
 // ------------------------------------------------------------------ kernels
 
-// Forward spectrum of real columns: spec[c] (N+1 complex, stored order) =
-// DFT_m(x_c zero-padded) [* phi(k) when phi_h > 0].
-// phi(k) = (h/m) w^(k ofs) (odd n) or (h/m) w^(k ofs) (1 + w^k)/2 (even n).
+// Forward spectrum of real columns, stored in DIT order (N+1 entries, the
+// Nyquist term last).  mode 0: complex X (density side);  mode 1: real
+// R[k] = (h/m) c(k) Re(X[k] e^{2 pi i k (n-1)/(2m)}), c = 1 (odd n) or
+// cos(pi k/m) (even n);  mode 2: complex X * (h/m) e^{2 pi i k ofs/m} *
+// (1 or (1 + e^{2 pi i k/m})/2)  (general kernel columns).
 __global__ void __launch_bounds__(kMaxThreads, 1)
     spectrum_kernel(PlanArgs pa, const double* __restrict__ X, int64_t ldx, const int* __restrict__ colidx,
-                    double2* __restrict__ spec, double phi_h) {
-  extern __shared__ double2 smem[];
-  double2* sm = smem;
-  double2* tw = smem + pidx(pa.N) + 1;
-  load_twiddles(tw, pa);
+                    void* __restrict__ spec, int mode, double h) {
+  extern __shared__ double2 sm[];
   const int c = blockIdx.x;
   const double* x = X + (colidx ? colidx[c] : c) * ldx;
   const int n = pa.n, N = pa.N;
@@ -468,28 +589,55 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     sm[pidx(pos)] = make_double2(x0, x1);
   }
   __syncthreads();
-  run_passes<-1>(sm, pa, tw, 0);
-  double2* out = spec + static_cast<int64_t>(c) * (N + 1);
-  const double hm = phi_h / pa.m;
+  // forward DIT; pass 0 has no twiddles (L = 1)
+  switch (pa.r[0]) {
+    case 2: dit_pass<2, -1>(sm, N, 1, nullptr); break;
+    case 3: dit_pass<3, -1>(sm, N, 1, nullptr); break;
+    case 4: dit_pass<4, -1>(sm, N, 1, nullptr); break;
+    case 5: dit_pass<5, -1>(sm, N, 1, nullptr); break;
+    case 6: dit_pass<6, -1>(sm, N, 1, nullptr); break;
+    case 8: dit_pass<8, -1>(sm, N, 1, nullptr); break;
+    case 10: dit_pass<10, -1>(sm, N, 1, nullptr); break;
+    case 16: dit_pass<16, -1>(sm, N, 1, nullptr); break;
+  }
+  __syncthreads();
+  for (int p = 1; p < pa.P; ++p) {
+    dit_pass_rt<-1>(sm, pa, p);
+    __syncthreads();
+  }
+  const double hm = h / pa.m;
   for (int k = threadIdx.x; k <= N; k += blockDim.x) {
     const double2 zk = sm[pidx(k == N ? 0 : k)];
     double2 zm = sm[pidx(k == 0 ? 0 : N - k)];
     zm.y = -zm.y;
     const double2 sum = cadd(zk, zm), dif = csub(zk, zm);
-    double2 w = tw_m(tw, k);  // k <= N < m
-    w.y = -w.y;               // w^-k
+    double2 w = ld2(pa.twpost + k);
+    w.y = -w.y;  // w^-k
     const double2 wd = cmul(w, dif);
-    double2 X = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
-    if (phi_h > 0.0) {
-      const int e = static_cast<int>((static_cast<int64_t>(k) * pa.ofs) % pa.m);
-      double2 ph = tw_m(tw, e);
+    const double2 Xk = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
+    const int pos = k < N ? pa.inv[k] : N;
+    if (mode == 0) {
+      static_cast<double2*>(spec)[static_cast<int64_t>(c) * (N + 1) + pos] = Xk;
+    } else if (mode == 1) {
+      // remove the centring phase e^{-2 pi i k c/m}, c = (n-1)/2
+      const int64_t e = (static_cast<int64_t>(k) * (n - 1)) % (2 * static_cast<int64_t>(pa.m));
+      double sn, cn;
+      sincospi(static_cast<double>(e) / pa.m, &sn, &cn);
+      double r = Xk.x * cn - Xk.y * sn;
+      if (pa.even) r *= cospi(static_cast<double>(k) / pa.m);
+      static_cast<double*>(spec)[static_cast<int64_t>(c) * (N + 1) + pos] = hm * r;
+    } else {
+      const int64_t e = (static_cast<int64_t>(k) * pa.ofs) % pa.m;
+      double sn, cn;
+      sincospi(2.0 * static_cast<double>(e) / pa.m, &sn, &cn);
+      double2 ph = make_double2(cn, sn);
       if (pa.even) {
-        const double2 wk = tw_m(tw, k);
-        ph = cmul(ph, make_double2(0.5 * (1.0 + wk.x), 0.5 * wk.y));
+        double s2, c2;
+        sincospi(2.0 * static_cast<double>(k) / pa.m, &s2, &c2);
+        ph = cmul(ph, make_double2(0.5 * (1.0 + c2), 0.5 * s2));
       }
-      X = cmul(X, cscale(ph, hm));
+      static_cast<double2*>(spec)[static_cast<int64_t>(c) * (N + 1) + pos] = cmul(Xk, cscale(ph, hm));
     }
-    out[k < N ? pa.inv[k] : N] = X;
   }
 }
 
@@ -498,40 +646,52 @@ struct PairEntry {
   int64_t out0, out1;  // element offsets of the destination columns (-1: none)
 };
 
-// One windowed 1D convolution per CTA: out = window(IFFT(A_i * B_j)).
+// Persistent: CTA loops over work entries; one windowed convolution each.
+template <int R0, bool BREAL>
 __global__ void __launch_bounds__(kMaxThreads, 1)
-    pair_kernel(PlanArgs pa, const double2* __restrict__ specA, const double2* __restrict__ specB,
-                const PairEntry* __restrict__ work, double* __restrict__ out) {
-  extern __shared__ double2 smem[];
-  double2* sm = smem;
-  double2* tw = smem + pidx(pa.N) + 1;
-  load_twiddles(tw, pa);
-  const PairEntry e = work[blockIdx.x];
+    pair_kernel(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
+                const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
+  extern __shared__ double2 sm[];
   const int N = pa.N;
-  const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
-  const double2* b = specB + static_cast<int64_t>(e.jb) * (N + 1);
-  for (int pos = threadIdx.x; pos <= N; pos += blockDim.x) sm[pidx(pos)] = cmul(__ldg(a + pos), __ldg(b + pos));
-  __syncthreads();
-  switch (pa.r[0]) {
-    case 2: first_pass_inv<2>(sm, pa, tw); break;
-    case 3: first_pass_inv<3>(sm, pa, tw); break;
-    case 4: first_pass_inv<4>(sm, pa, tw); break;
-    case 5: first_pass_inv<5>(sm, pa, tw); break;
-    case 6: first_pass_inv<6>(sm, pa, tw); break;
-    case 8: first_pass_inv<8>(sm, pa, tw); break;
-    case 10: first_pass_inv<10>(sm, pa, tw); break;
-    case 16: first_pass_inv<16>(sm, pa, tw); break;
-  }
-  __syncthreads();
-  run_passes<1>(sm, pa, tw, 1);
-  const int n = pa.n;
-  double* o0 = out + e.out0;
-  double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double2 z = sm[pidx(i >> 1)];
-    const double v = (i & 1) ? z.y : z.x;
-    o0[i] = v;
-    if (o1) o1[i] = v;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const PairEntry e = work[w];
+    const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
+    first_pass_inv<R0, BREAL>(sm, pa, a, b);
+    __syncthreads();
+    for (int p = 1; p + 1 < pa.P; ++p) {
+      dit_pass_rt<1>(sm, pa, p);
+      __syncthreads();
+    }
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+    if (pa.P == 1) {
+      // single pass: outputs are already natural-order in shared memory
+      const int nz = (pa.n + 1) >> 1;
+      for (int t = threadIdx.x; t < nz; t += blockDim.x) {
+        const double2 z = sm[pidx(t)];
+        o0[2 * t] = z.x;
+        if (2 * t + 1 < pa.n) o0[2 * t + 1] = z.y;
+        if (o1) {
+          o1[2 * t] = z.x;
+          if (2 * t + 1 < pa.n) o1[2 * t + 1] = z.y;
+        }
+      }
+    } else {
+      switch (pa.r[pa.P - 1]) {
+        case 2: last_pass_store<2>(sm, pa, o0, o1, aligned); break;
+        case 3: last_pass_store<3>(sm, pa, o0, o1, aligned); break;
+        case 4: last_pass_store<4>(sm, pa, o0, o1, aligned); break;
+        case 5: last_pass_store<5>(sm, pa, o0, o1, aligned); break;
+        case 6: last_pass_store<6>(sm, pa, o0, o1, aligned); break;
+        case 8: last_pass_store<8>(sm, pa, o0, o1, aligned); break;
+        case 10: last_pass_store<10>(sm, pa, o0, o1, aligned); break;
+        case 16: last_pass_store<16>(sm, pa, o0, o1, aligned); break;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -557,19 +717,30 @@ __global__ void direct_conv_kernel(int n, int ofs, int even, const double* __res
   }
 }
 
-// flags[j * rb + j2] = 1 iff columns j and j2 (j < j2) of B are bitwise equal.
+// flags[j * rb + j2] = 1 iff columns j and j2 (j < j2) of B are bitwise equal;
+// flags[j * rb + j] = 1 iff column j is mirror-symmetric (b[i] == b[n-1-i]).
 __global__ void dup_columns_kernel(const double* __restrict__ B, int64_t n, int rb, unsigned char* flags) {
   const int p = blockIdx.x;
-  int j = 0, rem = p;
-  while (rem >= rb - 1 - j) {
-    rem -= rb - 1 - j;
-    ++j;
+  int j, j2;
+  if (p < rb) {
+    j = j2 = p;
+  } else {
+    int rem = p - rb;
+    j = 0;
+    while (rem >= rb - 1 - j) {
+      rem -= rb - 1 - j;
+      ++j;
+    }
+    j2 = j + 1 + rem;
   }
-  const int j2 = j + 1 + rem;
   const unsigned long long* x = reinterpret_cast<const unsigned long long*>(B + j * n);
   const unsigned long long* y = reinterpret_cast<const unsigned long long*>(B + j2 * n);
   int same = 1;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) same &= (x[i] == y[i]);
+  if (j == j2) {
+    for (int64_t i = threadIdx.x; i < n / 2; i += blockDim.x) same &= (x[i] == x[n - 1 - i]);
+  } else {
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) same &= (x[i] == y[i]);
+  }
   same = __syncthreads_and(same);
   if (threadIdx.x == 0) flags[j * rb + j2] = static_cast<unsigned char>(same);
 }
@@ -595,32 +766,63 @@ void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const
   TGB_LAUNCHED(ctx);
 }
 
+template <int R0, bool BREAL>
+static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
+                        const PairEntry* dwork, int nwork, double* out) {
+  static bool attr = false;
+  if (!attr) {
+    TGB_CUDA(cudaFuncSetAttribute(pair_kernel<R0, BREAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ctx->smem_optin)));
+    attr = true;
+  }
+  int per_sm = 1;
+  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel<R0, BREAL>, pl.threads, pl.smem));
+  const int grid = std::max(1, std::min(nwork, std::max(1, per_sm) * ctx->num_sms));
+  prof_begin(ctx);
+  pair_kernel<R0, BREAL><<<grid, pl.threads, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, nwork, out);
+  TGB_LAUNCHED(ctx);
+  prof_end(ctx);
+}
+
+template <bool BREAL>
+static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
+                          const PairEntry* dwork, int nwork, double* out) {
+  switch (pl.a.r[0]) {
+    case 2: launch_pair<2, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 3: launch_pair<3, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 4: launch_pair<4, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 5: launch_pair<5, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 6: launch_pair<6, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 8: launch_pair<8, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 10: launch_pair<10, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    default: throw Error(TGB_CUDA_ERROR, "fftconv: unsupported first radix");
+  }
+}
+
 static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* X, int64_t ldx, const int* colidx,
-                            int cols, double2* spec, double phi_h) {
+                            int cols, void* spec, int mode, double h) {
   if (!cols) return;
   static bool attr_set = false;
   if (!attr_set) {
     TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin)));
-    TGB_CUDA(cudaFuncSetAttribute(pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(ctx->smem_optin)));
     attr_set = true;
   }
-  spectrum_kernel<<<cols, pl.threads, pl.smem, ctx->stream>>>(pl.a, X, ldx, colidx, spec, phi_h);
+  spectrum_kernel<<<cols, pl.threads, pl.smem, ctx->stream>>>(pl.a, X, ldx, colidx, spec, mode, h);
   TGB_LAUNCHED(ctx);
 }
 
-// Group bitwise-identical columns of B (device); returns representative list
-// and, per representative, its member columns.
-static std::vector<std::vector<int>> group_columns(tgb_ctx* ctx, int64_t n, int64_t rb, const double* B) {
-  std::vector<std::vector<int>> groups;
-  if (rb <= 1) {
-    if (rb == 1) groups.push_back({0});
-    return groups;
-  }
-  const int64_t npairs = rb * (rb - 1) / 2;
+struct ColumnGroups {
+  std::vector<std::vector<int>> groups;  // bitwise-identical columns, representative first
+  bool all_symmetric = true;
+};
+
+static ColumnGroups group_columns(tgb_ctx* ctx, int64_t n, int64_t rb, const double* B) {
+  ColumnGroups cg;
+  if (rb == 0) return cg;
+  const int64_t nblocks = rb + rb * (rb - 1) / 2;
   auto* flags = static_cast<unsigned char*>(ctx->ws_flags.get(rb * rb));
-  dup_columns_kernel<<<static_cast<unsigned>(npairs), 256, 0, ctx->stream>>>(B, n, static_cast<int>(rb), flags);
+  dup_columns_kernel<<<static_cast<unsigned>(nblocks), 256, 0, ctx->stream>>>(B, n, static_cast<int>(rb), flags);
   TGB_LAUNCHED(ctx);
   std::vector<unsigned char> h(rb * rb, 0);
   TGB_CUDA(cudaMemcpyAsync(h.data(), flags, rb * rb, cudaMemcpyDeviceToHost, ctx->stream));
@@ -628,15 +830,16 @@ static std::vector<std::vector<int>> group_columns(tgb_ctx* ctx, int64_t n, int6
   std::vector<int> rep(rb, -1);
   for (int j = 0; j < rb; ++j) {
     if (rep[j] >= 0) continue;
-    rep[j] = static_cast<int>(groups.size());
-    groups.push_back({j});
+    rep[j] = static_cast<int>(cg.groups.size());
+    cg.groups.push_back({j});
+    cg.all_symmetric = cg.all_symmetric && h[j * rb + j];
     for (int j2 = j + 1; j2 < rb; ++j2)
       if (rep[j2] < 0 && h[j * rb + j2]) {
         rep[j2] = rep[j];
-        groups.back().push_back(j2);
+        cg.groups.back().push_back(j2);
       }
   }
-  return groups;
+  return cg;
 }
 
 // out (n x ra*rb, column i + ra*j) = h * window(conv(A_i, B_j)); device pointers.
@@ -644,8 +847,9 @@ void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t
                    double* out) {
   if (ra == 0 || rb == 0) return;
   auto pl = get_plan(ctx, n);
-  const auto groups = group_columns(ctx, n, rb, B);
-  // work list: i-major so consecutive CTAs reuse A_i from L2
+  const ColumnGroups cg = group_columns(ctx, n, rb, B);
+  const auto& groups = cg.groups;
+  // work list: i-major so CTAs running concurrently share A_i and all B_j in L2
   std::vector<PairEntry> work;
   work.reserve(static_cast<size_t>(ra * groups.size()));
   for (int64_t i = 0; i < ra; ++i)
@@ -667,23 +871,23 @@ void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t
     direct_conv_kernel<<<static_cast<unsigned>(work.size()), th, 0, ctx->stream>>>(
         static_cast<int>(n), pl->a.ofs, pl->a.even, A, n, B, n, dwork, h, out);
     TGB_LAUNCHED(ctx);
-  } else {
-    const int N = pl->a.N;
-    auto* specA = static_cast<double2*>(ctx->ws_spec_a.get(static_cast<size_t>(ra) * (N + 1) * sizeof(double2)));
-    auto* specB =
-        static_cast<double2*>(ctx->ws_spec_b.get(static_cast<size_t>(groups.size()) * (N + 1) * sizeof(double2)));
-    std::vector<int> reps;
-    for (auto& g : groups) reps.push_back(g[0]);
-    auto* dreps = static_cast<int*>(ctx->ws_misc.get(reps.size() * sizeof(int)));
-    TGB_CUDA(cudaMemcpyAsync(dreps, reps.data(), reps.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-    launch_spectrum(ctx, *pl, A, n, nullptr, static_cast<int>(ra), specA, 0.0);
-    launch_spectrum(ctx, *pl, B, n, dreps, static_cast<int>(reps.size()), specB, h);
-    prof_begin(ctx);
-    pair_kernel<<<static_cast<unsigned>(work.size()), pl->threads, pl->smem, ctx->stream>>>(pl->a, specA, specB,
-                                                                                            dwork, out);
-    TGB_LAUNCHED(ctx);
-    prof_end(ctx);
+    return;
   }
+  const int N = pl->a.N;
+  const bool breal = cg.all_symmetric;
+  auto* specA = static_cast<double2*>(ctx->ws_spec_a.get(static_cast<size_t>(ra) * (N + 1) * sizeof(double2)));
+  void* specB =
+      ctx->ws_spec_b.get(static_cast<size_t>(groups.size()) * (N + 1) * (breal ? sizeof(double) : sizeof(double2)));
+  std::vector<int> reps;
+  for (auto& g : groups) reps.push_back(g[0]);
+  auto* dreps = static_cast<int*>(ctx->ws_misc.get(reps.size() * sizeof(int)));
+  TGB_CUDA(cudaMemcpyAsync(dreps, reps.data(), reps.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
+  launch_spectrum(ctx, *pl, A, n, nullptr, static_cast<int>(ra), specA, 0, 1.0);
+  launch_spectrum(ctx, *pl, B, n, dreps, static_cast<int>(reps.size()), specB, breal ? 1 : 2, h);
+  if (breal)
+    launch_pair_r<true>(ctx, *pl, specA, specB, dwork, static_cast<int>(work.size()), out);
+  else
+    launch_pair_r<false>(ctx, *pl, specA, specB, dwork, static_cast<int>(work.size()), out);
   // (pageable-source cudaMemcpyAsync stages the host vectors before returning)
 }
 
