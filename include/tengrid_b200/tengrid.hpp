@@ -1,0 +1,139 @@
+// tengrid_b200/tengrid.hpp — header-only C++ mirror of the reference's
+// hot-path API over the libtgb C-ABI (include/tgb.h).
+//
+// A reference build switches to the B200 path by replacing the bodies of
+// tg::convolve / tg::hartree_potential / tg::scalar_product /
+// tg::coulomb_matrix / tg::conv_central_many with calls into this header
+// (INTEGRATION.md).  It is templated on the matrix type so it works with
+// Eigen::MatrixXd / Eigen::VectorXd (column-major, data()/rows()/cols()/
+// size()) without including Eigen here.  Errors are rethrown as the
+// reference's exception classes (proj/include/tengrid/common.hpp:11-25).
+#pragma once
+
+#include <array>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "tgb.h"
+
+namespace tgb_cpp {
+
+struct SnapError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NumericalError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+inline void check(int rc) {
+  if (rc == TGB_OK) return;
+  const std::string msg = tgb_last_error();
+  switch (rc) {
+    case TGB_INVALID_ARGUMENT: throw std::invalid_argument(msg);
+    case TGB_DOMAIN_ERROR: throw std::domain_error(msg);
+    case TGB_SNAP_ERROR: throw SnapError(msg);
+    case TGB_NUMERICAL_ERROR: throw NumericalError(msg);
+    default: throw CudaError(msg);
+  }
+}
+
+// One context per thread per device (contexts are not shared across threads).
+inline tgb_ctx* context(int device = 0) {
+  struct Holder {
+    tgb_ctx* c = nullptr;
+    ~Holder() {
+      if (c) tgb_ctx_destroy(c);
+    }
+  };
+  thread_local Holder h;
+  if (!h.c) check(tgb_ctx_create(device, nullptr, &h.c));
+  return h.c;
+}
+
+// Canonical tensor with the reference's layout: factor[ax] n_ax x R
+// column-major, weight R.  Works for tg::CanonicalTensor3 (Eigen members).
+template <class Cp>
+tgb_cp view(const Cp& t) {
+  tgb_cp c{};
+  c.rank = static_cast<int64_t>(t.weight.size());
+  for (int ax = 0; ax < 3; ++ax) {
+    c.n[ax] = static_cast<int64_t>(t.factor[ax].rows());
+    c.factor[ax] = const_cast<double*>(t.factor[ax].data());
+  }
+  c.weight = const_cast<double*>(t.weight.data());
+  return c;
+}
+
+// tg::convolve (tensor.cpp:179-198).  Cp must be default-constructible with
+// resizable Eigen-like members (factor[ax] = Matrix(n, r); weight = Vector(r)).
+template <class Cp, class Matrix, class Vector>
+Cp convolve(const Cp& a, const Cp& b, const std::array<double, 3>& h) {
+  Cp out;
+  const auto r = a.weight.size() * b.weight.size();
+  for (int ax = 0; ax < 3; ++ax) out.factor[ax] = Matrix(a.factor[ax].rows(), r);
+  out.weight = Vector(r);
+  tgb_cp ca = view(a), cb = view(b), co = view(out);
+  check(tgb_convolve(context(), &ca, &cb, h.data(), &co, TGB_MEM_HOST));
+  return out;
+}
+
+// tg::hartree_potential (hf.cpp:131-138) on a primary-grid kernel tensor.
+template <class Cp, class Matrix, class Vector>
+Cp hartree_potential(const Cp& theta, const Cp& kernel, const std::array<double, 3>& h) {
+  Cp out;
+  const auto r = theta.weight.size() * kernel.weight.size();
+  for (int ax = 0; ax < 3; ++ax) out.factor[ax] = Matrix(theta.factor[ax].rows(), r);
+  out.weight = Vector(r);
+  tgb_cp ct = view(theta), ck = view(kernel), co = view(out);
+  check(tgb_hartree_potential(context(), &ct, &ck, h.data(), &co, TGB_MEM_HOST));
+  return out;
+}
+
+// tg::conv_central_many (fft.cpp:97-122).
+template <class Matrix, class Vec>
+Matrix conv_central_many(const Matrix& U, const Vec& v) {
+  Matrix out(U.rows(), U.cols());
+  check(tgb_conv_central_many(context(), U.rows(), U.cols(), U.data(), v.data(), out.data(), TGB_MEM_HOST));
+  return out;
+}
+
+// tg::scalar_product (tensor.cpp:88-98).
+template <class Cp>
+double scalar_product(const Cp& a, const Cp& b) {
+  tgb_cp ca = view(a), cb = view(b);
+  double r = 0.0;
+  check(tgb_scalar_product(context(), &ca, &cb, &r, TGB_MEM_HOST));
+  return r;
+}
+
+// tg::coulomb_matrix (hf.cpp:140-151): disc = discretize_basis(bs).
+template <class Cp, class Matrix>
+Matrix coulomb_matrix(const std::vector<Cp>& disc, const Cp& vh, const std::array<double, 3>& h) {
+  const int64_t nb = static_cast<int64_t>(disc.size());
+  std::vector<int64_t> off(nb + 1, 0);
+  for (int64_t k = 0; k < nb; ++k) off[k + 1] = off[k] + static_cast<int64_t>(disc[k].weight.size());
+  // flatten primitives into one canonical tensor (host copy, small)
+  std::array<std::vector<double>, 3> f;
+  std::vector<double> w;
+  for (const auto& d : disc) {
+    for (int ax = 0; ax < 3; ++ax) f[ax].insert(f[ax].end(), d.factor[ax].data(), d.factor[ax].data() + d.factor[ax].size());
+    w.insert(w.end(), d.weight.data(), d.weight.data() + d.weight.size());
+  }
+  tgb_cp flat{};
+  flat.rank = off[nb];
+  for (int ax = 0; ax < 3; ++ax) {
+    flat.n[ax] = disc.empty() ? 0 : static_cast<int64_t>(disc[0].factor[ax].rows());
+    flat.factor[ax] = f[ax].data();
+  }
+  flat.weight = w.data();
+  tgb_cp cv = view(vh);
+  Matrix J(nb, nb);
+  check(tgb_coulomb_matrix(context(), &flat, off.data(), nb, &cv, h.data(), J.data(), TGB_MEM_HOST));
+  return J;
+}
+
+}  // namespace tgb_cpp

@@ -392,13 +392,21 @@ __device__ __forceinline__ void apply_twiddles(double2* v, double2 w) {
 template <int R, int S>
 __device__ __forceinline__ void dit_pass(double2* sm, int N, int L, const double2* __restrict__ twp) {
   const int nbf = N / R;
-  for (int bf = threadIdx.x; bf < nbf; bf += blockDim.x) {
-    const int j = bf % L;
-    const int base = (bf - j) * R + j;
+  const int T = blockDim.x, dT = T / L, mT = T - dT * L;
+  int j = threadIdx.x % L, G = threadIdx.x / L;
+  for (int bf = threadIdx.x; bf < nbf; bf += T) {
+    const int base = G * L * R + j;
+    const int jt = j;
+    j += mT;
+    G += dT;
+    if (j >= L) {
+      j -= L;
+      ++G;
+    }
     double2 v[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) v[s] = sm[pidx(base + s * L)];
-    if (L > 1) apply_twiddles<R, S>(v, ld2(twp + j));
+    if (L > 1) apply_twiddles<R, S>(v, ld2(twp + jt));
     dft<R, S>(v);
 #pragma unroll
     for (int t = 0; t < R; ++t) sm[pidx(base + t * L)] = v[t];
@@ -463,55 +471,59 @@ __device__ __forceinline__ double2 zsplit(double2 p, double2 q, double2 w) {
   return make_double2(sum.x - wd.y, sum.y + wd.x);
 }
 
-// product P = A * B for R consecutive stored positions starting at pos
-template <int R, bool BREAL>
-__device__ __forceinline__ void load_product(double2* v, const double2* __restrict__ A, const void* __restrict__ Bv,
-                                             int pos) {
-  if constexpr (BREAL) {
-    const double* B = static_cast<const double*>(Bv) + pos;
-    double b[R];
+// Stage P = A * B (stored order, N+1 entries) into shared memory with fully
+// coalesced, 8-deep batched L2 loads.
+template <bool BREAL>
+__device__ __forceinline__ void stage_product(double2* sm, int N, const double2* __restrict__ A,
+                                              const void* __restrict__ Bv) {
+  constexpr int U = 8;
+  const int T = blockDim.x;
+  int pos0 = threadIdx.x;
+  for (; pos0 + (U - 1) * T <= N; pos0 += U * T) {
+    double2 a[U];
+    if constexpr (BREAL) {
+      double b[U];
 #pragma unroll
-    for (int s = 0; s < R; ++s) {
-      v[s] = ld2(A + pos + s);
-      b[s] = __ldg(B + s);
+      for (int u = 0; u < U; ++u) {
+        a[u] = ld2(A + pos0 + u * T);
+        b[u] = __ldg(static_cast<const double*>(Bv) + pos0 + u * T);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) sm[pidx(pos0 + u * T)] = cscale(a[u], b[u]);
+    } else {
+      double2 b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        a[u] = ld2(A + pos0 + u * T);
+        b[u] = ld2(static_cast<const double2*>(Bv) + pos0 + u * T);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) sm[pidx(pos0 + u * T)] = cmul(a[u], b[u]);
     }
-#pragma unroll
-    for (int s = 0; s < R; ++s) v[s] = cscale(v[s], b[s]);
-  } else {
-    const double2* B = static_cast<const double2*>(Bv) + pos;
-    double2 b[R];
-#pragma unroll
-    for (int s = 0; s < R; ++s) {
-      v[s] = ld2(A + pos + s);
-      b[s] = ld2(B + s);
-    }
-#pragma unroll
-    for (int s = 0; s < R; ++s) v[s] = cmul(v[s], b[s]);
+  }
+  for (int pos = pos0; pos <= N; pos += T) {
+    if constexpr (BREAL)
+      sm[pidx(pos)] = cscale(ld2(A + pos), __ldg(static_cast<const double*>(Bv) + pos));
+    else
+      sm[pidx(pos)] = cmul(ld2(A + pos), ld2(static_cast<const double2*>(Bv) + pos));
   }
 }
 
-template <bool BREAL>
-__device__ __forceinline__ double2 load_product1(const double2* __restrict__ A, const void* __restrict__ Bv, int pos) {
-  if constexpr (BREAL) return cscale(ld2(A + pos), __ldg(static_cast<const double*>(Bv) + pos));
-  else return cmul(ld2(A + pos), ld2(static_cast<const double2*>(Bv) + pos));
-}
-
-// First inverse pass straight from the spectra in L2: product, real split,
-// radix-R butterflies on the paired blocks, results to shared memory.
-template <int R, bool BREAL>
-__device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa, const double2* __restrict__ A,
-                                               const void* __restrict__ B) {
+// First inverse pass on the staged product: real split, radix-R butterflies
+// on the paired blocks g (frequencies kk + s N/R) and g2 (the mirrors N - k),
+// in place in shared memory.
+template <int R>
+__device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa) {
   const int N = pa.N;
   for (int q = threadIdx.x; q < pa.npl; q += blockDim.x) {
     const int2 gg = __ldg(pa.leader + q);
     const int g = gg.x, g2 = gg.y;
     double2 a[R];
-    load_product<R, BREAL>(a, A, B, g * R);
-    const double2 wk = ld2(pa.twz + g);
+#pragma unroll
+    for (int s = 0; s < R; ++s) a[s] = sm[pidx(g * R + s)];
     if (g == 0) {
       // natural frequencies s*N/R; mirror of s is R-s (s=0 mirrors to N)
-      const double2 pn = load_product1<BREAL>(A, B, N);
-      const double2 z0 = zsplit(a[0], pn, make_double2(1.0, 0.0));
+      const double2 z0 = zsplit(a[0], sm[pidx(N)], make_double2(1.0, 0.0));
 #pragma unroll
       for (int s = 1; 2 * s <= R; ++s) {
         const double2 ws = ld2(pa.cs + s), wr = ld2(pa.cs + (R - s));
@@ -529,6 +541,7 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa, 
 #pragma unroll
       for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
     } else if (g2 == g) {
+      const double2 wk = ld2(pa.twz + g);
 #pragma unroll
       for (int s = 0; 2 * s < R - 1; ++s) {
         const double2 w1 = cmul(wk, ld2(pa.cs + s)), w2 = cmul(wk, ld2(pa.cs + (R - 1 - s)));
@@ -545,9 +558,10 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa, 
 #pragma unroll
       for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
     } else {
+      const double2 wk = ld2(pa.twz + g), wk2 = ld2(pa.twz + g2);
       double2 b[R];
-      load_product<R, BREAL>(b, A, B, g2 * R);
-      const double2 wk2 = ld2(pa.twz + g2);
+#pragma unroll
+      for (int s = 0; s < R; ++s) b[s] = sm[pidx(g2 * R + s)];
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const double2 cs1 = ld2(pa.cs + s), cs2 = ld2(pa.cs + (R - 1 - s));
@@ -581,12 +595,11 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   const int c = blockIdx.x;
   const double* x = X + (colidx ? colidx[c] : c) * ldx;
   const int n = pa.n, N = pa.N;
-  for (int pos = threadIdx.x; pos < N; pos += blockDim.x) {
-    const int k = pa.perm[pos];
+  for (int k = threadIdx.x; k < N; k += blockDim.x) {  // natural order: coalesced reads
     const int i0 = 2 * k;
     const double x0 = i0 < n ? __ldg(x + i0) : 0.0;
     const double x1 = i0 + 1 < n ? __ldg(x + i0 + 1) : 0.0;
-    sm[pidx(pos)] = make_double2(x0, x1);
+    sm[pidx(__ldg(pa.inv + k))] = make_double2(x0, x1);
   }
   __syncthreads();
   // forward DIT; pass 0 has no twiddles (L = 1)
@@ -606,7 +619,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     __syncthreads();
   }
   const double hm = h / pa.m;
-  for (int k = threadIdx.x; k <= N; k += blockDim.x) {
+  for (int pos = threadIdx.x; pos <= N; pos += blockDim.x) {  // stored order: coalesced writes
+    const int k = pos < N ? __ldg(pa.perm + pos) : N;
     const double2 zk = sm[pidx(k == N ? 0 : k)];
     double2 zm = sm[pidx(k == 0 ? 0 : N - k)];
     zm.y = -zm.y;
@@ -615,7 +629,6 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     w.y = -w.y;  // w^-k
     const double2 wd = cmul(w, dif);
     const double2 Xk = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
-    const int pos = k < N ? pa.inv[k] : N;
     if (mode == 0) {
       static_cast<double2*>(spec)[static_cast<int64_t>(c) * (N + 1) + pos] = Xk;
     } else if (mode == 1) {
@@ -658,7 +671,9 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
     const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
                           : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
-    first_pass_inv<R0, BREAL>(sm, pa, a, b);
+    stage_product<BREAL>(sm, N, a, b);
+    __syncthreads();
+    first_pass_inv<R0>(sm, pa);
     __syncthreads();
     for (int p = 1; p + 1 < pa.P; ++p) {
       dit_pass_rt<1>(sm, pa, p);
