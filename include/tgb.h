@@ -106,6 +106,14 @@ int tgb_scalar_product(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, double* r
 int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
                        const double h[3], double* J, int mem);
 
+/* ---- dense FP64 building block -------------------------------------------
+ * C = alpha op(A) op(B) + beta C on the FP64 tensor cores (DMMA), column-major
+ * DEVICE pointers, stream-ordered on the context stream.  The dense products
+ * of reduction.cpp / tei.cpp (Gram matrices, projections, unfoldings) run on
+ * it; exported for tests and callers that hold device matrices. */
+int tgb_dgemm(tgb_ctx* ctx, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+              int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
+
 /* ---- lattice sums ------------------------------------------------------------
  * replaces the per-axis assembly of tg::lattice_sum_canonical / _tucker /
  * _composite (lattice.hpp:56-69, lattice.cpp:50-61,116-165):

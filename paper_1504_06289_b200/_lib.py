@@ -75,6 +75,7 @@ def lib() -> C.CDLL:
             "tgb_scalar_product": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), C.POINTER(D), I]),
             "tgb_coulomb_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, P, I]),
             "tgb_lattice_assemble_axis": (I, [P, I64, I64, P, P, I64, P, I]),
+            "tgb_dgemm": (I, [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64]),
             "tgb_host_last_error": (C.c_char_p, []),
             "tgb_mesh_size": (D, [D, I64]),
             "tgb_snap_to_node": (I, [D, I64, D, C.POINTER(I64)]),

@@ -143,6 +143,10 @@ struct DevCP {
 
 }  // namespace
 
+namespace tgb {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace tgb
+
 extern "C" {
 
 const char* tgb_last_error(void) { return g_last_error.c_str(); }

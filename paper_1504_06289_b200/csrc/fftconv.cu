@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <tuple>
@@ -51,14 +52,18 @@ constexpr int kMaxThreads = 384;
 
 struct PlanArgs {
   int n, N, m, P, ofs, even, npl;
+  int dbg;  // analysis only (TGB_PAIR_DBG): 1 skip stores, 2 skip L2 loads, 4 skip passes
   int r[kMaxPasses];
   int L[kMaxPasses];
   const int* perm;       // stored position -> natural frequency index (N entries)
   const int* inv;        // natural frequency index -> stored position (N entries)
-  const int2* leader;    // first-pass block pairs (g, g2), g <= g2 (npl entries)
-  const double2* twz;    // first pass: w_m^{kk(g)} per block g (N/r0 entries)
-  const double2* cs;     // first pass: w_m^{s N/r0}, s < r0
-  const double2* twp[kMaxPasses];  // pass p >= 1: w_{L_p r_p}^j, j < L_p   (w = exp(+2 pi i / .))
+  const int4* leader;    // first-pass block pairs (g, g2, kk(g), kk(g2)), g <= g2 (npl entries)
+  const double2* tw;     // twiddle tables, copied to shared memory by every CTA (ntw entries):
+                         //   [off_cs]   w_m^{s N/r0}, s < r0
+                         //   [off_zlo]  w_m^i, i < 64;  [off_zhi] w_m^{64 h}
+                         //   [off_lo[p]] w_{L_p r_p}^i, i < 64;  [off_hi[p]] w_{L_p r_p}^{64 h}   (p >= 1)
+  int ntw, off_cs, off_zlo, off_zhi;
+  int off_lo[kMaxPasses], off_hi[kMaxPasses];
   const double2* twpost; // forward post-processing: w_m^k, k <= N
 };
 
@@ -67,7 +72,7 @@ struct ConvPlan {
   bool direct = false;
   int threads = 0;
   size_t smem = 0;
-  DevBuf perm, inv, leader, twz, cs, twp, twpost;
+  DevBuf perm, inv, leader, tw, twpost;
 };
 
 __host__ __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
@@ -79,8 +84,7 @@ static bool five_smooth(int64_t x) {
   return x == 1;
 }
 
-// Fewest passes; then a first radix of 8..10 (pass 0 holds two blocks in
-// registers); then the largest smallest radix.
+// Radix sequence (pass order) for an N-point transform.
 static bool factor_radices(int N, std::vector<int>& best) {
   static const int kR[] = {16, 10, 8, 6, 5, 4, 3, 2};
   std::vector<std::vector<int>> all;
@@ -100,26 +104,16 @@ static bool factor_radices(int N, std::vector<int>& best) {
   };
   rec(N, 16);
   if (all.empty()) return false;
-  auto score = [](const std::vector<int>& v) {
-    int first = 0;
-    for (int r : v)
-      if (r <= 10) {
-        first = r;
-        break;
-      }
-    return std::make_tuple(static_cast<int>(v.size()), first >= 8 ? 0 : (first >= 4 ? 1 : 2), -v.back());
+  // fewest passes; then a radix-16 first pass (its padded block stride is
+  // bank-conflict free), else the largest first radix; then the largest
+  // smallest radix
+  auto first_of = [](const std::vector<int>& v) { return v.front(); };
+  auto score = [&](const std::vector<int>& v) {
+    const int f = first_of(v);
+    return std::make_tuple(static_cast<int>(v.size()), f == 16 ? 0 : 1, -f, -v.back());
   };
   std::stable_sort(all.begin(), all.end(), [&](const auto& x, const auto& y) { return score(x) < score(y); });
   best = all.front();
-  // pass 0 = largest radix <= 10, the rest descending
-  int idx = -1;
-  for (size_t i = 0; i < best.size(); ++i)
-    if (best[i] <= 10) {
-      idx = static_cast<int>(i);
-      break;
-    }
-  if (idx < 0) return false;
-  if (idx > 0) std::rotate(best.begin(), best.begin() + idx, best.begin() + idx + 1);
   return true;
 }
 
@@ -147,8 +141,9 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
   a.N = static_cast<int>(N);
   a.m = static_cast<int>(2 * N);
   std::vector<int> rad;
-  const bool fits = N < (1 << 24) && plan_smem(a.N) <= ctx->smem_optin && factor_radices(a.N, rad);
+  const bool fits = N < (1 << 24) && plan_smem(a.N) + 8192 <= ctx->smem_optin && factor_radices(a.N, rad);
   pl->direct = n <= ctx->direct_max || !fits;
+  a.dbg = getenv("TGB_PAIR_DBG") ? atoi(getenv("TGB_PAIR_DBG")) : 0;
   if (!pl->direct) {
     a.P = static_cast<int>(rad.size());
     int L = 1;
@@ -171,22 +166,28 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
       inv[k] = static_cast<int>(pos);
     }
     const int r0 = rad[0], nblk = a.N / r0;
-    std::vector<int2> leaders;
-    std::vector<double2> twz(nblk), cs(r0);
+    std::vector<int4> leaders;
     for (int g = 0; g < nblk; ++g) {
       const int kk = perm[static_cast<size_t>(g) * r0];
       const int g2 = kk == 0 ? g : inv[nblk - kk] / r0;
-      if (g2 >= g) leaders.push_back(make_int2(g, g2));
-      twz[g] = unit_root(kk, a.m);
+      if (g2 >= g) leaders.push_back(make_int4(g, g2, kk, perm[static_cast<size_t>(g2) * r0]));
     }
-    for (int s = 0; s < r0; ++s) cs[s] = unit_root(static_cast<int64_t>(s) * nblk, a.m);
     a.npl = static_cast<int>(leaders.size());
-    std::vector<double2> twp;
-    std::vector<size_t> twp_off(a.P, 0);
+    std::vector<double2> tw;
+    a.off_cs = 0;
+    for (int s = 0; s < r0; ++s) tw.push_back(unit_root(static_cast<int64_t>(s) * nblk, a.m));
+    a.off_zlo = static_cast<int>(tw.size());
+    for (int i = 0; i < 64; ++i) tw.push_back(unit_root(i, a.m));
+    a.off_zhi = static_cast<int>(tw.size());
+    for (int h = 0; h <= nblk / 64; ++h) tw.push_back(unit_root(64LL * h, a.m));
     for (int p = 1; p < a.P; ++p) {
-      twp_off[p] = twp.size();
-      for (int j = 0; j < a.L[p]; ++j) twp.push_back(unit_root(j, static_cast<int64_t>(a.L[p]) * a.r[p]));
+      const int64_t LR = static_cast<int64_t>(a.L[p]) * a.r[p];
+      a.off_lo[p] = static_cast<int>(tw.size());
+      for (int i = 0; i < std::min(64, a.L[p]); ++i) tw.push_back(unit_root(i, LR));
+      a.off_hi[p] = static_cast<int>(tw.size());
+      for (int h = 0; h <= (a.L[p] - 1) / 64; ++h) tw.push_back(unit_root(64LL * h, LR));
     }
+    a.ntw = static_cast<int>(tw.size());
     std::vector<double2> twpost(a.N + 1);
     for (int k = 0; k <= a.N; ++k) twpost[k] = unit_root(k, a.m);
     auto up = [&](DevBuf& b, const void* src, size_t bytes) {
@@ -196,13 +197,10 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
     };
     a.perm = static_cast<const int*>(up(pl->perm, perm.data(), perm.size() * sizeof(int)));
     a.inv = static_cast<const int*>(up(pl->inv, inv.data(), inv.size() * sizeof(int)));
-    a.leader = static_cast<const int2*>(up(pl->leader, leaders.data(), leaders.size() * sizeof(int2)));
-    a.twz = static_cast<const double2*>(up(pl->twz, twz.data(), twz.size() * sizeof(double2)));
-    a.cs = static_cast<const double2*>(up(pl->cs, cs.data(), cs.size() * sizeof(double2)));
-    auto* tp = static_cast<const double2*>(up(pl->twp, twp.data(), twp.size() * sizeof(double2)));
-    for (int p = 1; p < a.P; ++p) a.twp[p] = tp + twp_off[p];
+    a.leader = static_cast<const int4*>(up(pl->leader, leaders.data(), leaders.size() * sizeof(int4)));
+    a.tw = static_cast<const double2*>(up(pl->tw, tw.data(), tw.size() * sizeof(double2)));
     a.twpost = static_cast<const double2*>(up(pl->twpost, twpost.data(), twpost.size() * sizeof(double2)));
-    pl->smem = plan_smem(a.N);
+    pl->smem = plan_smem(a.N) + static_cast<size_t>(a.ntw) * sizeof(double2);
     // threads: best butterfly balance over the passes, at least 8 warps when possible
     double best_eff = -1.0;
     int best_t = 64;
@@ -389,77 +387,157 @@ __device__ __forceinline__ void apply_twiddles(double2* v, double2 w) {
 }
 
 // In-place DIT pass of radix R and span L over N elements in shared memory.
+// K butterflies per thread are loaded, computed and stored together (ILP);
+// the remainder runs one at a time.
 template <int R, int S>
-__device__ __forceinline__ void dit_pass(double2* sm, int N, int L, const double2* __restrict__ twp) {
+__device__ __forceinline__ void bfly_one(double2* sm, int base, int jt, int L, const double2* lo, const double2* hi) {
+  double2 v[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) v[s] = sm[pidx(base + s * L)];
+  if (L > 1) apply_twiddles<R, S>(v, cmul(lo[jt & 63], hi[jt >> 6]));
+  dft<R, S>(v);
+#pragma unroll
+  for (int t = 0; t < R; ++t) sm[pidx(base + t * L)] = v[t];
+}
+
+template <int R, int S>
+__device__ __forceinline__ void bfly_two(double2* sm, int b0, int j0, int b1, int j1, int L, const double2* lo,
+                                         const double2* hi) {
+  double2 v[R], u[R];
+#pragma unroll
+  for (int s = 0; s < R; ++s) {
+    v[s] = sm[pidx(b0 + s * L)];
+    u[s] = sm[pidx(b1 + s * L)];
+  }
+  if (L > 1) {
+    apply_twiddles<R, S>(v, cmul(lo[j0 & 63], hi[j0 >> 6]));
+    apply_twiddles<R, S>(u, cmul(lo[j1 & 63], hi[j1 >> 6]));
+  }
+  dft<R, S>(v);
+  dft<R, S>(u);
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    sm[pidx(b0 + t * L)] = v[t];
+    sm[pidx(b1 + t * L)] = u[t];
+  }
+}
+
+template <int R, int S, int K>
+__device__ __forceinline__ void dit_pass_k(double2* sm, int N, int L, const double2* lo, const double2* hi) {
   const int nbf = N / R;
   const int T = blockDim.x, dT = T / L, mT = T - dT * L;
   int j = threadIdx.x % L, G = threadIdx.x / L;
-  for (int bf = threadIdx.x; bf < nbf; bf += T) {
-    const int base = G * L * R + j;
-    const int jt = j;
+  int bf = threadIdx.x;
+  if constexpr (K == 2) {
+    for (; bf + T < nbf; bf += 2 * T) {
+      const int b0 = G * L * R + j, j0 = j;
+      j += mT;
+      G += dT;
+      if (j >= L) {
+        j -= L;
+        ++G;
+      }
+      const int b1 = G * L * R + j, j1 = j;
+      j += mT;
+      G += dT;
+      if (j >= L) {
+        j -= L;
+        ++G;
+      }
+      bfly_two<R, S>(sm, b0, j0, b1, j1, L, lo, hi);
+    }
+  }
+  for (; bf < nbf; bf += T) {
+    bfly_one<R, S>(sm, G * L * R + j, j, L, lo, hi);
     j += mT;
     G += dT;
     if (j >= L) {
       j -= L;
       ++G;
     }
-    double2 v[R];
-#pragma unroll
-    for (int s = 0; s < R; ++s) v[s] = sm[pidx(base + s * L)];
-    if (L > 1) apply_twiddles<R, S>(v, ld2(twp + jt));
-    dft<R, S>(v);
-#pragma unroll
-    for (int t = 0; t < R; ++t) sm[pidx(base + t * L)] = v[t];
   }
 }
 
+template <int R, int S>
+__device__ __forceinline__ void dit_pass(double2* sm, int N, int L, const double2* lo, const double2* hi) {
+  dit_pass_k<R, S, 1>(sm, N, L, lo, hi);  // 2-way interleave measured slower (v5)
+}
+
 template <int S>
-__device__ __forceinline__ void dit_pass_rt(double2* sm, const PlanArgs& pa, int p) {
-  const double2* tw = pa.twp[p];
+__device__ __forceinline__ void dit_pass_rt(double2* sm, const double2* tws, const PlanArgs& pa, int p) {
+  const double2* lo = tws + pa.off_lo[p];
+  const double2* hi = tws + pa.off_hi[p];
   switch (pa.r[p]) {
-    case 2: dit_pass<2, S>(sm, pa.N, pa.L[p], tw); break;
-    case 3: dit_pass<3, S>(sm, pa.N, pa.L[p], tw); break;
-    case 4: dit_pass<4, S>(sm, pa.N, pa.L[p], tw); break;
-    case 5: dit_pass<5, S>(sm, pa.N, pa.L[p], tw); break;
-    case 6: dit_pass<6, S>(sm, pa.N, pa.L[p], tw); break;
-    case 8: dit_pass<8, S>(sm, pa.N, pa.L[p], tw); break;
-    case 10: dit_pass<10, S>(sm, pa.N, pa.L[p], tw); break;
-    case 16: dit_pass<16, S>(sm, pa.N, pa.L[p], tw); break;
+    case 2: dit_pass<2, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 3: dit_pass<3, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 4: dit_pass<4, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 5: dit_pass<5, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 6: dit_pass<6, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 8: dit_pass<8, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 10: dit_pass<10, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 16: dit_pass<16, S>(sm, pa.N, pa.L[p], lo, hi); break;
   }
 }
 
 // Last inverse pass: butterflies, then the windowed outputs straight to HBM.
 // z[t] = x[2t] + i x[2t+1]; only t < ceil(n/2) is stored.
 template <int R>
-__device__ __forceinline__ void last_pass_store(const double2* sm, const PlanArgs& pa, double* o0, double* o1,
-                                                bool aligned) {
+__device__ __forceinline__ void store_outputs(const double2* v, int j, int L, int nz, bool odd_n, double* o0,
+                                              double* o1, bool aligned) {
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    const int idx = j + t * L;
+    if (idx >= nz || !o0) continue;
+    const bool full = !(odd_n && idx == nz - 1);
+    if (aligned && full) {
+      __stcs(reinterpret_cast<double2*>(o0 + 2 * idx), v[t]);
+      if (o1) __stcs(reinterpret_cast<double2*>(o1 + 2 * idx), v[t]);
+    } else {
+      __stcs(o0 + 2 * idx, v[t].x);
+      if (full) __stcs(o0 + 2 * idx + 1, v[t].y);
+      if (o1) {
+        __stcs(o1 + 2 * idx, v[t].x);
+        if (full) __stcs(o1 + 2 * idx + 1, v[t].y);
+      }
+    }
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void last_pass_store(const double2* sm, const double2* tws, const PlanArgs& pa, double* o0,
+                                                double* o1, bool aligned) {
   const int N = pa.N, L = pa.L[pa.P - 1], nbf = N / R;
   const int nz = (pa.n + 1) >> 1;
   const bool odd_n = pa.n & 1;
-  const double2* tw = pa.twp[pa.P - 1];
-  for (int j = threadIdx.x; j < nbf; j += blockDim.x) {
+  const double2* lo = tws + pa.off_lo[pa.P - 1];
+  const double2* hi = tws + pa.off_hi[pa.P - 1];
+  const int T = blockDim.x;
+  int j = threadIdx.x;
+  if constexpr (false) {
+    for (; j + T < nbf; j += 2 * T) {
+      double2 v[R], u[R];
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        v[s] = sm[pidx(j + s * L)];
+        u[s] = sm[pidx(j + T + s * L)];
+      }
+      if (L > 1) {
+        apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
+        apply_twiddles<R, 1>(u, cmul(lo[(j + T) & 63], hi[(j + T) >> 6]));
+      }
+      dft<R, 1>(v);
+      dft<R, 1>(u);
+      store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
+      store_outputs<R>(u, j + T, L, nz, odd_n, o0, o1, aligned);
+    }
+  }
+  for (; j < nbf; j += T) {
     double2 v[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) v[s] = sm[pidx(j + s * L)];
-    if (L > 1) apply_twiddles<R, 1>(v, ld2(tw + j));
+    if (L > 1) apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
     dft<R, 1>(v);
-#pragma unroll
-    for (int t = 0; t < R; ++t) {
-      const int idx = j + t * L;
-      if (idx >= nz) continue;
-      const bool full = !(odd_n && idx == nz - 1);
-      if (aligned && full) {
-        __stcs(reinterpret_cast<double2*>(o0 + 2 * idx), v[t]);
-        if (o1) __stcs(reinterpret_cast<double2*>(o1 + 2 * idx), v[t]);
-      } else {
-        __stcs(o0 + 2 * idx, v[t].x);
-        if (full) __stcs(o0 + 2 * idx + 1, v[t].y);
-        if (o1) {
-          __stcs(o1 + 2 * idx, v[t].x);
-          if (full) __stcs(o1 + 2 * idx + 1, v[t].y);
-        }
-      }
-    }
+    store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
   }
 }
 
@@ -479,7 +557,7 @@ __device__ __forceinline__ void stage_product(double2* sm, int N, const double2*
   constexpr int U = 8;
   const int T = blockDim.x;
   int pos0 = threadIdx.x;
-  for (; pos0 + (U - 1) * T <= N; pos0 += U * T) {
+  for (; pos0 + (U - 1) * T < N; pos0 += U * T) {
     double2 a[U];
     if constexpr (BREAL) {
       double b[U];
@@ -501,7 +579,7 @@ __device__ __forceinline__ void stage_product(double2* sm, int N, const double2*
       for (int u = 0; u < U; ++u) sm[pidx(pos0 + u * T)] = cmul(a[u], b[u]);
     }
   }
-  for (int pos = pos0; pos <= N; pos += T) {
+  for (int pos = pos0; pos < N; pos += T) {
     if constexpr (BREAL)
       sm[pidx(pos)] = cscale(ld2(A + pos), __ldg(static_cast<const double*>(Bv) + pos));
     else
@@ -511,29 +589,36 @@ __device__ __forceinline__ void stage_product(double2* sm, int N, const double2*
 
 // First inverse pass on the staged product: real split, radix-R butterflies
 // on the paired blocks g (frequencies kk + s N/R) and g2 (the mirrors N - k),
-// in place in shared memory.
+// in place in shared memory.  Twiddles w_m^{kk} from the two-level table.
 template <int R>
-__device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa) {
+__device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, const PlanArgs& pa,
+                                               const double2* __restrict__ A, const void* __restrict__ B,
+                                               bool breal) {
   const int N = pa.N;
+  const double2* cs = tws + pa.off_cs;
+  const double2* zlo = tws + pa.off_zlo;
+  const double2* zhi = tws + pa.off_zhi;
   for (int q = threadIdx.x; q < pa.npl; q += blockDim.x) {
-    const int2 gg = __ldg(pa.leader + q);
+    const int4 gg = __ldg(pa.leader + q);
     const int g = gg.x, g2 = gg.y;
     double2 a[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) a[s] = sm[pidx(g * R + s)];
     if (g == 0) {
-      // natural frequencies s*N/R; mirror of s is R-s (s=0 mirrors to N)
-      const double2 z0 = zsplit(a[0], sm[pidx(N)], make_double2(1.0, 0.0));
+      // natural frequencies s*N/R; mirror of s is R-s (s = 0 mirrors to the Nyquist term N)
+      const double2 an = ld2(A + N);
+      const double2 pn = breal ? cscale(an, __ldg(static_cast<const double*>(B) + N))
+                               : cmul(an, ld2(static_cast<const double2*>(B) + N));
+      const double2 z0 = zsplit(a[0], pn, make_double2(1.0, 0.0));
 #pragma unroll
       for (int s = 1; 2 * s <= R; ++s) {
-        const double2 ws = ld2(pa.cs + s), wr = ld2(pa.cs + (R - s));
         if (2 * s < R) {
-          const double2 zs = zsplit(a[s], a[R - s], ws);
-          const double2 zr = zsplit(a[R - s], a[s], wr);
+          const double2 zs = zsplit(a[s], a[R - s], cs[s]);
+          const double2 zr = zsplit(a[R - s], a[s], cs[R - s]);
           a[s] = zs;
           a[R - s] = zr;
         } else {
-          a[s] = zsplit(a[s], a[s], ws);
+          a[s] = zsplit(a[s], a[s], cs[s]);
         }
       }
       a[0] = z0;
@@ -541,32 +626,31 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa) 
 #pragma unroll
       for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
     } else if (g2 == g) {
-      const double2 wk = ld2(pa.twz + g);
+      const double2 wk = cmul(zlo[gg.z & 63], zhi[gg.z >> 6]);
 #pragma unroll
       for (int s = 0; 2 * s < R - 1; ++s) {
-        const double2 w1 = cmul(wk, ld2(pa.cs + s)), w2 = cmul(wk, ld2(pa.cs + (R - 1 - s)));
-        const double2 z1 = zsplit(a[s], a[R - 1 - s], w1);
-        const double2 z2 = zsplit(a[R - 1 - s], a[s], w2);
+        const double2 z1 = zsplit(a[s], a[R - 1 - s], cmul(wk, cs[s]));
+        const double2 z2 = zsplit(a[R - 1 - s], a[s], cmul(wk, cs[R - 1 - s]));
         a[s] = z1;
         a[R - 1 - s] = z2;
       }
       if (R & 1) {
         const int s = (R - 1) / 2;
-        a[s] = zsplit(a[s], a[s], cmul(wk, ld2(pa.cs + s)));
+        a[s] = zsplit(a[s], a[s], cmul(wk, cs[s]));
       }
       dft<R, 1>(a);
 #pragma unroll
       for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
     } else {
-      const double2 wk = ld2(pa.twz + g), wk2 = ld2(pa.twz + g2);
+      const double2 wk = cmul(zlo[gg.z & 63], zhi[gg.z >> 6]);
+      const double2 wk2 = cmul(zlo[gg.w & 63], zhi[gg.w >> 6]);
       double2 b[R];
 #pragma unroll
       for (int s = 0; s < R; ++s) b[s] = sm[pidx(g2 * R + s)];
 #pragma unroll
       for (int s = 0; s < R; ++s) {
-        const double2 cs1 = ld2(pa.cs + s), cs2 = ld2(pa.cs + (R - 1 - s));
-        const double2 za = zsplit(a[s], b[R - 1 - s], cmul(wk, cs1));
-        const double2 zb = zsplit(b[R - 1 - s], a[s], cmul(wk2, cs2));
+        const double2 za = zsplit(a[s], b[R - 1 - s], cmul(wk, cs[s]));
+        const double2 zb = zsplit(b[R - 1 - s], a[s], cmul(wk2, cs[R - 1 - s]));
         a[s] = za;
         b[R - 1 - s] = zb;
       }
@@ -581,6 +665,12 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const PlanArgs& pa) 
   }
 }
 
+__device__ __forceinline__ double2* load_tables(double2* sm, const PlanArgs& pa) {
+  double2* tws = sm + pidx(pa.N) + 1;
+  for (int i = threadIdx.x; i < pa.ntw; i += blockDim.x) tws[i] = ld2(pa.tw + i);
+  return tws;
+}
+
 // ------------------------------------------------------------------ kernels
 
 // Forward spectrum of real columns, stored in DIT order (N+1 entries, the
@@ -592,6 +682,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     spectrum_kernel(PlanArgs pa, const double* __restrict__ X, int64_t ldx, const int* __restrict__ colidx,
                     void* __restrict__ spec, int mode, double h) {
   extern __shared__ double2 sm[];
+  const double2* tws = load_tables(sm, pa);
   const int c = blockIdx.x;
   const double* x = X + (colidx ? colidx[c] : c) * ldx;
   const int n = pa.n, N = pa.N;
@@ -604,18 +695,18 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
   __syncthreads();
   // forward DIT; pass 0 has no twiddles (L = 1)
   switch (pa.r[0]) {
-    case 2: dit_pass<2, -1>(sm, N, 1, nullptr); break;
-    case 3: dit_pass<3, -1>(sm, N, 1, nullptr); break;
-    case 4: dit_pass<4, -1>(sm, N, 1, nullptr); break;
-    case 5: dit_pass<5, -1>(sm, N, 1, nullptr); break;
-    case 6: dit_pass<6, -1>(sm, N, 1, nullptr); break;
-    case 8: dit_pass<8, -1>(sm, N, 1, nullptr); break;
-    case 10: dit_pass<10, -1>(sm, N, 1, nullptr); break;
-    case 16: dit_pass<16, -1>(sm, N, 1, nullptr); break;
+    case 2: dit_pass<2, -1>(sm, N, 1, tws, tws); break;
+    case 3: dit_pass<3, -1>(sm, N, 1, tws, tws); break;
+    case 4: dit_pass<4, -1>(sm, N, 1, tws, tws); break;
+    case 5: dit_pass<5, -1>(sm, N, 1, tws, tws); break;
+    case 6: dit_pass<6, -1>(sm, N, 1, tws, tws); break;
+    case 8: dit_pass<8, -1>(sm, N, 1, tws, tws); break;
+    case 10: dit_pass<10, -1>(sm, N, 1, tws, tws); break;
+    case 16: dit_pass<16, -1>(sm, N, 1, tws, tws); break;
   }
   __syncthreads();
   for (int p = 1; p < pa.P; ++p) {
-    dit_pass_rt<-1>(sm, pa, p);
+    dit_pass_rt<-1>(sm, tws, pa, p);
     __syncthreads();
   }
   const double hm = h / pa.m;
@@ -665,22 +756,29 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     pair_kernel(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
                 const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
   extern __shared__ double2 sm[];
+  const double2* tws = load_tables(sm, pa);
   const int N = pa.N;
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
     const PairEntry e = work[w];
     const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
     const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
                           : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
-    stage_product<BREAL>(sm, N, a, b);
+    if (!(pa.dbg & 2)) stage_product<BREAL>(sm, N, a, b);
     __syncthreads();
-    first_pass_inv<R0>(sm, pa);
-    __syncthreads();
-    for (int p = 1; p + 1 < pa.P; ++p) {
-      dit_pass_rt<1>(sm, pa, p);
+    if (!(pa.dbg & 4)) {
+      first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
       __syncthreads();
+      for (int p = 1; p + 1 < pa.P; ++p) {
+        dit_pass_rt<1>(sm, tws, pa, p);
+        __syncthreads();
+      }
     }
     double* o0 = out + e.out0;
     double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    if (pa.dbg & 1) {
+      o0 = nullptr;
+      o1 = nullptr;
+    }
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
     if (pa.P == 1) {
       // single pass: outputs are already natural-order in shared memory
@@ -696,16 +794,91 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
       }
     } else {
       switch (pa.r[pa.P - 1]) {
-        case 2: last_pass_store<2>(sm, pa, o0, o1, aligned); break;
-        case 3: last_pass_store<3>(sm, pa, o0, o1, aligned); break;
-        case 4: last_pass_store<4>(sm, pa, o0, o1, aligned); break;
-        case 5: last_pass_store<5>(sm, pa, o0, o1, aligned); break;
-        case 6: last_pass_store<6>(sm, pa, o0, o1, aligned); break;
-        case 8: last_pass_store<8>(sm, pa, o0, o1, aligned); break;
-        case 10: last_pass_store<10>(sm, pa, o0, o1, aligned); break;
-        case 16: last_pass_store<16>(sm, pa, o0, o1, aligned); break;
+        case 2: last_pass_store<2>(sm, tws, pa, o0, o1, aligned); break;
+        case 3: last_pass_store<3>(sm, tws, pa, o0, o1, aligned); break;
+        case 4: last_pass_store<4>(sm, tws, pa, o0, o1, aligned); break;
+        case 5: last_pass_store<5>(sm, tws, pa, o0, o1, aligned); break;
+        case 6: last_pass_store<6>(sm, tws, pa, o0, o1, aligned); break;
+        case 8: last_pass_store<8>(sm, tws, pa, o0, o1, aligned); break;
+        case 10: last_pass_store<10>(sm, tws, pa, o0, o1, aligned); break;
+        case 16: last_pass_store<16>(sm, tws, pa, o0, o1, aligned); break;
       }
     }
+    __syncthreads();
+  }
+}
+
+// ---- compile-time plans: every span L and stride is a constant, so the
+// padded shared-memory offsets of a butterfly fold into immediates.
+template <int R, int L, int N, int S>
+__device__ __forceinline__ void static_pass(double2* sm, const double2* lo, const double2* hi) {
+  constexpr int NBF = N / R;
+  for (int bf = threadIdx.x; bf < NBF; bf += blockDim.x) {
+    const int j = bf % L, G = bf / L;
+    const int base = G * (L * R) + j;
+    double2 v[R];
+    if constexpr (L % 16 == 0) {
+      double2* p = sm + pidx(base);
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[s] = p[s * (L + L / 16)];
+      apply_twiddles<R, S>(v, cmul(lo[j & 63], hi[j >> 6]));
+      dft<R, S>(v);
+#pragma unroll
+      for (int t = 0; t < R; ++t) p[t * (L + L / 16)] = v[t];
+    } else {
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[s] = sm[pidx(base + s * L)];
+      if (L > 1) apply_twiddles<R, S>(v, cmul(lo[j & 63], hi[j >> 6]));
+      dft<R, S>(v);
+#pragma unroll
+      for (int t = 0; t < R; ++t) sm[pidx(base + t * L)] = v[t];
+    }
+  }
+}
+
+template <int R, int L, int N>
+__device__ __forceinline__ void static_last(const double2* sm, const double2* lo, const double2* hi, int nz,
+                                            bool odd_n, double* o0, double* o1, bool aligned) {
+  constexpr int NBF = N / R;
+  static_assert(L % 16 == 0 && NBF == L, "last pass spans the whole transform");
+  for (int j = threadIdx.x; j < NBF; j += blockDim.x) {
+    const double2* p = sm + pidx(j);
+    double2 v[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) v[s] = p[s * (L + L / 16)];
+    apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
+    dft<R, 1>(v);
+    store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
+  }
+}
+
+template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    pair_kernel_static(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
+                       const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
+  constexpr int N = R0 * R1 * R2 * R3;
+  constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
+  extern __shared__ double2 sm[];
+  const double2* tws = load_tables(sm, pa);
+  const int nz = (pa.n + 1) >> 1;
+  const bool odd_n = pa.n & 1;
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const PairEntry e = work[w];
+    const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
+    stage_product<BREAL>(sm, N, a, b);
+    __syncthreads();
+    first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
+    __syncthreads();
+    static_pass<R1, L1, N, 1>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
+    __syncthreads();
+    static_pass<R2, L2, N, 1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+    __syncthreads();
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+    static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
     __syncthreads();
   }
 }
@@ -799,9 +972,33 @@ static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, 
   prof_end(ctx);
 }
 
+template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
+static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
+                       const PairEntry* dwork, int nwork, double* out) {
+  const PlanArgs& a = pl.a;
+  if (!(a.P == 4 && a.r[0] == R0 && a.r[1] == R1 && a.r[2] == R2 && a.r[3] == R3) || a.dbg || getenv("TGB_NO_STATIC"))
+    return false;
+  auto kern = pair_kernel_static<R0, R1, R2, R3, TT, BREAL>;
+  static bool attr = false;
+  if (!attr) {
+    TGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+    attr = true;
+  }
+  int per_sm = 1;
+  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, pl.smem));
+  const int grid = std::max(1, std::min(nwork, std::max(1, per_sm) * ctx->num_sms));
+  prof_begin(ctx);
+  kern<<<grid, TT, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, nwork, out);
+  TGB_LAUNCHED(ctx);
+  prof_end(ctx);
+  return true;
+}
+
 template <bool BREAL>
 static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                           const PairEntry* dwork, int nwork, double* out) {
+  // compile-time plans (config 2: n = 16385 -> N = 12800)
+  if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, nwork, out)) return;
   switch (pl.a.r[0]) {
     case 2: launch_pair<2, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
     case 3: launch_pair<3, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
@@ -810,6 +1007,7 @@ static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA
     case 6: launch_pair<6, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
     case 8: launch_pair<8, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
     case 10: launch_pair<10, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 16: launch_pair<16, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
     default: throw Error(TGB_CUDA_ERROR, "fftconv: unsupported first radix");
   }
 }

@@ -1,0 +1,167 @@
+// FP64 GEMM on the sm_100a tensor cores (DMMA, mma.sync m16n8k4 f64) for the
+// dense products of the rank-reduction and TEI rows:
+//   Gram matrices W W^T (reduction.cpp:94, tei.cpp:124), projections Z^T F
+//   (reduction.cpp:64,209-217, tei.cpp:139), ALS unfoldings F C
+//   (reduction.cpp:217), the convolution-matrix products U^T (conv) (tei.cpp:155).
+// tcgen05 has no f64 kind, so DMMA is the FP64 tensor path on B200; measured
+// 37.1 TFLOP/s vs 36.6 for DFMA (profiles/r01_box_probe.txt).
+//
+// C (M x N) = alpha * op(A) * op(B) + beta * C, all column-major.
+// CTA tile 64 x 64, K-step 16, 4 warps (2 x 2) of 32 x 32, register-staged
+// double buffering of the global loads.
+#include <cuda_runtime.h>
+
+#include "tgb_internal.hpp"
+
+namespace tgb {
+
+namespace {
+
+constexpr int BM = 64, BN = 64, BK = 16, LDS_ = 68;  // LDS_ = 64 + 4: conflict-free fragment loads
+constexpr int GEMM_THREADS = 128;
+
+__device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K, double alpha,
+                                                             const double* __restrict__ A, int64_t lda,
+                                                             const double* __restrict__ B, int64_t ldb, double beta,
+                                                             double* __restrict__ C, int64_t ldc) {
+  __shared__ double As[2][BK][LDS_];
+  __shared__ double Bs[2][BK][LDS_];
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+
+  // each thread stages 8 A and 8 B elements per K-step
+  double ra[8], rb[8];
+  auto load_tile = [&](int k0) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int idx = tid + e * GEMM_THREADS;  // 0..1023
+      int mm, kk;
+      if (!TA) {  // A (m, k) at A[m + lda k]: m fastest
+        mm = idx % BM;
+        kk = idx / BM;
+      } else {  // A^T: (m, k) at A[k + lda m]: k fastest
+        kk = idx % BK;
+        mm = idx / BK;
+      }
+      const int gm = m0 + mm, gk = k0 + kk;
+      ra[e] = (gm < M && gk < K) ? (TA ? __ldg(A + gk + lda * gm) : __ldg(A + gm + lda * gk)) : 0.0;
+      int nn, kb;
+      if (!TB) {  // B (k, n) at B[k + ldb n]: k fastest
+        kb = idx % BK;
+        nn = idx / BK;
+      } else {  // B^T: (k, n) at B[n + ldb k]: n fastest
+        nn = idx % BN;
+        kb = idx / BN;
+      }
+      const int gn = n0 + nn, gk2 = k0 + kb;
+      rb[e] = (gn < N && gk2 < K) ? (TB ? __ldg(B + gn + ldb * gk2) : __ldg(B + gk2 + ldb * gn)) : 0.0;
+    }
+  };
+  auto store_tile = [&](int buf) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int idx = tid + e * GEMM_THREADS;
+      int mm, kk;
+      if (!TA) {
+        mm = idx % BM;
+        kk = idx / BM;
+      } else {
+        kk = idx % BK;
+        mm = idx / BK;
+      }
+      As[buf][kk][mm] = ra[e];
+      int nn, kb;
+      if (!TB) {
+        kb = idx % BK;
+        nn = idx / BK;
+      } else {
+        nn = idx % BN;
+        kb = idx / BN;
+      }
+      Bs[buf][kb][nn] = rb[e];
+    }
+  };
+
+  double acc[2][4][4];
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+
+  const int nk = (K + BK - 1) / BK;
+  load_tile(0);
+  store_tile(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) load_tile((kt + 1) * BK);
+#pragma unroll
+    for (int k4 = 0; k4 < BK; k4 += 4) {
+      double a[2][2], b[4];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        a[i][0] = As[buf][k4 + t][wm + 16 * i + g];
+        a[i][1] = As[buf][k4 + t][wm + 16 * i + g + 8];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][k4 + t][wn + 8 * j + g];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma16x8x4(acc[i][j], a[i][0], a[i][1], b[j]);
+    }
+    if (kt + 1 < nk) store_tile(buf ^ 1);
+    __syncthreads();
+  }
+  // epilogue: c0,c1 at (g, 2t..2t+1), c2,c3 at (g+8, 2t..2t+1)
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int row = m0 + wm + 16 * i + g + (r >= 2 ? 8 : 0);
+        const int col = n0 + wn + 8 * j + 2 * t + (r & 1);
+        if (row < M && col < N) {
+          double* cp = C + row + ldc * col;
+          *cp = beta == 0.0 ? alpha * acc[i][j][r] : alpha * acc[i][j][r] + beta * *cp;
+        }
+      }
+}
+
+}  // namespace
+
+void dgemm(tgb_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+           int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
+  if (M <= 0 || N <= 0) return;
+  dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
+  const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
+  if (!ta && !tb) dgemm_kernel<false, false><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (!ta && tb) dgemm_kernel<false, true><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (ta && !tb) dgemm_kernel<true, false><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (ta && tb) dgemm_kernel<true, true><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  TGB_LAUNCHED(ctx);
+}
+
+}  // namespace tgb
+
+extern "C" int tgb_dgemm(tgb_ctx* ctx, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, double alpha,
+                         const double* A, int64_t lda, const double* B, int64_t ldb, double beta, double* C,
+                         int64_t ldc) {
+  return tgb::guarded_call([&] {
+    tgb::require(M >= 0 && N >= 0 && K >= 0, "dgemm: negative size");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::dgemm(ctx, trans_a != 0, trans_b != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
+  });
+}

@@ -63,6 +63,23 @@ struct DevBuf {
 
 struct ConvPlan;  // fftconv.cu
 
+void set_last_error(const std::string& msg);  // capi.cpp
+
+// Run f, mapping exceptions to the C-ABI return codes (tgb.h).
+template <class F>
+int guarded_call(F&& f) {
+  try {
+    f();
+    return TGB_OK;
+  } catch (const Error& e) {
+    set_last_error(e.what());
+    return e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    return TGB_CUDA_ERROR;
+  }
+}
+
 }  // namespace tgb
 
 struct tgb_ctx {
@@ -107,6 +124,8 @@ void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const
 double scalar_product_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b);
 void coulomb_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const tgb_cp& vh,
                         double vol, double* J);
+void dgemm(tgb_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
+           int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ijk, double* out);
 void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
                           double* out);
