@@ -136,12 +136,28 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
   a.ofs = static_cast<int>(even ? n / 2 - 1 : (n - 1) / 2);
   // alias-free circular length for the window [ofs, ofs + n - 1 (+1 even)]
   const int64_t m0 = std::max<int64_t>(2 * n - 2 - a.ofs, a.ofs + n - 1 + (even ? 1 : 0)) + 1;
-  int64_t N = std::max<int64_t>(2, (m0 + 1) / 2);
-  while (!five_smooth(N)) ++N;
+  // cheapest 5-smooth length >= the alias-free minimum: each pass is one
+  // shared-memory round trip, so cost ~ N * (passes + 1.5) (staging + split)
+  const int64_t Nmin = std::max<int64_t>(2, (m0 + 1) / 2);
+  int64_t N = Nmin;
+  std::vector<int> rad;
+  {
+    double best_cost = 1e300;
+    for (int64_t c = Nmin; c <= Nmin + Nmin / 4 + 8; ++c) {
+      if (!five_smooth(c) || c >= (1 << 24) || plan_smem(static_cast<int>(c)) + 8192 > ctx->smem_optin) continue;
+      std::vector<int> rc;
+      if (!factor_radices(static_cast<int>(c), rc)) continue;
+      const double cost = static_cast<double>(c) * (rc.size() + 1.5) * (rc.front() == 16 ? 0.97 : 1.0);
+      if (cost < best_cost) {
+        best_cost = cost;
+        N = c;
+        rad = rc;
+      }
+    }
+  }
   a.N = static_cast<int>(N);
   a.m = static_cast<int>(2 * N);
-  std::vector<int> rad;
-  const bool fits = N < (1 << 24) && plan_smem(a.N) + 8192 <= ctx->smem_optin && factor_radices(a.N, rad);
+  const bool fits = !rad.empty();
   pl->direct = n <= ctx->direct_max || !fits;
   a.dbg = getenv("TGB_PAIR_DBG") ? atoi(getenv("TGB_PAIR_DBG")) : 0;
   if (!pl->direct) {

@@ -1,0 +1,805 @@
+// Factorised two-electron integrals on sm_100a (reference proj/src/tei.cpp):
+//   1D density fitting per axis (tei.cpp:92-143): product side matrix G,
+//     Gram G G^T on the DMMA tensor cores, pivoted Cholesky with trace stop
+//     (single-CTA device loop, first-maximal-index pivots as Eigen's
+//     maxCoeff(&p)), Householder QR with Eigen's reflector convention,
+//     V = G^T U;
+//   convolution matrices M_k = U^T (h conv(U, p_k)) (tei.cpp:145-158) through
+//     the FFT mode-convolution path + one GEMM per axis;
+//   the TEI diagonal from the bilinear forms V[j2,:] M_k V[j,:]^T
+//      instead of whole columns (tei.cpp:182-196);
+//   TEI columns (tei.cpp:33-44,160-174) as three GEMMs + a fused
+//     product-over-axes / sum-over-terms kernel;
+//   the TEI pivoted Cholesky (tei.cpp:48-90,198-204) as a host-driven loop of
+//     device steps (argmax, column, downdate).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "tgb_internal.hpp"
+
+namespace tgb {
+
+namespace {
+
+constexpr int kRedThreads = 1024;
+
+// ---------------------------------------------------------------- helpers
+
+// block-wide argmax with the FIRST maximal index (ties -> lowest index)
+__device__ __forceinline__ void argmax_combine(double& v, int& i, double v2, int i2) {
+  if (v2 > v || (v2 == v && i2 < i)) {
+    v = v2;
+    i = i2;
+  }
+}
+
+__device__ void block_argmax(double& v, int& i, double* sv, int* si) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) {
+    const double v2 = __shfl_down_sync(0xffffffffu, v, o);
+    const int i2 = __shfl_down_sync(0xffffffffu, i, o);
+    argmax_combine(v, i, v2, i2);
+  }
+  if (lane == 0) {
+    sv[warp] = v;
+    si[warp] = i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    v = lane < nw ? sv[lane] : -INFINITY;
+    i = lane < nw ? si[lane] : 0x7fffffff;
+    for (int o = 16; o; o >>= 1) {
+      const double v2 = __shfl_down_sync(0xffffffffu, v, o);
+      const int i2 = __shfl_down_sync(0xffffffffu, i, o);
+      argmax_combine(v, i, v2, i2);
+    }
+    if (lane == 0) {
+      sv[0] = v;
+      si[0] = i;
+    }
+  }
+  __syncthreads();
+  v = sv[0];
+  i = si[0];
+  __syncthreads();
+}
+
+__device__ double block_sum(double v, double* sv) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) sv[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    v = lane < nw ? sv[lane] : 0.0;
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sv[0] = v;
+  }
+  __syncthreads();
+  v = sv[0];
+  __syncthreads();
+  return v;
+}
+
+// ---------------------------------------------------------------- density fitting
+
+// G[i + n (p + np q)] = prim[i, p] * prim[i, q]            (tei.cpp:118-121)
+__global__ void gprod_kernel(int64_t n, int np, const double* __restrict__ prim, double* __restrict__ G) {
+  const int64_t col = blockIdx.y;  // p + np q
+  const int p = static_cast<int>(col % np), q = static_cast<int>(col / np);
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    G[i + n * col] = prim[i + n * p] * prim[i + n * q];
+}
+
+// Pivoted Cholesky of an explicit SPD n x n matrix A (tei.cpp:48-90), single
+// CTA.  info[0] = rank, info[1] = clamped_negative, info[2] = error (1 = not
+// PSD beyond tolerance); pivots[rank]; residual[0] = stop measure ratio.
+__global__ void __launch_bounds__(kRedThreads) pivchol_explicit_kernel(int n, const double* __restrict__ A,
+                                                                       double tol, int trace_stop, int cap,
+                                                                       double neg_tol, double* __restrict__ diag,
+                                                                       double* __restrict__ L, int* pivots, int* info,
+                                                                       double* residual) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  __shared__ double s_dmax;
+  __shared__ int s_p;
+  // diagonal and its max / sum
+  double lmax = -INFINITY, lsum = 0.0;
+  int imax = 0x7fffffff;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double d = A[i + static_cast<int64_t>(n) * i];
+    diag[i] = d;
+    argmax_combine(lmax, imax, d, i);
+    lsum += d;
+  }
+  block_argmax(lmax, imax, sv, si);
+  const double max0 = lmax;
+  const double trace0 = block_sum(lsum, sv);
+  int rank = 0, clamped = 0, err = 0;
+  if (max0 > 0.0) {
+    const double target = tol * (trace_stop ? trace0 : max0);
+    while (rank < cap) {
+      double dm = -INFINITY, ds = 0.0;
+      int p = 0x7fffffff;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        argmax_combine(dm, p, diag[i], i);
+        ds += diag[i];
+      }
+      block_argmax(dm, p, sv, si);
+      const double meas = trace_stop ? block_sum(ds, sv) : dm;
+      if (meas <= target || dm <= 0.0) break;
+      if (threadIdx.x == 0) {
+        s_dmax = dm;
+        s_p = p;
+        pivots[rank] = p;
+      }
+      __syncthreads();
+      const double piv = sqrt(s_dmax);
+      const int pp = s_p;
+      int bad = 0, cl = 0;
+      for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double c = A[i + static_cast<int64_t>(n) * pp];
+        for (int r = 0; r < rank; ++r) c -= L[i + static_cast<int64_t>(n) * r] * L[pp + static_cast<int64_t>(n) * r];
+        double l = c / piv;
+        if (i == pp) l = piv;
+        L[i + static_cast<int64_t>(n) * rank] = l;
+        double d = diag[i] - l * l;
+        if (i == pp) d = 0.0;
+        if (d < 0.0) {
+          if (d < -neg_tol * max0) bad = 1;
+          d = 0.0;
+          cl = 1;
+        }
+        diag[i] = d;
+      }
+      bad = __syncthreads_or(bad);
+      cl = __syncthreads_or(cl);
+      clamped |= cl;
+      ++rank;
+      if (bad) {
+        err = 1;
+        break;
+      }
+    }
+  }
+  // final stop measure
+  double dm = -INFINITY, ds = 0.0;
+  int p = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    argmax_combine(dm, p, diag[i], i);
+    ds += diag[i];
+  }
+  block_argmax(dm, p, sv, si);
+  const double fs = block_sum(ds, sv);
+  if (threadIdx.x == 0) {
+    info[0] = rank;
+    info[1] = clamped;
+    info[2] = err;
+    residual[0] = max0 > 0.0 ? (trace_stop ? fs : dm) / (trace_stop ? trace0 : max0) : 0.0;
+  }
+}
+
+// Thin Householder QR of a tall n x r matrix (in place), Eigen's convention
+// (beta = -sign(c0) * norm, tau = (beta - c0) / beta), then Q (n x r)
+// explicitly.  Single CTA.
+__global__ void __launch_bounds__(kRedThreads) householder_qr_kernel(int n, int r, double* __restrict__ W,
+                                                                     double* __restrict__ tau,
+                                                                     double* __restrict__ Q) {
+  __shared__ double sv[32];
+  __shared__ double s_beta, s_tau, s_c0;
+  for (int j = 0; j < r; ++j) {
+    double* wj = W + static_cast<int64_t>(n) * j;
+    double part = 0.0;
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) part += wj[i] * wj[i];
+    const double tail = block_sum(part, sv);
+    if (threadIdx.x == 0) {
+      const double c0 = wj[j];
+      s_c0 = c0;
+      if (tail <= 2.2250738585072014e-308) {
+        s_tau = 0.0;
+        s_beta = c0;
+      } else {
+        double beta = sqrt(c0 * c0 + tail);
+        if (c0 >= 0.0) beta = -beta;
+        s_beta = beta;
+        s_tau = (beta - c0) / beta;
+      }
+      tau[j] = s_tau;
+    }
+    __syncthreads();
+    const double tj = s_tau, beta = s_beta, c0 = s_c0;
+    if (tj == 0.0) {
+      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) wj[i] = 0.0;
+      __syncthreads();
+      continue;
+    }
+    const double scale = 1.0 / (c0 - beta);
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) wj[i] *= scale;
+    __syncthreads();
+    if (threadIdx.x == 0) wj[j] = beta;
+    // apply H = I - tau v v^T (v = [1; essential]) to columns c > j
+    for (int c = j + 1; c < r; ++c) {
+      double* wc = W + static_cast<int64_t>(n) * c;
+      const double wcj = wc[j];
+      double part2 = 0.0;
+      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) part2 += wj[i] * wc[i];
+      const double s = (block_sum(part2, sv) + wcj) * tj;
+      if (threadIdx.x == 0) wc[j] -= s;
+      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) wc[i] -= s * wj[i];
+      __syncthreads();
+    }
+  }
+  // Q = H_0 ... H_{r-1} [I; 0]
+  for (int c = 0; c < r; ++c)
+    for (int i = threadIdx.x; i < n; i += blockDim.x) Q[i + static_cast<int64_t>(n) * c] = (i == c) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int j = r - 1; j >= 0; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    const double* wj = W + static_cast<int64_t>(n) * j;
+    for (int c = 0; c < r; ++c) {
+      double* qc = Q + static_cast<int64_t>(n) * c;
+      const double qcj = qc[j];
+      double part = 0.0;
+      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) part += wj[i] * qc[i];
+      const double s = (block_sum(part, sv) + qcj) * tj;
+      if (threadIdx.x == 0) qc[j] -= s;
+      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) qc[i] -= s * wj[i];
+      __syncthreads();
+    }
+  }
+}
+
+// partial sums of (G - T)^2 and G^2 (fit residual, tei.cpp:140-141)
+__global__ void resid_kernel(int64_t total, const double* __restrict__ G, const double* __restrict__ T,
+                             double* __restrict__ out) {
+  __shared__ double sv[32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double d = G[i] - T[i];
+    a += d * d;
+    b += G[i] * G[i];
+  }
+  a = block_sum(a, sv);
+  b = block_sum(b, sv);
+  if (threadIdx.x == 0) {
+    out[2 * blockIdx.x] = a;
+    out[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// ---------------------------------------------------------------- TEI diagonal / columns
+
+// acc[c] (+)= sum over the primitive pairs (j, j2) of contracted pair c of
+//   w_j w_j2 prod_ax <V_ax[j2, :], Y_ax[j, :]>,  Y_ax = V_ax M_k^T
+// (tei.cpp:182-196 with b_prim_column expanded; one kernel term k per call).
+__global__ void tei_diag_term_kernel(int nc, const int* __restrict__ cstart, const int* __restrict__ cpairs,
+                                     const double* __restrict__ cw, int64_t np2, const double* __restrict__ V0,
+                                     const double* __restrict__ V1, const double* __restrict__ V2, int r0, int r1,
+                                     int r2, const double* __restrict__ Y0, const double* __restrict__ Y1,
+                                     const double* __restrict__ Y2, double* __restrict__ acc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double s = 0.0;
+  for (int a = cstart[c]; a < cstart[c + 1]; ++a)
+    for (int b = cstart[c]; b < cstart[c + 1]; ++b) {
+      const int j = cpairs[a], j2 = cpairs[b];
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+      for (int q = 0; q < r0; ++q) d0 += V0[j2 + np2 * q] * Y0[j + np2 * q];
+      for (int q = 0; q < r1; ++q) d1 += V1[j2 + np2 * q] * Y1[j + np2 * q];
+      for (int q = 0; q < r2; ++q) d2 += V2[j2 + np2 * q] * Y2[j + np2 * q];
+      s += cw[a] * cw[b] * (d0 * d1 * d2);
+    }
+  acc[c] += s;
+}
+
+// col[i] = sum_k prod_ax W_ax[i, k]   (b_prim_column, tei.cpp:33-44)
+__global__ void tei_col_combine_kernel(int64_t np2, int K, const double* __restrict__ W0,
+                                       const double* __restrict__ W1, const double* __restrict__ W2,
+                                       double* __restrict__ col) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= np2) return;
+  double s = 0.0;
+  for (int k = 0; k < K; ++k) s += W0[i + np2 * k] * W1[i + np2 * k] * W2[i + np2 * k];
+  col[i] = s;
+}
+
+// gather rows V_ax[j, :] (j = primitive pair) into Vj (r x 1) for each axis
+__global__ void gather_row_kernel(const double* __restrict__ V, int64_t np2, int r, int j, double* __restrict__ out) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < r) out[q] = V[j + np2 * q];
+}
+
+// contraction: out[owner[p] + nb owner[q]] += pw[p] pw[q] z[p + np q]  (tei.cpp:166-172),
+// as a gather over contracted pairs (deterministic order p-major within q as the reference loop)
+__global__ void contract_kernel(int nb, int np, const int* __restrict__ fstart, const double* __restrict__ pw,
+                                const double* __restrict__ z, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nb * nb) return;
+  const int mu = c % nb, nu = c / nb;
+  double s = 0.0;
+  for (int q = fstart[nu]; q < fstart[nu + 1]; ++q)
+    for (int p = fstart[mu]; p < fstart[mu + 1]; ++p) s += pw[p] * pw[q] * z[p + static_cast<int64_t>(np) * q];
+  out[c] = s;
+}
+
+__global__ void axpy_kernel(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y, int init) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) y[i] = init ? a * x[i] : y[i] + a * x[i];
+}
+
+// side-by-side [M_0 | M_1 | ...] (r x rK) -> stacked [M_0; M_1; ...] (rK x r)
+__global__ void stack_kernel(int r, int K, const double* __restrict__ Mcat, double* __restrict__ Mst) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t tot = static_cast<int64_t>(r) * r * K;
+  if (idx >= tot) return;
+  const int a = static_cast<int>(idx % r);
+  const int64_t rest = idx / r;  // b + r k
+  const int b = static_cast<int>(rest % r), k = static_cast<int>(rest / r);
+  Mst[(a + static_cast<int64_t>(r) * k) + static_cast<int64_t>(r) * K * b] = Mcat[idx];
+}
+
+__global__ void argmax_kernel(int n, const double* __restrict__ d, double* out_v, int* out_i) {
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  double v = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) argmax_combine(v, idx, d[i], i);
+  block_argmax(v, idx, sv, si);
+  if (threadIdx.x == 0) {
+    *out_v = v;
+    *out_i = idx;
+  }
+}
+
+// Cholesky step (tei.cpp:70-83): col -= L[:, :rank] L[p, :rank]^T; L[:, rank] = col / piv,
+// L[p, rank] = piv; diag -= L^2, diag[p] = 0; clamp negatives.  flags[0] |= clamped, flags[1] |= bad
+__global__ void chol_step_kernel(int64_t n, int rank, int p, double dmax, double max0, double neg_tol,
+                                 const double* __restrict__ col, double* __restrict__ L, double* __restrict__ diag,
+                                 int* flags) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double piv = sqrt(dmax);
+  double c = col[i];
+  for (int r = 0; r < rank; ++r) c -= L[i + n * r] * L[p + n * r];
+  double l = c / piv;
+  if (i == p) l = piv;
+  L[i + n * rank] = l;
+  double d = diag[i] - l * l;
+  if (i == p) d = 0.0;
+  if (d < 0.0) {
+    if (d < -neg_tol * max0) atomicOr(flags + 1, 1);
+    d = 0.0;
+    atomicOr(flags, 1);
+  }
+  diag[i] = d;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- host orchestration
+
+struct TEI {
+  int64_t nb = 0, np = 0;
+  std::vector<int> fstart;  // primitives of function f: fstart[f] .. fstart[f+1]-1
+  std::vector<double> pw;   // primitive weights
+  std::array<int64_t, 3> n{};
+  std::array<double, 3> h{};
+  std::array<int64_t, 3> R{};
+  std::array<DevBuf, 3> U, V, M, Mst;  // M: R x (R K) = [M_0 | M_1 | ...]; Mst: (R K) x R stacked
+  int64_t K = 0;
+  std::array<double, 3> fit_res{};
+  bool fit_clamped = false;
+  DevBuf L, diag;
+  int64_t RB = 0;
+  std::vector<int64_t> chol_piv;
+  DevBuf d_fstart, d_pw, d_cstart, d_cpairs, d_cw;
+};
+
+}  // namespace tgb
+
+struct tgb_tei {
+  tgb::TEI t;
+};
+
+namespace tgb {
+
+static double* dptr(DevBuf& b) { return static_cast<double*>(b.p); }
+
+void tei_fit(tgb_ctx* ctx, TEI& f, const tgb_cp& basis_dev, const int64_t* fn_offset, int64_t nb, const double h[3],
+             double eps_fit) {
+  f.nb = nb;
+  f.np = basis_dev.rank;
+  f.fstart.assign(fn_offset, fn_offset + nb + 1);
+  f.pw.resize(f.np);
+  if (f.np) TGB_CUDA(cudaMemcpy(f.pw.data(), basis_dev.weight, f.np * sizeof(double), cudaMemcpyDeviceToHost));
+  const int64_t np = f.np, np2 = np * np;
+  for (int ax = 0; ax < 3; ++ax) {
+    const int64_t n = basis_dev.n[ax];
+    f.n[ax] = n;
+    f.h[ax] = h[ax];
+    auto* G = static_cast<double*>(ctx->ws_in.get(static_cast<size_t>(n) * np2 * sizeof(double)));
+    dim3 g1(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), static_cast<unsigned>(np2));
+    gprod_kernel<<<g1, 256, 0, ctx->stream>>>(n, static_cast<int>(np), basis_dev.factor[ax], G);
+    TGB_LAUNCHED(ctx);
+    auto* gram = static_cast<double*>(ctx->ws_out.get(static_cast<size_t>(n) * n * sizeof(double)));
+    dgemm(ctx, false, true, n, n, np2, 1.0, G, n, G, n, 0.0, gram, n);
+    const int64_t cap = std::min(n, np2);
+    auto* Lw = static_cast<double*>(ctx->ws_misc.get(static_cast<size_t>(n) * cap * sizeof(double) + n * sizeof(double) +
+                                                     64 + cap * sizeof(int) + 64));
+    double* dg = Lw + n * cap;
+    int* piv = reinterpret_cast<int*>(dg + n + 8);
+    auto* small = static_cast<double*>(ctx->ws_misc2.get(64 * sizeof(double)));
+    int* info = reinterpret_cast<int*>(small);
+    double* resid = small + 4;
+    pivchol_explicit_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(n), gram, eps_fit * eps_fit, 1,
+                                                                static_cast<int>(cap), 1e-12, dg, Lw, piv, info,
+                                                                resid);
+    TGB_LAUNCHED(ctx);
+    int hinfo[3];
+    TGB_CUDA(cudaMemcpyAsync(hinfo, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hinfo[2]) throw Error(TGB_NUMERICAL_ERROR, "tei_density_fitting: Gram matrix indefinite beyond tolerance");
+    f.fit_clamped = f.fit_clamped || hinfo[1];
+    const int64_t r = hinfo[0];
+    f.R[ax] = r;
+    f.U[ax].get(std::max<int64_t>(1, n * r) * sizeof(double));
+    f.V[ax].get(std::max<int64_t>(1, np2 * r) * sizeof(double));
+    if (r > 0) {
+      auto* tau = static_cast<double*>(ctx->ws_misc3.get(std::max<int64_t>(r, 1) * sizeof(double)));
+      householder_qr_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(n), static_cast<int>(r), Lw, tau,
+                                                                dptr(f.U[ax]));
+      TGB_LAUNCHED(ctx);
+      dgemm(ctx, true, false, np2, r, n, 1.0, G, n, dptr(f.U[ax]), n, 0.0, dptr(f.V[ax]), np2);
+    }
+    // residual ||G - U V^T|| / ||G||  (T reuses the Gram workspace when large enough)
+    auto* T = static_cast<double*>(ctx->ws_out.get(std::max(static_cast<size_t>(n) * n, static_cast<size_t>(n) * np2) *
+                                                   sizeof(double)));
+    if (r > 0)
+      dgemm(ctx, false, true, n, np2, r, 1.0, dptr(f.U[ax]), n, dptr(f.V[ax]), np2, 0.0, T, n);
+    else
+      TGB_CUDA(cudaMemsetAsync(T, 0, static_cast<size_t>(n) * np2 * sizeof(double), ctx->stream));
+    const int nblk = 256;
+    auto* part = static_cast<double*>(ctx->ws_misc2.get(2 * nblk * sizeof(double)));
+    resid_kernel<<<nblk, 256, 0, ctx->stream>>>(n * np2, G, T, part);
+    TGB_LAUNCHED(ctx);
+    std::vector<double> hp(2 * nblk);
+    TGB_CUDA(cudaMemcpyAsync(hp.data(), part, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    double a = 0, b = 0;
+    for (int i = 0; i < nblk; ++i) {
+      a += hp[2 * i];
+      b += hp[2 * i + 1];
+    }
+    f.fit_res[ax] = std::sqrt(a) / std::max(std::sqrt(b), 1e-300);
+  }
+}
+
+void tei_conv(tgb_ctx* ctx, TEI& f, const tgb_cp& kernel_dev) {
+  f.K = kernel_dev.rank;
+  for (int ax = 0; ax < 3; ++ax) {
+    require(kernel_dev.n[ax] == f.n[ax], "tei_convolution_matrices: kernel grid mismatch");
+    const int64_t n = f.n[ax], r = f.R[ax], K = f.K;
+    f.M[ax].get(std::max<int64_t>(1, r * r * K) * sizeof(double));
+    if (r == 0 || K == 0) continue;
+    // conv columns: column i + r k = h * window(conv(U_i, p_k))   (tei.cpp:153-154)
+    auto* co = static_cast<double*>(ctx->ws_out.get(static_cast<size_t>(n) * r * K * sizeof(double)));
+    convolve_axis(ctx, n, r, dptr(f.U[ax]), K, kernel_dev.factor[ax], f.h[ax], co);
+    // [M_0 | ... | M_{K-1}] = U^T [conv_0 | ...]   (tei.cpp:155)
+    dgemm(ctx, true, false, r, r * K, n, 1.0, dptr(f.U[ax]), n, co, n, 0.0, dptr(f.M[ax]), r);
+    f.Mst[ax].get(std::max<int64_t>(1, r * r * K) * sizeof(double));
+    stack_kernel<<<static_cast<unsigned>((r * r * K + 255) / 256), 256, 0, ctx->stream>>>(
+        static_cast<int>(r), static_cast<int>(K), dptr(f.M[ax]), dptr(f.Mst[ax]));
+    TGB_LAUNCHED(ctx);
+  }
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void ensure_contraction_tables(tgb_ctx* ctx, TEI& f) {
+  // contracted pair c = mu + nb nu -> primitive pairs (p + np q) with weights pw[p] pw[q]
+  if (f.d_cstart.p) return;
+  const int64_t nb = f.nb, np = f.np;
+  std::vector<int> cstart(nb * nb + 1, 0), cpairs;
+  std::vector<double> cw;
+  for (int64_t nu = 0; nu < nb; ++nu)
+    for (int64_t mu = 0; mu < nb; ++mu) {
+      const int64_t c = mu + nb * nu;
+      for (int p = f.fstart[mu]; p < f.fstart[mu + 1]; ++p)
+        for (int q = f.fstart[nu]; q < f.fstart[nu + 1]; ++q) {
+          cpairs.push_back(static_cast<int>(p + np * q));
+          cw.push_back(f.pw[p] * f.pw[q]);
+        }
+      cstart[c + 1] = static_cast<int>(cpairs.size());
+    }
+  auto up = [&](DevBuf& b, const void* src, size_t bytes) {
+    b.get(std::max<size_t>(bytes, 16));
+    if (bytes) TGB_CUDA(cudaMemcpyAsync(b.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  };
+  up(f.d_cstart, cstart.data(), cstart.size() * sizeof(int));
+  up(f.d_cpairs, cpairs.data(), cpairs.size() * sizeof(int));
+  up(f.d_cw, cw.data(), cw.size() * sizeof(double));
+  std::vector<int> fs(f.fstart.begin(), f.fstart.end());
+  up(f.d_fstart, fs.data(), fs.size() * sizeof(int));
+  up(f.d_pw, f.pw.data(), f.pw.size() * sizeof(double));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// diag[c], c = mu + nb nu (device output, nb^2 entries)
+void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
+  ensure_contraction_tables(ctx, f);
+  const int64_t nb = f.nb, np2 = f.np * f.np;
+  const int nc = static_cast<int>(nb * nb);
+  TGB_CUDA(cudaMemsetAsync(diag, 0, nc * sizeof(double), ctx->stream));
+  std::array<double*, 3> Y{};
+  static thread_local std::array<DevBuf, 3> ybuf;
+  for (int ax = 0; ax < 3; ++ax) Y[ax] = static_cast<double*>(ybuf[ax].get(std::max<int64_t>(1, np2 * f.R[ax]) * sizeof(double)));
+  for (int64_t k = 0; k < f.K; ++k) {
+    for (int ax = 0; ax < 3; ++ax) {
+      const int64_t r = f.R[ax];
+      if (r == 0) continue;
+      // Y = V M_k^T
+      dgemm(ctx, false, true, np2, r, r, 1.0, dptr(f.V[ax]), np2, dptr(f.M[ax]) + r * r * k, r, 0.0, Y[ax], np2);
+    }
+    tei_diag_term_kernel<<<(nc + 127) / 128, 128, 0, ctx->stream>>>(
+        nc, static_cast<const int*>(f.d_cstart.p), static_cast<const int*>(f.d_cpairs.p),
+        static_cast<const double*>(f.d_cw.p), np2, dptr(f.V[0]), dptr(f.V[1]), dptr(f.V[2]),
+        static_cast<int>(f.R[0]), static_cast<int>(f.R[1]), static_cast<int>(f.R[2]), Y[0], Y[1], Y[2], diag);
+    TGB_LAUNCHED(ctx);
+  }
+}
+
+// primitive-level column b_prim_column(j) (np^2, device) via three GEMMs + combine
+static void b_prim_column_dev(tgb_ctx* ctx, TEI& f, int64_t j, double* col) {
+  const int64_t np2 = f.np * f.np, K = f.K;
+  static thread_local std::array<DevBuf, 3> wbuf, ybuf, vrow;
+  std::array<double*, 3> W{};
+  for (int ax = 0; ax < 3; ++ax) {
+    const int64_t r = f.R[ax];
+    W[ax] = static_cast<double*>(wbuf[ax].get(std::max<int64_t>(1, np2 * K) * sizeof(double)));
+    auto* y = static_cast<double*>(ybuf[ax].get(std::max<int64_t>(1, r * K) * sizeof(double)));
+    auto* vr = static_cast<double*>(vrow[ax].get(std::max<int64_t>(1, r) * sizeof(double)));
+    if (r == 0) {
+      TGB_CUDA(cudaMemsetAsync(W[ax], 0, np2 * K * sizeof(double), ctx->stream));
+      continue;
+    }
+    gather_row_kernel<<<static_cast<unsigned>((r + 127) / 128), 128, 0, ctx->stream>>>(dptr(f.V[ax]), np2,
+                                                                                      static_cast<int>(r),
+                                                                                      static_cast<int>(j), vr);
+    TGB_LAUNCHED(ctx);
+    // Y (r x K, column k = M_k V[j, :]^T) = stacked [M_0; ...; M_{K-1}] (rK x r) * vr
+    dgemm(ctx, false, false, r * K, 1, r, 1.0, dptr(f.Mst[ax]), r * K, vr, r, 0.0, y, r * K);
+    // W_ax (np2 x K) = V_ax (np2 x r) Y (r x K)
+    dgemm(ctx, false, false, np2, K, r, 1.0, dptr(f.V[ax]), np2, y, r, 0.0, W[ax], np2);
+  }
+  tei_col_combine_kernel<<<static_cast<unsigned>((np2 + 255) / 256), 256, 0, ctx->stream>>>(np2, static_cast<int>(K),
+                                                                                           W[0], W[1], W[2], col);
+  TGB_LAUNCHED(ctx);
+}
+
+// tei_column(pair) (nb^2, device)
+void tei_column_dev(tgb_ctx* ctx, TEI& f, int64_t pair, double* out) {
+  ensure_contraction_tables(ctx, f);
+  const int64_t nb = f.nb, np = f.np, np2 = np * np;
+  const int64_t kappa = pair % nb, lambda = pair / nb;
+  static thread_local DevBuf zbuf, cbuf;
+  auto* z = static_cast<double*>(zbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
+  auto* c = static_cast<double*>(cbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
+  // z = sum over primitive pairs (p, q) of (kappa, lambda) of w_p w_q b_prim_column(p + np q)
+  bool first = true;
+  for (int q = f.fstart[lambda]; q < f.fstart[lambda + 1]; ++q)
+    for (int p = f.fstart[kappa]; p < f.fstart[kappa + 1]; ++p) {
+      const double w = f.pw[p] * f.pw[q];
+      b_prim_column_dev(ctx, f, p + np * q, c);
+      axpy_kernel<<<static_cast<unsigned>((np2 + 255) / 256), 256, 0, ctx->stream>>>(np2, w, c, z, first ? 1 : 0);
+      TGB_LAUNCHED(ctx);
+      first = false;
+    }
+  // the contraction weights are applied in contract_kernel (pw[p] pw[q] on both sides)
+  contract_kernel<<<static_cast<unsigned>((nb * nb + 127) / 128), 128, 0, ctx->stream>>>(
+      static_cast<int>(nb), static_cast<int>(np), static_cast<const int*>(f.d_fstart.p),
+      static_cast<const double*>(f.d_pw.p), z, out);
+  TGB_LAUNCHED(ctx);
+}
+
+void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
+  const int64_t nb2 = f.nb * f.nb;
+  auto* dg = static_cast<double*>(f.diag.get(std::max<int64_t>(1, nb2) * sizeof(double)));
+  tei_diagonal_dev(ctx, f, dg);
+  f.L.get(std::max<int64_t>(1, nb2 * nb2) * sizeof(double));
+  auto* L = dptr(f.L);
+  static thread_local DevBuf colbuf, small;
+  auto* col = static_cast<double*>(colbuf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
+  auto* sm = static_cast<double*>(small.get(64 * sizeof(double)));
+  int* flags = reinterpret_cast<int*>(sm + 4);
+  TGB_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), ctx->stream));
+  // max0 of the initial diagonal
+  struct VI {
+    double v;
+    int i;
+  };
+  auto argmax = [&](VI& out) {
+    argmax_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(nb2), dg, sm, reinterpret_cast<int*>(sm + 1));
+    TGB_LAUNCHED(ctx);
+    double hv[2];
+    TGB_CUDA(cudaMemcpyAsync(hv, sm, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    out.v = hv[0];
+    std::memcpy(&out.i, &hv[1], sizeof(int));
+  };
+  VI m0;
+  argmax(m0);
+  const double max0 = m0.v;
+  f.chol_piv.clear();
+  int64_t rank = 0;
+  if (max0 > 0.0) {
+    const double target = eps_chol * max0;  // max-diagonal stop (tei.cpp:202)
+    const int64_t cap = nb2;
+    while (rank < cap) {
+      VI cur;
+      argmax(cur);
+      if (cur.v <= target || cur.v <= 0.0) break;
+      tei_column_dev(ctx, f, cur.i, col);
+      chol_step_kernel<<<static_cast<unsigned>((nb2 + 255) / 256), 256, 0, ctx->stream>>>(
+          nb2, static_cast<int>(rank), cur.i, cur.v, max0, 1e-10, col, L, dg, flags);
+      TGB_LAUNCHED(ctx);
+      f.chol_piv.push_back(cur.i);
+      ++rank;
+      int hf[2];
+      TGB_CUDA(cudaMemcpyAsync(hf, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (hf[1]) throw Error(TGB_NUMERICAL_ERROR, "pivoted_cholesky: negative diagonal beyond tolerance; matrix not PSD");
+    }
+  }
+  f.RB = rank;
+}
+
+}  // namespace tgb
+
+// ---------------------------------------------------------------- C-ABI
+
+namespace {
+struct DevCopy {
+  tgb_cp t{};
+  std::vector<double*> bufs;
+  DevCopy(const tgb_cp* h, bool on_device) {
+    t = *h;
+    if (on_device) return;
+    for (int ax = 0; ax < 3; ++ax) {
+      double* p = nullptr;
+      const size_t bytes = h->n[ax] * h->rank * sizeof(double);
+      if (bytes) {
+        TGB_CUDA(cudaMalloc(&p, bytes));
+        TGB_CUDA(cudaMemcpy(p, h->factor[ax], bytes, cudaMemcpyHostToDevice));
+      }
+      t.factor[ax] = p;
+      bufs.push_back(p);
+    }
+    double* w = nullptr;
+    if (h->rank) {
+      TGB_CUDA(cudaMalloc(&w, h->rank * sizeof(double)));
+      TGB_CUDA(cudaMemcpy(w, h->weight, h->rank * sizeof(double), cudaMemcpyHostToDevice));
+    }
+    t.weight = w;
+    bufs.push_back(w);
+  }
+  ~DevCopy() {
+    for (double* p : bufs)
+      if (p) cudaFree(p);
+  }
+};
+
+void copy_out(double* dst, const void* src, size_t bytes, int mem) {
+  if (!bytes) return;
+  TGB_CUDA(cudaMemcpy(dst, src, bytes, mem == TGB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost));
+}
+}  // namespace
+
+extern "C" {
+
+int tgb_tei_create(tgb_tei** out) {
+  return tgb::guarded_call([&] { *out = new tgb_tei(); });
+}
+
+int tgb_tei_destroy(tgb_tei* t) {
+  return tgb::guarded_call([&] { delete t; });
+}
+
+int tgb_tei_density_fitting(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
+                            const double h[3], double eps_fit, int mem) {
+  return tgb::guarded_call([&] {
+    tgb::require(basis && fn_offset && nb >= 1, "tei_density_fitting: empty basis");
+    tgb::require(fn_offset[0] == 0 && fn_offset[nb] == basis->rank, "tei_density_fitting: bad function offsets");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCopy d(basis, mem == TGB_MEM_DEVICE);
+    tgb::tei_fit(ctx, t->t, d.t, fn_offset, nb, h, eps_fit);
+  });
+}
+
+int tgb_tei_convolution_matrices(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* kernel, int mem) {
+  return tgb::guarded_call([&] {
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCopy d(kernel, mem == TGB_MEM_DEVICE);
+    tgb::tei_conv(ctx, t->t, d.t);
+  });
+}
+
+int tgb_tei_diagonal(tgb_ctx* ctx, tgb_tei* t, double* out, int mem) {
+  return tgb::guarded_call([&] {
+    const int64_t nb2 = t->t.nb * t->t.nb;
+    static thread_local tgb::DevBuf buf;
+    auto* d = static_cast<double*>(buf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
+    tgb::tei_diagonal_dev(ctx, t->t, d);
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    copy_out(out, d, nb2 * sizeof(double), mem);
+  });
+}
+
+int tgb_tei_column(tgb_ctx* ctx, tgb_tei* t, int64_t pair, double* out, int mem) {
+  return tgb::guarded_call([&] {
+    tgb::require(pair >= 0 && pair < t->t.nb * t->t.nb, "tei_column: index out of range");
+    const int64_t nb2 = t->t.nb * t->t.nb;
+    static thread_local tgb::DevBuf buf;
+    auto* d = static_cast<double*>(buf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
+    tgb::tei_column_dev(ctx, t->t, pair, d);
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    copy_out(out, d, nb2 * sizeof(double), mem);
+  });
+}
+
+int tgb_tei_cholesky(tgb_ctx* ctx, tgb_tei* t, double eps_chol) {
+  return tgb::guarded_call([&] {
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::tei_cholesky(ctx, t->t, eps_chol);
+  });
+}
+
+int tgb_tei_info(tgb_tei* t, int64_t* info, double* fit_residual) {
+  return tgb::guarded_call([&] {
+    const auto& f = t->t;
+    for (int ax = 0; ax < 3; ++ax) {
+      info[ax] = f.R[ax];
+      fit_residual[ax] = f.fit_res[ax];
+    }
+    info[3] = f.np;
+    info[4] = f.nb;
+    info[5] = f.RB;
+    info[6] = f.fit_clamped;
+    info[7] = f.K;
+  });
+}
+
+int tgb_tei_get_fit(tgb_tei* t, int ax, double* U, double* V, int mem) {
+  return tgb::guarded_call([&] {
+    auto& f = t->t;
+    copy_out(U, f.U[ax].p, f.n[ax] * f.R[ax] * sizeof(double), mem);
+    copy_out(V, f.V[ax].p, f.np * f.np * f.R[ax] * sizeof(double), mem);
+  });
+}
+
+int tgb_tei_get_conv(tgb_tei* t, int64_t k, int ax, double* M, int mem) {
+  return tgb::guarded_call([&] {
+    auto& f = t->t;
+    tgb::require(k >= 0 && k < f.K, "tei: kernel term out of range");
+    const int64_t r = f.R[ax];
+    copy_out(M, static_cast<double*>(f.M[ax].p) + r * r * k, r * r * sizeof(double), mem);
+  });
+}
+
+int tgb_tei_get_cholesky(tgb_tei* t, double* L, int64_t* pivots, int mem) {
+  return tgb::guarded_call([&] {
+    auto& f = t->t;
+    const int64_t nb2 = f.nb * f.nb;
+    copy_out(L, f.L.p, nb2 * f.RB * sizeof(double), mem);
+    for (size_t i = 0; i < f.chol_piv.size(); ++i) pivots[i] = f.chol_piv[i];
+  });
+}
+
+}  // extern "C"
