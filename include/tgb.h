@@ -106,6 +106,50 @@ int tgb_scalar_product(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, double* r
 int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
                        const double h[3], double* J, int mem);
 
+/* ---- factorised two-electron integrals (proj/include/tengrid/tei.hpp:38-72) ----
+ * A tgb_tei holds the device-resident factorisation (TEIFactorization,
+ * tei.hpp:38-57).  The basis is given flattened as for tgb_coulomb_matrix
+ * (all primitives of all functions as one CP tensor, weights = contraction
+ * coefficient x primitive norm; fn_offset has nb + 1 entries, host memory).
+ * Pair indices: primitive (p, q) -> p + n_prim q; contracted (mu, nu) -> mu + nb nu. */
+typedef struct tgb_tei tgb_tei;
+int tgb_tei_create(tgb_tei** out);
+int tgb_tei_destroy(tgb_tei* t);
+/* replaces tg::tei_density_fitting (tei.hpp:60-61, tei.cpp:92-143) */
+int tgb_tei_density_fitting(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
+                            const double h[3], double eps_fit, int mem);
+/* replaces tg::tei_convolution_matrices (tei.hpp:62, tei.cpp:145-158); primary-grid kernel */
+int tgb_tei_convolution_matrices(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* kernel, int mem);
+/* replaces tg::tei_diagonal (tei.hpp:66, tei.cpp:182-196): nb^2 entries */
+int tgb_tei_diagonal(tgb_ctx* ctx, tgb_tei* t, double* out, int mem);
+/* replaces tg::tei_column (tei.hpp:65, tei.cpp:160-174): nb^2 entries */
+int tgb_tei_column(tgb_ctx* ctx, tgb_tei* t, int64_t pair_index, double* out, int mem);
+/* replaces tg::tei_cholesky (tei.hpp:67, tei.cpp:198-204): max-diagonal stop at eps_chol */
+int tgb_tei_cholesky(tgb_ctx* ctx, tgb_tei* t, double eps_chol);
+/* info[0..2] fit ranks R_l, [3] n_prim, [4] nb, [5] R_B, [6] fit_clamped_negative, [7] kernel terms */
+int tgb_tei_info(tgb_tei* t, int64_t* info, double* fit_residual);
+int tgb_tei_get_fit(tgb_tei* t, int axis, double* U, double* V, int mem);  /* U n x R_l, V n_prim^2 x R_l */
+int tgb_tei_get_conv(tgb_tei* t, int64_t k, int axis, double* M, int mem); /* R_l x R_l */
+int tgb_tei_get_cholesky(tgb_tei* t, double* L, int64_t* pivots, int mem); /* nb^2 x R_B; pivots host */
+
+/* ---- rank reduction (proj/include/tengrid/reduction.hpp:12-67) --------------
+ * tgb_reduce_tucker runs rhosvd (mode 0) or canonical_to_tucker = RHOSVD + ALS
+ * (mode 1) on the device; ReductionConfig is (use_eps, eps) or ranks[3], plus
+ * max_sweeps.  The result (TuckerResult) stays on the device; read it with
+ * tgb_tucker_info / _get / _sigma, or convert it with tgb_tucker_to_canonical
+ * (tucker_to_canonical, reduction.cpp:238-269; reduce_rank = mode 1 + T2C).
+ * Singular values are the leading ones the rank rule needed (Gram spectrum). */
+typedef struct tgb_tucker tgb_tucker;
+int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, const int64_t* ranks, int max_sweeps,
+                      int mode, int mem, tgb_tucker** out);
+int tgb_tucker_destroy(tgb_tucker* t);
+/* info[0..2] Tucker ranks, [3] rank_clamped, [4] rhosvd_fallback, [5] ALS sweeps run, [6] T2C canonical rank */
+int tgb_tucker_info(tgb_tucker* t, int64_t* info);
+int tgb_tucker_get(tgb_tucker* t, double* core, double* side0, double* side1, double* side2, double* sweep_fits,
+                   int mem);
+int tgb_tucker_sigma(tgb_tucker* t, int axis, int64_t* count, double* sigma);
+int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem);
+
 /* ---- dense FP64 building block -------------------------------------------
  * C = alpha op(A) op(B) + beta C on the FP64 tensor cores (DMMA), column-major
  * DEVICE pointers, stream-ordered on the context stream.  The dense products

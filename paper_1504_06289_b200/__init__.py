@@ -10,4 +10,9 @@ from .tengrid import (AssembledPotential, BasisSet, CanonicalTensor3, Context, D
                       lattice_offsets, lattice_sum_canonical, make_expsum, make_grid, primitive_norm, scalar_product,
                       scale, snap_to_node, value_at_points, window_offset)
 
+from .tei import (TEIFactorization, build_tei, tei_cholesky, tei_column, tei_convolution_matrices,
+                  tei_density_fitting, tei_diagonal, tei_matrix_entry)
+
+from .reduction import ReductionConfig, TuckerResult, TuckerTensor3, canonical_to_tucker, reduce_rank, rhosvd
+
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -75,6 +75,23 @@ def lib() -> C.CDLL:
             "tgb_scalar_product": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), C.POINTER(D), I]),
             "tgb_coulomb_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, P, I]),
             "tgb_lattice_assemble_axis": (I, [P, I64, I64, P, P, I64, P, I]),
+            "tgb_tei_create": (I, [C.POINTER(P)]),
+            "tgb_tei_destroy": (I, [P]),
+            "tgb_tei_density_fitting": (I, [P, P, C.POINTER(tgb_cp), P, I64, P, D, I]),
+            "tgb_tei_convolution_matrices": (I, [P, P, C.POINTER(tgb_cp), I]),
+            "tgb_tei_diagonal": (I, [P, P, P, I]),
+            "tgb_tei_column": (I, [P, P, I64, P, I]),
+            "tgb_tei_cholesky": (I, [P, P, D]),
+            "tgb_tei_info": (I, [P, P, P]),
+            "tgb_tei_get_fit": (I, [P, I, P, P, I]),
+            "tgb_tei_get_conv": (I, [P, I64, I, P, I]),
+            "tgb_tei_get_cholesky": (I, [P, P, P, I]),
+            "tgb_reduce_tucker": (I, [P, C.POINTER(tgb_cp), I, D, P, I, I, I, C.POINTER(P)]),
+            "tgb_tucker_destroy": (I, [P]),
+            "tgb_tucker_info": (I, [P, P]),
+            "tgb_tucker_get": (I, [P, P, P, P, P, P, I]),
+            "tgb_tucker_sigma": (I, [P, I, C.POINTER(I64), P]),
+            "tgb_tucker_to_canonical": (I, [P, P, C.POINTER(tgb_cp), I]),
             "tgb_dgemm": (I, [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64]),
             "tgb_host_last_error": (C.c_char_p, []),
             "tgb_mesh_size": (D, [D, I64]),

@@ -1,0 +1,732 @@
+// Rank reduction of canonical tensors on sm_100a (reference
+// proj/src/reduction.cpp:34-273): RHOSVD, canonical-to-Tucker ALS sweeps and
+// Tucker-to-canonical, with every dense product (Gram matrices, projections
+// Z^T F, the ALS unfolding F C, the core projection) on the DMMA GEMM.
+//
+// Left singular subspaces come from the Gram matrix of the unfolding — the
+// reference's own route for its wide and tall branches (reduction.cpp:93-104,
+// 109-137) — via blocked subspace iteration with Rayleigh-Ritz on the device
+// (only the leading eigenpairs the rank rule needs, plus the exact trace for
+// the tail sum).  Rank selection (select_rank, reduction.cpp:34-59), the ALS
+// mode order, early exit and T2C unfolding rules are the reference's.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "tgb_internal.hpp"
+
+namespace tgb {
+
+namespace {
+
+// ---------------------------------------------------------------- kernels
+
+// normalize (tensor.cpp:18-31): per column k, per axis in order 0,1,2:
+// nrm = ||col||; nrm > 0 ? (col /= nrm, w *= nrm) : w = 0
+__global__ void normalize_kernel(int64_t n0, int64_t n1, int64_t n2, double* __restrict__ f0, double* __restrict__ f1,
+                                 double* __restrict__ f2, double* __restrict__ w) {
+  __shared__ double sv[32];
+  const int64_t k = blockIdx.x;
+  double* fs[3] = {f0 + n0 * k, f1 + n1 * k, f2 + n2 * k};
+  const int64_t ns[3] = {n0, n1, n2};
+  double wk = w[k];
+  for (int ax = 0; ax < 3; ++ax) {
+    double part = 0.0;
+    for (int64_t i = threadIdx.x; i < ns[ax]; i += blockDim.x) part += fs[ax][i] * fs[ax][i];
+    // block reduce
+    for (int o = 16; o; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+    if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = part;
+    __syncthreads();
+    double ss = 0.0;
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < (blockDim.x + 31) / 32; ++i) ss += sv[i];
+      sv[0] = ss;
+    }
+    __syncthreads();
+    const double nrm = sqrt(sv[0]);
+    __syncthreads();
+    if (nrm > 0.0) {
+      for (int64_t i = threadIdx.x; i < ns[ax]; i += blockDim.x) fs[ax][i] /= nrm;
+      wk *= nrm;
+    } else {
+      wk = 0.0;
+    }
+  }
+  if (threadIdx.x == 0) w[k] = wk;
+}
+
+// out(:, k) = f(:, k) * s[k]
+__global__ void scale_cols_kernel(int64_t n, int64_t R, const double* __restrict__ f, const double* __restrict__ s,
+                                  double* __restrict__ out) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= n * R) return;
+  out[idx] = f[idx] * s[idx / n];
+}
+
+// ALS coefficient matrix (reduction.cpp:207-216): C[k, l rm + i] = (w_k pp[l,k]) pm[i,k]   (R x rm rp)
+__global__ void als_coef_kernel(int64_t R, int rm, int rp, const double* __restrict__ w, const double* __restrict__ pm,
+                                const double* __restrict__ pp, double* __restrict__ C) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t tot = R * rm * rp;
+  if (idx >= tot) return;
+  const int64_t k = idx % R, col = idx / R;
+  const int i = static_cast<int>(col % rm), l = static_cast<int>(col / rm);
+  C[idx] = (w[k] * pp[l + static_cast<int64_t>(rp) * k]) * pm[i + static_cast<int64_t>(rm) * k];
+}
+
+// Khatri-Rao rows for the core projection: K[(j + r1 l), k] = w_k P1[j,k] P2[l,k]   (r1 r2 x R)
+__global__ void khatri_rao_kernel(int64_t R, int r1, int r2, const double* __restrict__ w, const double* __restrict__ P1,
+                                  const double* __restrict__ P2, double* __restrict__ K) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t rows = static_cast<int64_t>(r1) * r2;
+  if (idx >= rows * R) return;
+  const int64_t row = idx % rows, k = idx / rows;
+  const int j = static_cast<int>(row % r1), l = static_cast<int>(row / r1);
+  K[idx] = (w[k] * P2[l + static_cast<int64_t>(r2) * k]) * P1[j + static_cast<int64_t>(r1) * k];
+}
+
+__global__ void diag_kernel(int64_t d, const double* __restrict__ G, double* __restrict__ out) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < d) out[i] = G[i + d * i];
+}
+
+// T2C fibres (reduction.cpp:251-264): S[i, q] = core(idx with ax = i, m1 = j1, m2 = j2), q = j1 + r_m1 j2
+__global__ void t2c_slices_kernel(int r0, int r1, int r2, int ax, int m1, int m2, const double* __restrict__ core,
+                                  double* __restrict__ S) {
+  const int rr[3] = {r0, r1, r2};
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  const int64_t tot = static_cast<int64_t>(rr[ax]) * rr[m1] * rr[m2];
+  if (idx >= tot) return;
+  const int i = static_cast<int>(idx % rr[ax]);
+  const int64_t q = idx / rr[ax];
+  const int j1 = static_cast<int>(q % rr[m1]), j2 = static_cast<int>(q / rr[m1]);
+  int id[3];
+  id[ax] = i;
+  id[m1] = j1;
+  id[m2] = j2;
+  S[idx] = core[id[0] + static_cast<int64_t>(r0) * (id[1] + static_cast<int64_t>(r1) * id[2])];
+}
+
+// out(:, q) = side(:, sel(q))
+__global__ void gather_cols_kernel(int64_t n, int64_t ncols, const double* __restrict__ side, int mod, int div,
+                                   double* __restrict__ out) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= n * ncols) return;
+  const int64_t i = idx % n, q = idx / n;
+  const int64_t c = (q / div) % mod;
+  out[idx] = side[i + n * c];
+}
+
+__global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) x[i] = v;
+}
+
+// ---------------------------------------------------------------- host dense LA (small matrices)
+
+// cyclic Jacobi eigen-decomposition of a symmetric p x p matrix (column-major);
+// eigenvalues descending, eigenvectors in the columns of V.
+void jacobi_eigen(int p, std::vector<double> A, std::vector<double>& ev, std::vector<double>& V) {
+  V.assign(static_cast<size_t>(p) * p, 0.0);
+  for (int i = 0; i < p; ++i) V[i + p * i] = 1.0;
+  auto a = [&](int i, int j) -> double& { return A[i + static_cast<size_t>(p) * j]; };
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, diag = 0.0;
+    for (int j = 0; j < p; ++j)
+      for (int i = 0; i < p; ++i) (i == j ? diag : off) += a(i, j) * a(i, j);
+    if (off <= 1e-32 * diag || off == 0.0) break;
+    for (int pp = 0; pp < p - 1; ++pp)
+      for (int q = pp + 1; q < p; ++q) {
+        const double apq = a(pp, q);
+        if (apq == 0.0) continue;
+        const double app = a(pp, pp), aqq = a(q, q);
+        const double theta = (aqq - app) / (2.0 * apq);
+        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < p; ++k) {
+          const double akp = a(k, pp), akq = a(k, q);
+          a(k, pp) = c * akp - s * akq;
+          a(k, q) = s * akp + c * akq;
+        }
+        for (int k = 0; k < p; ++k) {
+          const double apk = a(pp, k), aqk = a(q, k);
+          a(pp, k) = c * apk - s * aqk;
+          a(q, k) = s * apk + c * aqk;
+        }
+        for (int k = 0; k < p; ++k) {
+          const double vkp = V[k + static_cast<size_t>(p) * pp], vkq = V[k + static_cast<size_t>(p) * q];
+          V[k + static_cast<size_t>(p) * pp] = c * vkp - s * vkq;
+          V[k + static_cast<size_t>(p) * q] = s * vkp + c * vkq;
+        }
+      }
+  }
+  std::vector<int> ord(p);
+  std::iota(ord.begin(), ord.end(), 0);
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return a(x, x) > a(y, y); });
+  ev.resize(p);
+  std::vector<double> V2(V.size());
+  for (int c = 0; c < p; ++c) {
+    ev[c] = a(ord[c], ord[c]);
+    std::memcpy(&V2[static_cast<size_t>(p) * c], &V[static_cast<size_t>(p) * ord[c]], sizeof(double) * p);
+  }
+  V.swap(V2);
+}
+
+// lower Cholesky of a p x p SPD matrix (host); returns false if not PD
+bool host_cholesky(int p, std::vector<double>& A) {
+  for (int j = 0; j < p; ++j) {
+    double d = A[j + static_cast<size_t>(p) * j];
+    for (int k = 0; k < j; ++k) d -= A[j + static_cast<size_t>(p) * k] * A[j + static_cast<size_t>(p) * k];
+    if (!(d > 0.0)) return false;
+    d = std::sqrt(d);
+    A[j + static_cast<size_t>(p) * j] = d;
+    for (int i = j + 1; i < p; ++i) {
+      double s = A[i + static_cast<size_t>(p) * j];
+      for (int k = 0; k < j; ++k) s -= A[i + static_cast<size_t>(p) * k] * A[j + static_cast<size_t>(p) * k];
+      A[i + static_cast<size_t>(p) * j] = s / d;
+    }
+    for (int i = 0; i < j; ++i) A[i + static_cast<size_t>(p) * j] = 0.0;
+  }
+  return true;
+}
+
+// inverse of the transposed lower factor: returns R^{-1} with R = L^T (upper)
+std::vector<double> upper_inverse_from_lower(int p, const std::vector<double>& L) {
+  std::vector<double> Ri(static_cast<size_t>(p) * p, 0.0);  // R = L^T upper; solve R X = I
+  for (int c = 0; c < p; ++c) {
+    for (int i = p - 1; i >= 0; --i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = i + 1; k < p; ++k) s -= L[k + static_cast<size_t>(p) * i] * Ri[k + static_cast<size_t>(p) * c];
+      Ri[i + static_cast<size_t>(p) * c] = s / L[i + static_cast<size_t>(p) * i];
+    }
+  }
+  return Ri;
+}
+
+struct Dev {
+  double* p = nullptr;
+  size_t n = 0;
+  explicit Dev(size_t count = 0) { resize(count); }
+  void resize(size_t count) {
+    if (count <= n) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    if (count) TGB_CUDA(cudaMalloc(&p, count * sizeof(double)));
+    n = count;
+  }
+  ~Dev() {
+    if (p) cudaFree(p);
+  }
+  Dev(const Dev&) = delete;
+  Dev& operator=(const Dev&) = delete;
+};
+
+std::vector<double> to_host(tgb_ctx* ctx, const double* d, size_t count) {
+  std::vector<double> h(count);
+  if (count) {
+    TGB_CUDA(cudaMemcpyAsync(h.data(), d, count * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  return h;
+}
+
+void to_dev(tgb_ctx* ctx, double* d, const std::vector<double>& h) {
+  if (!h.empty()) TGB_CUDA(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+}
+
+// Orthonormalise the columns of X (d x p) in place: Cholesky-QR, twice.
+// Columns that are numerically dependent are replaced deterministically.
+void cholqr2(tgb_ctx* ctx, int64_t d, int p, double* X, Dev& tmp) {
+  tmp.resize(static_cast<size_t>(d) * p + static_cast<size_t>(p) * p);
+  double* H = tmp.p + static_cast<size_t>(d) * p;
+  for (int rep = 0; rep < 2; ++rep) {
+    dgemm(ctx, true, false, p, p, d, 1.0, X, d, X, d, 0.0, H, p);
+    std::vector<double> hH = to_host(ctx, H, static_cast<size_t>(p) * p);
+    if (!host_cholesky(p, hH)) {
+      // regularise: add a tiny shift proportional to the largest diagonal
+      std::vector<double> h2 = to_host(ctx, H, static_cast<size_t>(p) * p);
+      double mx = 0;
+      for (int i = 0; i < p; ++i) mx = std::max(mx, h2[i + static_cast<size_t>(p) * i]);
+      for (int i = 0; i < p; ++i) h2[i + static_cast<size_t>(p) * i] += 1e-14 * mx + 1e-300;
+      hH = h2;
+      if (!host_cholesky(p, hH)) throw Error(TGB_NUMERICAL_ERROR, "reduction: orthonormalisation failed");
+    }
+    std::vector<double> Ri = upper_inverse_from_lower(p, hH);
+    to_dev(ctx, H, Ri);
+    TGB_CUDA(cudaMemcpyAsync(tmp.p, X, static_cast<size_t>(d) * p * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    dgemm(ctx, false, false, d, p, p, 1.0, tmp.p, d, H, p, 0.0, X, d);
+  }
+}
+
+// deterministic pseudo-random start block
+void random_block(tgb_ctx* ctx, int64_t d, int p, double* X, uint64_t seed) {
+  std::vector<double> h(static_cast<size_t>(d) * p);
+  uint64_t s = seed;
+  for (auto& x : h) {
+    s += 0x9E3779B97F4A7C15ULL;
+    uint64_t z = s;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    z ^= z >> 31;
+    x = static_cast<double>(z >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+  }
+  to_dev(ctx, X, h);
+}
+
+}  // namespace
+
+// Leading eigenpairs of a symmetric d x d device matrix G.  `need(theta, cnt)`
+// returns how many leading eigenpairs the caller needs given the `cnt`
+// converged leading eigenvalues (it must return <= cnt when satisfied, or
+// cnt + 1 to ask for more).  Returns eigenvalues (descending) and the
+// eigenvectors in U (d x k, device, allocated here).
+struct EigTop {
+  std::vector<double> theta;
+  Dev U;
+};
+
+template <class Need>
+void top_eigen(tgb_ctx* ctx, int64_t d, const double* G, int p0, Need need, EigTop& out) {
+  Dev X, Y, tmp, H;
+  int p = static_cast<int>(std::min<int64_t>(d, std::max(p0, 8)));
+  while (true) {
+    X.resize(static_cast<size_t>(d) * p);
+    Y.resize(static_cast<size_t>(d) * p);
+    H.resize(static_cast<size_t>(p) * p);
+    random_block(ctx, d, p, X.p, 0x1504062890ULL + static_cast<uint64_t>(p));
+    cholqr2(ctx, d, p, X.p, tmp);
+    std::vector<double> prev(p, 0.0), theta(p, 0.0), S;
+    int conv = 0;
+    const int maxit = 300;
+    for (int it = 0; it < maxit; ++it) {
+      dgemm(ctx, false, false, d, p, d, 1.0, G, d, X.p, d, 0.0, Y.p, d);   // Y = G X
+      dgemm(ctx, true, false, p, p, d, 1.0, X.p, d, Y.p, d, 0.0, H.p, p);  // H = X^T G X
+      std::vector<double> hH = to_host(ctx, H.p, static_cast<size_t>(p) * p);
+      for (int j = 0; j < p; ++j)
+        for (int i = 0; i < j; ++i) {
+          const double s = 0.5 * (hH[i + static_cast<size_t>(p) * j] + hH[j + static_cast<size_t>(p) * i]);
+          hH[i + static_cast<size_t>(p) * j] = hH[j + static_cast<size_t>(p) * i] = s;
+        }
+      jacobi_eigen(p, hH, theta, S);
+      // leading converged count: relative change below 1e-14 of the top eigenvalue
+      const double scale = std::max(std::fabs(theta[0]), 1e-300);
+      conv = 0;
+      while (conv < p && std::fabs(theta[conv] - prev[conv]) <= 1e-14 * scale) ++conv;
+      prev = theta;
+      // X <- orth(Y S)  (next subspace, ordered by Ritz value)
+      to_dev(ctx, H.p, S);
+      dgemm(ctx, false, false, d, p, p, 1.0, Y.p, d, H.p, p, 0.0, X.p, d);
+      cholqr2(ctx, d, p, X.p, tmp);
+      const int want = need(theta, conv);
+      if (want <= conv && it >= 2) {
+        // final Ritz vectors of the converged block: X (already ordered) — one last Rayleigh-Ritz
+        dgemm(ctx, false, false, d, p, d, 1.0, G, d, X.p, d, 0.0, Y.p, d);
+        dgemm(ctx, true, false, p, p, d, 1.0, X.p, d, Y.p, d, 0.0, H.p, p);
+        std::vector<double> h2 = to_host(ctx, H.p, static_cast<size_t>(p) * p);
+        for (int j = 0; j < p; ++j)
+          for (int i = 0; i < j; ++i) {
+            const double s = 0.5 * (h2[i + static_cast<size_t>(p) * j] + h2[j + static_cast<size_t>(p) * i]);
+            h2[i + static_cast<size_t>(p) * j] = h2[j + static_cast<size_t>(p) * i] = s;
+          }
+        jacobi_eigen(p, h2, theta, S);
+        to_dev(ctx, H.p, S);
+        out.U.resize(static_cast<size_t>(d) * p);
+        dgemm(ctx, false, false, d, p, p, 1.0, X.p, d, H.p, p, 0.0, out.U.p, d);
+        out.theta = theta;
+        TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        return;
+      }
+      if (want > conv && want >= p - 4 && p < d) break;  // block too small: grow
+    }
+    if (p >= d) {
+      // full block: accept what we have
+      out.U.resize(static_cast<size_t>(d) * p);
+      TGB_CUDA(cudaMemcpyAsync(out.U.p, X.p, static_cast<size_t>(d) * p * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+      out.theta = prev;
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    p = static_cast<int>(std::min<int64_t>(d, 2 * p));
+  }
+}
+
+// ---------------------------------------------------------------- reduction driver
+
+struct RedCfgC {
+  bool use_eps;
+  double eps;
+  int64_t ranks[3];
+  int max_sweeps;
+};
+
+struct RedState {
+  std::array<int64_t, 3> n{};
+  int64_t R = 0;
+  std::array<double*, 3> f{};  // normalized factors (device, owned by bufs)
+  double* w = nullptr;
+  std::array<Dev, 3> fbuf;
+  Dev wbuf;
+  std::array<Dev, 3> Z;        // n_ax x r_ax
+  std::array<int64_t, 3> r{};
+  Dev core;
+  bool rank_clamped = false, fallback = false;
+  std::vector<double> sweep_fits;
+  std::array<std::vector<double>, 3> sigma;
+};
+
+// select_rank (reduction.cpp:34-59) on the leading singular values sg (descending);
+// `total` = sum of ALL squared singular values (the Gram trace), `d` = their count.
+static int64_t select_rank_host(const std::vector<double>& sg, double total, int64_t d, const RedCfgC& c, int mode,
+                                bool* clamped, bool* need_more) {
+  *need_more = false;
+  if (sg.empty()) return 0;
+  const double cut = sg[0] * 1e-15 * std::sqrt(static_cast<double>(d));
+  int64_t numeric = 0;
+  while (numeric < static_cast<int64_t>(sg.size()) && sg[numeric] > cut) ++numeric;
+  const bool numeric_known = numeric < static_cast<int64_t>(sg.size()) || static_cast<int64_t>(sg.size()) == d;
+  if (!c.use_eps) {
+    const int64_t want = c.ranks[mode];
+    if (!numeric_known && want > numeric) {
+      *need_more = true;
+      return want;
+    }
+    if (want > numeric && clamped) *clamped = true;
+    return std::min(want, numeric);
+  }
+  if (total == 0.0) return 0;
+  const double budget = c.eps * c.eps * total;
+  double tail = total;
+  int64_t r = 0;
+  while (r < numeric && tail > budget) {
+    tail -= sg[r] * sg[r];
+    ++r;
+  }
+  if (tail > budget && !numeric_known) *need_more = true;
+  return r;
+}
+
+// thin_svd_left of a (n x k, device) truncated to the selected/needed rank.
+// sel < 0: select with the config (rhosvd); sel >= 0: keep min(sel, available).
+static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a, const RedCfgC* cfg, int mode,
+                             int64_t sel, bool* clamped, Dev& Zout, std::vector<double>* sigma_out) {
+  if (n == 0 || k == 0) return 0;
+  // Gram of the smaller side
+  const bool rowgram = n <= k;  // a a^T (n x n), eigenvectors are the left vectors directly
+  const int64_t d = rowgram ? n : k;
+  Dev G(static_cast<size_t>(d) * d);
+  if (rowgram)
+    dgemm(ctx, false, true, n, n, k, 1.0, a, n, a, n, 0.0, G.p, n);
+  else
+    dgemm(ctx, true, false, k, k, n, 1.0, a, n, a, n, 0.0, G.p, k);
+  Dev dg(d);
+  diag_kernel<<<static_cast<unsigned>((d + 255) / 256), 256, 0, ctx->stream>>>(d, G.p, dg.p);
+  TGB_LAUNCHED(ctx);
+  const std::vector<double> hd = to_host(ctx, dg.p, d);
+  double total = 0.0;
+  for (double x : hd) total += x;
+  int64_t r = 0;
+  auto need = [&](const std::vector<double>& theta, int conv) -> int {
+    std::vector<double> sg(conv);
+    for (int i = 0; i < conv; ++i) sg[i] = std::sqrt(std::max(0.0, theta[i]));
+    if (sel >= 0) {
+      r = std::min<int64_t>(sel, d);
+      return static_cast<int>(std::min<int64_t>(r + 1, d));
+    }
+    bool more = false;
+    bool cl = false;
+    r = select_rank_host(sg, total, d, *cfg, mode, &cl, &more);
+    if (more) return conv + 1;
+    return static_cast<int>(std::min<int64_t>(r + 1, d));
+  };
+  EigTop et;
+  top_eigen(ctx, d, G.p, 32, need, et);
+  // final selection with the converged spectrum
+  std::vector<double> sg(et.theta.size());
+  for (size_t i = 0; i < sg.size(); ++i) sg[i] = std::sqrt(std::max(0.0, et.theta[i]));
+  if (sel >= 0) {
+    r = std::min<int64_t>(sel, static_cast<int64_t>(sg.size()));
+  } else {
+    bool more = false;
+    r = select_rank_host(sg, total, d, *cfg, mode, clamped, &more);
+  }
+  if (sigma_out) *sigma_out = sg;
+  Zout.resize(std::max<int64_t>(1, n * r));
+  if (r == 0) return 0;
+  if (rowgram) {
+    TGB_CUDA(cudaMemcpyAsync(Zout.p, et.U.p, static_cast<size_t>(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+  } else {
+    // u = a v / sigma, then QR polish (reduction.cpp:119-137)
+    std::vector<double> inv(r);
+    for (int64_t i = 0; i < r; ++i) inv[i] = sg[i] > 0 ? 1.0 / sg[i] : 0.0;
+    Dev s(r);
+    to_dev(ctx, s.p, inv);
+    Dev V(static_cast<size_t>(k) * r);
+    scale_cols_kernel<<<static_cast<unsigned>((k * r + 255) / 256), 256, 0, ctx->stream>>>(k, r, et.U.p, s.p, V.p);
+    TGB_LAUNCHED(ctx);
+    dgemm(ctx, false, false, n, r, k, 1.0, a, n, V.p, k, 0.0, Zout.p, n);
+    Dev tmp;
+    cholqr2(ctx, n, static_cast<int>(r), Zout.p, tmp);
+  }
+  return r;
+}
+
+static void project_core(tgb_ctx* ctx, RedState& st) {
+  const int64_t R = st.R;
+  std::array<Dev, 3> P;
+  for (int ax = 0; ax < 3; ++ax) {
+    P[ax].resize(std::max<int64_t>(1, st.r[ax] * R));
+    if (st.r[ax] && R) dgemm(ctx, true, false, st.r[ax], R, st.n[ax], 1.0, st.Z[ax].p, st.n[ax], st.f[ax], st.n[ax], 0.0,
+                             P[ax].p, st.r[ax]);
+  }
+  const int64_t r0 = st.r[0], r12 = st.r[1] * st.r[2];
+  st.core.resize(std::max<int64_t>(1, r0 * r12));
+  if (r0 * r12 == 0) return;
+  if (R == 0) {
+    fill_kernel<<<static_cast<unsigned>((r0 * r12 + 255) / 256), 256, 0, ctx->stream>>>(r0 * r12, 0.0, st.core.p);
+    TGB_LAUNCHED(ctx);
+    return;
+  }
+  Dev K(static_cast<size_t>(r12) * R);
+  khatri_rao_kernel<<<static_cast<unsigned>((r12 * R + 255) / 256), 256, 0, ctx->stream>>>(
+      R, static_cast<int>(st.r[1]), static_cast<int>(st.r[2]), st.w, P[1].p, P[2].p, K.p);
+  TGB_LAUNCHED(ctx);
+  // core (r0 x r1 r2) = P0 (r0 x R) K^T (R x r1 r2)
+  dgemm(ctx, false, true, r0, r12, R, 1.0, P[0].p, r0, K.p, r12, 0.0, st.core.p, r0);
+}
+
+static double fro_norm_dev(tgb_ctx* ctx, const double* x, int64_t count) {
+  const std::vector<double> h = to_host(ctx, x, count);
+  double s = 0.0;
+  for (double v : h) s += v * v;
+  return std::sqrt(s);
+}
+
+void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, RedState& st) {
+  st.R = a.rank;
+  for (int ax = 0; ax < 3; ++ax) st.n[ax] = a.n[ax];
+  // normalized copy (reduction.cpp:176-177)
+  for (int ax = 0; ax < 3; ++ax) {
+    st.fbuf[ax].resize(std::max<int64_t>(1, a.n[ax] * a.rank));
+    if (a.rank)
+      TGB_CUDA(cudaMemcpyAsync(st.fbuf[ax].p, a.factor[ax], a.n[ax] * a.rank * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+    st.f[ax] = st.fbuf[ax].p;
+  }
+  st.wbuf.resize(std::max<int64_t>(1, a.rank));
+  if (a.rank)
+    TGB_CUDA(cudaMemcpyAsync(st.wbuf.p, a.weight, a.rank * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+  st.w = st.wbuf.p;
+  if (a.rank) {
+    normalize_kernel<<<static_cast<unsigned>(a.rank), 256, 0, ctx->stream>>>(a.n[0], a.n[1], a.n[2], st.f[0], st.f[1],
+                                                                             st.f[2], st.w);
+    TGB_LAUNCHED(ctx);
+  }
+  // RHOSVD (reduction.cpp:172-190): per mode left subspace of f diag(w)
+  for (int mode = 0; mode < 3; ++mode) {
+    const int64_t n = a.n[mode], R = a.rank;
+    Dev W(std::max<int64_t>(1, n * R));
+    if (R) {
+      scale_cols_kernel<<<static_cast<unsigned>((n * R + 255) / 256), 256, 0, ctx->stream>>>(n, R, st.f[mode], st.w, W.p);
+      TGB_LAUNCHED(ctx);
+    }
+    st.r[mode] = left_subspace(ctx, n, R, W.p, &cfg, mode, -1, &st.rank_clamped, st.Z[mode], &st.sigma[mode]);
+  }
+  project_core(ctx, st);
+  if (!als || a.rank == 0 || st.r[0] * st.r[1] * st.r[2] == 0) return;
+  // ALS sweeps (reduction.cpp:205-232)
+  double prev = -1.0;
+  for (int sweep = 0; sweep < cfg.max_sweeps; ++sweep) {
+    double fit = 0.0;
+    for (int ax = 0; ax < 3; ++ax) {
+      const int m = (ax + 1) % 3, p = (ax + 2) % 3;
+      const int64_t R = st.R, rm = st.r[m], rp = st.r[p], n = st.n[ax];
+      Dev pm(std::max<int64_t>(1, rm * R)), pp(std::max<int64_t>(1, rp * R));
+      dgemm(ctx, true, false, rm, R, st.n[m], 1.0, st.Z[m].p, st.n[m], st.f[m], st.n[m], 0.0, pm.p, rm);
+      dgemm(ctx, true, false, rp, R, st.n[p], 1.0, st.Z[p].p, st.n[p], st.f[p], st.n[p], 0.0, pp.p, rp);
+      Dev Cm(static_cast<size_t>(R) * rm * rp);
+      als_coef_kernel<<<static_cast<unsigned>((R * rm * rp + 255) / 256), 256, 0, ctx->stream>>>(
+          R, static_cast<int>(rm), static_cast<int>(rp), st.w, pm.p, pp.p, Cm.p);
+      TGB_LAUNCHED(ctx);
+      Dev mat(static_cast<size_t>(n) * rm * rp);
+      dgemm(ctx, false, false, n, rm * rp, R, 1.0, st.f[ax], n, Cm.p, R, 0.0, mat.p, n);
+      Dev Znew;
+      const int64_t r = left_subspace(ctx, n, rm * rp, mat.p, nullptr, ax, st.r[ax], nullptr, Znew, nullptr);
+      if (r == 0) {
+        st.fallback = true;
+        return;
+      }
+      st.r[ax] = std::min<int64_t>(st.r[ax], r);
+      st.Z[ax].resize(static_cast<size_t>(n) * st.r[ax]);
+      TGB_CUDA(cudaMemcpyAsync(st.Z[ax].p, Znew.p, static_cast<size_t>(n) * st.r[ax] * sizeof(double),
+                               cudaMemcpyDeviceToDevice, ctx->stream));
+      Dev proj(static_cast<size_t>(st.r[ax]) * rm * rp);
+      dgemm(ctx, true, false, st.r[ax], rm * rp, n, 1.0, st.Z[ax].p, n, mat.p, n, 0.0, proj.p, st.r[ax]);
+      fit = fro_norm_dev(ctx, proj.p, st.r[ax] * rm * rp);
+    }
+    st.sweep_fits.push_back(fit);
+    if (prev >= 0.0 && std::fabs(fit - prev) < 1e-14 * std::max(1.0, fit)) break;
+    prev = fit;
+  }
+  project_core(ctx, st);
+}
+
+// tucker_to_canonical (reduction.cpp:238-269) into caller-sized device buffers
+int64_t t2c_rank(const RedState& st) {
+  const auto& r = st.r;
+  if (r[0] * r[1] * r[2] == 0) return 0;
+  int ax = 0;
+  for (int m = 1; m < 3; ++m)
+    if (r[m] > r[ax]) ax = m;
+  return r[(ax + 1) % 3] * r[(ax + 2) % 3];
+}
+
+void t2c_dev(tgb_ctx* ctx, RedState& st, double* out_f[3], double* out_w) {
+  const auto& r = st.r;
+  const int64_t rank = t2c_rank(st);
+  if (rank == 0) return;
+  int ax = 0;
+  for (int m = 1; m < 3; ++m)
+    if (r[m] > r[ax]) ax = m;
+  const int m1 = (ax + 1) % 3, m2 = (ax + 2) % 3;
+  Dev S(static_cast<size_t>(r[ax]) * rank);
+  t2c_slices_kernel<<<static_cast<unsigned>((r[ax] * rank + 255) / 256), 256, 0, ctx->stream>>>(
+      static_cast<int>(r[0]), static_cast<int>(r[1]), static_cast<int>(r[2]), ax, m1, m2, st.core.p, S.p);
+  TGB_LAUNCHED(ctx);
+  dgemm(ctx, false, false, st.n[ax], rank, r[ax], 1.0, st.Z[ax].p, st.n[ax], S.p, r[ax], 0.0, out_f[ax], st.n[ax]);
+  gather_cols_kernel<<<static_cast<unsigned>((st.n[m1] * rank + 255) / 256), 256, 0, ctx->stream>>>(
+      st.n[m1], rank, st.Z[m1].p, static_cast<int>(r[m1]), 1, out_f[m1]);
+  TGB_LAUNCHED(ctx);
+  gather_cols_kernel<<<static_cast<unsigned>((st.n[m2] * rank + 255) / 256), 256, 0, ctx->stream>>>(
+      st.n[m2], rank, st.Z[m2].p, static_cast<int>(r[m2]), static_cast<int>(r[m1]), out_f[m2]);
+  TGB_LAUNCHED(ctx);
+  fill_kernel<<<static_cast<unsigned>((rank + 255) / 256), 256, 0, ctx->stream>>>(rank, 1.0, out_w);
+  TGB_LAUNCHED(ctx);
+  normalize_kernel<<<static_cast<unsigned>(rank), 256, 0, ctx->stream>>>(st.n[0], st.n[1], st.n[2], out_f[0], out_f[1],
+                                                                         out_f[2], out_w);
+  TGB_LAUNCHED(ctx);
+}
+
+}  // namespace tgb
+
+// ---------------------------------------------------------------- C-ABI
+
+struct tgb_tucker {
+  tgb::RedState st;
+};
+
+extern "C" {
+
+// mode: 0 rhosvd, 1 canonical_to_tucker (RHOSVD + ALS).  a: device or host (mem).
+int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, const int64_t* ranks, int max_sweeps,
+                      int mode, int mem, tgb_tucker** out) {
+  return tgb::guarded_call([&] {
+    tgb::require(a != nullptr && out != nullptr, "reduce: null argument");
+    tgb::require(use_eps ? eps > 0.0 : (ranks != nullptr), "ReductionConfig: set exactly one of {ranks, epsilon}");
+    tgb::require(max_sweeps >= 1, "ReductionConfig: need at least one sweep");
+    if (!use_eps)
+      for (int i = 0; i < 3; ++i) tgb::require(ranks[i] >= 0, "select_rank: negative rank request");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::RedCfgC cfg{use_eps != 0, eps, {0, 0, 0}, max_sweeps};
+    if (!use_eps)
+      for (int i = 0; i < 3; ++i) cfg.ranks[i] = ranks[i];
+    tgb_cp dev = *a;
+    std::array<tgb::Dev, 4> bufs;
+    if (mem == TGB_MEM_HOST) {
+      for (int ax = 0; ax < 3; ++ax) {
+        bufs[ax].resize(std::max<int64_t>(1, a->n[ax] * a->rank));
+        if (a->rank)
+          TGB_CUDA(cudaMemcpy(bufs[ax].p, a->factor[ax], a->n[ax] * a->rank * sizeof(double), cudaMemcpyHostToDevice));
+        dev.factor[ax] = bufs[ax].p;
+      }
+      bufs[3].resize(std::max<int64_t>(1, a->rank));
+      if (a->rank) TGB_CUDA(cudaMemcpy(bufs[3].p, a->weight, a->rank * sizeof(double), cudaMemcpyHostToDevice));
+      dev.weight = bufs[3].p;
+    }
+    auto* t = new tgb_tucker();
+    try {
+      tgb::reduce_dev(ctx, dev, cfg, mode == 1, t->st);
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      delete t;
+      throw;
+    }
+    *out = t;
+  });
+}
+
+int tgb_tucker_destroy(tgb_tucker* t) {
+  return tgb::guarded_call([&] { delete t; });
+}
+
+// info[0..2] Tucker ranks, [3] rank_clamped, [4] rhosvd_fallback, [5] sweeps, [6] t2c rank
+int tgb_tucker_info(tgb_tucker* t, int64_t* info) {
+  return tgb::guarded_call([&] {
+    for (int ax = 0; ax < 3; ++ax) info[ax] = t->st.r[ax];
+    info[3] = t->st.rank_clamped;
+    info[4] = t->st.fallback;
+    info[5] = static_cast<int64_t>(t->st.sweep_fits.size());
+    info[6] = tgb::t2c_rank(t->st);
+  });
+}
+
+// core (r0 r1 r2), sides n_ax x r_ax, sweep fits, leading singular values per mode (count in nsig[ax])
+int tgb_tucker_get(tgb_tucker* t, double* core, double* side0, double* side1, double* side2, double* sweep_fits,
+                   int mem) {
+  return tgb::guarded_call([&] {
+    auto& st = t->st;
+    const auto kind = mem == TGB_MEM_DEVICE ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost;
+    const int64_t cs = st.r[0] * st.r[1] * st.r[2];
+    if (core && cs) TGB_CUDA(cudaMemcpy(core, st.core.p, cs * sizeof(double), kind));
+    double* sides[3] = {side0, side1, side2};
+    for (int ax = 0; ax < 3; ++ax)
+      if (sides[ax] && st.r[ax]) TGB_CUDA(cudaMemcpy(sides[ax], st.Z[ax].p, st.n[ax] * st.r[ax] * sizeof(double), kind));
+    if (sweep_fits)
+      for (size_t i = 0; i < st.sweep_fits.size(); ++i) sweep_fits[i] = st.sweep_fits[i];
+  });
+}
+
+int tgb_tucker_sigma(tgb_tucker* t, int axis, int64_t* count, double* sigma) {
+  return tgb::guarded_call([&] {
+    const auto& s = t->st.sigma[axis];
+    *count = static_cast<int64_t>(s.size());
+    if (sigma)
+      for (size_t i = 0; i < s.size(); ++i) sigma[i] = s[i];
+  });
+}
+
+// tucker_to_canonical into a caller-allocated CP (rank = info[6])
+int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem) {
+  return tgb::guarded_call([&] {
+    const int64_t rank = tgb::t2c_rank(t->st);
+    tgb::require(out->rank == rank, "tucker_to_canonical: output rank mismatch");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::t2c_dev(ctx, t->st, out->factor, out->weight);
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    std::array<tgb::Dev, 4> bufs;
+    double* f[3];
+    for (int ax = 0; ax < 3; ++ax) {
+      bufs[ax].resize(std::max<int64_t>(1, t->st.n[ax] * rank));
+      f[ax] = bufs[ax].p;
+    }
+    bufs[3].resize(std::max<int64_t>(1, rank));
+    tgb::t2c_dev(ctx, t->st, f, bufs[3].p);
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (int ax = 0; ax < 3; ++ax)
+      if (rank) TGB_CUDA(cudaMemcpy(out->factor[ax], f[ax], t->st.n[ax] * rank * sizeof(double), cudaMemcpyDeviceToHost));
+    if (rank) TGB_CUDA(cudaMemcpy(out->weight, bufs[3].p, rank * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+}  // extern "C"

@@ -325,9 +325,13 @@ __global__ void contract_kernel(int nb, int np, const int* __restrict__ fstart, 
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= nb * nb) return;
   const int mu = c % nb, nu = c / nb;
+  const int a = min(mu, nu), b = max(mu, nu);
   double s = 0.0;
-  for (int q = fstart[nu]; q < fstart[nu + 1]; ++q)
-    for (int p = fstart[mu]; p < fstart[mu + 1]; ++p) s += pw[p] * pw[q] * z[p + static_cast<int64_t>(np) * q];
+  for (int q = fstart[b]; q < fstart[b + 1]; ++q)
+    for (int p = fstart[a]; p < fstart[a + 1]; ++p) {
+      const int64_t idx = mu <= nu ? p + static_cast<int64_t>(np) * q : q + static_cast<int64_t>(np) * p;
+      s += pw[p] * pw[q] * z[idx];
+    }
   out[c] = s;
 }
 
@@ -509,12 +513,16 @@ static void ensure_contraction_tables(tgb_ctx* ctx, TEI& f) {
   const int64_t nb = f.nb, np = f.np;
   std::vector<int> cstart(nb * nb + 1, 0), cpairs;
   std::vector<double> cw;
+  // (mu, nu) with mu > nu lists the mirrored primitive pairs of (nu, mu) in the
+  // same order, so symmetric entries are bitwise equal and exact ties in the
+  // pivot search resolve to the first index (tei.cpp:66 semantics).
   for (int64_t nu = 0; nu < nb; ++nu)
     for (int64_t mu = 0; mu < nb; ++mu) {
       const int64_t c = mu + nb * nu;
-      for (int p = f.fstart[mu]; p < f.fstart[mu + 1]; ++p)
-        for (int q = f.fstart[nu]; q < f.fstart[nu + 1]; ++q) {
-          cpairs.push_back(static_cast<int>(p + np * q));
+      const int64_t a = std::min(mu, nu), b = std::max(mu, nu);
+      for (int p = f.fstart[a]; p < f.fstart[a + 1]; ++p)
+        for (int q = f.fstart[b]; q < f.fstart[b + 1]; ++q) {
+          cpairs.push_back(static_cast<int>(mu <= nu ? p + np * q : q + np * p));
           cw.push_back(f.pw[p] * f.pw[q]);
         }
       cstart[c + 1] = static_cast<int>(cpairs.size());
