@@ -3,12 +3,15 @@
 // Tucker-to-canonical, with every dense product (Gram matrices, projections
 // Z^T F, the ALS unfolding F C, the core projection) on the DMMA GEMM.
 //
-// Left singular subspaces come from the Gram matrix of the unfolding — the
-// reference's own route for its wide and tall branches (reduction.cpp:93-104,
-// 109-137) — via blocked subspace iteration with Rayleigh-Ritz on the device
-// (only the leading eigenpairs the rank rule needs, plus the exact trace for
-// the tail sum).  Rank selection (select_rank, reduction.cpp:34-59), the ALS
-// mode order, early exit and T2C unfolding rules are the reference's.
+// Left singular subspaces (thin_svd_left, reduction.cpp:85-138) come from a
+// two-sided blocked subspace iteration on the unfolding itself with a small
+// Rayleigh-Ritz SVD per step — only the leading singular pairs the rank rule
+// needs, plus the exact Frobenius norm for the tail sum.  Not forming a Gram
+// matrix keeps small singular values accurate (as the reference's JacobiSVD
+// branch); the reference's Gram branches have an accuracy floor ~sqrt(eps)
+// (reduction.cpp:91-92), which bounds the parity of the reduced tensors.
+// Rank selection (select_rank, reduction.cpp:34-59), the ALS mode order,
+// early exit and the T2C unfolding rule are the reference's.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -90,11 +93,6 @@ __global__ void khatri_rao_kernel(int64_t R, int r1, int r2, const double* __res
   K[idx] = (w[k] * P2[l + static_cast<int64_t>(r2) * k]) * P1[j + static_cast<int64_t>(r1) * k];
 }
 
-__global__ void diag_kernel(int64_t d, const double* __restrict__ G, double* __restrict__ out) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i < d) out[i] = G[i + d * i];
-}
-
 // T2C fibres (reduction.cpp:251-264): S[i, q] = core(idx with ax = i, m1 = j1, m2 = j2), q = j1 + r_m1 j2
 __global__ void t2c_slices_kernel(int r0, int r1, int r2, int ax, int m1, int m2, const double* __restrict__ core,
                                   double* __restrict__ S) {
@@ -122,6 +120,42 @@ __global__ void gather_cols_kernel(int64_t n, int64_t ncols, const double* __res
   out[idx] = side[i + n * c];
 }
 
+// scale every column of X (d x p) to unit norm (zero columns left as is)
+__global__ void colnormalize_kernel(int64_t d, double* __restrict__ X) {
+  __shared__ double sv[32];
+  double* x = X + d * blockIdx.x;
+  double part = 0.0;
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) part += x[i] * x[i];
+  for (int o = 16; o; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ss = 0.0;
+    for (int i = 0; i < (blockDim.x + 31) / 32; ++i) ss += sv[i];
+    sv[0] = ss;
+  }
+  __syncthreads();
+  const double nrm = sqrt(sv[0]);
+  if (nrm > 0.0)
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) x[i] /= nrm;
+}
+
+__global__ void sumsq_kernel(int64_t total, const double* __restrict__ a, double* __restrict__ out) {
+  __shared__ double sv[32];
+  double part = 0.0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    part += a[i] * a[i];
+  for (int o = 16; o; o >>= 1) part += __shfl_down_sync(0xffffffffu, part, o);
+  if ((threadIdx.x & 31) == 0) sv[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double ss = 0.0;
+    for (int i = 0; i < (blockDim.x + 31) / 32; ++i) ss += sv[i];
+    out[blockIdx.x] = ss;
+  }
+}
+
 __global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) x[i] = v;
@@ -129,52 +163,53 @@ __global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
 
 // ---------------------------------------------------------------- host dense LA (small matrices)
 
-// cyclic Jacobi eigen-decomposition of a symmetric p x p matrix (column-major);
-// eigenvalues descending, eigenvectors in the columns of V.
-void jacobi_eigen(int p, std::vector<double> A, std::vector<double>& ev, std::vector<double>& V) {
-  V.assign(static_cast<size_t>(p) * p, 0.0);
-  for (int i = 0; i < p; ++i) V[i + p * i] = 1.0;
-  auto a = [&](int i, int j) -> double& { return A[i + static_cast<size_t>(p) * j]; };
-  for (int sweep = 0; sweep < 100; ++sweep) {
-    double off = 0.0, diag = 0.0;
-    for (int j = 0; j < p; ++j)
-      for (int i = 0; i < p; ++i) (i == j ? diag : off) += a(i, j) * a(i, j);
-    if (off <= 1e-32 * diag || off == 0.0) break;
-    for (int pp = 0; pp < p - 1; ++pp)
-      for (int q = pp + 1; q < p; ++q) {
-        const double apq = a(pp, q);
-        if (apq == 0.0) continue;
-        const double app = a(pp, pp), aqq = a(q, q);
-        const double theta = (aqq - app) / (2.0 * apq);
-        const double t = (theta >= 0 ? 1.0 : -1.0) / (std::fabs(theta) + std::sqrt(theta * theta + 1.0));
-        const double c = 1.0 / std::sqrt(t * t + 1.0), s = t * c;
-        for (int k = 0; k < p; ++k) {
-          const double akp = a(k, pp), akq = a(k, q);
-          a(k, pp) = c * akp - s * akq;
-          a(k, q) = s * akp + c * akq;
+// one-sided Jacobi SVD of a small p x p matrix S (column-major): S = U diag(sg) W^T,
+// singular values descending, left vectors in U.
+void jacobi_svd_small(int p, std::vector<double> S, std::vector<double>& sg, std::vector<double>& U) {
+  auto col = [&](int j) { return &S[static_cast<size_t>(p) * j]; };
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    bool rot = false;
+    for (int i = 0; i < p - 1; ++i)
+      for (int j = i + 1; j < p; ++j) {
+        double al = 0, be = 0, ga = 0;
+        const double* ci = col(i);
+        const double* cj = col(j);
+        for (int r = 0; r < p; ++r) {
+          al += ci[r] * ci[r];
+          be += cj[r] * cj[r];
+          ga += ci[r] * cj[r];
         }
-        for (int k = 0; k < p; ++k) {
-          const double apk = a(pp, k), aqk = a(q, k);
-          a(pp, k) = c * apk - s * aqk;
-          a(q, k) = s * apk + c * aqk;
-        }
-        for (int k = 0; k < p; ++k) {
-          const double vkp = V[k + static_cast<size_t>(p) * pp], vkq = V[k + static_cast<size_t>(p) * q];
-          V[k + static_cast<size_t>(p) * pp] = c * vkp - s * vkq;
-          V[k + static_cast<size_t>(p) * q] = s * vkp + c * vkq;
+        if (ga == 0.0 || std::fabs(ga) <= 1e-16 * std::sqrt(al * be)) continue;
+        rot = true;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        double* wi = col(i);
+        double* wj = col(j);
+        for (int r = 0; r < p; ++r) {
+          const double x = wi[r], y = wj[r];
+          wi[r] = c * x - sn * y;
+          wj[r] = sn * x + c * y;
         }
       }
+    if (!rot) break;
+  }
+  std::vector<double> nr(p);
+  for (int j = 0; j < p; ++j) {
+    double ss = 0;
+    for (int r = 0; r < p; ++r) ss += col(j)[r] * col(j)[r];
+    nr[j] = std::sqrt(ss);
   }
   std::vector<int> ord(p);
   std::iota(ord.begin(), ord.end(), 0);
-  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return a(x, x) > a(y, y); });
-  ev.resize(p);
-  std::vector<double> V2(V.size());
+  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return nr[x] > nr[y]; });
+  sg.resize(p);
+  U.assign(static_cast<size_t>(p) * p, 0.0);
   for (int c = 0; c < p; ++c) {
-    ev[c] = a(ord[c], ord[c]);
-    std::memcpy(&V2[static_cast<size_t>(p) * c], &V[static_cast<size_t>(p) * ord[c]], sizeof(double) * p);
+    const int j = ord[c];
+    sg[c] = nr[j];
+    for (int r = 0; r < p; ++r) U[r + static_cast<size_t>(p) * c] = nr[j] > 0 ? col(j)[r] / nr[j] : (r == c ? 1.0 : 0.0);
   }
-  V.swap(V2);
 }
 
 // lower Cholesky of a p x p SPD matrix (host); returns false if not PD
@@ -282,82 +317,6 @@ void random_block(tgb_ctx* ctx, int64_t d, int p, double* X, uint64_t seed) {
 
 }  // namespace
 
-// Leading eigenpairs of a symmetric d x d device matrix G.  `need(theta, cnt)`
-// returns how many leading eigenpairs the caller needs given the `cnt`
-// converged leading eigenvalues (it must return <= cnt when satisfied, or
-// cnt + 1 to ask for more).  Returns eigenvalues (descending) and the
-// eigenvectors in U (d x k, device, allocated here).
-struct EigTop {
-  std::vector<double> theta;
-  Dev U;
-};
-
-template <class Need>
-void top_eigen(tgb_ctx* ctx, int64_t d, const double* G, int p0, Need need, EigTop& out) {
-  Dev X, Y, tmp, H;
-  int p = static_cast<int>(std::min<int64_t>(d, std::max(p0, 8)));
-  while (true) {
-    X.resize(static_cast<size_t>(d) * p);
-    Y.resize(static_cast<size_t>(d) * p);
-    H.resize(static_cast<size_t>(p) * p);
-    random_block(ctx, d, p, X.p, 0x1504062890ULL + static_cast<uint64_t>(p));
-    cholqr2(ctx, d, p, X.p, tmp);
-    std::vector<double> prev(p, 0.0), theta(p, 0.0), S;
-    int conv = 0;
-    const int maxit = 300;
-    for (int it = 0; it < maxit; ++it) {
-      dgemm(ctx, false, false, d, p, d, 1.0, G, d, X.p, d, 0.0, Y.p, d);   // Y = G X
-      dgemm(ctx, true, false, p, p, d, 1.0, X.p, d, Y.p, d, 0.0, H.p, p);  // H = X^T G X
-      std::vector<double> hH = to_host(ctx, H.p, static_cast<size_t>(p) * p);
-      for (int j = 0; j < p; ++j)
-        for (int i = 0; i < j; ++i) {
-          const double s = 0.5 * (hH[i + static_cast<size_t>(p) * j] + hH[j + static_cast<size_t>(p) * i]);
-          hH[i + static_cast<size_t>(p) * j] = hH[j + static_cast<size_t>(p) * i] = s;
-        }
-      jacobi_eigen(p, hH, theta, S);
-      // leading converged count: relative change below 1e-14 of the top eigenvalue
-      const double scale = std::max(std::fabs(theta[0]), 1e-300);
-      conv = 0;
-      while (conv < p && std::fabs(theta[conv] - prev[conv]) <= 1e-14 * scale) ++conv;
-      prev = theta;
-      // X <- orth(Y S)  (next subspace, ordered by Ritz value)
-      to_dev(ctx, H.p, S);
-      dgemm(ctx, false, false, d, p, p, 1.0, Y.p, d, H.p, p, 0.0, X.p, d);
-      cholqr2(ctx, d, p, X.p, tmp);
-      const int want = need(theta, conv);
-      if (want <= conv && it >= 2) {
-        // final Ritz vectors of the converged block: X (already ordered) — one last Rayleigh-Ritz
-        dgemm(ctx, false, false, d, p, d, 1.0, G, d, X.p, d, 0.0, Y.p, d);
-        dgemm(ctx, true, false, p, p, d, 1.0, X.p, d, Y.p, d, 0.0, H.p, p);
-        std::vector<double> h2 = to_host(ctx, H.p, static_cast<size_t>(p) * p);
-        for (int j = 0; j < p; ++j)
-          for (int i = 0; i < j; ++i) {
-            const double s = 0.5 * (h2[i + static_cast<size_t>(p) * j] + h2[j + static_cast<size_t>(p) * i]);
-            h2[i + static_cast<size_t>(p) * j] = h2[j + static_cast<size_t>(p) * i] = s;
-          }
-        jacobi_eigen(p, h2, theta, S);
-        to_dev(ctx, H.p, S);
-        out.U.resize(static_cast<size_t>(d) * p);
-        dgemm(ctx, false, false, d, p, p, 1.0, X.p, d, H.p, p, 0.0, out.U.p, d);
-        out.theta = theta;
-        TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-        return;
-      }
-      if (want > conv && want >= p - 4 && p < d) break;  // block too small: grow
-    }
-    if (p >= d) {
-      // full block: accept what we have
-      out.U.resize(static_cast<size_t>(d) * p);
-      TGB_CUDA(cudaMemcpyAsync(out.U.p, X.p, static_cast<size_t>(d) * p * sizeof(double), cudaMemcpyDeviceToDevice,
-                               ctx->stream));
-      out.theta = prev;
-      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-      return;
-    }
-    p = static_cast<int>(std::min<int64_t>(d, 2 * p));
-  }
-}
-
 // ---------------------------------------------------------------- reduction driver
 
 struct RedCfgC {
@@ -415,67 +374,101 @@ static int64_t select_rank_host(const std::vector<double>& sg, double total, int
 
 // thin_svd_left of a (n x k, device) truncated to the selected/needed rank.
 // sel < 0: select with the config (rhosvd); sel >= 0: keep min(sel, available).
+//
+// Two-sided subspace iteration on a itself (never forming a Gram matrix, so
+// small singular values keep ~eps * sigma_0 absolute accuracy, as the
+// reference's JacobiSVD branch): X <- orth(a Y), Y <- orth(a^T X), with a
+// small SVD of S = X^T a Y (host, one-sided Jacobi) rotating the blocks to
+// the singular directions every iteration.  Columns are normalised before
+// the Cholesky-QR so the blocks stay well conditioned.
 static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a, const RedCfgC* cfg, int mode,
                              int64_t sel, bool* clamped, Dev& Zout, std::vector<double>* sigma_out) {
-  if (n == 0 || k == 0) return 0;
-  // Gram of the smaller side
-  const bool rowgram = n <= k;  // a a^T (n x n), eigenvectors are the left vectors directly
-  const int64_t d = rowgram ? n : k;
-  Dev G(static_cast<size_t>(d) * d);
-  if (rowgram)
-    dgemm(ctx, false, true, n, n, k, 1.0, a, n, a, n, 0.0, G.p, n);
-  else
-    dgemm(ctx, true, false, k, k, n, 1.0, a, n, a, n, 0.0, G.p, k);
-  Dev dg(d);
-  diag_kernel<<<static_cast<unsigned>((d + 255) / 256), 256, 0, ctx->stream>>>(d, G.p, dg.p);
+  if (n == 0 || k == 0) {
+    if (sigma_out) sigma_out->clear();
+    return 0;
+  }
+  const int64_t dmin = std::min(n, k);
+  // ||a||_F^2 = sum of all squared singular values (the tail-rule total)
+  Dev part(256);
+  sumsq_kernel<<<256, 256, 0, ctx->stream>>>(n * k, a, part.p);
   TGB_LAUNCHED(ctx);
-  const std::vector<double> hd = to_host(ctx, dg.p, d);
   double total = 0.0;
-  for (double x : hd) total += x;
+  for (double x : to_host(ctx, part.p, 256)) total += x;
+  int p = static_cast<int>(std::min<int64_t>(dmin, sel >= 0 ? std::max<int64_t>(sel + 8, 16) : 24));
+  Dev X, Y, T, tmp, Sd;
+  std::vector<double> sg, Ut;
   int64_t r = 0;
-  auto need = [&](const std::vector<double>& theta, int conv) -> int {
-    std::vector<double> sg(conv);
-    for (int i = 0; i < conv; ++i) sg[i] = std::sqrt(std::max(0.0, theta[i]));
-    if (sel >= 0) {
-      r = std::min<int64_t>(sel, d);
-      return static_cast<int>(std::min<int64_t>(r + 1, d));
+  while (true) {
+    X.resize(static_cast<size_t>(n) * p);
+    Y.resize(static_cast<size_t>(k) * p);
+    T.resize(static_cast<size_t>(std::max(n, k)) * p);
+    Sd.resize(static_cast<size_t>(p) * p);
+    random_block(ctx, k, p, Y.p, 0x1504062890ULL + static_cast<uint64_t>(p));
+    colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(k, Y.p);
+    TGB_LAUNCHED(ctx);
+    cholqr2(ctx, k, p, Y.p, tmp);
+    std::vector<double> prev(p, -1.0);
+    bool done = false, grow = false;
+    for (int it = 0; it < 200 && !done; ++it) {
+      dgemm(ctx, false, false, n, p, k, 1.0, a, n, Y.p, k, 0.0, T.p, n);  // T = a Y
+      TGB_CUDA(cudaMemcpyAsync(X.p, T.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+      colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(n, X.p);
+      TGB_LAUNCHED(ctx);
+      cholqr2(ctx, n, p, X.p, tmp);
+      dgemm(ctx, true, false, p, p, n, 1.0, X.p, n, T.p, n, 0.0, Sd.p, p);  // S = X^T a Y
+      jacobi_svd_small(p, to_host(ctx, Sd.p, static_cast<size_t>(p) * p), sg, Ut);
+      to_dev(ctx, Sd.p, Ut);
+      dgemm(ctx, false, false, n, p, p, 1.0, X.p, n, Sd.p, p, 0.0, T.p, n);  // rotate X to singular directions
+      TGB_CUDA(cudaMemcpyAsync(X.p, T.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+      // converged leading count
+      int conv = 0;
+      while (conv < p && std::fabs(sg[conv] - prev[conv]) <= 1e-14 * std::max(sg[0], 1e-300)) ++conv;
+      prev = sg;
+      // how many leading pairs are needed?
+      int64_t want;
+      if (sel >= 0) {
+        r = std::min<int64_t>(sel, dmin);
+        want = std::min<int64_t>(r + 1, dmin);
+      } else {
+        std::vector<double> lead(sg.begin(), sg.begin() + conv);
+        bool more = false, cl = false;
+        r = select_rank_host(lead, total, dmin, *cfg, mode, &cl, &more);
+        want = more ? conv + 1 : std::min<int64_t>(r + 1, dmin);
+      }
+      if (want <= conv && it >= 2) {
+        done = true;
+        break;
+      }
+      if (want >= p - 2 && p < dmin && it >= 4 && conv >= p - 4) {
+        grow = true;
+        break;
+      }
+      if (p == dmin && conv == p && it >= 2) {
+        done = true;
+        break;
+      }
+      // Y <- orth(a^T X)
+      dgemm(ctx, true, false, k, p, n, 1.0, a, n, X.p, n, 0.0, Y.p, k);
+      colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(k, Y.p);
+      TGB_LAUNCHED(ctx);
+      cholqr2(ctx, k, p, Y.p, tmp);
     }
-    bool more = false;
-    bool cl = false;
-    r = select_rank_host(sg, total, d, *cfg, mode, &cl, &more);
-    if (more) return conv + 1;
-    return static_cast<int>(std::min<int64_t>(r + 1, d));
-  };
-  EigTop et;
-  top_eigen(ctx, d, G.p, 32, need, et);
-  // final selection with the converged spectrum
-  std::vector<double> sg(et.theta.size());
-  for (size_t i = 0; i < sg.size(); ++i) sg[i] = std::sqrt(std::max(0.0, et.theta[i]));
+    if (done || !grow) break;
+    p = static_cast<int>(std::min<int64_t>(dmin, 2 * p));
+  }
   if (sel >= 0) {
     r = std::min<int64_t>(sel, static_cast<int64_t>(sg.size()));
   } else {
     bool more = false;
-    r = select_rank_host(sg, total, d, *cfg, mode, clamped, &more);
+    r = select_rank_host(sg, total, dmin, *cfg, mode, clamped, &more);
   }
   if (sigma_out) *sigma_out = sg;
   Zout.resize(std::max<int64_t>(1, n * r));
-  if (r == 0) return 0;
-  if (rowgram) {
-    TGB_CUDA(cudaMemcpyAsync(Zout.p, et.U.p, static_cast<size_t>(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
+  if (r > 0)
+    TGB_CUDA(cudaMemcpyAsync(Zout.p, X.p, static_cast<size_t>(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
-  } else {
-    // u = a v / sigma, then QR polish (reduction.cpp:119-137)
-    std::vector<double> inv(r);
-    for (int64_t i = 0; i < r; ++i) inv[i] = sg[i] > 0 ? 1.0 / sg[i] : 0.0;
-    Dev s(r);
-    to_dev(ctx, s.p, inv);
-    Dev V(static_cast<size_t>(k) * r);
-    scale_cols_kernel<<<static_cast<unsigned>((k * r + 255) / 256), 256, 0, ctx->stream>>>(k, r, et.U.p, s.p, V.p);
-    TGB_LAUNCHED(ctx);
-    dgemm(ctx, false, false, n, r, k, 1.0, a, n, V.p, k, 0.0, Zout.p, n);
-    Dev tmp;
-    cholqr2(ctx, n, static_cast<int>(r), Zout.p, tmp);
-  }
   return r;
 }
 

@@ -577,3 +577,34 @@ def lattice_sum_canonical(spec: LatticeSpec, grid: Grid3, reference: KernelTenso
         out.window_ops += len(offs)
     out.canonical = CanonicalTensor3(facs, spec.charge * reference.tensor.weight)
     return out
+
+
+# --------------------------------------------------------------------------- Hartree-Fock pieces on the path
+
+
+def orbital_tensor(disc: list, coeff) -> CanonicalTensor3:
+    """hf.cpp:39-46 — phi = sum_k c_k G_k (concatenation in k order)."""
+    phi = CanonicalTensor3.zero(disc[0].extents())
+    for k, c in enumerate(np.asarray(coeff, dtype=np.float64)):
+        if c == 0.0:
+            continue
+        phi = add(phi, scale(disc[k], float(c)))
+    return phi
+
+
+def density_tensor(disc: list, c_occ, reduce_eps: float = 1e-7, ctx: Context | None = None) -> CanonicalTensor3:
+    """hf.cpp:118-129 — Theta = sum_a 2 phi_a . phi_a, then reduce_rank on the device."""
+    from .reduction import ReductionConfig, reduce_rank
+
+    if not disc:
+        raise InvalidArgument("density_tensor: empty basis")
+    c_occ = np.asarray(c_occ, dtype=np.float64)
+    if c_occ.shape[0] != len(disc):
+        raise InvalidArgument("density_tensor: coefficient shape mismatch")
+    theta = CanonicalTensor3.zero(disc[0].extents())
+    for a in range(c_occ.shape[1]):
+        phi = orbital_tensor(disc, c_occ[:, a])
+        theta = add(theta, scale(hadamard(phi, phi), 2.0))
+    if theta.rank() <= 1 or reduce_eps <= 0.0:
+        return theta
+    return reduce_rank(theta, ReductionConfig.tolerance(reduce_eps), ctx)
