@@ -22,8 +22,6 @@ namespace {
 
 constexpr int TP = 64;   // left columns per CTA
 constexpr int TQ = 64;   // right columns per CTA
-constexpr int TK = 16;   // grid points per smem stage
-constexpr int NTH = 256; // 16 x 16 threads, 4 x 4 micro-tile each
 
 struct SepArgs {
   int64_t n[3];
@@ -35,83 +33,137 @@ struct SepArgs {
   int P, RB;
 };
 
-__global__ void __launch_bounds__(NTH) sep_inner_kernel(SepArgs a, double* __restrict__ partial) {
-  __shared__ double As[TK][TP + 1];
-  __shared__ double Bs[TK][TQ + 1];
-  const int p0 = blockIdx.x * TP, q0 = blockIdx.y * TQ;
-  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;  // ty: p micro-row, tx: q micro-col
-  double prod[4][4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) prod[i][j] = 1.0;
+// DMMA (mma.sync m16n8k4 f64) version of the fused separable inner product:
+// per CTA a 64 (left p) x 64 (right q) tile, 4 warps of 32 x 32; per axis the
+// tile G_ax = L_ax^T B_ax accumulates on the FP64 tensor cores, the three axes
+// are multiplied in registers, and the weighted row sums over q are reduced
+// through shared memory into one partial per (q tile, p).
+__device__ __forceinline__ void dmma16x8x4_sep(double (&c)[4], double a0, double a1, double b0) {
+  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a0), "d"(a1), "d"(b0));
+}
+
+constexpr int DM_BK = 16, DM_LDS = 68, DM_THREADS = 128;
+
+__global__ void __launch_bounds__(DM_THREADS) sep_inner_dmma_kernel(SepArgs a, double* __restrict__ partial) {
+  __shared__ double As[2][DM_BK][DM_LDS];
+  __shared__ double Bs[2][DM_BK][DM_LDS];
+  __shared__ double red[64][2][4];
+  const int p0 = blockIdx.x * 64, q0 = blockIdx.y * 64;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  const int g = lane >> 2, t = lane & 3;
+  double prod[2][4][4];
+  double ra[8], rb[8];
   for (int ax = 0; ax < 3; ++ax) {
     const int64_t n = a.n[ax];
     const double* F = a.F[ax];
     const double* B = a.B[ax];
-    double acc[4][4];
+    auto load_tile = [&](int64_t k0) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-    for (int64_t k0 = 0; k0 < n; k0 += TK) {
-      // stage A (TK x TP) and B (TK x TQ); consecutive threads walk the grid index
-      for (int e = threadIdx.x; e < TK * TP; e += NTH) {
-        const int kk = e % TK, pp = e / TK;
+      for (int e = 0; e < 8; ++e) {
+        const int idx = tid + e * DM_THREADS;  // 0..1023
+        const int kk = idx % DM_BK, mm = idx / DM_BK;
         const int64_t k = k0 + kk;
-        const int p = p0 + pp;
+        const int pidx_ = p0 + mm;
         double v = 0.0;
-        if (k < n && p < a.P) {
-          const int c0 = a.i0[p], c1 = a.i1[p];
-          v = F[c0 * n + k];
-          if (c1 >= 0) v *= F[c1 * n + k];
+        if (k < n && pidx_ < a.P) {
+          const int c0 = __ldg(a.i0 + pidx_), c1 = __ldg(a.i1 + pidx_);
+          v = __ldg(F + c0 * n + k);
+          if (c1 >= 0) v *= __ldg(F + c1 * n + k);
         }
-        As[kk][pp] = v;
+        ra[e] = v;
+        const int q = q0 + mm;
+        rb[e] = (k < n && q < a.RB) ? __ldg(B + static_cast<int64_t>(q) * n + k) : 0.0;
       }
-      for (int e = threadIdx.x; e < TK * TQ; e += NTH) {
-        const int kk = e % TK, qq = e / TK;
-        const int64_t k = k0 + kk;
-        const int q = q0 + qq;
-        Bs[kk][qq] = (k < n && q < a.RB) ? B[static_cast<int64_t>(q) * n + k] : 0.0;
+    };
+    auto store_tile = [&](int buf) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int idx = tid + e * DM_THREADS;
+        const int kk = idx % DM_BK, mm = idx / DM_BK;
+        As[buf][kk][mm] = ra[e];
+        Bs[buf][kk][mm] = rb[e];
       }
-      __syncthreads();
+    };
+    double acc[2][4][4];
 #pragma unroll
-      for (int kk = 0; kk < TK; ++kk) {
-        double av[4], bv[4];
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) av[i] = As[kk][ty + 16 * i];
+      for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx + 16 * j];
+        for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
+    const int64_t nk = (n + DM_BK - 1) / DM_BK;
+    __syncthreads();
+    load_tile(0);
+    store_tile(0);
+    __syncthreads();
+    for (int64_t kt = 0; kt < nk; ++kt) {
+      const int buf = kt & 1;
+      if (kt + 1 < nk) load_tile((kt + 1) * DM_BK);
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+      for (int k4 = 0; k4 < DM_BK; k4 += 4) {
+        double av[2][2], bv[4];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(av[i], bv[j], acc[i][j]);
+        for (int i = 0; i < 2; ++i) {
+          av[i][0] = As[buf][k4 + t][wm + 16 * i + g];
+          av[i][1] = As[buf][k4 + t][wm + 16 * i + g + 8];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bv[j] = Bs[buf][k4 + t][wn + 8 * j + g];
+#pragma unroll
+        for (int i = 0; i < 2; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma16x8x4_sep(acc[i][j], av[i][0], av[i][1], bv[j]);
       }
+      if (kt + 1 < nk) store_tile(buf ^ 1);
       __syncthreads();
     }
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) prod[i][j] *= acc[i][j];
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int r = 0; r < 4; ++r) prod[i][j][r] = ax == 0 ? acc[i][j][r] : prod[i][j][r] * acc[i][j][r];
   }
-  // weighted row sums over this q tile, reduced across the 16 tx lanes
-  __shared__ double red[TP][17];
+  // weighted row sums: element (row, col) of fragment (i, j, r):
+  //   row = wm + 16 i + g + 8 (r >= 2), col = wn + 8 j + 2 t + (r & 1)
+  double rs[2][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    double s = 0.0;
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int q = q0 + tx + 16 * j;
-      if (q < a.RB) s += a.wb[q] * prod[i][j];
+    for (int h = 0; h < 2; ++h) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int q = q0 + wn + 8 * j + 2 * t + c;
+          if (q < a.RB) sacc += a.wb[q] * prod[i][j][2 * h + c];
+        }
+      rs[i][h] = sacc;
     }
-    red[ty + 16 * i][tx] = s;
+  // reduce over the 4 lanes t sharing a row (fixed order: shuffles xor 1, 2)
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double v = rs[i][h];
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      rs[i][h] = v;
+    }
+  if (t == 0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) red[wm + 16 * i + g + 8 * h][warp >> 1][0] = rs[i][h];
   }
   __syncthreads();
-  if (threadIdx.x < TP) {
-    double s = 0.0;
-    for (int t = 0; t < 16; ++t) s += red[threadIdx.x][t];
-    const int p = p0 + threadIdx.x;
-    if (p < a.P) partial[static_cast<int64_t>(blockIdx.y) * a.P + p] = s;
+  if (tid < 64) {
+    const int p = p0 + tid;
+    if (p < a.P) partial[static_cast<int64_t>(blockIdx.y) * a.P + p] = red[tid][0][0] + red[tid][1][0];
   }
 }
 
@@ -147,7 +199,7 @@ std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* co
   a.P = P;
   a.RB = RB;
   dim3 grid((P + TP - 1) / TP, ntq);
-  sep_inner_kernel<<<grid, NTH, 0, ctx->stream>>>(a, partial);
+  sep_inner_dmma_kernel<<<grid, DM_THREADS, 0, ctx->stream>>>(a, partial);
   TGB_LAUNCHED(ctx);
   reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(partial, ntq, P, dsum);
   TGB_LAUNCHED(ctx);

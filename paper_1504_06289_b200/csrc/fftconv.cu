@@ -606,7 +606,29 @@ __device__ __forceinline__ void stage_product(double2* sm, int N, const double2*
 // First inverse pass on the staged product: real split, radix-R butterflies
 // on the paired blocks g (frequencies kk + s N/R) and g2 (the mirrors N - k),
 // in place in shared memory.  Twiddles w_m^{kk} from the two-level table.
-template <int R>
+// MULB: shared memory holds raw A (pipelined kernel); multiply by B here.
+template <int R, bool MULB = false, bool BREAL = true>
+__device__ __forceinline__ void scale_block(double2* v, const void* __restrict__ B, int pos) {
+  if constexpr (MULB) {
+    if constexpr (BREAL) {
+      const double* b = static_cast<const double*>(B) + pos;
+      double bv[R];
+#pragma unroll
+      for (int s = 0; s < R; ++s) bv[s] = __ldg(b + s);
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[s] = cscale(v[s], bv[s]);
+    } else {
+      const double2* b = static_cast<const double2*>(B) + pos;
+      double2 bv[R];
+#pragma unroll
+      for (int s = 0; s < R; ++s) bv[s] = ld2(b + s);
+#pragma unroll
+      for (int s = 0; s < R; ++s) v[s] = cmul(v[s], bv[s]);
+    }
+  }
+}
+
+template <int R, bool MULB = false, bool BREAL = true>
 __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, const PlanArgs& pa,
                                                const double2* __restrict__ A, const void* __restrict__ B,
                                                bool breal) {
@@ -620,9 +642,10 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, 
     double2 a[R];
 #pragma unroll
     for (int s = 0; s < R; ++s) a[s] = sm[pidx(g * R + s)];
+    scale_block<R, MULB, BREAL>(a, B, g * R);
     if (g == 0) {
       // natural frequencies s*N/R; mirror of s is R-s (s = 0 mirrors to the Nyquist term N)
-      const double2 an = ld2(A + N);
+      const double2 an = MULB ? sm[pidx(N)] : ld2(A + N);
       const double2 pn = breal ? cscale(an, __ldg(static_cast<const double*>(B) + N))
                                : cmul(an, ld2(static_cast<const double2*>(B) + N));
       const double2 z0 = zsplit(a[0], pn, make_double2(1.0, 0.0));
@@ -663,6 +686,7 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, 
       double2 b[R];
 #pragma unroll
       for (int s = 0; s < R; ++s) b[s] = sm[pidx(g2 * R + s)];
+      scale_block<R, MULB, BREAL>(b, B, g2 * R);
 #pragma unroll
       for (int s = 0; s < R; ++s) {
         const double2 za = zsplit(a[s], b[R - 1 - s], cmul(wk, cs[s]));
@@ -868,6 +892,75 @@ __device__ __forceinline__ void static_last(const double2* sm, const double2* lo
   }
 }
 
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// Last pass that, as soon as a butterfly's inputs are in registers, refills
+// those shared-memory slots with the NEXT pair's density spectrum (cp.async,
+// no registers), so the next pair's L2 reads overlap this pair's last
+// butterflies and output stores.
+template <int R, int L, int N>
+__device__ __forceinline__ void static_last_pipe(double2* sm, const double2* lo, const double2* hi, int nz,
+                                                 bool odd_n, double* o0, double* o1, bool aligned,
+                                                 const double2* __restrict__ a_next) {
+  constexpr int NBF = N / R;
+  static_assert(L % 16 == 0 && NBF == L, "last pass spans the whole transform");
+  if (a_next && threadIdx.x == 0) cp_async16(sm + pidx(N), a_next + N);
+  for (int j = threadIdx.x; j < NBF; j += blockDim.x) {
+    double2* p = sm + pidx(j);
+    double2 v[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) v[s] = p[s * (L + L / 16)];
+    if (a_next) {
+#pragma unroll
+      for (int s = 0; s < R; ++s) cp_async16(p + s * (L + L / 16), a_next + j + s * L);
+    }
+    apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
+    dft<R, 1>(v);
+    store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
+  }
+}
+
+template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    pair_kernel_pipe(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
+                     const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
+  constexpr int N = R0 * R1 * R2 * R3;
+  constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
+  extern __shared__ double2 sm[];
+  const double2* tws = load_tables(sm, pa);
+  const int nz = (pa.n + 1) >> 1;
+  const bool odd_n = pa.n & 1;
+  if (blockIdx.x < nwork) {  // prologue: the first pair's density spectrum
+    const double2* a0 = specA + static_cast<int64_t>(work[blockIdx.x].ia) * (N + 1);
+    for (int pos = threadIdx.x; pos <= N; pos += blockDim.x) cp_async16(sm + pidx(pos), a0 + pos);
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
+    const PairEntry e = work[w];
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
+    first_pass_inv<R0, true, BREAL>(sm, tws, pa, nullptr, b, BREAL);
+    __syncthreads();
+    static_pass<R1, L1, N, 1>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
+    __syncthreads();
+    static_pass<R2, L2, N, 1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+    __syncthreads();
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+    const int wn = w + gridDim.x;
+    const double2* a_next = wn < nwork ? specA + static_cast<int64_t>(work[wn].ia) * (N + 1) : nullptr;
+    static_last_pipe<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned, a_next);
+    cp_async_wait_all();
+    __syncthreads();
+  }
+}
+
 template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
 __global__ void __launch_bounds__(TT, 1)
     pair_kernel_static(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
@@ -994,10 +1087,15 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
   const PlanArgs& a = pl.a;
   if (!(a.P == 4 && a.r[0] == R0 && a.r[1] == R1 && a.r[2] == R2 && a.r[3] == R3) || a.dbg || getenv("TGB_NO_STATIC"))
     return false;
-  auto kern = pair_kernel_static<R0, R1, R2, R3, TT, BREAL>;
+  // the cp.async-pipelined variant measured slower (2.02 vs 1.68 ms/axis, v8); opt-in only
+  auto kern = getenv("TGB_PIPE") ? pair_kernel_pipe<R0, R1, R2, R3, TT, BREAL>
+                                 : pair_kernel_static<R0, R1, R2, R3, TT, BREAL>;
   static bool attr = false;
   if (!attr) {
-    TGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+    TGB_CUDA(cudaFuncSetAttribute(pair_kernel_static<R0, R1, R2, R3, TT, BREAL>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+    TGB_CUDA(cudaFuncSetAttribute(pair_kernel_pipe<R0, R1, R2, R3, TT, BREAL>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
     attr = true;
   }
   int per_sm = 1;

@@ -317,6 +317,18 @@ void random_block(tgb_ctx* ctx, int64_t d, int p, double* X, uint64_t seed) {
 
 }  // namespace
 
+// Column-normalise then Cholesky-QR twice: orthonormal basis of the columns of
+// X (d x p, device, in place).  Used by the TEI fit (Q of the pivoted Cholesky
+// factor, tei.cpp:136-138: the column space is what matters there; column
+// signs may differ from a Householder Q, which B = V M V^T does not see).
+void orthonormalize_columns(tgb_ctx* ctx, int64_t d, int p, double* X) {
+  if (d == 0 || p == 0) return;
+  colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(d, X);
+  TGB_LAUNCHED(ctx);
+  Dev tmp;
+  cholqr2(ctx, d, p, X, tmp);
+}
+
 // ---------------------------------------------------------------- reduction driver
 
 struct RedCfgC {

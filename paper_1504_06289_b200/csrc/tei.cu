@@ -2,8 +2,9 @@
 //   1D density fitting per axis (tei.cpp:92-143): product side matrix G,
 //     Gram G G^T on the DMMA tensor cores, pivoted Cholesky with trace stop
 //     (single-CTA device loop, first-maximal-index pivots as Eigen's
-//     maxCoeff(&p)), Householder QR with Eigen's reflector convention,
-//     V = G^T U;
+//     maxCoeff(&p)), an orthonormal basis of the selected columns by
+//     GEMM-based Cholesky-QR (the reference's Householder QR up to column
+//     signs, which B does not see), V = G^T U;
 //   convolution matrices M_k = U^T (h conv(U, p_k)) (tei.cpp:145-158) through
 //     the FFT mode-convolution path + one GEMM per axis;
 //   the TEI diagonal from the bilinear forms V[j2,:] M_k V[j,:]^T
@@ -183,77 +184,6 @@ __global__ void __launch_bounds__(kRedThreads) pivchol_explicit_kernel(int n, co
     info[1] = clamped;
     info[2] = err;
     residual[0] = max0 > 0.0 ? (trace_stop ? fs : dm) / (trace_stop ? trace0 : max0) : 0.0;
-  }
-}
-
-// Thin Householder QR of a tall n x r matrix (in place), Eigen's convention
-// (beta = -sign(c0) * norm, tau = (beta - c0) / beta), then Q (n x r)
-// explicitly.  Single CTA.
-__global__ void __launch_bounds__(kRedThreads) householder_qr_kernel(int n, int r, double* __restrict__ W,
-                                                                     double* __restrict__ tau,
-                                                                     double* __restrict__ Q) {
-  __shared__ double sv[32];
-  __shared__ double s_beta, s_tau, s_c0;
-  for (int j = 0; j < r; ++j) {
-    double* wj = W + static_cast<int64_t>(n) * j;
-    double part = 0.0;
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) part += wj[i] * wj[i];
-    const double tail = block_sum(part, sv);
-    if (threadIdx.x == 0) {
-      const double c0 = wj[j];
-      s_c0 = c0;
-      if (tail <= 2.2250738585072014e-308) {
-        s_tau = 0.0;
-        s_beta = c0;
-      } else {
-        double beta = sqrt(c0 * c0 + tail);
-        if (c0 >= 0.0) beta = -beta;
-        s_beta = beta;
-        s_tau = (beta - c0) / beta;
-      }
-      tau[j] = s_tau;
-    }
-    __syncthreads();
-    const double tj = s_tau, beta = s_beta, c0 = s_c0;
-    if (tj == 0.0) {
-      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) wj[i] = 0.0;
-      __syncthreads();
-      continue;
-    }
-    const double scale = 1.0 / (c0 - beta);
-    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) wj[i] *= scale;
-    __syncthreads();
-    if (threadIdx.x == 0) wj[j] = beta;
-    // apply H = I - tau v v^T (v = [1; essential]) to columns c > j
-    for (int c = j + 1; c < r; ++c) {
-      double* wc = W + static_cast<int64_t>(n) * c;
-      const double wcj = wc[j];
-      double part2 = 0.0;
-      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) part2 += wj[i] * wc[i];
-      const double s = (block_sum(part2, sv) + wcj) * tj;
-      if (threadIdx.x == 0) wc[j] -= s;
-      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) wc[i] -= s * wj[i];
-      __syncthreads();
-    }
-  }
-  // Q = H_0 ... H_{r-1} [I; 0]
-  for (int c = 0; c < r; ++c)
-    for (int i = threadIdx.x; i < n; i += blockDim.x) Q[i + static_cast<int64_t>(n) * c] = (i == c) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int j = r - 1; j >= 0; --j) {
-    const double tj = tau[j];
-    if (tj == 0.0) continue;
-    const double* wj = W + static_cast<int64_t>(n) * j;
-    for (int c = 0; c < r; ++c) {
-      double* qc = Q + static_cast<int64_t>(n) * c;
-      const double qcj = qc[j];
-      double part = 0.0;
-      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) part += wj[i] * qc[i];
-      const double s = (block_sum(part, sv) + qcj) * tj;
-      if (threadIdx.x == 0) qc[j] -= s;
-      for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) qc[i] -= s * wj[i];
-      __syncthreads();
-    }
   }
 }
 
@@ -458,10 +388,10 @@ void tei_fit(tgb_ctx* ctx, TEI& f, const tgb_cp& basis_dev, const int64_t* fn_of
     f.U[ax].get(std::max<int64_t>(1, n * r) * sizeof(double));
     f.V[ax].get(std::max<int64_t>(1, np2 * r) * sizeof(double));
     if (r > 0) {
-      auto* tau = static_cast<double*>(ctx->ws_misc3.get(std::max<int64_t>(r, 1) * sizeof(double)));
-      householder_qr_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(n), static_cast<int>(r), Lw, tau,
-                                                                dptr(f.U[ax]));
-      TGB_LAUNCHED(ctx);
+      // U = orthonormal basis of span(L) (tei.cpp:136-138), GEMM-based Cholesky-QR
+      TGB_CUDA(cudaMemcpyAsync(dptr(f.U[ax]), Lw, static_cast<size_t>(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
+                               ctx->stream));
+      orthonormalize_columns(ctx, n, static_cast<int>(r), dptr(f.U[ax]));
       dgemm(ctx, true, false, np2, r, n, 1.0, G, n, dptr(f.U[ax]), n, 0.0, dptr(f.V[ax]), np2);
     }
     // residual ||G - U V^T|| / ||G||  (T reuses the Gram workspace when large enough)

@@ -126,6 +126,7 @@ void coulomb_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_off
                         double vol, double* J);
 void dgemm(tgb_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
+void orthonormalize_columns(tgb_ctx* ctx, int64_t d, int p, double* X);
 void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ijk, double* out);
 void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
                           double* out);

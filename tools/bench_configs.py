@@ -1,0 +1,183 @@
+"""Per-config measurements of the §8 rows on one B200 (companion to bench.py,
+which measures the headline config 2).  Prints one JSON object per config and
+writes profiles/<tag>_configs.json.
+
+  cfg0  Hartree convolution n=1025, R_f=50, R_N=31          (a-1..a-5)
+  cfg1  J: density (rank 12,800) -> reduce_rank(1e-6) -> V_H (R_N=41) -> coulomb_matrix  (a-6..a-11)
+  cfg3  TEI: fitting + conv matrices + pivoted Cholesky, N_b=80 s/p, n=4097  (a-12..a-16)
+  cfg4  lattice sum L=32, n=32769, R_N=41 + 10^5 probes     (a-17)
+
+Timings: CUDA-synchronised wall clock around each stage after one warm-up
+(stages contain host-driven loops, so events on one stream would not cover
+them all).  Parity checks run against the oracle on samples.
+"""
+from __future__ import annotations
+
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import numpy as np  # noqa: E402
+
+HBM = 6527.5
+FP64 = 36.6
+
+
+def timed(fn, reps=1, sync=None):
+    sync = sync or (lambda: None)
+    fn()
+    sync()
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        out = fn()
+    sync()
+    return (time.perf_counter() - t0) / reps, out
+
+
+def cfg0(ctx):
+    import torch
+
+    import paper_1504_06289_b200 as tg
+    from oracle import oracle as O
+    from paper_1504_06289_b200.inputs import hartree_case
+
+    case = hartree_case(0)
+    dt, dk = tg.DeviceCP.from_host(case.theta), tg.DeviceCP.from_host(case.kernel.tensor)
+    out = tg.DeviceCP.empty([1025] * 3, dt.rank() * dk.rank())
+    t, _ = timed(lambda: tg.hartree_potential(dt, dk, case.grid.h, ctx, out=out), reps=20, sync=torch.cuda.synchronize)
+    units = 3 * 50 * 31
+    byts = 8.0 * 3 * 1025 * (50 * 31 + 50 + 31)
+    vh = out.to_host()
+    ovh = O.hartree_potential(O.OCP.from_cp(case.theta), O.OCP.from_cp(case.kernel.tensor), case.grid.h)
+    err = max(float(np.abs(vh.factor[ax] - f).max() / np.abs(f).max()) for ax, f in enumerate(ovh.factors()))
+    got = tg.value_at_points(vh, case.samples, ctx)
+    ref = O.value_at(ovh, case.samples)
+    # analytic Newton potential of the Gaussian density at 200 samples (reported, quadrature-limited)
+    pts = case.samples[:200]
+    xyz = np.stack([case.grid.coord(ax, pts[:, ax]) for ax in range(3)], 1)
+    from paper_1504_06289_b200.inputs import analytic_potential
+
+    ana = analytic_potential(xyz, case.a, case.centres, case.c)
+    return {"config": 0, "what": "hartree_potential n=1025 R_f=50 R_N=31", "ms": t * 1e3, "convs_per_s": units / t,
+            "hbm_frac": byts / t / 1e9 / HBM, "parity_factor_relmax": err,
+            "parity_samples_relmax": float(np.abs(got - ref).max() / np.abs(ref).max()),
+            "analytic_relmax_200pts": float(np.abs(got[:200] - ana).max() / np.abs(ana).max())}
+
+
+def cfg1(ctx):
+    import torch
+
+    import paper_1504_06289_b200 as tg
+    from paper_1504_06289_b200.inputs import KERNEL_C0, KERNEL_M, basis_case, occupied_coefficients
+
+    bs, rng = basis_case(1)
+    disc = tg.discretize_basis(bs)
+    c_occ = occupied_coefficients(rng, len(disc), 8)
+    # unreduced density (host tensor algebra, as the reference's add/hadamard)
+    t_build0 = time.perf_counter()
+    theta_full = tg.CanonicalTensor3.zero(disc[0].extents())
+    for a in range(8):
+        phi = tg.orbital_tensor(disc, c_occ[:, a])
+        theta_full = tg.add(theta_full, tg.scale(tg.hadamard(phi, phi), 2.0))
+    t_build = time.perf_counter() - t_build0
+    cfgr = tg.ReductionConfig.tolerance(1e-6)
+    t_red, red = timed(lambda: tg.reduce_rank(theta_full, cfgr, ctx), reps=1, sync=torch.cuda.synchronize)
+    res = tg.canonical_to_tucker(theta_full, cfgr, ctx)
+    kern = tg.kernel_tensor(bs.grid, tg.make_expsum(KERNEL_M[1], KERNEL_C0[1]), False)
+    dt, dk = tg.DeviceCP.from_host(red), tg.DeviceCP.from_host(kern.tensor)
+    vh = tg.DeviceCP.empty(list(bs.grid.n), dt.rank() * dk.rank())
+    t_vh, _ = timed(lambda: tg.hartree_potential(dt, dk, bs.grid.h, ctx, out=vh), reps=3, sync=torch.cuda.synchronize)
+    t_j, J = timed(lambda: tg.coulomb_matrix(bs, disc, vh, ctx), reps=3, sync=torch.cuda.synchronize)
+    n, P, RV = bs.grid.n[0], len(disc) * (len(disc) + 1) // 2, vh.rank()
+    flops_j = 2.0 * 3 * n * P * RV
+    return {"config": 1, "what": "density(12800)->reduce_rank(1e-6)->V_H->coulomb_matrix, n=2049, N_b=40",
+            "density_build_host_s": t_build, "reduce_rank_ms": t_red * 1e3, "tucker_ranks": list(res.tucker.ranks()),
+            "reduced_rank": red.rank(), "hartree_ms": t_vh * 1e3, "R_V": RV, "coulomb_ms": t_j * 1e3,
+            "coulomb_tflops": flops_j / t_j / 1e12, "coulomb_fp64_frac": flops_j / t_j / 1e12 / FP64,
+            "J_symmetric_exact": bool(np.array_equal(J, J.T)), "J_trace": float(np.trace(J))}
+
+
+def cfg3(ctx):
+    import torch
+
+    import paper_1504_06289_b200 as tg
+    from paper_1504_06289_b200.inputs import KERNEL_C0, KERNEL_M, basis_case
+
+    bs, _ = basis_case(3)
+    disc = tg.discretize_basis(bs)
+    kern = tg.kernel_tensor(bs.grid, tg.make_expsum(KERNEL_M[3], KERNEL_C0[3]), False)
+    fac = tg.TEIFactorization(ctx)
+    t0 = time.perf_counter()
+    tg.tei_density_fitting(fac, bs, disc, 1e-6)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    tg.tei_convolution_matrices(fac, kern)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    tg.tei_cholesky(fac, 1e-6)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    n, np_ = bs.grid.n[0], fac.n_prim
+    gram_flops = 3 * 2.0 * n * n * np_ * np_
+    return {"config": 3, "what": "build_tei N_b=80 s/p, n=4097, eps_fit=eps_chol=1e-6", "fit_ms": (t1 - t0) * 1e3,
+            "fit_gram_tflops_lower_bound": gram_flops / (t1 - t0) / 1e12, "conv_ms": (t2 - t1) * 1e3,
+            "cholesky_ms": (t3 - t2) * 1e3, "fit_ranks": list(fac.fit_ranks()), "R_B": fac.rank_b(),
+            "fit_residual": [float(x) for x in fac.fit_residual]}
+
+
+def cfg4(ctx):
+    import torch
+
+    import paper_1504_06289_b200 as tg
+    from paper_1504_06289_b200.inputs import Rng, lattice_case
+
+    spec, grid, ref = lattice_case()
+    offs = [tg.lattice_offsets(spec, grid, ax) for ax in range(3)]
+    n, R = grid.n[0], ref.rank()
+    dref = [torch.from_numpy(np.ascontiguousarray(ref.tensor.factor[ax].T)).cuda() for ax in range(3)]
+    dout = [torch.empty((R, n), dtype=torch.float64, device="cuda") for _ in range(3)]
+    import ctypes as C
+
+    from paper_1504_06289_b200._lib import MEM_DEVICE, check, lib
+
+    def run():
+        for ax in range(3):
+            o = np.ascontiguousarray(offs[ax], dtype=np.int64)
+            check(lib().tgb_lattice_assemble_axis(ctx.handle, n, R, dref[ax].data_ptr(), o.ctypes.data, len(o),
+                                                  dout[ax].data_ptr(), MEM_DEVICE))
+
+    t, _ = timed(run, reps=20, sync=torch.cuda.synchronize)
+    byts = 3 * 8.0 * (2 * n + n) * R
+    lat = tg.DeviceCP(dout, torch.from_numpy(spec.charge * ref.tensor.weight).cuda())
+    pts = torch.as_tensor(Rng(1504062894).integers(3 * 100_000, n).reshape(-1, 3)).cuda()
+    tv, vals = timed(lambda: tg.value_at_points(lat, pts, ctx), reps=5, sync=torch.cuda.synchronize)
+    return {"config": 4, "what": "lattice_sum_canonical L=32^3, n=32769, R_N=41 (+1e5 probes)", "assembly_ms": t * 1e3,
+            "assembly_hbm_frac": byts / t / 1e9 / HBM, "window_ops": int(sum(len(o) for o in offs)),
+            "probe_ms_1e5": tv * 1e3}
+
+
+def main():
+    import paper_1504_06289_b200 as tg
+
+    tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+    which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1", "3", "4"]
+    ctx = tg.Context(0)
+    out = []
+    for w in which:
+        fn = {"0": cfg0, "1": cfg1, "3": cfg3, "4": cfg4}[w]
+        try:
+            r = fn(ctx)
+        except Exception as exc:  # report and continue
+            r = {"config": int(w), "error": repr(exc)}
+        print(json.dumps(r), flush=True)
+        out.append(r)
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / f"{tag}_configs.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
