@@ -66,8 +66,9 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
   TGB_CUDA(cudaSetDevice(ctx->device));
   if (mem == TGB_MEM_DEVICE) {
     tgb::weights_outer(ctx, ra, a->weight, rb, b->weight, bscale, out->weight);
-    for (int ax = 0; ax < 3; ++ax)
-      tgb::convolve_axis(ctx, a->n[ax], ra, a->factor[ax], rb, b->factor[ax], h[ax], out->factor[ax]);
+    const double* fa[3] = {a->factor[0], a->factor[1], a->factor[2]};
+    const double* fb[3] = {b->factor[0], b->factor[1], b->factor[2]};
+    tgb::convolve_axes(ctx, 3, a->n, ra, fa, rb, fb, h, out->factor);
     return;
   }
   tgb::require(mem == TGB_MEM_HOST, "convolve: bad memory space");
@@ -183,6 +184,8 @@ int tgb_ctx_destroy(tgb_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
     for (auto e : ctx->events) cudaEventDestroy(e);
+    if (ctx->pinned_event) cudaEventDestroy(ctx->pinned_event);
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto& pe : ctx->prof_events) {
       cudaEventDestroy(pe.first);
       cudaEventDestroy(pe.second);

@@ -718,13 +718,20 @@ __device__ __forceinline__ double2* load_tables(double2* sm, const PlanArgs& pa)
 // R[k] = (h/m) c(k) Re(X[k] e^{2 pi i k (n-1)/(2m)}), c = 1 (odd n) or
 // cos(pi k/m) (even n);  mode 2: complex X * (h/m) e^{2 pi i k ofs/m} *
 // (1 or (1 + e^{2 pi i k/m})/2)  (general kernel columns).
+// One launch covers the density columns (CTAs [0, nA): mode 0 into specA)
+// and the distinct kernel columns (CTAs [nA, ...): colidx, modeB into specB),
+// so the few, latency-bound kernel transforms overlap the density ones.
 __global__ void __launch_bounds__(kMaxThreads, 1)
-    spectrum_kernel(PlanArgs pa, const double* __restrict__ X, int64_t ldx, const int* __restrict__ colidx,
-                    void* __restrict__ spec, int mode, double h) {
+    spectrum_kernel(PlanArgs pa, const double* __restrict__ XA, int nA, void* __restrict__ specA,
+                    const double* __restrict__ XB, const int* __restrict__ colidx, void* __restrict__ specB,
+                    int modeB, int64_t ldx, double h) {
   extern __shared__ double2 sm[];
   const double2* tws = load_tables(sm, pa);
-  const int c = blockIdx.x;
-  const double* x = X + (colidx ? colidx[c] : c) * ldx;
+  const bool isA = static_cast<int>(blockIdx.x) < nA;
+  const int c = isA ? blockIdx.x : blockIdx.x - nA;
+  const int mode = isA ? 0 : modeB;
+  void* spec = isA ? specA : specB;
+  const double* x = isA ? XA + c * ldx : XB + colidx[c] * ldx;
   const int n = pa.n, N = pa.N;
   for (int k = threadIdx.x; k < N; k += blockDim.x) {  // natural order: coalesced reads
     const int i0 = 2 * k;
@@ -750,8 +757,8 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     __syncthreads();
   }
   const double hm = h / pa.m;
-  for (int pos = threadIdx.x; pos <= N; pos += blockDim.x) {  // stored order: coalesced writes
-    const int k = pos < N ? __ldg(pa.perm + pos) : N;
+  for (int k = threadIdx.x; k <= N; k += blockDim.x) {  // natural order: coalesced table reads
+    const int pos = k < N ? __ldg(pa.inv + k) : N;        // (scattered 16-byte stores)
     const double2 zk = sm[pidx(k == N ? 0 : k)];
     double2 zm = sm[pidx(k == 0 ? 0 : N - k)];
     zm.y = -zm.y;
@@ -1126,16 +1133,16 @@ static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA
   }
 }
 
-static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* X, int64_t ldx, const int* colidx,
-                            int cols, void* spec, int mode, double h) {
-  if (!cols) return;
+static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, int nA, void* specA, const double* B,
+                            const int* colidx, int nB, void* specB, int modeB, int64_t ldx, double h) {
+  if (nA + nB == 0) return;
   static bool attr_set = false;
   if (!attr_set) {
     TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin)));
     attr_set = true;
   }
-  spectrum_kernel<<<cols, pl.threads, pl.smem, ctx->stream>>>(pl.a, X, ldx, colidx, spec, mode, h);
+  spectrum_kernel<<<nA + nB, pl.threads, pl.smem, ctx->stream>>>(pl.a, A, nA, specA, B, colidx, specB, modeB, ldx, h);
   TGB_LAUNCHED(ctx);
 }
 
@@ -1144,78 +1151,132 @@ struct ColumnGroups {
   bool all_symmetric = true;
 };
 
-static ColumnGroups group_columns(tgb_ctx* ctx, int64_t n, int64_t rb, const double* B) {
-  ColumnGroups cg;
-  if (rb == 0) return cg;
+// Bitwise-identical / mirror-symmetric kernel columns of every axis, with ONE
+// device->host synchronisation for all axes.
+static std::vector<ColumnGroups> group_columns(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t rb,
+                                               const double* const* B) {
+  std::vector<ColumnGroups> out(naxes);
+  if (rb == 0) return out;
   const int64_t nblocks = rb + rb * (rb - 1) / 2;
-  auto* flags = static_cast<unsigned char*>(ctx->ws_flags.get(rb * rb));
-  dup_columns_kernel<<<static_cast<unsigned>(nblocks), 256, 0, ctx->stream>>>(B, n, static_cast<int>(rb), flags);
-  TGB_LAUNCHED(ctx);
-  std::vector<unsigned char> h(rb * rb, 0);
-  TGB_CUDA(cudaMemcpyAsync(h.data(), flags, rb * rb, cudaMemcpyDeviceToHost, ctx->stream));
-  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-  std::vector<int> rep(rb, -1);
-  for (int j = 0; j < rb; ++j) {
-    if (rep[j] >= 0) continue;
-    rep[j] = static_cast<int>(cg.groups.size());
-    cg.groups.push_back({j});
-    cg.all_symmetric = cg.all_symmetric && h[j * rb + j];
-    for (int j2 = j + 1; j2 < rb; ++j2)
-      if (rep[j2] < 0 && h[j * rb + j2]) {
-        rep[j2] = rep[j];
-        cg.groups.back().push_back(j2);
-      }
+  auto* flags = static_cast<unsigned char*>(ctx->ws_flags.get(naxes * rb * rb));
+  for (int ax = 0; ax < naxes; ++ax) {
+    dup_columns_kernel<<<static_cast<unsigned>(nblocks), 256, 0, ctx->stream>>>(B[ax], n[ax], static_cast<int>(rb),
+                                                                               flags + ax * rb * rb);
+    TGB_LAUNCHED(ctx);
   }
-  return cg;
+  std::vector<unsigned char> h(naxes * rb * rb, 0);
+  TGB_CUDA(cudaMemcpyAsync(h.data(), flags, h.size(), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int ax = 0; ax < naxes; ++ax) {
+    ColumnGroups& cg = out[ax];
+    const unsigned char* f = h.data() + ax * rb * rb;
+    std::vector<int> rep(rb, -1);
+    for (int j = 0; j < rb; ++j) {
+      if (rep[j] >= 0) continue;
+      rep[j] = static_cast<int>(cg.groups.size());
+      cg.groups.push_back({j});
+      cg.all_symmetric = cg.all_symmetric && f[j * rb + j];
+      for (int j2 = j + 1; j2 < rb; ++j2)
+        if (rep[j2] < 0 && f[j * rb + j2]) {
+          rep[j2] = rep[j];
+          cg.groups.back().push_back(j2);
+        }
+    }
+  }
+  return out;
 }
 
-// out (n x ra*rb, column i + ra*j) = h * window(conv(A_i, B_j)); device pointers.
+// Pinned host staging for the per-call work lists, so their uploads are truly
+// asynchronous (a pageable cudaMemcpyAsync would synchronise the stream).
+static void* pinned_staging(tgb_ctx* ctx, size_t bytes) {
+  if (ctx->pinned_event) TGB_CUDA(cudaEventSynchronize(ctx->pinned_event));  // previous uploads done
+  if (bytes > ctx->pinned_bytes) {
+    if (ctx->pinned) cudaFreeHost(ctx->pinned);
+    ctx->pinned = nullptr;
+    TGB_CUDA(cudaHostAlloc(&ctx->pinned, bytes, cudaHostAllocDefault));
+    ctx->pinned_bytes = bytes;
+  }
+  return ctx->pinned;
+}
+
+// out[ax] (n x ra*rb, column i + ra*j) = h[ax] * window(conv(A_i, B_j)) for
+// naxes axes; device pointers, stream-ordered, one host sync in total.
+void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const double* const* A, int64_t rb,
+                   const double* const* B, const double* h, double* const* out) {
+  if (ra == 0 || rb == 0 || naxes == 0) return;
+  const std::vector<ColumnGroups> cgs = group_columns(ctx, naxes, n, rb, B);
+  // work lists (i-major: concurrently running CTAs share A_i and every B_j in L2)
+  std::vector<std::vector<PairEntry>> works(naxes);
+  std::vector<std::vector<int>> reps(naxes);
+  size_t total_entries = 0, total_reps = 0;
+  std::vector<std::shared_ptr<ConvPlan>> plans(naxes);
+  for (int ax = 0; ax < naxes; ++ax) {
+    plans[ax] = get_plan(ctx, n[ax]);
+    const auto& groups = cgs[ax].groups;
+    auto& work = works[ax];
+    work.reserve(static_cast<size_t>(ra * groups.size()));
+    for (int64_t i = 0; i < ra; ++i)
+      for (size_t g = 0; g < groups.size(); ++g) {
+        const auto& mem = groups[g];
+        for (size_t q = 0; q < mem.size(); q += 2) {
+          PairEntry e;
+          e.ia = static_cast<int>(i);
+          e.jb = plans[ax]->direct ? mem[0] : static_cast<int>(g);
+          e.out0 = (i + ra * mem[q]) * n[ax];
+          e.out1 = q + 1 < mem.size() ? (i + ra * mem[q + 1]) * n[ax] : -1;
+          work.push_back(e);
+        }
+      }
+    for (auto& g : groups) reps[ax].push_back(g[0]);
+    total_entries += work.size();
+    total_reps += reps[ax].size();
+  }
+  const size_t wbytes = total_entries * sizeof(PairEntry), rbytes = total_reps * sizeof(int);
+  auto* host = static_cast<char*>(pinned_staging(ctx, wbytes + rbytes + 64));
+  auto* dbuf = static_cast<char*>(ctx->ws_pairs.get(wbytes + rbytes + 64));
+  std::vector<PairEntry*> dwork(naxes);
+  std::vector<int*> dreps(naxes);
+  size_t off = 0;
+  for (int ax = 0; ax < naxes; ++ax) {
+    std::memcpy(host + off, works[ax].data(), works[ax].size() * sizeof(PairEntry));
+    dwork[ax] = reinterpret_cast<PairEntry*>(dbuf + off);
+    off += works[ax].size() * sizeof(PairEntry);
+  }
+  for (int ax = 0; ax < naxes; ++ax) {
+    std::memcpy(host + off, reps[ax].data(), reps[ax].size() * sizeof(int));
+    dreps[ax] = reinterpret_cast<int*>(dbuf + off);
+    off += reps[ax].size() * sizeof(int);
+  }
+  TGB_CUDA(cudaMemcpyAsync(dbuf, host, off, cudaMemcpyHostToDevice, ctx->stream));
+  if (!ctx->pinned_event) TGB_CUDA(cudaEventCreateWithFlags(&ctx->pinned_event, cudaEventDisableTiming));
+  TGB_CUDA(cudaEventRecord(ctx->pinned_event, ctx->stream));
+  for (int ax = 0; ax < naxes; ++ax) {
+    const ConvPlan& pl = *plans[ax];
+    const int nw = static_cast<int>(works[ax].size());
+    if (pl.direct) {
+      const int th = static_cast<int>(std::min<int64_t>(256, ((n[ax] + 31) / 32) * 32));
+      direct_conv_kernel<<<static_cast<unsigned>(nw), th, 0, ctx->stream>>>(
+          static_cast<int>(n[ax]), pl.a.ofs, pl.a.even, A[ax], n[ax], B[ax], n[ax], dwork[ax], h[ax], out[ax]);
+      TGB_LAUNCHED(ctx);
+      continue;
+    }
+    const int N = pl.a.N;
+    const bool breal = cgs[ax].all_symmetric;
+    const size_t nd = reps[ax].size();
+    auto* specA = static_cast<double2*>(ctx->ws_spec_a.get(static_cast<size_t>(ra) * (N + 1) * sizeof(double2)));
+    void* specB = ctx->ws_spec_b.get(nd * (N + 1) * (breal ? sizeof(double) : sizeof(double2)));
+    launch_spectrum(ctx, pl, A[ax], static_cast<int>(ra), specA, B[ax], dreps[ax], static_cast<int>(nd), specB,
+                    breal ? 1 : 2, n[ax], h[ax]);
+    if (breal)
+      launch_pair_r<true>(ctx, pl, specA, specB, dwork[ax], nw, out[ax]);
+    else
+      launch_pair_r<false>(ctx, pl, specA, specB, dwork[ax], nw, out[ax]);
+  }
+}
+
 void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t rb, const double* B, double h,
                    double* out) {
-  if (ra == 0 || rb == 0) return;
-  auto pl = get_plan(ctx, n);
-  const ColumnGroups cg = group_columns(ctx, n, rb, B);
-  const auto& groups = cg.groups;
-  // work list: i-major so CTAs running concurrently share A_i and all B_j in L2
-  std::vector<PairEntry> work;
-  work.reserve(static_cast<size_t>(ra * groups.size()));
-  for (int64_t i = 0; i < ra; ++i)
-    for (size_t g = 0; g < groups.size(); ++g) {
-      const auto& mem = groups[g];
-      for (size_t q = 0; q < mem.size(); q += 2) {
-        PairEntry e;
-        e.ia = static_cast<int>(i);
-        e.jb = pl->direct ? mem[0] : static_cast<int>(g);
-        e.out0 = (i + ra * mem[q]) * n;
-        e.out1 = q + 1 < mem.size() ? (i + ra * mem[q + 1]) * n : -1;
-        work.push_back(e);
-      }
-    }
-  auto* dwork = static_cast<PairEntry*>(ctx->ws_pairs.get(work.size() * sizeof(PairEntry)));
-  TGB_CUDA(cudaMemcpyAsync(dwork, work.data(), work.size() * sizeof(PairEntry), cudaMemcpyHostToDevice, ctx->stream));
-  if (pl->direct) {
-    const int th = static_cast<int>(std::min<int64_t>(256, ((n + 31) / 32) * 32));
-    direct_conv_kernel<<<static_cast<unsigned>(work.size()), th, 0, ctx->stream>>>(
-        static_cast<int>(n), pl->a.ofs, pl->a.even, A, n, B, n, dwork, h, out);
-    TGB_LAUNCHED(ctx);
-    return;
-  }
-  const int N = pl->a.N;
-  const bool breal = cg.all_symmetric;
-  auto* specA = static_cast<double2*>(ctx->ws_spec_a.get(static_cast<size_t>(ra) * (N + 1) * sizeof(double2)));
-  void* specB =
-      ctx->ws_spec_b.get(static_cast<size_t>(groups.size()) * (N + 1) * (breal ? sizeof(double) : sizeof(double2)));
-  std::vector<int> reps;
-  for (auto& g : groups) reps.push_back(g[0]);
-  auto* dreps = static_cast<int*>(ctx->ws_misc.get(reps.size() * sizeof(int)));
-  TGB_CUDA(cudaMemcpyAsync(dreps, reps.data(), reps.size() * sizeof(int), cudaMemcpyHostToDevice, ctx->stream));
-  launch_spectrum(ctx, *pl, A, n, nullptr, static_cast<int>(ra), specA, 0, 1.0);
-  launch_spectrum(ctx, *pl, B, n, dreps, static_cast<int>(reps.size()), specB, breal ? 1 : 2, h);
-  if (breal)
-    launch_pair_r<true>(ctx, *pl, specA, specB, dwork, static_cast<int>(work.size()), out);
-  else
-    launch_pair_r<false>(ctx, *pl, specA, specB, dwork, static_cast<int>(work.size()), out);
-  // (pageable-source cudaMemcpyAsync stages the host vectors before returning)
+  convolve_axes(ctx, 1, &n, ra, &A, rb, &B, &h, &out);
 }
 
 void conv_central_many_dev(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out) {

@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -156,6 +158,53 @@ __global__ void sumsq_kernel(int64_t total, const double* __restrict__ a, double
   }
 }
 
+// H (p x p Gram of column-normalised X, global) -> R^{-1} with H = R^T R
+// (R upper), single CTA.  A column whose component orthogonal to the previous
+// ones is below 1e-13 of its norm is numerically dependent (the unfolding has
+// lower rank than the block): it is retired — its column of R^{-1} is zero, so
+// it comes out as an exact zero column that adds no spurious singular value.
+constexpr int kMaxBlock = 1024;
+__global__ void chol_inv_kernel(int p, double* __restrict__ H, double* __restrict__ Wk) {
+  __shared__ double s_mx;
+  __shared__ unsigned char dead[kMaxBlock];
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int i = 0; i < p; ++i) mx = fmax(mx, H[i + static_cast<int64_t>(p) * i]);
+    s_mx = mx;
+  }
+  for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) Wk[idx] = H[idx];
+  __syncthreads();
+  const double tiny = 1e-26 * s_mx;
+  for (int j = 0; j < p; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = Wk[j + p * j];
+      dead[j] = !(d > tiny);
+      Wk[j + p * j] = dead[j] ? 1.0 : sqrt(d);
+    }
+    __syncthreads();
+    const bool dj = dead[j];
+    const double djj = Wk[j + p * j];
+    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) Wk[i + p * j] = dj ? 0.0 : Wk[i + p * j] / djj;
+    __syncthreads();
+    if (!dj) {
+      const int m = p - j - 1;
+      for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+        const int i = j + 1 + e % m, k = j + 1 + e / m;
+        if (i >= k) Wk[i + p * k] -= Wk[i + p * j] * Wk[k + p * j];
+      }
+    }
+    __syncthreads();
+  }
+  // R = L^T upper; R^{-1} column c by back substitution (one thread per column)
+  for (int c = threadIdx.x; c < p; c += blockDim.x) {
+    for (int i = p - 1; i >= 0; --i) {
+      double sum = (i == c) ? 1.0 : 0.0;
+      for (int k = i + 1; k <= c; ++k) sum -= Wk[k + p * i] * H[k + p * c];
+      H[i + p * c] = (i > c || dead[c]) ? 0.0 : sum / Wk[i + p * i];
+    }
+  }
+}
+
 __global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) x[i] = v;
@@ -278,22 +327,19 @@ void to_dev(tgb_ctx* ctx, double* d, const std::vector<double>& h) {
 // Orthonormalise the columns of X (d x p) in place: Cholesky-QR, twice.
 // Columns that are numerically dependent are replaced deterministically.
 void cholqr2(tgb_ctx* ctx, int64_t d, int p, double* X, Dev& tmp) {
-  tmp.resize(static_cast<size_t>(d) * p + static_cast<size_t>(p) * p);
+  tmp.resize(static_cast<size_t>(d) * p + 2 * static_cast<size_t>(p) * p);
   double* H = tmp.p + static_cast<size_t>(d) * p;
+  double* Wk = H + static_cast<size_t>(p) * p;
   for (int rep = 0; rep < 2; ++rep) {
-    dgemm(ctx, true, false, p, p, d, 1.0, X, d, X, d, 0.0, H, p);
-    std::vector<double> hH = to_host(ctx, H, static_cast<size_t>(p) * p);
-    if (!host_cholesky(p, hH)) {
-      // regularise: add a tiny shift proportional to the largest diagonal
-      std::vector<double> h2 = to_host(ctx, H, static_cast<size_t>(p) * p);
-      double mx = 0;
-      for (int i = 0; i < p; ++i) mx = std::max(mx, h2[i + static_cast<size_t>(p) * i]);
-      for (int i = 0; i < p; ++i) h2[i + static_cast<size_t>(p) * i] += 1e-14 * mx + 1e-300;
-      hH = h2;
-      if (!host_cholesky(p, hH)) throw Error(TGB_NUMERICAL_ERROR, "reduction: orthonormalisation failed");
+    if (rep) {
+      colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(d, X);
+      TGB_LAUNCHED(ctx);
     }
-    std::vector<double> Ri = upper_inverse_from_lower(p, hH);
-    to_dev(ctx, H, Ri);
+    dgemm(ctx, true, false, p, p, d, 1.0, X, d, X, d, 0.0, H, p);
+    // H is written in place with R^{-1}; back substitution reads H's upper part as it goes,
+    // so each column c only reads entries (k, c) with k > i that it already produced.
+    chol_inv_kernel<<<1, 256, 0, ctx->stream>>>(p, H, Wk);
+    TGB_LAUNCHED(ctx);
     TGB_CUDA(cudaMemcpyAsync(tmp.p, X, static_cast<size_t>(d) * p * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
     dgemm(ctx, false, false, d, p, p, 1.0, tmp.p, d, H, p, 0.0, X, d);
@@ -394,7 +440,8 @@ static int64_t select_rank_host(const std::vector<double>& sg, double total, int
 // the singular directions every iteration.  Columns are normalised before
 // the Cholesky-QR so the blocks stay well conditioned.
 static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a, const RedCfgC* cfg, int mode,
-                             int64_t sel, bool* clamped, Dev& Zout, std::vector<double>* sigma_out) {
+                             int64_t sel, bool* clamped, Dev& Zout, std::vector<double>* sigma_out,
+                             const double* warm = nullptr, int64_t warm_cols = 0) {
   if (n == 0 || k == 0) {
     if (sigma_out) sigma_out->clear();
     return 0;
@@ -406,60 +453,82 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
   TGB_LAUNCHED(ctx);
   double total = 0.0;
   for (double x : to_host(ctx, part.p, 256)) total += x;
-  int p = static_cast<int>(std::min<int64_t>(dmin, sel >= 0 ? std::max<int64_t>(sel + 8, 16) : 24));
+  int p = static_cast<int>(std::min<int64_t>(std::min<int64_t>(dmin, kMaxBlock), sel >= 0 ? std::max<int64_t>(sel + 8, 16) : 48));
   Dev X, Y, T, tmp, Sd;
   std::vector<double> sg, Ut;
   int64_t r = 0;
+  int pcur = 0;  // columns of X already holding a (partially converged) subspace
+  bool have_x = false;
+  if (warm && warm_cols > 0) {
+    pcur = static_cast<int>(std::min<int64_t>(warm_cols, p));
+    X.resize(static_cast<size_t>(n) * p);
+    TGB_CUDA(cudaMemcpyAsync(X.p, warm, static_cast<size_t>(n) * pcur * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    have_x = true;
+  }
+  int iters = 0;
   while (true) {
     X.resize(static_cast<size_t>(n) * p);
     Y.resize(static_cast<size_t>(k) * p);
     T.resize(static_cast<size_t>(std::max(n, k)) * p);
     Sd.resize(static_cast<size_t>(p) * p);
-    random_block(ctx, k, p, Y.p, 0x1504062890ULL + static_cast<uint64_t>(p));
+    if (have_x) {
+      // keep the current subspace, fill the new columns at random, Y = orth(a^T X)
+      if (pcur < p) random_block(ctx, n, p - pcur, X.p + static_cast<size_t>(n) * pcur, 0x5EEDULL + pcur);
+      colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(n, X.p);
+      TGB_LAUNCHED(ctx);
+      cholqr2(ctx, n, p, X.p, tmp);
+      dgemm(ctx, true, false, k, p, n, 1.0, a, n, X.p, n, 0.0, Y.p, k);
+    } else {
+      random_block(ctx, k, p, Y.p, 0x1504062890ULL + static_cast<uint64_t>(p));
+    }
     colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(k, Y.p);
     TGB_LAUNCHED(ctx);
     cholqr2(ctx, k, p, Y.p, tmp);
     std::vector<double> prev(p, -1.0);
     bool done = false, grow = false;
-    for (int it = 0; it < 200 && !done; ++it) {
+    for (int it = 0; it < 400 && !done; ++it, ++iters) {
       dgemm(ctx, false, false, n, p, k, 1.0, a, n, Y.p, k, 0.0, T.p, n);  // T = a Y
       TGB_CUDA(cudaMemcpyAsync(X.p, T.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
                                ctx->stream));
       colnormalize_kernel<<<p, 256, 0, ctx->stream>>>(n, X.p);
       TGB_LAUNCHED(ctx);
       cholqr2(ctx, n, p, X.p, tmp);
-      dgemm(ctx, true, false, p, p, n, 1.0, X.p, n, T.p, n, 0.0, Sd.p, p);  // S = X^T a Y
-      jacobi_svd_small(p, to_host(ctx, Sd.p, static_cast<size_t>(p) * p), sg, Ut);
-      to_dev(ctx, Sd.p, Ut);
-      dgemm(ctx, false, false, n, p, p, 1.0, X.p, n, Sd.p, p, 0.0, T.p, n);  // rotate X to singular directions
-      TGB_CUDA(cudaMemcpyAsync(X.p, T.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
-                               ctx->stream));
-      // converged leading count
-      int conv = 0;
-      while (conv < p && std::fabs(sg[conv] - prev[conv]) <= 1e-14 * std::max(sg[0], 1e-300)) ++conv;
-      prev = sg;
-      // how many leading pairs are needed?
-      int64_t want;
-      if (sel >= 0) {
-        r = std::min<int64_t>(sel, dmin);
-        want = std::min<int64_t>(r + 1, dmin);
-      } else {
-        std::vector<double> lead(sg.begin(), sg.begin() + conv);
-        bool more = false, cl = false;
-        r = select_rank_host(lead, total, dmin, *cfg, mode, &cl, &more);
-        want = more ? conv + 1 : std::min<int64_t>(r + 1, dmin);
-      }
-      if (want <= conv && it >= 2) {
-        done = true;
-        break;
-      }
-      if (want >= p - 2 && p < dmin && it >= 4 && conv >= p - 4) {
-        grow = true;
-        break;
-      }
-      if (p == dmin && conv == p && it >= 2) {
-        done = true;
-        break;
+      have_x = true;
+      pcur = p;
+      if (it % 2 == 1 || it >= 40) {
+        // Rayleigh-Ritz: S = X^T a Y, rotate X to the singular directions
+        dgemm(ctx, true, false, p, p, n, 1.0, X.p, n, T.p, n, 0.0, Sd.p, p);
+        jacobi_svd_small(p, to_host(ctx, Sd.p, static_cast<size_t>(p) * p), sg, Ut);
+        to_dev(ctx, Sd.p, Ut);
+        dgemm(ctx, false, false, n, p, p, 1.0, X.p, n, Sd.p, p, 0.0, T.p, n);
+        TGB_CUDA(cudaMemcpyAsync(X.p, T.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
+                                 ctx->stream));
+        int conv = 0;
+        while (conv < p && std::fabs(sg[conv] - prev[conv]) <= 1e-14 * std::max(sg[0], 1e-300)) ++conv;
+        prev = sg;
+        // rank estimate from the whole (possibly unconverged) block
+        int64_t r_est;
+        if (sel >= 0) {
+          r_est = std::min<int64_t>(sel, dmin);
+        } else {
+          bool more = false, cl = false;
+          r_est = select_rank_host(sg, total, dmin, *cfg, mode, &cl, &more);
+          if (more) r_est = p;  // tail rule not met inside this block
+        }
+        if (getenv("TGB_RED_DEBUG") && getenv("TGB_RED_DEBUG")[0] == '2')
+          fprintf(stderr, "[tgb]   it=%d p=%d conv=%d r_est=%lld s0=%.3e s_last=%.3e\n", it, p, conv,
+                  static_cast<long long>(r_est), sg[0], sg[p - 1]);
+        if (r_est + 4 > p && p < dmin) {
+          grow = true;
+          break;
+        }
+        const int64_t need = std::min<int64_t>(r_est + 1, dmin);
+        if (conv >= need || (p == dmin && conv == p)) {
+          r = r_est;
+          done = true;
+          break;
+        }
       }
       // Y <- orth(a^T X)
       dgemm(ctx, true, false, k, p, n, 1.0, a, n, X.p, n, 0.0, Y.p, k);
@@ -468,8 +537,20 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
       cholqr2(ctx, k, p, Y.p, tmp);
     }
     if (done || !grow) break;
-    p = static_cast<int>(std::min<int64_t>(dmin, 2 * p));
+    // grow the block: keep X, double p
+    const int pn = static_cast<int>(std::min<int64_t>(std::min<int64_t>(dmin, 2 * p), kMaxBlock));
+    Dev X2(static_cast<size_t>(n) * pn);
+    TGB_CUDA(cudaMemcpyAsync(X2.p, X.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    X.resize(static_cast<size_t>(n) * pn);
+    TGB_CUDA(cudaMemcpyAsync(X.p, X2.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    pcur = p;
+    p = pn;
   }
+  if (getenv("TGB_RED_DEBUG"))
+    fprintf(stderr, "[tgb] left_subspace n=%lld k=%lld p=%d iters=%d\n", static_cast<long long>(n),
+            static_cast<long long>(k), p, iters);
   if (sel >= 0) {
     r = std::min<int64_t>(sel, static_cast<int64_t>(sg.size()));
   } else {
@@ -564,7 +645,8 @@ void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, Red
       Dev mat(static_cast<size_t>(n) * rm * rp);
       dgemm(ctx, false, false, n, rm * rp, R, 1.0, st.f[ax], n, Cm.p, R, 0.0, mat.p, n);
       Dev Znew;
-      const int64_t r = left_subspace(ctx, n, rm * rp, mat.p, nullptr, ax, st.r[ax], nullptr, Znew, nullptr);
+      const int64_t r = left_subspace(ctx, n, rm * rp, mat.p, nullptr, ax, st.r[ax], nullptr, Znew, nullptr,
+                                      st.Z[ax].p, st.r[ax]);
       if (r == 0) {
         st.fallback = true;
         return;

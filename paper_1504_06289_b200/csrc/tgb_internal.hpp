@@ -95,6 +95,9 @@ struct tgb_ctx {
   tgb::DevBuf ws_spec_a, ws_spec_b, ws_pairs, ws_flags, ws_in, ws_out, ws_misc, ws_misc2, ws_misc3;
   std::vector<cudaEvent_t> events;
   bool profiling = false;
+  void* pinned = nullptr;
+  size_t pinned_bytes = 0;
+  cudaEvent_t pinned_event = nullptr;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   std::map<int64_t, std::shared_ptr<tgb::ConvPlan>> plans;
@@ -119,6 +122,8 @@ inline void prof_end(tgb_ctx* ctx) {
 }
 void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t rb, const double* B, double h,
                    double* out);
+void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const double* const* A, int64_t rb,
+                   const double* const* B, const double* h, double* const* out);
 void conv_central_many_dev(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out);
 void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const double* wb, double scale, double* out);
 double scalar_product_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b);
