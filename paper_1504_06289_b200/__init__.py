@@ -8,7 +8,9 @@ from .tengrid import (AssembledPotential, BasisSet, CanonicalTensor3, Context, D
                       convolve, coulomb_matrix, default_context, discretize_basis, flatten_basis,
                       gauss_cell_integral, hadamard, hartree_potential, kernel_tensor, lattice_assemble_axis,
                       lattice_offsets, lattice_sum_canonical, make_expsum, make_grid, primitive_norm, scalar_product,
-                      scale, snap_to_node, value_at_points, window_offset, orbital_tensor, density_tensor)
+                      scale, snap_to_node, value_at_points, window_offset, orbital_tensor, density_tensor,
+                      LatticeBlock, lattice_grid, resolve_blocks, lattice_nodes, lattice_sum_tucker,
+                      lattice_sum_composite)
 
 from .tei import (TEIFactorization, build_tei, tei_cholesky, tei_column, tei_convolution_matrices,
                   tei_density_fitting, tei_diagonal, tei_matrix_entry)

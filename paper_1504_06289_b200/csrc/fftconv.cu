@@ -391,15 +391,18 @@ __device__ __forceinline__ void dft(double2* v) {
 // ------------------------------------------------------------------ passes
 
 // Butterfly input twiddles w^{j s}, s = 1..R-1 (w from the per-pass table).
+// Powers by a log-depth product tree (w^{2s} = (w^s)^2, w^{2s+1} = w^{2s} w)
+// rather than the serial recurrence, so the dependent-FP64 chain per
+// butterfly is ~log2(R) complex multiplies long.
 template <int R, int S>
 __device__ __forceinline__ void apply_twiddles(double2* v, double2 w) {
   if (S < 0) w.y = -w.y;
-  double2 ws = w;
+  double2 wp[R];
+  wp[1] = w;
 #pragma unroll
-  for (int s = 1; s < R; ++s) {
-    v[s] = cmul(v[s], ws);
-    if (s + 1 < R) ws = cmul(ws, w);
-  }
+  for (int s = 2; s < R; ++s) wp[s] = (s & 1) ? cmul(wp[s - 1], w) : cmul(wp[s >> 1], wp[s >> 1]);
+#pragma unroll
+  for (int s = 1; s < R; ++s) v[s] = cmul(v[s], wp[s]);
 }
 
 // In-place DIT pass of radix R and span L over N elements in shared memory.

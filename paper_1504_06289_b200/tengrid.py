@@ -539,8 +539,11 @@ class LatticeSpec:
 
 @dataclass
 class AssembledPotential:
+    """lattice.hpp:41-45."""
+
     canonical: CanonicalTensor3 | None = None
     window_ops: int = 0
+    tucker: object = None
 
 
 def lattice_offsets(spec: LatticeSpec, grid: Grid3, ax: int, lo: int = 0, hi: int | None = None) -> np.ndarray:
@@ -608,3 +611,138 @@ def density_tensor(disc: list, c_occ, reduce_eps: float = 1e-7, ctx: Context | N
     if theta.rank() <= 1 or reduce_eps <= 0.0:
         return theta
     return reduce_rank(theta, ReductionConfig.tolerance(reduce_eps), ctx)
+
+
+@dataclass
+class LatticeBlock:
+    """lattice.hpp:13-18 — inclusive node-index box, include/exclude, charge scale."""
+
+    lo: tuple = (0, 0, 0)
+    hi: tuple = (0, 0, 0)
+    include: bool = True
+    charge_scale: float = 1.0
+
+
+def _validate_spec(spec: LatticeSpec) -> None:
+    """lattice.cpp:13-18."""
+    for ax in range(3):
+        if spec.counts[ax] < 1:
+            raise InvalidArgument("LatticeSpec: counts must be >= 1")
+    if not spec.spacing > 0.0:
+        raise InvalidArgument("LatticeSpec: spacing must be positive")
+    if spec.n0 < 2 or spec.n0 % 2:
+        raise InvalidArgument("LatticeSpec: n0 must be even (node alignment)")
+    if spec.margin_cells < 1:
+        raise InvalidArgument("LatticeSpec: need at least one margin cell")
+
+
+def lattice_grid(spec: LatticeSpec) -> Grid3:
+    """lattice.cpp:65-75 — n = n0 (L - 1 + 2 margin) - 1 so every node is a cell centre."""
+    _validate_spec(spec)
+    cells = [spec.counts[ax] - 1 + 2 * spec.margin_cells for ax in range(3)]
+    return make_grid([0.5 * c * spec.spacing for c in cells], [spec.n0 * c - 1 for c in cells])
+
+
+def _overlap(a: LatticeBlock, b: LatticeBlock) -> bool:
+    return all(not (a.hi[ax] < b.lo[ax] or b.hi[ax] < a.lo[ax]) for ax in range(3))
+
+
+def resolve_blocks(spec: LatticeSpec) -> list:
+    """lattice.cpp:77-104 — disjoint included rectangles (the full lattice when no blocks)."""
+    _validate_spec(spec)
+    full = LatticeBlock((0, 0, 0), tuple(c - 1 for c in spec.counts), True, 1.0)
+    included = []
+    for b in spec.blocks:
+        if not b.include:
+            continue
+        if not b.charge_scale > 0.0:
+            raise InvalidArgument("resolve_blocks: charge scale must be positive")
+        for ax in range(3):
+            if not (0 <= b.lo[ax] <= b.hi[ax] < spec.counts[ax]):
+                raise InvalidArgument("resolve_blocks: block outside the lattice")
+        if any(_overlap(p, b) for p in included):
+            raise InvalidArgument("resolve_blocks: overlapping include blocks")
+        included.append(b)
+    if not included:
+        included.append(full)
+    for cut in spec.blocks:
+        if cut.include:
+            continue
+        nxt = []
+        for box in included:
+            if not _overlap(box, cut):
+                nxt.append(box)
+                continue
+            rest_lo, rest_hi = list(box.lo), list(box.hi)
+            for ax in range(3):  # lattice.cpp:31-48
+                if cut.lo[ax] > rest_lo[ax]:
+                    hi = list(rest_hi)
+                    hi[ax] = cut.lo[ax] - 1
+                    nxt.append(LatticeBlock(tuple(rest_lo), tuple(hi), True, box.charge_scale))
+                    rest_lo[ax] = cut.lo[ax]
+                if cut.hi[ax] < rest_hi[ax]:
+                    lo = list(rest_lo)
+                    lo[ax] = cut.hi[ax] + 1
+                    nxt.append(LatticeBlock(tuple(lo), tuple(rest_hi), True, box.charge_scale))
+                    rest_hi[ax] = cut.hi[ax]
+        included = nxt
+    if not included:
+        raise InvalidArgument("resolve_blocks: empty composite lattice")
+    return included
+
+
+def lattice_nodes(spec: LatticeSpec) -> np.ndarray:
+    """lattice.cpp:106-114."""
+    out = []
+    for r in resolve_blocks(spec):
+        for k in range(r.lo[2], r.hi[2] + 1):
+            for j in range(r.lo[1], r.hi[1] + 1):
+                for i in range(r.lo[0], r.hi[0] + 1):
+                    out.append((spec.position(0, i), spec.position(1, j), spec.position(2, k)))
+    return np.array(out)
+
+
+def lattice_sum_tucker(spec: LatticeSpec, grid: Grid3, master, ctx: Context | None = None):
+    """lattice.cpp:131-145 — the same window assembly on the Tucker side
+    matrices of a doubled-grid master; the core is scaled by the charge."""
+    _validate_spec(spec)
+    if spec.blocks:
+        raise InvalidArgument("lattice_sum_tucker: use lattice_sum_composite for block geometries")
+    for ax in range(3):
+        if master.side[ax].shape[0] != 2 * grid.n[ax]:
+            raise InvalidArgument("lattice_sum_tucker: master must live on the doubled grid")
+    from .reduction import TuckerTensor3
+
+    sides, ops = [], 0
+    for ax in range(3):
+        offs = lattice_offsets(spec, grid, ax)
+        sides.append(lattice_assemble_axis(master.side[ax], offs, grid.n[ax], ctx))
+        ops += len(offs)
+    out = AssembledPotential()
+    out.tucker = TuckerTensor3(sides, np.asfortranarray(master.core * spec.charge))
+    out.window_ops = ops
+    return out
+
+
+def lattice_sum_composite(spec: LatticeSpec, grid: Grid3, reference: KernelTensor, reduce_eps: float | None = None,
+                          ctx: Context | None = None) -> AssembledPotential:
+    """lattice.cpp:147-165 — per-block assembled sums concatenated (rank R per
+    block), then optionally rank-reduced on the device."""
+    if not reference.doubled:
+        raise InvalidArgument("lattice_sum_composite: reference must live on the doubled grid")
+    rects = resolve_blocks(spec)
+    out = AssembledPotential()
+    total = CanonicalTensor3.zero(grid.n)
+    for r in rects:
+        facs = []
+        for ax in range(3):
+            offs = lattice_offsets(spec, grid, ax, r.lo[ax], r.hi[ax])
+            facs.append(lattice_assemble_axis(reference.tensor.factor[ax], offs, grid.n[ax], ctx))
+            out.window_ops += len(offs)
+        total = add(total, CanonicalTensor3(facs, spec.charge * r.charge_scale * reference.tensor.weight))
+    if reduce_eps is not None:
+        from .reduction import ReductionConfig, reduce_rank
+
+        total = reduce_rank(total, ReductionConfig.tolerance(reduce_eps), ctx)
+    out.canonical = total
+    return out
