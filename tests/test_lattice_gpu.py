@@ -89,7 +89,7 @@ def test_composite_shapes_vs_node_sum(ctx, shape):
     ref = ref_kernel(grid, 5, 0.9)
     ap = tg.lattice_sum_composite(spec, grid, ref, None, ctx)
     rng = Rng(7)
-    pts = rng.integers(120, grid.n[0]).reshape(40, 3)
+    pts = np.stack([rng.integers(40, grid.n[ax]) for ax in range(3)], axis=1)
     got = tg.value_at_points(ap.canonical, pts, ctx)
     direct = np.zeros(len(pts))
     for c in tg.lattice_nodes(spec):
