@@ -35,6 +35,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -65,6 +66,7 @@ struct PlanArgs {
   int ntw, off_cs, off_zlo, off_zhi;
   int off_lo[kMaxPasses], off_hi[kMaxPasses];
   const double2* twpost; // forward post-processing: w_m^k, k <= N
+  unsigned long long* phase;  // analysis only (TGB_PHASE_CLK): per-phase SM cycles of the pair kernel
 };
 
 struct ConvPlan {
@@ -72,7 +74,7 @@ struct ConvPlan {
   bool direct = false;
   int threads = 0;
   size_t smem = 0;
-  DevBuf perm, inv, leader, tw, twpost;
+  DevBuf perm, inv, leader, tw, twpost, phase;
 };
 
 __host__ __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
@@ -155,11 +157,19 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
       }
     }
   }
+  // (10, 20, 8, 8) balances every pass at 320 threads but its stride-10 first
+  // pass bank-conflicts: measured slower (v14), opt-in only
+  if (N == 12800 && getenv("TGB_PLAN_10208")) rad = {10, 20, 8, 8};
   a.N = static_cast<int>(N);
   a.m = static_cast<int>(2 * N);
   const bool fits = !rad.empty();
   pl->direct = n <= ctx->direct_max || !fits;
   a.dbg = getenv("TGB_PAIR_DBG") ? atoi(getenv("TGB_PAIR_DBG")) : 0;
+  a.phase = nullptr;
+  if (getenv("TGB_PHASE_CLK")) {
+    a.phase = static_cast<unsigned long long*>(pl->phase.get(8 * sizeof(unsigned long long)));
+    TGB_CUDA(cudaMemset(a.phase, 0, 8 * sizeof(unsigned long long)));
+  }
   if (!pl->direct) {
     a.P = static_cast<int>(rad.size());
     int L = 1;
@@ -186,7 +196,13 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
     for (int g = 0; g < nblk; ++g) {
       const int kk = perm[static_cast<size_t>(g) * r0];
       const int g2 = kk == 0 ? g : inv[nblk - kk] / r0;
-      if (g2 >= g) leaders.push_back(make_int4(g, g2, kk, perm[static_cast<size_t>(g2) * r0]));
+      if (g2 > g || g == 0) leaders.push_back(make_int4(g, g2, kk, perm[static_cast<size_t>(g2) * r0]));
+    }
+    // self-mirror blocks (half the work of a pair) last: with 2 of them and
+    // npl - 1 a multiple of the thread count, thread 0 takes both singles
+    for (int g = 1; g < nblk; ++g) {
+      const int kk = perm[static_cast<size_t>(g) * r0];
+      if (inv[nblk - kk] / r0 == g) leaders.push_back(make_int4(g, g, kk, kk));
     }
     a.npl = static_cast<int>(leaders.size());
     std::vector<double2> tw;
@@ -344,24 +360,36 @@ __device__ __forceinline__ void dft(double2* v) {
     v[3] = cadd(e3, o3);
     v[7] = csub(e3, o3);
   } else if constexpr (R == 10) {
-    double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6], e4 = v[8];
-    double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7], o4 = v[9];
-    dft5<S>(e0, e1, e2, e3, e4);
-    dft5<S>(o0, o1, o2, o3, o4);
-    o1 = mul_cs<S>(o1, 0.80901699437494742410, 0.58778525229247312917);
-    o2 = mul_cs<S>(o2, 0.30901699437494742410, 0.95105651629515357212);
-    o3 = mul_cs<S>(o3, -0.30901699437494742410, 0.95105651629515357212);
-    o4 = mul_cs<S>(o4, -0.80901699437494742410, 0.58778525229247312917);
-    v[0] = cadd(e0, o0);
-    v[5] = csub(e0, o0);
-    v[1] = cadd(e1, o1);
-    v[6] = csub(e1, o1);
-    v[2] = cadd(e2, o2);
-    v[7] = csub(e2, o2);
-    v[3] = cadd(e3, o3);
-    v[8] = csub(e3, o3);
-    v[4] = cadd(e4, o4);
-    v[9] = csub(e4, o4);
+    // Good-Thomas 2 x 5 (no twiddles): n = (5 n1 + 2 n2) mod 10, k = (5 k1 + 6 k2) mod 10
+    double2 a0 = v[0], a1 = v[2], a2 = v[4], a3 = v[6], a4 = v[8];  // n1 = 0: n = 2 n2
+    double2 b0 = v[5], b1 = v[7], b2 = v[9], b3 = v[1], b4 = v[3];  // n1 = 1: n = 5 + 2 n2
+    dft5<S>(a0, a1, a2, a3, a4);
+    dft5<S>(b0, b1, b2, b3, b4);
+    v[0] = cadd(a0, b0);
+    v[5] = csub(a0, b0);
+    v[6] = cadd(a1, b1);
+    v[1] = csub(a1, b1);
+    v[2] = cadd(a2, b2);
+    v[7] = csub(a2, b2);
+    v[8] = cadd(a3, b3);
+    v[3] = csub(a3, b3);
+    v[4] = cadd(a4, b4);
+    v[9] = csub(a4, b4);
+  } else if constexpr (R == 20) {
+    // Good-Thomas 4 x 5 (no twiddles): n = (5 n1 + 4 n2) mod 20, k = (5 k1 + 16 k2) mod 20
+    double2 t[4][5];
+#pragma unroll
+    for (int n1 = 0; n1 < 4; ++n1) {
+#pragma unroll
+      for (int n2 = 0; n2 < 5; ++n2) t[n1][n2] = v[(5 * n1 + 4 * n2) % 20];
+      dft5<S>(t[n1][0], t[n1][1], t[n1][2], t[n1][3], t[n1][4]);
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < 5; ++k2) {
+      dft4<S>(t[0][k2], t[1][k2], t[2][k2], t[3][k2]);
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) v[(5 * k1 + 16 * k2) % 20] = t[k1][k2];
+    }
   } else if constexpr (R == 16) {
     // s = s2 + 4 s1: four radix-4 DFTs over s1, twiddle w16^(s2 k1), radix-4 over s2.
     constexpr double c1 = 0.92387953251128675613, s1 = 0.38268343236508977173;
@@ -495,6 +523,7 @@ __device__ __forceinline__ void dit_pass_rt(double2* sm, const double2* tws, con
     case 8: dit_pass<8, S>(sm, pa.N, pa.L[p], lo, hi); break;
     case 10: dit_pass<10, S>(sm, pa.N, pa.L[p], lo, hi); break;
     case 16: dit_pass<16, S>(sm, pa.N, pa.L[p], lo, hi); break;
+    case 20: dit_pass<20, S>(sm, pa.N, pa.L[p], lo, hi); break;
   }
 }
 
@@ -570,10 +599,9 @@ __device__ __forceinline__ double2 zsplit(double2 p, double2 q, double2 w) {
 
 // Stage P = A * B (stored order, N+1 entries) into shared memory with fully
 // coalesced, 8-deep batched L2 loads.
-template <bool BREAL>
+template <bool BREAL, int U = 8>
 __device__ __forceinline__ void stage_product(double2* sm, int N, const double2* __restrict__ A,
                                               const void* __restrict__ Bv) {
-  constexpr int U = 8;
   const int T = blockDim.x;
   int pos0 = threadIdx.x;
   for (; pos0 + (U - 1) * T < N; pos0 += U * T) {
@@ -753,6 +781,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     case 8: dit_pass<8, -1>(sm, N, 1, tws, tws); break;
     case 10: dit_pass<10, -1>(sm, N, 1, tws, tws); break;
     case 16: dit_pass<16, -1>(sm, N, 1, tws, tws); break;
+    case 20: dit_pass<20, -1>(sm, N, 1, tws, tws); break;
   }
   __syncthreads();
   for (int p = 1; p < pa.P; ++p) {
@@ -852,6 +881,7 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
         case 8: last_pass_store<8>(sm, tws, pa, o0, o1, aligned); break;
         case 10: last_pass_store<10>(sm, tws, pa, o0, o1, aligned); break;
         case 16: last_pass_store<16>(sm, tws, pa, o0, o1, aligned); break;
+        case 20: last_pass_store<20>(sm, tws, pa, o0, o1, aligned); break;
       }
     }
     __syncthreads();
@@ -986,20 +1016,183 @@ __global__ void __launch_bounds__(TT, 1)
     const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
     const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
                           : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
+    long long t0 = pa.phase ? clock64() : 0;
     stage_product<BREAL>(sm, N, a, b);
     __syncthreads();
+    long long t1 = pa.phase ? clock64() : 0;
     first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
     __syncthreads();
+    long long t2 = pa.phase ? clock64() : 0;
     static_pass<R1, L1, N, 1>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
     __syncthreads();
+    long long t3 = pa.phase ? clock64() : 0;
     static_pass<R2, L2, N, 1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
     __syncthreads();
+    long long t4 = pa.phase ? clock64() : 0;
     double* o0 = out + e.out0;
     double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
     static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
     __syncthreads();
+    if (pa.phase && threadIdx.x == 0) {
+      const long long t5 = clock64();
+      atomicAdd(pa.phase + 0, static_cast<unsigned long long>(t1 - t0));
+      atomicAdd(pa.phase + 1, static_cast<unsigned long long>(t2 - t1));
+      atomicAdd(pa.phase + 2, static_cast<unsigned long long>(t3 - t2));
+      atomicAdd(pa.phase + 3, static_cast<unsigned long long>(t4 - t3));
+      atomicAdd(pa.phase + 4, static_cast<unsigned long long>(t5 - t4));
+      atomicAdd(pa.phase + 5, 1ULL);
+    }
   }
+}
+
+// ---- TMEM-resident density spectra.  The staging of A*B is bound by the
+// SM's L2 read rate (~30-50 B/clk measured, v15), and A is 2/3 of those bytes.
+// A CTA takes a CONTIGUOUS, i-major run of the work list, so consecutive pairs
+// share A_i: it is loaded once per run into tensor memory (512 columns x 128
+// lanes x 4 B = 256 KB per SM, otherwise idle here) and each pair then reads
+// only B_j from L2.  Thread t stages positions t + TT k (k < N/TT); its
+// values live in its own TMEM lane (warp w -> lanes 32 (w % 4) + lane),
+// columns [(w / 4) * 4 N/TT, ...).
+
+#define TGB_R8(p) "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]), "r"(p[6]), "r"(p[7])
+#define TGB_W8(p) "=r"(p[0]), "=r"(p[1]), "=r"(p[2]), "=r"(p[3]), "=r"(p[4]), "=r"(p[5]), "=r"(p[6]), "=r"(p[7])
+
+// 8 doubles2 = 32 columns of this thread's lane
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      TGB_R8((r + 0)), TGB_R8((r + 8)), TGB_R8((r + 16)), TGB_R8((r + 24))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : TGB_W8((r + 0)), TGB_W8((r + 8)), TGB_W8((r + 16)), TGB_W8((r + 24))
+      : "r"(taddr)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+
+template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    pair_kernel_tmem(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
+                     const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
+  constexpr int N = R0 * R1 * R2 * R3;
+  constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
+  constexpr int K = N / TT;  // staged positions per thread
+  static_assert(N % TT == 0 && K % 8 == 0, "whole 8-element TMEM chunks per thread");
+  static_assert(((TT / 32 + 3) / 4) * 4 * K <= 512, "density spectrum exceeds tensor memory");
+  __shared__ uint32_t tmem_base_sh;
+  extern __shared__ double2 sm[];
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base_sh));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  const double2* tws = load_tables(sm, pa);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                         static_cast<uint32_t>((warp >> 2) * 4 * K);
+  const int nz = (pa.n + 1) >> 1;
+  const bool odd_n = pa.n & 1;
+  const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
+  const int w1 = static_cast<int>((static_cast<int64_t>(nwork) * (blockIdx.x + 1)) / gridDim.x);
+  int ia_cur = -1;
+  for (int w = w0; w < w1; ++w) {
+    const PairEntry e = work[w];
+    const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
+    long long t0 = pa.phase ? clock64() : 0;
+    if (e.ia != ia_cur) {  // CTA-uniform: a new density column -> tensor memory
+      ia_cur = e.ia;
+#pragma unroll 1
+      for (int c = 0; c < K; c += 8) {
+        uint32_t r[32];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double2 v = ld2(a + threadIdx.x + TT * (c + u));
+          r[4 * u + 0] = __double2loint(v.x);
+          r[4 * u + 1] = __double2hiint(v.x);
+          r[4 * u + 2] = __double2loint(v.y);
+          r[4 * u + 3] = __double2hiint(v.y);
+        }
+        tmem_st32(tbase + 4 * c, r);
+      }
+      tmem_wait_st();
+    }
+    // stage P = A * B: A from tensor memory, B from L2 (all K loads in flight)
+    if constexpr (BREAL) {
+      const double* bb = static_cast<const double*>(b) + threadIdx.x;
+      double bv[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) bv[k] = __ldg(bb + TT * k);
+#pragma unroll
+      for (int c = 0; c < K; c += 8) {
+        uint32_t r[32];
+        tmem_ld32(tbase + 4 * c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double2 v = make_double2(__hiloint2double(r[4 * u + 1], r[4 * u + 0]),
+                                         __hiloint2double(r[4 * u + 3], r[4 * u + 2]));
+          sm[pidx(threadIdx.x + TT * (c + u))] = cscale(v, bv[c + u]);
+        }
+      }
+    } else {
+      const double2* bb = static_cast<const double2*>(b) + threadIdx.x;
+#pragma unroll 1
+      for (int c = 0; c < K; c += 8) {
+        double2 bv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) bv[u] = ld2(bb + TT * (c + u));
+        uint32_t r[32];
+        tmem_ld32(tbase + 4 * c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double2 v = make_double2(__hiloint2double(r[4 * u + 1], r[4 * u + 0]),
+                                         __hiloint2double(r[4 * u + 3], r[4 * u + 2]));
+          sm[pidx(threadIdx.x + TT * (c + u))] = cmul(v, bv[u]);
+        }
+      }
+    }
+    __syncthreads();
+    long long t1 = pa.phase ? clock64() : 0;
+    first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
+    __syncthreads();
+    long long t2 = pa.phase ? clock64() : 0;
+    static_pass<R1, L1, N, 1>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
+    __syncthreads();
+    long long t3 = pa.phase ? clock64() : 0;
+    static_pass<R2, L2, N, 1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+    __syncthreads();
+    long long t4 = pa.phase ? clock64() : 0;
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+    static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
+    __syncthreads();
+    if (pa.phase && threadIdx.x == 0) {
+      const long long t5 = clock64();
+      atomicAdd(pa.phase + 0, static_cast<unsigned long long>(t1 - t0));
+      atomicAdd(pa.phase + 1, static_cast<unsigned long long>(t2 - t1));
+      atomicAdd(pa.phase + 2, static_cast<unsigned long long>(t3 - t2));
+      atomicAdd(pa.phase + 3, static_cast<unsigned long long>(t4 - t3));
+      atomicAdd(pa.phase + 4, static_cast<unsigned long long>(t5 - t4));
+      atomicAdd(pa.phase + 5, 1ULL);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh) : "memory");
 }
 
 // Direct windowed convolution (small n, or n beyond the single-CTA FFT).
@@ -1099,22 +1292,41 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
     return false;
   // the cp.async-pipelined variant measured slower (2.02 vs 1.68 ms/axis, v8); opt-in only
   auto kern = getenv("TGB_PIPE") ? pair_kernel_pipe<R0, R1, R2, R3, TT, BREAL>
-                                 : pair_kernel_static<R0, R1, R2, R3, TT, BREAL>;
+              : (getenv("TGB_NO_TMEM") || a.N % TT) ? pair_kernel_static<R0, R1, R2, R3, TT, BREAL>
+                                                    : pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>;
   static bool attr = false;
   if (!attr) {
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel_static<R0, R1, R2, R3, TT, BREAL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+    cudaFuncAttributes fa{};
+    TGB_CUDA(cudaFuncGetAttributes(&fa, pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>));
+    TGB_CUDA(cudaFuncSetAttribute(pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel_pipe<R0, R1, R2, R3, TT, BREAL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
     attr = true;
   }
   int per_sm = 1;
   TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, pl.smem));
+  if (per_sm > 1 && kern == pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>) {  // TMEM: one CTA per SM
+    kern = pair_kernel_static<R0, R1, R2, R3, TT, BREAL>;
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, pl.smem));
+  }
   const int grid = std::max(1, std::min(nwork, std::max(1, per_sm) * ctx->num_sms));
   prof_begin(ctx);
   kern<<<grid, TT, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, nwork, out);
   TGB_LAUNCHED(ctx);
   prof_end(ctx);
+  if (a.phase) {  // analysis only: cumulative per-phase cycles (summed over CTAs) per pair
+    unsigned long long h[8];
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    TGB_CUDA(cudaMemcpy(h, a.phase, sizeof(h), cudaMemcpyDeviceToHost));
+    const double np = static_cast<double>(h[5] ? h[5] : 1);
+    fprintf(stderr, "phase cycles/pair: stage %.0f pass0 %.0f pass1 %.0f pass2 %.0f last %.0f (pairs %llu)\n",
+            h[0] / np, h[1] / np, h[2] / np, h[3] / np, h[4] / np, h[5]);
+    TGB_CUDA(cudaMemset(a.phase, 0, sizeof(h)));
+  }
   return true;
 }
 
@@ -1122,6 +1334,7 @@ template <bool BREAL>
 static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                           const PairEntry* dwork, int nwork, double* out) {
   // compile-time plans (config 2: n = 16385 -> N = 12800)
+  if (try_static<10, 20, 8, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, nwork, out)) return;
   if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, nwork, out)) return;
   switch (pl.a.r[0]) {
     case 2: launch_pair<2, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
