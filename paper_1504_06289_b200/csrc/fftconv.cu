@@ -53,6 +53,7 @@ constexpr int kMaxThreads = 384;
 
 struct PlanArgs {
   int n, N, m, P, ofs, even, npl;
+  int nsp;  // single (self-mirror) first-pass blocks, stored last in the leader list
   int dbg;  // analysis only (TGB_PAIR_DBG): 1 skip stores, 2 skip L2 loads, 4 skip passes
   int r[kMaxPasses];
   int L[kMaxPasses];
@@ -66,6 +67,7 @@ struct PlanArgs {
   int ntw, off_cs, off_zlo, off_zhi;
   int off_lo[kMaxPasses], off_hi[kMaxPasses];
   const double2* twpost; // forward post-processing: w_m^k, k <= N
+  int store_dbg;              // analysis only (TGB_STORE_DBG): 1 first column only, 2 no stores
   unsigned long long* phase;  // analysis only (TGB_PHASE_CLK): per-phase SM cycles of the pair kernel
 };
 
@@ -166,6 +168,7 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
   pl->direct = n <= ctx->direct_max || !fits;
   a.dbg = getenv("TGB_PAIR_DBG") ? atoi(getenv("TGB_PAIR_DBG")) : 0;
   a.phase = nullptr;
+  a.store_dbg = getenv("TGB_STORE_DBG") ? atoi(getenv("TGB_STORE_DBG")) : 0;
   if (getenv("TGB_PHASE_CLK")) {
     a.phase = static_cast<unsigned long long*>(pl->phase.get(8 * sizeof(unsigned long long)));
     TGB_CUDA(cudaMemset(a.phase, 0, 8 * sizeof(unsigned long long)));
@@ -193,16 +196,22 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
     }
     const int r0 = rad[0], nblk = a.N / r0;
     std::vector<int4> leaders;
+    // order: the regular pairs (g2 > g), then block 0 and the self-mirror
+    // blocks — pair_kernel_tmem's split first pass gives those single blocks
+    // lanes of their own in warps without half items
     for (int g = 0; g < nblk; ++g) {
       const int kk = perm[static_cast<size_t>(g) * r0];
       const int g2 = kk == 0 ? g : inv[nblk - kk] / r0;
-      if (g2 > g || g == 0) leaders.push_back(make_int4(g, g2, kk, perm[static_cast<size_t>(g2) * r0]));
+      if (g2 > g) leaders.push_back(make_int4(g, g2, kk, perm[static_cast<size_t>(g2) * r0]));
     }
-    // self-mirror blocks (half the work of a pair) last: with 2 of them and
-    // npl - 1 a multiple of the thread count, thread 0 takes both singles
-    for (int g = 1; g < nblk; ++g) {
+    a.nsp = 0;
+    for (int g = 0; g < nblk; ++g) {
       const int kk = perm[static_cast<size_t>(g) * r0];
-      if (inv[nblk - kk] / r0 == g) leaders.push_back(make_int4(g, g, kk, kk));
+      const int g2 = kk == 0 ? g : inv[nblk - kk] / r0;
+      if (g2 == g) {
+        leaders.push_back(make_int4(g, g2, kk, kk));
+        ++a.nsp;
+      }
     }
     a.npl = static_cast<int>(leaders.size());
     std::vector<double2> tw;
@@ -551,6 +560,30 @@ __device__ __forceinline__ void store_outputs(const double2* v, int j, int L, in
   }
 }
 
+// Same, with the per-pair constant lim = number of leading outputs that are
+// whole 16-byte pairs in aligned columns (0 when unaligned): one compare per
+// output on the fast path.
+template <int R, int L>
+__device__ __forceinline__ void store_outputs_fast(const double2* v, int j, int lim, int nz, bool odd_n, double* o0,
+                                                   double* o1) {
+#pragma unroll
+  for (int t = 0; t < R; ++t) {
+    const int idx = j + t * L;
+    if (idx < lim) {
+      __stcs(reinterpret_cast<double2*>(o0 + 2 * idx), v[t]);
+      if (o1) __stcs(reinterpret_cast<double2*>(o1 + 2 * idx), v[t]);
+    } else if (idx < nz && o0) {
+      const bool full = !(odd_n && idx == nz - 1);
+      __stcs(o0 + 2 * idx, v[t].x);
+      if (full) __stcs(o0 + 2 * idx + 1, v[t].y);
+      if (o1) {
+        __stcs(o1 + 2 * idx, v[t].x);
+        if (full) __stcs(o1 + 2 * idx + 1, v[t].y);
+      }
+    }
+  }
+}
+
 template <int R>
 __device__ __forceinline__ void last_pass_store(const double2* sm, const double2* tws, const PlanArgs& pa, double* o0,
                                                 double* o1, bool aligned) {
@@ -595,6 +628,16 @@ __device__ __forceinline__ double2 zsplit(double2 p, double2 q, double2 w) {
   const double2 dif = make_double2(p.x - q.x, p.y + q.y);
   const double2 wd = cmul(w, dif);
   return make_double2(sum.x - wd.y, sum.y + wd.x);
+}
+
+// Both halves of a mirror pair at once: with w' = w_m^{N-k} = -conj(w_m^k),
+// zsplit(q, p, w') = conj(sum - i w dif) where zsplit(p, q, w) = sum + i w dif.
+__device__ __forceinline__ void zsplit_pair(double2 p, double2 q, double2 w, double2& zp, double2& zq) {
+  const double2 sum = make_double2(p.x + q.x, p.y - q.y);
+  const double2 dif = make_double2(p.x - q.x, p.y + q.y);
+  const double2 wd = cmul(w, dif);
+  zp = make_double2(sum.x - wd.y, sum.y + wd.x);
+  zq = make_double2(sum.x + wd.y, wd.x - sum.y);
 }
 
 // Stage P = A * B (stored order, N+1 entries) into shared memory with fully
@@ -660,14 +703,14 @@ __device__ __forceinline__ void scale_block(double2* v, const void* __restrict__
 }
 
 template <int R, bool MULB = false, bool BREAL = true>
-__device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, const PlanArgs& pa,
-                                               const double2* __restrict__ A, const void* __restrict__ B,
-                                               bool breal) {
+__device__ __forceinline__ void first_item(double2* sm, const double2* tws, const PlanArgs& pa,
+                                           const double2* __restrict__ A, const void* __restrict__ B, bool breal,
+                                           int q) {
   const int N = pa.N;
   const double2* cs = tws + pa.off_cs;
   const double2* zlo = tws + pa.off_zlo;
   const double2* zhi = tws + pa.off_zhi;
-  for (int q = threadIdx.x; q < pa.npl; q += blockDim.x) {
+  {
     const int4 gg = __ldg(pa.leader + q);
     const int g = gg.x, g2 = gg.y;
     double2 a[R];
@@ -683,8 +726,8 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, 
 #pragma unroll
       for (int s = 1; 2 * s <= R; ++s) {
         if (2 * s < R) {
-          const double2 zs = zsplit(a[s], a[R - s], cs[s]);
-          const double2 zr = zsplit(a[R - s], a[s], cs[R - s]);
+          double2 zs, zr;
+          zsplit_pair(a[s], a[R - s], cs[s], zs, zr);
           a[s] = zs;
           a[R - s] = zr;
         } else {
@@ -699,8 +742,8 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, 
       const double2 wk = cmul(zlo[gg.z & 63], zhi[gg.z >> 6]);
 #pragma unroll
       for (int s = 0; 2 * s < R - 1; ++s) {
-        const double2 z1 = zsplit(a[s], a[R - 1 - s], cmul(wk, cs[s]));
-        const double2 z2 = zsplit(a[R - 1 - s], a[s], cmul(wk, cs[R - 1 - s]));
+        double2 z1, z2;
+        zsplit_pair(a[s], a[R - 1 - s], cmul(wk, cs[s]), z1, z2);
         a[s] = z1;
         a[R - 1 - s] = z2;
       }
@@ -713,15 +756,14 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, 
       for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
     } else {
       const double2 wk = cmul(zlo[gg.z & 63], zhi[gg.z >> 6]);
-      const double2 wk2 = cmul(zlo[gg.w & 63], zhi[gg.w >> 6]);
       double2 b[R];
 #pragma unroll
       for (int s = 0; s < R; ++s) b[s] = sm[pidx(g2 * R + s)];
       scale_block<R, MULB, BREAL>(b, B, g2 * R);
 #pragma unroll
       for (int s = 0; s < R; ++s) {
-        const double2 za = zsplit(a[s], b[R - 1 - s], cmul(wk, cs[s]));
-        const double2 zb = zsplit(b[R - 1 - s], a[s], cmul(wk2, cs[R - 1 - s]));
+        double2 za, zb;
+        zsplit_pair(a[s], b[R - 1 - s], cmul(wk, cs[s]), za, zb);
         a[s] = za;
         b[R - 1 - s] = zb;
       }
@@ -733,6 +775,57 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, 
         sm[pidx(g2 * R + s)] = b[s];
       }
     }
+  }
+}
+
+template <int R, bool MULB = false, bool BREAL = true>
+__device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, const PlanArgs& pa,
+                                               const double2* __restrict__ A, const void* __restrict__ B,
+                                               bool breal) {
+  for (int q = threadIdx.x; q < pa.npl; q += blockDim.x) first_item<R, MULB, BREAL>(sm, tws, pa, A, B, breal, q);
+}
+
+// First pass with TT threads when TT < npl <= 2 TT: one full round, then the
+// leftover block pairs (regular, g2 > g) as half items — lanes 2u and 2u+1
+// both load blocks g and g2; the even lane splits + transforms block g, the
+// odd lane block g2 (the same code with the roles swapped), so the second
+// round costs half a pair instead of a whole one.
+template <int R, int TT>
+__device__ __forceinline__ void first_pass_split(double2* sm, const double2* tws, const PlanArgs& pa,
+                                                 const double2* __restrict__ A, const void* __restrict__ B,
+                                                 bool breal) {
+  const int nreg = pa.npl - pa.nsp;  // regular pairs first in the leader list
+  if (nreg < TT || nreg > 2 * TT || 2 * (nreg - TT) > TT - 32 * pa.nsp) {
+    first_pass_inv<R>(sm, tws, pa, A, B, breal);  // shapes this split is not laid out for
+    return;
+  }
+  first_item<R>(sm, tws, pa, A, B, breal, threadIdx.x);
+  const int nrem = nreg - TT;
+  const int u = threadIdx.x >> 1, h = threadIdx.x & 1;
+  if (u < nrem) {  // partners share a warp
+    const double2* cs = tws + pa.off_cs;
+    const double2* zlo = tws + pa.off_zlo;
+    const double2* zhi = tws + pa.off_zhi;
+    const int4 gg = __ldg(pa.leader + TT + u);
+    const int gx = h ? gg.y : gg.x, gy = h ? gg.x : gg.y, kx = h ? gg.w : gg.z;
+    double2 x[R], y[R];
+#pragma unroll
+    for (int s = 0; s < R; ++s) {
+      x[s] = sm[pidx(gx * R + s)];
+      y[s] = sm[pidx(gy * R + s)];
+    }
+    __syncwarp(__activemask());
+    const double2 wk = cmul(zlo[kx & 63], zhi[kx >> 6]);
+#pragma unroll
+    for (int s = 0; s < R; ++s) x[s] = zsplit(x[s], y[R - 1 - s], cmul(wk, cs[s]));
+    dft<R, 1>(x);
+#pragma unroll
+    for (int s = 0; s < R; ++s) sm[pidx(gx * R + s)] = x[s];
+  } else {
+    // single blocks: lane 0 of each of the last nsp warps
+    const int sp = pa.nsp - (TT - static_cast<int>(threadIdx.x)) / 32;
+    if ((threadIdx.x & 31) == 0 && sp >= 0 && sp < pa.nsp && static_cast<int>(threadIdx.x) >= TT - 32 * pa.nsp)
+      first_item<R>(sm, tws, pa, A, B, breal, nreg + sp);
   }
 }
 
@@ -916,11 +1009,55 @@ __device__ __forceinline__ void static_pass(double2* sm, const double2* lo, cons
   }
 }
 
+// Same pass when every thread's butterflies share one span index j
+// (TT % L == 0): the R - 1 twiddle powers are formed once per pass, not per
+// butterfly.
+template <int R, int L, int N, int S, int TT>
+__device__ __forceinline__ void static_pass_t(double2* sm, const double2* lo, const double2* hi) {
+  constexpr int NBF = N / R;
+  if constexpr (L > 1 && TT % L == 0 && NBF % TT == 0) {
+    const int j = threadIdx.x % L;
+    double2 w = L <= 64 ? lo[j] : cmul(lo[j & 63], hi[j >> 6]);
+    if (S < 0) w.y = -w.y;
+    double2 wp[R];
+    wp[1] = w;
+#pragma unroll
+    for (int q = 2; q < R; ++q) wp[q] = (q & 1) ? cmul(wp[q - 1], w) : cmul(wp[q >> 1], wp[q >> 1]);
+#pragma unroll 1
+    for (int G = threadIdx.x / L; G < NBF / L; G += TT / L) {
+      const int base = G * (L * R) + j;
+      double2 v[R];
+      if constexpr (L % 16 == 0) {
+        double2* p = sm + pidx(base);
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = p[q * (L + L / 16)];
+#pragma unroll
+        for (int q = 1; q < R; ++q) v[q] = cmul(v[q], wp[q]);
+        dft<R, S>(v);
+#pragma unroll
+        for (int t = 0; t < R; ++t) p[t * (L + L / 16)] = v[t];
+      } else {
+#pragma unroll
+        for (int q = 0; q < R; ++q) v[q] = sm[pidx(base + q * L)];
+#pragma unroll
+        for (int q = 1; q < R; ++q) v[q] = cmul(v[q], wp[q]);
+        dft<R, S>(v);
+#pragma unroll
+        for (int t = 0; t < R; ++t) sm[pidx(base + t * L)] = v[t];
+      }
+    }
+  } else {
+    static_pass<R, L, N, S>(sm, lo, hi);
+  }
+}
+
 template <int R, int L, int N>
 __device__ __forceinline__ void static_last(const double2* sm, const double2* lo, const double2* hi, int nz,
                                             bool odd_n, double* o0, double* o1, bool aligned) {
   constexpr int NBF = N / R;
   static_assert(L % 16 == 0 && NBF == L, "last pass spans the whole transform");
+  const int lim = (aligned && o0) ? (odd_n ? nz - 1 : nz) : 0;
+  constexpr bool getenv_fast_store = false;  // v17: the branchy fast path measured slower
   for (int j = threadIdx.x; j < NBF; j += blockDim.x) {
     const double2* p = sm + pidx(j);
     double2 v[R];
@@ -928,7 +1065,8 @@ __device__ __forceinline__ void static_last(const double2* sm, const double2* lo
     for (int s = 0; s < R; ++s) v[s] = p[s * (L + L / 16)];
     apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
     dft<R, 1>(v);
-    store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
+    if (getenv_fast_store) store_outputs_fast<R, L>(v, j, lim, nz, odd_n, o0, o1);
+    else store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
   }
 }
 
@@ -1166,17 +1304,17 @@ __global__ void __launch_bounds__(TT, 1)
     }
     __syncthreads();
     long long t1 = pa.phase ? clock64() : 0;
-    first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
+    first_pass_split<R0, TT>(sm, tws, pa, a, b, BREAL);
     __syncthreads();
     long long t2 = pa.phase ? clock64() : 0;
-    static_pass<R1, L1, N, 1>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
+    static_pass_t<R1, L1, N, 1, TT>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
     __syncthreads();
     long long t3 = pa.phase ? clock64() : 0;
-    static_pass<R2, L2, N, 1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+    static_pass_t<R2, L2, N, 1, TT>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
     __syncthreads();
     long long t4 = pa.phase ? clock64() : 0;
-    double* o0 = out + e.out0;
-    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    double* o0 = pa.store_dbg >= 2 ? nullptr : out + e.out0;
+    double* o1 = e.out1 >= 0 && !pa.store_dbg ? out + e.out1 : nullptr;
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
     static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
     __syncthreads();
