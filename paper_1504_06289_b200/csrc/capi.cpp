@@ -173,6 +173,9 @@ int tgb_ctx_create(int device, void* stream, tgb_ctx** out) {
       c->own_stream = true;
     }
     TGB_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    TGB_CUDA(cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    TGB_CUDA(cudaEventCreateWithFlags(&c->aux_in, cudaEventDisableTiming));
+    TGB_CUDA(cudaEventCreateWithFlags(&c->aux_done, cudaEventDisableTiming));
     *out = c;
   });
 }
@@ -183,7 +186,11 @@ int tgb_ctx_destroy(tgb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamSynchronize(ctx->aux_stream);
     for (auto e : ctx->events) cudaEventDestroy(e);
+    cudaEventDestroy(ctx->aux_in);
+    cudaEventDestroy(ctx->aux_done);
+    if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
     if (ctx->pinned_event) cudaEventDestroy(ctx->pinned_event);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto& pe : ctx->prof_events) {
@@ -191,6 +198,7 @@ int tgb_ctx_destroy(tgb_ctx* ctx) {
       cudaEventDestroy(pe.second);
     }
     cudaStreamDestroy(ctx->copy_stream);
+    cudaStreamDestroy(ctx->aux_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });

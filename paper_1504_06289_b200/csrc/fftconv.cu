@@ -67,6 +67,8 @@ struct PlanArgs {
   int ntw, off_cs, off_zlo, off_zhi;
   int off_lo[kMaxPasses], off_hi[kMaxPasses];
   const double2* twpost; // forward post-processing: w_m^k, k <= N
+  const double2* ph1;    // mode 1: e^{-i pi k (n-1)/m} * (cos(pi k/m) for even n), k <= N
+  const double2* ph2;    // mode 2: e^{2 pi i k ofs/m} * ((1 + e^{2 pi i k/m})/2 for even n), k <= N
   int store_dbg;              // analysis only (TGB_STORE_DBG): 1 first column only, 2 no stores
   unsigned long long* phase;  // analysis only (TGB_PHASE_CLK): per-phase SM cycles of the pair kernel
 };
@@ -76,7 +78,7 @@ struct ConvPlan {
   bool direct = false;
   int threads = 0;
   size_t smem = 0;
-  DevBuf perm, inv, leader, tw, twpost, phase;
+  DevBuf perm, inv, leader, tw, twpost, ph1, ph2, phase;
 };
 
 __host__ __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
@@ -170,8 +172,8 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
   a.phase = nullptr;
   a.store_dbg = getenv("TGB_STORE_DBG") ? atoi(getenv("TGB_STORE_DBG")) : 0;
   if (getenv("TGB_PHASE_CLK")) {
-    a.phase = static_cast<unsigned long long*>(pl->phase.get(8 * sizeof(unsigned long long)));
-    TGB_CUDA(cudaMemset(a.phase, 0, 8 * sizeof(unsigned long long)));
+    a.phase = static_cast<unsigned long long*>(pl->phase.get(16 * sizeof(unsigned long long)));
+    TGB_CUDA(cudaMemset(a.phase, 0, 16 * sizeof(unsigned long long)));
   }
   if (!pl->direct) {
     a.P = static_cast<int>(rad.size());
@@ -241,6 +243,31 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
     a.leader = static_cast<const int4*>(up(pl->leader, leaders.data(), leaders.size() * sizeof(int4)));
     a.tw = static_cast<const double2*>(up(pl->tw, tw.data(), tw.size() * sizeof(double2)));
     a.twpost = static_cast<const double2*>(up(pl->twpost, twpost.data(), twpost.size() * sizeof(double2)));
+    {
+      std::vector<double2> t1(a.N + 1), t2(a.N + 1);
+      const long double pi = 3.141592653589793238462643383279502884L;
+      for (int64_t k = 0; k <= a.N; ++k) {
+        const int64_t e1 = (k * (n - 1)) % (2 * static_cast<int64_t>(a.m));
+        long double c1 = cosl(pi * e1 / a.m), s1 = sinl(pi * e1 / a.m);
+        if (even) {
+          const long double ce = cosl(pi * k / a.m);
+          c1 *= ce;
+          s1 *= ce;
+        }
+        t1[k] = make_double2(static_cast<double>(c1), static_cast<double>(s1));
+        const int64_t e2 = (k * a.ofs) % a.m;
+        long double c2 = cosl(2 * pi * e2 / a.m), s2 = sinl(2 * pi * e2 / a.m);
+        if (even) {
+          const long double hc = 0.5L * (1 + cosl(2 * pi * k / a.m)), hs = 0.5L * sinl(2 * pi * k / a.m);
+          const long double rc = c2 * hc - s2 * hs, rs = c2 * hs + s2 * hc;
+          c2 = rc;
+          s2 = rs;
+        }
+        t2[k] = make_double2(static_cast<double>(c2), static_cast<double>(s2));
+      }
+      a.ph1 = static_cast<const double2*>(up(pl->ph1, t1.data(), t1.size() * sizeof(double2)));
+      a.ph2 = static_cast<const double2*>(up(pl->ph2, t2.data(), t2.size() * sizeof(double2)));
+    }
     pl->smem = plan_smem(a.N) + static_cast<size_t>(a.ntw) * sizeof(double2);
     // threads: best butterfly balance over the passes, at least 8 warps when possible
     double best_eff = -1.0;
@@ -847,15 +874,15 @@ __device__ __forceinline__ double2* load_tables(double2* sm, const PlanArgs& pa)
 // so the few, latency-bound kernel transforms overlap the density ones.
 __global__ void __launch_bounds__(kMaxThreads, 1)
     spectrum_kernel(PlanArgs pa, const double* __restrict__ XA, int nA, void* __restrict__ specA,
-                    const double* __restrict__ XB, const int* __restrict__ colidx, void* __restrict__ specB,
-                    int modeB, int64_t ldx, double h) {
+                    const double* __restrict__ XB, const int* __restrict__ colidx, int nB, void* __restrict__ specB,
+                    void* __restrict__ specB2, int modeB, int64_t ldx, double h) {
   extern __shared__ double2 sm[];
   const double2* tws = load_tables(sm, pa);
-  const bool isA = static_cast<int>(blockIdx.x) < nA;
-  const int c = isA ? blockIdx.x : blockIdx.x - nA;
+  const bool isA = static_cast<int>(blockIdx.x) >= nB;  // kernel columns first (they carry the extra work)
+  const int c = isA ? blockIdx.x - nB : blockIdx.x;
   const int mode = isA ? 0 : modeB;
   void* spec = isA ? specA : specB;
-  const double* x = isA ? XA + c * ldx : XB + colidx[c] * ldx;
+  const double* x = isA ? XA + c * ldx : XB + (colidx ? colidx[c] : c) * ldx;
   const int n = pa.n, N = pa.N;
   for (int k = threadIdx.x; k < N; k += blockDim.x) {  // natural order: coalesced reads
     const int i0 = 2 * k;
@@ -894,6 +921,10 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     const double2 Xk = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
     if (mode == 0) {
       static_cast<double2*>(spec)[static_cast<int64_t>(c) * (N + 1) + pos] = Xk;
+    } else if (mode == 3) {  // both forms (symmetry decided later on the host)
+      const double2 t = ld2(pa.ph1 + k);
+      static_cast<double*>(spec)[static_cast<int64_t>(c) * (N + 1) + pos] = hm * (Xk.x * t.x - Xk.y * t.y);
+      static_cast<double2*>(specB2)[static_cast<int64_t>(c) * (N + 1) + pos] = cmul(Xk, cscale(ld2(pa.ph2 + k), hm));
     } else if (mode == 1) {
       // remove the centring phase e^{-2 pi i k c/m}, c = (n-1)/2
       const int64_t e = (static_cast<int64_t>(k) * (n - 1)) % (2 * static_cast<int64_t>(pa.m));
@@ -924,9 +955,9 @@ struct PairEntry {
 
 // Persistent: CTA loops over work entries; one windowed convolution each.
 template <int R0, bool BREAL>
-__global__ void __launch_bounds__(kMaxThreads, 1)
-    pair_kernel(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
-                const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
+__device__ __forceinline__ void pair_body(const PlanArgs& pa, const double2* __restrict__ specA,
+                                          const void* __restrict__ specB, const PairEntry* __restrict__ work,
+                                          int nwork, double* __restrict__ out) {
   extern __shared__ double2 sm[];
   const double2* tws = load_tables(sm, pa);
   const int N = pa.N;
@@ -979,6 +1010,17 @@ __global__ void __launch_bounds__(kMaxThreads, 1)
     }
     __syncthreads();
   }
+}
+
+// The work count and the kernel-column symmetry come from the device-built
+// work list (build_work_kernel), so no host round trip sits between the
+// grouping and this launch.
+template <int R0, bool BREAL>
+__global__ void __launch_bounds__(kMaxThreads, 1)
+    pair_kernel(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
+                const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out) {
+  if ((winfo[1] != 0) != BREAL) return;
+  pair_body<R0, BREAL>(pa, specA, specB, work, winfo[0], out);
 }
 
 // ---- compile-time plans: every span L and stride is a constant, so the
@@ -1070,79 +1112,10 @@ __device__ __forceinline__ void static_last(const double2* sm, const double2* lo
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
-// Last pass that, as soon as a butterfly's inputs are in registers, refills
-// those shared-memory slots with the NEXT pair's density spectrum (cp.async,
-// no registers), so the next pair's L2 reads overlap this pair's last
-// butterflies and output stores.
-template <int R, int L, int N>
-__device__ __forceinline__ void static_last_pipe(double2* sm, const double2* lo, const double2* hi, int nz,
-                                                 bool odd_n, double* o0, double* o1, bool aligned,
-                                                 const double2* __restrict__ a_next) {
-  constexpr int NBF = N / R;
-  static_assert(L % 16 == 0 && NBF == L, "last pass spans the whole transform");
-  if (a_next && threadIdx.x == 0) cp_async16(sm + pidx(N), a_next + N);
-  for (int j = threadIdx.x; j < NBF; j += blockDim.x) {
-    double2* p = sm + pidx(j);
-    double2 v[R];
-#pragma unroll
-    for (int s = 0; s < R; ++s) v[s] = p[s * (L + L / 16)];
-    if (a_next) {
-#pragma unroll
-      for (int s = 0; s < R; ++s) cp_async16(p + s * (L + L / 16), a_next + j + s * L);
-    }
-    apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
-    dft<R, 1>(v);
-    store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
-  }
-}
-
 template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
-__global__ void __launch_bounds__(TT, 1)
-    pair_kernel_pipe(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
-                     const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
-  constexpr int N = R0 * R1 * R2 * R3;
-  constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
-  extern __shared__ double2 sm[];
-  const double2* tws = load_tables(sm, pa);
-  const int nz = (pa.n + 1) >> 1;
-  const bool odd_n = pa.n & 1;
-  if (blockIdx.x < nwork) {  // prologue: the first pair's density spectrum
-    const double2* a0 = specA + static_cast<int64_t>(work[blockIdx.x].ia) * (N + 1);
-    for (int pos = threadIdx.x; pos <= N; pos += blockDim.x) cp_async16(sm + pidx(pos), a0 + pos);
-    cp_async_wait_all();
-  }
-  __syncthreads();
-  for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-    const PairEntry e = work[w];
-    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
-                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
-    first_pass_inv<R0, true, BREAL>(sm, tws, pa, nullptr, b, BREAL);
-    __syncthreads();
-    static_pass<R1, L1, N, 1>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
-    __syncthreads();
-    static_pass<R2, L2, N, 1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
-    __syncthreads();
-    double* o0 = out + e.out0;
-    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
-    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
-    const int wn = w + gridDim.x;
-    const double2* a_next = wn < nwork ? specA + static_cast<int64_t>(work[wn].ia) * (N + 1) : nullptr;
-    static_last_pipe<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned, a_next);
-    cp_async_wait_all();
-    __syncthreads();
-  }
-}
-
-template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
-__global__ void __launch_bounds__(TT, 1)
-    pair_kernel_static(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
-                       const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
+__device__ __forceinline__ void pair_body_static(const PlanArgs& pa, const double2* __restrict__ specA,
+                                                 const void* __restrict__ specB, const PairEntry* __restrict__ work,
+                                                 int nwork, double* __restrict__ out) {
   constexpr int N = R0 * R1 * R2 * R3;
   constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
   extern __shared__ double2 sm[];
@@ -1184,6 +1157,17 @@ __global__ void __launch_bounds__(TT, 1)
   }
 }
 
+// Launched once per form of the kernel-column spectra; the instance whose
+// form disagrees with the device-side symmetry flag exits at once (a
+// single-path kernel keeps its register allocation spill-free).
+template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    pair_kernel_static(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
+             const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out) {
+  if ((winfo[1] != 0) != BREAL) return;
+  pair_body_static<R0, R1, R2, R3, TT, BREAL>(pa, specA, specB, work, winfo[0], out);
+}
+
 // ---- TMEM-resident density spectra.  The staging of A*B is bound by the
 // SM's L2 read rate (~30-50 B/clk measured, v15), and A is 2/3 of those bytes.
 // A CTA takes a CONTIGUOUS, i-major run of the work list, so consecutive pairs
@@ -1215,10 +1199,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// Launched once per form of the kernel-column spectra; the instance whose
+// form disagrees with the device-side symmetry flag exits at once (a
+// single-path kernel keeps its register allocation spill-free).
 template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
 __global__ void __launch_bounds__(TT, 1)
     pair_kernel_tmem(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
-                     const PairEntry* __restrict__ work, int nwork, double* __restrict__ out) {
+                     const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out) {
+  if ((winfo[1] != 0) != BREAL) return;
+  const int nwork = winfo[0];
   constexpr int N = R0 * R1 * R2 * R3;
   constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
   constexpr int K = N / TT;  // staged positions per thread
@@ -1333,10 +1322,116 @@ __global__ void __launch_bounds__(TT, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh) : "memory");
 }
 
+
+// Forward spectra with a compile-time plan: static passes (hoisted twiddles
+// where TT % L == 0), then the real post-processing iterated in STORAGE order
+// so the spectrum stores are coalesced; the phase factors of modes 1/2 come
+// from per-plan tables instead of sincospi.
+template <int R0, int R1, int R2, int R3, int TT>
+__global__ void __launch_bounds__(TT, 1)
+    spectrum_kernel_static(PlanArgs pa, const double* __restrict__ XA, int nA, void* __restrict__ specA,
+                           const double* __restrict__ XB, const int* __restrict__ colidx, int nB,
+                           void* __restrict__ specB, void* __restrict__ specB2, int modeB, int64_t ldx, double h) {
+  constexpr int N = R0 * R1 * R2 * R3;
+  constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
+  extern __shared__ double2 sm[];
+  const double2* tws = load_tables(sm, pa);
+  const bool isA = static_cast<int>(blockIdx.x) >= nB;  // kernel columns first (they carry the extra work)
+  const int c = isA ? blockIdx.x - nB : blockIdx.x;
+  const int mode = isA ? 0 : modeB;
+  const double* x = isA ? XA + c * ldx : XB + (colidx ? colidx[c] : c) * ldx;
+  const int n = pa.n;
+  long long c0 = pa.phase ? clock64() : 0;
+  static_assert(N % (8 * TT) == 0, "whole batches");
+#pragma unroll 1
+  for (int k0 = threadIdx.x; k0 < N; k0 += 8 * TT) {  // 8-deep batched loads
+    double2 v[8];
+    int p[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i0 = 2 * (k0 + u * TT);
+      v[u].x = i0 < n ? __ldg(x + i0) : 0.0;
+      v[u].y = i0 + 1 < n ? __ldg(x + i0 + 1) : 0.0;
+      p[u] = __ldg(pa.inv + k0 + u * TT);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) sm[pidx(p[u])] = v[u];
+  }
+  __syncthreads();
+  long long c1 = pa.phase ? clock64() : 0;
+  static_pass<R0, 1, N, -1>(sm, tws, tws);
+  __syncthreads();
+  static_pass_t<R1, L1, N, -1, TT>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
+  __syncthreads();
+  static_pass_t<R2, L2, N, -1, TT>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+  __syncthreads();
+  static_pass<R3, L3, N, -1>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3]);
+  __syncthreads();
+  long long c2 = pa.phase ? clock64() : 0;
+  const double hm = h / pa.m;
+  const int64_t base = static_cast<int64_t>(c) * (N + 1);
+  // (1) real post-processing in natural order, one mirror pair (k, N-k) per
+  // thread, results in place: X[N-k] = conj-mirror of the X[k] terms (one
+  // twiddle per pair); k = 0 also produces the Nyquist term into slot N.
+  for (int k = threadIdx.x; k <= N / 2; k += TT) {
+    const double2 zk = sm[pidx(k)];
+    double2 zm = sm[pidx(k == 0 ? 0 : N - k)];
+    zm.y = -zm.y;
+    const double2 sum = cadd(zk, zm), dif = csub(zk, zm);
+    double2 w = ld2(pa.twpost + k);
+    w.y = -w.y;  // w^-k
+    const double2 wd = cmul(w, dif);
+    double2 xk = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
+    double2 xm;
+    if (k == 0) {  // Nyquist: w^-N = -1
+      xm = make_double2(0.5 * (sum.x - dif.y), 0.5 * (sum.y + dif.x));
+    } else {
+      xm = make_double2(0.5 * (sum.x - wd.y), 0.5 * (-sum.y - wd.x));
+    }
+    const int km = N - k;
+    if (mode == 1) {
+      const double2 t = ld2(pa.ph1 + k), tm = ld2(pa.ph1 + km);
+      xk = make_double2(hm * (xk.x * t.x - xk.y * t.y), 0.0);
+      xm = make_double2(hm * (xm.x * tm.x - xm.y * tm.y), 0.0);
+    } else if (mode == 2) {
+      xk = cmul(xk, cscale(ld2(pa.ph2 + k), hm));
+      xm = cmul(xm, cscale(ld2(pa.ph2 + km), hm));
+    }
+    sm[pidx(k)] = xk;
+    if (k != N / 2 || k == 0) sm[pidx(k == 0 ? N : km)] = xm;
+  }
+  __syncthreads();
+  // (2) storage order: coalesced spectrum stores
+  for (int pos = threadIdx.x; pos <= N; pos += TT) {
+    const int k = pos < N ? __ldg(pa.perm + pos) : N;
+    const double2 v = sm[pidx(k)];
+    if (mode == 1) {
+      static_cast<double*>(specB)[base + pos] = v.x;
+    } else if (mode == 3) {  // raw X in smem: both forms (symmetry decided later on the host)
+      const double2 t = ld2(pa.ph1 + k);
+      static_cast<double*>(specB)[base + pos] = hm * (v.x * t.x - v.y * t.y);
+      static_cast<double2*>(specB2)[base + pos] = cmul(v, cscale(ld2(pa.ph2 + k), hm));
+    } else {
+      static_cast<double2*>(isA ? specA : specB)[base + pos] = v;
+    }
+  }
+  if (pa.phase) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const long long c3 = clock64();
+      atomicAdd(pa.phase + 8, static_cast<unsigned long long>(c1 - c0));
+      atomicAdd(pa.phase + 9, static_cast<unsigned long long>(c2 - c1));
+      atomicAdd(pa.phase + 10, static_cast<unsigned long long>(c3 - c2));
+      atomicAdd(pa.phase + 11, 1ULL);
+    }
+  }
+}
+
 // Direct windowed convolution (small n, or n beyond the single-CTA FFT).
 __global__ void direct_conv_kernel(int n, int ofs, int even, const double* __restrict__ U, int64_t ldu,
                                    const double* __restrict__ V, int64_t ldv, const PairEntry* __restrict__ work,
-                                   double scale, double* __restrict__ out) {
+                                   const int* __restrict__ winfo, double scale, double* __restrict__ out) {
+  if (static_cast<int>(blockIdx.x) >= winfo[0]) return;  // grid sized for the ungrouped worst case
   const PairEntry e = work[blockIdx.x];
   const double* u = U + e.ia * ldu;
   const double* v = V + e.jb * ldv;
@@ -1383,6 +1478,62 @@ __global__ void dup_columns_kernel(const double* __restrict__ B, int64_t n, int 
   if (threadIdx.x == 0) flags[j * rb + j2] = static_cast<unsigned char>(same);
 }
 
+// Device-side grouping of the kernel columns (one CTA per axis) from the
+// dup/symmetry flags, and the i-major pair work list: for each density
+// column i, one entry per pair of identical kernel columns (the entry's
+// result is stored to both).  winfo = {entries, all columns symmetric}.
+__global__ void build_work_kernel(const unsigned char* __restrict__ f, int rb, int64_t ra, int64_t n,
+                                  PairEntry* __restrict__ w, int* __restrict__ winfo) {
+  extern __shared__ int wsh[];  // members[rb], gstart[rb + 1], pg[rb], pq[rb]
+  int* members = wsh;
+  int* gstart = members + rb;
+  int* pg = gstart + rb + 1;
+  int* pq = pg + rb;
+  __shared__ int s_np;
+  if (threadIdx.x == 0) {
+    int* rep = pg;  // scratch before the pair map is built
+    for (int j = 0; j < rb; ++j) rep[j] = -1;
+    int ng = 0, nm = 0, sym = 1;
+    for (int j = 0; j < rb; ++j) {
+      if (rep[j] >= 0) continue;
+      gstart[ng] = nm;
+      rep[j] = ng;
+      members[nm++] = j;
+      sym &= f[j * rb + j];
+      for (int j2 = j + 1; j2 < rb; ++j2)
+        if (rep[j2] < 0 && f[j * rb + j2]) {
+          rep[j2] = ng;
+          members[nm++] = j2;
+        }
+      ++ng;
+    }
+    gstart[ng] = nm;
+    int np = 0;
+    for (int g = 0; g < ng; ++g)
+      for (int q = gstart[g]; q < gstart[g + 1]; q += 2) {
+        pg[np] = g;
+        pq[np] = q;
+        ++np;
+      }
+    s_np = np;
+    winfo[0] = static_cast<int>(ra * np);
+    winfo[1] = sym;
+  }
+  __syncthreads();
+  const int np = s_np;
+  for (int64_t idx = threadIdx.x; idx < ra * np; idx += blockDim.x) {
+    const int64_t i = idx / np;
+    const int r = static_cast<int>(idx - i * np);
+    const int g = pg[r], q = pq[r];
+    PairEntry e;
+    e.ia = static_cast<int>(i);
+    e.jb = members[gstart[g]];
+    e.out0 = (i + ra * members[q]) * n;
+    e.out1 = q + 1 < gstart[g + 1] ? (i + ra * members[q + 1]) * n : -1;
+    w[idx] = e;
+  }
+}
+
 __global__ void weights_outer_kernel(int64_t ra, const double* __restrict__ wa, int64_t rb,
                                      const double* __restrict__ wb, double scale, int use_scale, double* out) {
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -1406,7 +1557,7 @@ void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const
 
 template <int R0, bool BREAL>
 static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
-                        const PairEntry* dwork, int nwork, double* out) {
+                        const PairEntry* dwork, const int* winfo, double* out) {
   static bool attr = false;
   if (!attr) {
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel<R0, BREAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1415,23 +1566,21 @@ static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, 
   }
   int per_sm = 1;
   TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel<R0, BREAL>, pl.threads, pl.smem));
-  const int grid = std::max(1, std::min(nwork, std::max(1, per_sm) * ctx->num_sms));
+  const int grid = std::max(1, per_sm) * ctx->num_sms;
   prof_begin(ctx);
-  pair_kernel<R0, BREAL><<<grid, pl.threads, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, nwork, out);
+  pair_kernel<R0, BREAL><<<grid, pl.threads, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);
   TGB_LAUNCHED(ctx);
   prof_end(ctx);
 }
 
 template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
 static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
-                       const PairEntry* dwork, int nwork, double* out) {
+                       const PairEntry* dwork, const int* winfo, double* out) {
   const PlanArgs& a = pl.a;
   if (!(a.P == 4 && a.r[0] == R0 && a.r[1] == R1 && a.r[2] == R2 && a.r[3] == R3) || a.dbg || getenv("TGB_NO_STATIC"))
     return false;
-  // the cp.async-pipelined variant measured slower (2.02 vs 1.68 ms/axis, v8); opt-in only
-  auto kern = getenv("TGB_PIPE") ? pair_kernel_pipe<R0, R1, R2, R3, TT, BREAL>
-              : (getenv("TGB_NO_TMEM") || a.N % TT) ? pair_kernel_static<R0, R1, R2, R3, TT, BREAL>
-                                                    : pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>;
+  auto kern = (getenv("TGB_NO_TMEM") || a.N % TT) ? pair_kernel_static<R0, R1, R2, R3, TT, BREAL>
+                                                  : pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>;
   static bool attr = false;
   if (!attr) {
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel_static<R0, R1, R2, R3, TT, BREAL>,
@@ -1441,8 +1590,6 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
-    TGB_CUDA(cudaFuncSetAttribute(pair_kernel_pipe<R0, R1, R2, R3, TT, BREAL>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
     attr = true;
   }
   int per_sm = 1;
@@ -1451,44 +1598,46 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
     kern = pair_kernel_static<R0, R1, R2, R3, TT, BREAL>;
     TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, pl.smem));
   }
-  const int grid = std::max(1, std::min(nwork, std::max(1, per_sm) * ctx->num_sms));
+  const int grid = std::max(1, per_sm) * ctx->num_sms;
   prof_begin(ctx);
-  kern<<<grid, TT, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, nwork, out);
+  kern<<<grid, TT, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);
   TGB_LAUNCHED(ctx);
   prof_end(ctx);
   if (a.phase) {  // analysis only: cumulative per-phase cycles (summed over CTAs) per pair
     unsigned long long h[8];
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-    TGB_CUDA(cudaMemcpy(h, a.phase, sizeof(h), cudaMemcpyDeviceToHost));
+    TGB_CUDA(cudaMemcpy(h, a.phase, sizeof(h), cudaMemcpyDeviceToHost));  // first 8 slots
     const double np = static_cast<double>(h[5] ? h[5] : 1);
     fprintf(stderr, "phase cycles/pair: stage %.0f pass0 %.0f pass1 %.0f pass2 %.0f last %.0f (pairs %llu)\n",
             h[0] / np, h[1] / np, h[2] / np, h[3] / np, h[4] / np, h[5]);
-    TGB_CUDA(cudaMemset(a.phase, 0, sizeof(h)));
+    TGB_CUDA(cudaMemset(a.phase, 0, sizeof(h)));  // pair slots only
   }
   return true;
 }
 
 template <bool BREAL>
 static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
-                          const PairEntry* dwork, int nwork, double* out) {
+                          const PairEntry* dwork, const int* winfo, double* out) {
   // compile-time plans (config 2: n = 16385 -> N = 12800)
-  if (try_static<10, 20, 8, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, nwork, out)) return;
-  if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, nwork, out)) return;
+  if (try_static<10, 20, 8, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
+  if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
   switch (pl.a.r[0]) {
-    case 2: launch_pair<2, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
-    case 3: launch_pair<3, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
-    case 4: launch_pair<4, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
-    case 5: launch_pair<5, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
-    case 6: launch_pair<6, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
-    case 8: launch_pair<8, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
-    case 10: launch_pair<10, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
-    case 16: launch_pair<16, BREAL>(ctx, pl, specA, specB, dwork, nwork, out); break;
+    case 2: launch_pair<2, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 3: launch_pair<3, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 4: launch_pair<4, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 5: launch_pair<5, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 6: launch_pair<6, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 8: launch_pair<8, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 10: launch_pair<10, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 16: launch_pair<16, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
     default: throw Error(TGB_CUDA_ERROR, "fftconv: unsupported first radix");
   }
 }
 
+// One launch: nB kernel columns (CTAs [0, nB), mode modeB; colidx == nullptr:
+// columns 0..nB-1) and nA density columns (mode 0).
 static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, int nA, void* specA, const double* B,
-                            const int* colidx, int nB, void* specB, int modeB, int64_t ldx, double h) {
+                            const int* colidx, int nB, void* specB, void* specB2, int modeB, int64_t ldx, double h) {
   if (nA + nB == 0) return;
   static bool attr_set = false;
   if (!attr_set) {
@@ -1496,135 +1645,96 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
                                   static_cast<int>(ctx->smem_optin)));
     attr_set = true;
   }
-  spectrum_kernel<<<nA + nB, pl.threads, pl.smem, ctx->stream>>>(pl.a, A, nA, specA, B, colidx, specB, modeB, ldx, h);
+  const PlanArgs& a = pl.a;
+  if (a.P == 4 && a.r[0] == 16 && a.r[1] == 10 && a.r[2] == 10 && a.r[3] == 8 && !getenv("TGB_NO_STATIC")) {
+    static bool attr2 = false;
+    if (!attr2) {
+      TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel_static<16, 10, 10, 8, 320>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+      attr2 = true;
+    }
+    spectrum_kernel_static<16, 10, 10, 8, 320><<<nA + nB, 320, pl.smem, ctx->stream>>>(
+        pl.a, A, nA, specA, B, colidx, nB, specB, specB2, modeB, ldx, h);
+    TGB_LAUNCHED(ctx);
+    if (a.phase) {
+      unsigned long long hb[16];
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      TGB_CUDA(cudaMemcpy(hb, a.phase, sizeof(hb), cudaMemcpyDeviceToHost));
+      const double nc = static_cast<double>(hb[11] ? hb[11] : 1);
+      fprintf(stderr, "spectrum cycles/column: input %.0f passes %.0f post %.0f (columns %llu)\n", hb[8] / nc,
+              hb[9] / nc, hb[10] / nc, hb[11]);
+      TGB_CUDA(cudaMemset(a.phase + 8, 0, 8 * sizeof(unsigned long long)));
+    }
+    return;
+  }
+  spectrum_kernel<<<nA + nB, pl.threads, pl.smem, ctx->stream>>>(pl.a, A, nA, specA, B, colidx, nB, specB, specB2,
+                                                                  modeB, ldx, h);
   TGB_LAUNCHED(ctx);
 }
 
-struct ColumnGroups {
-  std::vector<std::vector<int>> groups;  // bitwise-identical columns, representative first
-  bool all_symmetric = true;
-};
-
-// Bitwise-identical / mirror-symmetric kernel columns of every axis, with ONE
-// device->host synchronisation for all axes.
-static std::vector<ColumnGroups> group_columns(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t rb,
-                                               const double* const* B) {
-  std::vector<ColumnGroups> out(naxes);
-  if (rb == 0) return out;
-  const int64_t nblocks = rb + rb * (rb - 1) / 2;
-  auto* flags = static_cast<unsigned char*>(ctx->ws_flags.get(naxes * rb * rb));
-  for (int ax = 0; ax < naxes; ++ax) {
-    dup_columns_kernel<<<static_cast<unsigned>(nblocks), 256, 0, ctx->stream>>>(B[ax], n[ax], static_cast<int>(rb),
-                                                                               flags + ax * rb * rb);
-    TGB_LAUNCHED(ctx);
-  }
-  std::vector<unsigned char> h(naxes * rb * rb, 0);
-  TGB_CUDA(cudaMemcpyAsync(h.data(), flags, h.size(), cudaMemcpyDeviceToHost, ctx->stream));
-  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-  for (int ax = 0; ax < naxes; ++ax) {
-    ColumnGroups& cg = out[ax];
-    const unsigned char* f = h.data() + ax * rb * rb;
-    std::vector<int> rep(rb, -1);
-    for (int j = 0; j < rb; ++j) {
-      if (rep[j] >= 0) continue;
-      rep[j] = static_cast<int>(cg.groups.size());
-      cg.groups.push_back({j});
-      cg.all_symmetric = cg.all_symmetric && f[j * rb + j];
-      for (int j2 = j + 1; j2 < rb; ++j2)
-        if (rep[j2] < 0 && f[j * rb + j2]) {
-          rep[j2] = rep[j];
-          cg.groups.back().push_back(j2);
-        }
-    }
-  }
-  return out;
-}
-
-// Pinned host staging for the per-call work lists, so their uploads are truly
-// asynchronous (a pageable cudaMemcpyAsync would synchronise the stream).
-static void* pinned_staging(tgb_ctx* ctx, size_t bytes) {
-  if (ctx->pinned_event) TGB_CUDA(cudaEventSynchronize(ctx->pinned_event));  // previous uploads done
-  if (bytes > ctx->pinned_bytes) {
-    if (ctx->pinned) cudaFreeHost(ctx->pinned);
-    ctx->pinned = nullptr;
-    TGB_CUDA(cudaHostAlloc(&ctx->pinned, bytes, cudaHostAllocDefault));
-    ctx->pinned_bytes = bytes;
-  }
-  return ctx->pinned;
-}
-
 // out[ax] (n x ra*rb, column i + ra*j) = h[ax] * window(conv(A_i, B_j)) for
-// naxes axes; device pointers, stream-ordered, one host sync in total.
+// naxes axes; device pointers, stream-ordered, no host synchronisation.
+// The kernel columns' duplicate/symmetry flags and the pair work lists are
+// built on the device (aux stream, overlapping the first spectra); every
+// kernel column's spectrum is formed in both the real and the complex form,
+// and each pair kernel picks one from the device-side symmetry flag.
 void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const double* const* A, int64_t rb,
                    const double* const* B, const double* h, double* const* out) {
   if (ra == 0 || rb == 0 || naxes == 0) return;
-  const std::vector<ColumnGroups> cgs = group_columns(ctx, naxes, n, rb, B);
-  // work lists (i-major: concurrently running CTAs share A_i and every B_j in L2)
-  std::vector<std::vector<PairEntry>> works(naxes);
-  std::vector<std::vector<int>> reps(naxes);
-  size_t total_entries = 0, total_reps = 0;
   std::vector<std::shared_ptr<ConvPlan>> plans(naxes);
-  for (int ax = 0; ax < naxes; ++ax) {
-    plans[ax] = get_plan(ctx, n[ax]);
-    const auto& groups = cgs[ax].groups;
-    auto& work = works[ax];
-    work.reserve(static_cast<size_t>(ra * groups.size()));
-    for (int64_t i = 0; i < ra; ++i)
-      for (size_t g = 0; g < groups.size(); ++g) {
-        const auto& mem = groups[g];
-        for (size_t q = 0; q < mem.size(); q += 2) {
-          PairEntry e;
-          e.ia = static_cast<int>(i);
-          e.jb = plans[ax]->direct ? mem[0] : static_cast<int>(g);
-          e.out0 = (i + ra * mem[q]) * n[ax];
-          e.out1 = q + 1 < mem.size() ? (i + ra * mem[q + 1]) * n[ax] : -1;
-          work.push_back(e);
-        }
-      }
-    for (auto& g : groups) reps[ax].push_back(g[0]);
-    total_entries += work.size();
-    total_reps += reps[ax].size();
-  }
-  const size_t wbytes = total_entries * sizeof(PairEntry), rbytes = total_reps * sizeof(int);
-  auto* host = static_cast<char*>(pinned_staging(ctx, wbytes + rbytes + 64));
-  auto* dbuf = static_cast<char*>(ctx->ws_pairs.get(wbytes + rbytes + 64));
+  for (int ax = 0; ax < naxes; ++ax) plans[ax] = get_plan(ctx, n[ax]);
+  // ---- aux stream: flags -> groups -> work lists
+  const int64_t nblocks = rb + rb * (rb - 1) / 2;
+  const size_t fbytes = (static_cast<size_t>(naxes * rb * rb) + 255) & ~size_t(255);
+  const size_t wentries = static_cast<size_t>(ra * rb);
+  char* wsp = static_cast<char*>(
+      ctx->ws_pairs.get(fbytes + naxes * (wentries * sizeof(PairEntry) + 256) + 256));
+  auto* flags = reinterpret_cast<unsigned char*>(wsp);
+  auto* winfo = reinterpret_cast<int*>(wsp + fbytes);  // 2 ints per axis
+  char* wlist = wsp + fbytes + 256;
+  TGB_CUDA(cudaEventRecord(ctx->aux_in, ctx->stream));  // B is ready in stream order
+  TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
+  const size_t wsmem = static_cast<size_t>(4 * rb + 1) * sizeof(int);
+  if (wsmem > 48 * 1024) throw Error(TGB_INVALID_ARGUMENT, "convolve: kernel rank too large for the work builder");
   std::vector<PairEntry*> dwork(naxes);
-  std::vector<int*> dreps(naxes);
-  size_t off = 0;
   for (int ax = 0; ax < naxes; ++ax) {
-    std::memcpy(host + off, works[ax].data(), works[ax].size() * sizeof(PairEntry));
-    dwork[ax] = reinterpret_cast<PairEntry*>(dbuf + off);
-    off += works[ax].size() * sizeof(PairEntry);
+    unsigned char* f = flags + ax * rb * rb;
+    dwork[ax] = reinterpret_cast<PairEntry*>(wlist + ax * (wentries * sizeof(PairEntry) + 256));
+    dup_columns_kernel<<<static_cast<unsigned>(nblocks), 256, 0, ctx->aux_stream>>>(B[ax], n[ax],
+                                                                                   static_cast<int>(rb), f);
+    TGB_LAUNCHED(ctx);
+    build_work_kernel<<<1, 256, wsmem, ctx->aux_stream>>>(f, static_cast<int>(rb), ra, n[ax], dwork[ax],
+                                                         winfo + 2 * ax);
+    TGB_LAUNCHED(ctx);
   }
-  for (int ax = 0; ax < naxes; ++ax) {
-    std::memcpy(host + off, reps[ax].data(), reps[ax].size() * sizeof(int));
-    dreps[ax] = reinterpret_cast<int*>(dbuf + off);
-    off += reps[ax].size() * sizeof(int);
-  }
-  TGB_CUDA(cudaMemcpyAsync(dbuf, host, off, cudaMemcpyHostToDevice, ctx->stream));
-  if (!ctx->pinned_event) TGB_CUDA(cudaEventCreateWithFlags(&ctx->pinned_event, cudaEventDisableTiming));
-  TGB_CUDA(cudaEventRecord(ctx->pinned_event, ctx->stream));
+  TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
+  // ---- main stream: spectra (independent of the grouping), then the pairs
+  bool joined = false;
   for (int ax = 0; ax < naxes; ++ax) {
     const ConvPlan& pl = *plans[ax];
-    const int nw = static_cast<int>(works[ax].size());
     if (pl.direct) {
+      if (!joined) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
+      joined = true;
       const int th = static_cast<int>(std::min<int64_t>(256, ((n[ax] + 31) / 32) * 32));
-      direct_conv_kernel<<<static_cast<unsigned>(nw), th, 0, ctx->stream>>>(
-          static_cast<int>(n[ax]), pl.a.ofs, pl.a.even, A[ax], n[ax], B[ax], n[ax], dwork[ax], h[ax], out[ax]);
+      direct_conv_kernel<<<static_cast<unsigned>(wentries), th, 0, ctx->stream>>>(
+          static_cast<int>(n[ax]), pl.a.ofs, pl.a.even, A[ax], n[ax], B[ax], n[ax], dwork[ax], winfo + 2 * ax,
+          h[ax], out[ax]);
       TGB_LAUNCHED(ctx);
       continue;
     }
-    const int N = pl.a.N;
-    const bool breal = cgs[ax].all_symmetric;
-    const size_t nd = reps[ax].size();
-    auto* specA = static_cast<double2*>(ctx->ws_spec_a.get(static_cast<size_t>(ra) * (N + 1) * sizeof(double2)));
-    void* specB = ctx->ws_spec_b.get(nd * (N + 1) * (breal ? sizeof(double) : sizeof(double2)));
-    launch_spectrum(ctx, pl, A[ax], static_cast<int>(ra), specA, B[ax], dreps[ax], static_cast<int>(nd), specB,
-                    breal ? 1 : 2, n[ax], h[ax]);
-    if (breal)
-      launch_pair_r<true>(ctx, pl, specA, specB, dwork[ax], nw, out[ax]);
-    else
-      launch_pair_r<false>(ctx, pl, specA, specB, dwork[ax], nw, out[ax]);
+    const size_t N1 = static_cast<size_t>(pl.a.N) + 1;
+    void* specA = ctx->ws_spec_a.get(static_cast<size_t>(ra) * N1 * sizeof(double2));
+    const size_t real_bytes = (static_cast<size_t>(rb) * N1 * sizeof(double) + 255) & ~size_t(255);
+    char* sb = static_cast<char*>(ctx->ws_spec_b.get(real_bytes + static_cast<size_t>(rb) * N1 * sizeof(double2)));
+    void* specBr = sb;
+    void* specBc = sb + real_bytes;  // 16-byte aligned complex spectra
+    launch_spectrum(ctx, pl, A[ax], static_cast<int>(ra), specA, B[ax], nullptr, static_cast<int>(rb), specBr,
+                    specBc, 3, n[ax], h[ax]);
+    if (!joined) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
+    joined = true;
+    // both forms; the one that disagrees with the device-side symmetry flag returns at once
+    launch_pair_r<true>(ctx, pl, static_cast<const double2*>(specA), specBr, dwork[ax], winfo + 2 * ax, out[ax]);
+    launch_pair_r<false>(ctx, pl, static_cast<const double2*>(specA), specBc, dwork[ax], winfo + 2 * ax, out[ax]);
   }
 }
 

@@ -86,6 +86,10 @@ struct tgb_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;
+  cudaStream_t aux_stream = nullptr;  // kernel-column grouping, overlapped with the spectra
+  cudaEvent_t aux_in = nullptr, aux_done = nullptr;
+  void* pinned_flags = nullptr;
+  size_t pinned_flags_bytes = 0;
   bool own_stream = false;
   int64_t launches = 0;
   int64_t direct_max = 64;
