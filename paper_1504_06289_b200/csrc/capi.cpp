@@ -191,6 +191,7 @@ int tgb_ctx_destroy(tgb_ctx* ctx) {
     cudaEventDestroy(ctx->aux_in);
     cudaEventDestroy(ctx->aux_done);
     if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
+    for (auto& kv : ctx->scratch_free) cudaFree(kv.second);
     if (ctx->pinned_event) cudaEventDestroy(ctx->pinned_event);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto& pe : ctx->prof_events) {

@@ -11,6 +11,9 @@
 // double buffering of the global loads.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "tgb_internal.hpp"
 
 namespace tgb {
@@ -26,14 +29,20 @@ __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1,
                : "d"(a0), "d"(a1), "d"(b0));
 }
 
+// Split-K: blockIdx.z covers K range [z kchunk, (z+1) kchunk); with
+// gridDim.z > 1 the raw partial tile goes to P[z] (M x N, ld M) and
+// splitk_reduce_kernel sums the slices in order (deterministic).
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K, double alpha,
+__global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K, int kchunk, double alpha,
                                                              const double* __restrict__ A, int64_t lda,
                                                              const double* __restrict__ B, int64_t ldb, double beta,
-                                                             double* __restrict__ C, int64_t ldc) {
+                                                             double* __restrict__ C, int64_t ldc,
+                                                             double* __restrict__ P) {
   __shared__ double As[2][BK][LDS_];
   __shared__ double Bs[2][BK][LDS_];
   const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kb0 = blockIdx.z * kchunk;
+  const int kend = min(K, kb0 + kchunk);
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
   const int g = lane >> 2, t = lane & 3;
@@ -53,7 +62,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
         mm = idx / BK;
       }
       const int gm = m0 + mm, gk = k0 + kk;
-      ra[e] = (gm < M && gk < K) ? (TA ? __ldg(A + gk + lda * gm) : __ldg(A + gm + lda * gk)) : 0.0;
+      ra[e] = (gm < M && gk < kend) ? (TA ? __ldg(A + gk + lda * gm) : __ldg(A + gm + lda * gk)) : 0.0;
       int nn, kb;
       if (!TB) {  // B (k, n) at B[k + ldb n]: k fastest
         kb = idx % BK;
@@ -63,7 +72,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
         kb = idx / BN;
       }
       const int gn = n0 + nn, gk2 = k0 + kb;
-      rb[e] = (gn < N && gk2 < K) ? (TB ? __ldg(B + gn + ldb * gk2) : __ldg(B + gk2 + ldb * gn)) : 0.0;
+      rb[e] = (gn < N && gk2 < kend) ? (TB ? __ldg(B + gn + ldb * gk2) : __ldg(B + gk2 + ldb * gn)) : 0.0;
     }
   };
   auto store_tile = [&](int buf) {
@@ -99,13 +108,13 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
 #pragma unroll
       for (int r = 0; r < 4; ++r) acc[i][j][r] = 0.0;
 
-  const int nk = (K + BK - 1) / BK;
-  load_tile(0);
+  const int nk = (kend - kb0 + BK - 1) / BK;
+  load_tile(kb0);
   store_tile(0);
   __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
     const int buf = kt & 1;
-    if (kt + 1 < nk) load_tile((kt + 1) * BK);
+    if (kt + 1 < nk) load_tile(kb0 + (kt + 1) * BK);
 #pragma unroll
     for (int k4 = 0; k4 < BK; k4 += 4) {
       double a[2][2], b[4];
@@ -134,10 +143,27 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
         const int row = m0 + wm + 16 * i + g + (r >= 2 ? 8 : 0);
         const int col = n0 + wn + 8 * j + 2 * t + (r & 1);
         if (row < M && col < N) {
-          double* cp = C + row + ldc * col;
-          *cp = beta == 0.0 ? alpha * acc[i][j][r] : alpha * acc[i][j][r] + beta * *cp;
+          if (P) {
+            P[static_cast<int64_t>(blockIdx.z) * M * N + row + static_cast<int64_t>(M) * col] = acc[i][j][r];
+          } else {
+            double* cp = C + row + ldc * col;
+            *cp = beta == 0.0 ? alpha * acc[i][j][r] : alpha * acc[i][j][r] + beta * *cp;
+          }
         }
       }
+}
+
+__global__ void splitk_reduce_kernel(int M, int N, int S, double alpha, const double* __restrict__ P, double beta,
+                                    double* __restrict__ C, int64_t ldc) {
+  const int64_t MN = static_cast<int64_t>(M) * N;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < MN;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < S; ++z) s += P[z * MN + e];
+    const int64_t row = e % M, col = e / M;
+    double* cp = C + row + ldc * col;
+    *cp = beta == 0.0 ? alpha * s : alpha * s + beta * *cp;
+  }
 }
 
 }  // namespace
@@ -145,13 +171,30 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
 void dgemm(tgb_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc) {
   if (M <= 0 || N <= 0) return;
-  dim3 grid(static_cast<unsigned>((M + BM - 1) / BM), static_cast<unsigned>((N + BN - 1) / BN));
+  const int64_t gm = (M + BM - 1) / BM, gn = (N + BN - 1) / BN, tiles = gm * gn;
+  // split K when the output tiles cannot fill the SMs and K is long
+  int splits = 1;
+  if (tiles < ctx->num_sms && K >= 1024 && !getenv("TGB_NO_SPLITK")) {
+    splits = static_cast<int>(std::min<int64_t>({(2 * ctx->num_sms + tiles - 1) / tiles, K / 512, 32}));
+    splits = std::max(splits, 1);
+  }
+  const int kchunk = static_cast<int>(((K + splits - 1) / splits + BK - 1) / BK * BK);
+  splits = static_cast<int>((K + kchunk - 1) / kchunk);
+  double* P = nullptr;
+  if (splits > 1) P = static_cast<double*>(ctx->ws_gemm.get(static_cast<size_t>(splits) * M * N * sizeof(double)));
+  dim3 grid(static_cast<unsigned>(gm), static_cast<unsigned>(gn), static_cast<unsigned>(splits));
   const int m = static_cast<int>(M), n = static_cast<int>(N), k = static_cast<int>(K);
-  if (!ta && !tb) dgemm_kernel<false, false><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-  if (!ta && tb) dgemm_kernel<false, true><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-  if (ta && !tb) dgemm_kernel<true, false><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
-  if (ta && tb) dgemm_kernel<true, true><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, alpha, A, lda, B, ldb, beta, C, ldc);
+  if (!ta && !tb) dgemm_kernel<false, false><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, P);
+  if (!ta && tb) dgemm_kernel<false, true><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, P);
+  if (ta && !tb) dgemm_kernel<true, false><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, P);
+  if (ta && tb) dgemm_kernel<true, true><<<grid, GEMM_THREADS, 0, ctx->stream>>>(m, n, k, kchunk, alpha, A, lda, B, ldb, beta, C, ldc, P);
   TGB_LAUNCHED(ctx);
+  if (splits > 1) {
+    const int64_t MN = M * N;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((MN + 255) / 256, 4 * ctx->num_sms));
+    splitk_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(m, n, splits, alpha, P, beta, C, ldc);
+    TGB_LAUNCHED(ctx);
+  }
 }
 
 }  // namespace tgb

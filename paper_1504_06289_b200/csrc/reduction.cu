@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -205,6 +206,84 @@ __global__ void chol_inv_kernel(int p, double* __restrict__ H, double* __restric
   }
 }
 
+// Same factorisation for p <= kCholSmem with L in shared memory: right-looking
+// Cholesky (one barrier pair per column), then R^{-1} = (L^{-1})^T by forward
+// substitution, one thread per column of L^{-1} (= row of R^{-1}); the
+// retired-column rule is the global-memory version's.
+constexpr int kCholSmem = 128;
+constexpr int kCholSmemBytes = 200 * 1024;  // L (+ L^{-1} when 2 p^2 doubles fit)
+__global__ void __launch_bounds__(256) chol_inv_smem_kernel(int p, double* __restrict__ H) {
+  extern __shared__ double Ls[];  // p x p, column-major; then X = L^{-1} (p x p) when it fits
+  __shared__ double s_mx;
+  __shared__ unsigned char dead[kCholSmem];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) Ls[idx] = H[idx];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double mx = 0.0;
+    for (int i = threadIdx.x; i < p; i += 32) mx = fmax(mx, Ls[i + p * i]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) s_mx = mx;
+  }
+  __syncthreads();
+  const double tiny = 1e-26 * s_mx;
+  for (int j = 0; j < p; ++j) {
+    __syncthreads();                 // previous trailing update complete
+    const double d = Ls[j + p * j];  // every thread reads the pivot
+    const bool dj = !(d > tiny);
+    const double djj = dj ? 1.0 : sqrt(d);
+    const double inv = 1.0 / djj;
+    for (int i = j + 1 + threadIdx.x; i < p; i += blockDim.x) Ls[i + p * j] = dj ? 0.0 : Ls[i + p * j] * inv;
+    __syncthreads();  // column j scaled; the pivot slot is rewritten only after every read of it
+    if (threadIdx.x == 0) {
+      dead[j] = dj;
+      Ls[j + p * j] = djj;
+    }
+    if (!dj) {  // trailing update, column k per warp, rows i >= k per lane
+      for (int k = j + 1 + warp; k < p; k += nw) {
+        const double lkj = Ls[k + p * j];
+        for (int i = k + lane; i < p; i += 32) Ls[i + p * k] -= Ls[i + p * j] * lkj;
+      }
+    }
+  }
+  __syncthreads();
+  // X = L^{-1} by right-looking forward substitution over rows (all columns at
+  // once); R^{-1} = X^T, retired columns of R^{-1} (rows of X) are zero.
+  const bool xs = 2 * p * p * static_cast<int>(sizeof(double)) <= kCholSmemBytes;
+  double* X = xs ? Ls + p * p : nullptr;
+  if (xs) {
+    for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) X[idx] = (idx % p == idx / p) ? 1.0 : 0.0;
+    __syncthreads();
+    for (int i = 0; i < p; ++i) {
+      // row i final: x_i(c) = acc_i(c) / L_ii for c <= i
+      const double rl = dead[i] ? 0.0 : 1.0 / Ls[i + p * i];
+      for (int c = threadIdx.x; c <= i; c += blockDim.x) X[i + p * c] *= rl;
+      __syncthreads();
+      // rows r > i: acc_r(c) -= L_ri x_i(c)
+      for (int c = warp; c <= i; c += nw) {
+        const double xic = X[i + p * c];
+        if (xic != 0.0)
+          for (int r = i + 1 + lane; r < p; r += 32) X[r + p * c] -= Ls[r + p * i] * xic;
+      }
+      __syncthreads();
+    }
+    for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) {
+      const int r = idx % p, c = idx / p;  // H(r, c) = R^{-1}(r, c) = X(c, r)
+      H[idx] = X[c + p * r];
+    }
+  } else {
+    for (int c = threadIdx.x; c < p; c += blockDim.x) {  // one thread per column of L^{-1}
+      for (int i = 0; i < c; ++i) H[c + p * i] = 0.0;
+      for (int i = c; i < p; ++i) {
+        double s0 = (i == c) ? 1.0 : 0.0;
+        for (int k = c; k < i; ++k) s0 -= Ls[i + p * k] * H[c + p * k];
+        H[c + p * i] = dead[i] ? 0.0 : s0 / Ls[i + p * i];
+      }
+    }
+  }
+}
+
 __global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) x[i] = v;
@@ -261,6 +340,97 @@ void jacobi_svd_small(int p, std::vector<double> S, std::vector<double>& sg, std
   }
 }
 
+// The same one-sided Jacobi SVD on the device for p <= kJacMax: one CTA,
+// columns in shared memory, round-robin (tournament) ordering so the p/2
+// rotations of a round are disjoint and run on separate warps; the rotation
+// formula and the stopping test are the host version's.  Output: U (sorted
+// columns, in place of S) and sg, descending, stable in the column index.
+constexpr int kJacMax = 128;
+constexpr int kJacThreads = 1024;
+
+__global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(int p, double* __restrict__ S,
+                                                                 double* __restrict__ sg_out) {
+  extern __shared__ double js[];
+  const int pe = p + (p & 1);  // even column count (a zero column pads odd p)
+  double* col = js;            // pe columns of length p
+  __shared__ int rot_any;
+  __shared__ int perm_sh[kJacMax + 1];
+  __shared__ double nr_sh[kJacMax + 1];
+  for (int i = threadIdx.x; i < p * pe; i += blockDim.x) col[i] = i < p * p ? S[i] : 0.0;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int half = pe / 2;
+  // convergence |c_i . c_j| <= tol |c_i| |c_j| with tol = p eps: below the
+  // rounding level of the dot products a stricter test never settles
+  const double tol = fmax(1e-16, p * 1.1102230246251565e-16);
+  const double tol2 = tol * tol;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) rot_any = 0;
+    __syncthreads();
+    int any = 0;
+    for (int round = 0; round < pe - 1; ++round) {
+      for (int q = warp; q < half; q += nw) {
+        // tournament pairing: fixed element pe-1, the rest rotate
+        int a = (q == 0) ? pe - 1 : (round + q) % (pe - 1);
+        int b = (round + pe - 1 - q) % (pe - 1);
+        if (q == 0) b = round % (pe - 1);
+        int i = min(a, b), j = max(a, b);
+        double* ci = col + static_cast<size_t>(p) * i;
+        double* cj = col + static_cast<size_t>(p) * j;
+        double al = 0, be = 0, ga = 0;
+        for (int r = lane; r < p; r += 32) {
+          const double x = ci[r], y = cj[r];
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga == 0.0 || ga * ga <= tol2 * (al * be)) continue;
+        any = 1;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = rsqrt(1.0 + t * t), sn = c * t;
+        for (int r = lane; r < p; r += 32) {
+          const double x = ci[r], y = cj[r];
+          ci[r] = c * x - sn * y;
+          cj[r] = sn * x + c * y;
+        }
+      }
+      __syncthreads();
+    }
+    if (any && lane == 0) rot_any = 1;
+    __syncthreads();
+    if (!rot_any) break;
+    __syncthreads();
+  }
+  for (int j = warp; j < p; j += nw) {
+    double ss = 0;
+    for (int r = lane; r < p; r += 32) ss += col[r + static_cast<size_t>(p) * j] * col[r + static_cast<size_t>(p) * j];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) nr_sh[j] = sqrt(ss);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {  // stable descending rank
+    int rk = 0;
+    for (int k = 0; k < p; ++k) rk += (nr_sh[k] > nr_sh[j]) || (nr_sh[k] == nr_sh[j] && k < j);
+    perm_sh[rk] = j;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < p * p; i += blockDim.x) {
+    const int r = i % p, c = i / p;
+    const int j = perm_sh[c];
+    const double nj = nr_sh[j];
+    S[i] = nj > 0 ? col[r + static_cast<size_t>(p) * j] / nj : (r == c ? 1.0 : 0.0);
+  }
+  for (int c = threadIdx.x; c < p; c += blockDim.x) sg_out[c] = nr_sh[perm_sh[c]];
+}
+
 // lower Cholesky of a p x p SPD matrix (host); returns false if not PD
 bool host_cholesky(int p, std::vector<double>& A) {
   for (int j = 0; j < p; ++j) {
@@ -292,23 +462,62 @@ std::vector<double> upper_inverse_from_lower(int p, const std::vector<double>& L
   return Ri;
 }
 
+// Scratch of the reduction / TEI drivers: while a DevStreamScope is alive,
+// blocks come from the context's cache (best fit) and go back to it, so the
+// many short-lived buffers of the iterations cost neither cudaMalloc latency
+// nor the device-wide synchronisation of cudaFree.  All users run on
+// ctx->stream, so reuse is stream-ordered.
+thread_local tgb_ctx* g_dev_ctx = nullptr;
+
 struct Dev {
   double* p = nullptr;
   size_t n = 0;
+  size_t bytes = 0;
+  tgb_ctx* c = nullptr;
   explicit Dev(size_t count = 0) { resize(count); }
   void resize(size_t count) {
     if (count <= n) return;
-    if (p) cudaFree(p);
-    p = nullptr;
-    n = 0;
-    if (count) TGB_CUDA(cudaMalloc(&p, count * sizeof(double)));
+    release();
+    c = g_dev_ctx;
+    if (count) {
+      if (c) {
+        p = static_cast<double*>(scratch_alloc(c, count * sizeof(double), &bytes));
+      } else {
+        TGB_CUDA(cudaMalloc(&p, count * sizeof(double)));
+        bytes = count * sizeof(double);
+      }
+    }
     n = count;
   }
-  ~Dev() {
-    if (p) cudaFree(p);
+  void release() {
+    if (p) {
+      if (c)
+        scratch_free(c, p, bytes);
+      else
+        cudaFree(p);
+    }
+    p = nullptr;
+    n = 0;
+    bytes = 0;
   }
+  ~Dev() { release(); }
   Dev(const Dev&) = delete;
   Dev& operator=(const Dev&) = delete;
+};
+
+// analysis only (TGB_RED_TIME): host-side stage timer, synchronising the stream
+struct StageTimer {
+  tgb_ctx* ctx;
+  bool on;
+  std::chrono::steady_clock::time_point t;
+  explicit StageTimer(tgb_ctx* c) : ctx(c), on(getenv("TGB_RED_TIME") != nullptr), t(std::chrono::steady_clock::now()) {}
+  void mark(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(ctx->stream);
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[tgb-time] %-28s %8.2f ms\n", what, std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
 };
 
 std::vector<double> to_host(tgb_ctx* ctx, const double* d, size_t count) {
@@ -338,7 +547,19 @@ void cholqr2(tgb_ctx* ctx, int64_t d, int p, double* X, Dev& tmp) {
     dgemm(ctx, true, false, p, p, d, 1.0, X, d, X, d, 0.0, H, p);
     // H is written in place with R^{-1}; back substitution reads H's upper part as it goes,
     // so each column c only reads entries (k, c) with k > i that it already produced.
-    chol_inv_kernel<<<1, 256, 0, ctx->stream>>>(p, H, Wk);
+    if (p <= kCholSmem && !getenv("TGB_CHOL_GLOBAL")) {
+      static bool cattr = false;
+      if (!cattr) {
+        TGB_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kCholSmemBytes));
+        cattr = true;
+      }
+      const size_t l_bytes = static_cast<size_t>(p) * p * sizeof(double);
+      const size_t bytes = 2 * l_bytes <= static_cast<size_t>(kCholSmemBytes) ? 2 * l_bytes : l_bytes;
+      chol_inv_smem_kernel<<<1, 256, bytes, ctx->stream>>>(p, H);
+    } else {
+      chol_inv_kernel<<<1, 256, 0, ctx->stream>>>(p, H, Wk);
+    }
     TGB_LAUNCHED(ctx);
     TGB_CUDA(cudaMemcpyAsync(tmp.p, X, static_cast<size_t>(d) * p * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
@@ -362,6 +583,34 @@ void random_block(tgb_ctx* ctx, int64_t d, int p, double* X, uint64_t seed) {
 }
 
 }  // namespace
+
+DevStreamScope::DevStreamScope(tgb_ctx* ctx) : prev(g_dev_ctx) {
+  if (!getenv("TGB_NO_SCRATCH_CACHE")) g_dev_ctx = ctx;
+}
+DevStreamScope::~DevStreamScope() { g_dev_ctx = prev; }
+
+void* scratch_alloc(tgb_ctx* ctx, size_t bytes, size_t* got) {
+  auto it = ctx->scratch_free.lower_bound(bytes);
+  if (it != ctx->scratch_free.end() && it->first <= 2 * bytes + (1 << 20)) {  // best fit, bounded waste
+    void* p = it->second;
+    *got = it->first;
+    ctx->scratch_free.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, bytes);
+  if (e != cudaSuccess) {  // release the cache and retry once
+    cudaGetLastError();
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    for (auto& kv : ctx->scratch_free) cudaFree(kv.second);
+    ctx->scratch_free.clear();
+    TGB_CUDA(cudaMalloc(&p, bytes));
+  }
+  *got = bytes;
+  return p;
+}
+
+void scratch_free(tgb_ctx* ctx, void* p, size_t bytes) { ctx->scratch_free.emplace(bytes, p); }
 
 // Column-normalise then Cholesky-QR twice: orthonormal basis of the columns of
 // X (d x p, device, in place).  Used by the TEI fit (Q of the pivoted Cholesky
@@ -454,7 +703,7 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
   double total = 0.0;
   for (double x : to_host(ctx, part.p, 256)) total += x;
   int p = static_cast<int>(std::min<int64_t>(std::min<int64_t>(dmin, kMaxBlock), sel >= 0 ? std::max<int64_t>(sel + 8, 16) : 48));
-  Dev X, Y, T, tmp, Sd;
+  Dev X, Y, T, tmp, Sd, sgd;
   std::vector<double> sg, Ut;
   int64_t r = 0;
   int pcur = 0;  // columns of X already holding a (partially converged) subspace
@@ -499,8 +748,25 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
       if (it % 2 == 1 || it >= 40) {
         // Rayleigh-Ritz: S = X^T a Y, rotate X to the singular directions
         dgemm(ctx, true, false, p, p, n, 1.0, X.p, n, T.p, n, 0.0, Sd.p, p);
-        jacobi_svd_small(p, to_host(ctx, Sd.p, static_cast<size_t>(p) * p), sg, Ut);
-        to_dev(ctx, Sd.p, Ut);
+        if (p <= kJacMax && !getenv("TGB_HOST_JACOBI")) {
+          // device Jacobi: U replaces S in place, only the p singular values come back
+          const size_t jsm = static_cast<size_t>(p) * (p + (p & 1)) * sizeof(double);
+          static bool jattr = false;
+          if (!jattr) {
+            cudaFuncAttributes fa{};
+            TGB_CUDA(cudaFuncGetAttributes(&fa, jacobi_svd_kernel));
+            TGB_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
+            jattr = true;
+          }
+          sgd.resize(p);
+          jacobi_svd_kernel<<<1, kJacThreads, jsm, ctx->stream>>>(p, Sd.p, sgd.p);
+          TGB_LAUNCHED(ctx);
+          sg = to_host(ctx, sgd.p, p);
+        } else {
+          jacobi_svd_small(p, to_host(ctx, Sd.p, static_cast<size_t>(p) * p), sg, Ut);
+          to_dev(ctx, Sd.p, Ut);
+        }
         dgemm(ctx, false, false, n, p, p, 1.0, X.p, n, Sd.p, p, 0.0, T.p, n);
         TGB_CUDA(cudaMemcpyAsync(X.p, T.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
                                  ctx->stream));
@@ -597,6 +863,7 @@ static double fro_norm_dev(tgb_ctx* ctx, const double* x, int64_t count) {
 }
 
 void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, RedState& st) {
+  StageTimer tm(ctx);
   st.R = a.rank;
   for (int ax = 0; ax < 3; ++ax) st.n[ax] = a.n[ax];
   // normalized copy (reduction.cpp:176-177)
@@ -625,8 +892,10 @@ void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, Red
       TGB_LAUNCHED(ctx);
     }
     st.r[mode] = left_subspace(ctx, n, R, W.p, &cfg, mode, -1, &st.rank_clamped, st.Z[mode], &st.sigma[mode]);
+    tm.mark("rhosvd left subspace");
   }
   project_core(ctx, st);
+  tm.mark("project core");
   if (!als || a.rank == 0 || st.r[0] * st.r[1] * st.r[2] == 0) return;
   // ALS sweeps (reduction.cpp:205-232)
   double prev = -1.0;
@@ -644,6 +913,7 @@ void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, Red
       TGB_LAUNCHED(ctx);
       Dev mat(static_cast<size_t>(n) * rm * rp);
       dgemm(ctx, false, false, n, rm * rp, R, 1.0, st.f[ax], n, Cm.p, R, 0.0, mat.p, n);
+      tm.mark("als unfolding");
       Dev Znew;
       const int64_t r = left_subspace(ctx, n, rm * rp, mat.p, nullptr, ax, st.r[ax], nullptr, Znew, nullptr,
                                       st.Z[ax].p, st.r[ax]);
@@ -658,12 +928,14 @@ void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, Red
       Dev proj(static_cast<size_t>(st.r[ax]) * rm * rp);
       dgemm(ctx, true, false, st.r[ax], rm * rp, n, 1.0, st.Z[ax].p, n, mat.p, n, 0.0, proj.p, st.r[ax]);
       fit = fro_norm_dev(ctx, proj.p, st.r[ax] * rm * rp);
+      tm.mark("als subspace + fit");
     }
     st.sweep_fits.push_back(fit);
     if (prev >= 0.0 && std::fabs(fit - prev) < 1e-14 * std::max(1.0, fit)) break;
     prev = fit;
   }
   project_core(ctx, st);
+  tm.mark("final core");
 }
 
 // tucker_to_canonical (reduction.cpp:238-269) into caller-sized device buffers
@@ -722,6 +994,8 @@ int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, co
     if (!use_eps)
       for (int i = 0; i < 3; ++i) tgb::require(ranks[i] >= 0, "select_rank: negative rank request");
     TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::DevStreamScope scope(ctx);
+    tgb::StageTimer tm(ctx);
     tgb::RedCfgC cfg{use_eps != 0, eps, {0, 0, 0}, max_sweeps};
     if (!use_eps)
       for (int i = 0; i < 3; ++i) cfg.ranks[i] = ranks[i];
@@ -738,6 +1012,7 @@ int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, co
       if (a->rank) TGB_CUDA(cudaMemcpy(bufs[3].p, a->weight, a->rank * sizeof(double), cudaMemcpyHostToDevice));
       dev.weight = bufs[3].p;
     }
+    tm.mark("input to device");
     auto* t = new tgb_tucker();
     try {
       tgb::reduce_dev(ctx, dev, cfg, mode == 1, t->st);
@@ -796,6 +1071,7 @@ int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem) {
     const int64_t rank = tgb::t2c_rank(t->st);
     tgb::require(out->rank == rank, "tucker_to_canonical: output rank mismatch");
     TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::DevStreamScope scope(ctx);
     if (mem == TGB_MEM_DEVICE) {
       tgb::t2c_dev(ctx, t->st, out->factor, out->weight);
       TGB_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -653,6 +653,7 @@ int tgb_tei_destroy(tgb_tei* t) {
 int tgb_tei_density_fitting(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
                             const double h[3], double eps_fit, int mem) {
   return tgb::guarded_call([&] {
+    tgb::DevStreamScope scope(ctx);
     tgb::require(basis && fn_offset && nb >= 1, "tei_density_fitting: empty basis");
     tgb::require(fn_offset[0] == 0 && fn_offset[nb] == basis->rank, "tei_density_fitting: bad function offsets");
     TGB_CUDA(cudaSetDevice(ctx->device));
@@ -663,6 +664,7 @@ int tgb_tei_density_fitting(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* basis, const
 
 int tgb_tei_convolution_matrices(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* kernel, int mem) {
   return tgb::guarded_call([&] {
+    tgb::DevStreamScope scope(ctx);
     TGB_CUDA(cudaSetDevice(ctx->device));
     DevCopy d(kernel, mem == TGB_MEM_DEVICE);
     tgb::tei_conv(ctx, t->t, d.t);
@@ -671,6 +673,7 @@ int tgb_tei_convolution_matrices(tgb_ctx* ctx, tgb_tei* t, const tgb_cp* kernel,
 
 int tgb_tei_diagonal(tgb_ctx* ctx, tgb_tei* t, double* out, int mem) {
   return tgb::guarded_call([&] {
+    tgb::DevStreamScope scope(ctx);
     const int64_t nb2 = t->t.nb * t->t.nb;
     static thread_local tgb::DevBuf buf;
     auto* d = static_cast<double*>(buf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
@@ -682,6 +685,7 @@ int tgb_tei_diagonal(tgb_ctx* ctx, tgb_tei* t, double* out, int mem) {
 
 int tgb_tei_column(tgb_ctx* ctx, tgb_tei* t, int64_t pair, double* out, int mem) {
   return tgb::guarded_call([&] {
+    tgb::DevStreamScope scope(ctx);
     tgb::require(pair >= 0 && pair < t->t.nb * t->t.nb, "tei_column: index out of range");
     const int64_t nb2 = t->t.nb * t->t.nb;
     static thread_local tgb::DevBuf buf;
@@ -694,6 +698,7 @@ int tgb_tei_column(tgb_ctx* ctx, tgb_tei* t, int64_t pair, double* out, int mem)
 
 int tgb_tei_cholesky(tgb_ctx* ctx, tgb_tei* t, double eps_chol) {
   return tgb::guarded_call([&] {
+    tgb::DevStreamScope scope(ctx);
     TGB_CUDA(cudaSetDevice(ctx->device));
     tgb::tei_cholesky(ctx, t->t, eps_chol);
   });

@@ -65,6 +65,16 @@ struct ConvPlan;  // fftconv.cu
 
 void set_last_error(const std::string& msg);  // capi.cpp
 
+// Scratch allocations of the reduction / TEI drivers become stream-ordered
+// (pooled) on ctx->stream while one of these is alive (reduction.cu).
+struct DevStreamScope {
+  tgb_ctx* prev;
+  explicit DevStreamScope(tgb_ctx* ctx);
+  ~DevStreamScope();
+};
+void* scratch_alloc(tgb_ctx* ctx, size_t bytes, size_t* got);
+void scratch_free(tgb_ctx* ctx, void* p, size_t bytes);
+
 // Run f, mapping exceptions to the C-ABI return codes (tgb.h).
 template <class F>
 int guarded_call(F&& f) {
@@ -96,7 +106,7 @@ struct tgb_ctx {
   int num_sms = 148;
   size_t smem_optin = 232448;
   // workspaces (named so independent stages never alias)
-  tgb::DevBuf ws_spec_a, ws_spec_b, ws_pairs, ws_flags, ws_in, ws_out, ws_misc, ws_misc2, ws_misc3;
+  tgb::DevBuf ws_spec_a, ws_spec_b, ws_pairs, ws_flags, ws_in, ws_out, ws_misc, ws_misc2, ws_misc3, ws_gemm;
   std::vector<cudaEvent_t> events;
   bool profiling = false;
   void* pinned = nullptr;
@@ -105,6 +115,7 @@ struct tgb_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> prof_events;
   size_t prof_used = 0;
   std::map<int64_t, std::shared_ptr<tgb::ConvPlan>> plans;
+  std::multimap<size_t, void*> scratch_free;  // cached Dev blocks (reduction.cu)
 };
 
 namespace tgb {
