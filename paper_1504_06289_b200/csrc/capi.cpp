@@ -96,10 +96,8 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
     ooff += a->n[ax] * r;
   }
   for (int ax = 0; ax < 3; ++ax) {
-    TGB_CUDA(cudaMemcpyAsync(da[ax], a->factor[ax], a->n[ax] * ra * sizeof(double), cudaMemcpyHostToDevice,
-                             ctx->stream));
-    TGB_CUDA(cudaMemcpyAsync(db[ax], b->factor[ax], a->n[ax] * rb * sizeof(double), cudaMemcpyHostToDevice,
-                             ctx->stream));
+    tgb::h2d(ctx, da[ax], a->factor[ax], a->n[ax] * ra * sizeof(double), ctx->stream);
+    tgb::h2d(ctx, db[ax], b->factor[ax], a->n[ax] * rb * sizeof(double), ctx->stream);
     tgb::convolve_axis(ctx, a->n[ax], ra, da[ax], rb, db[ax], h[ax], dout_ax[ax]);
     cudaEvent_t ev = ctx_event(ctx, ax);
     TGB_CUDA(cudaEventRecord(ev, ctx->stream));
@@ -192,6 +190,10 @@ int tgb_ctx_destroy(tgb_ctx* ctx) {
     cudaEventDestroy(ctx->aux_done);
     if (ctx->pinned_flags) cudaFreeHost(ctx->pinned_flags);
     for (auto& kv : ctx->scratch_free) cudaFree(kv.second);
+    for (int i = 0; i < 2; ++i) {
+      if (ctx->stage_pin[i]) cudaFreeHost(ctx->stage_pin[i]);
+      if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+    }
     if (ctx->pinned_event) cudaEventDestroy(ctx->pinned_event);
     if (ctx->pinned) cudaFreeHost(ctx->pinned);
     for (auto& pe : ctx->prof_events) {

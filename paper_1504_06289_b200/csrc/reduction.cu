@@ -1004,12 +1004,11 @@ int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, co
     if (mem == TGB_MEM_HOST) {
       for (int ax = 0; ax < 3; ++ax) {
         bufs[ax].resize(std::max<int64_t>(1, a->n[ax] * a->rank));
-        if (a->rank)
-          TGB_CUDA(cudaMemcpy(bufs[ax].p, a->factor[ax], a->n[ax] * a->rank * sizeof(double), cudaMemcpyHostToDevice));
+        if (a->rank) tgb::h2d(ctx, bufs[ax].p, a->factor[ax], a->n[ax] * a->rank * sizeof(double), ctx->stream);
         dev.factor[ax] = bufs[ax].p;
       }
       bufs[3].resize(std::max<int64_t>(1, a->rank));
-      if (a->rank) TGB_CUDA(cudaMemcpy(bufs[3].p, a->weight, a->rank * sizeof(double), cudaMemcpyHostToDevice));
+      if (a->rank) tgb::h2d(ctx, bufs[3].p, a->weight, a->rank * sizeof(double), ctx->stream);
       dev.weight = bufs[3].p;
     }
     tm.mark("input to device");
@@ -1087,8 +1086,8 @@ int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem) {
     tgb::t2c_dev(ctx, t->st, f, bufs[3].p);
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
     for (int ax = 0; ax < 3; ++ax)
-      if (rank) TGB_CUDA(cudaMemcpy(out->factor[ax], f[ax], t->st.n[ax] * rank * sizeof(double), cudaMemcpyDeviceToHost));
-    if (rank) TGB_CUDA(cudaMemcpy(out->weight, bufs[3].p, rank * sizeof(double), cudaMemcpyDeviceToHost));
+      if (rank) tgb::d2h(ctx, out->factor[ax], f[ax], t->st.n[ax] * rank * sizeof(double), ctx->stream);
+    if (rank) tgb::d2h(ctx, out->weight, bufs[3].p, rank * sizeof(double), ctx->stream);
   });
 }
 

@@ -73,6 +73,9 @@ struct DevStreamScope {
   ~DevStreamScope();
 };
 void* scratch_alloc(tgb_ctx* ctx, size_t bytes, size_t* got);
+// host <-> device copies; pageable host memory is staged through pinned chunks (hostcopy.cpp)
+void h2d(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t stream);
+void d2h(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t stream);
 void scratch_free(tgb_ctx* ctx, void* p, size_t bytes);
 
 // Run f, mapping exceptions to the C-ABI return codes (tgb.h).
@@ -116,6 +119,8 @@ struct tgb_ctx {
   size_t prof_used = 0;
   std::map<int64_t, std::shared_ptr<tgb::ConvPlan>> plans;
   std::multimap<size_t, void*> scratch_free;  // cached Dev blocks (reduction.cu)
+  void* stage_pin[2] = {nullptr, nullptr};     // pinned chunks for pageable host copies (hostcopy.cpp)
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
 };
 
 namespace tgb {
