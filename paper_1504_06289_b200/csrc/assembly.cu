@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "tgb_internal.hpp"
@@ -181,6 +182,40 @@ __global__ void reduce_tiles_kernel(const double* __restrict__ partial, int ntil
   s[p] = acc;
 }
 
+// Hadamard left columns materialised (n x P per axis) for the GEMM route.
+__global__ void hadamard_cols_kernel(int64_t n, const double* __restrict__ F, const int* __restrict__ i0,
+                                     const int* __restrict__ i1, int P, double* __restrict__ L) {
+  const int p = blockIdx.y;
+  if (p >= P) return;
+  const int c0 = i0[p], c1 = i1[p];
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    double v = F[c0 * n + k];
+    if (c1 >= 0) v *= F[c1 * n + k];
+    L[p * n + k] = v;
+  }
+}
+
+// part[chunk * P + p] = sum_{q in chunk} w_q T0[q, p] T1[q, p] T2[q, p]; T_ax are
+// (nq x P) column-major, so row p is contiguous in q.  Fixed-order reduction.
+__global__ void __launch_bounds__(256) triple_dot_kernel(int nq, int P, const double* __restrict__ T0,
+                                                         const double* __restrict__ T1,
+                                                         const double* __restrict__ T2, const double* __restrict__ w,
+                                                         double* __restrict__ part) {
+  const int p = blockIdx.x;
+  const int64_t o = static_cast<int64_t>(p) * nq;
+  double acc = 0.0;
+  for (int q = threadIdx.x; q < nq; q += blockDim.x) acc += w[q] * T0[o + q] * T1[o + q] * T2[o + q];
+  __shared__ double sh[256];
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  for (int st = 128; st; st >>= 1) {
+    if (threadIdx.x < st) sh[threadIdx.x] += sh[threadIdx.x + st];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.y * static_cast<int64_t>(P) + p] = sh[0];
+}
+
 // s[p] = sum_q wb[q] prod_ax <left_p^ax, B_q^ax>, returned to the host.
 std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* const F[3], const double* const B[3],
                               const double* wb, int RB, const std::vector<int>& i0, const std::vector<int>& i1) {
@@ -206,11 +241,47 @@ std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* co
   a.wb = wb;
   a.P = P;
   a.RB = RB;
-  dim3 grid((P + TP - 1) / TP, ntq);
-  sep_inner_dmma_kernel<<<grid, DM_THREADS, 0, ctx->stream>>>(a, partial);
-  TGB_LAUNCHED(ctx);
-  reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(partial, ntq, P, dsum);
-  TGB_LAUNCHED(ctx);
+  if (P >= 128 && !getenv("TGB_SEP_FUSED")) {
+    // GEMM route for many left columns (the Coulomb matrix): per axis
+    // T_ax = B_ax^T L_ax on the DGEMM (chunks of q), then one fused
+    // weighted triple-product reduction.  The fused tile kernel needs ~190
+    // live doubles per thread (two axis tiles + staging), which caps it at
+    // two CTAs per SM; the split route runs each GEMM at full occupancy.
+    int64_t tot = 0;
+    for (int ax = 0; ax < 3; ++ax) tot += n[ax] * P;
+    const int chunk = static_cast<int>(std::min<int64_t>(RB, 32768));
+    const int nch = (RB + chunk - 1) / chunk;
+    auto* work = static_cast<double*>(ctx->ws_misc3.get((static_cast<size_t>(tot) + 3 * static_cast<size_t>(chunk) * P +
+                                                         static_cast<size_t>(nch) * P) * sizeof(double)));
+    double* Lh[3];
+    int64_t off = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+      Lh[ax] = work + off;
+      dim3 hg(static_cast<unsigned>(std::min<int64_t>((n[ax] + 255) / 256, 8)), static_cast<unsigned>(P));
+      hadamard_cols_kernel<<<hg, 256, 0, ctx->stream>>>(n[ax], F[ax], idx, idx + P, P, Lh[ax]);
+      TGB_LAUNCHED(ctx);
+      off += n[ax] * P;
+    }
+    double* T[3] = {work + off, work + off + static_cast<size_t>(chunk) * P, work + off + 2 * static_cast<size_t>(chunk) * P};
+    double* parts = work + off + 3 * static_cast<size_t>(chunk) * P;
+    for (int c = 0; c < nch; ++c) {
+      const int q0 = c * chunk, nq = std::min(chunk, RB - q0);
+      for (int ax = 0; ax < 3; ++ax)  // T_ax (nq x P) = B_ax(:, q0:q0+nq)^T L_ax
+        dgemm(ctx, true, false, nq, P, n[ax], 1.0, B[ax] + static_cast<int64_t>(q0) * n[ax], n[ax], Lh[ax], n[ax], 0.0,
+              T[ax], nq);
+      triple_dot_kernel<<<dim3(static_cast<unsigned>(P), 1), 256, 0, ctx->stream>>>(nq, P, T[0], T[1], T[2], wb + q0,
+                                                                                    parts + static_cast<size_t>(c) * P);
+      TGB_LAUNCHED(ctx);
+    }
+    reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(parts, nch, P, dsum);
+    TGB_LAUNCHED(ctx);
+  } else {
+    dim3 grid((P + TP - 1) / TP, ntq);
+    sep_inner_dmma_kernel<<<grid, DM_THREADS, 0, ctx->stream>>>(a, partial);
+    TGB_LAUNCHED(ctx);
+    reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(partial, ntq, P, dsum);
+    TGB_LAUNCHED(ctx);
+  }
   TGB_CUDA(cudaMemcpyAsync(s.data(), dsum, P * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
   TGB_CUDA(cudaStreamSynchronize(ctx->stream));
   return s;
