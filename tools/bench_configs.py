@@ -127,9 +127,9 @@ def cfg3(ctx):
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     n, np_ = bs.grid.n[0], fac.n_prim
-    gram_flops = 3 * 2.0 * n * n * np_ * np_
+    gram_flops = 3 * 2.0 * n * n * np_ * np_  # the reference's dense G G^T (ours forms (F F^T)^2: np x fewer)
     return {"config": 3, "what": "build_tei N_b=80 s/p, n=4097, eps_fit=eps_chol=1e-6", "fit_ms": (t1 - t0) * 1e3,
-            "fit_gram_tflops_lower_bound": gram_flops / (t1 - t0) / 1e12, "conv_ms": (t2 - t1) * 1e3,
+            "fit_dense_gram_equiv_tflops": gram_flops / (t1 - t0) / 1e12, "conv_ms": (t2 - t1) * 1e3,
             "cholesky_ms": (t3 - t2) * 1e3, "fit_ranks": list(fac.fit_ranks()), "R_B": fac.rank_b(),
             "fit_residual": [float(x) for x in fac.fit_residual]}
 
