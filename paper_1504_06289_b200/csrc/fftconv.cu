@@ -1478,59 +1478,87 @@ __global__ void dup_columns_kernel(const double* __restrict__ B, int64_t n, int 
   if (threadIdx.x == 0) flags[j * rb + j2] = static_cast<unsigned char>(same);
 }
 
-// Device-side grouping of the kernel columns (one CTA per axis) from the
+// Device-side grouping of the kernel columns (per axis) from the
 // dup/symmetry flags, and the i-major pair work list: for each density
 // column i, one entry per pair of identical kernel columns (the entry's
 // result is stored to both).  winfo = {entries, all columns symmetric}.
 __global__ void build_work_kernel(const unsigned char* __restrict__ f, int rb, int64_t ra, int64_t n,
-                                  PairEntry* __restrict__ w, int* __restrict__ winfo) {
-  extern __shared__ int wsh[];  // members[rb], gstart[rb + 1], pg[rb], pq[rb]
-  int* members = wsh;
-  int* gstart = members + rb;
-  int* pg = gstart + rb + 1;
-  int* pq = pg + rb;
-  __shared__ int s_np;
-  if (threadIdx.x == 0) {
-    int* rep = pg;  // scratch before the pair map is built
-    for (int j = 0; j < rb; ++j) rep[j] = -1;
-    int ng = 0, nm = 0, sym = 1;
-    for (int j = 0; j < rb; ++j) {
-      if (rep[j] >= 0) continue;
-      gstart[ng] = nm;
-      rep[j] = ng;
-      members[nm++] = j;
-      sym &= f[j * rb + j];
-      for (int j2 = j + 1; j2 < rb; ++j2)
-        if (rep[j2] < 0 && f[j * rb + j2]) {
-          rep[j2] = ng;
-          members[nm++] = j2;
-        }
-      ++ng;
-    }
-    gstart[ng] = nm;
-    int np = 0;
-    for (int g = 0; g < ng; ++g)
-      for (int q = gstart[g]; q < gstart[g + 1]; q += 2) {
-        pg[np] = g;
-        pq[np] = q;
-        ++np;
+                                  PairEntry* __restrict__ w, int* __restrict__ winfo, int flags_in_smem) {
+  // Grouping in parallel (bitwise identity is an equivalence): rep[j] = the
+  // smallest j' <= j identical to j; a member's rank in its group = the number
+  // of earlier members; groups are ordered by representative.  Every CTA
+  // repeats this O(rb^2 / threads) step and writes its share of the density
+  // columns i.
+  extern __shared__ int wsh[];  // rep[rb], rank[rb], goff[rb] (pair offset of group rep j), then flags
+  int* rep = wsh;
+  int* rnk = rep + rb;
+  int* goff = rnk + rb;
+  unsigned char* fs = reinterpret_cast<unsigned char*>(goff + rb);
+  __shared__ int s_np, s_sym;
+  if (flags_in_smem) {
+    for (int i = threadIdx.x; i < rb * rb; i += blockDim.x) fs[i] = f[i];
+    __syncthreads();
+    f = fs;
+  }
+  if (threadIdx.x == 0) s_sym = 1;
+  __syncthreads();
+  for (int j = threadIdx.x; j < rb; j += blockDim.x) {
+    int r = j;
+    for (int jp = 0; jp < j; ++jp)
+      if (f[jp * rb + j]) {
+        r = jp;
+        break;
       }
-    s_np = np;
-    winfo[0] = static_cast<int>(ra * np);
-    winfo[1] = sym;
+    rep[j] = r;
+    if (!f[j * rb + j]) atomicAnd(&s_sym, 0);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < rb; j += blockDim.x) {
+    int k = 0, size = 0;
+    for (int jp = 0; jp < rb; ++jp)
+      if (rep[jp] == rep[j]) {
+        k += jp < j;
+        ++size;
+      }
+    rnk[j] = k;
+    goff[j] = (size + 1) / 2;  // pairs of this group (read at the representative)
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // exclusive prefix over representatives in index order (rb steps)
+    int acc = 0;
+    for (int j = 0; j < rb; ++j)
+      if (rep[j] == j) {
+        const int c = goff[j];
+        goff[j] = acc;
+        acc += c;
+      }
+    s_np = acc;
+    if (blockIdx.x == 0) {
+      winfo[0] = static_cast<int>(ra * acc);
+      winfo[1] = s_sym;
+    }
   }
   __syncthreads();
   const int np = s_np;
-  for (int64_t idx = threadIdx.x; idx < ra * np; idx += blockDim.x) {
-    const int64_t i = idx / np;
-    const int r = static_cast<int>(idx - i * np);
-    const int g = pg[r], q = pq[r];
-    PairEntry e;
-    e.ia = static_cast<int>(i);
-    e.jb = members[gstart[g]];
-    e.out0 = (i + ra * members[q]) * n;
-    e.out1 = q + 1 < gstart[g + 1] ? (i + ra * members[q + 1]) * n : -1;
-    w[idx] = e;
+  const int64_t i0 = ra * blockIdx.x / gridDim.x, i1 = ra * (blockIdx.x + 1) / gridDim.x;
+  for (int j = threadIdx.x; j < rb; j += blockDim.x) {  // j = the member stored to out0 of its pair
+    if (rnk[j] & 1) continue;
+    const int r = rep[j];
+    const int slot = goff[r] + rnk[j] / 2;
+    int partner = -1;  // next member of the group
+    for (int jp = j + 1; jp < rb; ++jp)
+      if (rep[jp] == r) {
+        partner = jp;
+        break;
+      }
+    for (int64_t i = i0; i < i1; ++i) {
+      PairEntry e;
+      e.ia = static_cast<int>(i);
+      e.jb = r;
+      e.out0 = (i + ra * j) * n;
+      e.out1 = partner >= 0 ? (i + ra * partner) * n : -1;
+      w[i * np + slot] = e;
+    }
   }
 }
 
@@ -1694,8 +1722,10 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
   char* wlist = wsp + fbytes + 256;
   TGB_CUDA(cudaEventRecord(ctx->aux_in, ctx->stream));  // B is ready in stream order
   TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
-  const size_t wsmem = static_cast<size_t>(4 * rb + 1) * sizeof(int);
+  size_t wsmem = static_cast<size_t>(3 * rb) * sizeof(int);
   if (wsmem > 48 * 1024) throw Error(TGB_INVALID_ARGUMENT, "convolve: kernel rank too large for the work builder");
+  const int flags_in_smem = wsmem + static_cast<size_t>(rb * rb) <= 48 * 1024;
+  if (flags_in_smem) wsmem += static_cast<size_t>(rb * rb);
   std::vector<PairEntry*> dwork(naxes);
   for (int ax = 0; ax < naxes; ++ax) {
     unsigned char* f = flags + ax * rb * rb;
@@ -1703,8 +1733,9 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
     dup_columns_kernel<<<static_cast<unsigned>(nblocks), 256, 0, ctx->aux_stream>>>(B[ax], n[ax],
                                                                                    static_cast<int>(rb), f);
     TGB_LAUNCHED(ctx);
-    build_work_kernel<<<1, 256, wsmem, ctx->aux_stream>>>(f, static_cast<int>(rb), ra, n[ax], dwork[ax],
-                                                         winfo + 2 * ax);
+    const unsigned wblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ra / 4, 2 * ctx->num_sms)));
+    build_work_kernel<<<wblocks, 128, wsmem, ctx->aux_stream>>>(f, static_cast<int>(rb), ra, n[ax], dwork[ax],
+                                                               winfo + 2 * ax, flags_in_smem);
     TGB_LAUNCHED(ctx);
   }
   TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
