@@ -54,6 +54,10 @@ constexpr int kMaxThreads = 384;
 struct PlanArgs {
   int n, N, m, P, ofs, even, npl;
   int nsp;  // single (self-mirror) first-pass blocks, stored last in the leader list
+  const int* spos;  // pair_kernel_fused: positions of the leftover first-pass blocks (leaders 320..), 8 per thread
+  int nspos;
+  int fused;        // spectra stored in the fused order kf (pair_kernel_fused) instead of the DIT order
+  const int* kf;    // fused order: slot -> natural frequency (N + 1 slots, Nyquist last)
   int dbg;  // analysis only (TGB_PAIR_DBG): 1 skip stores, 2 skip L2 loads, 4 skip passes
   int r[kMaxPasses];
   int L[kMaxPasses];
@@ -78,7 +82,7 @@ struct ConvPlan {
   bool direct = false;
   int threads = 0;
   size_t smem = 0;
-  DevBuf perm, inv, leader, tw, twpost, ph1, ph2, phase;
+  DevBuf perm, inv, leader, tw, twpost, ph1, ph2, phase, spos, kf;
 };
 
 __host__ __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
@@ -216,6 +220,46 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
       }
     }
     a.npl = static_cast<int>(leaders.size());
+    // positions of the blocks of leaders[320 ..] (the fused kernel stages these
+    // through shared memory; leaders[0 .. 320) are transformed in registers)
+    std::vector<int> spos;
+    if (a.npl > 320) {
+      for (size_t q = 320; q < leaders.size(); ++q) {
+        for (int s2 = 0; s2 < r0; ++s2) spos.push_back(leaders[q].x * r0 + s2);
+        if (leaders[q].y != leaders[q].x)
+          for (int s2 = 0; s2 < r0; ++s2) spos.push_back(leaders[q].y * r0 + s2);
+      }
+    }
+    a.nspos = static_cast<int>(spos.size());
+    a.spos = nullptr;
+    if (!spos.empty()) {
+      void* p = pl->spos.get(spos.size() * sizeof(int));
+      TGB_CUDA(cudaMemcpy(p, spos.data(), spos.size() * sizeof(int), cudaMemcpyHostToDevice));
+      a.spos = static_cast<const int*>(p);
+    }
+    // fused storage order (pair_kernel_fused, 320 threads, radix-16 first pass):
+    // slot s * 320 + t = element s of thread t's block pair (s < 16: block g,
+    // else block g2), then the staged positions u * 320 + t, then Nyquist
+    a.fused = 0;
+    a.kf = nullptr;
+    const bool fused_plan = rad.size() == 4 && rad[0] == 16 && rad[1] == 10 && rad[2] == 10 && rad[3] == 8 &&
+                            a.nspos == 8 * 320 && a.npl - a.nsp >= 320 && !getenv("TGB_NO_FUSED") &&
+                            !getenv("TGB_NO_TMEM") && !getenv("TGB_NO_STATIC") && a.dbg == 0;
+    if (fused_plan) {
+      std::vector<int> kf(static_cast<size_t>(N) + 1);
+      for (int t = 0; t < 320; ++t)
+        for (int s2 = 0; s2 < 32; ++s2) {
+          const int g = s2 < 16 ? leaders[t].x : leaders[t].y;
+          kf[static_cast<size_t>(s2) * 320 + t] = perm[static_cast<size_t>(g) * 16 + (s2 & 15)];
+        }
+      for (int u = 0; u < 8; ++u)
+        for (int t = 0; t < 320; ++t) kf[static_cast<size_t>(32 + u) * 320 + t] = perm[spos[t + 320 * u]];
+      kf[N] = static_cast<int>(N);
+      void* p = pl->kf.get(kf.size() * sizeof(int));
+      TGB_CUDA(cudaMemcpy(p, kf.data(), kf.size() * sizeof(int), cudaMemcpyHostToDevice));
+      a.kf = static_cast<const int*>(p);
+      a.fused = 1;
+    }
     std::vector<double2> tw;
     a.off_cs = 0;
     for (int s = 0; s < r0; ++s) tw.push_back(unit_root(static_cast<int64_t>(s) * nblk, a.m));
@@ -817,16 +861,20 @@ __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, 
 // both load blocks g and g2; the even lane splits + transforms block g, the
 // odd lane block g2 (the same code with the roles swapped), so the second
 // round costs half a pair instead of a whole one.
+// Leftover items of the split first pass (leader indices TT .. npl-1): the
+// regular pairs as half items on lanes 2u / 2u+1, the single blocks on lane 0
+// of the last nsp warps.  Returns false when the shape is not laid out for it.
 template <int R, int TT>
-__device__ __forceinline__ void first_pass_split(double2* sm, const double2* tws, const PlanArgs& pa,
-                                                 const double2* __restrict__ A, const void* __restrict__ B,
-                                                 bool breal) {
+__device__ __forceinline__ bool first_pass_shape_ok(const PlanArgs& pa) {
   const int nreg = pa.npl - pa.nsp;  // regular pairs first in the leader list
-  if (nreg < TT || nreg > 2 * TT || 2 * (nreg - TT) > TT - 32 * pa.nsp) {
-    first_pass_inv<R>(sm, tws, pa, A, B, breal);  // shapes this split is not laid out for
-    return;
-  }
-  first_item<R>(sm, tws, pa, A, B, breal, threadIdx.x);
+  return !(nreg < TT || nreg > 2 * TT || 2 * (nreg - TT) > TT - 32 * pa.nsp);
+}
+
+template <int R, int TT>
+__device__ __forceinline__ void first_pass_tail(double2* sm, const double2* tws, const PlanArgs& pa,
+                                                const double2* __restrict__ A, const void* __restrict__ B,
+                                                bool breal) {
+  const int nreg = pa.npl - pa.nsp;
   const int nrem = nreg - TT;
   const int u = threadIdx.x >> 1, h = threadIdx.x & 1;
   if (u < nrem) {  // partners share a warp
@@ -854,6 +902,18 @@ __device__ __forceinline__ void first_pass_split(double2* sm, const double2* tws
     if ((threadIdx.x & 31) == 0 && sp >= 0 && sp < pa.nsp && static_cast<int>(threadIdx.x) >= TT - 32 * pa.nsp)
       first_item<R>(sm, tws, pa, A, B, breal, nreg + sp);
   }
+}
+
+template <int R, int TT>
+__device__ __forceinline__ void first_pass_split(double2* sm, const double2* tws, const PlanArgs& pa,
+                                                 const double2* __restrict__ A, const void* __restrict__ B,
+                                                 bool breal) {
+  if (!first_pass_shape_ok<R, TT>(pa)) {
+    first_pass_inv<R>(sm, tws, pa, A, B, breal);  // shapes this split is not laid out for
+    return;
+  }
+  first_item<R>(sm, tws, pa, A, B, breal, threadIdx.x);
+  first_pass_tail<R, TT>(sm, tws, pa, A, B, breal);
 }
 
 __device__ __forceinline__ double2* load_tables(double2* sm, const PlanArgs& pa) {
@@ -1402,8 +1462,9 @@ __global__ void __launch_bounds__(TT, 1)
   }
   __syncthreads();
   // (2) storage order: coalesced spectrum stores
+  const int* order = pa.fused ? pa.kf : pa.perm;
   for (int pos = threadIdx.x; pos <= N; pos += TT) {
-    const int k = pos < N ? __ldg(pa.perm + pos) : N;
+    const int k = pos < N ? __ldg(order + pos) : N;
     const double2 v = sm[pidx(k)];
     if (mode == 1) {
       static_cast<double*>(specB)[base + pos] = v.x;
@@ -1425,6 +1486,158 @@ __global__ void __launch_bounds__(TT, 1)
       atomicAdd(pa.phase + 11, 1ULL);
     }
   }
+}
+
+// ---- Fused first pass.  Leaders 0..TT-1 (regular block pairs, one per
+// thread) never touch shared memory before their transform: the thread
+// reads its two blocks' density spectrum from its TMEM lane and the kernel
+// spectrum from L2, forms the product, the real split and both radix-R0
+// butterflies in registers, and writes pass-0 outputs.  The remaining
+// leaders' blocks (8 positions per thread) are staged through shared memory
+// and finished by first_pass_tail.  TMEM per thread: [0, 4 R0) block g,
+// [4 R0, 8 R0) block g2, then 4 per staged position.
+template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    pair_kernel_fused(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
+                      const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out) {
+  if ((winfo[1] != 0) != BREAL) return;
+  const int nwork = winfo[0];
+  constexpr int N = R0 * R1 * R2 * R3;
+  constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
+  constexpr int NS = 8;  // staged positions per thread
+  static_assert(R0 == 16, "fused first pass is laid out for radix-16 blocks (two x32 TMEM chunks each)");
+  constexpr int COLS = 8 * R0 + 4 * NS;  // 160
+  static_assert(((TT / 32 + 3) / 4) * COLS <= 512, "tensor memory per lane");
+  __shared__ uint32_t tmem_base_sh;
+  extern __shared__ double2 sm[];
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base_sh));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  const double2* tws = load_tables(sm, pa);
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                         static_cast<uint32_t>((warp >> 2) * COLS);
+  const int nz = (pa.n + 1) >> 1;
+  const bool odd_n = pa.n & 1;
+  // this thread's fused item and staged positions (fixed for the whole launch)
+  const int4 it = __ldg(pa.leader + threadIdx.x);
+  const int g = it.x, g2 = it.y;
+  const double2* cs = tws + pa.off_cs;
+  const double2 wk = cmul(tws[pa.off_zlo + (it.z & 63)], tws[pa.off_zhi + (it.z >> 6)]);
+  int sp[NS];
+#pragma unroll
+  for (int u = 0; u < NS; ++u) sp[u] = __ldg(pa.spos + threadIdx.x + TT * u);
+  const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
+  const int w1 = static_cast<int>((static_cast<int64_t>(nwork) * (blockIdx.x + 1)) / gridDim.x);
+  int ia_cur = -1;
+  for (int w = w0; w < w1; ++w) {
+    const PairEntry e = work[w];
+    const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
+    long long t0 = pa.phase ? clock64() : 0;
+    if (e.ia != ia_cur) {  // CTA-uniform: a new density column -> tensor memory
+      ia_cur = e.ia;
+#pragma unroll 1
+      for (int c = 0; c < 5; ++c) {  // chunks: g[0..8), g[8..16), g2[0..8), g2[8..16), staged
+        uint32_t r[32];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double2 v = ld2(a + (8 * c + u) * TT + threadIdx.x);  // fused order: coalesced
+          r[4 * u + 0] = __double2loint(v.x);
+          r[4 * u + 1] = __double2hiint(v.x);
+          r[4 * u + 2] = __double2loint(v.y);
+          r[4 * u + 3] = __double2hiint(v.y);
+        }
+        tmem_st32(tbase + 32 * c, r);
+      }
+      tmem_wait_st();
+    }
+    auto bval = [&](int slot, double2 v) -> double2 {  // slot in the fused order
+      if constexpr (BREAL)
+        return cscale(v, __ldg(static_cast<const double*>(b) + slot * TT + threadIdx.x));
+      else
+        return cmul(v, ld2(static_cast<const double2*>(b) + slot * TT + threadIdx.x));
+    };
+    auto tm2 = [&](const uint32_t* r, int u) {
+      return make_double2(__hiloint2double(r[4 * u + 1], r[4 * u + 0]), __hiloint2double(r[4 * u + 3], r[4 * u + 2]));
+    };
+    // (1) staged positions -> shared memory
+    {
+      uint32_t r[32];
+      tmem_ld32(tbase + 128, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int u = 0; u < NS; ++u) sm[pidx(sp[u])] = bval(32 + u, tm2(r, u));
+    }
+    // (2) the fused item: product, real split, two radix-16 butterflies
+    {
+      double2 x[R0], y[R0];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tbase + 32 * c, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const double2 v = bval(8 * c + u, tm2(r, u));
+          if (c < 2)
+            x[8 * c + u] = v;
+          else
+            y[8 * (c - 2) + u] = v;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < R0; ++q) {
+        double2 za, zb;
+        zsplit_pair(x[q], y[R0 - 1 - q], cmul(wk, cs[q]), za, zb);
+        x[q] = za;
+        y[R0 - 1 - q] = zb;
+      }
+      dft<R0, 1>(x);
+      dft<R0, 1>(y);
+      double2* px = sm + pidx(g * R0);
+      double2* py = sm + pidx(g2 * R0);
+#pragma unroll
+      for (int q = 0; q < R0; ++q) {  // blocks of 16 start on a padded row: offsets are immediate
+        px[q] = x[q];
+        py[q] = y[q];
+      }
+    }
+    __syncthreads();
+    long long t1 = pa.phase ? clock64() : 0;
+    first_pass_tail<R0, TT>(sm, tws, pa, a, b, BREAL);
+    __syncthreads();
+    long long t2 = pa.phase ? clock64() : 0;
+    static_pass_t<R1, L1, N, 1, TT>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
+    __syncthreads();
+    long long t3 = pa.phase ? clock64() : 0;
+    static_pass_t<R2, L2, N, 1, TT>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+    __syncthreads();
+    long long t4 = pa.phase ? clock64() : 0;
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+    static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
+    __syncthreads();
+    if (pa.phase && threadIdx.x == 0) {
+      const long long t5 = clock64();
+      atomicAdd(pa.phase + 0, static_cast<unsigned long long>(t1 - t0));
+      atomicAdd(pa.phase + 1, static_cast<unsigned long long>(t2 - t1));
+      atomicAdd(pa.phase + 2, static_cast<unsigned long long>(t3 - t2));
+      atomicAdd(pa.phase + 3, static_cast<unsigned long long>(t4 - t3));
+      atomicAdd(pa.phase + 4, static_cast<unsigned long long>(t5 - t4));
+      atomicAdd(pa.phase + 5, 1ULL);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh) : "memory");
 }
 
 // Direct windowed convolution (small n, or n beyond the single-CTA FFT).
@@ -1607,8 +1820,12 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
   const PlanArgs& a = pl.a;
   if (!(a.P == 4 && a.r[0] == R0 && a.r[1] == R1 && a.r[2] == R2 && a.r[3] == R3) || a.dbg || getenv("TGB_NO_STATIC"))
     return false;
+  const bool fused_ok = R0 == 16 && TT == 320 && a.fused;  // the spectra were written in the fused order
   auto kern = (getenv("TGB_NO_TMEM") || a.N % TT) ? pair_kernel_static<R0, R1, R2, R3, TT, BREAL>
                                                   : pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>;
+  if constexpr (R0 == 16) {
+    if (fused_ok && kern == pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>) kern = pair_kernel_fused<R0, R1, R2, R3, TT, BREAL>;
+  }
   static bool attr = false;
   if (!attr) {
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel_static<R0, R1, R2, R3, TT, BREAL>,
@@ -1618,11 +1835,19 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
+    if constexpr (R0 == 16) {
+      TGB_CUDA(cudaFuncGetAttributes(&fa, pair_kernel_fused<R0, R1, R2, R3, TT, BREAL>));
+      TGB_CUDA(cudaFuncSetAttribute(pair_kernel_fused<R0, R1, R2, R3, TT, BREAL>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
+    }
     attr = true;
   }
   int per_sm = 1;
   TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, pl.smem));
-  if (per_sm > 1 && kern == pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>) {  // TMEM: one CTA per SM
+  if (a.fused && (per_sm > 1 || !fused_ok))  // the spectra are in the fused order: only that kernel reads them
+    throw Error(TGB_CUDA_ERROR, "fftconv: fused spectrum order without the fused pair kernel");
+  if (per_sm > 1 && kern != pair_kernel_static<R0, R1, R2, R3, TT, BREAL>) {  // TMEM: one CTA per SM
     kern = pair_kernel_static<R0, R1, R2, R3, TT, BREAL>;
     TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, pl.smem));
   }
