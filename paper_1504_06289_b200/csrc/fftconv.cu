@@ -68,7 +68,7 @@ struct PlanArgs {
                          //   [off_cs]   w_m^{s N/r0}, s < r0
                          //   [off_zlo]  w_m^i, i < 64;  [off_zhi] w_m^{64 h}
                          //   [off_lo[p]] w_{L_p r_p}^i, i < 64;  [off_hi[p]] w_{L_p r_p}^{64 h}   (p >= 1)
-  int ntw, off_cs, off_zlo, off_zhi;
+  int ntw, off_cs, off_zlo, off_zhi, off_zhi2;
   int off_lo[kMaxPasses], off_hi[kMaxPasses];
   const double2* twpost; // forward post-processing: w_m^k, k <= N
   const double2* ph1;    // mode 1: e^{-i pi k (n-1)/m} * (cos(pi k/m) for even n), k <= N
@@ -267,6 +267,8 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
     for (int i = 0; i < 64; ++i) tw.push_back(unit_root(i, a.m));
     a.off_zhi = static_cast<int>(tw.size());
     for (int h = 0; h <= nblk / 64; ++h) tw.push_back(unit_root(64LL * h, a.m));
+    a.off_zhi2 = static_cast<int>(tw.size());  // w_m^{64 h}, h <= N / 64 (spectrum post-processing)
+    for (int h = 0; h <= a.N / 64; ++h) tw.push_back(unit_root(64LL * h, a.m));
     for (int p = 1; p < a.P; ++p) {
       const int64_t LR = static_cast<int64_t>(a.L[p]) * a.r[p];
       a.off_lo[p] = static_cast<int>(tw.size());
@@ -1402,20 +1404,21 @@ __global__ void __launch_bounds__(TT, 1)
   const double* x = isA ? XA + c * ldx : XB + (colidx ? colidx[c] : c) * ldx;
   const int n = pa.n;
   long long c0 = pa.phase ? clock64() : 0;
-  static_assert(N % (8 * TT) == 0, "whole batches");
+  constexpr int UB = 8;  // loads in flight per thread (20 measured no faster)
+  static_assert(N % (UB * TT) == 0, "whole batches");
 #pragma unroll 1
-  for (int k0 = threadIdx.x; k0 < N; k0 += 8 * TT) {  // 8-deep batched loads
-    double2 v[8];
-    int p[8];
+  for (int k0 = threadIdx.x; k0 < N; k0 += UB * TT) {
+    double2 v[UB];
+    int p[UB];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) {
+    for (int u = 0; u < UB; ++u) {
       const int i0 = 2 * (k0 + u * TT);
       v[u].x = i0 < n ? __ldg(x + i0) : 0.0;
       v[u].y = i0 + 1 < n ? __ldg(x + i0 + 1) : 0.0;
       p[u] = __ldg(pa.inv + k0 + u * TT);
     }
 #pragma unroll
-    for (int u = 0; u < 8; ++u) sm[pidx(p[u])] = v[u];
+    for (int u = 0; u < UB; ++u) sm[pidx(p[u])] = v[u];
   }
   __syncthreads();
   long long c1 = pa.phase ? clock64() : 0;
@@ -1430,52 +1433,46 @@ __global__ void __launch_bounds__(TT, 1)
   long long c2 = pa.phase ? clock64() : 0;
   const double hm = h / pa.m;
   const int64_t base = static_cast<int64_t>(c) * (N + 1);
-  // (1) real post-processing in natural order, one mirror pair (k, N-k) per
-  // thread, results in place: X[N-k] = conj-mirror of the X[k] terms (one
-  // twiddle per pair); k = 0 also produces the Nyquist term into slot N.
-  for (int k = threadIdx.x; k <= N / 2; k += TT) {
-    const double2 zk = sm[pidx(k)];
-    double2 zm = sm[pidx(k == 0 ? 0 : N - k)];
+  // real post-processing straight in the consumer's storage order (coalesced
+  // stores): X[k] = (z_k + conj z_{N-k})/2 - i w^-k (z_k - conj z_{N-k})/2,
+  // w^k = zlo[k % 64] zhi2[k / 64] from the shared tables; slot N = Nyquist
+  const int* order = pa.fused ? pa.kf : pa.perm;
+  const double2* zlo = tws + pa.off_zlo;
+  const double2* zhi2 = tws + pa.off_zhi2;
+  static_assert(N % (8 * TT) == 0, "whole batches");
+  auto post = [&](int pos, int k) {
+    const int kk = k == N ? 0 : k;
+    const double2 zk = sm[pidx(kk)];
+    double2 zm = sm[pidx(kk == 0 ? 0 : N - kk)];
     zm.y = -zm.y;
     const double2 sum = cadd(zk, zm), dif = csub(zk, zm);
-    double2 w = ld2(pa.twpost + k);
+    double2 w = cmul(zlo[k & 63], zhi2[k >> 6]);
     w.y = -w.y;  // w^-k
     const double2 wd = cmul(w, dif);
-    double2 xk = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
-    double2 xm;
-    if (k == 0) {  // Nyquist: w^-N = -1
-      xm = make_double2(0.5 * (sum.x - dif.y), 0.5 * (sum.y + dif.x));
-    } else {
-      xm = make_double2(0.5 * (sum.x - wd.y), 0.5 * (-sum.y - wd.x));
-    }
-    const int km = N - k;
-    if (mode == 1) {
-      const double2 t = ld2(pa.ph1 + k), tm = ld2(pa.ph1 + km);
-      xk = make_double2(hm * (xk.x * t.x - xk.y * t.y), 0.0);
-      xm = make_double2(hm * (xm.x * tm.x - xm.y * tm.y), 0.0);
+    const double2 v = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
+    if (mode == 0) {
+      static_cast<double2*>(specA)[base + pos] = v;
+    } else if (mode == 1) {
+      const double2 t = ld2(pa.ph1 + k);
+      static_cast<double*>(specB)[base + pos] = hm * (v.x * t.x - v.y * t.y);
     } else if (mode == 2) {
-      xk = cmul(xk, cscale(ld2(pa.ph2 + k), hm));
-      xm = cmul(xm, cscale(ld2(pa.ph2 + km), hm));
-    }
-    sm[pidx(k)] = xk;
-    if (k != N / 2 || k == 0) sm[pidx(k == 0 ? N : km)] = xm;
-  }
-  __syncthreads();
-  // (2) storage order: coalesced spectrum stores
-  const int* order = pa.fused ? pa.kf : pa.perm;
-  for (int pos = threadIdx.x; pos <= N; pos += TT) {
-    const int k = pos < N ? __ldg(order + pos) : N;
-    const double2 v = sm[pidx(k)];
-    if (mode == 1) {
-      static_cast<double*>(specB)[base + pos] = v.x;
-    } else if (mode == 3) {  // raw X in smem: both forms (symmetry decided later on the host)
+      static_cast<double2*>(specB)[base + pos] = cmul(v, cscale(ld2(pa.ph2 + k), hm));
+    } else {  // both forms (the symmetry is decided on the device later)
       const double2 t = ld2(pa.ph1 + k);
       static_cast<double*>(specB)[base + pos] = hm * (v.x * t.x - v.y * t.y);
       static_cast<double2*>(specB2)[base + pos] = cmul(v, cscale(ld2(pa.ph2 + k), hm));
-    } else {
-      static_cast<double2*>(isA ? specA : specB)[base + pos] = v;
     }
+  };
+  // order[] loads batched 8 deep: the loop is otherwise one L2 round trip per slot
+#pragma unroll 1
+  for (int p0 = threadIdx.x; p0 < N; p0 += 8 * TT) {
+    int kb[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) kb[u] = __ldg(order + p0 + u * TT);
+#pragma unroll
+    for (int u = 0; u < 8; ++u) post(p0 + u * TT, kb[u]);
   }
+  if (threadIdx.x == 0) post(N, N);
   if (pa.phase) {
     __syncthreads();
     if (threadIdx.x == 0) {
