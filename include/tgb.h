@@ -106,6 +106,52 @@ int tgb_scalar_product(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, double* r
 int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
                        const double h[3], double* J, int mem);
 
+/* ---- Hartree-Fock operators on the same path -------------------
+ * replaces tg::nuclear_potential_tensor (hf.hpp:29-30, hf.cpp:89-101):
+ * P_c = sum_a Z_a W_a Ptilde.  `reference` is the DOUBLED-grid kernel tensor
+ * (2 n[ax] x R per axis); `offsets` (nnuc x 3, row-major, host memory) are
+ * tg::window_for_center(grid, center_a).offset and `charges` (nnuc, host) the
+ * nuclear charges.  `out` has extents n[ax] = reference.n[ax] / 2 and rank
+ * nnuc R: columns a R + q = reference(offset_a : offset_a + n, q), weights
+ * charge_a * reference.w[q] (the reference's add() order). */
+int tgb_nuclear_potential_tensor(tgb_ctx* ctx, const tgb_cp* reference, const int64_t* offsets,
+                                 const double* charges, int64_t nnuc, tgb_cp* out, int mem);
+
+/* replaces tg::nuclear_matrix (hf.hpp:25-26, hf.cpp:103-116):
+ * V_km = -<G_k . G_m, P_c> for k <= m, mirrored.  Basis flattened as for
+ * tgb_coulomb_matrix; `pc` from tgb_nuclear_potential_tensor. */
+int tgb_nuclear_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* pc,
+                       double* V, int mem);
+
+/* replaces tg::exchange_matrix (hf.hpp:49-50, hf.cpp:153-170):
+ * K_km = sum_a h^3 <G_k . phi_a, (G_m . phi_a) * (P / h^3)>, returned as
+ * (K + K^T) / 2.  c_occ is nb x nocc (column-major, space given by `mem`);
+ * `kernel` is a PRIMARY-grid kernel tensor (doubled kernels are rejected by
+ * the caller, hf.cpp:155). */
+int tgb_exchange_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
+                        const double* c_occ, int64_t nocc, const tgb_cp* kernel, const double h[3], double* K,
+                        int mem);
+
+/* replace tg::coulomb_from_factors / exchange_from_factors / fock_from_factors
+ * (tei.hpp:76-79, tei.cpp:215-238).  chol is the TEI Cholesky factor
+ * (nb^2 x rank, column-major), density and h_core nb x nb; the result is nb x nb
+ * and exactly symmetric.  All pointers in the space given by `mem`. */
+int tgb_coulomb_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* chol, const double* density,
+                             double* J, int mem);
+int tgb_exchange_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* chol, const double* density,
+                              double* K, int mem);
+int tgb_fock_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* h_core, const double* chol,
+                          const double* density, double* F, int mem);
+
+/* replaces tg::overlap_matrix (hf.hpp:14, hf.cpp:48-58): S_km = h^3 <G_k, G_m>. */
+int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
+                       double* S, int mem);
+/* replaces tg::kinetic_matrix (hf.hpp:19-20, hf.cpp:60-87): Kronecker FEM
+ * Laplacian, lumped (exact_mass = 0) or P1 (exact_mass = 1) mass on the
+ * non-derivative axes. */
+int tgb_kinetic_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
+                       int exact_mass, double* T, int mem);
+
 /* ---- factorised two-electron integrals (proj/include/tengrid/tei.hpp:38-72) ----
  * A tgb_tei holds the device-resident factorisation (TEIFactorization,
  * tei.hpp:38-57).  The basis is given flattened as for tgb_coulomb_matrix

@@ -52,7 +52,18 @@ def rlib() -> C.CDLL | None:
         if not REF_LIB.exists():
             return None
         L = C.CDLL(str(REF_LIB))
+        P = C.c_void_p
         L.ref_last_error.restype = C.c_char_p
+        L.ref_cp_new.restype = P
+        L.ref_cp_free.argtypes = [P]
+        L.ref_cp_rank.restype = C.c_longlong
+        L.ref_cp_rank.argtypes = [P]
+        L.ref_cp_extent.restype = C.c_longlong
+        L.ref_cp_extent.argtypes = [P, C.c_int]
+        L.ref_cp_get.argtypes = [P, C.c_int, P]
+        L.ref_cp_get_w.argtypes = [P, P]
+        L.ref_tei_get.argtypes = [P, C.c_int, C.c_longlong, P]
+        L.ref_tei_free.argtypes = [P]
         L.ref_gauss_cell_integral.restype = C.c_double
         L.ref_gauss_cell_integral.argtypes = [C.c_double, C.c_double, C.c_double]
         _r = L
@@ -336,3 +347,186 @@ def pivoted_cholesky(a, tol, trace_stop: bool, max_rank: int, neg_tol: float):
                                      C.byref(res), C.byref(cl)))
     k = rank.value
     return L[:, :k].copy(order="F"), piv[:k].copy(), res.value, bool(cl.value)
+
+
+# --------------------------------------------------------------------------- hf.cpp / tei.cpp operators (§8f)
+
+def _grid_args(b_half, n):
+    b = np.ascontiguousarray(np.broadcast_to(np.asarray(b_half, dtype=np.float64), (3,)))
+    nn = (C.c_longlong * 3)(*np.broadcast_to(np.asarray(n), (3,)).tolist())
+    return b, nn
+
+
+def _handles(disc):
+    return (C.c_void_p * len(disc))(*[d.h.value for d in disc])
+
+
+def one_electron(b_half, n, disc: list, which: int) -> np.ndarray:
+    """which 0: overlap_matrix (hf.cpp:48-58); 1/2: kinetic_matrix lumped / exact mass (hf.cpp:60-87)."""
+    b, nn = _grid_args(b_half, n)
+    nb = len(disc)
+    out = np.zeros((nb, nb), order="F")
+    _chk(olib().orc_one_electron(_p(b), nn, C.c_int(nb), _handles(disc), C.c_int(which), _p(out)))
+    return out
+
+
+def nuclear_potential_tensor(b_half, n, centers, charges, ref: OCP) -> OCP:
+    """hf.cpp:89-101 on a doubled-grid reference kernel."""
+    b, nn = _grid_args(b_half, n)
+    c = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1)
+    q = np.ascontiguousarray(charges, dtype=np.float64)
+    out = OCP()
+    _chk(olib().orc_nuclear_potential_tensor(_p(b), nn, C.c_int(q.shape[0]), _p(c), _p(q), ref.h, out.h))
+    return out
+
+
+def nuclear_matrix(disc: list, pc: OCP) -> np.ndarray:
+    nb = len(disc)
+    V = np.zeros((nb, nb), order="F")
+    _chk(olib().orc_nuclear_matrix(C.c_int(nb), _handles(disc), pc.h, _p(V)))
+    return V
+
+
+def exchange_matrix(b_half, n, disc: list, c_occ, kernel: OCP) -> np.ndarray:
+    """hf.cpp:153-170 (primary-grid kernel)."""
+    b, nn = _grid_args(b_half, n)
+    c = _f(c_occ)
+    nb = len(disc)
+    K = np.zeros((nb, nb), order="F")
+    _chk(olib().orc_exchange_matrix(_p(b), nn, C.c_int(nb), _handles(disc), C.c_longlong(c.shape[1]), _p(c),
+                                    kernel.h, _p(K)))
+    return K
+
+
+def from_factors(which: int, chol, density, h_core=None) -> np.ndarray:
+    """which 0/1/2: coulomb_ / exchange_ / fock_from_factors (tei.cpp:215-238)."""
+    d = _f(density)
+    nb = d.shape[0]
+    L = _f(chol).reshape(nb * nb, -1, order="F")
+    h = _f(h_core) if h_core is not None else np.zeros((1, 1), order="F")
+    out = np.zeros((nb, nb), order="F")
+    _chk(olib().orc_from_factors(C.c_int(which), C.c_longlong(nb), C.c_longlong(L.shape[1]), _p(h), _p(L), _p(d),
+                                 _p(out)))
+    return out
+
+
+# --------------------------------------------------------------------------- the reference binary (oracle/_ref)
+
+def _basis_args(functions):
+    centers = np.ascontiguousarray([f[0] for f in functions], dtype=np.float64).reshape(-1)
+    degs = np.ascontiguousarray([f[1] for f in functions], dtype=np.int32).reshape(-1)
+    nprim = np.ascontiguousarray([len(f[2]) for f in functions], dtype=np.int32)
+    exps = np.ascontiguousarray([p[0] for f in functions for p in f[2]], dtype=np.float64)
+    coefs = np.ascontiguousarray([p[1] for f in functions for p in f[2]], dtype=np.float64)
+    return centers, degs, nprim, exps, coefs
+
+
+class Ref:
+    """Calls into the reference's own hf.cpp / tei.cpp / reduction.cpp (oracle/_ref, shim LA)."""
+
+    def __init__(self, b_half, n, functions):
+        self.R = rlib()
+        if self.R is None:
+            raise FileNotFoundError("oracle/_ref not built (needs /root/reference)")
+        self.b, self.nn = _grid_args(b_half, n)
+        self.nb = len(functions)
+        self.args = _basis_args(functions)
+        self._keep = self.args
+
+    def _basis(self):
+        c, d, npr, e, cf = self.args
+        return (_p(self.b), self.nn, C.c_int(self.nb), _p(c), _p(d), _p(npr), _p(e), _p(cf))
+
+    def _chk(self, rc):
+        if rc:
+            raise OracleError(rc, self.R.ref_last_error().decode())
+
+    def one_electron(self, which: int) -> np.ndarray:
+        out = np.zeros((self.nb, self.nb), order="F")
+        self._chk(self.R.ref_one_electron(*self._basis(), C.c_int(which), _p(out)))
+        return out
+
+    def nuclear(self, centers, charges, m: int, c0: float):
+        c = np.ascontiguousarray(centers, dtype=np.float64).reshape(-1)
+        q = np.ascontiguousarray(charges, dtype=np.float64)
+        V = np.zeros((self.nb, self.nb), order="F")
+        pc = OCP(lib=self.R)
+        self._chk(self.R.ref_nuclear(*self._basis(), C.c_int(q.shape[0]), _p(q), _p(c), C.c_longlong(m),
+                                     C.c_double(c0), _p(V), pc.h))
+        return V, pc
+
+    def coulomb_matrix(self, vh: OCP) -> np.ndarray:
+        J = np.zeros((self.nb, self.nb), order="F")
+        self._chk(self.R.ref_coulomb_matrix(*self._basis(), vh.h, _p(J)))
+        return J
+
+    def exchange_matrix(self, c_occ, m: int, c0: float) -> np.ndarray:
+        c = _f(c_occ)
+        K = np.zeros((self.nb, self.nb), order="F")
+        self._chk(self.R.ref_exchange_matrix(*self._basis(), C.c_longlong(c.shape[1]), _p(c), C.c_longlong(m),
+                                             C.c_double(c0), _p(K)))
+        return K
+
+    def density_tensor(self, c_occ, eps: float) -> OCP:
+        c = _f(c_occ)
+        out = OCP(lib=self.R)
+        self._chk(self.R.ref_density_tensor(*self._basis(), C.c_longlong(c.shape[1]), _p(c), C.c_double(eps),
+                                            out.h))
+        return out
+
+    def build_tei(self, m: int, c0: float, eps_fit: float, eps_chol: float):
+        """(fit ranks, R_B, clamped, fit residuals, chol, diagonal)."""
+        info = (C.c_longlong * 5)()
+        res = np.zeros(3)
+        h = C.c_void_p()
+        self._chk(self.R.ref_build_tei(*self._basis(), C.c_longlong(m), C.c_double(c0), C.c_double(eps_fit),
+                                       C.c_double(eps_chol), info, _p(res), C.byref(h)))
+        try:
+            nb2 = self.nb * self.nb
+            chol = np.zeros((nb2, info[3]), order="F")
+            diag = np.zeros(nb2)
+            self._chk(self.R.ref_tei_get(h, 0, 0, _p(chol)))
+            self._chk(self.R.ref_tei_get(h, 1, 0, _p(diag)))
+        finally:
+            self.R.ref_tei_free(h)
+        return (info[0], info[1], info[2]), info[3], bool(info[4]), res, chol, diag
+
+
+def ref_from_factors(which: int, chol, density, h_core=None) -> np.ndarray:
+    R = rlib()
+    d = _f(density)
+    nb = d.shape[0]
+    L = _f(chol).reshape(nb * nb, -1, order="F")
+    h = _f(h_core) if h_core is not None else np.zeros((1, 1), order="F")
+    out = np.zeros((nb, nb), order="F")
+    rc = R.ref_from_factors(C.c_int(which), C.c_longlong(nb), C.c_longlong(L.shape[1]), _p(h), _p(L), _p(d), _p(out))
+    if rc:
+        raise OracleError(rc, R.ref_last_error().decode())
+    return out
+
+
+def ref_generalized_eigensolve(f, s):
+    R = rlib()
+    f, s = _f(f), _f(s)
+    nb = f.shape[0]
+    c = np.zeros((nb, nb), order="F")
+    e = np.zeros(nb)
+    rc = R.ref_generalized_eigensolve(C.c_longlong(nb), _p(f), _p(s), _p(c), _p(e))
+    if rc:
+        raise OracleError(rc, R.ref_last_error().decode())
+    return c, e
+
+
+def ref_reduce(a: OCP, eps: float | None = None, ranks=None, sweeps: int = 3, mode: int = 2):
+    """The reference's rhosvd (0) / canonical_to_tucker (1) / reduce_rank (2) on a tensor held by
+    the reference library; returns (info dict, canonical OCP)."""
+    R = rlib()
+    info = (C.c_longlong * 7)()
+    rk = (C.c_longlong * 3)(*(ranks or (0, 0, 0)))
+    out = OCP(lib=R)
+    rc = R.ref_reduce(a.h, C.c_int(eps is not None), C.c_double(eps or 0.0), rk, C.c_int(sweeps), C.c_int(mode),
+                      info, out.h)
+    if rc:
+        raise OracleError(rc, R.ref_last_error().decode())
+    return {"ranks": (info[0], info[1], info[2]), "rank_clamped": bool(info[3]), "rhosvd_fallback": bool(info[4]),
+            "sweeps": info[5], "canonical_rank": info[6]}, out

@@ -180,6 +180,54 @@ int orc_density_tensor(int nb, void** disc_handles, long long nocc, const double
   });
 }
 
+// ---- hf.cpp / tei.cpp operators
+static std::vector<CP3> disc_from(int nb, void** h) {
+  std::vector<CP3> disc;
+  for (int i = 0; i < nb; ++i) disc.push_back(*static_cast<CP3*>(h[i]));
+  return disc;
+}
+int orc_one_electron(const double* b, const long long* n, int nb, void** disc_handles, int which, double* out) {
+  return guard([&] {
+    const auto disc = disc_from(nb, disc_handles);
+    const Grid g = grid_from(b, n);
+    Mat m = which == 0 ? overlap_matrix(g, disc) : kinetic_matrix(g, disc, which == 2);
+    if (!m.d.empty()) std::memcpy(out, m.d.data(), sizeof(double) * m.d.size());
+  });
+}
+int orc_nuclear_potential_tensor(const double* b, const long long* n, int nnuc, const double* centers,
+                                 const double* charges, void* ref, void* out) {
+  return guard([&] {
+    std::vector<std::array<double, 3>> c(nnuc);
+    for (int a = 0; a < nnuc; ++a) c[a] = {centers[3 * a], centers[3 * a + 1], centers[3 * a + 2]};
+    *static_cast<CP3*>(out) =
+        nuclear_potential_tensor(grid_from(b, n), c, Vec(charges, charges + nnuc), *static_cast<CP3*>(ref));
+  });
+}
+int orc_nuclear_matrix(int nb, void** disc_handles, void* pc, double* V) {
+  return guard([&] {
+    Mat v = nuclear_matrix(disc_from(nb, disc_handles), *static_cast<CP3*>(pc));
+    if (!v.d.empty()) std::memcpy(V, v.d.data(), sizeof(double) * v.d.size());
+  });
+}
+int orc_exchange_matrix(const double* b, const long long* n, int nb, void** disc_handles, long long nocc,
+                        const double* c_occ, void* kernel, double* K) {
+  return guard([&] {
+    Mat k = exchange_matrix(grid_from(b, n), disc_from(nb, disc_handles), mat_from(c_occ, nb, nocc),
+                            *static_cast<CP3*>(kernel));
+    if (!k.d.empty()) std::memcpy(K, k.d.data(), sizeof(double) * k.d.size());
+  });
+}
+int orc_from_factors(int which, long long nb, long long rank, const double* h_core, const double* chol,
+                     const double* density, double* out) {
+  return guard([&] {
+    const Mat l = mat_from(chol, nb * nb, rank), d = mat_from(density, nb, nb);
+    Mat r = which == 0 ? coulomb_from_factors(l, d)
+            : which == 1 ? exchange_from_factors(l, d)
+                         : fock_from_factors(mat_from(h_core, nb, nb), l, d);
+    if (!r.d.empty()) std::memcpy(out, r.d.data(), sizeof(double) * r.d.size());
+  });
+}
+
 // ---- reduction
 int orc_thin_svd_left(long long r, long long c, const double* a, double* u_out, double* s_out, long long* kept) {
   return guard([&] {

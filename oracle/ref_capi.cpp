@@ -10,6 +10,9 @@
 
 #include "tengrid/basis.hpp"
 #include "tengrid/fft.hpp"
+#include "tengrid/hf.hpp"
+#include "tengrid/reduction.hpp"
+#include "tengrid/tei.hpp"
 #include "tengrid/grid.hpp"
 #include "tengrid/kernel.hpp"
 #include "tengrid/lattice.hpp"
@@ -45,6 +48,36 @@ Eigen::MatrixXd mat(const double* p, long long r, long long c) {
   return m;
 }
 tg::Grid3 grid(const double* b, const long long* n) { return tg::make_grid({b[0], b[1], b[2]}, {n[0], n[1], n[2]}); }
+// basis given as in ref_discretize_basis
+struct BasisArgs {
+  const double* b;
+  const long long* n;
+  int nfn;
+  const double* centers;
+  const int* degs;
+  const int* nprim;
+  const double* exps;
+  const double* coefs;
+};
+tg::BasisSet basis_set(const BasisArgs& a) {
+  tg::BasisSet bs;
+  bs.grid = grid(a.b, a.n);
+  int off = 0;
+  for (int i = 0; i < a.nfn; ++i) {
+    tg::SeparableBasisFunction f;
+    for (int ax = 0; ax < 3; ++ax) {
+      f.center[ax] = a.centers[3 * i + ax];
+      f.degree[ax] = a.degs[3 * i + ax];
+    }
+    for (int p = 0; p < a.nprim[i]; ++p) f.primitives.push_back({a.exps[off + p], a.coefs[off + p]});
+    off += a.nprim[i];
+    bs.functions.push_back(f);
+  }
+  return bs;
+}
+void put(const Eigen::MatrixXd& m, double* out) {
+  if (m.size()) std::memcpy(out, m.data(), sizeof(double) * m.size());
+}
 }  // namespace
 
 extern "C" {
@@ -180,6 +213,124 @@ int ref_lattice_sum_canonical(const long long* counts, double spacing, double ch
     tg::AssembledPotential ap = tg::lattice_sum_canonical(spec, g, ref);
     *static_cast<tg::CanonicalTensor3*>(out) = *ap.canonical;
     *window_ops = ap.window_ops;
+  });
+}
+
+// ---- hf.cpp / tei.cpp / reduction.cpp (compiled against the shim's stand-in LA)
+#define TG_BASIS_ARGS const double *b, const long long *n, int nfn, const double *centers, const int *degs, \
+                      const int *nprim, const double *exps, const double *coefs
+#define TG_BASIS BasisArgs{b, n, nfn, centers, degs, nprim, exps, coefs}
+
+// which: 0 overlap_matrix, 1 kinetic_matrix (lumped), 2 kinetic_matrix (exact mass)   hf.cpp:48-87
+int ref_one_electron(TG_BASIS_ARGS, int which, double* out) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    const auto disc = tg::discretize_basis(bs);
+    put(which == 0 ? tg::overlap_matrix(bs, disc) : tg::kinetic_matrix(bs, disc, which == 2), out);
+  });
+}
+// nuclear_potential_tensor + nuclear_matrix with the doubled Newton reference (m, c0)   hf.cpp:89-116
+int ref_nuclear(TG_BASIS_ARGS, int nnuc, const double* charges, const double* ncenters, long long m, double c0,
+                double* V, void* pc_out) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    const auto disc = tg::discretize_basis(bs);
+    tg::Molecule mol;
+    for (int a = 0; a < nnuc; ++a) mol.nuclei.push_back({charges[a], {ncenters[3 * a], ncenters[3 * a + 1], ncenters[3 * a + 2]}});
+    const tg::KernelTensor ref = tg::kernel_tensor(bs.grid, tg::make_expsum(m, c0), true);
+    if (pc_out) *static_cast<tg::CanonicalTensor3*>(pc_out) = tg::nuclear_potential_tensor(bs, mol, ref);
+    if (V) put(tg::nuclear_matrix(bs, disc, mol, ref), V);
+  });
+}
+int ref_coulomb_matrix(TG_BASIS_ARGS, void* vh, double* J) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    put(tg::coulomb_matrix(bs, tg::discretize_basis(bs), *static_cast<tg::CanonicalTensor3*>(vh)), J);
+  });
+}
+int ref_exchange_matrix(TG_BASIS_ARGS, long long nocc, const double* c_occ, long long m, double c0, double* K) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    const tg::KernelTensor kern = tg::kernel_tensor(bs.grid, tg::make_expsum(m, c0), false);
+    put(tg::exchange_matrix(bs, tg::discretize_basis(bs), mat(c_occ, nfn, nocc), kern), K);
+  });
+}
+int ref_density_tensor(TG_BASIS_ARGS, long long nocc, const double* c_occ, double eps, void* out) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    *static_cast<tg::CanonicalTensor3*>(out) = tg::density_tensor(tg::discretize_basis(bs), mat(c_occ, nfn, nocc), eps);
+  });
+}
+// which: 0 coulomb_from_factors, 1 exchange_from_factors, 2 fock_from_factors   tei.cpp:215-238
+int ref_from_factors(int which, long long nb, long long rank, const double* h_core, const double* chol,
+                     const double* density, double* out) {
+  return guard([&] {
+    const Eigen::MatrixXd l = mat(chol, nb * nb, rank), d = mat(density, nb, nb);
+    if (which == 0) put(tg::coulomb_from_factors(l, d), out);
+    if (which == 1) put(tg::exchange_from_factors(l, d), out);
+    if (which == 2) put(tg::fock_from_factors(mat(h_core, nb, nb), l, d), out);
+  });
+}
+int ref_generalized_eigensolve(long long nb, const double* f, const double* s, double* c, double* e) {
+  return guard([&] {
+    Eigen::MatrixXd cc;
+    Eigen::VectorXd ee;
+    tg::generalized_eigensolve(mat(f, nb, nb), mat(s, nb, nb), cc, ee);
+    put(cc, c);
+    put(ee, e);
+  });
+}
+// build_tei with a primary Newton kernel (m, c0); info = {R_l[3], R_B, clamped}; chol / pivots optional
+int ref_build_tei(TG_BASIS_ARGS, long long m, double c0, double eps_fit, double eps_chol, long long* info,
+                  double* fit_residual, void** handle) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    const tg::KernelTensor kern = tg::kernel_tensor(bs.grid, tg::make_expsum(m, c0), false);
+    auto* fac = new tg::TEIFactorization(tg::build_tei(bs, tg::discretize_basis(bs), kern, eps_fit, eps_chol));
+    for (int ax = 0; ax < 3; ++ax) {
+      info[ax] = fac->fit_ranks()[ax];
+      fit_residual[ax] = fac->fit_residual[ax];
+    }
+    info[3] = fac->rank_b();
+    info[4] = fac->fit_clamped_negative ? 1 : 0;
+    *handle = fac;
+  });
+}
+void ref_tei_free(void* h) { delete static_cast<tg::TEIFactorization*>(h); }
+// what: 0 chol (nb^2 x R_B), 1 tei_diagonal (nb^2), 2 tei_column(j) (nb^2)
+int ref_tei_get(void* h, int what, long long j, double* out) {
+  return guard([&] {
+    auto& f = *static_cast<tg::TEIFactorization*>(h);
+    if (what == 0) put(f.chol, out);
+    if (what == 1) put(tg::tei_diagonal(f), out);
+    if (what == 2) put(tg::tei_column(f, j), out);
+  });
+}
+// mode 0 rhosvd, 1 canonical_to_tucker, 2 reduce_rank (C2T + T2C); ranks used when use_eps == 0.
+// info = {r0, r1, r2, rank_clamped, rhosvd_fallback, sweeps, canonical rank}
+int ref_reduce(void* a, int use_eps, double eps, const long long* ranks, int sweeps, int mode, long long* info,
+               void* out_cp) {
+  return guard([&] {
+    const auto& t = *static_cast<tg::CanonicalTensor3*>(a);
+    const tg::ReductionConfig cfg = use_eps ? tg::ReductionConfig::tolerance(eps, sweeps)
+                                            : tg::ReductionConfig::fixed(ranks[0], ranks[1], ranks[2], sweeps);
+    if (mode == 2) {
+      tg::CanonicalTensor3 c = tg::reduce_rank(t, cfg);
+      info[6] = c.rank();
+      if (out_cp) *static_cast<tg::CanonicalTensor3*>(out_cp) = std::move(c);
+      return;
+    }
+    tg::TuckerResult r = mode == 0 ? tg::rhosvd(t, cfg) : tg::canonical_to_tucker(t, cfg);
+    const auto rk = r.tucker.ranks();
+    for (int ax = 0; ax < 3; ++ax) info[ax] = rk[ax];
+    info[3] = r.rank_clamped;
+    info[4] = r.rhosvd_fallback;
+    info[5] = static_cast<long long>(r.sweep_fits.size());
+    if (out_cp) {
+      tg::CanonicalTensor3 c = tg::tucker_to_canonical(r.tucker);
+      info[6] = c.rank();
+      *static_cast<tg::CanonicalTensor3*>(out_cp) = std::move(c);
+    }
   });
 }
 }  // extern "C"

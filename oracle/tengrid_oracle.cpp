@@ -993,6 +993,174 @@ Mat coulomb_matrix(const Grid& g, const std::vector<CP3>& disc, const CP3& vh) {
   return j;
 }
 
+// S_km = h^3 <G_k, G_m>   (hf.cpp:48-58)
+Mat overlap_matrix(const Grid& g, const std::vector<CP3>& disc) {
+  const idx nb = static_cast<idx>(disc.size());
+  const double vol = g.h[0] * g.h[1] * g.h[2];
+  Mat s(nb, nb);
+  for (idx k = 0; k < nb; ++k)
+    for (idx m = k; m < nb; ++m) {
+      s(k, m) = vol * scalar_product(disc[k], disc[m]);
+      s(m, k) = s(k, m);
+    }
+  return s;
+}
+
+// u^T tridiag{-1,2,-1} v and u^T tridiag{1,4,1} v / 6   (hf.cpp:13-37)
+static double stencil_form(const double* u, const double* v, idx n) {
+  double s = 0.0;
+  for (idx i = 0; i < n; ++i) {
+    double av = 2.0 * v[i];
+    if (i > 0) av -= v[i - 1];
+    if (i + 1 < n) av -= v[i + 1];
+    s += u[i] * av;
+  }
+  return s;
+}
+static double mass_form(const double* u, const double* v, idx n) {
+  double s = 0.0;
+  for (idx i = 0; i < n; ++i) {
+    double av = 4.0 * v[i];
+    if (i > 0) av += v[i - 1];
+    if (i + 1 < n) av += v[i + 1];
+    s += u[i] * av;
+  }
+  return s / 6.0;
+}
+
+// T_km = 1/2 sum_ij w_i w_j sum_ax stiff_ax mass_{ax+1} mass_{ax+2}   (hf.cpp:60-87)
+Mat kinetic_matrix(const Grid& g, const std::vector<CP3>& disc, bool exact_mass) {
+  const idx nb = static_cast<idx>(disc.size());
+  Mat t(nb, nb);
+  for (idx k = 0; k < nb; ++k)
+    for (idx m = k; m < nb; ++m) {
+      const CP3& a = disc[k];
+      const CP3& b = disc[m];
+      double sum = 0.0;
+      for (idx i = 0; i < a.rank(); ++i)
+        for (idx j = 0; j < b.rank(); ++j) {
+          const double w = a.w[i] * b.w[j];
+          double stiff[3], mass[3];
+          for (int ax = 0; ax < 3; ++ax) {
+            const idx n = a.f[ax].rows;
+            const double* u = a.f[ax].col(i);
+            const double* v = b.f[ax].col(j);
+            stiff[ax] = stencil_form(u, v, n) / g.h[ax];
+            double dot = 0.0;
+            for (idx r = 0; r < n; ++r) dot += u[r] * v[r];
+            mass[ax] = exact_mass ? g.h[ax] * mass_form(u, v, n) : g.h[ax] * dot;
+          }
+          for (int ax = 0; ax < 3; ++ax) sum += w * stiff[ax] * mass[(ax + 1) % 3] * mass[(ax + 2) % 3];
+        }
+      t(k, m) = 0.5 * sum;
+      t(m, k) = t(k, m);
+    }
+  return t;
+}
+
+// P_c = sum_a Z_a W_a Ptilde: windows of the doubled reference   (hf.cpp:89-101)
+CP3 nuclear_potential_tensor(const Grid& g, const std::vector<std::array<double, 3>>& centers, const Vec& charges,
+                             const CP3& ref) {
+  for (int ax = 0; ax < 3; ++ax)
+    req(ref.extent(ax) == 2 * g.n[ax], "nuclear_potential_tensor: reference kernel must live on the doubled grid");
+  CP3 pc = zero_cp(g.n);
+  for (size_t a = 0; a < centers.size(); ++a) {
+    CP3 sh;
+    sh.w.resize(ref.w.size());
+    for (size_t q = 0; q < ref.w.size(); ++q) sh.w[q] = charges[a] * ref.w[q];
+    for (int ax = 0; ax < 3; ++ax) {
+      const idx ofs = window_offset(g, ax, centers[a][ax]);
+      sh.f[ax] = Mat(g.n[ax], ref.rank());
+      for (idx q = 0; q < ref.rank(); ++q)
+        for (idx i = 0; i < g.n[ax]; ++i) sh.f[ax](i, q) = ref.f[ax](ofs + i, q);
+    }
+    pc = add(pc, sh);
+  }
+  return pc;
+}
+
+// V_km = -<G_k . G_m, P_c>   (hf.cpp:103-116)
+Mat nuclear_matrix(const std::vector<CP3>& disc, const CP3& pc) {
+  const idx nb = static_cast<idx>(disc.size());
+  Mat v(nb, nb);
+  for (idx k = 0; k < nb; ++k)
+    for (idx m = k; m < nb; ++m) {
+      v(k, m) = -scalar_product(hadamard(disc[k], disc[m]), pc);
+      v(m, k) = v(k, m);
+    }
+  return v;
+}
+
+// K_km = sum_a h^3 <G_k . phi_a, (G_m . phi_a) * P/h^3>, symmetrised   (hf.cpp:153-170)
+Mat exchange_matrix(const Grid& g, const std::vector<CP3>& disc, const Mat& c_occ, const CP3& kernel) {
+  const idx nb = static_cast<idx>(disc.size());
+  const double vol = g.h[0] * g.h[1] * g.h[2];
+  const double inv_vol = 1.0 / vol;
+  Mat k_mat(nb, nb);
+  const CP3 kscaled = scaled(kernel, inv_vol);
+  for (idx a = 0; a < c_occ.cols; ++a) {
+    CP3 phi = zero_cp(g.n);
+    for (idx k = 0; k < nb; ++k) {
+      if (c_occ(k, a) == 0.0) continue;
+      phi = add(phi, scaled(disc[k], c_occ(k, a)));
+    }
+    std::vector<CP3> g_phi(nb);
+    for (idx m = 0; m < nb; ++m) g_phi[m] = hadamard(disc[m], phi);
+    for (idx m = 0; m < nb; ++m) {
+      const CP3 v_m = convolve(g_phi[m], kscaled, g.h);
+      for (idx k = 0; k < nb; ++k) k_mat(k, m) += vol * scalar_product(g_phi[k], v_m);
+    }
+  }
+  Mat out(nb, nb);
+  for (idx j = 0; j < nb; ++j)
+    for (idx i = 0; i < nb; ++i) out(i, j) = 0.5 * (k_mat(i, j) + k_mat(j, i));
+  return out;
+}
+
+// vec_j = L (L^T vec_d), J = (j + j^T) / 2   (tei.cpp:215-223)
+Mat coulomb_from_factors(const Mat& chol, const Mat& d) {
+  const idx n = d.rows;
+  req(chol.rows == n * n && d.cols == n, "coulomb_from_factors: shape mismatch");
+  Vec t(chol.cols, 0.0), vj(n * n, 0.0);
+  for (idx s = 0; s < chol.cols; ++s) {
+    double acc = 0.0;
+    for (idx r = 0; r < n * n; ++r) acc += chol(r, s) * d.d[r];
+    t[s] = acc;
+  }
+  for (idx s = 0; s < chol.cols; ++s)
+    for (idx r = 0; r < n * n; ++r) vj[r] += chol(r, s) * t[s];
+  Mat j(n, n);
+  for (idx c = 0; c < n; ++c)
+    for (idx r = 0; r < n; ++r) j(r, c) = 0.5 * (vj[r + n * c] + vj[c + n * r]);
+  return j;
+}
+
+// k = -1/2 sum_s M_s D M_s^T, K = (k + k^T) / 2   (tei.cpp:225-234)
+Mat exchange_from_factors(const Mat& chol, const Mat& d) {
+  const idx n = d.rows;
+  req(chol.rows == n * n && d.cols == n, "exchange_from_factors: shape mismatch");
+  Mat k(n, n);
+  for (idx s = 0; s < chol.cols; ++s) {
+    Mat m(n, n);
+    std::memcpy(m.d.data(), chol.col(s), sizeof(double) * n * n);
+    const Mat md = matmul(m, false, d, false);
+    const Mat mdm = matmul(md, false, m, true);
+    for (idx r = 0; r < n * n; ++r) k.d[r] -= 0.5 * mdm.d[r];
+  }
+  Mat out(n, n);
+  for (idx c = 0; c < n; ++c)
+    for (idx r = 0; r < n; ++r) out(r, c) = 0.5 * (k(r, c) + k(c, r));
+  return out;
+}
+
+// F = h_core + J + K   (tei.cpp:236-238)
+Mat fock_from_factors(const Mat& h_core, const Mat& chol, const Mat& d) {
+  const Mat j = coulomb_from_factors(chol, d), k = exchange_from_factors(chol, d);
+  Mat f(h_core.rows, h_core.cols);
+  for (size_t r = 0; r < f.d.size(); ++r) f.d[r] = (h_core.d[r] + j.d[r]) + k.d[r];
+  return f;
+}
+
 // ---------------------------------------------------------------- lattice.cpp
 
 Mat assemble_axis(const Grid& g, const Mat& ref, int ax, const std::vector<double>& centers, idx* ops) {  // lattice.cpp:50-61

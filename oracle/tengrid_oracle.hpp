@@ -113,6 +113,15 @@ CP3 reduce_rank(const CP3& a, const RedCfg& c);
 CP3 density_tensor(const std::vector<CP3>& disc, const Mat& c_occ, double eps);
 CP3 hartree_potential(const CP3& theta, const CP3& kernel, const std::array<double, 3>& h);
 Mat coulomb_matrix(const Grid& g, const std::vector<CP3>& disc, const CP3& vh);
+Mat overlap_matrix(const Grid& g, const std::vector<CP3>& disc);
+Mat kinetic_matrix(const Grid& g, const std::vector<CP3>& disc, bool exact_mass);
+CP3 nuclear_potential_tensor(const Grid& g, const std::vector<std::array<double, 3>>& centers, const Vec& charges,
+                             const CP3& ref);
+Mat nuclear_matrix(const std::vector<CP3>& disc, const CP3& pc);
+Mat exchange_matrix(const Grid& g, const std::vector<CP3>& disc, const Mat& c_occ, const CP3& kernel);
+Mat coulomb_from_factors(const Mat& chol, const Mat& d);
+Mat exchange_from_factors(const Mat& chol, const Mat& d);
+Mat fock_from_factors(const Mat& h_core, const Mat& chol, const Mat& d);
 
 // lattice.cpp
 Mat assemble_axis(const Grid& g, const Mat& ref, int ax, const std::vector<double>& centers, idx* ops);

@@ -75,6 +75,14 @@ def lib() -> C.CDLL:
             "tgb_scalar_product": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), C.POINTER(D), I]),
             "tgb_coulomb_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, P, I]),
             "tgb_lattice_assemble_axis": (I, [P, I64, I64, P, P, I64, P, I]),
+            "tgb_nuclear_potential_tensor": (I, [P, C.POINTER(tgb_cp), P, P, I64, C.POINTER(tgb_cp), I]),
+            "tgb_nuclear_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, I]),
+            "tgb_exchange_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, I64, C.POINTER(tgb_cp), P, P, I]),
+            "tgb_coulomb_from_factors": (I, [P, I64, I64, P, P, P, I]),
+            "tgb_exchange_from_factors": (I, [P, I64, I64, P, P, P, I]),
+            "tgb_fock_from_factors": (I, [P, I64, I64, P, P, P, P, I]),
+            "tgb_overlap_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, P, I]),
+            "tgb_kinetic_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, I, P, I]),
             "tgb_tei_create": (I, [C.POINTER(P)]),
             "tgb_tei_destroy": (I, [P]),
             "tgb_tei_density_fitting": (I, [P, P, C.POINTER(tgb_cp), P, I64, P, D, I]),

@@ -35,17 +35,32 @@ def _run(cmd: list[str]) -> None:
 
 
 def build_lib(force: bool = False) -> Path:
+    """Each source compiles to its own object (in parallel, only when stale),
+    then one link; objects live in build/ (git-ignored)."""
+    from concurrent.futures import ThreadPoolExecutor
+
     srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
-    deps = srcs + sorted(CSRC.glob("*.hpp")) + [ROOT / "include" / "tgb.h"]
-    deps += sorted((ROOT / "include" / "tengrid_b200").glob("*.hpp"))
-    if not force and not _stale(LIB, deps):
+    hdrs = sorted(CSRC.glob("*.hpp")) + [ROOT / "include" / "tgb.h"]
+    hdrs += sorted((ROOT / "include" / "tengrid_b200").glob("*.hpp"))
+    objdir = ROOT / "build" / "libtgb"
+    objdir.mkdir(parents=True, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xptxas", "-v" if os.environ.get("TGB_PTXAS_VERBOSE") else "-O3",
+             "-I", str(ROOT / "include"), "-I", str(CSRC)]
+    objs = [objdir / (s.name + ".o") for s in srcs]
+    todo = [(s, o) for s, o in zip(srcs, objs) if force or _stale(o, [s, *hdrs])]
+
+    def compile_one(so):
+        s, o = so
+        _run([NVCC, *flags, "-c", str(s), "-o", str(o)])
+
+    if todo:
+        with ThreadPoolExecutor(max_workers=min(8, len(todo))) as ex:
+            list(ex.map(compile_one, todo))
+    if not force and not todo and not _stale(LIB, objs):
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-Xptxas", "-v" if os.environ.get("TGB_PTXAS_VERBOSE") else "-O3",
-           "-I", str(ROOT / "include"), "-I", str(CSRC),
-           *[str(s) for s in srcs], "-o", str(tmp)]
-    _run(cmd)
+    _run([NVCC, *ARCH, "-shared", *[str(o) for o in objs], "-o", str(tmp)])
     tmp.replace(LIB)
     return LIB
 
@@ -61,18 +76,21 @@ def build_oracle(force: bool = False) -> Path:
     return ORACLE_LIB
 
 
-REF_TUS = ["fft.cpp", "tensor.cpp", "grid.cpp", "kernel.cpp", "basis.cpp", "lattice.cpp", "parallel.cpp"]
+REF_TUS = ["fft.cpp", "tensor.cpp", "grid.cpp", "kernel.cpp", "basis.cpp", "lattice.cpp", "parallel.cpp",
+           "hf.cpp", "tei.cpp", "reduction.cpp", "mp2.cpp"]
 
 
 def build_ref(force: bool = False) -> Path | None:
-    """Compile the reference's own conv-path translation units (read in place
-    from /root/reference) against oracle/eigen_shim -> oracle/_ref/.  Only
+    """Compile the reference's own translation units (read in place from
+    /root/reference) against oracle/eigen_shim -> oracle/_ref/; the shim's
+    dense decompositions come from the restatement's LA (tengrid_oracle.cpp).  Only
     possible where /root/reference exists (this container); the GPU box uses
     the prebuilt library that travels with the snapshot."""
     if not REFERENCE.exists():
         return REF_LIB if REF_LIB.exists() else None
-    srcs = [REFERENCE / "src" / t for t in REF_TUS] + [ORACLE_DIR / "ref_capi.cpp", ORACLE_DIR / "ref_support.cpp"]
-    deps = srcs + sorted((ORACLE_DIR / "eigen_shim" / "Eigen").glob("*"))
+    srcs = [REFERENCE / "src" / t for t in REF_TUS] + [ORACLE_DIR / "ref_capi.cpp", ORACLE_DIR / "ref_support.cpp",
+                                                      ORACLE_DIR / "tengrid_oracle.cpp"]
+    deps = srcs + sorted((ORACLE_DIR / "eigen_shim" / "Eigen").glob("*")) + [ORACLE_DIR / "tengrid_oracle.hpp"]
     if not all(s.exists() for s in srcs):
         return None
     if not force and not _stale(REF_LIB, deps):

@@ -333,6 +333,185 @@ int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offs
   });
 }
 
+namespace {
+void check_basis(const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const char* what) {
+  check_cp(basis, what);
+  tgb::require(nb >= 0 && fn_offset && fn_offset[0] == 0 && fn_offset[nb] == basis->rank,
+               std::string(what) + ": bad basis function offsets");
+  for (int64_t k = 0; k < nb; ++k) tgb::require(fn_offset[k + 1] > fn_offset[k], std::string(what) + ": empty function");
+}
+
+// copy a small host-side result matrix to `dst` in the call's memory space
+void put_result(double* dst, const std::vector<double>& v, int mem) {
+  if (v.empty()) return;
+  if (mem == TGB_MEM_DEVICE)
+    TGB_CUDA(cudaMemcpy(dst, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+  else
+    std::memcpy(dst, v.data(), v.size() * sizeof(double));
+}
+}  // namespace
+
+int tgb_nuclear_potential_tensor(tgb_ctx* ctx, const tgb_cp* reference, const int64_t* offsets,
+                                 const double* charges, int64_t nnuc, tgb_cp* out, int mem) {
+  return guarded([&] {
+    check_cp(reference, "nuclear_potential_tensor");
+    tgb::require(out != nullptr, "nuclear_potential_tensor: null output");
+    tgb::require(nnuc >= 0 && (nnuc == 0 || (offsets && charges)), "nuclear_potential_tensor: bad nuclei");
+    int64_t n[3];
+    for (int ax = 0; ax < 3; ++ax) {
+      tgb::require(reference->n[ax] % 2 == 0 && reference->n[ax] > 0,
+                   "nuclear_potential_tensor: reference kernel must live on the doubled grid");
+      n[ax] = reference->n[ax] / 2;
+      tgb::require(out->n[ax] == n[ax], "nuclear_potential_tensor: output extent mismatch");
+      for (int64_t a = 0; a < nnuc; ++a)
+        tgb::require(offsets[3 * a + ax] >= 0 && offsets[3 * a + ax] + n[ax] <= 2 * n[ax],
+                     "window_offset: window escapes the doubled grid");
+    }
+    tgb::require(out->rank == nnuc * reference->rank, "nuclear_potential_tensor: output rank must be nnuc * R");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::nuclear_potential_dev(ctx, *reference, n, offsets, charges, nnuc, *out);
+      return;
+    }
+    tgb::require(mem == TGB_MEM_HOST, "nuclear_potential_tensor: bad memory space");
+    if (out->rank == 0) return;
+    DevCP dr(reference, false);
+    tgb_cp dout = *out;
+    std::vector<double*> bufs;
+    for (int ax = 0; ax < 3; ++ax) {
+      TGB_CUDA(cudaMalloc(&dout.factor[ax], n[ax] * out->rank * sizeof(double)));
+      bufs.push_back(dout.factor[ax]);
+    }
+    TGB_CUDA(cudaMalloc(&dout.weight, out->rank * sizeof(double)));
+    bufs.push_back(dout.weight);
+    try {
+      tgb::nuclear_potential_dev(ctx, dr.t, n, offsets, charges, nnuc, dout);
+      for (int ax = 0; ax < 3; ++ax)
+        TGB_CUDA(cudaMemcpyAsync(out->factor[ax], dout.factor[ax], n[ax] * out->rank * sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaMemcpyAsync(out->weight, dout.weight, out->rank * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      for (double* p : bufs) cudaFree(p);
+      throw;
+    }
+    for (double* p : bufs) cudaFree(p);
+  });
+}
+
+int tgb_nuclear_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* pc,
+                       double* V, int mem) {
+  return guarded([&] {
+    check_basis(basis, fn_offset, nb, "nuclear_matrix");
+    check_cp(pc, "nuclear_matrix");
+    check_extents(basis, pc, "nuclear_matrix");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCP db(basis, mem == TGB_MEM_DEVICE), dp(pc, mem == TGB_MEM_DEVICE);
+    std::vector<double> hv(nb * nb);
+    // V_km = -scalar_product(hadamard(G_k, G_m), P_c)  (hf.cpp:111-112)
+    tgb::coulomb_matrix_dev(ctx, db.t, fn_offset, nb, dp.t, -1.0, hv.data());
+    put_result(V, hv, mem);
+  });
+}
+
+int tgb_exchange_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
+                        const double* c_occ, int64_t nocc, const tgb_cp* kernel, const double h[3], double* K,
+                        int mem) {
+  return guarded([&] {
+    check_basis(basis, fn_offset, nb, "exchange_matrix");
+    check_cp(kernel, "exchange_matrix");
+    check_extents(basis, kernel, "exchange_matrix");
+    tgb::require(h && h[0] > 0.0 && h[1] > 0.0 && h[2] > 0.0, "convolve: mesh size must be positive");
+    tgb::require(nocc >= 0 && (nocc == 0 || nb == 0 || c_occ), "exchange_matrix: bad occupied coefficients");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    std::vector<double> c(nb * nocc);
+    if (!c.empty()) {
+      if (mem == TGB_MEM_DEVICE)
+        TGB_CUDA(cudaMemcpy(c.data(), c_occ, c.size() * sizeof(double), cudaMemcpyDeviceToHost));
+      else
+        std::memcpy(c.data(), c_occ, c.size() * sizeof(double));
+    }
+    DevCP db(basis, mem == TGB_MEM_DEVICE), dk(kernel, mem == TGB_MEM_DEVICE);
+    std::vector<double> hk(nb * nb);
+    tgb::DevStreamScope scope(ctx);
+    tgb::exchange_matrix_dev(ctx, db.t, fn_offset, nb, c.data(), nocc, dk.t, h, hk.data());
+    put_result(K, hk, mem);
+  });
+}
+
+namespace {
+int factor_op(tgb_ctx* ctx, int which, int64_t nb, int64_t rank, const double* h_core, const double* chol,
+              const double* density, double* out, int mem) {
+  static const char* names[3] = {"coulomb_from_factors", "exchange_from_factors", "fock_from_factors"};
+  return guarded([&] {
+    tgb::require(nb >= 0 && rank >= 0, std::string(names[which]) + ": shape mismatch");
+    tgb::require(nb == 0 || (density && out && (rank == 0 || chol) && (which != 2 || h_core)),
+                 std::string(names[which]) + ": null operand");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    const int64_t nn = nb * nb;
+    if (nn == 0) return;
+    tgb::DevStreamScope scope(ctx);
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::factor_operator_dev(ctx, which, nb, rank, h_core, chol, density, out);
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    size_t got = 0;
+    const size_t elems = nn * rank + 3 * nn;
+    auto* d = static_cast<double*>(tgb::scratch_alloc(ctx, elems * sizeof(double), &got));
+    double *dl = d, *dd = d + nn * rank, *dh = dd + nn, *dout = dh + nn;
+    try {
+      tgb::h2d(ctx, dl, chol, nn * rank * sizeof(double), ctx->stream);
+      tgb::h2d(ctx, dd, density, nn * sizeof(double), ctx->stream);
+      if (which == 2) tgb::h2d(ctx, dh, h_core, nn * sizeof(double), ctx->stream);
+      tgb::factor_operator_dev(ctx, which, nb, rank, dh, dl, dd, dout);
+      TGB_CUDA(cudaMemcpyAsync(out, dout, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      tgb::scratch_free(ctx, d, got);
+      throw;
+    }
+    tgb::scratch_free(ctx, d, got);
+  });
+}
+
+int one_electron(tgb_ctx* ctx, int which, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
+                 const double h[3], double* M, int mem) {
+  return guarded([&] {
+    check_basis(basis, fn_offset, nb, which == 0 ? "overlap_matrix" : "kinetic_matrix");
+    tgb::require(h && h[0] > 0.0 && h[1] > 0.0 && h[2] > 0.0, "make_grid: mesh size must be positive");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCP db(basis, mem == TGB_MEM_DEVICE);
+    std::vector<double> hm(nb * nb);
+    tgb::DevStreamScope scope(ctx);
+    tgb::one_electron_dev(ctx, which, db.t, fn_offset, nb, h, hm.data());
+    put_result(M, hm, mem);
+  });
+}
+}  // namespace
+
+int tgb_coulomb_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* chol, const double* density,
+                             double* J, int mem) {
+  return factor_op(ctx, 0, nb, rank, nullptr, chol, density, J, mem);
+}
+int tgb_exchange_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* chol, const double* density,
+                              double* K, int mem) {
+  return factor_op(ctx, 1, nb, rank, nullptr, chol, density, K, mem);
+}
+int tgb_fock_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* h_core, const double* chol,
+                          const double* density, double* F, int mem) {
+  return factor_op(ctx, 2, nb, rank, h_core, chol, density, F, mem);
+}
+int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
+                       double* S, int mem) {
+  return one_electron(ctx, 0, basis, fn_offset, nb, h, S, mem);
+}
+int tgb_kinetic_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
+                       int exact_mass, double* T, int mem) {
+  return one_electron(ctx, exact_mass ? 2 : 1, basis, fn_offset, nb, h, T, mem);
+}
+
 int tgb_lattice_assemble_axis(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets,
                               int64_t L, double* out, int mem) {
   return guarded([&] {

@@ -1693,7 +1693,8 @@ __global__ void dup_columns_kernel(const double* __restrict__ B, int64_t n, int 
 // column i, one entry per pair of identical kernel columns (the entry's
 // result is stored to both).  winfo = {entries, all columns symmetric}.
 __global__ void build_work_kernel(const unsigned char* __restrict__ f, int rb, int64_t ra, int64_t n,
-                                  PairEntry* __restrict__ w, int* __restrict__ winfo, int flags_in_smem) {
+                                  PairEntry* __restrict__ w, int* __restrict__ winfo, int flags_in_smem,
+                                  const int64_t* __restrict__ cmap) {
   // Grouping in parallel (bitwise identity is an equivalence): rep[j] = the
   // smallest j' <= j identical to j; a member's rank in its group = the number
   // of earlier members; groups are ordered by representative.  Every CTA
@@ -1765,8 +1766,10 @@ __global__ void build_work_kernel(const unsigned char* __restrict__ f, int rb, i
       PairEntry e;
       e.ia = static_cast<int>(i);
       e.jb = r;
-      e.out0 = (i + ra * j) * n;
-      e.out1 = partner >= 0 ? (i + ra * partner) * n : -1;
+      // output column i + ra j, or base[i] + stride[i] j under a column map
+      const int64_t cb = cmap ? cmap[i] : i, cs = cmap ? cmap[ra + i] : ra;
+      e.out0 = (cb + cs * j) * n;
+      e.out1 = partner >= 0 ? (cb + cs * partner) * n : -1;
       w[i * np + slot] = e;
     }
   }
@@ -1929,7 +1932,7 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
 // kernel column's spectrum is formed in both the real and the complex form,
 // and each pair kernel picks one from the device-side symmetry flag.
 void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const double* const* A, int64_t rb,
-                   const double* const* B, const double* h, double* const* out) {
+                   const double* const* B, const double* h, double* const* out, const int64_t* colmap) {
   if (ra == 0 || rb == 0 || naxes == 0) return;
   std::vector<std::shared_ptr<ConvPlan>> plans(naxes);
   for (int ax = 0; ax < naxes; ++ax) plans[ax] = get_plan(ctx, n[ax]);
@@ -1957,7 +1960,7 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
     TGB_LAUNCHED(ctx);
     const unsigned wblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ra / 4, 2 * ctx->num_sms)));
     build_work_kernel<<<wblocks, 128, wsmem, ctx->aux_stream>>>(f, static_cast<int>(rb), ra, n[ax], dwork[ax],
-                                                               winfo + 2 * ax, flags_in_smem);
+                                                               winfo + 2 * ax, flags_in_smem, colmap);
     TGB_LAUNCHED(ctx);
   }
   TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));

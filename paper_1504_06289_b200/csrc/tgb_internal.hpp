@@ -142,8 +142,11 @@ inline void prof_end(tgb_ctx* ctx) {
 }
 void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t rb, const double* B, double h,
                    double* out);
+// colmap (device, optional): 2 ra entries; density column i's result for
+// kernel column j goes to output column colmap[i] + colmap[ra + i] * j
+// instead of i + ra * j.
 void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const double* const* A, int64_t rb,
-                   const double* const* B, const double* h, double* const* out);
+                   const double* const* B, const double* h, double* const* out, const int64_t* colmap = nullptr);
 void conv_central_many_dev(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out);
 void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const double* wb, double scale, double* out);
 double scalar_product_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b);
@@ -155,4 +158,13 @@ void orthonormalize_columns(tgb_ctx* ctx, int64_t d, int p, double* X);
 void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ijk, double* out);
 void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
                           double* out);
+// hf.cu
+void nuclear_potential_dev(tgb_ctx* ctx, const tgb_cp& ref, const int64_t n[3], const int64_t* offsets,
+                           const double* charges, int64_t nnuc, tgb_cp& out);
+void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,
+                         int64_t nocc, const tgb_cp& kernel, const double h[3], double* K);
+void factor_operator_dev(tgb_ctx* ctx, int which, int64_t nb, int64_t R, const double* h_core, const double* chol,
+                         const double* D, double* out);
+void one_electron_dev(tgb_ctx* ctx, int which, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb,
+                      const double h[3], double* M);
 }  // namespace tgb

@@ -1,0 +1,197 @@
+"""Hartree-Fock operators on the convolution path, mirroring
+/root/reference/proj/include/tengrid/hf.hpp and tei.hpp:76-79:
+overlap / kinetic / nuclear / exchange matrices, the nuclear potential
+tensor, and the Cholesky-factor Coulomb / exchange / Fock builders.  Every
+call goes through libtgb.so (include/tgb.h); there is no CPU fallback.
+
+Host numpy arrays run through the C ABI's host-memory mode (staged copies
+inside the call); torch CUDA tensors / DeviceCP run device-resident.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from ._lib import MEM_DEVICE, MEM_HOST, InvalidArgument, check, lib
+from .tengrid import (BasisSet, CanonicalTensor3, Context, DeviceCP, KernelTensor, _h3, _mem, _out_like,
+                      default_context, flatten_basis, snap_to_node, window_offset)
+
+
+@dataclass
+class Nucleus:
+    """basis.hpp:37-40."""
+
+    charge: float = 1.0
+    center: tuple = (0.0, 0.0, 0.0)
+
+
+@dataclass
+class Molecule:
+    """basis.hpp:42-52."""
+
+    nuclei: list = field(default_factory=list)
+    n_electrons: int = 0
+
+    def n_occupied(self) -> int:
+        if self.n_electrons == 1:
+            return 1
+        if self.n_electrons < 2 or self.n_electrons % 2:
+            raise InvalidArgument("Molecule: closed-shell treatment needs an even electron count (or exactly one)")
+        return self.n_electrons // 2
+
+
+def _flat(disc: list):
+    flat, offs = flatten_basis(disc)
+    return flat, np.ascontiguousarray(offs, dtype=np.int64)
+
+
+def _one_electron(fn, bs: BasisSet, disc: list, ctx: Context | None, *extra) -> np.ndarray:
+    ctx = ctx or default_context()
+    flat, offs = _flat(disc)
+    nb = len(disc)
+    out = np.zeros((nb, nb), order="F")
+    cf = flat._cstruct()
+    hh = _h3(bs.grid.h)
+    check(fn(ctx.handle, C.byref(cf), offs.ctypes.data, nb, hh.ctypes.data, *extra, out.ctypes.data, MEM_HOST))
+    return out
+
+
+def overlap_matrix(bs: BasisSet, disc: list, ctx: Context | None = None) -> np.ndarray:
+    """hf.cpp:48-58 — S_km = h^3 <G_k, G_m>."""
+    return _one_electron(lib().tgb_overlap_matrix, bs, disc, ctx)
+
+
+def kinetic_matrix(bs: BasisSet, disc: list, exact_mass: bool = False, ctx: Context | None = None) -> np.ndarray:
+    """hf.cpp:60-87 — Kronecker FEM Laplacian with lumped or P1 mass."""
+    return _one_electron(lib().tgb_kinetic_matrix, bs, disc, ctx, int(bool(exact_mass)))
+
+
+def window_for_center(grid, center) -> tuple:
+    """grid.cpp:40-47 — per-axis offsets into the doubled-grid reference."""
+    return tuple(window_offset(grid, ax, float(center[ax])) for ax in range(3))
+
+
+def nuclear_potential_tensor(bs: BasisSet, mol: Molecule, reference: KernelTensor, ctx: Context | None = None):
+    """hf.cpp:89-101 — P_c = sum_a Z_a W_a Ptilde (rank = #nuclei * kernel rank)."""
+    if not reference.doubled:
+        raise InvalidArgument("nuclear_potential_tensor: reference kernel must live on the doubled grid")
+    ctx = ctx or default_context()
+    ref = reference.tensor
+    offs = np.ascontiguousarray([window_for_center(bs.grid, nuc.center) for nuc in mol.nuclei],
+                                dtype=np.int64).reshape(-1)
+    q = np.ascontiguousarray([nuc.charge for nuc in mol.nuclei], dtype=np.float64)
+    nn = len(mol.nuclei)
+    mem = _mem(ref)
+    dims = [bs.grid.n[ax] for ax in range(3)]
+    if mem == MEM_DEVICE:
+        out = DeviceCP.empty(dims, nn * ref.rank(), device=ref.weight.device)
+    else:
+        out = CanonicalTensor3([np.zeros((d, nn * ref.rank()), order="F") for d in dims], np.zeros(nn * ref.rank()))
+    cr, co = ref._cstruct(), out._cstruct()
+    check(lib().tgb_nuclear_potential_tensor(ctx.handle, C.byref(cr), offs.ctypes.data if nn else None,
+                                             q.ctypes.data if nn else None, nn, C.byref(co), mem))
+    return out
+
+
+def nuclear_matrix(bs: BasisSet, disc: list, mol: Molecule, reference: KernelTensor,
+                   ctx: Context | None = None) -> np.ndarray:
+    """hf.cpp:103-116 — V_km = -<G_k . G_m, P_c>."""
+    ctx = ctx or default_context()
+    pc = nuclear_potential_tensor(bs, mol, reference, ctx)
+    flat, offs = _flat(disc)
+    nb = len(disc)
+    if isinstance(pc, DeviceCP):
+        flat = DeviceCP.from_host(flat, device=pc.weight.device)
+    mem = _mem(flat, pc)
+    cf, cp = flat._cstruct(), pc._cstruct()
+    if mem == MEM_DEVICE:
+        import torch
+
+        V = torch.empty((nb, nb), dtype=torch.float64, device=pc.weight.device)
+        check(lib().tgb_nuclear_matrix(ctx.handle, C.byref(cf), offs.ctypes.data, nb, C.byref(cp), V.data_ptr(), mem))
+        return V.cpu().numpy().T.copy(order="F")
+    V = np.zeros((nb, nb), order="F")
+    check(lib().tgb_nuclear_matrix(ctx.handle, C.byref(cf), offs.ctypes.data, nb, C.byref(cp), V.ctypes.data, mem))
+    return V
+
+
+def exchange_matrix(bs: BasisSet, disc: list, c_occ, kernel: KernelTensor, ctx: Context | None = None) -> np.ndarray:
+    """hf.cpp:153-170 — K_km = sum_a h^3 <G_k . phi_a, (G_m . phi_a) * P / h^3>, symmetrised."""
+    if kernel.doubled:
+        raise InvalidArgument("exchange_matrix: kernel must live on the primary grid")
+    ctx = ctx or default_context()
+    flat, offs = _flat(disc)
+    nb = len(disc)
+    c = np.asfortranarray(np.asarray(c_occ, dtype=np.float64).reshape(nb, -1))
+    kt = kernel.tensor
+    if isinstance(kt, DeviceCP):
+        flat = DeviceCP.from_host(flat, device=kt.weight.device)
+    mem = _mem(flat, kt)
+    K = np.zeros((nb, nb), order="F")
+    cf, ck = flat._cstruct(), kt._cstruct()
+    hh = _h3(bs.grid.h)
+    if mem == MEM_DEVICE:
+        import torch
+
+        cd = torch.from_numpy(np.ascontiguousarray(c.T)).to(kt.weight.device)
+        Kd = torch.empty((nb, nb), dtype=torch.float64, device=kt.weight.device)
+        check(lib().tgb_exchange_matrix(ctx.handle, C.byref(cf), offs.ctypes.data, nb, cd.data_ptr(), c.shape[1],
+                                        C.byref(ck), hh.ctypes.data, Kd.data_ptr(), mem))
+        return Kd.cpu().numpy().T.copy(order="F")
+    check(lib().tgb_exchange_matrix(ctx.handle, C.byref(cf), offs.ctypes.data, nb, c.ctypes.data if c.size else None,
+                                    c.shape[1], C.byref(ck), hh.ctypes.data, K.ctypes.data, mem))
+    return K
+
+
+def _factor_op(which: int, chol, density, h_core=None, ctx: Context | None = None):
+    ctx = ctx or default_context()
+    try:
+        import torch
+
+        on_dev = isinstance(chol, torch.Tensor) and chol.is_cuda
+    except ImportError:  # pragma: no cover
+        on_dev = False
+    names = ("coulomb_from_factors", "exchange_from_factors", "fock_from_factors")
+    if on_dev:
+        # torch tensors hold the column-major matrices transposed: chol as (R, nb^2), density as (nb, nb)^T
+        R, nn = chol.shape
+        nb = int(round(nn ** 0.5))
+        if nb * nb != nn or tuple(density.shape) != (nb, nb):
+            raise InvalidArgument(f"{names[which]}: shape mismatch")
+        out = torch.empty((nb, nb), dtype=torch.float64, device=chol.device)
+        args = [ctx.handle, nb, R]
+        if which == 2:
+            args.append(h_core.contiguous().data_ptr())
+        args += [chol.contiguous().data_ptr(), density.contiguous().data_ptr(), out.data_ptr(), MEM_DEVICE]
+        check([lib().tgb_coulomb_from_factors, lib().tgb_exchange_from_factors, lib().tgb_fock_from_factors][which](*args))
+        return out
+    d = np.asfortranarray(np.asarray(density, dtype=np.float64))
+    nb = d.shape[0]
+    L = np.asfortranarray(np.asarray(chol, dtype=np.float64))
+    if d.ndim != 2 or d.shape[1] != nb or L.shape[0] != nb * nb:
+        raise InvalidArgument(f"{names[which]}: shape mismatch")
+    out = np.zeros((nb, nb), order="F")
+    args = [ctx.handle, nb, L.shape[1]]
+    if which == 2:
+        h = np.asfortranarray(np.asarray(h_core, dtype=np.float64))
+        args.append(h.ctypes.data)
+    args += [L.ctypes.data if L.size else None, d.ctypes.data, out.ctypes.data, MEM_HOST]
+    check([lib().tgb_coulomb_from_factors, lib().tgb_exchange_from_factors, lib().tgb_fock_from_factors][which](*args))
+    return out
+
+
+def coulomb_from_factors(chol, density, ctx: Context | None = None):
+    """tei.cpp:215-223 — J = unvec(L L^T vec D), symmetrised."""
+    return _factor_op(0, chol, density, None, ctx)
+
+
+def exchange_from_factors(chol, density, ctx: Context | None = None):
+    """tei.cpp:225-234 — K = -1/2 sum_s M_s D M_s^T, symmetrised."""
+    return _factor_op(1, chol, density, None, ctx)
+
+
+def fock_from_factors(h_core, chol, density, ctx: Context | None = None):
+    """tei.cpp:236-238 — F = h_core + J + K."""
+    return _factor_op(2, chol, density, h_core, ctx)

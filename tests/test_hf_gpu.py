@@ -1,0 +1,168 @@
+"""GPU parity of the Hartree-Fock operators on the convolution path (SURVEY.md
+§8f) and of the TEI / rank-reduction pipelines, against fixtures produced by
+the reference's OWN hf.cpp / tei.cpp / reduction.cpp (tests/golden/
+reference_hf.npz, tools/make_golden_hf.py) and against the restatement.
+
+Tolerance: 1e-10 relative max-norm (BASELINE.json north_star); window gathers
+are bit-identical; symmetrised matrices must be exactly symmetric; ranks are
+identical.  Reduction results are compared as dense images (sign/rotation
+free) within the eps the rank rule guarantees."""
+import numpy as np
+import pytest
+
+import paper_1504_06289_b200 as tg
+from conftest import relmax
+from hf_case import functions, load, molecule, product_case
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def g():
+    return load()
+
+
+@pytest.fixture(scope="module")
+def case(g):
+    return product_case(g)
+
+
+def test_overlap_kinetic(g, case, ctx):
+    bs, disc, _, _ = case
+    S = tg.overlap_matrix(bs, disc, ctx)
+    assert relmax(S, g["S"]) <= TOL and np.array_equal(S, S.T)
+    for exact, key in ((False, "T_lumped"), (True, "T_exact")):
+        T = tg.kinetic_matrix(bs, disc, exact, ctx)
+        assert relmax(T, g[key]) <= TOL and np.array_equal(T, T.T)
+
+
+def test_nuclear_potential_tensor_bit_identical(g, case, ctx):
+    bs, _, _, kd = case
+    pc = tg.nuclear_potential_tensor(bs, molecule(g), kd, ctx)
+    for ax in range(3):
+        assert np.array_equal(pc.factor[ax], g[f"pc_f{ax}"])
+    assert np.array_equal(pc.weight, g["pc_w"])
+    # device-resident
+    kdev = tg.KernelTensor(tg.DeviceCP.from_host(kd.tensor), True, kd.expsum)
+    pcd = tg.nuclear_potential_tensor(bs, molecule(g), kdev, ctx).to_host()
+    for ax in range(3):
+        assert np.array_equal(pcd.factor[ax], g[f"pc_f{ax}"])
+
+
+def test_nuclear_matrix(g, case, ctx):
+    bs, disc, _, kd = case
+    V = tg.nuclear_matrix(bs, disc, molecule(g), kd, ctx)
+    assert relmax(V, g["V"]) <= TOL and np.array_equal(V, V.T)
+    kdev = tg.KernelTensor(tg.DeviceCP.from_host(kd.tensor), True, kd.expsum)
+    assert relmax(tg.nuclear_matrix(bs, disc, molecule(g), kdev, ctx), g["V"]) <= TOL
+
+
+def test_nuclear_errors(g, case, ctx):
+    bs, disc, kp, _ = case
+    with pytest.raises(tg.InvalidArgument):
+        tg.nuclear_potential_tensor(bs, molecule(g), kp, ctx)  # hf.cpp:91: doubled reference required
+    empty = tg.Molecule([], 0)
+    _, _, _, kd = case
+    pc = tg.nuclear_potential_tensor(bs, empty, kd, ctx)
+    assert pc.rank() == 0
+    assert np.array_equal(tg.nuclear_matrix(bs, disc, empty, kd, ctx), np.zeros((len(disc), len(disc))))
+
+
+def test_exchange_matrix(g, case, ctx):
+    bs, disc, kp, _ = case
+    K = tg.exchange_matrix(bs, disc, g["c_occ"], kp, ctx)
+    assert relmax(K, g["K"]) <= TOL
+    assert np.array_equal(K, K.T)  # (K + K^T) / 2, hf.cpp:169
+    kdev = tg.KernelTensor(tg.DeviceCP.from_host(kp.tensor), False, kp.expsum)
+    assert relmax(tg.exchange_matrix(bs, disc, g["c_occ"], kdev, ctx), g["K"]) <= TOL
+
+
+def test_exchange_matrix_vs_restatement_odd_even(ctx):
+    """Even extents (two-node window) and contracted functions, against the restatement."""
+    fns = [((0.2, 0.1, -0.3), (0, 0, 0), [(1.3, 0.8), (0.4, 0.3)]), ((-0.5, 0.2, 0.4), (0, 1, 0), [(0.9, 1.0)]),
+           ((0.6, -0.4, 0.1), (1, 0, 0), [(2.2, 1.0)])]
+    b, n = (4.0, 4.5, 5.0), (32, 33, 40)
+    grid = tg.make_grid(b, n)
+    bs = tg.BasisSet(grid, [tg.SeparableBasisFunction(c, d, [tg.GaussianPrimitive(e, k) for e, k in p])
+                            for c, d, p in fns])
+    disc = tg.discretize_basis(bs)
+    es = tg.make_expsum(5, 0.8)
+    kp = tg.kernel_tensor(grid, es, False)
+    c = np.asfortranarray([[0.6, 0.1], [0.3, -0.7], [-0.2, 0.5]])
+    K = tg.exchange_matrix(bs, disc, c, kp, ctx)
+    od = O.discretize_basis(b, n, fns)
+    ok = O.kernel_tensor(b, n, es.nodes, es.weights, False)
+    assert relmax(K, O.exchange_matrix(b, n, od, c, ok)) <= TOL
+    # no occupied orbitals -> zero matrix; a doubled kernel is rejected (hf.cpp:155)
+    assert np.array_equal(tg.exchange_matrix(bs, disc, np.zeros((3, 0)), kp, ctx), np.zeros((3, 3)))
+    with pytest.raises(tg.InvalidArgument):
+        tg.exchange_matrix(bs, disc, c, tg.kernel_tensor(grid, es, True), ctx)
+
+
+@pytest.mark.parametrize("which", [0, 1, 2])
+def test_from_factors(g, ctx, which):
+    fn = (tg.coulomb_from_factors, tg.exchange_from_factors, tg.fock_from_factors)[which]
+    key = ("ff_J", "ff_K", "ff_F")[which]
+    args = (g["ff_chol"], g["ff_density"])
+    got = fn(g["ff_hcore"], *args, ctx=ctx) if which == 2 else fn(*args, ctx=ctx)
+    assert relmax(got, g[key]) <= TOL
+    assert np.array_equal(got, got.T)
+    # device-resident operands (torch tensors hold the column-major matrices transposed)
+    import torch
+
+    L = torch.from_numpy(np.ascontiguousarray(g["ff_chol"].T)).cuda()
+    D = torch.from_numpy(np.ascontiguousarray(g["ff_density"].T)).cuda()
+    if which == 2:
+        H = torch.from_numpy(np.ascontiguousarray(g["ff_hcore"].T)).cuda()
+        dev = fn(H, L, D, ctx=ctx)
+    else:
+        dev = fn(L, D, ctx=ctx)
+    assert relmax(dev.cpu().numpy().T, g[key]) <= TOL
+
+
+def test_from_factors_rank_zero_and_shapes(ctx):
+    d = np.eye(4)
+    assert np.array_equal(tg.coulomb_from_factors(np.zeros((16, 0)), d, ctx), np.zeros((4, 4)))
+    assert np.array_equal(tg.exchange_from_factors(np.zeros((16, 0)), d, ctx), np.zeros((4, 4)))
+    with pytest.raises(tg.InvalidArgument):
+        tg.coulomb_from_factors(np.zeros((15, 2)), d, ctx)
+
+
+def test_coulomb_matrix_vs_reference_binary(g, case, ctx):
+    """J from the unreduced density: the reference's own hf.cpp:140-151."""
+    bs, disc, kp, _ = case
+    theta = tg.CanonicalTensor3([g[f"theta_f{ax}"] for ax in range(3)], g["theta_w"])
+    vh = tg.hartree_potential(theta, kp, bs.grid.h, ctx)
+    J = tg.coulomb_matrix(bs, disc, vh, ctx)
+    assert relmax(J, g["J"]) <= TOL and np.array_equal(J, J.T)
+
+
+def test_tei_vs_reference_binary(g, case, ctx):
+    """build_tei (tei.cpp:206-213) against the reference's own tei.cpp: fit ranks and R_B identical,
+    L L^T and the diagonal at 1e-10."""
+    bs, disc, kp, _ = case
+    fac = tg.build_tei(bs, disc, kp, 1e-6, 1e-6, ctx)
+    assert fac.fit_ranks() == tuple(int(x) for x in g["tei_fit_ranks"])
+    assert fac.rank_b() == int(g["tei_rank_b"][0])
+    L, oL = fac.chol, g["tei_chol"]
+    assert relmax(L @ L.T, oL @ oL.T) <= TOL
+    assert relmax(tg.tei_diagonal(fac), g["tei_diag"]) <= TOL
+
+
+def test_reduce_rank_vs_reference_binary(g, ctx):
+    """reduce_rank (reduction.cpp:271-273) of the density tensor against the reference's own
+    reduction.cpp: Tucker ranks and canonical rank identical, dense images within eps."""
+    theta = tg.CanonicalTensor3([g[f"theta_f{ax}"] for ax in range(3)], g["theta_w"])
+    eps = float(g["red_eps"][0])
+    res = tg.canonical_to_tucker(theta, tg.ReductionConfig.tolerance(eps), ctx)
+    assert tuple(res.tucker.ranks()) == tuple(int(x) for x in g["red_tucker_ranks"])
+    red = tg.reduce_rank(theta, tg.ReductionConfig.tolerance(eps), ctx)
+    assert red.rank() == int(g["red_canonical_rank"][0])
+    ref = tg.CanonicalTensor3([g[f"red_f{ax}"] for ax in range(3)], g["red_w"])
+    dense_ref, dense = ref.to_dense(), red.to_dense()
+    full = theta.to_dense()
+    scale = np.linalg.norm(full)
+    assert np.linalg.norm(dense - dense_ref) <= 0.5 * eps * scale
+    assert np.linalg.norm(dense - full) <= eps * scale

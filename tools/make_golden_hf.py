@@ -1,0 +1,125 @@
+"""Generate tests/golden/reference_hf.npz by running the REFERENCE's own
+hf.cpp / tei.cpp / reduction.cpp (oracle/_ref: /root/reference/proj/src
+compiled in place against oracle/eigen_shim, whose dense decompositions are
+the restatement's LA) on a small seeded basis.
+
+Run here (where /root/reference exists):  python tools/make_golden_hf.py
+The fixtures are committed; tests/test_hf_oracle.py pins the restatement and
+tests/test_hf_gpu.py the GPU path against them on any machine.
+"""
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from oracle import oracle as O  # noqa: E402
+from paper_1504_06289_b200.inputs import Rng  # noqa: E402
+
+B_HALF = np.array([5.0, 5.5, 4.5])
+N = np.array([41, 45, 37])
+KM, KC0 = 6, 0.9
+FUNCTIONS = [  # (center, degree, [(exponent, coeff)])
+    ((0.4, -0.3, 0.2), (0, 0, 0), [(1.1, 1.0)]),
+    ((0.4, -0.3, 0.2), (1, 0, 0), [(0.7, 1.0)]),
+    ((-0.8, 0.5, -0.1), (0, 0, 0), [(2.5, 0.6), (0.6, 0.5)]),
+    ((-0.8, 0.5, -0.1), (0, 0, 1), [(0.9, 1.0)]),
+    ((0.3, 0.9, -0.7), (0, 1, 0), [(1.4, 1.0)]),
+    ((0.3, 0.9, -0.7), (0, 0, 0), [(0.35, 1.0)]),
+]
+NUCLEI = [((0.4, -0.3, 0.2), 1.0), ((-0.8, 0.5, -0.1), 2.0), ((0.3, 0.9, -0.7), 1.5)]
+
+
+def basis_arrays():
+    c, d, npr, e, cf = O._basis_args(FUNCTIONS)
+    return {"basis_centers": c, "basis_degs": d, "basis_nprim": npr, "basis_exps": e, "basis_coefs": cf}
+
+
+def main():
+    from paper_1504_06289_b200 import build
+
+    build.build_ref()
+    assert O.rlib() is not None, "oracle/_ref not built (needs /root/reference)"
+    R = O.Ref(B_HALF, N, FUNCTIONS)
+    rng = Rng(4242)
+    nb = len(FUNCTIONS)
+    out = {"b_half": B_HALF, "n": N, "kernel_m_c0": np.array([KM, KC0]), **basis_arrays()}
+    out["nuc_centers"] = np.array([c for c, _ in NUCLEI])
+    out["nuc_charges"] = np.array([q for _, q in NUCLEI])
+
+    # one-electron matrices (hf.cpp:48-87)
+    out["S"] = R.one_electron(0)
+    out["T_lumped"] = R.one_electron(1)
+    out["T_exact"] = R.one_electron(2)
+    # nuclear potential tensor + matrix (hf.cpp:89-116), doubled Newton reference
+    V, pc = R.nuclear(out["nuc_centers"], out["nuc_charges"], KM, KC0)
+    out["V"] = V
+    for ax, f in enumerate(pc.factors()):
+        out[f"pc_f{ax}"] = f
+    out["pc_w"] = pc.weight()
+
+    # occupied coefficients, exchange (hf.cpp:153-170)
+    g = rng.normal(nb * 2).reshape(nb, 2, order="F")
+    c_occ, _ = np.linalg.qr(g)
+    c_occ = np.asfortranarray(c_occ)
+    c_occ[1, 1] = 0.0  # one zero coefficient: orbital_tensor skips it (hf.cpp:42)
+    out["c_occ"] = c_occ
+    out["K"] = R.exchange_matrix(c_occ, KM, KC0)
+
+    # Coulomb matrix from the unreduced density (density_tensor eps = 0 -> no reduction)
+    theta = R.density_tensor(c_occ, 0.0)
+    kern = O.OCP(lib=R.R)
+    import ctypes as C
+
+    rc = R.R.ref_kernel_tensor(O._p(R.b), R.nn, C.c_longlong(KM), C.c_double(KC0), C.c_int(0), kern.h)
+    assert rc == 0
+    hh = 2.0 * B_HALF / (N + 1)
+    ks = O.OCP(kern.factors(), kern.weight() / float(np.prod(hh)), lib=R.R)
+    vh = O.OCP(lib=R.R)
+    assert R.R.ref_convolve(theta.h, ks.h, O._p(np.ascontiguousarray(hh)), vh.h) == 0
+    out["J"] = R.coulomb_matrix(vh)
+    out["theta_rank"] = np.array([theta.rank()])
+
+    # Cholesky-factor builders (tei.cpp:215-238) on seeded factors
+    rb = 5
+    chol = np.asfortranarray(rng.normal(nb * nb * rb).reshape(nb * nb, rb, order="F"))
+    dens = np.asfortranarray(2.0 * c_occ @ c_occ.T)
+    hcore = np.asfortranarray(out["T_lumped"] + V)
+    out["ff_chol"], out["ff_density"], out["ff_hcore"] = chol, dens, hcore
+    for which, key in ((0, "ff_J"), (1, "ff_K"), (2, "ff_F")):
+        out[key] = O.ref_from_factors(which, chol, dens, hcore if which == 2 else None)
+
+    # generalized eigenproblem F C = S C e (hf.cpp:187-199)
+    cc, ee = O.ref_generalized_eigensolve(out["ff_F"], out["S"])
+    out["gen_C"], out["gen_e"] = cc, ee
+
+    # TEI factorisation (tei.cpp:19-213)
+    ranks, rb_tei, clamped, res, lchol, diag = R.build_tei(KM, KC0, 1e-6, 1e-6)
+    out["tei_fit_ranks"] = np.array(ranks)
+    out["tei_rank_b"] = np.array([rb_tei])
+    out["tei_chol"], out["tei_diag"], out["tei_fit_residual"] = lchol, diag, res
+
+    # rank reduction of the density tensor (reduction.cpp:172-273)
+    info, red = O.ref_reduce(theta, eps=1e-6, mode=2)
+    out["red_eps"] = np.array([1e-6])
+    info1, _ = O.ref_reduce(theta, eps=1e-6, mode=1)
+    out["red_tucker_ranks"] = np.array(info1["ranks"])
+    out["red_canonical_rank"] = np.array([info["canonical_rank"]])
+    for ax, f in enumerate(red.factors()):
+        out[f"red_f{ax}"] = f
+    out["red_w"] = red.weight()
+    for ax, f in enumerate(theta.factors()):
+        out[f"theta_f{ax}"] = f
+    out["theta_w"] = theta.weight()
+
+    path = ROOT / "tests" / "golden" / "reference_hf.npz"
+    np.savez_compressed(path, **out)
+    print(f"wrote {path} ({len(out)} arrays)")
+
+
+if __name__ == "__main__":
+    main()
