@@ -143,6 +143,69 @@ int tgb_exchange_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const doub
 int tgb_fock_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* h_core, const double* chol,
                           const double* density, double* F, int mem);
 
+/* replaces tg::generalized_eigensolve (hf.hpp:94-95, hf.cpp:187-199):
+ * F C = S C diag(e) by the Cholesky congruence of S; e ascending, columns of C
+ * S-orthonormal (eigenvector signs are not fixed, as in the reference).
+ * nb <= 112 (one-CTA solver).  NUMERICAL_ERROR when S is not positive definite. */
+int tgb_generalized_eigensolve(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e,
+                               int mem);
+
+/* ---- restricted closed-shell SCF on the grid (hf.hpp:54-91, hf.cpp:172-270) ----
+ * replaces tg::scf_solve: snapped nuclei, overlap / kinetic / nuclear matrices,
+ * Newton kernel from tg::expsum_for_interval(1.5 h_min, r_max, kernel_eps), the
+ * factorised TEI (build_tei), then the Roothaan iterations with
+ * fock_from_factors / generalized_eigensolve / linear density mixing, all on
+ * the device.  Inputs and outputs are HOST memory. */
+typedef struct tgb_scf_config { /* SCFConfig, hf.hpp:54-64 (same defaults) */
+  int max_iterations;           /* 60 */
+  double energy_tol;            /* 1e-9 */
+  double mixing;                /* 0.7 */
+  double eps_fit;               /* 1e-8 */
+  double eps_chol;              /* 1e-10 */
+  double kernel_eps;            /* 1e-6 */
+  double kernel_r_max;          /* 0: the box diagonal */
+  double density_reduce_eps;    /* 1e-7 (unused by the SCF loop, as in the reference) */
+  int exact_mass_kinetic;       /* 0 */
+} tgb_scf_config;
+
+typedef struct tgb_basis_spec { /* BasisSet, basis.hpp:18-35 */
+  double b_half[3];
+  int64_t n[3];
+  int64_t nfn;
+  const double* centers;      /* nfn x 3, row-major */
+  const int* degrees;         /* nfn x 3, row-major, each 0 or 1 */
+  const int64_t* prim_offset; /* nfn + 1 */
+  const double* exponents;    /* prim_offset[nfn] */
+  const double* coeffs;
+} tgb_basis_spec;
+
+typedef struct tgb_molecule { /* Molecule, basis.hpp:37-52 */
+  int64_t nnuc;
+  const double* charges; /* nnuc */
+  const double* centers; /* nnuc x 3, row-major */
+  int64_t n_electrons;
+} tgb_molecule;
+
+typedef struct tgb_scf_state { /* SCFState, hf.hpp:66-88; arrays caller-allocated (NULL: not returned) */
+  double energy, nuclear_energy;
+  int converged, iterations, n_occupied;
+  int64_t tei_rank_b;             /* 0 for one electron */
+  int64_t kernel_m;               /* quadrature M from expsum_for_interval */
+  double kernel_c0;
+  double* coefficients;           /* nb x nb */
+  double* orbital_energies;       /* nb */
+  double* density;                /* nb x nb */
+  double* overlap, *kinetic, *nuclear, *core_hamiltonian; /* nb x nb each */
+  double* energy_history;         /* max_iterations */
+  double* residual_history;       /* max_iterations */
+  double* orthonormality_defects; /* max_iterations */
+  double* snapped_centers;        /* nnuc x 3 */
+} tgb_scf_state;
+
+void tgb_scf_config_default(tgb_scf_config* cfg);
+int tgb_scf_solve(tgb_ctx* ctx, const tgb_molecule* mol, const tgb_basis_spec* basis, const tgb_scf_config* cfg,
+                  tgb_scf_state* out);
+
 /* replaces tg::overlap_matrix (hf.hpp:14, hf.cpp:48-58): S_km = h^3 <G_k, G_m>. */
 int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
                        double* S, int mem);

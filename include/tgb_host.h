@@ -6,6 +6,7 @@
  *   tgb_snap_to_node     <- tg::snap_to_node                     grid.cpp:23-30
  *   tgb_window_offset    <- tg::window_offset                    grid.cpp:32-38
  *   tgb_make_expsum      <- tg::make_expsum (Newton, 2M+1 nodes)  kernel.cpp:71-123
+ *   tgb_expsum_for_interval <- tg::expsum_for_interval (Newton)  kernel.cpp:131-165
  *   tgb_kernel_factors   <- tg::kernel_tensor (one axis)         kernel.cpp:182-203
  *   tgb_gauss_cell_integral <- tg::gauss_cell_integral           kernel.cpp:171-180
  *   tgb_primitive_norm   <- tg::primitive_norm                   basis.cpp:8-14
@@ -31,6 +32,10 @@ int tgb_make_expsum(int64_t m, double c0, double fit_lo, double fit_hi, double* 
 /* factor: (doubled ? 2n : n) x terms, column-major */
 int tgb_kernel_factors(double b_half, int64_t n, int64_t terms, const double* nodes, const double* weights,
                        int doubled, double* factor);
+/* kernel.cpp:125-165: the reference's M schedule and golden-section C0 for a
+ * Newton sum accurate to eps on [r_min, r_max] (m_cap = 2048 in the reference);
+ * build it with tgb_make_expsum(m, c0, r_min, r_max, ...). */
+int tgb_expsum_for_interval(double r_min, double r_max, double eps, int64_t m_cap, int64_t* m, double* c0);
 double tgb_gauss_cell_integral(double t, double center, double h);
 int tgb_primitive_norm(double alpha, int l, double* out);
 int tgb_gaussian_factor(double b_half, int64_t n, double center, double alpha, int degree, double* column);

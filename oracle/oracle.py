@@ -530,3 +530,33 @@ def ref_reduce(a: OCP, eps: float | None = None, ranks=None, sweeps: int = 3, mo
         raise OracleError(rc, R.ref_last_error().decode())
     return {"ranks": (info[0], info[1], info[2]), "rank_clamped": bool(info[3]), "rhosvd_fallback": bool(info[4]),
             "sweeps": info[5], "canonical_rank": info[6]}, out
+
+
+def ref_expsum_for_interval(r_min: float, r_max: float, eps: float):
+    R = rlib()
+    m, c0 = C.c_longlong(), C.c_double()
+    rc = R.ref_expsum_for_interval(C.c_double(r_min), C.c_double(r_max), C.c_double(eps), C.byref(m), C.byref(c0))
+    if rc:
+        raise OracleError(rc, R.ref_last_error().decode())
+    return m.value, c0.value
+
+
+def ref_scf_solve(ref: "Ref", nuclei, n_electrons: int, cfg: dict):
+    """The reference's tg::scf_solve (hf.cpp:201-270) on the stand-in LA."""
+    R = ref.R
+    c = np.array([cfg["max_iterations"], cfg["energy_tol"], cfg["mixing"], cfg["eps_fit"], cfg["eps_chol"],
+                  cfg["kernel_eps"], cfg.get("kernel_r_max", 0.0)], dtype=np.float64)
+    q = np.ascontiguousarray([z for _, z in nuclei], dtype=np.float64)
+    cen = np.ascontiguousarray([p for p, _ in nuclei], dtype=np.float64).reshape(-1)
+    out = np.zeros(6)
+    e = np.zeros(ref.nb)
+    d = np.zeros((ref.nb, ref.nb), order="F")
+    hist = np.zeros(int(cfg["max_iterations"]))
+    rc = R.ref_scf_solve(*ref._basis(), C.c_int(q.shape[0]), _p(q), _p(cen), C.c_int(n_electrons), _p(c), _p(out),
+                         _p(e), _p(d), _p(hist))
+    if rc:
+        raise OracleError(rc, R.ref_last_error().decode())
+    it = int(out[3])
+    return {"energy": out[0], "nuclear_energy": out[1], "converged": bool(out[2]), "iterations": it,
+            "n_occupied": int(out[4]), "tei_rank_b": int(out[5]), "orbital_energies": e, "density": d,
+            "energy_history": hist[:it]}

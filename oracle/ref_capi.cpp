@@ -333,4 +333,43 @@ int ref_reduce(void* a, int use_eps, double eps, const long long* ranks, int swe
     }
   });
 }
+
+// kernel.cpp:131-165
+int ref_expsum_for_interval(double r_min, double r_max, double eps, long long* m, double* c0) {
+  return guard([&] {
+    const tg::ExpSum es = tg::expsum_for_interval(r_min, r_max, eps);
+    *m = es.m;
+    *c0 = es.c0;
+  });
+}
+// hf.cpp:201-270.  cfg = {max_iterations, energy_tol, mixing, eps_fit, eps_chol, kernel_eps, kernel_r_max};
+// out = {energy, nuclear_energy, converged, iterations, n_occupied, tei_rank_b}; e (nb), density (nb x nb),
+// energy_history (max_iterations)
+int ref_scf_solve(TG_BASIS_ARGS, int nnuc, const double* charges, const double* ncenters, int n_electrons,
+                  const double* cfg, double* out, double* e, double* density, double* energy_history) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    tg::Molecule mol;
+    for (int a = 0; a < nnuc; ++a) mol.nuclei.push_back({charges[a], {ncenters[3 * a], ncenters[3 * a + 1], ncenters[3 * a + 2]}});
+    mol.n_electrons = n_electrons;
+    tg::SCFConfig c;
+    c.max_iterations = static_cast<int>(cfg[0]);
+    c.energy_tol = cfg[1];
+    c.mixing = cfg[2];
+    c.eps_fit = cfg[3];
+    c.eps_chol = cfg[4];
+    c.kernel_eps = cfg[5];
+    c.kernel_r_max = cfg[6];
+    const tg::SCFState st = tg::scf_solve(mol, bs, c);
+    out[0] = st.energy;
+    out[1] = st.nuclear_energy;
+    out[2] = st.converged;
+    out[3] = st.iterations;
+    out[4] = st.n_occupied;
+    out[5] = st.tei ? static_cast<double>(st.tei->rank_b()) : 0.0;
+    put(st.orbital_energies, e);
+    put(st.density, density);
+    for (size_t i = 0; i < st.energy_history.size(); ++i) energy_history[i] = st.energy_history[i];
+  });
+}
 }  // extern "C"

@@ -47,6 +47,31 @@ class tgb_cp(C.Structure):
     _fields_ = [("n", C.c_int64 * 3), ("rank", C.c_int64), ("factor", C.c_void_p * 3), ("weight", C.c_void_p)]
 
 
+class tgb_scf_config(C.Structure):
+    _fields_ = [("max_iterations", C.c_int), ("energy_tol", C.c_double), ("mixing", C.c_double),
+                ("eps_fit", C.c_double), ("eps_chol", C.c_double), ("kernel_eps", C.c_double),
+                ("kernel_r_max", C.c_double), ("density_reduce_eps", C.c_double), ("exact_mass_kinetic", C.c_int)]
+
+
+class tgb_basis_spec(C.Structure):
+    _fields_ = [("b_half", C.c_double * 3), ("n", C.c_int64 * 3), ("nfn", C.c_int64), ("centers", C.c_void_p),
+                ("degrees", C.c_void_p), ("prim_offset", C.c_void_p), ("exponents", C.c_void_p),
+                ("coeffs", C.c_void_p)]
+
+
+class tgb_molecule(C.Structure):
+    _fields_ = [("nnuc", C.c_int64), ("charges", C.c_void_p), ("centers", C.c_void_p), ("n_electrons", C.c_int64)]
+
+
+class tgb_scf_state(C.Structure):
+    _fields_ = [("energy", C.c_double), ("nuclear_energy", C.c_double), ("converged", C.c_int),
+                ("iterations", C.c_int), ("n_occupied", C.c_int), ("tei_rank_b", C.c_int64),
+                ("kernel_m", C.c_int64), ("kernel_c0", C.c_double)] + [
+                   (name, C.c_void_p) for name in ("coefficients", "orbital_energies", "density", "overlap", "kinetic",
+                                                   "nuclear", "core_hamiltonian", "energy_history", "residual_history",
+                                                   "orthonormality_defects", "snapped_centers")]
+
+
 _lib = None
 
 
@@ -81,6 +106,11 @@ def lib() -> C.CDLL:
             "tgb_coulomb_from_factors": (I, [P, I64, I64, P, P, P, I]),
             "tgb_exchange_from_factors": (I, [P, I64, I64, P, P, P, I]),
             "tgb_fock_from_factors": (I, [P, I64, I64, P, P, P, P, I]),
+            "tgb_generalized_eigensolve": (I, [P, I64, P, P, P, P, I]),
+            "tgb_scf_config_default": (None, [C.POINTER(tgb_scf_config)]),
+            "tgb_scf_solve": (I, [P, C.POINTER(tgb_molecule), C.POINTER(tgb_basis_spec), C.POINTER(tgb_scf_config),
+                                  C.POINTER(tgb_scf_state)]),
+            "tgb_expsum_for_interval": (I, [D, D, D, I64, C.POINTER(I64), C.POINTER(D)]),
             "tgb_overlap_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, P, I]),
             "tgb_kinetic_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, I, P, I]),
             "tgb_tei_create": (I, [C.POINTER(P)]),

@@ -503,6 +503,36 @@ int tgb_fock_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* 
                           const double* density, double* F, int mem) {
   return factor_op(ctx, 2, nb, rank, h_core, chol, density, F, mem);
 }
+int tgb_generalized_eigensolve(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e,
+                               int mem) {
+  return guarded([&] {
+    tgb::require(nb >= 0, "generalized_eigensolve: negative size");
+    if (nb == 0) return;
+    tgb::require(F && S && C && e, "generalized_eigensolve: null operand");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::DevStreamScope scope(ctx);
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::generalized_eigensolve_dev(ctx, nb, F, S, C, e);
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    const int64_t nn = nb * nb;
+    size_t got = 0;
+    auto* d = static_cast<double*>(tgb::scratch_alloc(ctx, (3 * nn + nb) * sizeof(double), &got));
+    try {
+      TGB_CUDA(cudaMemcpyAsync(d, F, nn * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      TGB_CUDA(cudaMemcpyAsync(d + nn, S, nn * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+      tgb::generalized_eigensolve_dev(ctx, nb, d, d + nn, d + 2 * nn, d + 3 * nn);
+      TGB_CUDA(cudaMemcpyAsync(C, d + 2 * nn, nn * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaMemcpyAsync(e, d + 3 * nn, nb * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      tgb::scratch_free(ctx, d, got);
+      throw;
+    }
+    tgb::scratch_free(ctx, d, got);
+  });
+}
 int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
                        double* S, int mem) {
   return one_electron(ctx, 0, basis, fn_offset, nb, h, S, mem);

@@ -164,6 +164,118 @@ __global__ void __launch_bounds__(256) pair_forms_kernel(int64_t n, const double
   }
 }
 
+// ---- generalized symmetric eigenproblem F C = S C diag(e) (hf.cpp:187-199),
+// one CTA: Cholesky S = L L^T, F~ = L^-1 F^T L^-T (the reference's two
+// triangular solves), B = (F~ + F~^T)/2 + sigma I with sigma = 1.5 ||B||_F so
+// B is positive definite and its one-sided Jacobi SVD is its eigen-
+// decomposition; e = s - sigma ascending, C = L^-T V.
+constexpr int kGenMax = 112;  // two n x n FP64 tiles in shared memory
+
+__global__ void __launch_bounds__(1024) gen_eig_prep_kernel(int n, const double* __restrict__ F,
+                                                            const double* __restrict__ S, double* __restrict__ Lg,
+                                                            double* __restrict__ B, double* __restrict__ sigma,
+                                                            int* __restrict__ fail) {
+  extern __shared__ double gsm[];
+  double* L = gsm;          // n x n, column-major, lower
+  double* Y = gsm + n * n;  // n x n work
+  __shared__ int bad;
+  __shared__ double red[32];
+  if (threadIdx.x == 0) bad = 0;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) L[i] = S[i];
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {  // right-looking Cholesky (LLT of S)
+    const double d = L[j + n * j];
+    if (!(d > 0.0)) {
+      if (threadIdx.x == 0) bad = 1;
+      break;
+    }
+    const double r = sqrt(d);
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) L[i + n * j] /= r;
+    if (threadIdx.x == 0) L[j + n * j] = r;
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int t = threadIdx.x; t < m * m; t += blockDim.x) {
+      const int i = j + 1 + t % m, k = j + 1 + t / m;
+      if (i >= k) L[i + n * k] -= L[i + n * j] * L[k + n * j];
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (bad) {
+    if (threadIdx.x == 0) *fail = 1;
+    return;
+  }
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    const int r = i % n, c = i / n;
+    if (r < c) L[i] = 0.0;
+    Lg[i] = r < c ? 0.0 : L[i];
+  }
+  __syncthreads();
+  // Y = L^-1 F^T (column c of F^T = row c of F), one thread per column
+  for (int c = threadIdx.x; c < n; c += blockDim.x)
+    for (int i = 0; i < n; ++i) {
+      double s = F[c + n * i];
+      for (int k = 0; k < i; ++k) s -= L[i + n * k] * Y[k + n * c];
+      Y[i + n * c] = s / L[i + n * i];
+    }
+  __syncthreads();
+  // F~ = L^-1 Y^T, written to B (global) column by column
+  for (int c = threadIdx.x; c < n; c += blockDim.x)
+    for (int i = 0; i < n; ++i) {
+      double s = Y[c + n * i];
+      for (int k = 0; k < i; ++k) s -= L[i + n * k] * B[k + n * c];
+      B[i + n * c] = s / L[i + n * i];
+    }
+  __syncthreads();
+  __threadfence_block();
+  // symmetrise into Y, Frobenius norm
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    const int r = i % n, c = i / n;
+    const double v = 0.5 * (B[r + n * c] + B[c + n * r]);
+    Y[i] = v;
+    ss += v * v;
+  }
+  for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) red[0] = 1.5 * sqrt(v) + 1e-300;
+  }
+  __syncthreads();
+  const double sg = red[0];
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) B[i] = Y[i] + ((i % n) == (i / n) ? sg : 0.0);
+  if (threadIdx.x == 0) {
+    *sigma = sg;
+    *fail = 0;
+  }
+}
+
+// e[i] = s[n-1-i] - sigma (ascending); C(:, i) = L^-T U(:, n-1-i)
+__global__ void __launch_bounds__(1024) gen_eig_finish_kernel(int n, const double* __restrict__ Lg,
+                                                              const double* __restrict__ U,
+                                                              const double* __restrict__ s,
+                                                              const double* __restrict__ sigma, double* __restrict__ C,
+                                                              double* __restrict__ e) {
+  extern __shared__ double gsm[];
+  double* L = gsm;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) L[i] = Lg[i];
+  __syncthreads();
+  const double sg = *sigma;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const double* u = U + static_cast<int64_t>(n - 1 - c) * n;
+    e[c] = s[n - 1 - c] - sg;
+    for (int i = n - 1; i >= 0; --i) {  // L^T x = u (back substitution)
+      double acc = u[i];
+      for (int k = i + 1; k < n; ++k) acc -= L[k + n * i] * C[k + n * c];
+      C[i + n * c] = acc / L[i + n * i];
+    }
+  }
+}
+
 dim3 col_grid(int64_t n, int64_t cols) {
   return dim3(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 16)),
               static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(cols, 65535))));
@@ -402,6 +514,37 @@ void one_electron_dev(tgb_ctx* ctx, int which, const tgb_cp& basis, const int64_
       M[k + nb * m] = v;
       M[m + nb * k] = v;
     }
+}
+
+// ---------------------------------------------------------------- generalized eigensolver
+
+void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e) {
+  if (nb == 0) return;
+  if (nb > kGenMax)
+    throw Error(TGB_INVALID_ARGUMENT, "generalized_eigensolve: basis larger than the one-CTA solver (112)");
+  const int n = static_cast<int>(nb);
+  Scratch sl(ctx, nb * nb), sb(ctx, nb * nb), ss(ctx, nb + 2);
+  const size_t smem = 2 * static_cast<size_t>(nb * nb) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    TGB_CUDA(cudaFuncSetAttribute(gen_eig_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(2 * kGenMax * kGenMax * sizeof(double))));
+    TGB_CUDA(cudaFuncSetAttribute(gen_eig_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kGenMax * kGenMax * sizeof(double))));
+    attr = true;
+  }
+  double* sigma = ss.p + nb;
+  int* fail = reinterpret_cast<int*>(ss.p + nb + 1);
+  gen_eig_prep_kernel<<<1, 1024, smem, ctx->stream>>>(n, F, S, sl.p, sb.p, sigma, fail);
+  TGB_LAUNCHED(ctx);
+  int hfail = 0;
+  TGB_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hfail)
+    throw Error(TGB_NUMERICAL_ERROR, "generalized_eigensolve: overlap not positive definite (basis near-dependence)");
+  jacobi_svd_dev(ctx, n, sb.p, ss.p);
+  gen_eig_finish_kernel<<<1, 1024, smem / 2, ctx->stream>>>(n, sl.p, sb.p, ss.p, sigma, C, e);
+  TGB_LAUNCHED(ctx);
 }
 
 }  // namespace tgb

@@ -133,6 +133,74 @@ int tgb_kernel_factors(double b_half, int64_t n, int64_t terms, const double* no
   });
 }
 
+// kernel.cpp:125-165 (Newton kernel): smallest M on the reference's schedule
+// whose golden-section-optimal C0 meets eps on [r_min, r_max].
+int tgb_expsum_for_interval(double r_min, double r_max, double eps, int64_t m_cap, int64_t* m_out, double* c0_out) {
+  return guarded([&] {
+    tgb::require(r_min > 0.0 && r_max >= r_min, "expsum_for_interval: bad interval");
+    tgb::require(eps > 0.0, "expsum_for_interval: eps must be positive");
+    std::vector<double> nodes, weights;
+    auto build = [&](int64_t m, double c0) {
+      nodes.assign(2 * m + 1, 0.0);
+      weights.assign(2 * m + 1, 0.0);
+      double sc, mesh;
+      if (tgb_make_expsum(m, c0, r_min, r_max, nodes.data(), weights.data(), &sc, &mesh) != TGB_OK)
+        throw tgb::Error(TGB_INVALID_ARGUMENT, g_host_err);
+    };
+    auto max_rel = [&](int samples) {  // ExpSum::max_relative_error (kernel.cpp:58-67), target 1/r
+      double worst = 0.0;
+      for (int i = 0; i < samples; ++i) {
+        const double r = r_min * std::pow(r_max / r_min, samples == 1 ? 0.0 : static_cast<double>(i) / (samples - 1));
+        double v = 0.0;
+        for (size_t k = 0; k < weights.size(); ++k) v += weights[k] * std::exp(-nodes[k] * nodes[k] * r * r);
+        const double f = 1.0 / r;
+        worst = std::max(worst, std::abs(v - f) / std::abs(f));
+      }
+      return worst;
+    };
+    auto measured = [&](int64_t m, double c0) {
+      build(m, c0);
+      return max_rel(300);
+    };
+    auto best_c0 = [&](int64_t m) {
+      const double phi = 0.5 * (std::sqrt(5.0) - 1.0);
+      double lo = std::log(0.15), hi = std::log(12.0);
+      double x1 = hi - phi * (hi - lo), x2 = lo + phi * (hi - lo);
+      double f1 = measured(m, std::exp(x1)), f2 = measured(m, std::exp(x2));
+      for (int it = 0; it < 22; ++it) {
+        if (f1 <= f2) {
+          hi = x2;
+          x2 = x1;
+          f2 = f1;
+          x1 = hi - phi * (hi - lo);
+          f1 = measured(m, std::exp(x1));
+        } else {
+          lo = x1;
+          x1 = x2;
+          f1 = f2;
+          x2 = lo + phi * (hi - lo);
+          f2 = measured(m, std::exp(x2));
+        }
+      }
+      return std::exp(0.5 * (lo + hi));
+    };
+    const double l = std::log(1.0 / std::min(eps * 1e3, 0.5));
+    tgb::require(std::min(eps * 1e3, 0.5) > 0.0 && std::min(eps * 1e3, 0.5) < 1.0,
+                 "expsum_terms_for_tolerance: eps in (0,1) required");
+    for (int64_t m = std::max<int64_t>(6, static_cast<int64_t>(std::ceil(0.30 * l * l))); m <= m_cap;
+         m = std::max<int64_t>(m + 4, static_cast<int64_t>(m * 1.3))) {
+      const double c0 = best_c0(m);
+      build(m, c0);
+      if (max_rel(600) <= eps) {
+        *m_out = m;
+        *c0_out = c0;
+        return;
+      }
+    }
+    throw tgb::Error(TGB_NUMERICAL_ERROR, "expsum_for_interval: tolerance unattainable within the term cap");
+  });
+}
+
 double tgb_gauss_cell_integral(double t, double c, double h) { return cell_integral(t, c, h); }
 
 int tgb_primitive_norm(double alpha, int l, double* out) {

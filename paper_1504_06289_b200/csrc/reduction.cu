@@ -584,6 +584,25 @@ void random_block(tgb_ctx* ctx, int64_t d, int p, double* X, uint64_t seed) {
 
 }  // namespace
 
+// One-CTA one-sided Jacobi SVD of a p x p device matrix (p <= 128): U
+// replaces S in place (columns sorted by descending singular value), sg gets
+// the p singular values.  Used by the generalized eigensolver (hf.cu).
+void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg) {
+  if (p > kJacMax) throw Error(TGB_INVALID_ARGUMENT, "jacobi_svd_dev: matrix too large for the one-CTA solver");
+  if (p <= 0) return;
+  const size_t jsm = static_cast<size_t>(p) * (p + (p & 1)) * sizeof(double);
+  static bool jattr = false;
+  if (!jattr) {
+    cudaFuncAttributes fa{};
+    TGB_CUDA(cudaFuncGetAttributes(&fa, jacobi_svd_kernel));
+    TGB_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
+    jattr = true;
+  }
+  jacobi_svd_kernel<<<1, kJacThreads, jsm, ctx->stream>>>(p, S, sg);
+  TGB_LAUNCHED(ctx);
+}
+
 DevStreamScope::DevStreamScope(tgb_ctx* ctx) : prev(g_dev_ctx) {
   if (!getenv("TGB_NO_SCRATCH_CACHE")) g_dev_ctx = ctx;
 }

@@ -158,7 +158,10 @@ void orthonormalize_columns(tgb_ctx* ctx, int64_t d, int p, double* X);
 void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ijk, double* out);
 void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
                           double* out);
+// reduction.cu
+void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg);
 // hf.cu
+void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e);
 void nuclear_potential_dev(tgb_ctx* ctx, const tgb_cp& ref, const int64_t n[3], const int64_t* offsets,
                            const double* charges, int64_t nnuc, tgb_cp& out);
 void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,

@@ -195,3 +195,117 @@ def exchange_from_factors(chol, density, ctx: Context | None = None):
 def fock_from_factors(h_core, chol, density, ctx: Context | None = None):
     """tei.cpp:236-238 — F = h_core + J + K."""
     return _factor_op(2, chol, density, h_core, ctx)
+
+
+def generalized_eigensolve(f, s, ctx: Context | None = None):
+    """hf.cpp:187-199 — F C = S C diag(e), e ascending, C S-orthonormal (device, nb <= 112)."""
+    ctx = ctx or default_context()
+    F = np.asfortranarray(np.asarray(f, dtype=np.float64))
+    S = np.asfortranarray(np.asarray(s, dtype=np.float64))
+    nb = F.shape[0]
+    if F.shape != (nb, nb) or S.shape != (nb, nb):
+        raise InvalidArgument("generalized_eigensolve: shape mismatch")
+    Cm = np.zeros((nb, nb), order="F")
+    e = np.zeros(nb)
+    check(lib().tgb_generalized_eigensolve(ctx.handle, nb, F.ctypes.data, S.ctypes.data, Cm.ctypes.data,
+                                           e.ctypes.data, MEM_HOST))
+    return Cm, e
+
+
+@dataclass
+class SCFConfig:
+    """hf.hpp:54-64."""
+
+    max_iterations: int = 60
+    energy_tol: float = 1e-9
+    mixing: float = 0.7
+    eps_fit: float = 1e-8
+    eps_chol: float = 1e-10
+    kernel_eps: float = 1e-6
+    kernel_r_max: float = 0.0
+    density_reduce_eps: float = 1e-7
+    exact_mass_kinetic: bool = False
+
+
+@dataclass
+class SCFState:
+    """hf.hpp:66-88 (tei: rank of the Cholesky factor only)."""
+
+    coefficients: np.ndarray = None
+    orbital_energies: np.ndarray = None
+    density: np.ndarray = None
+    n_occupied: int = 0
+    energy: float = 0.0
+    nuclear_energy: float = 0.0
+    converged: bool = False
+    iterations: int = 0
+    energy_history: list = field(default_factory=list)
+    residual_history: list = field(default_factory=list)
+    orthonormality_defects: list = field(default_factory=list)
+    overlap: np.ndarray = None
+    core_hamiltonian: np.ndarray = None
+    kinetic: np.ndarray = None
+    nuclear: np.ndarray = None
+    tei_rank_b: int = 0
+    kernel_m: int = 0
+    kernel_c0: float = 0.0
+    snapped: Molecule = None
+
+
+def scf_solve(mol: Molecule, bs: BasisSet, cfg: SCFConfig | None = None, ctx: Context | None = None) -> SCFState:
+    """hf.cpp:201-270 — restricted closed-shell SCF, every operator on the device (tgb_scf_solve)."""
+    from ._lib import tgb_basis_spec, tgb_molecule, tgb_scf_config, tgb_scf_state
+
+    cfg = cfg or SCFConfig()
+    ctx = ctx or default_context()
+    nb = len(bs.functions)
+    spec = tgb_basis_spec()
+    for ax in range(3):
+        spec.b_half[ax] = bs.grid.b_half[ax]
+        spec.n[ax] = bs.grid.n[ax]
+    spec.nfn = nb
+    centers = np.ascontiguousarray([f.center for f in bs.functions], dtype=np.float64).reshape(-1)
+    degs = np.ascontiguousarray([f.degree for f in bs.functions], dtype=np.int32).reshape(-1)
+    poff = np.zeros(nb + 1, dtype=np.int64)
+    poff[1:] = np.cumsum([len(f.primitives) for f in bs.functions])
+    exps = np.ascontiguousarray([p.exponent for f in bs.functions for p in f.primitives], dtype=np.float64)
+    coefs = np.ascontiguousarray([p.coeff for f in bs.functions for p in f.primitives], dtype=np.float64)
+    spec.centers, spec.degrees, spec.prim_offset = centers.ctypes.data, degs.ctypes.data, poff.ctypes.data
+    spec.exponents = exps.ctypes.data if exps.size else None
+    spec.coeffs = coefs.ctypes.data if coefs.size else None
+    m = tgb_molecule()
+    m.nnuc = len(mol.nuclei)
+    q = np.ascontiguousarray([nuc.charge for nuc in mol.nuclei], dtype=np.float64)
+    nc = np.ascontiguousarray([nuc.center for nuc in mol.nuclei], dtype=np.float64).reshape(-1)
+    m.charges = q.ctypes.data if q.size else None
+    m.centers = nc.ctypes.data if nc.size else None
+    m.n_electrons = mol.n_electrons
+    c = tgb_scf_config(cfg.max_iterations, cfg.energy_tol, cfg.mixing, cfg.eps_fit, cfg.eps_chol, cfg.kernel_eps,
+                       cfg.kernel_r_max, cfg.density_reduce_eps, int(cfg.exact_mass_kinetic))
+    out = SCFState()
+    mats = {k: np.zeros((nb, nb), order="F") for k in ("coefficients", "density", "overlap", "kinetic", "nuclear",
+                                                       "core_hamiltonian")}
+    e = np.zeros(nb)
+    hist = {k: np.zeros(max(cfg.max_iterations, 1)) for k in ("energy_history", "residual_history",
+                                                              "orthonormality_defects")}
+    snapped = np.zeros(max(3 * len(mol.nuclei), 1))
+    st = tgb_scf_state()
+    for k, v in mats.items():
+        setattr(st, k, v.ctypes.data)
+    for k, v in hist.items():
+        setattr(st, k, v.ctypes.data)
+    st.orbital_energies = e.ctypes.data
+    st.snapped_centers = snapped.ctypes.data
+    check(lib().tgb_scf_solve(ctx.handle, C.byref(m), C.byref(spec), C.byref(c), C.byref(st)))
+    for k, v in mats.items():
+        setattr(out, k, v)
+    out.orbital_energies = e
+    it = st.iterations
+    for k, v in hist.items():
+        setattr(out, k, list(v[:it]))
+    out.n_occupied, out.energy, out.nuclear_energy = st.n_occupied, st.energy, st.nuclear_energy
+    out.converged, out.iterations, out.tei_rank_b = bool(st.converged), it, st.tei_rank_b
+    out.kernel_m, out.kernel_c0 = st.kernel_m, st.kernel_c0
+    out.snapped = Molecule([Nucleus(nuc.charge, tuple(snapped[3 * a:3 * a + 3])) for a, nuc in enumerate(mol.nuclei)],
+                           mol.n_electrons)
+    return out

@@ -1,0 +1,18 @@
+"""Host input producers that need no GPU: tg::expsum_for_interval (kernel.cpp:131-165)
+is bit-identical to the reference binary's (tests/golden/reference_scf.npz)."""
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+import paper_1504_06289_b200 as tg
+from paper_1504_06289_b200._lib import check
+
+G = dict(np.load(Path(__file__).resolve().parent / "golden" / "reference_scf.npz"))
+
+
+def test_expsum_for_interval_bit_identical():
+    for (lo, hi, eps), (m_ref, c0_ref) in zip(G["expsum_in"], G["expsum_out"]):
+        m, c0 = C.c_int64(), C.c_double()
+        check(tg.lib().tgb_expsum_for_interval(lo, hi, eps, 2048, C.byref(m), C.byref(c0)), host=True)
+        assert m.value == int(m_ref) and c0.value == c0_ref
