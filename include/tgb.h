@@ -206,6 +206,19 @@ void tgb_scf_config_default(tgb_scf_config* cfg);
 int tgb_scf_solve(tgb_ctx* ctx, const tgb_molecule* mol, const tgb_basis_spec* basis, const tgb_scf_config* cfg,
                   tgb_scf_state* out);
 
+/* ---- MP2 on the factorised TEI (mp2.hpp:8-57, mp2.cpp:7-105) ----------------
+ * replaces tg::mo_transform_cholesky: out (N_ov x rank, row i n_vir + a) holds
+ * C_occ^T mat(L_s) C_vir for every Cholesky column s; coefficients nb x nb
+ * (occupied columns first).  chol is nb^2 x rank. */
+int tgb_mo_transform_cholesky(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* chol, int64_t n_occ,
+                              const double* coefficients, double* out, int mem);
+/* replaces tg::mp2_energy: mode 0 = MP2Mode::oracle (exact denominators), 1 =
+ * MP2Mode::factorized (exponential-sum denominators at expsum_eps).  mo_factor
+ * N_ov x rank (space given by `mem`); energies nb ascending (HOST memory);
+ * result in *energy (host). */
+int tgb_mp2_energy(tgb_ctx* ctx, int64_t n_occ, int64_t n_vir, int64_t rank, const double* mo_factor,
+                   const double* energies, int mode, double expsum_eps, double* energy, int mem);
+
 /* replaces tg::overlap_matrix (hf.hpp:14, hf.cpp:48-58): S_km = h^3 <G_k, G_m>. */
 int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
                        double* S, int mem);

@@ -7,6 +7,7 @@
  *   tgb_window_offset    <- tg::window_offset                    grid.cpp:32-38
  *   tgb_make_expsum      <- tg::make_expsum (Newton, 2M+1 nodes)  kernel.cpp:71-123
  *   tgb_expsum_for_interval <- tg::expsum_for_interval (Newton)  kernel.cpp:131-165
+ *   tgb_reciprocal_expsum <- tg::reciprocal_expsum                kernel.cpp:205-250
  *   tgb_kernel_factors   <- tg::kernel_tensor (one axis)         kernel.cpp:182-203
  *   tgb_gauss_cell_integral <- tg::gauss_cell_integral           kernel.cpp:171-180
  *   tgb_primitive_norm   <- tg::primitive_norm                   basis.cpp:8-14
@@ -36,6 +37,10 @@ int tgb_kernel_factors(double b_half, int64_t n, int64_t terms, const double* no
  * Newton sum accurate to eps on [r_min, r_max] (m_cap = 2048 in the reference);
  * build it with tgb_make_expsum(m, c0, r_min, r_max, ...). */
 int tgb_expsum_for_interval(double r_min, double r_max, double eps, int64_t m_cap, int64_t* m, double* c0);
+/* kernel.cpp:205-250 (tg::reciprocal_expsum, term_cap 256 in the reference): rates and
+ * weights need term_cap entries; *ok = 0 when the cap is hit. */
+int tgb_reciprocal_expsum(double lo, double hi, double eps, int64_t term_cap, int64_t* terms, double* rates,
+                          double* weights, double* achieved, int* ok);
 double tgb_gauss_cell_integral(double t, double center, double h);
 int tgb_primitive_norm(double alpha, int l, double* out);
 int tgb_gaussian_factor(double b_half, int64_t n, double center, double alpha, int degree, double* column);

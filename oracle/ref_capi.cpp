@@ -11,6 +11,7 @@
 #include "tengrid/basis.hpp"
 #include "tengrid/fft.hpp"
 #include "tengrid/hf.hpp"
+#include "tengrid/mp2.hpp"
 #include "tengrid/reduction.hpp"
 #include "tengrid/tei.hpp"
 #include "tengrid/grid.hpp"
@@ -370,6 +371,55 @@ int ref_scf_solve(TG_BASIS_ARGS, int nnuc, const double* charges, const double* 
     put(st.orbital_energies, e);
     put(st.density, density);
     for (size_t i = 0; i < st.energy_history.size(); ++i) energy_history[i] = st.energy_history[i];
+  });
+}
+
+// scf_solve then the MP2 chain of mp2.cpp on its MO space.  Returns the
+// inputs the device path needs (chol, coefficients, energies) and the
+// reference's outputs: the MO factor and both MP2 energies.
+// sizes = {nb, R_B, n_occ}; call first with chol == nullptr to get sizes.
+int ref_mp2_case(TG_BASIS_ARGS, int nnuc, const double* charges, const double* ncenters, int n_electrons,
+                 const double* cfg, double expsum_eps, long long* sizes, double* chol, double* coef, double* energies,
+                 double* mo_factor, double* e2) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    tg::Molecule mol;
+    for (int a = 0; a < nnuc; ++a) mol.nuclei.push_back({charges[a], {ncenters[3 * a], ncenters[3 * a + 1], ncenters[3 * a + 2]}});
+    mol.n_electrons = n_electrons;
+    tg::SCFConfig c;
+    c.max_iterations = static_cast<int>(cfg[0]);
+    c.energy_tol = cfg[1];
+    c.mixing = cfg[2];
+    c.eps_fit = cfg[3];
+    c.eps_chol = cfg[4];
+    c.kernel_eps = cfg[5];
+    const tg::SCFState st = tg::scf_solve(mol, bs, c);
+    sizes[0] = bs.size();
+    sizes[1] = st.tei->chol.cols();
+    sizes[2] = st.n_occupied;
+    if (!chol) return;
+    put(st.tei->chol, chol);
+    put(st.coefficients, coef);
+    put(st.orbital_energies, energies);
+    tg::MOSpace mos;
+    mos.coefficients = st.coefficients;
+    mos.energies = st.orbital_energies;
+    mos.n_occ = st.n_occupied;
+    const tg::MOCholesky mo = tg::mo_transform_cholesky(st.tei->chol, mos);
+    put(mo.factor, mo_factor);
+    e2[0] = tg::mp2_energy(mo, mos, tg::MP2Mode::oracle);
+    e2[1] = tg::mp2_energy(mo, mos, tg::MP2Mode::factorized, expsum_eps);
+  });
+}
+int ref_reciprocal_expsum(double lo, double hi, double eps, long long* terms, double* rates, double* weights,
+                          double* achieved, int* ok) {
+  return guard([&] {
+    const tg::ReciprocalExpSum rs = tg::reciprocal_expsum(lo, hi, eps);
+    *terms = rs.terms();
+    put(rs.rates, rates);
+    put(rs.weights, weights);
+    *achieved = rs.achieved_error;
+    *ok = rs.ok;
   });
 }
 }  // extern "C"

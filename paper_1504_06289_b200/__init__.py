@@ -15,7 +15,8 @@ from .tengrid import (AssembledPotential, BasisSet, CanonicalTensor3, Context, D
 from .tei import (TEIFactorization, build_tei, tei_cholesky, tei_column, tei_convolution_matrices,
                   tei_density_fitting, tei_diagonal, tei_matrix_entry)
 
-from .hf import (Molecule, Nucleus, SCFConfig, SCFState, generalized_eigensolve, scf_solve, coulomb_from_factors, exchange_from_factors, exchange_matrix,
+from .hf import (Molecule, Nucleus, SCFConfig, SCFState, generalized_eigensolve, scf_solve, MOSpace, MOCholesky,
+                 mo_transform_cholesky, mp2_energy, coulomb_from_factors, exchange_from_factors, exchange_matrix,
                  fock_from_factors, kinetic_matrix, nuclear_matrix, nuclear_potential_tensor, overlap_matrix,
                  window_for_center)
 

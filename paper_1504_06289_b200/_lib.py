@@ -111,6 +111,9 @@ def lib() -> C.CDLL:
             "tgb_scf_solve": (I, [P, C.POINTER(tgb_molecule), C.POINTER(tgb_basis_spec), C.POINTER(tgb_scf_config),
                                   C.POINTER(tgb_scf_state)]),
             "tgb_expsum_for_interval": (I, [D, D, D, I64, C.POINTER(I64), C.POINTER(D)]),
+            "tgb_mo_transform_cholesky": (I, [P, I64, I64, P, I64, P, P, I]),
+            "tgb_mp2_energy": (I, [P, I64, I64, I64, P, P, I, D, C.POINTER(D), I]),
+            "tgb_reciprocal_expsum": (I, [D, D, D, I64, C.POINTER(I64), P, P, C.POINTER(D), C.POINTER(I)]),
             "tgb_overlap_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, P, I]),
             "tgb_kinetic_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, I, P, I]),
             "tgb_tei_create": (I, [C.POINTER(P)]),

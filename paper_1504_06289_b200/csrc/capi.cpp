@@ -533,6 +533,61 @@ int tgb_generalized_eigensolve(tgb_ctx* ctx, int64_t nb, const double* F, const 
     tgb::scratch_free(ctx, d, got);
   });
 }
+int tgb_mo_transform_cholesky(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* chol, int64_t n_occ,
+                              const double* coefficients, double* out, int mem) {
+  return guarded([&] {
+    tgb::require(nb >= 1 && rank >= 0 && n_occ >= 0 && n_occ <= nb, "mo_transform_cholesky: factor/basis shape mismatch");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::DevStreamScope scope(ctx);
+    const int64_t nn = nb * nb, nov = n_occ * (nb - n_occ);
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::mo_transform_dev(ctx, nb, rank, chol, n_occ, coefficients, out);
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      return;
+    }
+    if (nov * rank == 0) return;
+    size_t got = 0;
+    auto* d = static_cast<double*>(tgb::scratch_alloc(ctx, (nn * rank + nn + nov * rank) * sizeof(double), &got));
+    try {
+      tgb::h2d(ctx, d, chol, nn * rank * sizeof(double), ctx->stream);
+      tgb::h2d(ctx, d + nn * rank, coefficients, nn * sizeof(double), ctx->stream);
+      tgb::mo_transform_dev(ctx, nb, rank, d, n_occ, d + nn * rank, d + nn * rank + nn);
+      TGB_CUDA(cudaMemcpyAsync(out, d + nn * rank + nn, nov * rank * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    } catch (...) {
+      tgb::scratch_free(ctx, d, got);
+      throw;
+    }
+    tgb::scratch_free(ctx, d, got);
+  });
+}
+
+int tgb_mp2_energy(tgb_ctx* ctx, int64_t n_occ, int64_t n_vir, int64_t rank, const double* mo_factor,
+                   const double* energies, int mode, double expsum_eps, double* energy, int mem) {
+  return guarded([&] {
+    tgb::require(n_occ >= 0 && n_vir >= 0 && rank >= 0 && energy && energies, "mp2_energy: MO space mismatch");
+    tgb::require(mode == 0 || mode == 1, "mp2_energy: unknown mode");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::DevStreamScope scope(ctx);
+    const int64_t nov = n_occ * n_vir;
+    if (mem == TGB_MEM_DEVICE) {
+      *energy = tgb::mp2_energy_dev(ctx, n_occ, n_vir, rank, mo_factor, energies, mode, expsum_eps);
+      return;
+    }
+    size_t got = 0;
+    auto* d = static_cast<double*>(tgb::scratch_alloc(ctx, std::max<int64_t>(1, nov * rank) * sizeof(double), &got));
+    try {
+      if (nov * rank) tgb::h2d(ctx, d, mo_factor, nov * rank * sizeof(double), ctx->stream);
+      *energy = tgb::mp2_energy_dev(ctx, n_occ, n_vir, rank, d, energies, mode, expsum_eps);
+    } catch (...) {
+      tgb::scratch_free(ctx, d, got);
+      throw;
+    }
+    tgb::scratch_free(ctx, d, got);
+  });
+}
+
 int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
                        double* S, int mem) {
   return one_electron(ctx, 0, basis, fn_offset, nb, h, S, mem);

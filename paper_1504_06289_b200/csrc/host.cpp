@@ -201,6 +201,62 @@ int tgb_expsum_for_interval(double r_min, double r_max, double eps, int64_t m_ca
   });
 }
 
+// kernel.cpp:205-250: 1/x ~ sum_j w_j exp(-r_j x) on [lo, hi] (sinc quadrature of
+// 1/x = int exp(-x e^u + u) du, mesh shrunk by 0.8 until eps is met).  rates /
+// weights need term_cap entries; *ok = 0 when the cap is hit (the reference's
+// ReciprocalExpSum::ok).
+int tgb_reciprocal_expsum(double lo, double hi, double eps, int64_t term_cap, int64_t* terms, double* rates,
+                          double* weights, double* achieved, int* ok) {
+  return guarded([&] {
+    tgb::require(0.0 < lo && lo <= hi, "reciprocal_expsum: need 0 < lo <= hi");
+    tgb::require(eps > 0.0, "reciprocal_expsum: eps must be positive");
+    *ok = 0;
+    *terms = 0;
+    *achieved = 0.0;
+    if (lo == hi) {
+      tgb::require(term_cap >= 1, "reciprocal_expsum: term cap below one");
+      rates[0] = 1.0 / lo;
+      weights[0] = 2.71828182845904523536 / lo;  // std::numbers::e
+      *terms = 1;
+      *ok = 1;
+      return;
+    }
+    const double q = hi / lo;
+    const double u_min = std::log(eps / (6.0 * q));
+    const double u_max = std::log(std::log(6.0 * q / eps)) + 1.0;
+    std::vector<double> r, w;
+    for (double mesh = 2.0 * kPi / (std::log(1.0 / eps) + 6.0);; mesh *= 0.8) {
+      const int64_t n = static_cast<int64_t>(std::ceil((u_max - u_min) / mesh)) + 1;
+      if (n > term_cap) return;
+      r.assign(n, 0.0);
+      w.assign(n, 0.0);
+      for (int64_t j = 0; j < n; ++j) {
+        const double u = u_min + static_cast<double>(j) * mesh;
+        r[j] = std::exp(u);
+        w[j] = mesh * std::exp(u);
+      }
+      double worst = 0.0;
+      const int samples = 1000;
+      for (int i = 0; i < samples; ++i) {
+        const double x = std::pow(q, static_cast<double>(i) / (samples - 1));
+        double sum = 0.0;
+        for (int64_t j = 0; j < n; ++j) sum += w[j] * std::exp(-r[j] * x);
+        worst = std::max(worst, std::abs(sum - 1.0 / x) * x);
+      }
+      if (worst <= eps) {
+        for (int64_t j = 0; j < n; ++j) {
+          rates[j] = r[j] / lo;
+          weights[j] = w[j] / lo;
+        }
+        *terms = n;
+        *achieved = worst;
+        *ok = 1;
+        return;
+      }
+    }
+  });
+}
+
 double tgb_gauss_cell_integral(double t, double c, double h) { return cell_integral(t, c, h); }
 
 int tgb_primitive_norm(double alpha, int l, double* out) {

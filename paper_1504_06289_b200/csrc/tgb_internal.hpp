@@ -160,6 +160,11 @@ void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref,
                           double* out);
 // reduction.cu
 void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg);
+// mp2.cu
+void mo_transform_dev(tgb_ctx* ctx, int64_t nb, int64_t R, const double* chol, int64_t n_occ, const double* C,
+                      double* out);
+double mp2_energy_dev(tgb_ctx* ctx, int64_t n_occ, int64_t n_vir, int64_t R, const double* F, const double* e_host,
+                      int mode, double expsum_eps);
 // hf.cu
 void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e);
 void nuclear_potential_dev(tgb_ctx* ctx, const tgb_cp& ref, const int64_t n[3], const int64_t* offsets,

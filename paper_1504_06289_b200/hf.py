@@ -309,3 +309,65 @@ def scf_solve(mol: Molecule, bs: BasisSet, cfg: SCFConfig | None = None, ctx: Co
     out.snapped = Molecule([Nucleus(nuc.charge, tuple(snapped[3 * a:3 * a + 3])) for a, nuc in enumerate(mol.nuclei)],
                            mol.n_electrons)
     return out
+
+
+# --------------------------------------------------------------------------- MP2 (mp2.hpp)
+
+
+@dataclass
+class MOSpace:
+    """mp2.hpp:10-24."""
+
+    coefficients: np.ndarray
+    energies: np.ndarray
+    n_occ: int
+
+    def n_basis(self) -> int:
+        return int(np.asarray(self.energies).shape[0])
+
+    def n_virtual(self) -> int:
+        return self.n_basis() - self.n_occ
+
+    def gap(self) -> float:
+        if self.n_occ < 1 or self.n_virtual() < 1:
+            raise InvalidArgument("MOSpace: need occupied and virtual orbitals")
+        return float(self.energies[self.n_occ] - self.energies[self.n_occ - 1])
+
+
+@dataclass
+class MOCholesky:
+    """mp2.hpp:28-37 — rows i * n_vir + a."""
+
+    factor: np.ndarray
+    n_occ: int
+    n_vir: int
+
+
+def mo_transform_cholesky(chol, mos: MOSpace, ctx: Context | None = None) -> MOCholesky:
+    """mp2.cpp:7-24 — C_occ^T mat(L_s) C_vir for every Cholesky column."""
+    ctx = ctx or default_context()
+    nb = mos.n_basis()
+    L = np.asfortranarray(np.asarray(chol, dtype=np.float64))
+    if L.shape[0] != nb * nb:
+        raise InvalidArgument("mo_transform_cholesky: factor/basis shape mismatch")
+    Cm = np.asfortranarray(np.asarray(mos.coefficients, dtype=np.float64))
+    nov = mos.n_occ * mos.n_virtual()
+    out = np.zeros((nov, L.shape[1]), order="F")
+    check(lib().tgb_mo_transform_cholesky(ctx.handle, nb, L.shape[1], L.ctypes.data if L.size else None, mos.n_occ,
+                                          Cm.ctypes.data, out.ctypes.data if out.size else None, MEM_HOST))
+    return MOCholesky(out, mos.n_occ, mos.n_virtual())
+
+
+def mp2_energy(mo: MOCholesky, mos: MOSpace, mode: str = "oracle", expsum_eps: float = 1e-9,
+               ctx: Context | None = None) -> float:
+    """mp2.cpp:97-103 — mode "oracle" (exact denominators) or "factorized" (exponential sums)."""
+    ctx = ctx or default_context()
+    if mo.n_occ != mos.n_occ or mo.n_vir != mos.n_virtual():
+        raise InvalidArgument("mp2_energy: MO space mismatch")
+    F = np.asfortranarray(np.asarray(mo.factor, dtype=np.float64))
+    e = np.ascontiguousarray(mos.energies, dtype=np.float64)
+    res = C.c_double()
+    check(lib().tgb_mp2_energy(ctx.handle, mo.n_occ, mo.n_vir, F.shape[1], F.ctypes.data if F.size else None,
+                               e.ctypes.data, {"oracle": 0, "factorized": 1}[mode], expsum_eps, C.byref(res),
+                               MEM_HOST))
+    return res.value

@@ -16,3 +16,15 @@ def test_expsum_for_interval_bit_identical():
         m, c0 = C.c_int64(), C.c_double()
         check(tg.lib().tgb_expsum_for_interval(lo, hi, eps, 2048, C.byref(m), C.byref(c0)), host=True)
         assert m.value == int(m_ref) and c0.value == c0_ref
+
+
+def test_reciprocal_expsum_bit_identical():
+    """tg::reciprocal_expsum (kernel.cpp:205-250) against the reference binary's output."""
+    for idx, (lo, hi, eps, terms, ach, ok) in enumerate(G["recip_cases"]):
+        t, a, k = C.c_int64(), C.c_double(), C.c_int()
+        r, w = np.zeros(256), np.zeros(256)
+        check(tg.lib().tgb_reciprocal_expsum(lo, hi, eps, 256, C.byref(t), r.ctypes.data, w.ctypes.data, C.byref(a),
+                                             C.byref(k)), host=True)
+        assert (t.value, k.value) == (int(terms), int(ok)) and a.value == ach
+        assert np.array_equal(r[:t.value], G[f"recip_{idx}_rates"]) and np.array_equal(w[:t.value],
+                                                                                    G[f"recip_{idx}_weights"])

@@ -17,6 +17,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent / "tools"))
 from make_golden_scf import CASES  # noqa: E402
 
 pytestmark = pytest.mark.gpu
+TOL = 1e-10
 G = dict(np.load(Path(__file__).resolve().parent / "golden" / "reference_scf.npz"))
 
 
@@ -73,3 +74,19 @@ def test_scf_errors(ctx):
         tg.scf_solve(tg.Molecule(mol.nuclei, 3), bs, cfg, ctx)  # odd electron count
     with pytest.raises(tg.InvalidArgument):
         tg.scf_solve(tg.Molecule(mol.nuclei, 12), bs, cfg, ctx)  # more occupied orbitals than functions
+
+
+def test_mp2_matches_reference(ctx):
+    """mo_transform_cholesky + mp2_energy (mp2.cpp) on the reference's own SCF of the 'chain' case."""
+    nocc = int(G["mp2_nocc"][0])
+    mos = tg.MOSpace(G["mp2_coef"], G["mp2_energies"], nocc)
+    mo = tg.mo_transform_cholesky(G["mp2_chol"], mos, ctx)
+    assert relmax(mo.factor, G["mp2_mo_factor"]) <= TOL
+    e_or = tg.mp2_energy(mo, mos, "oracle", ctx=ctx)
+    e_fa = tg.mp2_energy(mo, mos, "factorized", float(G["mp2_expsum_eps"][0]), ctx=ctx)
+    assert abs(e_or - G["mp2_e2"][0]) <= TOL * abs(G["mp2_e2"][0])
+    assert abs(e_fa - G["mp2_e2"][1]) <= TOL * abs(G["mp2_e2"][1])
+    with pytest.raises(tg.NumericalError):  # reversed orbital energies: no positive gap (mp2.cpp:99-100)
+        tg.mp2_energy(mo, tg.MOSpace(G["mp2_coef"], G["mp2_energies"][::-1].copy(), nocc), ctx=ctx)
+    with pytest.raises(tg.InvalidArgument):
+        tg.mp2_energy(mo, tg.MOSpace(G["mp2_coef"], G["mp2_energies"], nocc + 1), ctx=ctx)
