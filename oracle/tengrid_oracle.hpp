@@ -5,15 +5,15 @@
 // Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
 // --impl reference legs may load it; the product path never does.
 //
-// Pinning: the conv-path translation units of the reference itself
-// (fft.cpp, tensor.cpp, grid.cpp, kernel.cpp, basis.cpp, lattice.cpp) are
-// compiled against oracle/eigen_shim into oracle/_ref/ (see oracle/Makefile)
-// and this restatement is checked against them and against the committed
-// fixtures in tests/golden/.  reduction.cpp and tei.cpp need Eigen's dense
-// decompositions (SelfAdjointEigenSolver, JacobiSVD, HouseholderQR), which are
-// absent from the image: for those rows this restatement is "parity unpinned"
-// against the reference binary and is pinned only by the reference's own
-// property tests (re-expressed in tests/test_oracle_*.py).
+// Pinning: the reference's own translation units (fft, tensor, grid, kernel,
+// basis, lattice, parallel, hf, tei, reduction, mp2 .cpp) are compiled in
+// place from /root/reference against oracle/eigen_shim into oracle/_ref/
+// (paper_1504_06289_b200/build.py build_ref).  The shim's dense
+// decompositions (SelfAdjointEigenSolver, HouseholderQR, JacobiSVD, LLT)
+// delegate to THIS restatement's LA, so oracle/_ref runs the reference's own
+// control flow (thresholds, pivots, rank rules, loop orders) on a stand-in LA.
+// The restatement is checked against oracle/_ref and the committed fixtures in
+// tests/golden/ (reference_conv_path.npz, reference_hf.npz, reference_scf.npz).
 //
 // Every function names the reference file:line it restates.  Matrices are
 // column-major (Eigen's default), entry (i, j) at data[i + rows * j].

@@ -165,6 +165,69 @@ def cfg4(ctx):
             "probe_ms_1e5": tv * 1e3}
 
 
+def cfg_hf(ctx):
+    """§8f operators on the config-1 basis (N_b=40 s/p, n=2049, R_N=41) and config-3-sized factors."""
+    import torch
+
+    import paper_1504_06289_b200 as tg
+    from paper_1504_06289_b200.inputs import KERNEL_C0, KERNEL_M, Rng, basis_case, occupied_coefficients
+
+    sync = torch.cuda.synchronize
+    bs, rng = basis_case(1)
+    disc = tg.discretize_basis(bs)
+    nb = len(disc)
+    c_occ = occupied_coefficients(rng, nb, 8)
+    es = tg.make_expsum(KERNEL_M[1], KERNEL_C0[1])
+    kp = tg.kernel_tensor(bs.grid, es, False)
+    kd = tg.kernel_tensor(bs.grid, es, True)
+    centres = sorted({f.center for f in bs.functions})
+    mol = tg.Molecule([tg.Nucleus(2.0, c) for c in centres], 2 * len(centres))
+    t_s, _ = timed(lambda: tg.overlap_matrix(bs, disc, ctx), reps=3, sync=sync)
+    t_t, _ = timed(lambda: tg.kinetic_matrix(bs, disc, False, ctx), reps=3, sync=sync)
+    t_v, V = timed(lambda: tg.nuclear_matrix(bs, disc, mol, kd, ctx), reps=3, sync=sync)
+    t_k, K = timed(lambda: tg.exchange_matrix(bs, disc, c_occ, kp, ctx), reps=1, sync=sync)
+    n, P, RN = bs.grid.n[0], nb, kp.rank()
+    G = P * P  # Hadamard columns per orbital (single-primitive functions, phi rank = nb)
+    flops_k = 8 * 2.0 * 3 * n * G * G * RN
+    out = {"config": "hf", "what": "config-1 basis: overlap/kinetic/nuclear/exchange; N_b=80 factor ops",
+           "overlap_ms": t_s * 1e3, "kinetic_ms": t_t * 1e3, "nuclear_ms": t_v * 1e3, "exchange_ms": t_k * 1e3,
+           "exchange_gemm_tflops": flops_k / t_k / 1e12, "exchange_fp64_frac": flops_k / t_k / 1e12 / FP64,
+           "exchange_convolutions": 8 * 3 * G * RN, "K_symmetric_exact": bool(np.array_equal(K, K.T))}
+    # Cholesky-factor operators at config-3 size (N_b=80, R_B=362)
+    r2 = Rng(77)
+    nb3, rb = 80, 362
+    Lh = np.asfortranarray(r2.normal(nb3 * nb3 * rb).reshape(nb3 * nb3, rb, order="F"))
+    cc = occupied_coefficients(r2, nb3, 20)
+    Dh = np.asfortranarray(2.0 * cc @ cc.T)
+    Hh = np.asfortranarray(np.diag(np.linspace(-5.0, 5.0, nb3)))
+    L = torch.from_numpy(np.ascontiguousarray(Lh.T)).cuda()
+    D = torch.from_numpy(np.ascontiguousarray(Dh.T)).cuda()
+    H = torch.from_numpy(np.ascontiguousarray(Hh.T)).cuda()
+    t_f, _ = timed(lambda: tg.fock_from_factors(H, L, D, ctx=ctx), reps=20, sync=sync)
+    flops_f = 2.0 * 2 * nb3 * nb3 * rb + 2.0 * nb3 ** 3 * rb * 2
+    S = np.eye(nb3) + 0.01 * (lambda a: a @ a.T)(r2.normal(nb3 * nb3).reshape(nb3, nb3))
+    F = 0.5 * (Lh[:, :nb3].reshape(nb3, nb3, nb3)[:, :, 0] + Lh[:, :nb3].reshape(nb3, nb3, nb3)[:, :, 0].T)
+    t_e, _ = timed(lambda: tg.generalized_eigensolve(F, S, ctx), reps=5, sync=sync)
+    # MP2 (oracle and factorized) with n_occ = 20 of 80
+    _, ev = tg.generalized_eigensolve(F, S, ctx)
+    Cm, _ = tg.generalized_eigensolve(F, S, ctx)
+    mos = tg.MOSpace(Cm, np.sort(ev) + np.where(np.arange(nb3) >= 20, 1.0, 0.0), 20)
+    t_mo, mo = timed(lambda: tg.mo_transform_cholesky(Lh, mos, ctx), reps=3, sync=sync)
+    t_m0, e0 = timed(lambda: tg.mp2_energy(mo, mos, "oracle", ctx=ctx), reps=3, sync=sync)
+    t_m1, e1 = timed(lambda: tg.mp2_energy(mo, mos, "factorized", 1e-9, ctx=ctx), reps=3, sync=sync)
+    out.update({"fock_from_factors_ms_nb80_rb362": t_f * 1e3, "fock_tflops": flops_f / t_f / 1e12,
+                "generalized_eigensolve_ms_nb80": t_e * 1e3, "mo_transform_ms": t_mo * 1e3,
+                "mp2_oracle_ms": t_m0 * 1e3, "mp2_factorized_ms": t_m1 * 1e3,
+                "mp2_rel_diff_oracle_vs_factorized": abs(e0 - e1) / abs(e0)})
+    # full SCF on the config-1 geometry: 4 centres, Z = 2 each, 8 electrons, N_b = 40 at n = 513
+    bs5 = tg.BasisSet(tg.make_grid(12.0, 513), bs.functions)
+    cfg = tg.SCFConfig(kernel_eps=1e-4, kernel_r_max=20.0, eps_fit=1e-7, eps_chol=1e-8)
+    t_scf, st = timed(lambda: tg.scf_solve(mol, bs5, cfg, ctx), reps=1, sync=sync)
+    out.update({"scf_s_n513_nb40": t_scf, "scf_iterations": st.iterations, "scf_converged": st.converged,
+                "scf_energy": st.energy, "scf_tei_rank_b": st.tei_rank_b, "scf_kernel_terms": 2 * st.kernel_m + 1})
+    return out
+
+
 def main():
     import paper_1504_06289_b200 as tg
 
@@ -173,11 +236,11 @@ def main():
     ctx = tg.Context(0)
     out = []
     for w in which:
-        fn = {"0": cfg0, "1": cfg1, "3": cfg3, "4": cfg4}[w]
+        fn = {"0": cfg0, "1": cfg1, "3": cfg3, "4": cfg4, "hf": cfg_hf}[w]
         try:
             r = fn(ctx)
         except Exception as exc:  # report and continue
-            r = {"config": int(w), "error": repr(exc)}
+            r = {"config": w, "error": repr(exc)}
         print(json.dumps(r), flush=True)
         out.append(r)
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
