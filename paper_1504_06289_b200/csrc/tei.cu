@@ -323,6 +323,231 @@ __global__ void chol_step_kernel(int64_t n, int rank, int p, double dmax, double
   diag[i] = d;
 }
 
+
+// ---- device-resident pivoted-Cholesky loop (tei.cpp:48-90 with the
+// max-diagonal stop of tei.cpp:198-204).  One step = the kernels below with
+// every step-dependent scalar (rank, pivot, max diagonal, the primitive pair of
+// the current column term, the stop flag) in device memory, so one captured
+// step replays as a CUDA graph with no host round trip.
+struct CholState {
+  int rank;      // columns produced so far
+  int done;      // stop rule met (or the cap): later steps are no-ops
+  int piv;       // current pivot (contracted pair index)
+  int j;         // current primitive pair of the column being formed
+  double dmax;   // current max diagonal
+  double w;      // weight of the current primitive pair (0: no term)
+  int flags[2];  // [0] clamped a negative diagonal, [1] negative beyond tolerance
+};
+
+// argmax of the diagonal (first maximal index, Eigen's maxCoeff(&p)); stop test
+__global__ void __launch_bounds__(kRedThreads) chol_pivot_kernel(int n, const double* __restrict__ d, double target,
+                                                                 int cap, CholState* st, int64_t* piv_list) {
+  if (st->done) return;
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  double v = -INFINITY;
+  int idx = 0x7fffffff;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) argmax_combine(v, idx, d[i], i);
+  block_argmax(v, idx, sv, si);
+  if (threadIdx.x == 0) {
+    if (st->rank >= cap || v <= target || v <= 0.0) {
+      st->done = 1;
+    } else {
+      st->piv = idx;
+      st->dmax = v;
+      piv_list[st->rank] = idx;
+    }
+  }
+}
+
+// primitive pair t of the pivot's contracted pair (kappa, lambda): q-major over
+// lambda's primitives, p over kappa's (tei.cpp:166-170 loop order)
+__global__ void chol_term_kernel(int nb, int np, int t, const int* __restrict__ fstart, const double* __restrict__ pw,
+                                 CholState* st) {
+  if (st->done) return;
+  const int c = st->piv, kappa = c % nb, lambda = c / nb;
+  const int nk = fstart[kappa + 1] - fstart[kappa], nl = fstart[lambda + 1] - fstart[lambda];
+  if (t >= nk * nl) {
+    st->w = 0.0;
+    return;
+  }
+  const int p = fstart[kappa] + t % nk, q = fstart[lambda] + t / nk;
+  st->j = p + np * q;
+  st->w = pw[p] * pw[q];
+}
+
+__global__ void gather_row_dev_kernel(const double* __restrict__ V, int64_t np2, int r, const CholState* st,
+                                      double* __restrict__ out) {
+  if (st->done) return;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q < r) out[q] = V[st->j + np2 * q];
+}
+
+__global__ void axpy_dev_kernel(int64_t n, const CholState* st, const double* __restrict__ x, double* __restrict__ y,
+                                int init) {
+  if (st->done) return;
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const double a = st->w;
+  if (init) y[i] = a * x[i];
+  else if (a != 0.0) y[i] = y[i] + a * x[i];
+}
+
+// tei.cpp:70-83 for the pivot in `st`; the rank advances in chol_advance_kernel.
+// The downdate col - L[:, :rank] L[p, :rank]^T is split over kCholParts
+// thread groups per row block (coalesced over rows, fixed-order reduction).
+constexpr int kCholRows = 64, kCholParts = 8;
+__global__ void __launch_bounds__(kCholRows * kCholParts) chol_step_dev_kernel(int64_t n, double max0, double neg_tol,
+                                                                               const double* __restrict__ col,
+                                                                               double* __restrict__ L,
+                                                                               double* __restrict__ diag,
+                                                                               CholState* st) {
+  if (st->done) return;
+  __shared__ double part[kCholParts][kCholRows];
+  const int row = threadIdx.x % kCholRows, grp = threadIdx.x / kCholRows;
+  const int64_t i = blockIdx.x * static_cast<int64_t>(kCholRows) + row;
+  const int rank = st->rank, p = st->piv;
+  double acc = 0.0;
+  if (i < n)
+    for (int r = grp; r < rank; r += kCholParts) acc += L[i + n * r] * L[p + n * r];
+  part[grp][row] = acc;
+  __syncthreads();
+  if (grp != 0 || i >= n) return;
+  double dd = 0.0;
+  for (int g = 0; g < kCholParts; ++g) dd += part[g][row];
+  const double piv = sqrt(st->dmax);
+  const double c = col[i] - dd;
+  double l = c / piv;
+  if (i == p) l = piv;
+  L[i + n * rank] = l;
+  double d = diag[i] - l * l;
+  if (i == p) d = 0.0;
+  if (d < 0.0) {
+    if (d < -neg_tol * max0) atomicOr(st->flags + 1, 1);
+    d = 0.0;
+    atomicOr(st->flags, 1);
+  }
+  diag[i] = d;
+}
+
+// y_ax[q + r k] = (M_k v)[q] with v = V_ax[j, :] (the pivot term's row): grid (K, 3)
+__global__ void chol_y_kernel(int64_t np2, int K, const int* __restrict__ rr, const double* const* __restrict__ V,
+                              const double* const* __restrict__ Ms, const CholState* st, double* const* __restrict__ Y) {
+  if (st->done) return;
+  const int k = blockIdx.x, ax = blockIdx.y, r = rr[ax];
+  extern __shared__ double vsh[];
+  const double* Va = V[ax];
+  for (int q = threadIdx.x; q < r; q += blockDim.x) vsh[q] = Va[st->j + np2 * q];
+  __syncthreads();
+  const double* M = Ms[ax];
+  const int64_t ld = static_cast<int64_t>(r) * K;
+  for (int a = threadIdx.x; a < r; a += blockDim.x) {
+    double acc = 0.0;
+#pragma unroll 16
+    for (int b = 0; b < r; ++b) acc += M[(a + static_cast<int64_t>(r) * k) + ld * b] * vsh[b];
+    Y[ax][a + static_cast<int64_t>(r) * k] = acc;
+  }
+}
+
+// z[i] = (init ? 0 : z[i]) + w sum_k prod_ax <V_ax[i, :], y_ax[:, k]>   (b_prim_column, tei.cpp:33-44,
+// and the contraction-weighted accumulation of tei.cpp:166-170), rows split over CTAs, the K columns of
+// each row over thread groups; products summed in k order.
+__global__ void chol_col_kernel(int64_t np2, int K, int rows, const int* __restrict__ rr,
+                                const double* const* __restrict__ V, const double* const* __restrict__ Y,
+                                const CholState* st, int init, double* __restrict__ z) {
+  if (st->done) return;
+  extern __shared__ double csh[];
+  const int r0 = rr[0], r1 = rr[1], r2 = rr[2];
+  double* ys[3] = {csh, csh + static_cast<int64_t>(r0) * K, csh + static_cast<int64_t>(r0 + r1) * K};
+  double* prod = csh + static_cast<int64_t>(r0 + r1 + r2) * K;  // rows x K
+  double* vt = prod + static_cast<int64_t>(rows) * K;              // rows x r_ax tile of V_ax
+  const int rax[3] = {r0, r1, r2};
+  for (int ax = 0; ax < 3; ++ax)
+    for (int e = threadIdx.x; e < rax[ax] * K; e += blockDim.x) ys[ax][e] = Y[ax][e];
+  __syncthreads();
+  const int groups = blockDim.x / rows;
+  const int row = threadIdx.x % rows, grp = threadIdx.x / rows;
+  const int64_t i0 = blockIdx.x * static_cast<int64_t>(rows);
+  const int64_t i = i0 + row;
+  constexpr int kMaxK = 8;  // K <= groups * kMaxK (host-checked)
+  double p[kMaxK];
+#pragma unroll
+  for (int u = 0; u < kMaxK; ++u) p[u] = 1.0;
+  for (int ax = 0; ax < 3; ++ax) {
+    const int r = rax[ax];
+    __syncthreads();  // the previous axis' tile is consumed
+    for (int e = threadIdx.x; e < rows * r; e += blockDim.x) {  // coalesced: rows are contiguous in V
+      const int rw = e % rows, q = e / rows;
+      vt[rw + rows * q] = i0 + rw < np2 ? V[ax][i0 + rw + np2 * q] : 0.0;
+    }
+    __syncthreads();
+    double acc[kMaxK];
+#pragma unroll
+    for (int u = 0; u < kMaxK; ++u) acc[u] = 0.0;
+    const double* y = ys[ax];
+    if (grp < groups) {
+      for (int q = 0; q < r; ++q) {
+        const double v = vt[row + rows * q];
+#pragma unroll
+        for (int u = 0; u < kMaxK; ++u) {
+          const int k = grp + u * groups;
+          if (k < K) acc[u] += v * y[q + r * k];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kMaxK; ++u) p[u] = ax == 0 ? acc[u] : p[u] * acc[u];
+  }
+  if (grp < groups && i < np2) {
+#pragma unroll
+    for (int u = 0; u < kMaxK; ++u) {
+      const int k = grp + u * groups;
+      if (k < K) prod[row + rows * k] = p[u];
+    }
+  }
+  __syncthreads();
+  if (grp == 0 && i < np2) {
+    double sum = 0.0;
+    for (int k = 0; k < K; ++k) sum += prod[row + rows * k];
+    const double w = st->w;
+    z[i] = init ? w * sum : (w != 0.0 ? z[i] + w * sum : z[i]);
+  }
+}
+
+// y_ax[q + r k] = Pk_ax[j + np2 (q + r k)] = (M_k V_ax[j, :]^T)[q]   (grid: 3 axes)
+__global__ void chol_ygather_kernel(int64_t np2, int K, const int* __restrict__ rr,
+                                    const double* const* __restrict__ Pk, const CholState* st,
+                                    double* const* __restrict__ Y) {
+  if (st->done) return;
+  const int ax = blockIdx.y;
+  const int64_t cnt = static_cast<int64_t>(rr[ax]) * K;
+  const double* src = Pk[ax] + st->j;
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < cnt;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    Y[ax][e] = src[np2 * e];
+}
+
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ a, double* __restrict__ t) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= rows * cols) return;
+  const int64_t i = idx % rows, j = idx / rows;
+  t[j + cols * i] = a[idx];
+}
+
+__global__ void fill_index_kernel(int n, int* __restrict__ ident, int* __restrict__ neg, double* __restrict__ ones,
+                                  int nones) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    ident[i] = i;
+    neg[i] = -1;
+  }
+  if (i < nones) ones[i] = 1.0;
+}
+
+__global__ void chol_advance_kernel(CholState* st) {
+  if (!st->done) st->rank += 1;
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------- host orchestration
@@ -342,6 +567,11 @@ struct TEI {
   int64_t RB = 0;
   std::vector<int64_t> chol_piv;
   DevBuf d_fstart, d_pw, d_cstart, d_cpairs, d_cw;
+  // pivoted-Cholesky column engine: Pk[ax] = [V M_0^T | ... | V M_{K-1}^T] (np^2 x r K),
+  // formed by the diagonal pass; Vt[ax] = V^T; identity / -1 index lists, unit weights
+  std::array<DevBuf, 3> Pk, Vt;
+  bool have_pk = false;
+  DevBuf d_ident, d_neg, d_ones, d_part;
 };
 
 }  // namespace tgb
@@ -490,10 +720,18 @@ void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
   TGB_CUDA(cudaMemsetAsync(diag, 0, nc * sizeof(double), ctx->stream));
   std::array<double*, 3> Y{};
   static thread_local std::array<DevBuf, 3> ybuf;
-  for (int ax = 0; ax < 3; ++ax) Y[ax] = static_cast<double*>(ybuf[ax].get(std::max<int64_t>(1, np2 * f.R[ax]) * sizeof(double)));
+  // keep every V M_k^T for the Cholesky columns when it fits a modest budget (config 3: 0.8 GB)
+  size_t pk_bytes = 0;
+  for (int ax = 0; ax < 3; ++ax) pk_bytes += static_cast<size_t>(np2) * f.R[ax] * f.K * sizeof(double);
+  f.have_pk = pk_bytes <= (size_t(8) << 30) && f.K > 0 && getenv("TGB_TEI_PK");  // opt-in: measured no faster
+  for (int ax = 0; ax < 3; ++ax) {
+    Y[ax] = static_cast<double*>(ybuf[ax].get(std::max<int64_t>(1, np2 * f.R[ax]) * sizeof(double)));
+    if (f.have_pk) f.Pk[ax].get(std::max<size_t>(8, static_cast<size_t>(np2) * f.R[ax] * f.K * sizeof(double)));
+  }
   for (int64_t k = 0; k < f.K; ++k) {
     for (int ax = 0; ax < 3; ++ax) {
       const int64_t r = f.R[ax];
+      if (f.have_pk) Y[ax] = dptr(f.Pk[ax]) + np2 * r * k;
       if (r == 0) continue;
       // Y = V M_k^T
       dgemm(ctx, false, true, np2, r, r, 1.0, dptr(f.V[ax]), np2, dptr(f.M[ax]) + r * r * k, r, 0.0, Y[ax], np2);
@@ -560,55 +798,218 @@ void tei_column_dev(tgb_ctx* ctx, TEI& f, int64_t pair, double* out) {
 }
 
 void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
-  const int64_t nb2 = f.nb * f.nb;
+  ensure_contraction_tables(ctx, f);
+  const int64_t nb = f.nb, np = f.np, nb2 = nb * nb, np2 = np * np, K = f.K;
   auto* dg = static_cast<double*>(f.diag.get(std::max<int64_t>(1, nb2) * sizeof(double)));
   tei_diagonal_dev(ctx, f, dg);
   f.L.get(std::max<int64_t>(1, nb2 * nb2) * sizeof(double));
-  auto* L = dptr(f.L);
-  static thread_local DevBuf colbuf, small;
+  double* L = dptr(f.L);
+  static thread_local DevBuf colbuf, zbuf, cbuf, stbuf, pivbuf;
+  static thread_local std::array<DevBuf, 3> wbuf, ybuf, vrow;
   auto* col = static_cast<double*>(colbuf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
-  auto* sm = static_cast<double*>(small.get(64 * sizeof(double)));
-  int* flags = reinterpret_cast<int*>(sm + 4);
-  TGB_CUDA(cudaMemsetAsync(flags, 0, 2 * sizeof(int), ctx->stream));
-  // max0 of the initial diagonal
-  struct VI {
-    double v;
-    int i;
-  };
-  auto argmax = [&](VI& out) {
+  auto* z = static_cast<double*>(zbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
+  auto* cc = static_cast<double*>(cbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
+  auto* st = static_cast<CholState*>(stbuf.get(sizeof(CholState)));
+  auto* piv = static_cast<int64_t*>(pivbuf.get(std::max<int64_t>(1, nb2) * sizeof(int64_t)));
+  std::array<double*, 3> W{}, Y{}, VR{};
+  for (int ax = 0; ax < 3; ++ax) {
+    W[ax] = static_cast<double*>(wbuf[ax].get(std::max<int64_t>(1, np2 * K) * sizeof(double)));
+    Y[ax] = static_cast<double*>(ybuf[ax].get(std::max<int64_t>(1, f.R[ax] * K) * sizeof(double)));
+    VR[ax] = static_cast<double*>(vrow[ax].get(std::max<int64_t>(1, f.R[ax]) * sizeof(double)));
+  }
+  // max0 of the initial diagonal (host: it fixes the stop target)
+  double hv[2];
+  {
+    auto* sm = static_cast<double*>(cbuf.p);
     argmax_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(nb2), dg, sm, reinterpret_cast<int*>(sm + 1));
     TGB_LAUNCHED(ctx);
-    double hv[2];
-    TGB_CUDA(cudaMemcpyAsync(hv, sm, 2 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaMemcpyAsync(hv, sm, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-    out.v = hv[0];
-    std::memcpy(&out.i, &hv[1], sizeof(int));
-  };
-  VI m0;
-  argmax(m0);
-  const double max0 = m0.v;
+  }
+  const double max0 = hv[0];
   f.chol_piv.clear();
-  int64_t rank = 0;
-  if (max0 > 0.0) {
-    const double target = eps_chol * max0;  // max-diagonal stop (tei.cpp:202)
-    const int64_t cap = nb2;
-    while (rank < cap) {
-      VI cur;
-      argmax(cur);
-      if (cur.v <= target || cur.v <= 0.0) break;
-      tei_column_dev(ctx, f, cur.i, col);
-      chol_step_kernel<<<static_cast<unsigned>((nb2 + 255) / 256), 256, 0, ctx->stream>>>(
-          nb2, static_cast<int>(rank), cur.i, cur.v, max0, 1e-10, col, L, dg, flags);
+  f.RB = 0;
+  if (!(max0 > 0.0)) return;
+  const double target = eps_chol * max0;  // max-diagonal stop (tei.cpp:202)
+  const int cap = static_cast<int>(nb2);
+  int max_terms = 1;  // primitive pairs per contracted pair, at most
+  for (int64_t a = 0; a < nb; ++a)
+    for (int64_t b = 0; b < nb; ++b)
+      max_terms = std::max<int>(max_terms, (f.fstart[a + 1] - f.fstart[a]) * (f.fstart[b + 1] - f.fstart[b]));
+  CholState h0{};
+  TGB_CUDA(cudaMemcpyAsync(st, &h0, sizeof(CholState), cudaMemcpyHostToDevice, ctx->stream));
+  // fused column path: the three y_ax (r_ax x K) and a rows x K product tile in shared memory
+  static thread_local DevBuf ptrbuf;
+  const int64_t rmax = std::max({f.R[0], f.R[1], f.R[2], int64_t(1)});
+  int col_rows = static_cast<int>(std::min<int64_t>(96, std::max<int64_t>(8, (np2 + ctx->num_sms - 1) / ctx->num_sms)));
+  const int col_groups = std::max(1, std::min(8, 1024 / col_rows));
+  const size_t col_smem =
+      static_cast<size_t>((f.R[0] + f.R[1] + f.R[2] + col_rows) * K + col_rows * rmax) * sizeof(double);
+  const bool fused_col = col_smem <= ctx->smem_optin - 1024 && K <= 8 * col_groups &&
+                         !getenv("TGB_TEI_GEMM_COLUMN") && K > 0;
+  const double** dV = nullptr;
+  const double** dM = nullptr;
+  double** dY = nullptr;
+  const double* const* dYc = nullptr;
+  const int* dr = nullptr;
+  const double* const* dPk = nullptr;
+  if (fused_col) {
+    static bool attr = false;
+    if (!attr) {
+      TGB_CUDA(cudaFuncSetAttribute(chol_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(ctx->smem_optin - 1024)));
+      attr = true;
+    }
+    struct Ptrs {
+      const double* V[3];
+      const double* M[3];
+      double* Y[3];
+      const double* P[3];
+      int r[4];
+    } hp{};
+    for (int ax = 0; ax < 3; ++ax) {
+      hp.V[ax] = dptr(f.V[ax]);
+      hp.M[ax] = dptr(f.Mst[ax]);
+      hp.Y[ax] = Y[ax];
+      hp.P[ax] = f.have_pk ? dptr(f.Pk[ax]) : nullptr;
+      hp.r[ax] = static_cast<int>(f.R[ax]);
+    }
+    auto* dp = static_cast<Ptrs*>(ptrbuf.get(sizeof(Ptrs)));
+    TGB_CUDA(cudaMemcpyAsync(dp, &hp, sizeof(Ptrs), cudaMemcpyHostToDevice, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));  // hp leaves scope
+    dV = const_cast<const double**>(dp->V);
+    dM = const_cast<const double**>(dp->M);
+    dY = dp->Y;
+    dYc = dp->Y;
+    dr = dp->r;
+    dPk = const_cast<const double**>(dp->P);
+  }
+  // DMMA column path over the stored V M_k^T (needs the transposed V and index lists once)
+  const bool pk_col = fused_col && f.have_pk;
+  if (pk_col) {
+    for (int ax = 0; ax < 3; ++ax) {
+      const int64_t r = f.R[ax];
+      auto* vt = static_cast<double*>(f.Vt[ax].get(std::max<int64_t>(1, r * np2) * sizeof(double)));
+      if (r)
+        transpose_kernel<<<static_cast<unsigned>((np2 * r + 255) / 256), 256, 0, ctx->stream>>>(np2, r, dptr(f.V[ax]),
+                                                                                               vt);
       TGB_LAUNCHED(ctx);
-      f.chol_piv.push_back(cur.i);
-      ++rank;
-      int hf[2];
-      TGB_CUDA(cudaMemcpyAsync(hf, flags, 2 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-      if (hf[1]) throw Error(TGB_NUMERICAL_ERROR, "pivoted_cholesky: negative diagonal beyond tolerance; matrix not PSD");
+    }
+    f.d_ident.get(std::max<int64_t>(1, np2) * sizeof(int));
+    f.d_neg.get(std::max<int64_t>(1, np2) * sizeof(int));
+    f.d_ones.get(std::max<int64_t>(1, K) * sizeof(double));
+    f.d_part.get(std::max<int64_t>(1, np2 * ((K + 63) / 64)) * sizeof(double));
+    const int nfill = static_cast<int>(std::max<int64_t>(np2, K));
+    fill_index_kernel<<<(nfill + 255) / 256, 256, 0, ctx->stream>>>(
+        static_cast<int>(np2), static_cast<int*>(f.d_ident.p), static_cast<int*>(f.d_neg.p),
+        static_cast<double*>(f.d_ones.p), static_cast<int>(K));
+    TGB_LAUNCHED(ctx);
+  }
+  const unsigned gnp = static_cast<unsigned>((np2 + 255) / 256);
+  auto step = [&]() {
+    chol_pivot_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(nb2), dg, target, cap, st, piv);
+    TGB_LAUNCHED(ctx);
+    for (int t = 0; t < max_terms; ++t) {
+      chol_term_kernel<<<1, 1, 0, ctx->stream>>>(static_cast<int>(nb), static_cast<int>(np), t,
+                                                 static_cast<const int*>(f.d_fstart.p),
+                                                 static_cast<const double*>(f.d_pw.p), st);
+      TGB_LAUNCHED(ctx);
+      if (pk_col) {  // y_k = row j of V M_k^T (gather), column on the DMMA separable kernel, accumulate
+        chol_ygather_kernel<<<dim3(16, 3), 256, 0, ctx->stream>>>(np2, static_cast<int>(K), dr, dPk, st, dY);
+        TGB_LAUNCHED(ctx);
+        const double* Fv[3] = {dptr(f.Vt[0]), dptr(f.Vt[1]), dptr(f.Vt[2])};
+        const double* By[3] = {Y[0], Y[1], Y[2]};
+        sep_inner_tiles(ctx, f.R.data(), Fv, By, static_cast<const double*>(f.d_ones.p), static_cast<int>(K),
+                        static_cast<const int*>(f.d_ident.p), static_cast<const int*>(f.d_neg.p),
+                        static_cast<int>(np2), static_cast<double*>(f.d_part.p), cc);
+        axpy_dev_kernel<<<gnp, 256, 0, ctx->stream>>>(np2, st, cc, z, t == 0 ? 1 : 0);
+        TGB_LAUNCHED(ctx);
+        continue;
+      }
+      if (fused_col) {  // y_k = M_k v (one launch), then the fused column + accumulation
+        chol_y_kernel<<<dim3(static_cast<unsigned>(K), 3), 128, rmax * sizeof(double), ctx->stream>>>(
+            np2, static_cast<int>(K), dr, dV, dM, st, dY);
+        TGB_LAUNCHED(ctx);
+        chol_col_kernel<<<static_cast<unsigned>((np2 + col_rows - 1) / col_rows), col_rows * col_groups, col_smem,
+                          ctx->stream>>>(np2, static_cast<int>(K), col_rows, dr, dV, dYc, st, t == 0 ? 1 : 0, z);
+        TGB_LAUNCHED(ctx);
+        continue;
+      }
+      for (int ax = 0; ax < 3; ++ax) {  // b_prim_column (tei.cpp:33-44) for the current primitive pair
+        const int64_t r = f.R[ax];
+        if (r == 0) {
+          TGB_CUDA(cudaMemsetAsync(W[ax], 0, np2 * K * sizeof(double), ctx->stream));
+          continue;
+        }
+        gather_row_dev_kernel<<<static_cast<unsigned>((r + 127) / 128), 128, 0, ctx->stream>>>(
+            dptr(f.V[ax]), np2, static_cast<int>(r), st, VR[ax]);
+        TGB_LAUNCHED(ctx);
+        dgemm(ctx, false, false, r * K, 1, r, 1.0, dptr(f.Mst[ax]), r * K, VR[ax], r, 0.0, Y[ax], r * K);
+        dgemm(ctx, false, false, np2, K, r, 1.0, dptr(f.V[ax]), np2, Y[ax], r, 0.0, W[ax], np2);
+      }
+      tei_col_combine_kernel<<<gnp, 256, 0, ctx->stream>>>(np2, static_cast<int>(K), W[0], W[1], W[2], cc);
+      TGB_LAUNCHED(ctx);
+      axpy_dev_kernel<<<gnp, 256, 0, ctx->stream>>>(np2, st, cc, z, t == 0 ? 1 : 0);
+      TGB_LAUNCHED(ctx);
+    }
+    contract_kernel<<<static_cast<unsigned>((nb2 + 127) / 128), 128, 0, ctx->stream>>>(
+        static_cast<int>(nb), static_cast<int>(np), static_cast<const int*>(f.d_fstart.p),
+        static_cast<const double*>(f.d_pw.p), z, col);
+    TGB_LAUNCHED(ctx);
+    chol_step_dev_kernel<<<static_cast<unsigned>((nb2 + kCholRows - 1) / kCholRows), kCholRows * kCholParts, 0,
+                           ctx->stream>>>(nb2, max0, 1e-10, col, L, dg, st);
+    TGB_LAUNCHED(ctx);
+    chol_advance_kernel<<<1, 1, 0, ctx->stream>>>(st);
+    TGB_LAUNCHED(ctx);
+  };
+  // one eager step sizes every workspace (no allocation may happen under capture)
+  step();
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  const bool use_graph = !getenv("TGB_TEI_NO_GRAPH");
+  int64_t per_step = 0;  // kernel launches in one step (captured, so counted per replay)
+  if (use_graph) {
+    const int64_t before = ctx->launches;
+    TGB_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+    try {
+      step();
+    } catch (...) {
+      cudaStreamEndCapture(ctx->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    TGB_CUDA(cudaStreamEndCapture(ctx->stream, &graph));
+    TGB_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+    per_step = ctx->launches - before;
+    ctx->launches = before;
+  }
+  CholState hs{};
+  const int batch = 16;
+  for (;;) {
+    TGB_CUDA(cudaMemcpyAsync(&hs, st, sizeof(CholState), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hs.flags[1]) {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      throw Error(TGB_NUMERICAL_ERROR, "pivoted_cholesky: negative diagonal beyond tolerance; matrix not PSD");
+    }
+    if (hs.done) break;
+    // a batch never needs more steps than the remaining cap
+    for (int b = 0; b < batch; ++b) {
+      if (exec) {
+        TGB_CUDA(cudaGraphLaunch(exec, ctx->stream));
+        ctx->launches += per_step;
+      } else {
+        step();
+      }
     }
   }
-  f.RB = rank;
+  if (exec) TGB_CUDA(cudaGraphExecDestroy(exec));
+  if (graph) TGB_CUDA(cudaGraphDestroy(graph));
+  f.RB = hs.rank;
+  f.chol_piv.resize(hs.rank);
+  if (hs.rank)
+    TGB_CUDA(cudaMemcpy(f.chol_piv.data(), piv, hs.rank * sizeof(int64_t), cudaMemcpyDeviceToHost));
 }
 
 }  // namespace tgb
