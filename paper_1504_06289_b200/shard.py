@@ -50,3 +50,26 @@ def allreduce_sum(x, group=None):
         return t.numpy()
     dist.all_reduce(x, group=group)
     return x
+
+
+def sharded_coulomb_matrix(bs, disc: list, theta, kernel, ctx=None, group=None, coulomb=None, hartree=None):
+    """J_km = h^3 <G_k . G_m, V_H> (hf.cpp:140-151) with the density columns
+    sharded over the ranks of `group`: each rank convolves its shard of theta
+    (its V_H columns, no exchange), assembles the partial J over those columns,
+    and ONE all-reduce of the N_b x N_b partials gives J on every rank (the
+    north-star's single allreduce of J blocks).  Exact symmetry survives: every
+    partial is mirrored before the sum.  `coulomb` / `hartree` default to the
+    libtgb operators (overridable so the CPU gloo test can stand the oracle in
+    for the per-rank GPU)."""
+    import torch.distributed as dist
+
+    from . import tengrid as tg
+
+    rank = dist.get_rank(group) if dist.is_available() and dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+    theta_r, _ = shard_canonical(theta, rank, world)
+    hartree = hartree or (lambda t: tg.hartree_potential(t, kernel, bs.grid.h, ctx))
+    coulomb = coulomb or (lambda v: tg.coulomb_matrix(bs, disc, v, ctx))
+    nb = len(disc)
+    part = coulomb(hartree(theta_r)) if theta_r.rank() else np.zeros((nb, nb))
+    return allreduce_sum(np.ascontiguousarray(part, dtype=np.float64), group)

@@ -166,3 +166,13 @@ def test_reduce_rank_vs_reference_binary(g, ctx):
     scale = np.linalg.norm(full)
     assert np.linalg.norm(dense - dense_ref) <= 0.5 * eps * scale
     assert np.linalg.norm(dense - full) <= eps * scale
+
+
+def test_sharded_coulomb_single_rank(g, case, ctx):
+    """The sharded J driver on one rank (no process group) is the plain device path."""
+    from paper_1504_06289_b200.shard import sharded_coulomb_matrix
+
+    bs, disc, kp, _ = case
+    theta = tg.CanonicalTensor3([g[f"theta_f{ax}"] for ax in range(3)], g["theta_w"])
+    J = sharded_coulomb_matrix(bs, disc, theta, kp, ctx)
+    assert relmax(J, g["J"]) <= TOL and np.array_equal(J, J.T)

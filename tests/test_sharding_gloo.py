@@ -74,3 +74,53 @@ def test_shards_cover_every_column_once(total, world):
         seen.append(global_columns(lo, hi, total, rb))
     allc = np.sort(np.concatenate(seen))
     assert np.array_equal(allc, np.arange(total * rb))
+
+
+def _worker_j(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from hf_case import functions, load
+        from oracle import oracle as O
+        from paper_1504_06289_b200.shard import sharded_coulomb_matrix
+        import paper_1504_06289_b200 as tg
+
+        g = load()
+        b, n = g["b_half"], g["n"]
+        theta = tg.CanonicalTensor3([g[f"theta_f{ax}"] for ax in range(3)], g["theta_w"])
+        m, c0 = int(g["kernel_m_c0"][0]), float(g["kernel_m_c0"][1])
+        nodes, w = O.make_expsum(m, c0)[:2]
+        kern = O.kernel_tensor(b, n, nodes, w, False)
+        disc = O.discretize_basis(b, n, functions(g))
+        hh = 2.0 * np.asarray(b) / (np.asarray(n) + 1)
+        J = sharded_coulomb_matrix(
+            None, disc, theta, None,
+            hartree=lambda t: O.hartree_potential(O.OCP.from_cp(t), kern, hh),
+            coulomb=lambda v: O.coulomb_matrix(b, n, disc, v))
+        if rank == 0:
+            q.put((float(np.abs(J - g["J"]).max() / np.abs(g["J"]).max()), bool(np.array_equal(J, J.T))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_coulomb_allreduce_gloo():
+    """J from density-column shards + one all-reduce equals the reference's own J (hf.cpp:140-151)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_j, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    err, sym = q.get(timeout=10)
+    assert err <= 1e-12 and sym
