@@ -56,6 +56,7 @@ struct PlanArgs {
   int nsp;  // single (self-mirror) first-pass blocks, stored last in the leader list
   const int* spos;  // pair_kernel_fused: positions of the leftover first-pass blocks (leaders 320..), 8 per thread
   int nspos;
+  int tt;           // pair_kernel_fused thread count the fused layout was built for (320 or 384)
   int fused;        // spectra stored in the fused order kf (pair_kernel_fused) instead of the DIT order
   const int* kf;    // fused order: slot -> natural frequency (N + 1 slots, Nyquist last)
   int dbg;  // analysis only (TGB_PAIR_DBG): 1 skip stores, 2 skip L2 loads, 4 skip passes
@@ -168,6 +169,13 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
   // (10, 20, 8, 8) balances every pass at 320 threads but its stride-10 first
   // pass bank-conflicts: measured slower (v14), opt-in only
   if (N == 12800 && getenv("TGB_PLAN_10208")) rad = {10, 20, 8, 8};
+  // opt-in 384-thread fused pair kernel (3 warps on every SM sub-partition;
+  // the plan's spans 16 and 128 divide 384 so every pass keeps hoisted
+  // twiddles).  Measured within 1.5 % of the 320-thread kernel (its radix-10
+  // last pass costs what the balanced sub-partitions gain), so not the default.
+  const bool tt384 = N == 12800 && getenv("TGB_TT384");
+  if (tt384) rad = {16, 8, 10, 10};
+  a.tt = tt384 ? 384 : 320;
   a.N = static_cast<int>(N);
   a.m = static_cast<int>(2 * N);
   const bool fits = !rad.empty();
@@ -220,11 +228,12 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
       }
     }
     a.npl = static_cast<int>(leaders.size());
-    // positions of the blocks of leaders[320 ..] (the fused kernel stages these
-    // through shared memory; leaders[0 .. 320) are transformed in registers)
+    // positions of the blocks of leaders[tt ..] (the fused kernel stages these
+    // through shared memory; leaders[0 .. tt) are transformed in registers)
+    const int tt = a.tt;
     std::vector<int> spos;
-    if (a.npl > 320) {
-      for (size_t q = 320; q < leaders.size(); ++q) {
+    if (a.npl > tt) {
+      for (size_t q = tt; q < leaders.size(); ++q) {
         for (int s2 = 0; s2 < r0; ++s2) spos.push_back(leaders[q].x * r0 + s2);
         if (leaders[q].y != leaders[q].x)
           for (int s2 = 0; s2 < r0; ++s2) spos.push_back(leaders[q].y * r0 + s2);
@@ -237,23 +246,26 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
       TGB_CUDA(cudaMemcpy(p, spos.data(), spos.size() * sizeof(int), cudaMemcpyHostToDevice));
       a.spos = static_cast<const int*>(p);
     }
-    // fused storage order (pair_kernel_fused, 320 threads, radix-16 first pass):
-    // slot s * 320 + t = element s of thread t's block pair (s < 16: block g,
-    // else block g2), then the staged positions u * 320 + t, then Nyquist
+    // fused storage order (pair_kernel_fused, tt threads, radix-16 first pass):
+    // slot s * tt + t = element s of thread t's block pair (s < 16: block g,
+    // else block g2), then staged position u * tt + t at slot 32 tt + u tt + t
+    // (contiguous: the staged count need not be a multiple of tt), then Nyquist
     a.fused = 0;
     a.kf = nullptr;
-    const bool fused_plan = rad.size() == 4 && rad[0] == 16 && rad[1] == 10 && rad[2] == 10 && rad[3] == 8 &&
-                            a.nspos == 8 * 320 && a.npl - a.nsp >= 320 && !getenv("TGB_NO_FUSED") &&
+    const bool plan_ok = rad.size() == 4 && rad[0] == 16 &&
+                         ((tt == 320 && rad[1] == 10 && rad[2] == 10 && rad[3] == 8) ||
+                          (tt == 384 && rad[1] == 8 && rad[2] == 10 && rad[3] == 10));
+    const bool fused_plan = plan_ok && a.nspos <= 8 * tt && a.nspos + 32 * tt == N && a.npl - a.nsp >= tt &&
+                            !getenv("TGB_NO_FUSED") &&
                             !getenv("TGB_NO_TMEM") && !getenv("TGB_NO_STATIC") && a.dbg == 0;
     if (fused_plan) {
       std::vector<int> kf(static_cast<size_t>(N) + 1);
-      for (int t = 0; t < 320; ++t)
+      for (int t = 0; t < tt; ++t)
         for (int s2 = 0; s2 < 32; ++s2) {
           const int g = s2 < 16 ? leaders[t].x : leaders[t].y;
-          kf[static_cast<size_t>(s2) * 320 + t] = perm[static_cast<size_t>(g) * 16 + (s2 & 15)];
+          kf[static_cast<size_t>(s2) * tt + t] = perm[static_cast<size_t>(g) * 16 + (s2 & 15)];
         }
-      for (int u = 0; u < 8; ++u)
-        for (int t = 0; t < 320; ++t) kf[static_cast<size_t>(32 + u) * 320 + t] = perm[spos[t + 320 * u]];
+      for (int idx = 0; idx < a.nspos; ++idx) kf[static_cast<size_t>(32) * tt + idx] = perm[spos[idx]];
       kf[N] = static_cast<int>(N);
       void* p = pl->kf.get(kf.size() * sizeof(int));
       TGB_CUDA(cudaMemcpy(p, kf.data(), kf.size() * sizeof(int), cudaMemcpyHostToDevice));
@@ -1119,7 +1131,7 @@ __device__ __forceinline__ void static_pass(double2* sm, const double2* lo, cons
 template <int R, int L, int N, int S, int TT>
 __device__ __forceinline__ void static_pass_t(double2* sm, const double2* lo, const double2* hi) {
   constexpr int NBF = N / R;
-  if constexpr (L > 1 && TT % L == 0 && NBF % TT == 0) {
+  if constexpr (L > 1 && TT % L == 0) {
     const int j = threadIdx.x % L;
     double2 w = L <= 64 ? lo[j] : cmul(lo[j & 63], hi[j >> 6]);
     if (S < 0) w.y = -w.y;
@@ -1528,7 +1540,8 @@ __global__ void __launch_bounds__(TT, 1)
   const double2 wk = cmul(tws[pa.off_zlo + (it.z & 63)], tws[pa.off_zhi + (it.z >> 6)]);
   int sp[NS];
 #pragma unroll
-  for (int u = 0; u < NS; ++u) sp[u] = __ldg(pa.spos + threadIdx.x + TT * u);
+  for (int u = 0; u < NS; ++u)  // -1: no staged position (the staged count need not be a multiple of TT)
+    sp[u] = static_cast<int>(threadIdx.x) + TT * u < pa.nspos ? __ldg(pa.spos + threadIdx.x + TT * u) : -1;
   const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
   const int w1 = static_cast<int>((static_cast<int64_t>(nwork) * (blockIdx.x + 1)) / gridDim.x);
   int ia_cur = -1;
@@ -1545,7 +1558,8 @@ __global__ void __launch_bounds__(TT, 1)
         uint32_t r[32];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const double2 v = ld2(a + (8 * c + u) * TT + threadIdx.x);  // fused order: coalesced
+          const bool live = c < 4 || static_cast<int>(threadIdx.x) + TT * u < pa.nspos;
+          const double2 v = live ? ld2(a + (8 * c + u) * TT + threadIdx.x) : make_double2(0.0, 0.0);  // coalesced
           r[4 * u + 0] = __double2loint(v.x);
           r[4 * u + 1] = __double2hiint(v.x);
           r[4 * u + 2] = __double2loint(v.y);
@@ -1570,7 +1584,8 @@ __global__ void __launch_bounds__(TT, 1)
       tmem_ld32(tbase + 128, r);
       tmem_wait_ld();
 #pragma unroll
-      for (int u = 0; u < NS; ++u) sm[pidx(sp[u])] = bval(32 + u, tm2(r, u));
+      for (int u = 0; u < NS; ++u)
+        if (sp[u] >= 0) sm[pidx(sp[u])] = bval(32 + u, tm2(r, u));
     }
     // (2) the fused item: product, real split, two radix-16 butterflies
     {
@@ -1820,7 +1835,7 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
   const PlanArgs& a = pl.a;
   if (!(a.P == 4 && a.r[0] == R0 && a.r[1] == R1 && a.r[2] == R2 && a.r[3] == R3) || a.dbg || getenv("TGB_NO_STATIC"))
     return false;
-  const bool fused_ok = R0 == 16 && TT == 320 && a.fused;  // the spectra were written in the fused order
+  const bool fused_ok = R0 == 16 && TT == a.tt && a.fused;  // the spectra were written in the fused order
   auto kern = (getenv("TGB_NO_TMEM") || a.N % TT) ? pair_kernel_static<R0, R1, R2, R3, TT, BREAL>
                                                   : pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>;
   if constexpr (R0 == 16) {
@@ -1868,10 +1883,47 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
   return true;
 }
 
+// The 384-thread fused pair kernel (plan 16 x 8 x 10 x 10): only the fused
+// kernel exists at this width (the spectra are in its storage order).
+static bool a_is_fused_elsewhere(const ConvPlan& pl) { return pl.a.fused && pl.a.tt != 320; }
+
+template <bool BREAL>
+static bool try_fused384(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
+                         const PairEntry* dwork, const int* winfo, double* out) {
+  const PlanArgs& a = pl.a;
+  if (!(a.P == 4 && a.r[0] == 16 && a.r[1] == 8 && a.r[2] == 10 && a.r[3] == 10 && a.fused && a.tt == 384))
+    return false;
+  auto kern = pair_kernel_fused<16, 8, 10, 10, 384, BREAL>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncAttributes fa{};
+    TGB_CUDA(cudaFuncGetAttributes(&fa, kern));
+    TGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
+    attr = true;
+  }
+  prof_begin(ctx);
+  kern<<<ctx->num_sms, 384, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);
+  TGB_LAUNCHED(ctx);
+  prof_end(ctx);
+  if (a.phase) {
+    unsigned long long h[8];
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    TGB_CUDA(cudaMemcpy(h, a.phase, sizeof(h), cudaMemcpyDeviceToHost));
+    const double np = static_cast<double>(h[5] ? h[5] : 1);
+    fprintf(stderr, "phase cycles/pair: stage %.0f pass0 %.0f pass1 %.0f pass2 %.0f last %.0f (pairs %llu)\n",
+            h[0] / np, h[1] / np, h[2] / np, h[3] / np, h[4] / np, h[5]);
+    TGB_CUDA(cudaMemset(a.phase, 0, sizeof(h)));
+  }
+  return true;
+}
+
 template <bool BREAL>
 static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                           const PairEntry* dwork, const int* winfo, double* out) {
   // compile-time plans (config 2: n = 16385 -> N = 12800)
+  if (try_fused384<BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
+  if (a_is_fused_elsewhere(pl)) throw Error(TGB_CUDA_ERROR, "fftconv: fused spectrum order without its pair kernel");
   if (try_static<10, 20, 8, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
   if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
   switch (pl.a.r[0]) {
@@ -1899,6 +1951,18 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
     attr_set = true;
   }
   const PlanArgs& a = pl.a;
+  if (a.P == 4 && a.r[0] == 16 && a.r[1] == 8 && a.r[2] == 10 && a.r[3] == 10 && !getenv("TGB_NO_STATIC")) {
+    static bool attr3 = false;
+    if (!attr3) {
+      TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel_static<16, 8, 10, 10, 320>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+      attr3 = true;
+    }
+    spectrum_kernel_static<16, 8, 10, 10, 320><<<nA + nB, 320, pl.smem, ctx->stream>>>(
+        pl.a, A, nA, specA, B, colidx, nB, specB, specB2, modeB, ldx, h);
+    TGB_LAUNCHED(ctx);
+    return;
+  }
   if (a.P == 4 && a.r[0] == 16 && a.r[1] == 10 && a.r[2] == 10 && a.r[3] == 8 && !getenv("TGB_NO_STATIC")) {
     static bool attr2 = false;
     if (!attr2) {
