@@ -38,6 +38,7 @@ extern "C" {
 #define TGB_MEM_DEVICE 1
 
 typedef struct tgb_ctx tgb_ctx;
+typedef struct tgb_tucker tgb_tucker; /* device-resident Tucker result (rank reduction, below) */
 
 /* Rank-R canonical tensor sum_k w_k u_k^(1) x u_k^(2) x u_k^(3)
  * (reference CanonicalTensor3, proj/include/tengrid/tensor.hpp:119-150). */
@@ -227,6 +228,21 @@ int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offs
  * non-derivative axes. */
 int tgb_kinetic_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
                        int exact_mass, double* T, int mem);
+
+/* replaces tg::density_tensor (hf.hpp:34-35, hf.cpp:118-129) with the tensor
+ * built on the device: Theta = sum_a 2 phi_a . phi_a from the flattened basis
+ * and c_occ (nb x nocc, HOST memory), then reduce_rank(reduce_eps) (RHOSVD +
+ * ALS + T2C) on the device when rank > 1 and reduce_eps > 0.
+ *  - tgb_density_rank: the unreduced rank sum_a R_phi_a^2;
+ *  - tgb_density_build: the unreduced Theta into `out` (rank = that value);
+ *  - tgb_density_reduce: build + canonical_to_tucker; *out receives the
+ *    Tucker handle (tgb_tucker_info / tgb_tucker_to_canonical as for
+ *    tgb_reduce_tucker, max_sweeps 3 as ReductionConfig::tolerance). */
+int tgb_density_rank(const int64_t* fn_offset, int64_t nb, const double* c_occ, int64_t nocc, int64_t* rank);
+int tgb_density_build(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,
+                      int64_t nocc, tgb_cp* out, int mem);
+int tgb_density_reduce(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,
+                       int64_t nocc, double reduce_eps, int mem, tgb_tucker** out);
 
 /* ---- factorised two-electron integrals (proj/include/tengrid/tei.hpp:38-72) ----
  * A tgb_tei holds the device-resident factorisation (TEIFactorization,

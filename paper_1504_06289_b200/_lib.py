@@ -114,6 +114,9 @@ def lib() -> C.CDLL:
             "tgb_mo_transform_cholesky": (I, [P, I64, I64, P, I64, P, P, I]),
             "tgb_mp2_energy": (I, [P, I64, I64, I64, P, P, I, D, C.POINTER(D), I]),
             "tgb_reciprocal_expsum": (I, [D, D, D, I64, C.POINTER(I64), P, P, C.POINTER(D), C.POINTER(I)]),
+            "tgb_density_rank": (I, [P, I64, P, I64, C.POINTER(I64)]),
+            "tgb_density_build": (I, [P, C.POINTER(tgb_cp), P, I64, P, I64, C.POINTER(tgb_cp), I]),
+            "tgb_density_reduce": (I, [P, C.POINTER(tgb_cp), P, I64, P, I64, D, I, C.POINTER(P)]),
             "tgb_overlap_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, P, I]),
             "tgb_kinetic_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, I, P, I]),
             "tgb_tei_create": (I, [C.POINTER(P)]),

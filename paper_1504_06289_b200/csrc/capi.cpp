@@ -588,6 +588,80 @@ int tgb_mp2_energy(tgb_ctx* ctx, int64_t n_occ, int64_t n_vir, int64_t rank, con
   });
 }
 
+int tgb_density_rank(const int64_t* fn_offset, int64_t nb, const double* c_occ, int64_t nocc, int64_t* rank) {
+  return guarded([&] {
+    tgb::require(nb >= 1, "density_tensor: empty basis");
+    tgb::require(nocc >= 0 && (nocc == 0 || c_occ) && rank, "density_tensor: coefficient shape mismatch");
+    *rank = tgb::density_rank(fn_offset, nb, c_occ, nocc);
+  });
+}
+
+int tgb_density_build(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,
+                      int64_t nocc, tgb_cp* out, int mem) {
+  return guarded([&] {
+    check_basis(basis, fn_offset, nb, "density_tensor");
+    tgb::require(nb >= 1, "density_tensor: empty basis");
+    tgb::require(out && (nocc == 0 || c_occ), "density_tensor: null argument");
+    check_extents(basis, out, "density_tensor");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    tgb::DevStreamScope scope(ctx);
+    DevCP db(basis, mem == TGB_MEM_DEVICE);
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::density_build_dev(ctx, db.t, fn_offset, nb, c_occ, nocc, *out);
+      return;
+    }
+    DevCP dout(out, false);  // device image of the (host) output
+    tgb::density_build_dev(ctx, db.t, fn_offset, nb, c_occ, nocc, dout.t);
+    for (int ax = 0; ax < 3; ++ax)
+      if (out->rank)
+        TGB_CUDA(cudaMemcpy(out->factor[ax], dout.t.factor[ax], out->n[ax] * out->rank * sizeof(double),
+                            cudaMemcpyDeviceToHost));
+    if (out->rank) TGB_CUDA(cudaMemcpy(out->weight, dout.t.weight, out->rank * sizeof(double), cudaMemcpyDeviceToHost));
+  });
+}
+
+int tgb_density_reduce(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,
+                       int64_t nocc, double reduce_eps, int mem, tgb_tucker** out) {
+  return guarded([&] {
+    check_basis(basis, fn_offset, nb, "density_tensor");
+    tgb::require(nb >= 1, "density_tensor: empty basis");
+    tgb::require(out && (nocc == 0 || c_occ), "density_tensor: null argument");
+    tgb::require(reduce_eps > 0.0, "ReductionConfig: set exactly one of {ranks, epsilon}");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    const int64_t rank = tgb::density_rank(fn_offset, nb, c_occ, nocc);
+    DevCP db(basis, mem == TGB_MEM_DEVICE);
+    tgb_cp theta{};
+    std::vector<double*> bufs;
+    auto cleanup = [&] {
+      for (double* p : bufs) cudaFree(p);
+    };
+    try {
+      for (int ax = 0; ax < 3; ++ax) {
+        theta.n[ax] = basis->n[ax];
+        double* p = nullptr;
+        TGB_CUDA(cudaMalloc(&p, std::max<int64_t>(1, basis->n[ax] * rank) * sizeof(double)));
+        bufs.push_back(p);
+        theta.factor[ax] = p;
+      }
+      double* w = nullptr;
+      TGB_CUDA(cudaMalloc(&w, std::max<int64_t>(1, rank) * sizeof(double)));
+      bufs.push_back(w);
+      theta.weight = w;
+      theta.rank = rank;
+      {
+        tgb::DevStreamScope scope(ctx);
+        tgb::density_build_dev(ctx, db.t, fn_offset, nb, c_occ, nocc, theta);
+      }
+      const int rc = tgb_reduce_tucker(ctx, &theta, 1, reduce_eps, nullptr, 3, 1, TGB_MEM_DEVICE, out);
+      if (rc != TGB_OK) throw tgb::Error(rc, tgb_last_error());
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+  });
+}
+
 int tgb_overlap_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const double h[3],
                        double* S, int mem) {
   return one_electron(ctx, 0, basis, fn_offset, nb, h, S, mem);

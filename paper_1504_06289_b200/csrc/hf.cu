@@ -516,6 +516,66 @@ void one_electron_dev(tgb_ctx* ctx, int which, const tgb_cp& basis, const int64_
     }
 }
 
+// ---------------------------------------------------------------- density tensor
+
+// Theta = sum_a 2 phi_a . phi_a (hf.cpp:118-127): phi_a = concatenation of
+// scale(G_k, c_ka) over c_ka != 0 (orbital_tensor, hf.cpp:39-46); the
+// Hadamard square has column i + R_phi j = F(:, p_i) .* F(:, p_j) and weight
+// (w_i c_i)(w_j c_j) * 2 (tensor.cpp:151-153, 176), orbitals concatenated in
+// order (add, tensor.cpp:159-171).  Builds the factors into `out` (device,
+// rank = density_rank()) without touching the host.
+int64_t density_rank(const int64_t* fn_offset, int64_t nb, const double* c_occ, int64_t nocc) {
+  int64_t tot = 0;
+  for (int64_t a = 0; a < nocc; ++a) {
+    int64_t r = 0;
+    for (int64_t k = 0; k < nb; ++k)
+      if (c_occ[k + nb * a] != 0.0) r += fn_offset[k + 1] - fn_offset[k];
+    tot += r * r;
+  }
+  return tot;
+}
+
+void density_build_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,
+                       int64_t nocc, tgb_cp& out) {
+  const int64_t P = basis.rank;
+  std::vector<double> wprim(P);
+  if (P) TGB_CUDA(cudaMemcpy(wprim.data(), basis.weight, P * sizeof(double), cudaMemcpyDeviceToHost));
+  std::vector<int> gi, gj;
+  std::vector<double> w;
+  for (int64_t a = 0; a < nocc; ++a) {
+    std::vector<int> pc;
+    std::vector<double> wphi;
+    for (int64_t k = 0; k < nb; ++k) {
+      const double c = c_occ[k + nb * a];
+      if (c == 0.0) continue;
+      for (int64_t p = fn_offset[k]; p < fn_offset[k + 1]; ++p) {
+        pc.push_back(static_cast<int>(p));
+        wphi.push_back(wprim[p] * c);
+      }
+    }
+    const size_t r = pc.size();
+    for (size_t j = 0; j < r; ++j)
+      for (size_t i = 0; i < r; ++i) {
+        gi.push_back(pc[i]);
+        gj.push_back(pc[j]);
+        w.push_back((wphi[i] * wphi[j]) * 2.0);
+      }
+  }
+  const int64_t cols = static_cast<int64_t>(w.size());
+  require(cols == out.rank, "density_tensor: output rank mismatch");
+  if (cols == 0) return;
+  Scratch sgi(ctx, (cols + 1) / 2), sgj(ctx, (cols + 1) / 2);
+  const int* dgi = upload(ctx, sgi, gi);
+  const int* dgj = upload(ctx, sgj, gj);
+  TGB_CUDA(cudaMemcpyAsync(out.weight, w.data(), cols * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+  for (int ax = 0; ax < 3; ++ax) {
+    hadamard_pairs_kernel<<<col_grid(basis.n[ax], cols), 256, 0, ctx->stream>>>(basis.n[ax], basis.factor[ax], dgi,
+                                                                                dgj, cols, out.factor[ax]);
+    TGB_LAUNCHED(ctx);
+  }
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));  // host index/weight vectors leave scope
+}
+
 // ---------------------------------------------------------------- generalized eigensolver
 
 void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e) {

@@ -169,6 +169,9 @@ void mo_transform_dev(tgb_ctx* ctx, int64_t nb, int64_t R, const double* chol, i
 double mp2_energy_dev(tgb_ctx* ctx, int64_t n_occ, int64_t n_vir, int64_t R, const double* F, const double* e_host,
                       int mode, double expsum_eps);
 // hf.cu
+int64_t density_rank(const int64_t* fn_offset, int64_t nb, const double* c_occ, int64_t nocc);
+void density_build_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const double* c_occ,
+                       int64_t nocc, tgb_cp& out);
 void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e);
 void nuclear_potential_dev(tgb_ctx* ctx, const tgb_cp& ref, const int64_t n[3], const int64_t* offsets,
                            const double* charges, int64_t nnuc, tgb_cp& out);

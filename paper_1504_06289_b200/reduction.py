@@ -78,12 +78,17 @@ def _run(a: CanonicalTensor3, cfg: ReductionConfig, mode: int, ctx: Context | No
     ranks = np.asarray(cfg.ranks if cfg.ranks is not None else (0, 0, 0), dtype=np.int64)
     check(lib().tgb_reduce_tucker(ctx.handle, C.byref(ca), int(cfg.epsilon is not None), cfg.epsilon or 0.0,
                                   ranks.ctypes.data, cfg.max_sweeps, mode, MEM_HOST, C.byref(h)))
+    return _tucker_result(h, a.extents(), ctx)
+
+
+def _tucker_result(h, dims, ctx: Context) -> TuckerResult:
+    """Read a device-resident Tucker result (tgb_tucker handle) back to the host."""
     hh = _Handle(h)
     info = np.zeros(7, dtype=np.int64)
     check(lib().tgb_tucker_info(h, info.ctypes.data))
     r = tuple(int(x) for x in info[:3])
     core = np.zeros(r, order="F")
-    sides = [np.zeros((a.extent(ax), r[ax]), order="F") for ax in range(3)]
+    sides = [np.zeros((dims[ax], r[ax]), order="F") for ax in range(3)]
     fits = np.zeros(max(1, int(info[5])))
     check(lib().tgb_tucker_get(h, core.ctypes.data if core.size else None,
                                *[s.ctypes.data if s.size else None for s in sides], fits.ctypes.data, MEM_HOST))

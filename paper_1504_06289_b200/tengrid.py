@@ -596,21 +596,33 @@ def orbital_tensor(disc: list, coeff) -> CanonicalTensor3:
 
 
 def density_tensor(disc: list, c_occ, reduce_eps: float = 1e-7, ctx: Context | None = None) -> CanonicalTensor3:
-    """hf.cpp:118-129 — Theta = sum_a 2 phi_a . phi_a, then reduce_rank on the device."""
-    from .reduction import ReductionConfig, reduce_rank
+    """hf.cpp:118-129 — Theta = sum_a 2 phi_a . phi_a built on the device from the
+    basis factors (tgb_density_build), then reduce_rank on the device
+    (tgb_density_reduce) when rank > 1 and reduce_eps > 0."""
+    from .reduction import _t2c, _tucker_result
 
     if not disc:
         raise InvalidArgument("density_tensor: empty basis")
-    c_occ = np.asarray(c_occ, dtype=np.float64)
-    if c_occ.shape[0] != len(disc):
+    ctx = ctx or default_context()
+    c = np.asfortranarray(np.asarray(c_occ, dtype=np.float64))
+    if c.ndim != 2 or c.shape[0] != len(disc):
         raise InvalidArgument("density_tensor: coefficient shape mismatch")
-    theta = CanonicalTensor3.zero(disc[0].extents())
-    for a in range(c_occ.shape[1]):
-        phi = orbital_tensor(disc, c_occ[:, a])
-        theta = add(theta, scale(hadamard(phi, phi), 2.0))
-    if theta.rank() <= 1 or reduce_eps <= 0.0:
+    flat, offs = flatten_basis(disc)
+    nb, nocc = len(disc), c.shape[1]
+    cf = flat._cstruct()
+    cp = c.ctypes.data if c.size else None
+    rank = C.c_int64()
+    check(lib().tgb_density_rank(offs.ctypes.data, nb, cp, nocc, C.byref(rank)))
+    dims = disc[0].extents()
+    if rank.value <= 1 or reduce_eps <= 0.0:
+        theta = CanonicalTensor3([np.zeros((d, rank.value), order="F") for d in dims], np.zeros(rank.value))
+        co = theta._cstruct()
+        check(lib().tgb_density_build(ctx.handle, C.byref(cf), offs.ctypes.data, nb, cp, nocc, C.byref(co), MEM_HOST))
         return theta
-    return reduce_rank(theta, ReductionConfig.tolerance(reduce_eps), ctx)
+    h = C.c_void_p()
+    check(lib().tgb_density_reduce(ctx.handle, C.byref(cf), offs.ctypes.data, nb, cp, nocc, reduce_eps, MEM_HOST,
+                                   C.byref(h)))
+    return _t2c(_tucker_result(h, dims, ctx), dims)
 
 
 @dataclass

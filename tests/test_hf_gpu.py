@@ -176,3 +176,23 @@ def test_sharded_coulomb_single_rank(g, case, ctx):
     theta = tg.CanonicalTensor3([g[f"theta_f{ax}"] for ax in range(3)], g["theta_w"])
     J = sharded_coulomb_matrix(bs, disc, theta, kp, ctx)
     assert relmax(J, g["J"]) <= TOL and np.array_equal(J, J.T)
+
+
+def test_density_tensor_device_build(g, case, ctx):
+    """density_tensor (hf.cpp:118-129) built on the device: the unreduced Theta is bit-identical to the
+    reference's own; the reduced one has the reference's Tucker/canonical ranks and dense image."""
+    _, disc, _, _ = case
+    theta = tg.density_tensor(disc, g["c_occ"], 0.0, ctx)
+    assert theta.rank() == int(g["theta_rank"][0])
+    for ax in range(3):
+        assert np.array_equal(theta.factor[ax], g[f"theta_f{ax}"])
+    assert np.array_equal(theta.weight, g["theta_w"])
+    eps = float(g["red_eps"][0])
+    red = tg.density_tensor(disc, g["c_occ"], eps, ctx)
+    assert red.rank() == int(g["red_canonical_rank"][0])
+    ref = tg.CanonicalTensor3([g[f"red_f{ax}"] for ax in range(3)], g["red_w"])
+    full = theta.to_dense()
+    scale = np.linalg.norm(full)
+    assert np.linalg.norm(red.to_dense() - ref.to_dense()) <= 0.5 * eps * scale
+    with pytest.raises(tg.InvalidArgument):
+        tg.density_tensor(disc, g["c_occ"][:-1], eps, ctx)

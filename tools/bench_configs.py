@@ -86,6 +86,8 @@ def cfg1(ctx):
     t_build = time.perf_counter() - t_build0
     cfgr = tg.ReductionConfig.tolerance(1e-6)
     t_red, red = timed(lambda: tg.reduce_rank(theta_full, cfgr, ctx), reps=1, sync=torch.cuda.synchronize)
+    # the drop-in density_tensor: Theta built on the device from the basis, reduced there
+    t_dens, red2 = timed(lambda: tg.density_tensor(disc, c_occ, 1e-6, ctx), reps=1, sync=torch.cuda.synchronize)
     res = tg.canonical_to_tucker(theta_full, cfgr, ctx)
     kern = tg.kernel_tensor(bs.grid, tg.make_expsum(KERNEL_M[1], KERNEL_C0[1]), False)
     dt, dk = tg.DeviceCP.from_host(red), tg.DeviceCP.from_host(kern.tensor)
@@ -95,7 +97,8 @@ def cfg1(ctx):
     n, P, RV = bs.grid.n[0], len(disc) * (len(disc) + 1) // 2, vh.rank()
     flops_j = 2.0 * 3 * n * P * RV
     return {"config": 1, "what": "density(12800)->reduce_rank(1e-6)->V_H->coulomb_matrix, n=2049, N_b=40",
-            "density_build_host_s": t_build, "reduce_rank_ms": t_red * 1e3, "tucker_ranks": list(res.tucker.ranks()),
+            "density_build_host_s": t_build, "reduce_rank_ms": t_red * 1e3,
+            "density_tensor_device_ms": t_dens * 1e3, "density_tensor_rank": red2.rank(), "tucker_ranks": list(res.tucker.ranks()),
             "reduced_rank": red.rank(), "hartree_ms": t_vh * 1e3, "R_V": RV, "coulomb_ms": t_j * 1e3,
             "coulomb_tflops": flops_j / t_j / 1e12, "coulomb_fp64_frac": flops_j / t_j / 1e12 / FP64,
             "J_symmetric_exact": bool(np.array_equal(J, J.T)), "J_trace": float(np.trace(J))}
