@@ -174,7 +174,7 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
   // twiddles).  Measured within 1.5 % of the 320-thread kernel (its radix-10
   // last pass costs what the balanced sub-partitions gain), so not the default.
   const bool tt384 = N == 12800 && getenv("TGB_TT384");
-  if (tt384) rad = {16, 8, 10, 10};
+  if (tt384) rad = atoi(getenv("TGB_TT384")) == 2 ? std::vector<int>{16, 10, 10, 8} : std::vector<int>{16, 8, 10, 10};
   a.tt = tt384 ? 384 : 320;
   a.N = static_cast<int>(N);
   a.m = static_cast<int>(2 * N);
@@ -254,7 +254,8 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
     a.kf = nullptr;
     const bool plan_ok = rad.size() == 4 && rad[0] == 16 &&
                          ((tt == 320 && rad[1] == 10 && rad[2] == 10 && rad[3] == 8) ||
-                          (tt == 384 && rad[1] == 8 && rad[2] == 10 && rad[3] == 10));
+                          (tt == 384 && ((rad[1] == 8 && rad[2] == 10 && rad[3] == 10) ||
+                                         (rad[1] == 10 && rad[2] == 10 && rad[3] == 8))));
     const bool fused_plan = plan_ok && a.nspos <= 8 * tt && a.nspos + 32 * tt == N && a.npl - a.nsp >= tt &&
                             !getenv("TGB_NO_FUSED") &&
                             !getenv("TGB_NO_TMEM") && !getenv("TGB_NO_STATIC") && a.dbg == 0;
@@ -1540,8 +1541,10 @@ __global__ void __launch_bounds__(TT, 1)
   const double2 wk = cmul(tws[pa.off_zlo + (it.z & 63)], tws[pa.off_zhi + (it.z >> 6)]);
   int sp[NS];
 #pragma unroll
-  for (int u = 0; u < NS; ++u)  // -1: no staged position (the staged count need not be a multiple of TT)
-    sp[u] = static_cast<int>(threadIdx.x) + TT * u < pa.nspos ? __ldg(pa.spos + threadIdx.x + TT * u) : -1;
+  // staged count N - 32 TT: a multiple of TT for the 320-thread layout (no guards compiled), ragged at 384
+  constexpr bool kRagged = (N - 32 * TT) % TT != 0;
+  for (int u = 0; u < NS; ++u)  // -1: no staged position
+    sp[u] = (!kRagged || static_cast<int>(threadIdx.x) + TT * u < pa.nspos) ? __ldg(pa.spos + threadIdx.x + TT * u) : -1;
   const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
   const int w1 = static_cast<int>((static_cast<int64_t>(nwork) * (blockIdx.x + 1)) / gridDim.x);
   int ia_cur = -1;
@@ -1558,7 +1561,7 @@ __global__ void __launch_bounds__(TT, 1)
         uint32_t r[32];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const bool live = c < 4 || static_cast<int>(threadIdx.x) + TT * u < pa.nspos;
+          const bool live = !kRagged || c < 4 || static_cast<int>(threadIdx.x) + TT * u < pa.nspos;
           const double2 v = live ? ld2(a + (8 * c + u) * TT + threadIdx.x) : make_double2(0.0, 0.0);  // coalesced
           r[4 * u + 0] = __double2loint(v.x);
           r[4 * u + 1] = __double2hiint(v.x);
@@ -1585,7 +1588,7 @@ __global__ void __launch_bounds__(TT, 1)
       tmem_wait_ld();
 #pragma unroll
       for (int u = 0; u < NS; ++u)
-        if (sp[u] >= 0) sm[pidx(sp[u])] = bval(32 + u, tm2(r, u));
+        if (!kRagged || sp[u] >= 0) sm[pidx(sp[u])] = bval(32 + u, tm2(r, u));
     }
     // (2) the fused item: product, real split, two radix-16 butterflies
     {
@@ -1891,16 +1894,17 @@ template <bool BREAL>
 static bool try_fused384(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                          const PairEntry* dwork, const int* winfo, double* out) {
   const PlanArgs& a = pl.a;
-  if (!(a.P == 4 && a.r[0] == 16 && a.r[1] == 8 && a.r[2] == 10 && a.r[3] == 10 && a.fused && a.tt == 384))
-    return false;
-  auto kern = pair_kernel_fused<16, 8, 10, 10, 384, BREAL>;
-  static bool attr = false;
-  if (!attr) {
+  if (!(a.P == 4 && a.r[0] == 16 && a.fused && a.tt == 384)) return false;
+  const bool p8 = a.r[1] == 8 && a.r[2] == 10 && a.r[3] == 10;
+  if (!p8 && !(a.r[1] == 10 && a.r[2] == 10 && a.r[3] == 8)) return false;
+  auto kern = p8 ? pair_kernel_fused<16, 8, 10, 10, 384, BREAL> : pair_kernel_fused<16, 10, 10, 8, 384, BREAL>;
+  static bool attr[2] = {false, false};
+  if (!attr[p8]) {
     cudaFuncAttributes fa{};
     TGB_CUDA(cudaFuncGetAttributes(&fa, kern));
     TGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
-    attr = true;
+    attr[p8] = true;
   }
   prof_begin(ctx);
   kern<<<ctx->num_sms, 384, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);

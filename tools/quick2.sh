@@ -1,6 +1,6 @@
 # pair-kernel A/B: parity of the conv path, then phase clocks + bench for each variant
 timeout 600 python -m pytest tests -x -q -m gpu -k "conv or golden or smoke" 2>&1 | tail -1
-for v in "" "TGB_TT384=1"; do
+for v in "" "TGB_TT384=1" "TGB_TT384=2"; do
   echo "== $v"
   env $v TGB_PHASE_CLK=1 timeout 120 python tools/prof_pair.py 2>&1 | grep "phase cycles" | tail -2 | head -1
   env $v timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/x.json 2> gpurun_out/x.err
