@@ -212,7 +212,7 @@ __global__ void chol_inv_kernel(int p, double* __restrict__ H, double* __restric
 // retired-column rule is the global-memory version's.
 constexpr int kCholSmem = 128;
 constexpr int kCholSmemBytes = 200 * 1024;  // L (+ L^{-1} when 2 p^2 doubles fit)
-__global__ void __launch_bounds__(256) chol_inv_smem_kernel(int p, double* __restrict__ H) {
+__global__ void __launch_bounds__(1024) chol_inv_smem_kernel(int p, double* __restrict__ H) {
   extern __shared__ double Ls[];  // p x p, column-major; then X = L^{-1} (p x p) when it fits
   __shared__ double s_mx;
   __shared__ unsigned char dead[kCholSmem];
@@ -556,7 +556,7 @@ void cholqr2(tgb_ctx* ctx, int64_t d, int p, double* X, Dev& tmp) {
       }
       const size_t l_bytes = static_cast<size_t>(p) * p * sizeof(double);
       const size_t bytes = 2 * l_bytes <= static_cast<size_t>(kCholSmemBytes) ? 2 * l_bytes : l_bytes;
-      chol_inv_smem_kernel<<<1, 256, bytes, ctx->stream>>>(p, H);
+      chol_inv_smem_kernel<<<1, p > 64 ? 1024 : 512, bytes, ctx->stream>>>(p, H);
     } else {
       chol_inv_kernel<<<1, 256, 0, ctx->stream>>>(p, H, Wk);
     }
