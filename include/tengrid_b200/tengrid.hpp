@@ -3,7 +3,9 @@
 //
 // A reference build switches to the B200 path by replacing the bodies of
 // tg::convolve / tg::hartree_potential / tg::scalar_product /
-// tg::coulomb_matrix / tg::conv_central_many with calls into this header
+// tg::coulomb_matrix / tg::conv_central_many / the HF operators
+// (overlap, kinetic, exchange, *_from_factors, generalized_eigensolve) with
+// calls into this header
 // (INTEGRATION.md).  It is templated on the matrix type so it works with
 // Eigen::MatrixXd / Eigen::VectorXd (column-major, data()/rows()/cols()/
 // size()) without including Eigen here.  Errors are rethrown as the
@@ -110,30 +112,100 @@ double scalar_product(const Cp& a, const Cp& b) {
   return r;
 }
 
+// The discretised basis (one canonical tensor per function, discretize_basis)
+// flattened into one tensor of all primitives + function offsets, the form
+// every basis-level tgb_* entry point takes (host copy, small).
+struct FlatBasis {
+  std::array<std::vector<double>, 3> f;
+  std::vector<double> w;
+  std::vector<int64_t> off;
+  tgb_cp cp{};
+  int64_t nb = 0;
+  template <class Cp>
+  explicit FlatBasis(const std::vector<Cp>& disc) : off(disc.size() + 1, 0), nb(static_cast<int64_t>(disc.size())) {
+    for (int64_t k = 0; k < nb; ++k) off[k + 1] = off[k] + static_cast<int64_t>(disc[k].weight.size());
+    for (const auto& d : disc) {
+      for (int ax = 0; ax < 3; ++ax)
+        f[ax].insert(f[ax].end(), d.factor[ax].data(), d.factor[ax].data() + d.factor[ax].size());
+      w.insert(w.end(), d.weight.data(), d.weight.data() + d.weight.size());
+    }
+    cp.rank = off[nb];
+    for (int ax = 0; ax < 3; ++ax) {
+      cp.n[ax] = disc.empty() ? 0 : static_cast<int64_t>(disc[0].factor[ax].rows());
+      cp.factor[ax] = f[ax].data();
+    }
+    cp.weight = w.data();
+  }
+};
+
 // tg::coulomb_matrix (hf.cpp:140-151): disc = discretize_basis(bs).
 template <class Cp, class Matrix>
 Matrix coulomb_matrix(const std::vector<Cp>& disc, const Cp& vh, const std::array<double, 3>& h) {
-  const int64_t nb = static_cast<int64_t>(disc.size());
-  std::vector<int64_t> off(nb + 1, 0);
-  for (int64_t k = 0; k < nb; ++k) off[k + 1] = off[k] + static_cast<int64_t>(disc[k].weight.size());
-  // flatten primitives into one canonical tensor (host copy, small)
-  std::array<std::vector<double>, 3> f;
-  std::vector<double> w;
-  for (const auto& d : disc) {
-    for (int ax = 0; ax < 3; ++ax) f[ax].insert(f[ax].end(), d.factor[ax].data(), d.factor[ax].data() + d.factor[ax].size());
-    w.insert(w.end(), d.weight.data(), d.weight.data() + d.weight.size());
-  }
-  tgb_cp flat{};
-  flat.rank = off[nb];
-  for (int ax = 0; ax < 3; ++ax) {
-    flat.n[ax] = disc.empty() ? 0 : static_cast<int64_t>(disc[0].factor[ax].rows());
-    flat.factor[ax] = f[ax].data();
-  }
-  flat.weight = w.data();
+  FlatBasis fb(disc);
   tgb_cp cv = view(vh);
-  Matrix J(nb, nb);
-  check(tgb_coulomb_matrix(context(), &flat, off.data(), nb, &cv, h.data(), J.data(), TGB_MEM_HOST));
+  Matrix J(fb.nb, fb.nb);
+  check(tgb_coulomb_matrix(context(), &fb.cp, fb.off.data(), fb.nb, &cv, h.data(), J.data(), TGB_MEM_HOST));
   return J;
+}
+
+// tg::overlap_matrix / tg::kinetic_matrix (hf.cpp:48-87).
+template <class Cp, class Matrix>
+Matrix overlap_matrix(const std::vector<Cp>& disc, const std::array<double, 3>& h) {
+  FlatBasis fb(disc);
+  Matrix S(fb.nb, fb.nb);
+  check(tgb_overlap_matrix(context(), &fb.cp, fb.off.data(), fb.nb, h.data(), S.data(), TGB_MEM_HOST));
+  return S;
+}
+template <class Cp, class Matrix>
+Matrix kinetic_matrix(const std::vector<Cp>& disc, const std::array<double, 3>& h, bool exact_mass = false) {
+  FlatBasis fb(disc);
+  Matrix T(fb.nb, fb.nb);
+  check(tgb_kinetic_matrix(context(), &fb.cp, fb.off.data(), fb.nb, h.data(), exact_mass ? 1 : 0, T.data(),
+                           TGB_MEM_HOST));
+  return T;
+}
+
+// tg::exchange_matrix (hf.cpp:153-170) with a primary-grid kernel tensor.
+template <class Cp, class Matrix>
+Matrix exchange_matrix(const std::vector<Cp>& disc, const Matrix& c_occ, const Cp& kernel,
+                       const std::array<double, 3>& h) {
+  FlatBasis fb(disc);
+  tgb_cp ck = view(kernel);
+  Matrix K(fb.nb, fb.nb);
+  check(tgb_exchange_matrix(context(), &fb.cp, fb.off.data(), fb.nb, c_occ.data(), c_occ.cols(), &ck, h.data(),
+                            K.data(), TGB_MEM_HOST));
+  return K;
+}
+
+// tg::coulomb_from_factors / exchange_from_factors / fock_from_factors (tei.cpp:215-238).
+template <class Matrix>
+Matrix coulomb_from_factors(const Matrix& chol, const Matrix& density) {
+  Matrix J(density.rows(), density.rows());
+  check(tgb_coulomb_from_factors(context(), density.rows(), chol.cols(), chol.data(), density.data(), J.data(),
+                                 TGB_MEM_HOST));
+  return J;
+}
+template <class Matrix>
+Matrix exchange_from_factors(const Matrix& chol, const Matrix& density) {
+  Matrix K(density.rows(), density.rows());
+  check(tgb_exchange_from_factors(context(), density.rows(), chol.cols(), chol.data(), density.data(), K.data(),
+                                  TGB_MEM_HOST));
+  return K;
+}
+template <class Matrix>
+Matrix fock_from_factors(const Matrix& h_core, const Matrix& chol, const Matrix& density) {
+  Matrix F(density.rows(), density.rows());
+  check(tgb_fock_from_factors(context(), density.rows(), chol.cols(), h_core.data(), chol.data(), density.data(),
+                              F.data(), TGB_MEM_HOST));
+  return F;
+}
+
+// tg::generalized_eigensolve (hf.cpp:187-199): F C = S C diag(e).
+template <class Matrix, class Vector>
+void generalized_eigensolve(const Matrix& f, const Matrix& s, Matrix& c, Vector& e) {
+  c = Matrix(f.rows(), f.rows());
+  e = Vector(f.rows());
+  check(tgb_generalized_eigensolve(context(), f.rows(), f.data(), s.data(), c.data(), e.data(), TGB_MEM_HOST));
 }
 
 }  // namespace tgb_cpp

@@ -10,7 +10,10 @@ import ctypes as C
 from pathlib import Path
 
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libtgb.so"
+import os
+
+# TGB_LIB: an alternative in-tree build of the same library (A/B experiments)
+LIB_PATH = _HERE / os.environ.get("TGB_LIB", "libtgb.so")
 
 
 class TengridError(Exception):

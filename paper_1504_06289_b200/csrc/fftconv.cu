@@ -49,6 +49,10 @@ namespace tgb {
 // ------------------------------------------------------------------ plan
 
 constexpr int kMaxPasses = 12;
+#ifndef TGB_MID_UNROLL
+#define TGB_MID_UNROLL 1  // middle-pass butterflies in flight per thread (2 measured: see profiles)
+#endif
+constexpr int kMidUnroll = TGB_MID_UNROLL;
 constexpr int kMaxThreads = 384;
 
 struct PlanArgs {
@@ -1140,7 +1144,7 @@ __device__ __forceinline__ void static_pass_t(double2* sm, const double2* lo, co
     wp[1] = w;
 #pragma unroll
     for (int q = 2; q < R; ++q) wp[q] = (q & 1) ? cmul(wp[q - 1], w) : cmul(wp[q >> 1], wp[q >> 1]);
-#pragma unroll 1
+#pragma unroll kMidUnroll
     for (int G = threadIdx.x / L; G < NBF / L; G += TT / L) {
       const int base = G * (L * R) + j;
       double2 v[R];

@@ -54,6 +54,34 @@ int main() {
     ++fails;
   } catch (const std::invalid_argument&) {
   }
+  // fock_from_factors (tei.cpp:215-238) against the defining loops
+  {
+    const long nb = 5, R = 3;
+    Eigen::MatrixXd L(nb * nb, R), D(nb, nb), H(nb, nb);
+    for (long i = 0; i < L.size(); ++i) L(i) = std::sin(0.37 * i + 0.1);
+    for (long i = 0; i < nb; ++i)
+      for (long j = 0; j < nb; ++j) {
+        D(i, j) = std::cos(0.5 * (i + j)) + (i == j ? 2.0 : 0.0);
+        H(i, j) = 0.1 * (i + 1) * (j + 1);
+      }
+    Eigen::MatrixXd F = tgb_cpp::fock_from_factors(H, L, D);
+    double ferr = 0.0;
+    for (long mu = 0; mu < nb; ++mu)
+      for (long nu = 0; nu < nb; ++nu) {
+        double j = 0.0, k = 0.0;
+        for (long s = 0; s < R; ++s)
+          for (long a = 0; a < nb; ++a)
+            for (long b = 0; b < nb; ++b) {
+              j += 0.5 * (L(mu + nb * nu, s) + L(nu + nb * mu, s)) * L(a + nb * b, s) * D(a, b);
+              k -= 0.25 * (L(mu + nb * a, s) * D(a, b) * L(nu + nb * b, s) + L(nu + nb * a, s) * D(a, b) * L(mu + nb * b, s));
+            }
+        ferr = std::max(ferr, std::abs(F(mu, nu) - (H(mu, nu) + j + k)));
+      }
+    if (ferr > 1e-12) { std::printf("fock_from_factors failed: %g\n", ferr); ++fails; }
+    for (long i = 0; i < nb; ++i)
+      for (long j = 0; j < nb; ++j)
+        if (F(i, j) != F(j, i)) { std::printf("fock not exactly symmetric\n"); ++fails; i = nb; break; }
+  }
   std::printf("cpp api: %d failures\n", fails);
   return fails;
 }
