@@ -288,6 +288,26 @@ int tgb_tucker_get(tgb_tucker* t, double* core, double* side0, double* side1, do
 int tgb_tucker_sigma(tgb_tucker* t, int axis, int64_t* count, double* sigma);
 int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem);
 
+/* replaces tg::thin_svd_left (reduction.hpp:67, reduction.cpp:85-138):
+ * left singular pairs of a rows x cols matrix A (column-major, space `mem`),
+ * sigma descending.  U needs rows x min(rows, cols), sigma min(rows, cols)
+ * entries; *kept = the pairs returned under the reference's branch rule
+ * (all min(rows, cols) except the tall Gram branch, which keeps sigma^2 >
+ * sigma_0^2 1e-24).  Device solver: min(rows, cols) <= 128.  Singular-vector
+ * signs are not fixed (as in the reference). */
+int tgb_thin_svd_left(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* U, double* sigma,
+                      int64_t* kept, int mem);
+
+/* replaces tg::pivoted_cholesky (tei.hpp:27-30, tei.cpp:48-90) for an explicit
+ * PSD matrix A (n x n; the reference's column callback reads A's columns and
+ * its diagonal argument is diag(A)).  stop: 0 max-diagonal, 1 trace.  L needs
+ * n x min(n, max_rank) doubles (space `mem`), pivots min(n, max_rank) entries
+ * (HOST); *rank, *residual (the stop measure ratio), *clamped_negative on the
+ * host.  NUMERICAL_ERROR when a diagonal goes below -neg_tol * max0. */
+int tgb_pivoted_cholesky(tgb_ctx* ctx, int64_t n, const double* A, double tol, int stop, int64_t max_rank,
+                         double neg_tol, double* L, int64_t* pivots, int64_t* rank, double* residual,
+                         int* clamped_negative, int mem);
+
 /* ---- dense FP64 building block -------------------------------------------
  * C = alpha op(A) op(B) + beta C on the FP64 tensor cores (DMMA), column-major
  * DEVICE pointers, stream-ordered on the context stream.  The dense products

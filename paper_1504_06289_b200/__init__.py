@@ -12,7 +12,7 @@ from .tengrid import (AssembledPotential, BasisSet, CanonicalTensor3, Context, D
                       LatticeBlock, lattice_grid, resolve_blocks, lattice_nodes, lattice_sum_tucker,
                       lattice_sum_composite)
 
-from .tei import (TEIFactorization, build_tei, tei_cholesky, tei_column, tei_convolution_matrices,
+from .tei import (PivotedCholesky, pivoted_cholesky, TEIFactorization, build_tei, tei_cholesky, tei_column, tei_convolution_matrices,
                   tei_density_fitting, tei_diagonal, tei_matrix_entry)
 
 from .hf import (Molecule, Nucleus, SCFConfig, SCFState, generalized_eigensolve, scf_solve, MOSpace, MOCholesky,
@@ -20,6 +20,7 @@ from .hf import (Molecule, Nucleus, SCFConfig, SCFState, generalized_eigensolve,
                  fock_from_factors, kinetic_matrix, nuclear_matrix, nuclear_potential_tensor, overlap_matrix,
                  window_for_center)
 
-from .reduction import ReductionConfig, TuckerResult, TuckerTensor3, canonical_to_tucker, reduce_rank, rhosvd
+from .reduction import (ReductionConfig, TuckerResult, TuckerTensor3, canonical_to_tucker, reduce_rank, rhosvd,
+                        thin_svd_left)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

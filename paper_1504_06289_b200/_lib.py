@@ -120,6 +120,8 @@ def lib() -> C.CDLL:
             "tgb_density_rank": (I, [P, I64, P, I64, C.POINTER(I64)]),
             "tgb_density_build": (I, [P, C.POINTER(tgb_cp), P, I64, P, I64, C.POINTER(tgb_cp), I]),
             "tgb_density_reduce": (I, [P, C.POINTER(tgb_cp), P, I64, P, I64, D, I, C.POINTER(P)]),
+            "tgb_thin_svd_left": (I, [P, I64, I64, P, P, P, C.POINTER(I64), I]),
+            "tgb_pivoted_cholesky": (I, [P, I64, P, D, I, I64, D, P, P, C.POINTER(I64), C.POINTER(D), C.POINTER(I), I]),
             "tgb_overlap_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, P, I]),
             "tgb_kinetic_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, I, P, I]),
             "tgb_tei_create": (I, [C.POINTER(P)]),

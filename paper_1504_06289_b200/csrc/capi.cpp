@@ -4,6 +4,7 @@
 // per-axis copy/compute overlap.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -659,6 +660,68 @@ int tgb_density_reduce(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offs
       throw;
     }
     cleanup();
+  });
+}
+
+int tgb_thin_svd_left(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* U, double* sigma,
+                      int64_t* kept, int mem) {
+  return guarded([&] {
+    tgb::require(rows >= 0 && cols >= 0 && kept, "thin_svd_left: bad shape");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    const int64_t p = std::min(rows, cols);
+    *kept = 0;
+    if (p == 0) return;
+    tgb::DevStreamScope scope(ctx);
+    if (mem == TGB_MEM_DEVICE) {
+      *kept = tgb::thin_svd_left_dev(ctx, rows, cols, A, U, sigma);
+      return;
+    }
+    size_t got = 0;
+    auto* d = static_cast<double*>(tgb::scratch_alloc(ctx, (rows * cols + rows * p + p) * sizeof(double), &got));
+    try {
+      tgb::h2d(ctx, d, A, rows * cols * sizeof(double), ctx->stream);
+      *kept = tgb::thin_svd_left_dev(ctx, rows, cols, d, d + rows * cols, d + rows * cols + rows * p);
+      TGB_CUDA(cudaMemcpy(U, d + rows * cols, rows * *kept * sizeof(double), cudaMemcpyDeviceToHost));
+      TGB_CUDA(cudaMemcpy(sigma, d + rows * cols + rows * p, *kept * sizeof(double), cudaMemcpyDeviceToHost));
+    } catch (...) {
+      tgb::scratch_free(ctx, d, got);
+      throw;
+    }
+    tgb::scratch_free(ctx, d, got);
+  });
+}
+
+int tgb_pivoted_cholesky(tgb_ctx* ctx, int64_t n, const double* A, double tol, int stop, int64_t max_rank,
+                         double neg_tol, double* L, int64_t* pivots, int64_t* rank, double* residual,
+                         int* clamped_negative, int mem) {
+  return guarded([&] {
+    tgb::require(n >= 0 && max_rank >= 0 && rank && residual && clamped_negative, "pivoted_cholesky: bad arguments");
+    tgb::require(stop == 0 || stop == 1, "pivoted_cholesky: unknown stop rule");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    *rank = 0;
+    *residual = 0.0;
+    *clamped_negative = 0;
+    if (n == 0) return;
+    const int64_t cap = std::min(n, max_rank);
+    bool cl = false;
+    if (mem == TGB_MEM_DEVICE) {
+      *rank = tgb::pivoted_cholesky_dev(ctx, n, A, tol, stop == 1, max_rank, neg_tol, L, pivots, residual, &cl);
+      *clamped_negative = cl;
+      return;
+    }
+    size_t got = 0;
+    auto* d = static_cast<double*>(tgb::scratch_alloc(ctx, (n * n + n * std::max<int64_t>(cap, 1)) * sizeof(double),
+                                                      &got));
+    try {
+      tgb::h2d(ctx, d, A, n * n * sizeof(double), ctx->stream);
+      *rank = tgb::pivoted_cholesky_dev(ctx, n, d, tol, stop == 1, max_rank, neg_tol, d + n * n, pivots, residual, &cl);
+      if (*rank) TGB_CUDA(cudaMemcpy(L, d + n * n, n * *rank * sizeof(double), cudaMemcpyDeviceToHost));
+      *clamped_negative = cl;
+    } catch (...) {
+      tgb::scratch_free(ctx, d, got);
+      throw;
+    }
+    tgb::scratch_free(ctx, d, got);
   });
 }
 

@@ -284,6 +284,117 @@ __global__ void __launch_bounds__(1024) chol_inv_smem_kernel(int p, double* __re
   }
 }
 
+// One-sided (Hestenes) Jacobi SVD of an m x p matrix X held in global memory
+// (L2-resident for the sizes thin_svd_left sends here), one CTA: X <- X V with
+// orthogonal columns; V (p x p, optional) accumulates the rotations.  The
+// rotation formula, the tournament ordering and the stopping test are those
+// of jacobi_svd_kernel; accurate singular values down to ~eps sigma_max
+// (no Gram squaring), as the reference's JacobiSVD.  Epilogue: sg = column
+// norms sorted descending (stable), perm[c] = source column of rank c.
+__global__ void __launch_bounds__(1024) jacobi_onesided_kernel(int64_t m, int p, double* __restrict__ X,
+                                                                double* __restrict__ V, double* __restrict__ sg,
+                                                                int* __restrict__ perm) {
+  __shared__ int rot_any;
+  __shared__ double nr_sh[129];  // p <= 128 (kJacMax)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int pe = p + (p & 1), half = pe / 2;
+  const double tol = fmax(1e-16, p * 1.1102230246251565e-16);
+  const double tol2 = tol * tol;
+  if (V)
+    for (int i = threadIdx.x; i < p * p; i += blockDim.x) V[i] = (i % p == i / p) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) rot_any = 0;
+    __syncthreads();
+    int any = 0;
+    for (int round = 0; round < pe - 1; ++round) {
+      for (int q = warp; q < half; q += nw) {
+        int a = (q == 0) ? pe - 1 : (round + q) % (pe - 1);
+        int b = (round + pe - 1 - q) % (pe - 1);
+        if (q == 0) b = round % (pe - 1);
+        const int i = min(a, b), j = max(a, b);
+        if (j >= p) continue;  // the padding column of odd p
+        double* ci = X + m * i;
+        double* cj = X + m * j;
+        double al = 0, be = 0, ga = 0;
+        for (int64_t r = lane; r < m; r += 32) {
+          const double x = ci[r], y = cj[r];
+          al += x * x;
+          be += y * y;
+          ga += x * y;
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        }
+        if (ga == 0.0 || ga * ga <= tol2 * (al * be)) continue;
+        any = 1;
+        const double zeta = (be - al) / (2.0 * ga);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = rsqrt(1.0 + t * t), sn = c * t;
+        for (int64_t r = lane; r < m; r += 32) {
+          const double x = ci[r], y = cj[r];
+          ci[r] = c * x - sn * y;
+          cj[r] = sn * x + c * y;
+        }
+        if (V) {
+          double* vi = V + static_cast<int64_t>(p) * i;
+          double* vj = V + static_cast<int64_t>(p) * j;
+          for (int r = lane; r < p; r += 32) {
+            const double x = vi[r], y = vj[r];
+            vi[r] = c * x - sn * y;
+            vj[r] = sn * x + c * y;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (any && lane == 0) rot_any = 1;
+    __syncthreads();
+    if (!rot_any) break;
+    __syncthreads();
+  }
+  for (int j = warp; j < p; j += nw) {
+    double ss = 0;
+    for (int64_t r = lane; r < m; r += 32) ss += X[r + m * j] * X[r + m * j];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if (lane == 0) nr_sh[j] = sqrt(ss);
+  }
+  __syncthreads();
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    int rk = 0;
+    for (int k = 0; k < p; ++k) rk += (nr_sh[k] > nr_sh[j]) || (nr_sh[k] == nr_sh[j] && k < j);
+    perm[rk] = j;
+    sg[rk] = nr_sh[j];
+  }
+}
+
+// U(:, c) = X(:, perm[c]) / sg[c] (left vectors of a tall matrix), or
+// U(:, c) = V(:, perm[c]) (left vectors of a wide one, from A^T's rotations)
+__global__ void jacobi_gather_kernel(int64_t m, int p, const double* __restrict__ src, const int* __restrict__ perm,
+                                     const double* __restrict__ sg, int normalize, double* __restrict__ U) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= m * p) return;
+  const int64_t r = idx % m;
+  const int c = static_cast<int>(idx / m);
+  const double v = src[r + m * perm[c]];
+  U[idx] = normalize ? (sg[c] > 0.0 ? v / sg[c] : 0.0) : v;
+}
+
+__global__ void sqrt_kernel(int64_t n, double* __restrict__ x) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i < n) x[i] = sqrt(fmax(0.0, x[i]));
+}
+
+__global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ a, double* __restrict__ t) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= rows * cols) return;
+  t[idx / rows + cols * (idx % rows)] = a[idx];  // t (cols x rows) = a^T
+}
+
 __global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
   const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
   if (i < n) x[i] = v;
@@ -583,6 +694,68 @@ void random_block(tgb_ctx* ctx, int64_t d, int p, double* X, uint64_t seed) {
 }
 
 }  // namespace
+
+// thin_svd_left (reduction.cpp:85-138) for min(rows, cols) <= 128 on the
+// device: Cholesky-QR2 of the taller side, then the one-CTA Jacobi SVD of the
+// small triangular-shaped factor (tall: A = Q R, SVD(R); wide: A^T = Q R, so
+// A = R^T Q^T and SVD(A Q)).  The reference's branch picks only the OUTPUT
+// shape here: the wide Gram branch (cols >= 4 rows, cols > 8192) and the
+// Jacobi branch return min(rows, cols) pairs; the tall Gram branch (rows >=
+// 4 cols, cols >= 8) keeps the leading pairs with sigma^2 > sigma_0^2 1e-24.
+// U (rows x min) and sigma (min) are device outputs; returns the kept count.
+void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg);
+static void dgemm_transpose(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* a, double* t) {
+  const int64_t tot = rows * cols;
+  transpose_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(rows, cols, a, t);
+  TGB_LAUNCHED(ctx);
+}
+int64_t thin_svd_left_dev(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* U, double* sigma) {
+  const int64_t p = std::min(rows, cols);
+  if (p == 0) return 0;
+  if (p > kJacMax) throw Error(TGB_INVALID_ARGUMENT, "thin_svd_left: min(rows, cols) above the device solver's 128");
+  DevStreamScope scope(ctx);
+  const bool gram_wide = cols >= 4 * rows && cols > 8192;               // reduction.cpp:93-104
+  const bool jacobi_branch = !gram_wide && (rows < 4 * cols || cols < 8);  // reduction.cpp:105-108
+  Dev perm_d(static_cast<size_t>(p)), V(static_cast<size_t>(p) * p);
+  int* perm = reinterpret_cast<int*>(perm_d.p);
+  const unsigned gb = static_cast<unsigned>((rows * p + 255) / 256);
+  if (rows >= cols) {  // tall: one-sided Jacobi on A itself, U = normalised rotated columns
+    Dev X(static_cast<size_t>(rows) * cols);
+    TGB_CUDA(cudaMemcpyAsync(X.p, A, static_cast<size_t>(rows) * cols * sizeof(double), cudaMemcpyDeviceToDevice,
+                             ctx->stream));
+    jacobi_onesided_kernel<<<1, 1024, 0, ctx->stream>>>(rows, static_cast<int>(p), X.p, nullptr, sigma, perm);
+    TGB_LAUNCHED(ctx);
+    jacobi_gather_kernel<<<gb, 256, 0, ctx->stream>>>(rows, static_cast<int>(p), X.p, perm, sigma, 1, U);
+    TGB_LAUNCHED(ctx);
+  } else if (gram_wide) {  // the reference's Gram branch: eigenpairs of A A^T (rows x rows)
+    Dev G(static_cast<size_t>(rows) * rows);
+    dgemm(ctx, false, true, rows, rows, cols, 1.0, A, rows, A, rows, 0.0, G.p, rows);
+    jacobi_onesided_kernel<<<1, 1024, 0, ctx->stream>>>(rows, static_cast<int>(p), G.p, nullptr, sigma, perm);
+    TGB_LAUNCHED(ctx);
+    jacobi_gather_kernel<<<gb, 256, 0, ctx->stream>>>(rows, static_cast<int>(p), G.p, perm, sigma, 1, U);
+    TGB_LAUNCHED(ctx);
+    sqrt_kernel<<<static_cast<unsigned>((p + 255) / 256), 256, 0, ctx->stream>>>(p, sigma);  // sigma = sqrt(lambda)
+    TGB_LAUNCHED(ctx);
+  } else {  // wide: Jacobi on A^T with the rotations accumulated; U = V
+    Dev X(static_cast<size_t>(rows) * cols);
+    dgemm_transpose(ctx, rows, cols, A, X.p);
+    jacobi_onesided_kernel<<<1, 1024, 0, ctx->stream>>>(cols, static_cast<int>(p), X.p, V.p, sigma, perm);
+    TGB_LAUNCHED(ctx);
+    jacobi_gather_kernel<<<gb, 256, 0, ctx->stream>>>(rows, static_cast<int>(p), V.p, perm, sigma, 0, U);
+    TGB_LAUNCHED(ctx);
+  }
+  int64_t kept = p;
+  if (!gram_wide && !jacobi_branch) {  // tall Gram branch: drop lambda <= lambda_max 1e-24 (reduction.cpp:119-122)
+    std::vector<double> hs(p);
+    TGB_CUDA(cudaMemcpyAsync(hs.data(), sigma, p * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    const double lmax = hs[0] * hs[0];
+    kept = 0;
+    while (kept < p && hs[kept] * hs[kept] > lmax * 1e-24 && hs[kept] > 0.0) ++kept;
+  }
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return kept;
+}
 
 // One-CTA one-sided Jacobi SVD of a p x p device matrix (p <= 128): U
 // replaces S in place (columns sorted by descending singular value), sg gets

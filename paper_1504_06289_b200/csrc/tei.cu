@@ -1012,6 +1012,35 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
     TGB_CUDA(cudaMemcpy(f.chol_piv.data(), piv, hs.rank * sizeof(int64_t), cudaMemcpyDeviceToHost));
 }
 
+// tg::pivoted_cholesky (tei.cpp:48-90) of an explicit PSD matrix on the device
+// (the column callback of the reference reads columns of A).  Returns rank;
+// L (n x min(n, max_rank)) and pivots device-side / host-side as documented
+// in tgb.h.
+int64_t pivoted_cholesky_dev(tgb_ctx* ctx, int64_t n, const double* A, double tol, bool trace_stop,
+                             int64_t max_rank, double neg_tol, double* L, int64_t* pivots_host, double* residual,
+                             bool* clamped) {
+  const int64_t cap = std::min(n, max_rank);
+  static thread_local DevBuf wbuf;
+  auto* w = static_cast<double*>(wbuf.get((n + 64 + std::max<int64_t>(cap, 1)) * sizeof(double)));
+  double* dg = w;
+  int* piv = reinterpret_cast<int*>(w + n + 8);
+  int* info = reinterpret_cast<int*>(w + n);
+  double* res = w + n + 4;
+  pivchol_explicit_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(n), A, tol, trace_stop ? 1 : 0,
+                                                              static_cast<int>(cap), neg_tol, dg, L, piv, info, res);
+  TGB_LAUNCHED(ctx);
+  int hinfo[3];
+  TGB_CUDA(cudaMemcpyAsync(hinfo, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaMemcpyAsync(residual, res, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hinfo[2]) throw Error(TGB_NUMERICAL_ERROR, "pivoted_cholesky: negative diagonal beyond tolerance; matrix not PSD");
+  std::vector<int> hp(std::max(hinfo[0], 1));
+  if (hinfo[0]) TGB_CUDA(cudaMemcpy(hp.data(), piv, hinfo[0] * sizeof(int), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < hinfo[0]; ++i) pivots_host[i] = hp[i];
+  *clamped = hinfo[1] != 0;
+  return hinfo[0];
+}
+
 }  // namespace tgb
 
 // ---------------------------------------------------------------- C-ABI

@@ -163,6 +163,11 @@ void sep_inner_tiles(tgb_ctx* ctx, const int64_t n[3], const double* const F[3],
                      const double* wb, int RB, const int* i0, const int* i1, int P, double* partial, double* out);
 // reduction.cu
 void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg);
+int64_t thin_svd_left_dev(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* U, double* sigma);
+// tei.cu
+int64_t pivoted_cholesky_dev(tgb_ctx* ctx, int64_t n, const double* A, double tol, bool trace_stop,
+                             int64_t max_rank, double neg_tol, double* L, int64_t* pivots_host, double* residual,
+                             bool* clamped);
 // mp2.cu
 void mo_transform_dev(tgb_ctx* ctx, int64_t nb, int64_t R, const double* chol, int64_t n_occ, const double* C,
                       double* out);

@@ -127,3 +127,21 @@ def reduce_rank(a: CanonicalTensor3, cfg: ReductionConfig, ctx: Context | None =
     """reduction.cpp:271-273 — canonical_to_tucker then tucker_to_canonical."""
     res = canonical_to_tucker(a, cfg, ctx)
     return _t2c(res, a.extents())
+
+
+def thin_svd_left(a, ctx: Context | None = None):
+    """reduction.cpp:85-138 — (u, sigma): left singular pairs, sigma descending, with the
+    reference's output shape per branch (device solver: min(rows, cols) <= 128)."""
+    ctx = ctx or default_context()
+    A = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if A.ndim != 2:
+        raise InvalidArgument("thin_svd_left: matrix expected")
+    r, c = A.shape
+    p = min(r, c)
+    u = np.zeros((r, p), order="F")
+    s = np.zeros(p)
+    kept = C.c_int64()
+    check(lib().tgb_thin_svd_left(ctx.handle, r, c, A.ctypes.data if A.size else None, u.ctypes.data if u.size else None,
+                                  s.ctypes.data if s.size else None, C.byref(kept), MEM_HOST))
+    k = kept.value
+    return np.asfortranarray(u[:, :k]), s[:k].copy()

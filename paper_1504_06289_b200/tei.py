@@ -140,3 +140,31 @@ def build_tei(bs, disc: list, kernel, eps_fit: float, eps_chol: float, ctx: Cont
     tei_convolution_matrices(fac, kernel)
     tei_cholesky(fac, eps_chol)
     return fac
+
+
+class PivotedCholesky:
+    """tei.hpp:12-17."""
+
+    def __init__(self, factor, pivots, residual, clamped_negative):
+        self.factor, self.pivots, self.residual, self.clamped_negative = factor, pivots, residual, clamped_negative
+
+
+def pivoted_cholesky(a, tol: float, stop: str = "max_diagonal", max_rank: int | None = None,
+                     negative_tol: float = 1e-12, ctx: Context | None = None) -> PivotedCholesky:
+    """tei.cpp:48-90 on an explicit PSD matrix (the reference's column callback reads its columns);
+    stop "max_diagonal" or "trace" (CholeskyStop, tei.hpp:19-22)."""
+    ctx = ctx or default_context()
+    A = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    n = A.shape[0]
+    if A.shape != (n, n):
+        raise InvalidArgument("pivoted_cholesky: square matrix expected")
+    max_rank = n if max_rank is None else max_rank
+    cap = min(n, max_rank)
+    L = np.zeros((n, max(cap, 1)), order="F")
+    piv = np.zeros(max(cap, 1), dtype=np.int64)
+    rank, res, cl = C.c_int64(), C.c_double(), C.c_int()
+    check(lib().tgb_pivoted_cholesky(ctx.handle, n, A.ctypes.data if A.size else None, tol,
+                                     {"max_diagonal": 0, "trace": 1}[stop], max_rank, negative_tol, L.ctypes.data,
+                                     piv.ctypes.data, C.byref(rank), C.byref(res), C.byref(cl), MEM_HOST))
+    k = rank.value
+    return PivotedCholesky(np.asfortranarray(L[:, :k]), piv[:k].copy(), res.value, bool(cl.value))
