@@ -196,3 +196,24 @@ def test_density_tensor_device_build(g, case, ctx):
     assert np.linalg.norm(red.to_dense() - ref.to_dense()) <= 0.5 * eps * scale
     with pytest.raises(tg.InvalidArgument):
         tg.density_tensor(disc, g["c_occ"][:-1], eps, ctx)
+
+
+def test_reduce_rank_config1_structure_vs_reference_binary(g, ctx):
+    """Config-1 structure at n = 129 (40 s/p functions, 8 orbitals -> Theta rank 12,800: the wide Gram
+    branch of thin_svd_left and the Jacobi ALS branch): Tucker and canonical ranks identical to the
+    reference's own reduce_rank; reduced values within eps of Theta and of the reference's."""
+    from paper_1504_06289_b200.inputs import basis_case
+
+    bs, _ = basis_case(1, n=int(g["cfg1s_n"][0]))
+    disc = tg.discretize_basis(bs)
+    c = g["cfg1s_c_occ"]
+    theta = tg.density_tensor(disc, c, 0.0, ctx)
+    res = tg.canonical_to_tucker(theta, tg.ReductionConfig.tolerance(1e-6), ctx)
+    assert tuple(res.tucker.ranks()) == tuple(int(x) for x in g["cfg1s_tucker_ranks"])
+    red = tg.density_tensor(disc, c, 1e-6, ctx)
+    assert red.rank() == int(g["cfg1s_canonical_rank"][0])
+    vals = tg.value_at_points(red, g["cfg1s_pts"], ctx)
+    rms = lambda x: float(np.sqrt(np.mean(np.square(x))))  # noqa: E731
+    scale = rms(g["cfg1s_theta_vals"])
+    assert rms(vals - g["cfg1s_theta_vals"]) <= 2e-6 * scale
+    assert rms(vals - g["cfg1s_red_vals"]) <= 4e-6 * scale

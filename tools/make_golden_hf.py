@@ -116,6 +116,30 @@ def main():
         out[f"theta_f{ax}"] = f
     out["theta_w"] = theta.weight()
 
+    # config-1 structure at n = 129: 40 s/p functions, 8 orbitals -> Theta rank 12,800 (the wide Gram
+    # branch of thin_svd_left and Jacobi ALS), reduced by the reference's own reduce_rank at 1e-6
+    from paper_1504_06289_b200.inputs import basis_case, occupied_coefficients
+
+    bs1, rng1 = basis_case(1, n=129)
+    c1 = occupied_coefficients(rng1, len(bs1.functions), 8)
+    fns1 = [(f.center, f.degree, [(q.exponent, q.coeff) for q in f.primitives]) for f in bs1.functions]
+    R1 = O.Ref(bs1.grid.b_half, bs1.grid.n, fns1)
+    th1 = R1.density_tensor(c1, 0.0)
+    info1, _ = O.ref_reduce(th1, eps=1e-6, mode=1)
+    info2, red1 = O.ref_reduce(th1, eps=1e-6, mode=2)
+    pts = np.ascontiguousarray(Rng(99).integers(3 * 2000, 129).reshape(2000, 3))
+    out["cfg1s_n"] = np.array([129])
+    out["cfg1s_c_occ"] = c1
+    out["cfg1s_tucker_ranks"] = np.array(info1["ranks"])
+    out["cfg1s_canonical_rank"] = np.array([info2["canonical_rank"]])
+    out["cfg1s_pts"] = pts
+    def ref_values(t):
+        vals = np.zeros(len(pts))
+        assert R1.R.ref_value_at(t.h, C.c_longlong(len(pts)), O._p(pts), O._p(vals)) == 0
+        return vals
+
+    out["cfg1s_theta_vals"] = ref_values(th1)
+    out["cfg1s_red_vals"] = ref_values(red1)
     path = ROOT / "tests" / "golden" / "reference_hf.npz"
     np.savez_compressed(path, **out)
     print(f"wrote {path} ({len(out)} arrays)")
