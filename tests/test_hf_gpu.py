@@ -217,3 +217,28 @@ def test_reduce_rank_config1_structure_vs_reference_binary(g, ctx):
     scale = rms(g["cfg1s_theta_vals"])
     assert rms(vals - g["cfg1s_theta_vals"]) <= 2e-6 * scale
     assert rms(vals - g["cfg1s_red_vals"]) <= 4e-6 * scale
+
+
+def test_tei_config3_structure_vs_reference_binary(g, ctx):
+    """build_tei at config-3 structure (24 s/p functions from config 3's distributions, n = 129,
+    R_N = 41, eps_fit = eps_chol = 1e-6) against the reference's own tei.cpp: fit ranks and R_B
+    identical, L L^T at 1e-10."""
+    from paper_1504_06289_b200.inputs import KERNEL_C0, KERNEL_M
+
+    grid = tg.make_grid(15.0, 129)
+    fns, off = [], 0
+    for i, npr in enumerate(g["tei3s_nprim"]):
+        c = tuple(g["tei3s_centers"][3 * i:3 * i + 3])
+        d = tuple(int(x) for x in g["tei3s_degs"][3 * i:3 * i + 3])
+        prims = [tg.GaussianPrimitive(float(g["tei3s_exps"][off + p]), float(g["tei3s_coefs"][off + p]))
+                 for p in range(npr)]
+        off += int(npr)
+        fns.append(tg.SeparableBasisFunction(c, d, prims))
+    bs = tg.BasisSet(grid, fns)
+    kern = tg.kernel_tensor(grid, tg.make_expsum(KERNEL_M[3], KERNEL_C0[3]), False)
+    fac = tg.build_tei(bs, tg.discretize_basis(bs), kern, 1e-6, 1e-6, ctx)
+    assert fac.fit_ranks() == tuple(int(x) for x in g["tei3s_fit_ranks"])
+    assert fac.rank_b() == int(g["tei3s_rank_b"][0])
+    assert fac.fit_clamped_negative == bool(g["tei3s_clamped"][0])
+    L, oL = fac.chol, g["tei3s_chol"]
+    assert relmax(L @ L.T, oL @ oL.T) <= TOL

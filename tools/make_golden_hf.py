@@ -140,6 +140,24 @@ def main():
 
     out["cfg1s_theta_vals"] = ref_values(th1)
     out["cfg1s_red_vals"] = ref_values(red1)
+    # config-3 structure at n = 129: 3 centres x (2 s + 2 p shells) = 24 functions, exponents
+    # log-uniform in [0.1, 80], box 15, R_N = 41: the reference's own build_tei at 1e-6 / 1e-6
+    from paper_1504_06289_b200.inputs import KERNEL_C0, KERNEL_M, SEED_BASE
+
+    rng3 = Rng(SEED_BASE + 3)
+    cent3 = rng3.uniform(9, -5.0, 5.0).reshape(3, 3)
+    fns3 = []
+    for ci in range(3):
+        for sh in ("s", "s", "p", "p"):
+            alpha = float(rng3.loguniform(1, 0.1, 80.0)[0])
+            for d in ([(0, 0, 0)] if sh == "s" else [(1, 0, 0), (0, 1, 0), (0, 0, 1)]):
+                fns3.append((tuple(cent3[ci]), d, [(alpha, 1.0)]))
+    R3 = O.Ref([15.0] * 3, [129] * 3, fns3)
+    r3, rb3, cl3, res3, L3, _ = R3.build_tei(KERNEL_M[3], KERNEL_C0[3], 1e-6, 1e-6)
+    c3, d3, np3, e3, cf3 = O._basis_args(fns3)
+    out.update(tei3s_centers=c3, tei3s_degs=d3, tei3s_nprim=np3, tei3s_exps=e3, tei3s_coefs=cf3,
+               tei3s_fit_ranks=np.array(r3), tei3s_rank_b=np.array([rb3]), tei3s_chol=L3,
+               tei3s_clamped=np.array([int(cl3)]))
     path = ROOT / "tests" / "golden" / "reference_hf.npz"
     np.savez_compressed(path, **out)
     print(f"wrote {path} ({len(out)} arrays)")
