@@ -108,11 +108,10 @@ __global__ void square_kernel(int64_t count, double* __restrict__ x) {
 // Pivoted Cholesky of an explicit SPD n x n matrix A (tei.cpp:48-90), single
 // CTA.  info[0] = rank, info[1] = clamped_negative, info[2] = error (1 = not
 // PSD beyond tolerance); pivots[rank]; residual[0] = stop measure ratio.
-__global__ void __launch_bounds__(kRedThreads) pivchol_explicit_kernel(int n, const double* __restrict__ A,
-                                                                       double tol, int trace_stop, int cap,
-                                                                       double neg_tol, double* __restrict__ diag,
-                                                                       double* __restrict__ L, int* pivots, int* info,
-                                                                       double* residual) {
+__device__ __forceinline__ void pivchol_explicit_body(int n, const double* __restrict__ A, double tol, int trace_stop,
+                                                      int cap, double neg_tol, double* __restrict__ diag,
+                                                      double* __restrict__ L, int* pivots, int* info,
+                                                      double* residual) {
   __shared__ double sv[32];
   __shared__ int si[32];
   __shared__ double s_dmax;
@@ -191,6 +190,30 @@ __global__ void __launch_bounds__(kRedThreads) pivchol_explicit_kernel(int n, co
     info[2] = err;
     residual[0] = max0 > 0.0 ? (trace_stop ? fs : dm) / (trace_stop ? trace0 : max0) : 0.0;
   }
+}
+
+__global__ void __launch_bounds__(kRedThreads) pivchol_explicit_kernel(int n, const double* __restrict__ A,
+                                                                       double tol, int trace_stop, int cap,
+                                                                       double neg_tol, double* __restrict__ diag,
+                                                                       double* __restrict__ L, int* pivots, int* info,
+                                                                       double* residual) {
+  pivchol_explicit_body(n, A, tol, trace_stop, cap, neg_tol, diag, L, pivots, info, residual);
+}
+
+// the three axes' factorisations of the density fit are independent: one CTA each
+struct PivAxis {
+  int n, cap;
+  const double* A;
+  double *diag, *L, *residual;
+  int *pivots, *info;
+};
+struct PivBatch {
+  PivAxis ax[3];
+};
+__global__ void __launch_bounds__(kRedThreads) pivchol_explicit3_kernel(PivBatch b, double tol, int trace_stop,
+                                                                        double neg_tol) {
+  const PivAxis& a = b.ax[blockIdx.x];
+  pivchol_explicit_body(a.n, a.A, tol, trace_stop, a.cap, neg_tol, a.diag, a.L, a.pivots, a.info, a.residual);
 }
 
 // partial sums of (G - T)^2 and G^2 (fit residual, tei.cpp:140-141)
@@ -592,52 +615,62 @@ void tei_fit(tgb_ctx* ctx, TEI& f, const tgb_cp& basis_dev, const int64_t* fn_of
   f.pw.resize(f.np);
   if (f.np) TGB_CUDA(cudaMemcpy(f.pw.data(), basis_dev.weight, f.np * sizeof(double), cudaMemcpyDeviceToHost));
   const int64_t np = f.np, np2 = np * np;
+  // phase 1: per axis G (n x np^2, column p + np q = g_p .* g_q) and its Gram GG^T as the elementwise
+  // square of F F^T (n x n x np instead of n x n x np^2 flops; tei.cpp:118-124)
+  static thread_local std::array<DevBuf, 3> gbuf, grambuf, lbuf, smallbuf;
+  std::array<double*, 3> G{}, gram{}, Lw{}, dg{}, resid{};
+  std::array<int*, 3> piv{}, info{};
+  std::array<int64_t, 3> cap{};
+  PivBatch pb{};
   for (int ax = 0; ax < 3; ++ax) {
     const int64_t n = basis_dev.n[ax];
     f.n[ax] = n;
     f.h[ax] = h[ax];
-    auto* G = static_cast<double*>(ctx->ws_in.get(static_cast<size_t>(n) * np2 * sizeof(double)));
+    G[ax] = static_cast<double*>(gbuf[ax].get(std::max<int64_t>(1, n * np2) * sizeof(double)));
     dim3 g1(static_cast<unsigned>(std::min<int64_t>((n + 255) / 256, 64)), static_cast<unsigned>(np2));
-    gprod_kernel<<<g1, 256, 0, ctx->stream>>>(n, static_cast<int>(np), basis_dev.factor[ax], G);
+    gprod_kernel<<<g1, 256, 0, ctx->stream>>>(n, static_cast<int>(np), basis_dev.factor[ax], G[ax]);
     TGB_LAUNCHED(ctx);
-    auto* gram = static_cast<double*>(ctx->ws_out.get(static_cast<size_t>(n) * n * sizeof(double)));
-    // Gram G G^T (tei.cpp:124) without the n x n x np^2 product: the columns of
-    // G are all products g_p .* g_q, so (G G^T)(x, y) = (sum_p g_p(x) g_p(y))^2,
-    // the elementwise square of S = F F^T (n x n x np: np times fewer flops)
-    dgemm(ctx, false, true, n, n, np, 1.0, basis_dev.factor[ax], n, basis_dev.factor[ax], n, 0.0, gram, n);
-    square_kernel<<<static_cast<unsigned>(std::min<int64_t>((n * n + 255) / 256, 4096)), 256, 0, ctx->stream>>>(n * n,
-                                                                                                             gram);
+    gram[ax] = static_cast<double*>(grambuf[ax].get(std::max<int64_t>(1, n * n) * sizeof(double)));
+    dgemm(ctx, false, true, n, n, np, 1.0, basis_dev.factor[ax], n, basis_dev.factor[ax], n, 0.0, gram[ax], n);
+    square_kernel<<<static_cast<unsigned>(std::min<int64_t>((n * n + 255) / 256, 4096)), 256, 0, ctx->stream>>>(
+        n * n, gram[ax]);
     TGB_LAUNCHED(ctx);
-    const int64_t cap = std::min(n, np2);
-    auto* Lw = static_cast<double*>(ctx->ws_misc.get(static_cast<size_t>(n) * cap * sizeof(double) + n * sizeof(double) +
-                                                     64 + cap * sizeof(int) + 64));
-    double* dg = Lw + n * cap;
-    int* piv = reinterpret_cast<int*>(dg + n + 8);
-    auto* small = static_cast<double*>(ctx->ws_misc2.get(64 * sizeof(double)));
-    int* info = reinterpret_cast<int*>(small);
-    double* resid = small + 4;
-    pivchol_explicit_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(n), gram, eps_fit * eps_fit, 1,
-                                                                static_cast<int>(cap), 1e-12, dg, Lw, piv, info,
-                                                                resid);
-    TGB_LAUNCHED(ctx);
-    int hinfo[3];
-    TGB_CUDA(cudaMemcpyAsync(hinfo, info, 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (hinfo[2]) throw Error(TGB_NUMERICAL_ERROR, "tei_density_fitting: Gram matrix indefinite beyond tolerance");
-    f.fit_clamped = f.fit_clamped || hinfo[1];
-    const int64_t r = hinfo[0];
+    cap[ax] = std::min(n, np2);
+    Lw[ax] = static_cast<double*>(lbuf[ax].get(static_cast<size_t>(n) * std::max<int64_t>(cap[ax], 1) * sizeof(double)));
+    auto* sm = static_cast<double*>(smallbuf[ax].get((n + 64 + std::max<int64_t>(cap[ax], 1)) * sizeof(double)));
+    dg[ax] = sm;
+    info[ax] = reinterpret_cast<int*>(sm + n);
+    resid[ax] = sm + n + 4;
+    piv[ax] = reinterpret_cast<int*>(sm + n + 8);
+    pb.ax[ax] = PivAxis{static_cast<int>(n), static_cast<int>(cap[ax]), gram[ax], dg[ax], Lw[ax], resid[ax], piv[ax],
+                        info[ax]};
+  }
+  // phase 2: the three pivoted Choleskys (tei.cpp:125-129, trace stop at eps_fit^2) concurrently
+  pivchol_explicit3_kernel<<<3, kRedThreads, 0, ctx->stream>>>(pb, eps_fit * eps_fit, 1, 1e-12);
+  TGB_LAUNCHED(ctx);
+  int hinfo[3][4];
+  for (int ax = 0; ax < 3; ++ax)
+    TGB_CUDA(cudaMemcpyAsync(hinfo[ax], info[ax], 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (int ax = 0; ax < 3; ++ax)
+    if (hinfo[ax][2]) throw Error(TGB_NUMERICAL_ERROR, "tei_density_fitting: Gram matrix indefinite beyond tolerance");
+  // phase 3: per axis U = Q of the factor, V = G^T U, residual (tei.cpp:130-142)
+  for (int ax = 0; ax < 3; ++ax) {
+    const int64_t n = f.n[ax];
+    f.fit_clamped = f.fit_clamped || hinfo[ax][1];
+    const int64_t r = hinfo[ax][0];
     f.R[ax] = r;
     f.U[ax].get(std::max<int64_t>(1, n * r) * sizeof(double));
     f.V[ax].get(std::max<int64_t>(1, np2 * r) * sizeof(double));
     if (r > 0) {
       // U = orthonormal basis of span(L) (tei.cpp:136-138), GEMM-based Cholesky-QR
-      TGB_CUDA(cudaMemcpyAsync(dptr(f.U[ax]), Lw, static_cast<size_t>(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
-                               ctx->stream));
+      TGB_CUDA(cudaMemcpyAsync(dptr(f.U[ax]), Lw[ax], static_cast<size_t>(n) * r * sizeof(double),
+                               cudaMemcpyDeviceToDevice, ctx->stream));
       orthonormalize_columns(ctx, n, static_cast<int>(r), dptr(f.U[ax]));
-      dgemm(ctx, true, false, np2, r, n, 1.0, G, n, dptr(f.U[ax]), n, 0.0, dptr(f.V[ax]), np2);
+      dgemm(ctx, true, false, np2, r, n, 1.0, G[ax], n, dptr(f.U[ax]), n, 0.0, dptr(f.V[ax]), np2);
     }
-    // residual ||G - U V^T|| / ||G||  (T reuses the Gram workspace when large enough)
-    auto* T = static_cast<double*>(ctx->ws_out.get(std::max(static_cast<size_t>(n) * n, static_cast<size_t>(n) * np2) *
+    // residual ||G - U V^T|| / ||G||  (T reuses the Gram buffer when large enough)
+    auto* T = static_cast<double*>(grambuf[ax].get(std::max(static_cast<size_t>(n) * n, static_cast<size_t>(n) * np2) *
                                                    sizeof(double)));
     if (r > 0)
       dgemm(ctx, false, true, n, np2, r, 1.0, dptr(f.U[ax]), n, dptr(f.V[ax]), np2, 0.0, T, n);
@@ -645,7 +678,7 @@ void tei_fit(tgb_ctx* ctx, TEI& f, const tgb_cp& basis_dev, const int64_t* fn_of
       TGB_CUDA(cudaMemsetAsync(T, 0, static_cast<size_t>(n) * np2 * sizeof(double), ctx->stream));
     const int nblk = 256;
     auto* part = static_cast<double*>(ctx->ws_misc2.get(2 * nblk * sizeof(double)));
-    resid_kernel<<<nblk, 256, 0, ctx->stream>>>(n * np2, G, T, part);
+    resid_kernel<<<nblk, 256, 0, ctx->stream>>>(n * np2, G[ax], T, part);
     TGB_LAUNCHED(ctx);
     std::vector<double> hp(2 * nblk);
     TGB_CUDA(cudaMemcpyAsync(hp.data(), part, hp.size() * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
