@@ -10,4 +10,4 @@ ctx=tg.Context(0)
 f=tg.TEIFactorization(ctx); tg.tei_density_fitting(f,bs,disc,1e-6); tg.tei_convolution_matrices(f,kern); tg.tei_cholesky(f,1e-6)
 torch.cuda.synchronize(); print("ok", f.rank_b())
 PY
-TGB_TEI_NO_GRAPH=1 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv python /tmp/tei_prof.py 2>/dev/null | python tools/ncu_sum.py
+TGB_TEI_NO_GRAPH=1 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 3000 --csv python /tmp/tei_prof.py 2>/dev/null | python tools/ncu_sum.py
