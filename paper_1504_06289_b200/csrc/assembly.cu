@@ -216,32 +216,6 @@ __global__ void __launch_bounds__(256) triple_dot_kernel(int nq, int P, const do
   if (threadIdx.x == 0) part[blockIdx.y * static_cast<int64_t>(P) + p] = sh[0];
 }
 
-}  // namespace
-
-// Device-only variant for graph capture (no host copies or synchronisation):
-// out[p] = sum_q wb[q] prod_ax <F_ax(:, i0[p]), B_ax(:, q)>, all pointers device.
-void sep_inner_tiles(tgb_ctx* ctx, const int64_t n[3], const double* const F[3], const double* const B[3],
-                     const double* wb, int RB, const int* i0, const int* i1, int P, double* partial, double* out) {
-  SepArgs a;
-  for (int ax = 0; ax < 3; ++ax) {
-    a.n[ax] = n[ax];
-    a.F[ax] = F[ax];
-    a.B[ax] = B[ax];
-  }
-  a.i0 = i0;
-  a.i1 = i1;
-  a.wb = wb;
-  a.P = P;
-  a.RB = RB;
-  const int ntq = (RB + TQ - 1) / TQ;
-  sep_inner_dmma_kernel<<<dim3((P + TP - 1) / TP, ntq), DM_THREADS, 0, ctx->stream>>>(a, partial);
-  TGB_LAUNCHED(ctx);
-  reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(partial, ntq, P, out);
-  TGB_LAUNCHED(ctx);
-}
-
-namespace {
-
 // s[p] = sum_q wb[q] prod_ax <left_p^ax, B_q^ax>, returned to the host.
 std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* const F[3], const double* const B[3],
                               const double* wb, int RB, const std::vector<int>& i0, const std::vector<int>& i1) {

@@ -542,37 +542,6 @@ __global__ void __launch_bounds__(kJacThreads) jacobi_svd_kernel(int p, double* 
   for (int c = threadIdx.x; c < p; c += blockDim.x) sg_out[c] = nr_sh[perm_sh[c]];
 }
 
-// lower Cholesky of a p x p SPD matrix (host); returns false if not PD
-bool host_cholesky(int p, std::vector<double>& A) {
-  for (int j = 0; j < p; ++j) {
-    double d = A[j + static_cast<size_t>(p) * j];
-    for (int k = 0; k < j; ++k) d -= A[j + static_cast<size_t>(p) * k] * A[j + static_cast<size_t>(p) * k];
-    if (!(d > 0.0)) return false;
-    d = std::sqrt(d);
-    A[j + static_cast<size_t>(p) * j] = d;
-    for (int i = j + 1; i < p; ++i) {
-      double s = A[i + static_cast<size_t>(p) * j];
-      for (int k = 0; k < j; ++k) s -= A[i + static_cast<size_t>(p) * k] * A[j + static_cast<size_t>(p) * k];
-      A[i + static_cast<size_t>(p) * j] = s / d;
-    }
-    for (int i = 0; i < j; ++i) A[i + static_cast<size_t>(p) * j] = 0.0;
-  }
-  return true;
-}
-
-// inverse of the transposed lower factor: returns R^{-1} with R = L^T (upper)
-std::vector<double> upper_inverse_from_lower(int p, const std::vector<double>& L) {
-  std::vector<double> Ri(static_cast<size_t>(p) * p, 0.0);  // R = L^T upper; solve R X = I
-  for (int c = 0; c < p; ++c) {
-    for (int i = p - 1; i >= 0; --i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int k = i + 1; k < p; ++k) s -= L[k + static_cast<size_t>(p) * i] * Ri[k + static_cast<size_t>(p) * c];
-      Ri[i + static_cast<size_t>(p) * c] = s / L[i + static_cast<size_t>(p) * i];
-    }
-  }
-  return Ri;
-}
-
 // Scratch of the reduction / TEI drivers: while a DevStreamScope is alive,
 // blocks come from the context's cache (best fit) and go back to it, so the
 // many short-lived buffers of the iterations cost neither cudaMalloc latency

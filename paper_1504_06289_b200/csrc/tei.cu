@@ -323,30 +323,6 @@ __global__ void argmax_kernel(int n, const double* __restrict__ d, double* out_v
   }
 }
 
-// Cholesky step (tei.cpp:70-83): col -= L[:, :rank] L[p, :rank]^T; L[:, rank] = col / piv,
-// L[p, rank] = piv; diag -= L^2, diag[p] = 0; clamp negatives.  flags[0] |= clamped, flags[1] |= bad
-__global__ void chol_step_kernel(int64_t n, int rank, int p, double dmax, double max0, double neg_tol,
-                                 const double* __restrict__ col, double* __restrict__ L, double* __restrict__ diag,
-                                 int* flags) {
-  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (i >= n) return;
-  const double piv = sqrt(dmax);
-  double c = col[i];
-  for (int r = 0; r < rank; ++r) c -= L[i + n * r] * L[p + n * r];
-  double l = c / piv;
-  if (i == p) l = piv;
-  L[i + n * rank] = l;
-  double d = diag[i] - l * l;
-  if (i == p) d = 0.0;
-  if (d < 0.0) {
-    if (d < -neg_tol * max0) atomicOr(flags + 1, 1);
-    d = 0.0;
-    atomicOr(flags, 1);
-  }
-  diag[i] = d;
-}
-
-
 // ---- device-resident pivoted-Cholesky loop (tei.cpp:48-90 with the
 // max-diagonal stop of tei.cpp:198-204).  One step = the kernels below with
 // every step-dependent scalar (rank, pivot, max diagonal, the primitive pair of
@@ -642,23 +618,6 @@ __global__ void chol_ygather_kernel(int64_t np2, int K, const int* __restrict__ 
     Y[ax][e] = src[np2 * e];
 }
 
-__global__ void transpose_kernel(int64_t rows, int64_t cols, const double* __restrict__ a, double* __restrict__ t) {
-  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
-  if (idx >= rows * cols) return;
-  const int64_t i = idx % rows, j = idx / rows;
-  t[j + cols * i] = a[idx];
-}
-
-__global__ void fill_index_kernel(int n, int* __restrict__ ident, int* __restrict__ neg, double* __restrict__ ones,
-                                  int nones) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) {
-    ident[i] = i;
-    neg[i] = -1;
-  }
-  if (i < nones) ones[i] = 1.0;
-}
-
 __global__ void chol_advance_kernel(CholState* st) {
   if (!st->done) st->rank += 1;
 }
@@ -683,10 +642,9 @@ struct TEI {
   std::vector<int64_t> chol_piv;
   DevBuf d_fstart, d_pw, d_cstart, d_cpairs, d_cw;
   // pivoted-Cholesky column engine: Pk[ax] = [V M_0^T | ... | V M_{K-1}^T] (np^2 x r K),
-  // formed by the diagonal pass; Vt[ax] = V^T; identity / -1 index lists, unit weights
-  std::array<DevBuf, 3> Pk, Vt;
+  // formed by the diagonal pass and kept when it fits (row j gives y_k = M_k V[j, :]^T)
+  std::array<DevBuf, 3> Pk;
   bool have_pk = false;
-  DevBuf d_ident, d_neg, d_ones, d_part;
 };
 
 }  // namespace tgb
@@ -848,7 +806,7 @@ void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
   // keep every V M_k^T for the Cholesky columns when it fits a modest budget (config 3: 0.8 GB)
   size_t pk_bytes = 0;
   for (int ax = 0; ax < 3; ++ax) pk_bytes += static_cast<size_t>(np2) * f.R[ax] * f.K * sizeof(double);
-  f.have_pk = pk_bytes <= (size_t(8) << 30) && f.K > 0 && getenv("TGB_TEI_PK");  // opt-in: measured no faster
+  f.have_pk = pk_bytes <= (size_t(8) << 30) && f.K > 0 && !getenv("TGB_TEI_NO_PK");
   for (int ax = 0; ax < 3; ++ax) {
     Y[ax] = static_cast<double*>(ybuf[ax].get(std::max<int64_t>(1, np2 * f.R[ax]) * sizeof(double)));
     if (f.have_pk) f.Pk[ax].get(std::max<size_t>(8, static_cast<size_t>(np2) * f.R[ax] * f.K * sizeof(double)));
@@ -1020,27 +978,6 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
     dr = dp->r;
     dPk = const_cast<const double**>(dp->P);
   }
-  // DMMA column path over the stored V M_k^T (needs the transposed V and index lists once)
-  const bool pk_col = fused_col && f.have_pk;
-  if (pk_col) {
-    for (int ax = 0; ax < 3; ++ax) {
-      const int64_t r = f.R[ax];
-      auto* vt = static_cast<double*>(f.Vt[ax].get(std::max<int64_t>(1, r * np2) * sizeof(double)));
-      if (r)
-        transpose_kernel<<<static_cast<unsigned>((np2 * r + 255) / 256), 256, 0, ctx->stream>>>(np2, r, dptr(f.V[ax]),
-                                                                                               vt);
-      TGB_LAUNCHED(ctx);
-    }
-    f.d_ident.get(std::max<int64_t>(1, np2) * sizeof(int));
-    f.d_neg.get(std::max<int64_t>(1, np2) * sizeof(int));
-    f.d_ones.get(std::max<int64_t>(1, K) * sizeof(double));
-    f.d_part.get(std::max<int64_t>(1, np2 * ((K + 63) / 64)) * sizeof(double));
-    const int nfill = static_cast<int>(std::max<int64_t>(np2, K));
-    fill_index_kernel<<<(nfill + 255) / 256, 256, 0, ctx->stream>>>(
-        static_cast<int>(np2), static_cast<int*>(f.d_ident.p), static_cast<int*>(f.d_neg.p),
-        static_cast<double*>(f.d_ones.p), static_cast<int>(K));
-    TGB_LAUNCHED(ctx);
-  }
   const unsigned gnp = static_cast<unsigned>((np2 + 255) / 256);
   auto step = [&]() {
     chol_pivot_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(nb2), dg, target, cap, st, piv);
@@ -1050,21 +987,13 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
                                                  static_cast<const int*>(f.d_fstart.p),
                                                  static_cast<const double*>(f.d_pw.p), st);
       TGB_LAUNCHED(ctx);
-      if (pk_col) {  // y_k = row j of V M_k^T (gather), column on the DMMA separable kernel, accumulate
-        chol_ygather_kernel<<<dim3(16, 3), 256, 0, ctx->stream>>>(np2, static_cast<int>(K), dr, dPk, st, dY);
-        TGB_LAUNCHED(ctx);
-        const double* Fv[3] = {dptr(f.Vt[0]), dptr(f.Vt[1]), dptr(f.Vt[2])};
-        const double* By[3] = {Y[0], Y[1], Y[2]};
-        sep_inner_tiles(ctx, f.R.data(), Fv, By, static_cast<const double*>(f.d_ones.p), static_cast<int>(K),
-                        static_cast<const int*>(f.d_ident.p), static_cast<const int*>(f.d_neg.p),
-                        static_cast<int>(np2), static_cast<double*>(f.d_part.p), cc);
-        axpy_dev_kernel<<<gnp, 256, 0, ctx->stream>>>(np2, st, cc, z, t == 0 ? 1 : 0);
-        TGB_LAUNCHED(ctx);
-        continue;
-      }
-      if (fused_col) {  // y_k = M_k v (one launch), then the fused column + accumulation
-        chol_y_kernel<<<dim3(static_cast<unsigned>(K), 3), 128, rmax * sizeof(double), ctx->stream>>>(
-            np2, static_cast<int>(K), dr, dV, dM, st, dY);
+      if (fused_col) {
+        if (f.have_pk) {  // y_k = row j of the stored V M_k^T (the diagonal pass formed them): a gather
+          chol_ygather_kernel<<<dim3(16, 3), 256, 0, ctx->stream>>>(np2, static_cast<int>(K), dr, dPk, st, dY);
+        } else {  // y_k = M_k v
+          chol_y_kernel<<<dim3(static_cast<unsigned>(K), 3), 128, rmax * sizeof(double), ctx->stream>>>(
+              np2, static_cast<int>(K), dr, dV, dM, st, dY);
+        }
         TGB_LAUNCHED(ctx);
         if (dmma_col) {
           chol_col_dmma_kernel<<<static_cast<unsigned>((np2 + kCD_ROWS - 1) / kCD_ROWS), 128, dmma_smem, ctx->stream>>>(

@@ -158,9 +158,6 @@ void orthonormalize_columns(tgb_ctx* ctx, int64_t d, int p, double* X);
 void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ijk, double* out);
 void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
                           double* out);
-// assembly.cu
-void sep_inner_tiles(tgb_ctx* ctx, const int64_t n[3], const double* const F[3], const double* const B[3],
-                     const double* wb, int RB, const int* i0, const int* i1, int P, double* partial, double* out);
 // reduction.cu
 void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg);
 int64_t thin_svd_left_dev(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* U, double* sigma);
