@@ -463,7 +463,7 @@ __device__ __forceinline__ void dmma_cd(double (&c)[4], double a0, double a1, do
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                : "d"(a0), "d"(a1), "d"(b0));
 }
-__global__ void __launch_bounds__(128) chol_col_dmma_kernel(int64_t np2, int K, const int* __restrict__ rr,
+__global__ void __launch_bounds__(256) chol_col_dmma_kernel(int64_t np2, int K, const int* __restrict__ rr,
                                                            const double* const* __restrict__ V,
                                                            const double* const* __restrict__ Y, const CholState* st,
                                                            int init, double* __restrict__ z) {
@@ -483,12 +483,12 @@ __global__ void __launch_bounds__(128) chol_col_dmma_kernel(int64_t np2, int K, 
     const double* Ya = Y[ax];
     __syncthreads();  // previous axis' tiles consumed
 #pragma unroll 8
-    for (int e = tid; e < r * kCD_ROWS; e += 128) {
+    for (int e = tid; e < r * kCD_ROWS; e += 256) {  // all 8 warps stage; warps 0-3 compute
       const int row = e % kCD_ROWS, q = e / kCD_ROWS;
       vt[q * kCD_LDV + row] = i0 + row < np2 ? __ldg(Va + i0 + row + np2 * q) : 0.0;
     }
 #pragma unroll 8
-    for (int e = tid; e < r * kCD_COLS; e += 128) {
+    for (int e = tid; e < r * kCD_COLS; e += 256) {
       const int q = e % r, col = e / r;  // y column-major (q fastest): coalesced reads
       ys[q * kCD_LDY + col] = col < K ? __ldg(Ya + q + static_cast<int64_t>(r) * col) : 0.0;
     }
@@ -499,15 +499,17 @@ __global__ void __launch_bounds__(128) chol_col_dmma_kernel(int64_t np2, int K, 
 #pragma unroll
       for (int c = 0; c < 4; ++c) acc[j][c] = 0.0;
     const int rows0 = mt * 16;
-    for (int k4 = 0; k4 < r; k4 += 4) {
-      const int q = k4 + t;
-      const bool qin = q < r;
-      const double a0 = qin ? vt[q * kCD_LDV + rows0 + g] : 0.0;
-      const double a1 = qin ? vt[q * kCD_LDV + rows0 + g + 8] : 0.0;
+    if (warp < 4) {
+      for (int k4 = 0; k4 < r; k4 += 4) {
+        const int q = k4 + t;
+        const bool qin = q < r;
+        const double a0 = qin ? vt[q * kCD_LDV + rows0 + g] : 0.0;
+        const double a1 = qin ? vt[q * kCD_LDV + rows0 + g + 8] : 0.0;
 #pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const double b0 = qin ? ys[q * kCD_LDY + (nt0 + j) * 8 + g] : 0.0;
-        dmma_cd(acc[j], a0, a1, b0);
+        for (int j = 0; j < 3; ++j) {
+          const double b0 = qin ? ys[q * kCD_LDY + (nt0 + j) * 8 + g] : 0.0;
+          dmma_cd(acc[j], a0, a1, b0);
+        }
       }
     }
 #pragma unroll
@@ -527,7 +529,7 @@ __global__ void __launch_bounds__(128) chol_col_dmma_kernel(int64_t np2, int K, 
     v += __shfl_xor_sync(0xffffffffu, v, 2);
     rs[h] = v;
   }
-  if (t == 0) {
+  if (t == 0 && warp < 4) {
     red[warp][g][0] = rs[0];
     red[warp][g][1] = rs[1];
   }
@@ -996,7 +998,7 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
         }
         TGB_LAUNCHED(ctx);
         if (dmma_col) {
-          chol_col_dmma_kernel<<<static_cast<unsigned>((np2 + kCD_ROWS - 1) / kCD_ROWS), 128, dmma_smem, ctx->stream>>>(
+          chol_col_dmma_kernel<<<static_cast<unsigned>((np2 + kCD_ROWS - 1) / kCD_ROWS), 256, dmma_smem, ctx->stream>>>(
               np2, static_cast<int>(K), dr, dV, dYc, st, t == 0 ? 1 : 0, z);
         } else {
           chol_col_kernel<<<static_cast<unsigned>((np2 + col_rows - 1) / col_rows), col_rows * col_groups, col_smem,
