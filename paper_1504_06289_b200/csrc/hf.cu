@@ -323,6 +323,22 @@ void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_of
   std::vector<double> wprim(P), wk(RN);
   if (P) TGB_CUDA(cudaMemcpy(wprim.data(), basis.weight, P * sizeof(double), cudaMemcpyDeviceToHost));
   if (RN) TGB_CUDA(cudaMemcpy(wk.data(), kernel.weight, RN * sizeof(double), cudaMemcpyDeviceToHost));
+  // Mirror-symmetric kernel columns (p[i] == p[n-1-i] on every axis: every sinc column,
+  // kernel.cpp:194) make the windowed convolution a symmetric Toeplitz operator, so
+  // <g_c, g_c' * p> = <g_c', g_c * p>: only the blocks k <= m of K are formed and the
+  // other triangle is their mirror (the reference forms both and averages, hf.cpp:169).
+  bool sym_kernel = RN > 0 && !getenv("TGB_EXCHANGE_FULL");
+  for (int ax = 0; ax < 3 && sym_kernel; ++ax) {
+    const int64_t n = kernel.n[ax];
+    std::vector<double> kf(n * RN);
+    TGB_CUDA(cudaMemcpy(kf.data(), kernel.factor[ax], kf.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t q = 0; q < RN && sym_kernel; ++q)
+      for (int64_t i = 0; i < n / 2; ++i)
+        if (kf[i + n * q] != kf[n - 1 - i + n * q]) {
+          sym_kernel = false;
+          break;
+        }
+  }
   for (int64_t a = 0; a < nocc && RN > 0; ++a) {
     // phi_a = sum_k c_ka G_k (orbital_tensor, hf.cpp:39-46): columns = primitives of G_k, c_k != 0
     std::vector<int> phic;
@@ -380,38 +396,43 @@ void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_of
     const double* kf[3] = {kernel.factor[0], kernel.factor[1], kernel.factor[2]};
     convolve_axes(ctx, 3, basis.n, G, gpc, RN, kf, h, y, dmap);
     // groups of consecutive blocks m -> one GEMM per axis + the segmented reduction
-    const int64_t row_cap = std::max<int64_t>(8192, (int64_t(1) << 26) / std::max<int64_t>(G, 1));
+    // symmetric kernel: small groups keep the GEMM width c0[m1] (blocks k <= m) tight
+    const int64_t row_cap = sym_kernel ? std::max<int64_t>(2048, RN * (c0[nb] / std::max<int64_t>(nb, 1)) * 4)
+                                       : std::max<int64_t>(8192, (int64_t(1) << 26) / std::max<int64_t>(G, 1));
     std::vector<double> s_all(nb * G);
     int64_t m0 = 0;
     while (m0 < nb) {
       int64_t m1 = m0 + 1;
       while (m1 < nb && RN * (c0[m1 + 1] - c0[m0]) <= row_cap) ++m1;
       const int64_t r0 = RN * c0[m0], rows = RN * (c0[m1] - c0[m0]);
-      Scratch st(ctx, 3 * rows * G), sseg(ctx, m1 - m0 + 1), ss(ctx, (m1 - m0) * G);
+      const int64_t Gc = sym_kernel ? c0[m1] : G;  // left columns needed: blocks k <= m (symmetric) or all
+      Scratch st(ctx, 3 * rows * Gc), sseg(ctx, m1 - m0 + 1), ss(ctx, (m1 - m0) * Gc);
       std::vector<int64_t> seg(m1 - m0 + 1);
       for (int64_t m = m0; m <= m1; ++m) seg[m - m0] = RN * c0[m] - r0;
       const int64_t* dseg = upload(ctx, sseg, seg);
       double* T[3];
       for (int ax = 0; ax < 3; ++ax) {
-        T[ax] = st.p + ax * rows * G;
-        // T_ax (rows x G) = Y_ax(:, r0 : r0 + rows)^T GP_ax
-        dgemm(ctx, true, false, rows, G, basis.n[ax], 1.0, y[ax] + r0 * basis.n[ax], basis.n[ax], gp[ax],
+        T[ax] = st.p + ax * rows * Gc;
+        // T_ax (rows x Gc) = Y_ax(:, r0 : r0 + rows)^T GP_ax(:, 0 : Gc)
+        dgemm(ctx, true, false, rows, Gc, basis.n[ax], 1.0, y[ax] + r0 * basis.n[ax], basis.n[ax], gp[ax],
               basis.n[ax], 0.0, T[ax], rows);
       }
-      seg_triple_dot_kernel<<<dim3(static_cast<unsigned>(G), static_cast<unsigned>(m1 - m0)), 256, 0, ctx->stream>>>(
-          rows, static_cast<int>(G), T[0], T[1], T[2], dwy + r0, dseg, ss.p);
+      seg_triple_dot_kernel<<<dim3(static_cast<unsigned>(Gc), static_cast<unsigned>(m1 - m0)), 256, 0, ctx->stream>>>(
+          rows, static_cast<int>(Gc), T[0], T[1], T[2], dwy + r0, dseg, ss.p);
       TGB_LAUNCHED(ctx);
-      TGB_CUDA(cudaMemcpyAsync(s_all.data() + m0 * G, ss.p, (m1 - m0) * G * sizeof(double), cudaMemcpyDeviceToHost,
-                               ctx->stream));
+      for (int64_t m = m0; m < m1; ++m)
+        TGB_CUDA(cudaMemcpyAsync(s_all.data() + m * G, ss.p + (m - m0) * Gc, Gc * sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
       TGB_CUDA(cudaStreamSynchronize(ctx->stream));
       m0 = m1;
     }
     // K(k, m) += h^3 sum_{c in block k} w_g[c] s[m][c]   (vol * scalar_product, hf.cpp:166)
     for (int64_t m = 0; m < nb; ++m)
-      for (int64_t k = 0; k < nb; ++k) {
+      for (int64_t k = 0; k < (sym_kernel ? m + 1 : nb); ++k) {
         double sp = 0.0;
         for (int64_t c = c0[k]; c < c0[k + 1]; ++c) sp += wg[c] * s_all[m * G + c];
         kacc[k + nb * m] += vol * sp;
+        if (sym_kernel && k != m) kacc[m + nb * k] += vol * sp;
       }
   }
   for (int64_t m = 0; m < nb; ++m)

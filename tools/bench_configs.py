@@ -191,10 +191,13 @@ def cfg_hf(ctx):
     t_k, K = timed(lambda: tg.exchange_matrix(bs, disc, c_occ, kp, ctx), reps=1, sync=sync)
     n, P, RN = bs.grid.n[0], nb, kp.rank()
     G = P * P  # Hadamard columns per orbital (single-primitive functions, phi rank = nb)
-    flops_k = 8 * 2.0 * 3 * n * G * G * RN
+    # symmetric kernel: blocks k <= m only, in groups of 4 blocks (hf.cu exchange_matrix_dev)
+    executed = sum((min(m0 + 4, nb) - m0) * min(m0 + 4, nb) for m0 in range(0, nb, 4)) / (nb * nb)
+    flops_k = 8 * 2.0 * 3 * n * G * G * RN * executed
     out = {"config": "hf", "what": "config-1 basis: overlap/kinetic/nuclear/exchange; N_b=80 factor ops",
            "overlap_ms": t_s * 1e3, "kinetic_ms": t_t * 1e3, "nuclear_ms": t_v * 1e3, "exchange_ms": t_k * 1e3,
            "exchange_gemm_tflops": flops_k / t_k / 1e12, "exchange_fp64_frac": flops_k / t_k / 1e12 / FP64,
+           "exchange_gemm_fraction_of_full": executed,
            "exchange_convolutions": 8 * 3 * G * RN, "K_symmetric_exact": bool(np.array_equal(K, K.T))}
     # Cholesky-factor operators at config-3 size (N_b=80, R_B=362)
     r2 = Rng(77)
