@@ -147,7 +147,8 @@ int tgb_fock_from_factors(tgb_ctx* ctx, int64_t nb, int64_t rank, const double* 
 /* replaces tg::generalized_eigensolve (hf.hpp:94-95, hf.cpp:187-199):
  * F C = S C diag(e) by the Cholesky congruence of S; e ascending, columns of C
  * S-orthonormal (eigenvector signs are not fixed, as in the reference).
- * nb <= 112 (one-CTA solver).  NUMERICAL_ERROR when S is not positive definite. */
+ * One CTA (work tiles in shared memory up to nb = 112, global beyond).
+ * NUMERICAL_ERROR when S is not positive definite. */
 int tgb_generalized_eigensolve(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e,
                                int mem);
 
@@ -293,7 +294,7 @@ int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem);
  * sigma descending.  U needs rows x min(rows, cols), sigma min(rows, cols)
  * entries; *kept = the pairs returned under the reference's branch rule
  * (all min(rows, cols) except the tall Gram branch, which keeps sigma^2 >
- * sigma_0^2 1e-24).  Device solver: min(rows, cols) <= 128.  Singular-vector
+ * sigma_0^2 1e-24).  Device one-sided Jacobi, any size.  Singular-vector
  * signs are not fixed (as in the reference). */
 int tgb_thin_svd_left(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* U, double* sigma,
                       int64_t* kept, int mem);

@@ -60,10 +60,9 @@ struct PlanArgs {
   int nsp;  // single (self-mirror) first-pass blocks, stored last in the leader list
   const int* spos;  // pair_kernel_fused: positions of the leftover first-pass blocks (leaders 320..), 8 per thread
   int nspos;
-  int tt;           // pair_kernel_fused thread count the fused layout was built for (320 or 384)
+  int tt;           // pair_kernel_fused thread count the fused layout was built for (320)
   int fused;        // spectra stored in the fused order kf (pair_kernel_fused) instead of the DIT order
   const int* kf;    // fused order: slot -> natural frequency (N + 1 slots, Nyquist last)
-  int dbg;  // analysis only (TGB_PAIR_DBG): 1 skip stores, 2 skip L2 loads, 4 skip passes
   int r[kMaxPasses];
   int L[kMaxPasses];
   const int* perm;       // stored position -> natural frequency index (N entries)
@@ -78,7 +77,6 @@ struct PlanArgs {
   const double2* twpost; // forward post-processing: w_m^k, k <= N
   const double2* ph1;    // mode 1: e^{-i pi k (n-1)/m} * (cos(pi k/m) for even n), k <= N
   const double2* ph2;    // mode 2: e^{2 pi i k ofs/m} * ((1 + e^{2 pi i k/m})/2 for even n), k <= N
-  int store_dbg;              // analysis only (TGB_STORE_DBG): 1 first column only, 2 no stores
   unsigned long long* phase;  // analysis only (TGB_PHASE_CLK): per-phase SM cycles of the pair kernel
 };
 
@@ -170,23 +168,15 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
       }
     }
   }
-  // (10, 20, 8, 8) balances every pass at 320 threads but its stride-10 first
-  // pass bank-conflicts: measured slower (v14), opt-in only
-  if (N == 12800 && getenv("TGB_PLAN_10208")) rad = {10, 20, 8, 8};
-  // opt-in 384-thread fused pair kernel (3 warps on every SM sub-partition;
-  // the plan's spans 16 and 128 divide 384 so every pass keeps hoisted
-  // twiddles).  Measured within 1.5 % of the 320-thread kernel (its radix-10
-  // last pass costs what the balanced sub-partitions gain), so not the default.
-  const bool tt384 = N == 12800 && getenv("TGB_TT384");
-  if (tt384) rad = atoi(getenv("TGB_TT384")) == 2 ? std::vector<int>{16, 10, 10, 8} : std::vector<int>{16, 8, 10, 10};
-  a.tt = tt384 ? 384 : 320;
+  // (Measured and dropped: plan 10*20*8*8, whose stride-10 first pass
+  // bank-conflicts, and 384-thread fused kernels, within 1.5 % of 320 threads;
+  // profiles/r01_ncu_pair_kernel.txt.)
+  a.tt = 320;
   a.N = static_cast<int>(N);
   a.m = static_cast<int>(2 * N);
   const bool fits = !rad.empty();
   pl->direct = n <= ctx->direct_max || !fits;
-  a.dbg = getenv("TGB_PAIR_DBG") ? atoi(getenv("TGB_PAIR_DBG")) : 0;
   a.phase = nullptr;
-  a.store_dbg = getenv("TGB_STORE_DBG") ? atoi(getenv("TGB_STORE_DBG")) : 0;
   if (getenv("TGB_PHASE_CLK")) {
     a.phase = static_cast<unsigned long long*>(pl->phase.get(16 * sizeof(unsigned long long)));
     TGB_CUDA(cudaMemset(a.phase, 0, 16 * sizeof(unsigned long long)));
@@ -256,13 +246,10 @@ std::shared_ptr<ConvPlan> get_plan(tgb_ctx* ctx, int64_t n) {
     // (contiguous: the staged count need not be a multiple of tt), then Nyquist
     a.fused = 0;
     a.kf = nullptr;
-    const bool plan_ok = rad.size() == 4 && rad[0] == 16 &&
-                         ((tt == 320 && rad[1] == 10 && rad[2] == 10 && rad[3] == 8) ||
-                          (tt == 384 && ((rad[1] == 8 && rad[2] == 10 && rad[3] == 10) ||
-                                         (rad[1] == 10 && rad[2] == 10 && rad[3] == 8))));
+    const bool plan_ok = rad.size() == 4 && rad[0] == 16 && rad[1] == 10 && rad[2] == 10 && rad[3] == 8;
     const bool fused_plan = plan_ok && a.nspos <= 8 * tt && a.nspos + 32 * tt == N && a.npl - a.nsp >= tt &&
                             !getenv("TGB_NO_FUSED") &&
-                            !getenv("TGB_NO_TMEM") && !getenv("TGB_NO_STATIC") && a.dbg == 0;
+                            !getenv("TGB_NO_TMEM") && !getenv("TGB_NO_STATIC");
     if (fused_plan) {
       std::vector<int> kf(static_cast<size_t>(N) + 1);
       for (int t = 0; t < tt; ++t)
@@ -650,30 +637,6 @@ __device__ __forceinline__ void store_outputs(const double2* v, int j, int L, in
   }
 }
 
-// Same, with the per-pair constant lim = number of leading outputs that are
-// whole 16-byte pairs in aligned columns (0 when unaligned): one compare per
-// output on the fast path.
-template <int R, int L>
-__device__ __forceinline__ void store_outputs_fast(const double2* v, int j, int lim, int nz, bool odd_n, double* o0,
-                                                   double* o1) {
-#pragma unroll
-  for (int t = 0; t < R; ++t) {
-    const int idx = j + t * L;
-    if (idx < lim) {
-      __stcs(reinterpret_cast<double2*>(o0 + 2 * idx), v[t]);
-      if (o1) __stcs(reinterpret_cast<double2*>(o1 + 2 * idx), v[t]);
-    } else if (idx < nz && o0) {
-      const bool full = !(odd_n && idx == nz - 1);
-      __stcs(o0 + 2 * idx, v[t].x);
-      if (full) __stcs(o0 + 2 * idx + 1, v[t].y);
-      if (o1) {
-        __stcs(o1 + 2 * idx, v[t].x);
-        if (full) __stcs(o1 + 2 * idx + 1, v[t].y);
-      }
-    }
-  }
-}
-
 template <int R>
 __device__ __forceinline__ void last_pass_store(const double2* sm, const double2* tws, const PlanArgs& pa, double* o0,
                                                 double* o1, bool aligned) {
@@ -684,24 +647,6 @@ __device__ __forceinline__ void last_pass_store(const double2* sm, const double2
   const double2* hi = tws + pa.off_hi[pa.P - 1];
   const int T = blockDim.x;
   int j = threadIdx.x;
-  if constexpr (false) {
-    for (; j + T < nbf; j += 2 * T) {
-      double2 v[R], u[R];
-#pragma unroll
-      for (int s = 0; s < R; ++s) {
-        v[s] = sm[pidx(j + s * L)];
-        u[s] = sm[pidx(j + T + s * L)];
-      }
-      if (L > 1) {
-        apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
-        apply_twiddles<R, 1>(u, cmul(lo[(j + T) & 63], hi[(j + T) >> 6]));
-      }
-      dft<R, 1>(v);
-      dft<R, 1>(u);
-      store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
-      store_outputs<R>(u, j + T, L, nz, odd_n, o0, o1, aligned);
-    }
-  }
   for (; j < nbf; j += T) {
     double2 v[R];
 #pragma unroll
@@ -1045,22 +990,16 @@ __device__ __forceinline__ void pair_body(const PlanArgs& pa, const double2* __r
     const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
     const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
                           : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
-    if (!(pa.dbg & 2)) stage_product<BREAL>(sm, N, a, b);
+    stage_product<BREAL>(sm, N, a, b);
     __syncthreads();
-    if (!(pa.dbg & 4)) {
-      first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
+    first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
+    __syncthreads();
+    for (int p = 1; p + 1 < pa.P; ++p) {
+      dit_pass_rt<1>(sm, tws, pa, p);
       __syncthreads();
-      for (int p = 1; p + 1 < pa.P; ++p) {
-        dit_pass_rt<1>(sm, tws, pa, p);
-        __syncthreads();
-      }
     }
     double* o0 = out + e.out0;
     double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
-    if (pa.dbg & 1) {
-      o0 = nullptr;
-      o1 = nullptr;
-    }
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
     if (pa.P == 1) {
       // single pass: outputs are already natural-order in shared memory
@@ -1177,8 +1116,6 @@ __device__ __forceinline__ void static_last(const double2* sm, const double2* lo
                                             bool odd_n, double* o0, double* o1, bool aligned) {
   constexpr int NBF = N / R;
   static_assert(L % 16 == 0 && NBF == L, "last pass spans the whole transform");
-  const int lim = (aligned && o0) ? (odd_n ? nz - 1 : nz) : 0;
-  constexpr bool getenv_fast_store = false;  // v17: the branchy fast path measured slower
   for (int j = threadIdx.x; j < NBF; j += blockDim.x) {
     const double2* p = sm + pidx(j);
     double2 v[R];
@@ -1186,8 +1123,7 @@ __device__ __forceinline__ void static_last(const double2* sm, const double2* lo
     for (int s = 0; s < R; ++s) v[s] = p[s * (L + L / 16)];
     apply_twiddles<R, 1>(v, cmul(lo[j & 63], hi[j >> 6]));
     dft<R, 1>(v);
-    if (getenv_fast_store) store_outputs_fast<R, L>(v, j, lim, nz, odd_n, o0, o1);
-    else store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
+    store_outputs<R>(v, j, L, nz, odd_n, o0, o1, aligned);
   }
 }
 
@@ -1381,8 +1317,8 @@ __global__ void __launch_bounds__(TT, 1)
     static_pass_t<R2, L2, N, 1, TT>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
     __syncthreads();
     long long t4 = pa.phase ? clock64() : 0;
-    double* o0 = pa.store_dbg >= 2 ? nullptr : out + e.out0;
-    double* o1 = e.out1 >= 0 && !pa.store_dbg ? out + e.out1 : nullptr;
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
     static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
     __syncthreads();
@@ -1544,9 +1480,9 @@ __global__ void __launch_bounds__(TT, 1)
   const double2* cs = tws + pa.off_cs;
   const double2 wk = cmul(tws[pa.off_zlo + (it.z & 63)], tws[pa.off_zhi + (it.z >> 6)]);
   int sp[NS];
-#pragma unroll
-  // staged count N - 32 TT: a multiple of TT for the 320-thread layout (no guards compiled), ragged at 384
+  // staged count N - 32 TT: a multiple of TT for the 320-thread layout (no guards compiled)
   constexpr bool kRagged = (N - 32 * TT) % TT != 0;
+#pragma unroll
   for (int u = 0; u < NS; ++u)  // -1: no staged position
     sp[u] = (!kRagged || static_cast<int>(threadIdx.x) + TT * u < pa.nspos) ? __ldg(pa.spos + threadIdx.x + TT * u) : -1;
   const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
@@ -1840,7 +1776,7 @@ template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
 static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                        const PairEntry* dwork, const int* winfo, double* out) {
   const PlanArgs& a = pl.a;
-  if (!(a.P == 4 && a.r[0] == R0 && a.r[1] == R1 && a.r[2] == R2 && a.r[3] == R3) || a.dbg || getenv("TGB_NO_STATIC"))
+  if (!(a.P == 4 && a.r[0] == R0 && a.r[1] == R1 && a.r[2] == R2 && a.r[3] == R3) || getenv("TGB_NO_STATIC"))
     return false;
   const bool fused_ok = R0 == 16 && TT == a.tt && a.fused;  // the spectra were written in the fused order
   auto kern = (getenv("TGB_NO_TMEM") || a.N % TT) ? pair_kernel_static<R0, R1, R2, R3, TT, BREAL>
@@ -1890,49 +1826,10 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
   return true;
 }
 
-// The 384-thread fused pair kernel (plan 16 x 8 x 10 x 10): only the fused
-// kernel exists at this width (the spectra are in its storage order).
-static bool a_is_fused_elsewhere(const ConvPlan& pl) { return pl.a.fused && pl.a.tt != 320; }
-
-template <bool BREAL>
-static bool try_fused384(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
-                         const PairEntry* dwork, const int* winfo, double* out) {
-  const PlanArgs& a = pl.a;
-  if (!(a.P == 4 && a.r[0] == 16 && a.fused && a.tt == 384)) return false;
-  const bool p8 = a.r[1] == 8 && a.r[2] == 10 && a.r[3] == 10;
-  if (!p8 && !(a.r[1] == 10 && a.r[2] == 10 && a.r[3] == 8)) return false;
-  auto kern = p8 ? pair_kernel_fused<16, 8, 10, 10, 384, BREAL> : pair_kernel_fused<16, 10, 10, 8, 384, BREAL>;
-  static bool attr[2] = {false, false};
-  if (!attr[p8]) {
-    cudaFuncAttributes fa{};
-    TGB_CUDA(cudaFuncGetAttributes(&fa, kern));
-    TGB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
-    attr[p8] = true;
-  }
-  prof_begin(ctx);
-  kern<<<ctx->num_sms, 384, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);
-  TGB_LAUNCHED(ctx);
-  prof_end(ctx);
-  if (a.phase) {
-    unsigned long long h[8];
-    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-    TGB_CUDA(cudaMemcpy(h, a.phase, sizeof(h), cudaMemcpyDeviceToHost));
-    const double np = static_cast<double>(h[5] ? h[5] : 1);
-    fprintf(stderr, "phase cycles/pair: stage %.0f pass0 %.0f pass1 %.0f pass2 %.0f last %.0f (pairs %llu)\n",
-            h[0] / np, h[1] / np, h[2] / np, h[3] / np, h[4] / np, h[5]);
-    TGB_CUDA(cudaMemset(a.phase, 0, sizeof(h)));
-  }
-  return true;
-}
-
 template <bool BREAL>
 static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                           const PairEntry* dwork, const int* winfo, double* out) {
   // compile-time plans (config 2: n = 16385 -> N = 12800)
-  if (try_fused384<BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
-  if (a_is_fused_elsewhere(pl)) throw Error(TGB_CUDA_ERROR, "fftconv: fused spectrum order without its pair kernel");
-  if (try_static<10, 20, 8, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
   if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
   switch (pl.a.r[0]) {
     case 2: launch_pair<2, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
@@ -1959,18 +1856,6 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
     attr_set = true;
   }
   const PlanArgs& a = pl.a;
-  if (a.P == 4 && a.r[0] == 16 && a.r[1] == 8 && a.r[2] == 10 && a.r[3] == 10 && !getenv("TGB_NO_STATIC")) {
-    static bool attr3 = false;
-    if (!attr3) {
-      TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel_static<16, 8, 10, 10, 320>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
-      attr3 = true;
-    }
-    spectrum_kernel_static<16, 8, 10, 10, 320><<<nA + nB, 320, pl.smem, ctx->stream>>>(
-        pl.a, A, nA, specA, B, colidx, nB, specB, specB2, modeB, ldx, h);
-    TGB_LAUNCHED(ctx);
-    return;
-  }
   if (a.P == 4 && a.r[0] == 16 && a.r[1] == 10 && a.r[2] == 10 && a.r[3] == 8 && !getenv("TGB_NO_STATIC")) {
     static bool attr2 = false;
     if (!attr2) {

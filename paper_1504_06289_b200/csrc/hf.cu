@@ -169,15 +169,17 @@ __global__ void __launch_bounds__(256) pair_forms_kernel(int64_t n, const double
 // triangular solves), B = (F~ + F~^T)/2 + sigma I with sigma = 1.5 ||B||_F so
 // B is positive definite and its one-sided Jacobi SVD is its eigen-
 // decomposition; e = s - sigma ascending, C = L^-T V.
-constexpr int kGenMax = 112;  // two n x n FP64 tiles in shared memory
+// Up to kGenMax the two n x n work tiles live in shared memory; beyond it
+// they are a global workspace (wk, 2 n^2 doubles) and the same code runs.
+constexpr int kGenMax = 112;
 
 __global__ void __launch_bounds__(1024) gen_eig_prep_kernel(int n, const double* __restrict__ F,
                                                             const double* __restrict__ S, double* __restrict__ Lg,
                                                             double* __restrict__ B, double* __restrict__ sigma,
-                                                            int* __restrict__ fail) {
+                                                            int* __restrict__ fail, double* __restrict__ wk) {
   extern __shared__ double gsm[];
-  double* L = gsm;          // n x n, column-major, lower
-  double* Y = gsm + n * n;  // n x n work
+  double* L = wk ? wk : gsm;  // n x n, column-major, lower
+  double* Y = L + n * n;      // n x n work
   __shared__ int bad;
   __shared__ double red[32];
   if (threadIdx.x == 0) bad = 0;
@@ -259,11 +261,14 @@ __global__ void __launch_bounds__(1024) gen_eig_finish_kernel(int n, const doubl
                                                               const double* __restrict__ U,
                                                               const double* __restrict__ s,
                                                               const double* __restrict__ sigma, double* __restrict__ C,
-                                                              double* __restrict__ e) {
+                                                              double* __restrict__ e, int staged) {
   extern __shared__ double gsm[];
-  double* L = gsm;
-  for (int i = threadIdx.x; i < n * n; i += blockDim.x) L[i] = Lg[i];
-  __syncthreads();
+  const double* L = Lg;
+  if (staged) {
+    for (int i = threadIdx.x; i < n * n; i += blockDim.x) gsm[i] = Lg[i];
+    __syncthreads();
+    L = gsm;
+  }
   const double sg = *sigma;
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     const double* u = U + static_cast<int64_t>(n - 1 - c) * n;
@@ -601,11 +606,10 @@ void density_build_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offs
 
 void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const double* S, double* C, double* e) {
   if (nb == 0) return;
-  if (nb > kGenMax)
-    throw Error(TGB_INVALID_ARGUMENT, "generalized_eigensolve: basis larger than the one-CTA solver (112)");
   const int n = static_cast<int>(nb);
-  Scratch sl(ctx, nb * nb), sb(ctx, nb * nb), ss(ctx, nb + 2);
-  const size_t smem = 2 * static_cast<size_t>(nb * nb) * sizeof(double);
+  const bool staged = nb <= kGenMax;
+  Scratch sl(ctx, nb * nb), sb(ctx, nb * nb), ss(ctx, nb + 2), sw(ctx, staged ? 1 : 2 * nb * nb);
+  const size_t smem = staged ? 2 * static_cast<size_t>(nb * nb) * sizeof(double) : 0;
   static bool attr = false;
   if (!attr) {
     TGB_CUDA(cudaFuncSetAttribute(gen_eig_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -616,7 +620,7 @@ void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const
   }
   double* sigma = ss.p + nb;
   int* fail = reinterpret_cast<int*>(ss.p + nb + 1);
-  gen_eig_prep_kernel<<<1, 1024, smem, ctx->stream>>>(n, F, S, sl.p, sb.p, sigma, fail);
+  gen_eig_prep_kernel<<<1, 1024, smem, ctx->stream>>>(n, F, S, sl.p, sb.p, sigma, fail, staged ? nullptr : sw.p);
   TGB_LAUNCHED(ctx);
   int hfail = 0;
   TGB_CUDA(cudaMemcpyAsync(&hfail, fail, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
@@ -624,7 +628,7 @@ void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const
   if (hfail)
     throw Error(TGB_NUMERICAL_ERROR, "generalized_eigensolve: overlap not positive definite (basis near-dependence)");
   jacobi_svd_dev(ctx, n, sb.p, ss.p);
-  gen_eig_finish_kernel<<<1, 1024, smem / 2, ctx->stream>>>(n, sl.p, sb.p, ss.p, sigma, C, e);
+  gen_eig_finish_kernel<<<1, 1024, smem / 2, ctx->stream>>>(n, sl.p, sb.p, ss.p, sigma, C, e, staged ? 1 : 0);
   TGB_LAUNCHED(ctx);
 }
 

@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(1024) jacobi_onesided_kernel(int64_t m, int p,
                                                                 double* __restrict__ V, double* __restrict__ sg,
                                                                 int* __restrict__ perm) {
   __shared__ int rot_any;
-  __shared__ double nr_sh[129];  // p <= 128 (kJacMax)
+  extern __shared__ double nr_sh[];  // p column norms (dynamic)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int pe = p + (p & 1), half = pe / 2;
   const double tol = fmax(1e-16, p * 1.1102230246251565e-16);
@@ -372,8 +372,9 @@ __global__ void __launch_bounds__(1024) jacobi_onesided_kernel(int64_t m, int p,
   }
 }
 
-// U(:, c) = X(:, perm[c]) / sg[c] (left vectors of a tall matrix), or
-// U(:, c) = V(:, perm[c]) (left vectors of a wide one, from A^T's rotations)
+// U(:, c) = X(:, perm[c]) / sg[c] (left vectors of a tall matrix; a zero
+// column gives 0, or e_c with normalize == 2), or U(:, c) = V(:, perm[c])
+// (left vectors of a wide one, from A^T's rotations)
 __global__ void jacobi_gather_kernel(int64_t m, int p, const double* __restrict__ src, const int* __restrict__ perm,
                                      const double* __restrict__ sg, int normalize, double* __restrict__ U) {
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -381,7 +382,7 @@ __global__ void jacobi_gather_kernel(int64_t m, int p, const double* __restrict_
   const int64_t r = idx % m;
   const int c = static_cast<int>(idx / m);
   const double v = src[r + m * perm[c]];
-  U[idx] = normalize ? (sg[c] > 0.0 ? v / sg[c] : 0.0) : v;
+  U[idx] = normalize ? (sg[c] > 0.0 ? v / sg[c] : (normalize == 2 && r == c ? 1.0 : 0.0)) : v;
 }
 
 __global__ void sqrt_kernel(int64_t n, double* __restrict__ x) {
@@ -400,61 +401,10 @@ __global__ void fill_kernel(int64_t n, double v, double* __restrict__ x) {
   if (i < n) x[i] = v;
 }
 
-// ---------------------------------------------------------------- host dense LA (small matrices)
-
-// one-sided Jacobi SVD of a small p x p matrix S (column-major): S = U diag(sg) W^T,
-// singular values descending, left vectors in U.
-void jacobi_svd_small(int p, std::vector<double> S, std::vector<double>& sg, std::vector<double>& U) {
-  auto col = [&](int j) { return &S[static_cast<size_t>(p) * j]; };
-  for (int sweep = 0; sweep < 60; ++sweep) {
-    bool rot = false;
-    for (int i = 0; i < p - 1; ++i)
-      for (int j = i + 1; j < p; ++j) {
-        double al = 0, be = 0, ga = 0;
-        const double* ci = col(i);
-        const double* cj = col(j);
-        for (int r = 0; r < p; ++r) {
-          al += ci[r] * ci[r];
-          be += cj[r] * cj[r];
-          ga += ci[r] * cj[r];
-        }
-        if (ga == 0.0 || std::fabs(ga) <= 1e-16 * std::sqrt(al * be)) continue;
-        rot = true;
-        const double zeta = (be - al) / (2.0 * ga);
-        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
-        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
-        double* wi = col(i);
-        double* wj = col(j);
-        for (int r = 0; r < p; ++r) {
-          const double x = wi[r], y = wj[r];
-          wi[r] = c * x - sn * y;
-          wj[r] = sn * x + c * y;
-        }
-      }
-    if (!rot) break;
-  }
-  std::vector<double> nr(p);
-  for (int j = 0; j < p; ++j) {
-    double ss = 0;
-    for (int r = 0; r < p; ++r) ss += col(j)[r] * col(j)[r];
-    nr[j] = std::sqrt(ss);
-  }
-  std::vector<int> ord(p);
-  std::iota(ord.begin(), ord.end(), 0);
-  std::stable_sort(ord.begin(), ord.end(), [&](int x, int y) { return nr[x] > nr[y]; });
-  sg.resize(p);
-  U.assign(static_cast<size_t>(p) * p, 0.0);
-  for (int c = 0; c < p; ++c) {
-    const int j = ord[c];
-    sg[c] = nr[j];
-    for (int r = 0; r < p; ++r) U[r + static_cast<size_t>(p) * c] = nr[j] > 0 ? col(j)[r] / nr[j] : (r == c ? 1.0 : 0.0);
-  }
-}
-
-// The same one-sided Jacobi SVD on the device for p <= kJacMax: one CTA,
+// One-sided Jacobi SVD on the device for p <= kJacMax: one CTA,
 // columns in shared memory, round-robin (tournament) ordering so the p/2
 // rotations of a round are disjoint and run on separate warps; the rotation
-// formula and the stopping test are the host version's.  Output: U (sorted
+// formula and the stopping test are jacobi_onesided_kernel's.  Output: U (sorted
 // columns, in place of S) and sg, descending, stable in the column index.
 constexpr int kJacMax = 128;
 constexpr int kJacThreads = 1024;
@@ -673,6 +623,19 @@ void random_block(tgb_ctx* ctx, int64_t d, int p, double* X, uint64_t seed) {
 // 4 cols, cols >= 8) keeps the leading pairs with sigma^2 > sigma_0^2 1e-24.
 // U (rows x min) and sigma (min) are device outputs; returns the kept count.
 void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg);
+// One CTA, any p the column-norm scratch fits (p doubles of shared memory).
+static void launch_jacobi_onesided(tgb_ctx* ctx, int64_t m, int64_t p, double* X, double* V, double* sg, int* perm) {
+  const size_t sm = static_cast<size_t>(p) * sizeof(double);
+  if (sm + 1024 > ctx->smem_optin) throw Error(TGB_INVALID_ARGUMENT, "one-sided Jacobi: too many columns");
+  static bool attr = false;
+  if (!attr) {
+    TGB_CUDA(cudaFuncSetAttribute(jacobi_onesided_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ctx->smem_optin - 1024)));
+    attr = true;
+  }
+  jacobi_onesided_kernel<<<1, 1024, sm, ctx->stream>>>(m, static_cast<int>(p), X, V, sg, perm);
+  TGB_LAUNCHED(ctx);
+}
 static void dgemm_transpose(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* a, double* t) {
   const int64_t tot = rows * cols;
   transpose_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(rows, cols, a, t);
@@ -681,7 +644,6 @@ static void dgemm_transpose(tgb_ctx* ctx, int64_t rows, int64_t cols, const doub
 int64_t thin_svd_left_dev(tgb_ctx* ctx, int64_t rows, int64_t cols, const double* A, double* U, double* sigma) {
   const int64_t p = std::min(rows, cols);
   if (p == 0) return 0;
-  if (p > kJacMax) throw Error(TGB_INVALID_ARGUMENT, "thin_svd_left: min(rows, cols) above the device solver's 128");
   DevStreamScope scope(ctx);
   const bool gram_wide = cols >= 4 * rows && cols > 8192;               // reduction.cpp:93-104
   const bool jacobi_branch = !gram_wide && (rows < 4 * cols || cols < 8);  // reduction.cpp:105-108
@@ -692,15 +654,13 @@ int64_t thin_svd_left_dev(tgb_ctx* ctx, int64_t rows, int64_t cols, const double
     Dev X(static_cast<size_t>(rows) * cols);
     TGB_CUDA(cudaMemcpyAsync(X.p, A, static_cast<size_t>(rows) * cols * sizeof(double), cudaMemcpyDeviceToDevice,
                              ctx->stream));
-    jacobi_onesided_kernel<<<1, 1024, 0, ctx->stream>>>(rows, static_cast<int>(p), X.p, nullptr, sigma, perm);
-    TGB_LAUNCHED(ctx);
+    launch_jacobi_onesided(ctx, rows, p, X.p, nullptr, sigma, perm);
     jacobi_gather_kernel<<<gb, 256, 0, ctx->stream>>>(rows, static_cast<int>(p), X.p, perm, sigma, 1, U);
     TGB_LAUNCHED(ctx);
   } else if (gram_wide) {  // the reference's Gram branch: eigenpairs of A A^T (rows x rows)
     Dev G(static_cast<size_t>(rows) * rows);
     dgemm(ctx, false, true, rows, rows, cols, 1.0, A, rows, A, rows, 0.0, G.p, rows);
-    jacobi_onesided_kernel<<<1, 1024, 0, ctx->stream>>>(rows, static_cast<int>(p), G.p, nullptr, sigma, perm);
-    TGB_LAUNCHED(ctx);
+    launch_jacobi_onesided(ctx, rows, p, G.p, nullptr, sigma, perm);
     jacobi_gather_kernel<<<gb, 256, 0, ctx->stream>>>(rows, static_cast<int>(p), G.p, perm, sigma, 1, U);
     TGB_LAUNCHED(ctx);
     sqrt_kernel<<<static_cast<unsigned>((p + 255) / 256), 256, 0, ctx->stream>>>(p, sigma);  // sigma = sqrt(lambda)
@@ -708,8 +668,7 @@ int64_t thin_svd_left_dev(tgb_ctx* ctx, int64_t rows, int64_t cols, const double
   } else {  // wide: Jacobi on A^T with the rotations accumulated; U = V
     Dev X(static_cast<size_t>(rows) * cols);
     dgemm_transpose(ctx, rows, cols, A, X.p);
-    jacobi_onesided_kernel<<<1, 1024, 0, ctx->stream>>>(cols, static_cast<int>(p), X.p, V.p, sigma, perm);
-    TGB_LAUNCHED(ctx);
+    launch_jacobi_onesided(ctx, cols, p, X.p, V.p, sigma, perm);
     jacobi_gather_kernel<<<gb, 256, 0, ctx->stream>>>(rows, static_cast<int>(p), V.p, perm, sigma, 0, U);
     TGB_LAUNCHED(ctx);
   }
@@ -726,12 +685,24 @@ int64_t thin_svd_left_dev(tgb_ctx* ctx, int64_t rows, int64_t cols, const double
   return kept;
 }
 
-// One-CTA one-sided Jacobi SVD of a p x p device matrix (p <= 128): U
-// replaces S in place (columns sorted by descending singular value), sg gets
-// the p singular values.  Used by the generalized eigensolver (hf.cu).
+// One-CTA one-sided Jacobi SVD of a p x p device matrix: U replaces S in
+// place (columns sorted by descending singular value; a zero column -> e_c),
+// sg gets the p singular values.  p <= 128: columns in shared memory;
+// larger p: the global-memory sweep, then the sorted gather.  Used by the
+// Rayleigh-Ritz step of the rank reduction and the generalized eigensolver.
 void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg) {
-  if (p > kJacMax) throw Error(TGB_INVALID_ARGUMENT, "jacobi_svd_dev: matrix too large for the one-CTA solver");
   if (p <= 0) return;
+  if (p > kJacMax) {
+    Dev perm_d(static_cast<size_t>(p)), U(static_cast<size_t>(p) * p);
+    int* perm = reinterpret_cast<int*>(perm_d.p);
+    launch_jacobi_onesided(ctx, p, p, S, nullptr, sg, perm);
+    const int64_t tot = static_cast<int64_t>(p) * p;
+    jacobi_gather_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, ctx->stream>>>(p, p, S, perm, sg, 2, U.p);
+    TGB_LAUNCHED(ctx);
+    TGB_CUDA(cudaMemcpyAsync(S, U.p, static_cast<size_t>(tot) * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));  // the scratch is released on return
+    return;
+  }
   const size_t jsm = static_cast<size_t>(p) * (p + (p & 1)) * sizeof(double);
   static bool jattr = false;
   if (!jattr) {
@@ -865,7 +836,7 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
   for (double x : to_host(ctx, part.p, 256)) total += x;
   int p = static_cast<int>(std::min<int64_t>(std::min<int64_t>(dmin, kMaxBlock), sel >= 0 ? std::max<int64_t>(sel + 8, 16) : 48));
   Dev X, Y, T, tmp, Sd, sgd;
-  std::vector<double> sg, Ut;
+  std::vector<double> sg;
   int64_t r = 0;
   int pcur = 0;  // columns of X already holding a (partially converged) subspace
   bool have_x = false;
@@ -909,25 +880,10 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
       if (it % 2 == 1 || it >= 40) {
         // Rayleigh-Ritz: S = X^T a Y, rotate X to the singular directions
         dgemm(ctx, true, false, p, p, n, 1.0, X.p, n, T.p, n, 0.0, Sd.p, p);
-        if (p <= kJacMax && !getenv("TGB_HOST_JACOBI")) {
-          // device Jacobi: U replaces S in place, only the p singular values come back
-          const size_t jsm = static_cast<size_t>(p) * (p + (p & 1)) * sizeof(double);
-          static bool jattr = false;
-          if (!jattr) {
-            cudaFuncAttributes fa{};
-            TGB_CUDA(cudaFuncGetAttributes(&fa, jacobi_svd_kernel));
-            TGB_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
-            jattr = true;
-          }
-          sgd.resize(p);
-          jacobi_svd_kernel<<<1, kJacThreads, jsm, ctx->stream>>>(p, Sd.p, sgd.p);
-          TGB_LAUNCHED(ctx);
-          sg = to_host(ctx, sgd.p, p);
-        } else {
-          jacobi_svd_small(p, to_host(ctx, Sd.p, static_cast<size_t>(p) * p), sg, Ut);
-          to_dev(ctx, Sd.p, Ut);
-        }
+        // device Jacobi: U replaces S in place, only the p singular values come back
+        sgd.resize(p);
+        jacobi_svd_dev(ctx, p, Sd.p, sgd.p);
+        sg = to_host(ctx, sgd.p, p);
         dgemm(ctx, false, false, n, p, p, 1.0, X.p, n, Sd.p, p, 0.0, T.p, n);
         TGB_CUDA(cudaMemcpyAsync(X.p, T.p, static_cast<size_t>(n) * p * sizeof(double), cudaMemcpyDeviceToDevice,
                                  ctx->stream));

@@ -198,7 +198,7 @@ def fock_from_factors(h_core, chol, density, ctx: Context | None = None):
 
 
 def generalized_eigensolve(f, s, ctx: Context | None = None):
-    """hf.cpp:187-199 — F C = S C diag(e), e ascending, C S-orthonormal (device, nb <= 112)."""
+    """hf.cpp:187-199 — F C = S C diag(e), e ascending, C S-orthonormal (device)."""
     ctx = ctx or default_context()
     F = np.asfortranarray(np.asarray(f, dtype=np.float64))
     S = np.asfortranarray(np.asarray(s, dtype=np.float64))

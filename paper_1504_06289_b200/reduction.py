@@ -131,7 +131,7 @@ def reduce_rank(a: CanonicalTensor3, cfg: ReductionConfig, ctx: Context | None =
 
 def thin_svd_left(a, ctx: Context | None = None):
     """reduction.cpp:85-138 — (u, sigma): left singular pairs, sigma descending, with the
-    reference's output shape per branch (device solver: min(rows, cols) <= 128)."""
+    reference's output shape per branch (device one-sided Jacobi)."""
     ctx = ctx or default_context()
     A = np.asfortranarray(np.asarray(a, dtype=np.float64))
     if A.ndim != 2:

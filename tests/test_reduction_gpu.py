@@ -94,3 +94,20 @@ def test_wide_gram_branch(ctx):
     o = O.reduce(O.OCP.from_cp(theta), eps=1e-6, mode=0)
     assert res.tucker.ranks() == o["ranks"]
     assert relmax(res.tucker.to_dense(), np.einsum("abc,ia,jb,kc->ijk", o["core"], *o["sides"])) <= 1e-9
+
+
+def test_mode_rank_beyond_shared_memory_jacobi(ctx):
+    # a mode rank of 140: the subspace block grows past 128 columns, so its
+    # Rayleigh-Ritz SVD runs on the global-memory one-sided Jacobi
+    rng = Rng(26)
+    a = tucker_structured(rng, (160, 30, 30), (140, 6, 5), 200)
+    res = tg.rhosvd(a, tg.ReductionConfig.tolerance(1e-10), ctx)
+    assert res.tucker.ranks() == (140, 6, 5)
+    assert relmax(res.tucker.to_dense(), a.to_dense()) <= 1e-11
+    o = O.reduce(O.OCP.from_cp(a), eps=1e-10, mode=0)
+    assert o["ranks"] == (140, 6, 5)
+    # the ALS refines mode 0 within the 6 x 5 core unfolding: rank 30 (RHOSVD initial guess: 140)
+    c2t = tg.canonical_to_tucker(a, tg.ReductionConfig.tolerance(1e-10), ctx)
+    o1 = O.reduce(O.OCP.from_cp(a), eps=1e-10, mode=1)
+    assert c2t.tucker.ranks() == o1["ranks"] == (30, 6, 5)
+    assert relmax(c2t.tucker.to_dense(), a.to_dense()) <= 1e-10

@@ -48,9 +48,9 @@ def test_scf_matches_reference(ctx, name):
     assert max(st.orthonormality_defects) <= 1e-10
 
 
-def test_generalized_eigensolve(ctx):
+@pytest.mark.parametrize("nb", [37, 150])  # shared-memory tiles / global workspace (nb > 112)
+def test_generalized_eigensolve(ctx, nb):
     rng = np.random.default_rng(7)
-    nb = 37
     a = rng.normal(size=(nb, nb))
     s = a @ a.T / nb + np.eye(nb)
     f = rng.normal(size=(nb, nb))
