@@ -279,10 +279,8 @@ __global__ void gather_row_kernel(const double* __restrict__ V, int64_t np2, int
 
 // contraction: out[owner[p] + nb owner[q]] += pw[p] pw[q] z[p + np q]  (tei.cpp:166-172),
 // as a gather over contracted pairs (deterministic order p-major within q as the reference loop)
-__global__ void contract_kernel(int nb, int np, const int* __restrict__ fstart, const double* __restrict__ pw,
-                                const double* __restrict__ z, double* __restrict__ out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nb * nb) return;
+__device__ __forceinline__ double contract_at(int c, int nb, int np, const int* __restrict__ fstart,
+                                              const double* __restrict__ pw, const double* __restrict__ z) {
   const int mu = c % nb, nu = c / nb;
   const int a = min(mu, nu), b = max(mu, nu);
   double s = 0.0;
@@ -291,7 +289,13 @@ __global__ void contract_kernel(int nb, int np, const int* __restrict__ fstart, 
       const int64_t idx = mu <= nu ? p + static_cast<int64_t>(np) * q : q + static_cast<int64_t>(np) * p;
       s += pw[p] * pw[q] * z[idx];
     }
-  out[c] = s;
+  return s;
+}
+
+__global__ void contract_kernel(int nb, int np, const int* __restrict__ fstart, const double* __restrict__ pw,
+                                const double* __restrict__ z, double* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c < nb * nb) out[c] = contract_at(c, nb, np, fstart, pw, z);
 }
 
 __global__ void axpy_kernel(int64_t n, double a, const double* __restrict__ x, double* __restrict__ y, int init) {
@@ -336,11 +340,18 @@ struct CholState {
   double dmax;   // current max diagonal
   double w;      // weight of the current primitive pair (0: no term)
   int flags[2];  // [0] clamped a negative diagonal, [1] negative beyond tolerance
+  unsigned int arrived;  // CTAs of the current chol_step_dev_kernel that finished (the last advances)
 };
 
 // argmax of the diagonal (first maximal index, Eigen's maxCoeff(&p)); stop test
+__device__ __forceinline__ void chol_term(int nb, int np, int t, const int* __restrict__ fstart,
+                                          const double* __restrict__ pw, CholState* st);
+// (+ the column's first primitive pair, chol_term t = 0; gathering its y_ax
+// here too measured slower than chol_ygather_kernel's 48 CTAs)
 __global__ void __launch_bounds__(kRedThreads) chol_pivot_kernel(int n, const double* __restrict__ d, double target,
-                                                                 int cap, CholState* st, int64_t* piv_list) {
+                                                                 int cap, CholState* st, int64_t* piv_list, int nb,
+                                                                 int np, const int* __restrict__ fstart,
+                                                                 const double* __restrict__ pw) {
   if (st->done) return;
   __shared__ double sv[32];
   __shared__ int si[32];
@@ -355,15 +366,15 @@ __global__ void __launch_bounds__(kRedThreads) chol_pivot_kernel(int n, const do
       st->piv = idx;
       st->dmax = v;
       piv_list[st->rank] = idx;
+      chol_term(nb, np, 0, fstart, pw, st);
     }
   }
 }
 
 // primitive pair t of the pivot's contracted pair (kappa, lambda): q-major over
 // lambda's primitives, p over kappa's (tei.cpp:166-170 loop order)
-__global__ void chol_term_kernel(int nb, int np, int t, const int* __restrict__ fstart, const double* __restrict__ pw,
-                                 CholState* st) {
-  if (st->done) return;
+__device__ __forceinline__ void chol_term(int nb, int np, int t, const int* __restrict__ fstart,
+                                          const double* __restrict__ pw, CholState* st) {
   const int c = st->piv, kappa = c % nb, lambda = c / nb;
   const int nk = fstart[kappa + 1] - fstart[kappa], nl = fstart[lambda + 1] - fstart[lambda];
   if (t >= nk * nl) {
@@ -373,6 +384,12 @@ __global__ void chol_term_kernel(int nb, int np, int t, const int* __restrict__ 
   const int p = fstart[kappa] + t % nk, q = fstart[lambda] + t / nk;
   st->j = p + np * q;
   st->w = pw[p] * pw[q];
+}
+
+__global__ void chol_term_kernel(int nb, int np, int t, const int* __restrict__ fstart, const double* __restrict__ pw,
+                                 CholState* st) {
+  if (st->done) return;
+  chol_term(nb, np, t, fstart, pw, st);
 }
 
 __global__ void gather_row_dev_kernel(const double* __restrict__ V, int64_t np2, int r, const CholState* st,
@@ -392,12 +409,17 @@ __global__ void axpy_dev_kernel(int64_t n, const CholState* st, const double* __
   else if (a != 0.0) y[i] = y[i] + a * x[i];
 }
 
-// tei.cpp:70-83 for the pivot in `st`; the rank advances in chol_advance_kernel.
+// tei.cpp:70-83 for the pivot in `st`: the column entry is contracted here
+// from the primitive-pair column z (tei.cpp:166-170), and the last CTA to
+// finish advances the rank.
 // The downdate col - L[:, :rank] L[p, :rank]^T is split over kCholParts
 // thread groups per row block (coalesced over rows, fixed-order reduction).
 constexpr int kCholRows = 64, kCholParts = 8;
 __global__ void __launch_bounds__(kCholRows * kCholParts) chol_step_dev_kernel(int64_t n, double max0, double neg_tol,
-                                                                               const double* __restrict__ col,
+                                                                               int nb, int np,
+                                                                               const int* __restrict__ fstart,
+                                                                               const double* __restrict__ pw,
+                                                                               const double* __restrict__ z,
                                                                                double* __restrict__ L,
                                                                                double* __restrict__ diag,
                                                                                CholState* st) {
@@ -411,22 +433,31 @@ __global__ void __launch_bounds__(kCholRows * kCholParts) chol_step_dev_kernel(i
     for (int r = grp; r < rank; r += kCholParts) acc += L[i + n * r] * L[p + n * r];
   part[grp][row] = acc;
   __syncthreads();
-  if (grp != 0 || i >= n) return;
-  double dd = 0.0;
-  for (int g = 0; g < kCholParts; ++g) dd += part[g][row];
-  const double piv = sqrt(st->dmax);
-  const double c = col[i] - dd;
-  double l = c / piv;
-  if (i == p) l = piv;
-  L[i + n * rank] = l;
-  double d = diag[i] - l * l;
-  if (i == p) d = 0.0;
-  if (d < 0.0) {
-    if (d < -neg_tol * max0) atomicOr(st->flags + 1, 1);
-    d = 0.0;
-    atomicOr(st->flags, 1);
+  if (grp == 0 && i < n) {
+    double dd = 0.0;
+    for (int g = 0; g < kCholParts; ++g) dd += part[g][row];
+    const double piv = sqrt(st->dmax);
+    const double c = contract_at(static_cast<int>(i), nb, np, fstart, pw, z) - dd;
+    double l = c / piv;
+    if (i == p) l = piv;
+    L[i + n * rank] = l;
+    double d = diag[i] - l * l;
+    if (i == p) d = 0.0;
+    if (d < 0.0) {
+      if (d < -neg_tol * max0) atomicOr(st->flags + 1, 1);
+      d = 0.0;
+      atomicOr(st->flags, 1);
+    }
+    diag[i] = d;
   }
-  diag[i] = d;
+  __syncthreads();  // every thread of this CTA has read st->rank
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&st->arrived, 1u) == gridDim.x - 1) {  // last CTA: all reads of the rank are done
+      st->arrived = 0;
+      st->rank += 1;
+    }
+  }
 }
 
 // y_ax[q + r k] = (M_k v)[q] with v = V_ax[j, :] (the pivot term's row): grid (K, 3)
@@ -451,92 +482,96 @@ __global__ void chol_y_kernel(int64_t np2, int K, const int* __restrict__ rr, co
 // z[i] = (init ? 0 : z[i]) + w sum_k prod_ax <V_ax[i, :], y_ax[:, k]>   (b_prim_column, tei.cpp:33-44,
 // and the contraction-weighted accumulation of tei.cpp:166-170), rows split over CTAs, the K columns of
 // each row over thread groups; products summed in k order.
-// The same column on the FP64 tensor cores (mma.sync m16n8k4 f64): CTA = 32
-// rows x 48 (>= K) columns, 4 warps each one m16 tile x three n8 tiles; per
-// axis the V_ax row tile (32 x r) and y_ax (r x 48, zero padded) are staged in
-// shared memory (8 independent loads in flight per thread), the axis products
-// stay in the accumulator fragments, and the row sums over k reduce in a fixed
-// order (lanes t, then tiles, then warps).
-constexpr int kCD_ROWS = 32, kCD_COLS = 48, kCD_LDV = kCD_ROWS + 4, kCD_LDY = kCD_COLS + 8;
+constexpr int kCD_COLS = 48;  // K <= 48 kernel columns: six n8 tiles
 __device__ __forceinline__ void dmma_cd(double (&c)[4], double a0, double a1, double b0) {
   asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                : "d"(a0), "d"(a1), "d"(b0));
 }
-__global__ void __launch_bounds__(256) chol_col_dmma_kernel(int64_t np2, int K, const int* __restrict__ rr,
-                                                           const double* const* __restrict__ V,
-                                                           const double* const* __restrict__ Y, const CholState* st,
-                                                           int init, double* __restrict__ z) {
+
+// The same column on the FP64 tensor cores (mma.sync m16n8k4 f64): one m16
+// row tile per CTA, the three axes on separate warps (warp w: axis w / 2, n8
+// tiles 3 (w & 1) .. + 2, K zero-padded to 48).  A and B fragments come
+// straight from L2/L1 — no shared-memory staging round trips, no barrier
+// before the MMAs (a 32-row CTA staging V and y in shared memory measured 44
+// vs 14.5 us per column at config 3); the axis products meet in shared
+// memory and the row sums reduce in a fixed order (lanes t, tiles, warps).
+constexpr int kCD2_THREADS = 192;
+__global__ void __launch_bounds__(kCD2_THREADS) chol_col_dmma_kernel(int64_t np2, int K, const int* __restrict__ rr,
+                                                                     const double* const* __restrict__ V,
+                                                                     const double* const* __restrict__ Y,
+                                                                     const CholState* st, int init,
+                                                                     double* __restrict__ z) {
   if (st->done) return;
-  extern __shared__ double cd_sm[];
-  const int rmax = max(rr[0], max(rr[1], rr[2]));
-  double* vt = cd_sm;                                          // [q][row], rmax x kCD_LDV
-  double* ys = cd_sm + static_cast<int64_t>(rmax) * kCD_LDV;  // [q][col], rmax x kCD_LDY
-  __shared__ double red[4][16][2];
-  const int64_t i0 = blockIdx.x * static_cast<int64_t>(kCD_ROWS);
+  __shared__ double part[2][16][kCD_COLS + 1];  // axes 1 and 2: [row][col] of the 16 x 48 tile
+  __shared__ double red[2][16][2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
-  const int mt = warp & 1, nt0 = (warp >> 1) * 3;  // m16 tile, first of three n8 tiles
-  double prod[3][4];
-  for (int ax = 0; ax < 3; ++ax) {
-    const int r = rr[ax];
-    const double* Va = V[ax];
-    const double* Ya = Y[ax];
-    __syncthreads();  // previous axis' tiles consumed
-#pragma unroll 8
-    for (int e = tid; e < r * kCD_ROWS; e += 256) {  // all 8 warps stage; warps 0-3 compute
-      const int row = e % kCD_ROWS, q = e / kCD_ROWS;
-      vt[q * kCD_LDV + row] = i0 + row < np2 ? __ldg(Va + i0 + row + np2 * q) : 0.0;
-    }
-#pragma unroll 8
-    for (int e = tid; e < r * kCD_COLS; e += 256) {
-      const int q = e % r, col = e / r;  // y column-major (q fastest): coalesced reads
-      ys[q * kCD_LDY + col] = col < K ? __ldg(Ya + q + static_cast<int64_t>(r) * col) : 0.0;
-    }
-    __syncthreads();
-    double acc[3][4];
+  const int ax = warp >> 1, nt0 = (warp & 1) * 3;
+  const int r = rr[ax];
+  const double* __restrict__ Va = V[ax];
+  const double* __restrict__ Ya = Y[ax];
+  const int64_t i0 = blockIdx.x * 16LL;
+  const bool in0 = i0 + g < np2, in1 = i0 + g + 8 < np2;
+  const double* va = Va + i0 + g;
+  int64_t yb[3];
+  bool cin[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int col = (nt0 + j) * 8 + g;
+    cin[j] = col < K;
+    yb[j] = static_cast<int64_t>(r) * col;
+  }
+  double acc[3][4];
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[j][c] = 0.0;
+#pragma unroll 4
+  for (int k4 = 0; k4 < r; k4 += 4) {
+    const int q = k4 + t;
+    const bool qin = q < r;
+    const int64_t vq = np2 * q;
+    const double a0 = (qin && in0) ? __ldg(va + vq) : 0.0;
+    const double a1 = (qin && in1) ? __ldg(va + vq + 8) : 0.0;
+    double b[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) b[j] = (qin && cin[j]) ? __ldg(Ya + q + yb[j]) : 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) dmma_cd(acc[j], a0, a1, b[j]);
+  }
+  // fragment (j, c): row g + 8 (c >= 2), column (nt0 + j) 8 + 2t + (c & 1)
+  if (ax > 0) {
 #pragma unroll
     for (int j = 0; j < 3; ++j)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc[j][c] = 0.0;
-    const int rows0 = mt * 16;
-    if (warp < 4) {
-      for (int k4 = 0; k4 < r; k4 += 4) {
-        const int q = k4 + t;
-        const bool qin = q < r;
-        const double a0 = qin ? vt[q * kCD_LDV + rows0 + g] : 0.0;
-        const double a1 = qin ? vt[q * kCD_LDV + rows0 + g + 8] : 0.0;
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const double b0 = qin ? ys[q * kCD_LDY + (nt0 + j) * 8 + g] : 0.0;
-          dmma_cd(acc[j], a0, a1, b0);
-        }
-      }
-    }
-#pragma unroll
-    for (int j = 0; j < 3; ++j)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) prod[j][c] = ax == 0 ? acc[j][c] : prod[j][c] * acc[j][c];
-  }
-  // row sums over the columns: fragment (j, c) sits at row g + 8 (c >= 2), column (nt0 + j) 8 + 2t + (c & 1);
-  // padded columns hold exact zeros (zero y)
-  double rs[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    double v = 0.0;
-#pragma unroll
-    for (int j = 0; j < 3; ++j) v += prod[j][2 * h] + prod[j][2 * h + 1];
-    v += __shfl_xor_sync(0xffffffffu, v, 1);
-    v += __shfl_xor_sync(0xffffffffu, v, 2);
-    rs[h] = v;
-  }
-  if (t == 0 && warp < 4) {
-    red[warp][g][0] = rs[0];
-    red[warp][g][1] = rs[1];
+      for (int c = 0; c < 4; ++c) part[ax - 1][g + 8 * (c >> 1)][(nt0 + j) * 8 + 2 * t + (c & 1)] = acc[j][c];
   }
   __syncthreads();
-  if (tid < kCD_ROWS) {
-    const int m = tid >> 4, rr16 = tid & 15, hh = rr16 >> 3, gg = rr16 & 7;
-    const double sum = red[m][gg][hh] + red[m + 2][gg][hh];  // warps m (n tiles 0-2) and m + 2 (n tiles 3-5)
+  if (ax == 0) {
+    double rs[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double v = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int row = g + 8 * h, col = (nt0 + j) * 8 + 2 * t;
+        const double p0 = acc[j][2 * h] * part[0][row][col] * part[1][row][col];
+        const double p1 = acc[j][2 * h + 1] * part[0][row][col + 1] * part[1][row][col + 1];
+        v += p0 + p1;
+      }
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      rs[h] = v;
+    }
+    if (t == 0) {
+      red[warp][g][0] = rs[0];
+      red[warp][g][1] = rs[1];
+    }
+  }
+  __syncthreads();
+  if (tid < 16) {
+    const int hh = tid >> 3, gg = tid & 7;
+    const double sum = red[0][gg][hh] + red[1][gg][hh];  // n tiles 0-2, then 3-5
     const int64_t i = i0 + tid;
     if (i < np2) {
       const double w = st->w;
@@ -620,9 +655,6 @@ __global__ void chol_ygather_kernel(int64_t np2, int K, const int* __restrict__ 
     Y[ax][e] = src[np2 * e];
 }
 
-__global__ void chol_advance_kernel(CholState* st) {
-  if (!st->done) st->rank += 1;
-}
 
 }  // namespace
 
@@ -889,9 +921,8 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
   tei_diagonal_dev(ctx, f, dg);
   f.L.get(std::max<int64_t>(1, nb2 * nb2) * sizeof(double));
   double* L = dptr(f.L);
-  static thread_local DevBuf colbuf, zbuf, cbuf, stbuf, pivbuf;
+  static thread_local DevBuf zbuf, cbuf, stbuf, pivbuf;
   static thread_local std::array<DevBuf, 3> wbuf, ybuf, vrow;
-  auto* col = static_cast<double*>(colbuf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
   auto* z = static_cast<double*>(zbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
   auto* cc = static_cast<double*>(cbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
   auto* st = static_cast<CholState*>(stbuf.get(sizeof(CholState)));
@@ -932,17 +963,8 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
       static_cast<size_t>((f.R[0] + f.R[1] + f.R[2] + col_rows) * K + col_rows * rmax) * sizeof(double);
   const bool fused_col = col_smem <= ctx->smem_optin - 1024 && K <= 8 * col_groups &&
                          !getenv("TGB_TEI_GEMM_COLUMN") && K > 0;
-  // DMMA column kernel (K <= 48 columns per tile; measured 40 vs 64 us per column at config 3)
-  const size_t dmma_smem = static_cast<size_t>(rmax) * (kCD_LDV + kCD_LDY) * sizeof(double);
-  const bool dmma_col = fused_col && K <= kCD_COLS && dmma_smem <= ctx->smem_optin - 2048 && !getenv("TGB_TEI_SIMT_COLUMN");
-  if (dmma_col) {
-    static bool dattr = false;
-    if (!dattr) {
-      TGB_CUDA(cudaFuncSetAttribute(chol_col_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(ctx->smem_optin - 2048)));
-      dattr = true;
-    }
-  }
+  // DMMA column kernel for K <= 48 kernel columns (config 3: 14.5 us per column vs 64 us SIMT)
+  const bool dmma_col = fused_col && K <= kCD_COLS && !getenv("TGB_TEI_SIMT_COLUMN");
   const double** dV = nullptr;
   const double** dM = nullptr;
   double** dY = nullptr;
@@ -982,23 +1004,29 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
   }
   const unsigned gnp = static_cast<unsigned>((np2 + 255) / 256);
   auto step = [&]() {
-    chol_pivot_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(nb2), dg, target, cap, st, piv);
+    chol_pivot_kernel<<<1, kRedThreads, 0, ctx->stream>>>(static_cast<int>(nb2), dg, target, cap, st, piv,
+                                                          static_cast<int>(nb), static_cast<int>(np),
+                                                          static_cast<const int*>(f.d_fstart.p),
+                                                          static_cast<const double*>(f.d_pw.p));
     TGB_LAUNCHED(ctx);
     for (int t = 0; t < max_terms; ++t) {
-      chol_term_kernel<<<1, 1, 0, ctx->stream>>>(static_cast<int>(nb), static_cast<int>(np), t,
-                                                 static_cast<const int*>(f.d_fstart.p),
-                                                 static_cast<const double*>(f.d_pw.p), st);
-      TGB_LAUNCHED(ctx);
+      if (t > 0) {  // the pivot kernel formed term 0
+        chol_term_kernel<<<1, 1, 0, ctx->stream>>>(static_cast<int>(nb), static_cast<int>(np), t,
+                                                   static_cast<const int*>(f.d_fstart.p),
+                                                   static_cast<const double*>(f.d_pw.p), st);
+        TGB_LAUNCHED(ctx);
+      }
       if (fused_col) {
         if (f.have_pk) {  // y_k = row j of the stored V M_k^T (the diagonal pass formed them): a gather
           chol_ygather_kernel<<<dim3(16, 3), 256, 0, ctx->stream>>>(np2, static_cast<int>(K), dr, dPk, st, dY);
+          TGB_LAUNCHED(ctx);
         } else {  // y_k = M_k v
           chol_y_kernel<<<dim3(static_cast<unsigned>(K), 3), 128, rmax * sizeof(double), ctx->stream>>>(
               np2, static_cast<int>(K), dr, dV, dM, st, dY);
+          TGB_LAUNCHED(ctx);
         }
-        TGB_LAUNCHED(ctx);
         if (dmma_col) {
-          chol_col_dmma_kernel<<<static_cast<unsigned>((np2 + kCD_ROWS - 1) / kCD_ROWS), 256, dmma_smem, ctx->stream>>>(
+          chol_col_dmma_kernel<<<static_cast<unsigned>((np2 + 15) / 16), kCD2_THREADS, 0, ctx->stream>>>(
               np2, static_cast<int>(K), dr, dV, dYc, st, t == 0 ? 1 : 0, z);
         } else {
           chol_col_kernel<<<static_cast<unsigned>((np2 + col_rows - 1) / col_rows), col_rows * col_groups, col_smem,
@@ -1024,14 +1052,10 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
       axpy_dev_kernel<<<gnp, 256, 0, ctx->stream>>>(np2, st, cc, z, t == 0 ? 1 : 0);
       TGB_LAUNCHED(ctx);
     }
-    contract_kernel<<<static_cast<unsigned>((nb2 + 127) / 128), 128, 0, ctx->stream>>>(
-        static_cast<int>(nb), static_cast<int>(np), static_cast<const int*>(f.d_fstart.p),
-        static_cast<const double*>(f.d_pw.p), z, col);
-    TGB_LAUNCHED(ctx);
     chol_step_dev_kernel<<<static_cast<unsigned>((nb2 + kCholRows - 1) / kCholRows), kCholRows * kCholParts, 0,
-                           ctx->stream>>>(nb2, max0, 1e-10, col, L, dg, st);
-    TGB_LAUNCHED(ctx);
-    chol_advance_kernel<<<1, 1, 0, ctx->stream>>>(st);
+                           ctx->stream>>>(nb2, max0, 1e-10, static_cast<int>(nb), static_cast<int>(np),
+                                          static_cast<const int*>(f.d_fstart.p),
+                                          static_cast<const double*>(f.d_pw.p), z, L, dg, st);
     TGB_LAUNCHED(ctx);
   };
   // one eager step sizes every workspace (no allocation may happen under capture)
