@@ -206,10 +206,10 @@ __global__ void chol_inv_kernel(int p, double* __restrict__ H, double* __restric
   }
 }
 
-// Same factorisation for p <= kCholSmem with L in shared memory: right-looking
-// Cholesky (one barrier pair per column), then R^{-1} = (L^{-1})^T by forward
-// substitution, one thread per column of L^{-1} (= row of R^{-1}); the
-// retired-column rule is the global-memory version's.
+// Same factorisation when L and L^{-1} both fit in shared memory (2 p^2
+// doubles): right-looking Cholesky (one barrier pair per column), then
+// R^{-1} = (L^{-1})^T by right-looking forward substitution over the rows of
+// L^{-1}; the retired-column rule is the global-memory version's.
 constexpr int kCholSmem = 128;
 constexpr int kCholSmemBytes = 200 * 1024;  // L (+ L^{-1} when 2 p^2 doubles fit)
 __global__ void __launch_bounds__(1024) chol_inv_smem_kernel(int p, double* __restrict__ H) {
@@ -250,9 +250,9 @@ __global__ void __launch_bounds__(1024) chol_inv_smem_kernel(int p, double* __re
   __syncthreads();
   // X = L^{-1} by right-looking forward substitution over rows (all columns at
   // once); R^{-1} = X^T, retired columns of R^{-1} (rows of X) are zero.
-  const bool xs = 2 * p * p * static_cast<int>(sizeof(double)) <= kCholSmemBytes;
-  double* X = xs ? Ls + p * p : nullptr;
-  if (xs) {
+  // launched only when 2 p^2 doubles fit (cholqr2); larger p: chol_inv_fast_kernel
+  double* X = Ls + p * p;
+  {
     for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) X[idx] = (idx % p == idx / p) ? 1.0 : 0.0;
     __syncthreads();
     for (int i = 0; i < p; ++i) {
@@ -272,15 +272,88 @@ __global__ void __launch_bounds__(1024) chol_inv_smem_kernel(int p, double* __re
       const int r = idx % p, c = idx / p;  // H(r, c) = R^{-1}(r, c) = X(c, r)
       H[idx] = X[c + p * r];
     }
-  } else {
-    for (int c = threadIdx.x; c < p; c += blockDim.x) {  // one thread per column of L^{-1}
-      for (int i = 0; i < c; ++i) H[c + p * i] = 0.0;
-      for (int i = c; i < p; ++i) {
-        double s0 = (i == c) ? 1.0 : 0.0;
-        for (int k = c; k < i; ++k) s0 -= Ls[i + p * k] * H[c + p * k];
-        H[c + p * i] = dead[i] ? 0.0 : s0 / Ls[i + p * i];
-      }
+  }
+}
+
+// The same factorisation for p <= kCholSmem, tuned for latency: 512 threads
+// as (row i, group g) pairs, so the right-looking Cholesky update of column j
+// splits each row's trailing columns k = j+1+g, j+5+g, ... over four groups
+// (element-wise the same operations in the same j order as the kernels
+// above); then L^{-1} in place column by column from the last (LAPACK trti2
+// order: column j = -(inverted trailing block) x / l_jj, the row sums split
+// over the groups and combined in a fixed order).  R^{-1} = (D L^{-1})^T with
+// D zeroing the retired rows (their L columns are zero below a unit pivot, so
+// every other row of L^{-1} is unaffected).  Two barriers per column in each
+// phase instead of the row-at-a-time forward substitution.
+constexpr int kCF_ROWS = 128, kCF_GRP = 4;
+__global__ void __launch_bounds__(kCF_ROWS * kCF_GRP) chol_inv_fast_kernel(int p, double* __restrict__ H) {
+  extern __shared__ double Lf[];  // p x p, column-major
+  __shared__ double xs[kCF_ROWS];
+  __shared__ double part[kCF_GRP][kCF_ROWS];
+  __shared__ unsigned char dead[kCF_ROWS];
+  __shared__ double s_mx;
+  const int i = threadIdx.x % kCF_ROWS, grp = threadIdx.x / kCF_ROWS;
+  for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) Lf[idx] = H[idx];
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double mx = 0.0;
+    for (int q = threadIdx.x; q < p; q += 32) mx = fmax(mx, Lf[q + p * q]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (threadIdx.x == 0) s_mx = mx;
+  }
+  __syncthreads();
+  const double tiny = 1e-26 * s_mx;
+  const bool row = i < p;
+  for (int j = 0; j < p; ++j) {
+    __syncthreads();  // previous trailing update complete
+    const double d = Lf[j + p * j];
+    const bool dj = !(d > tiny);
+    const double djj = dj ? 1.0 : sqrt(d);
+    const double inv = 1.0 / djj;
+    if (grp == 0 && row && i > j) Lf[i + p * j] = dj ? 0.0 : Lf[i + p * j] * inv;
+    __syncthreads();  // column j scaled; every read of the pivot done
+    if (threadIdx.x == 0) {
+      dead[j] = dj;
+      Lf[j + p * j] = djj;
     }
+    if (!dj && row && i > j) {
+      // loads of a batch issued before its stores (the compiler cannot prove
+      // the column-j reads and the row-i writes disjoint)
+      const double lij = Lf[i + p * j];
+      int k = j + 1 + grp;
+      for (; k + 3 * kCF_GRP <= i; k += 4 * kCF_GRP) {
+        double c[4], r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          c[u] = Lf[k + u * kCF_GRP + p * j];
+          r[u] = Lf[i + p * (k + u * kCF_GRP)];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Lf[i + p * (k + u * kCF_GRP)] = r[u] - lij * c[u];
+      }
+      for (; k <= i; k += kCF_GRP) Lf[i + p * k] -= lij * Lf[k + p * j];
+    }
+  }
+  for (int j = p - 1; j >= 0; --j) {
+    __syncthreads();  // column j + 1 of the inverse written
+    const double ljj = Lf[j + p * j];
+    if (grp == 0 && row && i > j) xs[i] = Lf[i + p * j];
+    __syncthreads();
+    double acc = 0.0;
+    if (row && i > j) {
+#pragma unroll 4
+      for (int k = j + 1 + grp; k <= i; k += kCF_GRP) acc += Lf[i + p * k] * xs[k];
+    }
+    part[grp][i] = acc;
+    __syncthreads();
+    if (grp == 0 && row && i >= j)
+      Lf[i + p * j] = i == j ? 1.0 / ljj : -((part[0][i] + part[1][i]) + (part[2][i] + part[3][i])) / ljj;
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) {
+    const int r = idx % p, c = idx / p;  // H(r, c) = R^{-1}(r, c) = (D L^{-1})(c, r)
+    H[idx] = (c >= r && !dead[c]) ? Lf[c + p * r] : 0.0;
   }
 }
 
@@ -577,16 +650,25 @@ void cholqr2(tgb_ctx* ctx, int64_t d, int p, double* X, Dev& tmp) {
     dgemm(ctx, true, false, p, p, d, 1.0, X, d, X, d, 0.0, H, p);
     // H is written in place with R^{-1}; back substitution reads H's upper part as it goes,
     // so each column c only reads entries (k, c) with k > i that it already produced.
-    if (p <= kCholSmem && !getenv("TGB_CHOL_GLOBAL")) {
+    const size_t l_bytes = static_cast<size_t>(p) * p * sizeof(double);
+    if (p <= kCholSmem && 2 * l_bytes <= static_cast<size_t>(kCholSmemBytes)) {
+      // L and L^{-1} both in shared memory: the row-at-a-time kernel (96 vs 101 us at config 1's blocks)
       static bool cattr = false;
       if (!cattr) {
         TGB_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kCholSmemBytes));
         cattr = true;
       }
-      const size_t l_bytes = static_cast<size_t>(p) * p * sizeof(double);
-      const size_t bytes = 2 * l_bytes <= static_cast<size_t>(kCholSmemBytes) ? 2 * l_bytes : l_bytes;
-      chol_inv_smem_kernel<<<1, p > 64 ? 1024 : 512, bytes, ctx->stream>>>(p, H);
+      chol_inv_smem_kernel<<<1, p > 64 ? 1024 : 512, 2 * l_bytes, ctx->stream>>>(p, H);
+    } else if (p <= kCF_ROWS) {
+      // in-place inverse (0.21 vs 0.38 ms at p = 110-128, the TEI fit's ranks)
+      static bool fattr = false;
+      if (!fattr) {
+        TGB_CUDA(cudaFuncSetAttribute(chol_inv_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      kCF_ROWS * kCF_ROWS * static_cast<int>(sizeof(double))));
+        fattr = true;
+      }
+      chol_inv_fast_kernel<<<1, kCF_ROWS * kCF_GRP, l_bytes, ctx->stream>>>(p, H);
     } else {
       chol_inv_kernel<<<1, 256, 0, ctx->stream>>>(p, H, Wk);
     }
