@@ -13,6 +13,7 @@
 //     product-over-axes / sum-over-terms kernel;
 //   the TEI pivoted Cholesky (tei.cpp:48-90,198-204) as a host-driven loop of
 //     device steps (argmax, column, downdate).
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -214,6 +215,182 @@ __global__ void __launch_bounds__(kRedThreads) pivchol_explicit3_kernel(PivBatch
                                                                         double neg_tol) {
   const PivAxis& a = b.ax[blockIdx.x];
   pivchol_explicit_body(a.n, a.A, tol, trace_stop, a.cap, neg_tol, a.diag, a.L, a.pivots, a.info, a.residual);
+}
+
+// The three fitting Choleskys as ONE cooperative grid: G CTAs per axis own
+// contiguous row blocks; per step each CTA forms its rows of the pivot column
+// (the same sequential r order as pivchol_explicit_body, so L is identical),
+// downdates its diagonal and publishes (argmax, sum, flags) partials; after
+// one grid barrier every CTA reduces all partials in CTA order and so takes
+// the same next pivot / stop decision for all three axes (no second barrier).
+// Partials are double-buffered by step parity.  The single-CTA body read
+// L (n x rank) through one SM per axis: bandwidth-bound at ~4.6 ms for the
+// config-3 fit.
+constexpr int kCoopThreads = 128;
+__device__ __forceinline__ double4 ldcg4(const double4* p) {  // L2 load (written by other CTAs in this grid)
+  const double2 lo = __ldcg(reinterpret_cast<const double2*>(p));
+  const double2 hi = __ldcg(reinterpret_cast<const double2*>(p) + 1);
+  return make_double4(lo.x, lo.y, hi.x, hi.y);
+}
+struct CoopAxis {
+  int rank, p, active, err, clamped;
+  double dm, max0, trace0, target, meas;
+};
+// one warp reduces one axis' G <= 64 partials: (argmax, sum, flag OR); the
+// shuffle tree is fixed, so every CTA obtains bit-identical results
+__device__ __forceinline__ void coop_reduce(const double4* __restrict__ pa, int G, double& dm, int& p, double& ds,
+                                            int& fl) {
+  const int lane = threadIdx.x & 31;
+  dm = -INFINITY;
+  p = 0x7fffffff;
+  ds = 0.0;
+  fl = 0;
+  for (int q = lane; q < G; q += 32) {
+    const double4 v = ldcg4(pa + q);
+    argmax_combine(dm, p, v.x, static_cast<int>(v.y));
+    ds += v.z;
+    fl |= static_cast<int>(v.w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, dm, o);
+    const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+    argmax_combine(dm, p, v2, p2);
+    ds += __shfl_xor_sync(0xffffffffu, ds, o);
+    fl |= __shfl_xor_sync(0xffffffffu, fl, o);
+  }
+}
+__global__ void __launch_bounds__(kCoopThreads) pivchol_coop3_kernel(PivBatch b, int G, double tol, int trace_stop,
+                                                                     double neg_tol, double4* __restrict__ part) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double s_lp[];  // L[p, :rank] of this CTA's axis
+  __shared__ CoopAxis S[3];
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  const int a = blockIdx.x / G, g = blockIdx.x % G, tid = threadIdx.x;
+  const PivAxis& X = b.ax[a];
+  const int n = X.n;
+  const int i0 = static_cast<int>((static_cast<int64_t>(n) * g) / G);
+  const int i1 = static_cast<int>((static_cast<int64_t>(n) * (g + 1)) / G);
+  double* __restrict__ L = X.L;
+  double* __restrict__ diag = X.diag;
+  // diagonal, its max and trace
+  {
+    double lm = -INFINITY, ls = 0.0;
+    int li = 0x7fffffff;
+    for (int i = i0 + tid; i < i1; i += blockDim.x) {
+      const double d = __ldg(X.A + i + static_cast<int64_t>(n) * i);
+      diag[i] = d;
+      argmax_combine(lm, li, d, i);
+      ls += d;
+    }
+    block_argmax(lm, li, sv, si);
+    ls = block_sum(ls, sv);
+    if (tid == 0) part[(0 * 3 + a) * G + g] = make_double4(lm, static_cast<double>(li), ls, 0.0);
+  }
+  grid.sync();
+  if (tid < 96) {  // warp ax reduces axis ax
+    const int ax = tid >> 5;
+    double dm, ds;
+    int p, fl;
+    coop_reduce(part + (0 * 3 + ax) * G, G, dm, p, ds, fl);
+    if ((tid & 31) == 0) {
+      CoopAxis& c = S[ax];
+      c.rank = 0;
+      c.err = 0;
+      c.clamped = 0;
+      c.max0 = dm;
+      c.trace0 = ds;
+      c.target = tol * (trace_stop ? ds : dm);
+      c.dm = dm;
+      c.p = p;
+      c.meas = trace_stop ? ds : dm;
+      c.active = dm > 0.0 && b.ax[ax].cap > 0 && !(c.meas <= c.target || dm <= 0.0);
+    }
+  }
+  __syncthreads();
+  for (int step = 1;; ++step) {
+    if (!(S[0].active || S[1].active || S[2].active)) break;
+    const int buf = step & 1;
+    if (S[a].active) {
+      const int rank = S[a].rank, pp = S[a].p;
+      const double piv = sqrt(S[a].dm), max0 = S[a].max0;
+      if (g == 0 && tid == 0) X.pivots[rank] = pp;
+      for (int r = tid; r < rank; r += blockDim.x) s_lp[r] = __ldcg(L + pp + static_cast<int64_t>(n) * r);
+      __syncthreads();
+      double lm = -INFINITY, ls = 0.0;
+      int li = 0x7fffffff, bad = 0, cl = 0;
+      for (int i = i0 + tid; i < i1; i += blockDim.x) {
+        double c = __ldg(X.A + i + static_cast<int64_t>(n) * pp);
+        // the rank-long dot product in the sequential r order, its L2 loads issued 32 at a time
+        const double* Li = L + i;
+        int r = 0;
+        for (; r + 32 <= rank; r += 32) {
+          double lv[32];
+#pragma unroll
+          for (int u = 0; u < 32; ++u) lv[u] = __ldcg(Li + static_cast<int64_t>(n) * (r + u));
+#pragma unroll
+          for (int u = 0; u < 32; ++u) c -= lv[u] * s_lp[r + u];
+        }
+        for (; r + 8 <= rank; r += 8) {
+          double lv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) lv[u] = __ldcg(Li + static_cast<int64_t>(n) * (r + u));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) c -= lv[u] * s_lp[r + u];
+        }
+        for (; r < rank; ++r) c -= __ldcg(Li + static_cast<int64_t>(n) * r) * s_lp[r];
+        double l = c / piv;
+        if (i == pp) l = piv;
+        L[i + static_cast<int64_t>(n) * rank] = l;
+        double d = diag[i] - l * l;
+        if (i == pp) d = 0.0;
+        if (d < 0.0) {
+          if (d < -neg_tol * max0) bad = 1;
+          d = 0.0;
+          cl = 1;
+        }
+        diag[i] = d;
+        argmax_combine(lm, li, d, i);
+        ls += d;
+      }
+      bad = __syncthreads_or(bad);
+      cl = __syncthreads_or(cl);
+      block_argmax(lm, li, sv, si);
+      ls = block_sum(ls, sv);
+      if (tid == 0) part[(buf * 3 + a) * G + g] = make_double4(lm, static_cast<double>(li), ls, 2.0 * bad + cl);
+    }
+    grid.sync();
+    if (tid < 96 && S[tid >> 5].active) {  // warp-uniform
+      const int ax = tid >> 5;
+      double dm, ds;
+      int p, fl;
+      coop_reduce(part + (buf * 3 + ax) * G, G, dm, p, ds, fl);
+      if ((tid & 31) == 0) {
+        CoopAxis& c = S[ax];
+        c.clamped |= fl & 1;
+        c.rank += 1;
+        c.dm = dm;
+        c.p = p;
+        c.meas = trace_stop ? ds : dm;
+        if (fl & 2) {
+          c.err = 1;
+          c.active = 0;
+        } else if (c.rank >= b.ax[ax].cap || c.meas <= c.target || dm <= 0.0) {
+          c.active = 0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (g == 0 && tid == 0) {
+    const CoopAxis& c = S[a];
+    X.info[0] = c.rank;
+    X.info[1] = c.clamped;
+    X.info[2] = c.err;
+    X.residual[0] = c.max0 > 0.0 ? c.meas / (trace_stop ? c.trace0 : c.max0) : 0.0;
+  }
 }
 
 // partial sums of (G - T)^2 and G^2 (fit residual, tei.cpp:140-141)
@@ -730,8 +907,28 @@ void tei_fit(tgb_ctx* ctx, TEI& f, const tgb_cp& basis_dev, const int64_t* fn_of
                         info[ax]};
   }
   // phase 2: the three pivoted Choleskys (tei.cpp:125-129, trace stop at eps_fit^2) concurrently
-  pivchol_explicit3_kernel<<<3, kRedThreads, 0, ctx->stream>>>(pb, eps_fit * eps_fit, 1, 1e-12);
-  TGB_LAUNCHED(ctx);
+  {
+    int nmax = 1, capmax = 1;
+    for (int ax = 0; ax < 3; ++ax) {
+      nmax = std::max(nmax, pb.ax[ax].n);
+      capmax = std::max(capmax, pb.ax[ax].cap);
+    }
+    const size_t lp_bytes = static_cast<size_t>(capmax) * sizeof(double);
+    int per_sm = 0;
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pivchol_coop3_kernel, kCoopThreads, lp_bytes));
+    int G = std::min<int>(ctx->num_sms / 3, (nmax + 63) / 64);
+    if (lp_bytes <= 48 * 1024 && per_sm >= 1 && G >= 2 && !getenv("TGB_FIT_SINGLE_CTA")) {
+      auto* part = static_cast<double4*>(ctx->ws_misc2.get(static_cast<size_t>(2 * 3 * G) * sizeof(double4)));
+      double tol2 = eps_fit * eps_fit, neg = 1e-12;
+      int trace = 1;
+      void* args[] = {&pb, &G, &tol2, &trace, &neg, &part};
+      TGB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(pivchol_coop3_kernel), dim3(3 * G),
+                                           dim3(kCoopThreads), args, lp_bytes, ctx->stream));
+    } else {
+      pivchol_explicit3_kernel<<<3, kRedThreads, 0, ctx->stream>>>(pb, eps_fit * eps_fit, 1, 1e-12);
+    }
+    TGB_LAUNCHED(ctx);
+  }
   int hinfo[3][4];
   for (int ax = 0; ax < 3; ++ax)
     TGB_CUDA(cudaMemcpyAsync(hinfo[ax], info[ax], 3 * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
