@@ -437,6 +437,41 @@ __global__ void tei_diag_term_kernel(int nc, const int* __restrict__ cstart, con
   acc[c] += s;
 }
 
+// All kernel terms at once when every Y_k = V M_k^T is stored (Pk): grid.y = k,
+// s[k nc + c] = tei_diag_term_kernel's per-term sum; tei_diag_sum_kernel then
+// adds the terms in k order, so diag is bit-identical to the per-term launches.
+__global__ void tei_diag_terms_kernel(int nc, const int* __restrict__ cstart, const int* __restrict__ cpairs,
+                                      const double* __restrict__ cw, int64_t np2, const double* __restrict__ V0,
+                                      const double* __restrict__ V1, const double* __restrict__ V2, int r0, int r1,
+                                      int r2, const double* __restrict__ P0, const double* __restrict__ P1,
+                                      const double* __restrict__ P2, double* __restrict__ s_out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  const int64_t k = blockIdx.y;
+  const double* Y0 = P0 + np2 * r0 * k;
+  const double* Y1 = P1 + np2 * r1 * k;
+  const double* Y2 = P2 + np2 * r2 * k;
+  double s = 0.0;
+  for (int a = cstart[c]; a < cstart[c + 1]; ++a)
+    for (int b = cstart[c]; b < cstart[c + 1]; ++b) {
+      const int j = cpairs[a], j2 = cpairs[b];
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0;
+      for (int q = 0; q < r0; ++q) d0 += V0[j2 + np2 * q] * Y0[j + np2 * q];
+      for (int q = 0; q < r1; ++q) d1 += V1[j2 + np2 * q] * Y1[j + np2 * q];
+      for (int q = 0; q < r2; ++q) d2 += V2[j2 + np2 * q] * Y2[j + np2 * q];
+      s += cw[a] * cw[b] * (d0 * d1 * d2);
+    }
+  s_out[k * nc + c] = s;
+}
+
+__global__ void tei_diag_sum_kernel(int nc, int K, const double* __restrict__ s_in, double* __restrict__ acc) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= nc) return;
+  double v = acc[c];
+  for (int k = 0; k < K; ++k) v += s_in[static_cast<int64_t>(k) * nc + c];
+  acc[c] = v;
+}
+
 // col[i] = sum_k prod_ax W_ax[i, k]   (b_prim_column, tei.cpp:33-44)
 __global__ void tei_col_combine_kernel(int64_t np2, int K, const double* __restrict__ W0,
                                        const double* __restrict__ W1, const double* __restrict__ W2,
@@ -456,6 +491,7 @@ __global__ void gather_row_kernel(const double* __restrict__ V, int64_t np2, int
 
 // contraction: out[owner[p] + nb owner[q]] += pw[p] pw[q] z[p + np q]  (tei.cpp:166-172),
 // as a gather over contracted pairs (deterministic order p-major within q as the reference loop)
+template <bool COHERENT = false>
 __device__ __forceinline__ double contract_at(int c, int nb, int np, const int* __restrict__ fstart,
                                               const double* __restrict__ pw, const double* __restrict__ z) {
   const int mu = c % nb, nu = c / nb;
@@ -464,7 +500,7 @@ __device__ __forceinline__ double contract_at(int c, int nb, int np, const int* 
   for (int q = fstart[b]; q < fstart[b + 1]; ++q)
     for (int p = fstart[a]; p < fstart[a + 1]; ++p) {
       const int64_t idx = mu <= nu ? p + static_cast<int64_t>(np) * q : q + static_cast<int64_t>(np) * p;
-      s += pw[p] * pw[q] * z[idx];
+      s += pw[p] * pw[q] * (COHERENT ? __ldcg(z + idx) : z[idx]);
     }
   return s;
 }
@@ -674,20 +710,18 @@ __device__ __forceinline__ void dmma_cd(double (&c)[4], double a0, double a1, do
 // vs 14.5 us per column at config 3); the axis products meet in shared
 // memory and the row sums reduce in a fixed order (lanes t, tiles, warps).
 constexpr int kCD2_THREADS = 192;
-__global__ void __launch_bounds__(kCD2_THREADS) chol_col_dmma_kernel(int64_t np2, int K, const int* __restrict__ rr,
-                                                                     const double* const* __restrict__ V,
-                                                                     const double* const* __restrict__ Y,
-                                                                     const CholState* st, int init,
-                                                                     double* __restrict__ z) {
-  if (st->done) return;
-  __shared__ double part[2][16][kCD_COLS + 1];  // axes 1 and 2: [row][col] of the 16 x 48 tile
-  __shared__ double red[2][16][2];
+// One 16-row tile (rows i0 .. i0 + 15) of the column; COHERENT: y was written
+// earlier in the same (cooperative) grid, so it is read through L2 only.
+template <bool COHERENT>
+__device__ __forceinline__ void col_dmma_tile(int64_t np2, int K, const int* __restrict__ rr,
+                                              const double* const* __restrict__ V, const double* const* Y,
+                                              int64_t i0, int init, double w, double* __restrict__ z,
+                                              double (&part)[2][16][kCD_COLS + 1], double (&red)[2][16][2]) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int ax = warp >> 1, nt0 = (warp & 1) * 3;
   const int r = rr[ax];
   const double* __restrict__ Va = V[ax];
-  const double* __restrict__ Ya = Y[ax];
-  const int64_t i0 = blockIdx.x * 16LL;
+  const double* Ya = Y[ax];
   const bool in0 = i0 + g < np2, in1 = i0 + g + 8 < np2;
   const double* va = Va + i0 + g;
   int64_t yb[3];
@@ -712,7 +746,8 @@ __global__ void __launch_bounds__(kCD2_THREADS) chol_col_dmma_kernel(int64_t np2
     const double a1 = (qin && in1) ? __ldg(va + vq + 8) : 0.0;
     double b[3];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) b[j] = (qin && cin[j]) ? __ldg(Ya + q + yb[j]) : 0.0;
+    for (int j = 0; j < 3; ++j)
+      b[j] = (qin && cin[j]) ? (COHERENT ? __ldcg(Ya + q + yb[j]) : __ldg(Ya + q + yb[j])) : 0.0;
 #pragma unroll
     for (int j = 0; j < 3; ++j) dmma_cd(acc[j], a0, a1, b[j]);
   }
@@ -750,10 +785,190 @@ __global__ void __launch_bounds__(kCD2_THREADS) chol_col_dmma_kernel(int64_t np2
     const int hh = tid >> 3, gg = tid & 7;
     const double sum = red[0][gg][hh] + red[1][gg][hh];  // n tiles 0-2, then 3-5
     const int64_t i = i0 + tid;
-    if (i < np2) {
-      const double w = st->w;
-      z[i] = init ? w * sum : (w != 0.0 ? z[i] + w * sum : z[i]);
+    if (i < np2) z[i] = init ? w * sum : (w != 0.0 ? (COHERENT ? __ldcg(z + i) : z[i]) + w * sum : z[i]);
+  }
+  __syncthreads();  // part / red reusable
+}
+
+__global__ void __launch_bounds__(kCD2_THREADS) chol_col_dmma_kernel(int64_t np2, int K, const int* __restrict__ rr,
+                                                                     const double* const* __restrict__ V,
+                                                                     const double* const* __restrict__ Y,
+                                                                     const CholState* st, int init,
+                                                                     double* __restrict__ z) {
+  if (st->done) return;
+  __shared__ double part[2][16][kCD_COLS + 1];  // axes 1 and 2: [row][col] of the 16 x 48 tile
+  __shared__ double red[2][16][2];
+  col_dmma_tile<false>(np2, K, rr, V, Y, blockIdx.x * 16LL, init, st->w, z, part, red);
+}
+
+// ---- The whole TEI pivoted Cholesky (tei.cpp:198-204 with pivoted_cholesky
+// :48-90) as ONE cooperative grid: per step, every CTA reduces the previous
+// step's (argmax, flags) partials itself in a fixed order (identical pivot and
+// stop decisions everywhere), the grid gathers y_k (rows of the stored
+// V M_k^T), forms the column with the DMMA tiles, then downdates its rows of
+// L and the diagonal with the contraction inline — three grid barriers per
+// step and no host or graph launches in the loop.  The per-row arithmetic is
+// chol_col_dmma_kernel's and chol_step_dev_kernel's, in the same order, so L,
+// the pivots and R_B are those of the graph-replayed loop.
+struct TeiCoopArgs {
+  int64_t np2;
+  int nb, np, K, cap, max_terms;
+  int r[3];
+  const double* V[3];
+  const double* Pk[3];
+  double* Y[3];
+  const int* fstart;
+  const double* pw;
+  double *z, *L, *diag;
+  int64_t* piv_list;
+  double target, max0, neg_tol;
+  double4* part;  // [2][gridDim]
+  CholState* st;  // out: rank, done, flags[1]
+};
+constexpr int kTC_ROWS = kCD2_THREADS / kCholParts;  // 24 downdate rows per pass
+__global__ void __launch_bounds__(kCD2_THREADS, 3) tei_chol_coop_kernel(TeiCoopArgs A) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ double tpart[2][16][kCD_COLS + 1];
+  __shared__ double tred[2][16][2];
+  __shared__ double dpart[kCholParts][kTC_ROWS];
+  __shared__ double sv[32];
+  __shared__ int si[32];
+  __shared__ int s_rank, s_p, s_done, s_err, s_j;
+  __shared__ double s_dm, s_w;
+  const int tid = threadIdx.x, nblk = gridDim.x;
+  const int64_t n = A.nb * static_cast<int64_t>(A.nb);
+  const int64_t np2 = A.np2;
+  const int ntiles = static_cast<int>((np2 + 15) / 16);
+  const int64_t gthreads = static_cast<int64_t>(nblk) * blockDim.x;
+  // partial argmax of the initial diagonal
+  {
+    double lm = -INFINITY;
+    int li = 0x7fffffff;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid; i < n; i += gthreads)
+      argmax_combine(lm, li, A.diag[i], static_cast<int>(i));
+    block_argmax(lm, li, sv, si);
+    if (tid == 0) A.part[blockIdx.x] = make_double4(lm, static_cast<double>(li), 0.0, 0.0);
+  }
+  grid.sync();
+  if (tid < 32) {
+    double dm, ds;
+    int p, fl;
+    coop_reduce(A.part, nblk, dm, p, ds, fl);
+    if (tid == 0) {
+      s_rank = 0;
+      s_err = 0;
+      s_dm = dm;
+      s_p = p;
+      s_done = A.cap <= 0 || dm <= A.target || dm <= 0.0;  // chol_pivot_kernel's stop rule
     }
+  }
+  __syncthreads();
+  for (int step = 1;; ++step) {
+    if (s_done) break;
+    const int buf = step & 1;
+    const int rank = s_rank, pp = s_p;
+    if (blockIdx.x == 0 && tid == 0) A.piv_list[rank] = pp;
+    for (int t = 0; t < A.max_terms; ++t) {
+      __syncthreads();  // s_w / s_j of the previous term read
+      if (tid == 0) {  // chol_term
+        const int kappa = pp % A.nb, lambda = pp / A.nb;
+        const int nk = A.fstart[kappa + 1] - A.fstart[kappa], nl = A.fstart[lambda + 1] - A.fstart[lambda];
+        if (t >= nk * nl) {
+          s_w = 0.0;
+        } else {
+          const int p = A.fstart[kappa] + t % nk, q = A.fstart[lambda] + t / nk;
+          s_j = p + A.np * q;
+          s_w = A.pw[p] * A.pw[q];
+        }
+      }
+      __syncthreads();
+      const double w = s_w;
+      if (w == 0.0) continue;  // grid-uniform: no term, z unchanged
+      const int64_t j = s_j;
+      // y_ax[e] = Pk_ax[j + np2 e], e < r_ax K, spread over the grid
+      for (int ax = 0; ax < 3; ++ax) {
+        const int64_t cnt = static_cast<int64_t>(A.r[ax]) * A.K;
+        const double* src = A.Pk[ax] + j;
+        for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + tid; e < cnt; e += gthreads)
+          A.Y[ax][e] = __ldg(src + np2 * e);
+      }
+      grid.sync();
+      for (int mt = blockIdx.x; mt < ntiles; mt += nblk)
+        col_dmma_tile<true>(np2, A.K, A.r, A.V, A.Y, mt * 16LL, t == 0 ? 1 : 0, w, A.z, tpart, tred);
+      grid.sync();
+    }
+    // downdate (chol_step_dev_kernel's arithmetic): rows in passes of kTC_ROWS, kCholParts partial sums each
+    const double piv = sqrt(s_dm);
+    double lm = -INFINITY;
+    int li = 0x7fffffff, bad = 0, cl = 0;
+    const int row = tid % kTC_ROWS, grp = tid / kTC_ROWS;
+    for (int64_t r0 = blockIdx.x * static_cast<int64_t>(kTC_ROWS); r0 < n; r0 += static_cast<int64_t>(nblk) * kTC_ROWS) {
+      const int64_t i = r0 + row;
+      double acc = 0.0;
+      if (i < n) {
+        // the same r order as chol_step_dev_kernel; loads issued 8 terms at a time
+        int r = grp;
+        for (; r + 7 * kCholParts < rank; r += 8 * kCholParts) {
+          double lv[8], pv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            lv[u] = __ldcg(A.L + i + n * (r + u * kCholParts));
+            pv[u] = __ldcg(A.L + pp + n * (r + u * kCholParts));
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) acc += lv[u] * pv[u];
+        }
+        for (; r < rank; r += kCholParts) acc += __ldcg(A.L + i + n * r) * __ldcg(A.L + pp + n * r);
+      }
+      dpart[grp][row] = acc;
+      __syncthreads();
+      if (grp == 0 && i < n) {
+        double dd = 0.0;
+        for (int g2 = 0; g2 < kCholParts; ++g2) dd += dpart[g2][row];
+        const double c = contract_at<true>(static_cast<int>(i), A.nb, A.np, A.fstart, A.pw, A.z) - dd;
+        double l = c / piv;
+        if (i == pp) l = piv;
+        A.L[i + n * rank] = l;
+        double d = A.diag[i] - l * l;
+        if (i == pp) d = 0.0;
+        if (d < 0.0) {
+          if (d < -A.neg_tol * A.max0) bad = 1;
+          d = 0.0;
+          cl = 1;
+        }
+        A.diag[i] = d;
+        argmax_combine(lm, li, d, static_cast<int>(i));
+      }
+      __syncthreads();
+    }
+    bad = __syncthreads_or(bad);
+    cl = __syncthreads_or(cl);
+    block_argmax(lm, li, sv, si);
+    if (tid == 0) A.part[buf * nblk + blockIdx.x] = make_double4(lm, static_cast<double>(li), 0.0, 2.0 * bad + cl);
+    grid.sync();
+    if (tid < 32) {
+      double dm, ds;
+      int p, fl;
+      coop_reduce(A.part + buf * nblk, nblk, dm, p, ds, fl);
+      if (tid == 0) {
+        s_rank = rank + 1;
+        if (fl & 2) {
+          s_err = 1;
+          s_done = 1;
+        } else {
+          s_dm = dm;
+          s_p = p;
+          s_done = s_rank >= A.cap || dm <= A.target || dm <= 0.0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    A.st->rank = s_rank;
+    A.st->done = 1;
+    A.st->flags[1] = s_err;
   }
 }
 
@@ -1042,10 +1257,30 @@ void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
     Y[ax] = static_cast<double*>(ybuf[ax].get(std::max<int64_t>(1, np2 * f.R[ax]) * sizeof(double)));
     if (f.have_pk) f.Pk[ax].get(std::max<size_t>(8, static_cast<size_t>(np2) * f.R[ax] * f.K * sizeof(double)));
   }
+  if (f.have_pk) {  // every Y_k first, then all terms in one launch and a k-ordered sum
+    // [Y_0 | Y_1 | ...] = V [M_0^T | M_1^T | ...] = V Mst^T: one GEMM per axis (same per-element k order
+    // as one GEMM per term)
+    for (int ax = 0; ax < 3; ++ax) {
+      const int64_t r = f.R[ax];
+      if (r == 0) continue;
+      dgemm(ctx, false, true, np2, r * f.K, r, 1.0, dptr(f.V[ax]), np2, dptr(f.Mst[ax]), r * f.K, 0.0,
+            dptr(f.Pk[ax]), np2);
+    }
+    static thread_local DevBuf sbuf;
+    auto* sk = static_cast<double*>(sbuf.get(std::max<size_t>(8, static_cast<size_t>(f.K) * nc * sizeof(double))));
+    tei_diag_terms_kernel<<<dim3((nc + 127) / 128, static_cast<unsigned>(f.K)), 128, 0, ctx->stream>>>(
+        nc, static_cast<const int*>(f.d_cstart.p), static_cast<const int*>(f.d_cpairs.p),
+        static_cast<const double*>(f.d_cw.p), np2, dptr(f.V[0]), dptr(f.V[1]), dptr(f.V[2]),
+        static_cast<int>(f.R[0]), static_cast<int>(f.R[1]), static_cast<int>(f.R[2]), dptr(f.Pk[0]), dptr(f.Pk[1]),
+        dptr(f.Pk[2]), sk);
+    TGB_LAUNCHED(ctx);
+    tei_diag_sum_kernel<<<(nc + 255) / 256, 256, 0, ctx->stream>>>(nc, static_cast<int>(f.K), sk, diag);
+    TGB_LAUNCHED(ctx);
+    return;
+  }
   for (int64_t k = 0; k < f.K; ++k) {
     for (int ax = 0; ax < 3; ++ax) {
       const int64_t r = f.R[ax];
-      if (f.have_pk) Y[ax] = dptr(f.Pk[ax]) + np2 * r * k;
       if (r == 0) continue;
       // Y = V M_k^T
       dgemm(ctx, false, true, np2, r, r, 1.0, dptr(f.V[ax]), np2, dptr(f.M[ax]) + r * r * k, r, 0.0, Y[ax], np2);
@@ -1255,6 +1490,53 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
                                           static_cast<const double*>(f.d_pw.p), z, L, dg, st);
     TGB_LAUNCHED(ctx);
   };
+  // the whole loop as one cooperative grid when the y_k come from the stored V M_k^T and the column fits
+  // the DMMA tile (config 3); otherwise the graph-replayed step below
+  if (dmma_col && f.have_pk && !getenv("TGB_TEI_GRAPH")) {
+    int per_sm = 0;
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tei_chol_coop_kernel, kCD2_THREADS, 0));
+    if (per_sm >= 1) {
+      const int nblk = ctx->num_sms * std::min(per_sm, 3);
+      TeiCoopArgs a{};
+      a.np2 = np2;
+      a.nb = static_cast<int>(nb);
+      a.np = static_cast<int>(np);
+      a.K = static_cast<int>(K);
+      a.cap = cap;
+      a.max_terms = max_terms;
+      for (int ax = 0; ax < 3; ++ax) {
+        a.r[ax] = static_cast<int>(f.R[ax]);
+        a.V[ax] = dptr(f.V[ax]);
+        a.Pk[ax] = dptr(f.Pk[ax]);
+        a.Y[ax] = Y[ax];
+      }
+      a.fstart = static_cast<const int*>(f.d_fstart.p);
+      a.pw = static_cast<const double*>(f.d_pw.p);
+      a.z = z;
+      a.L = L;
+      a.diag = dg;
+      a.piv_list = piv;
+      a.target = target;
+      a.max0 = max0;
+      a.neg_tol = 1e-10;  // tei.cpp:202
+      a.part = static_cast<double4*>(ctx->ws_misc3.get(static_cast<size_t>(2 * nblk) * sizeof(double4)));
+      a.st = st;
+      void* args[] = {&a};
+      TGB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tei_chol_coop_kernel), dim3(nblk),
+                                           dim3(kCD2_THREADS), args, 0, ctx->stream));
+      TGB_LAUNCHED(ctx);
+      CholState hs{};
+      TGB_CUDA(cudaMemcpyAsync(&hs, st, sizeof(CholState), cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (hs.flags[1])
+        throw Error(TGB_NUMERICAL_ERROR, "pivoted_cholesky: negative diagonal beyond tolerance; matrix not PSD");
+      f.RB = hs.rank;
+      f.chol_piv.resize(hs.rank);
+      if (hs.rank)
+        TGB_CUDA(cudaMemcpy(f.chol_piv.data(), piv, hs.rank * sizeof(int64_t), cudaMemcpyDeviceToHost));
+      return;
+    }
+  }
   // one eager step sizes every workspace (no allocation may happen under capture)
   step();
   cudaGraph_t graph = nullptr;
