@@ -135,3 +135,26 @@ def test_tei_duplicates_do_not_raise_rank(ctx):
     tg.tei_density_fitting(f2, bs2, tg.discretize_basis(bs2), 1e-6)
     assert f1.fit_ranks() == (1, 1, 1) == f2.fit_ranks()
     assert max(f2.fit_residual) <= 1e-6
+
+
+@pytest.mark.parametrize("contracted", [False, True])
+def test_tei_cholesky_cooperative_matches_graph_loop(ctx, monkeypatch, contracted):
+    # the one-grid Cholesky and the graph-replayed 4-kernel step share their arithmetic:
+    # identical pivots, rank and L
+    rng = Rng(15)
+    cents = rng.uniform(6, -1.2, 1.2).reshape(2, 3)
+    bs = make_basis(48, 6.0, cents, ("s", "p") if not contracted else ("s",), rng, contracted=contracted)
+    kern = tg.kernel_tensor(bs.grid, tg.make_expsum(8, 0.9), False)
+    disc = tg.discretize_basis(bs)
+    out = []
+    for graph in (False, True):
+        if graph:
+            monkeypatch.setenv("TGB_TEI_GRAPH", "1")
+        fac = tg.TEIFactorization(ctx)
+        tg.tei_density_fitting(fac, bs, disc, 1e-6)
+        tg.tei_convolution_matrices(fac, kern)
+        tg.tei_cholesky(fac, 1e-8)
+        out.append((fac.rank_b(), list(fac.pivots), np.array(fac.chol)))
+    assert out[0][0] == out[1][0] > 1
+    assert out[0][1] == out[1][1]
+    assert np.array_equal(out[0][2], out[1][2])
