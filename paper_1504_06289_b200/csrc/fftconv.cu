@@ -84,6 +84,7 @@ struct ConvPlan {
   PlanArgs a{};
   bool direct = false;
   int threads = 0;
+  mutable int pair_threads[2] = {0, 0};  // generic pair kernel, per kernel-spectrum form (chosen at first launch)
   size_t smem = 0;
   DevBuf perm, inv, leader, tw, twpost, ph1, ph2, phase, spos, kf;
 };
@@ -1763,11 +1764,40 @@ static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, 
                                   static_cast<int>(ctx->smem_optin)));
     attr = true;
   }
+  // threads per CTA: the most busy butterfly lanes per SM — the pass balance times the CTAs the
+  // register file and shared memory admit (the plan's balance-only choice left one 224-thread
+  // CTA per SM at N = 1600: 1.71 vs 0.73 ms per exchange launch)
+  int& tt = pl.pair_threads[BREAL ? 1 : 0];
+  if (!tt) {
+    const PlanArgs& a = pl.a;
+    const int tmax = std::min(kMaxThreads, std::max(64, ((a.N / 8 + 31) / 32) * 32));
+    double best = -1.0;
+    tt = pl.threads;
+    const char* force = getenv("TGB_PAIR_THREADS");  // A/B override
+    for (int t = 64; t <= tmax; t += 32) {
+      int per = 0;
+      TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pair_kernel<R0, BREAL>, t, pl.smem));
+      if (per < 1) continue;
+      double useful = 0.0, slots = 0.0;
+      for (int p = 0; p < a.P; ++p) {
+        const double bf = p == 0 ? a.npl : static_cast<double>(a.N) / a.r[p];
+        const double cost = p == 0 ? 2.0 * a.r[p] : a.r[p];
+        useful += bf * cost;
+        slots += std::ceil(bf / t) * t * cost;
+      }
+      const double score = useful / slots * t * per;
+      if (score > best * 1.0001) {
+        best = score;
+        tt = t;
+      }
+    }
+    if (force && atoi(force) > 0) tt = atoi(force);
+  }
   int per_sm = 1;
-  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel<R0, BREAL>, pl.threads, pl.smem));
+  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel<R0, BREAL>, tt, pl.smem));
   const int grid = std::max(1, per_sm) * ctx->num_sms;
   prof_begin(ctx);
-  pair_kernel<R0, BREAL><<<grid, pl.threads, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);
+  pair_kernel<R0, BREAL><<<grid, tt, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);
   TGB_LAUNCHED(ctx);
   prof_end(ctx);
 }
