@@ -85,6 +85,7 @@ struct ConvPlan {
   bool direct = false;
   int threads = 0;
   mutable int pair_threads[2] = {0, 0};  // generic pair kernel, per kernel-spectrum form (chosen at first launch)
+  mutable int spec_threads = 0;          // generic spectrum kernel
   size_t smem = 0;
   DevBuf perm, inv, leader, tw, twpost, ph1, ph2, phase, spos, kf;
 };
@@ -1755,6 +1756,38 @@ void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const
   TGB_LAUNCHED(ctx);
 }
 
+// CTA width of a runtime-generic kernel: the most busy butterfly lanes per SM —
+// pass balance times the CTAs that registers and shared memory admit (the
+// plan's balance-only width left one 224-thread CTA per SM at N = 1600).
+// pair: the first pass runs the mirror-pair leaders (2 blocks each).
+template <class Kern>
+static int busy_width(const ConvPlan& pl, Kern kern, bool pair) {
+  const PlanArgs& a = pl.a;
+  const int tmax = std::min(kMaxThreads, std::max(64, ((a.N / 8 + 31) / 32) * 32));
+  double best = -1.0;
+  int tt = pl.threads;
+  for (int t = 64; t <= tmax; t += 32) {
+    int per = 0;
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, t, pl.smem));
+    if (per < 1) continue;
+    double useful = 0.0, slots = 0.0;
+    for (int p = 0; p < a.P; ++p) {
+      const double bf = (p == 0 && pair) ? a.npl : static_cast<double>(a.N) / a.r[p];
+      const double cost = (p == 0 && pair) ? 2.0 * a.r[p] : a.r[p];
+      useful += bf * cost;
+      slots += std::ceil(bf / t) * t * cost;
+    }
+    const double score = useful / slots * t * per;
+    if (score > best * 1.0001) {
+      best = score;
+      tt = t;
+    }
+  }
+  const char* force = getenv("TGB_PAIR_THREADS");  // A/B override
+  if (force && atoi(force) > 0) tt = atoi(force);
+  return tt;
+}
+
 template <int R0, bool BREAL>
 static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                         const PairEntry* dwork, const int* winfo, double* out) {
@@ -1764,35 +1797,8 @@ static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, 
                                   static_cast<int>(ctx->smem_optin)));
     attr = true;
   }
-  // threads per CTA: the most busy butterfly lanes per SM — the pass balance times the CTAs the
-  // register file and shared memory admit (the plan's balance-only choice left one 224-thread
-  // CTA per SM at N = 1600: 1.71 vs 0.73 ms per exchange launch)
   int& tt = pl.pair_threads[BREAL ? 1 : 0];
-  if (!tt) {
-    const PlanArgs& a = pl.a;
-    const int tmax = std::min(kMaxThreads, std::max(64, ((a.N / 8 + 31) / 32) * 32));
-    double best = -1.0;
-    tt = pl.threads;
-    const char* force = getenv("TGB_PAIR_THREADS");  // A/B override
-    for (int t = 64; t <= tmax; t += 32) {
-      int per = 0;
-      TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, pair_kernel<R0, BREAL>, t, pl.smem));
-      if (per < 1) continue;
-      double useful = 0.0, slots = 0.0;
-      for (int p = 0; p < a.P; ++p) {
-        const double bf = p == 0 ? a.npl : static_cast<double>(a.N) / a.r[p];
-        const double cost = p == 0 ? 2.0 * a.r[p] : a.r[p];
-        useful += bf * cost;
-        slots += std::ceil(bf / t) * t * cost;
-      }
-      const double score = useful / slots * t * per;
-      if (score > best * 1.0001) {
-        best = score;
-        tt = t;
-      }
-    }
-    if (force && atoi(force) > 0) tt = atoi(force);
-  }
+  if (!tt) tt = busy_width(pl, pair_kernel<R0, BREAL>, true);
   int per_sm = 1;
   TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel<R0, BREAL>, tt, pl.smem));
   const int grid = std::max(1, per_sm) * ctx->num_sms;
@@ -1907,8 +1913,9 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
     }
     return;
   }
-  spectrum_kernel<<<nA + nB, pl.threads, pl.smem, ctx->stream>>>(pl.a, A, nA, specA, B, colidx, nB, specB, specB2,
-                                                                  modeB, ldx, h);
+  if (!pl.spec_threads) pl.spec_threads = busy_width(pl, spectrum_kernel, false);
+  spectrum_kernel<<<nA + nB, pl.spec_threads, pl.smem, ctx->stream>>>(pl.a, A, nA, specA, B, colidx, nB, specB,
+                                                                       specB2, modeB, ldx, h);
   TGB_LAUNCHED(ctx);
 }
 
