@@ -23,6 +23,16 @@ namespace {
 constexpr int BM = 64, BN = 64, BK = 16, LDS_ = 68;  // LDS_ = 64 + 4: conflict-free fragment loads
 constexpr int GEMM_THREADS = 128;
 
+// A k-fastest staging pattern (A^T, or B not transposed) stores 16 k rows of
+// one column per half-warp: rows kk and kk + 4 land 8 kk words apart modulo
+// 32, a 4-way bank conflict.  XOR-ing the column's low two bits with kk / 4
+// spreads them; fragment loads read 4 consecutive kk (one kk / 4) and 4
+// consecutive columns per half-warp, which the XOR only permutes.
+template <bool KFAST>
+__device__ __forceinline__ int swz(int kk, int col) {
+  return KFAST ? col ^ ((kk >> 2) & 3) : col;
+}
+
 __device__ __forceinline__ void dmma16x8x4(double (&c)[4], double a0, double a1, double b0) {
   asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
@@ -87,7 +97,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
         kk = idx % BK;
         mm = idx / BK;
       }
-      As[buf][kk][mm] = ra[e];
+      As[buf][kk][swz<TA>(kk, mm)] = ra[e];
       int nn, kb;
       if (!TB) {
         kb = idx % BK;
@@ -96,7 +106,7 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
         nn = idx % BN;
         kb = idx / BN;
       }
-      Bs[buf][kb][nn] = rb[e];
+      Bs[buf][kb][swz<!TB>(kb, nn)] = rb[e];
     }
   };
 
@@ -120,11 +130,11 @@ __global__ void __launch_bounds__(GEMM_THREADS) dgemm_kernel(int M, int N, int K
       double a[2][2], b[4];
 #pragma unroll
       for (int i = 0; i < 2; ++i) {
-        a[i][0] = As[buf][k4 + t][wm + 16 * i + g];
-        a[i][1] = As[buf][k4 + t][wm + 16 * i + g + 8];
+        a[i][0] = As[buf][k4 + t][swz<TA>(k4 + t, wm + 16 * i + g)];
+        a[i][1] = As[buf][k4 + t][swz<TA>(k4 + t, wm + 16 * i + g + 8)];
       }
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][k4 + t][wn + 8 * j + g];
+      for (int j = 0; j < 4; ++j) b[j] = Bs[buf][k4 + t][swz<!TB>(k4 + t, wn + 8 * j + g)];
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
