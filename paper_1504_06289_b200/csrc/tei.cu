@@ -824,6 +824,7 @@ struct TeiCoopArgs {
   double target, max0, neg_tol;
   double4* part;  // [2][gridDim]
   CholState* st;  // out: rank, done, flags[1]
+  unsigned long long* phase;  // analysis (TGB_PHASE_CLK): CTA 0's cycles in gather / column / downdate / reduce
 };
 constexpr int kTC_ROWS = kCD2_THREADS / kCholParts;  // 24 downdate rows per pass
 __global__ void __launch_bounds__(kCD2_THREADS, 3) tei_chol_coop_kernel(TeiCoopArgs A) {
@@ -886,6 +887,7 @@ __global__ void __launch_bounds__(kCD2_THREADS, 3) tei_chol_coop_kernel(TeiCoopA
       const double w = s_w;
       if (w == 0.0) continue;  // grid-uniform: no term, z unchanged
       const int64_t j = s_j;
+      long long c0 = A.phase ? clock64() : 0;
       // y_ax[e] = Pk_ax[j + np2 e], e < r_ax K, spread over the grid
       for (int ax = 0; ax < 3; ++ax) {
         const int64_t cnt = static_cast<int64_t>(A.r[ax]) * A.K;
@@ -894,10 +896,16 @@ __global__ void __launch_bounds__(kCD2_THREADS, 3) tei_chol_coop_kernel(TeiCoopA
           A.Y[ax][e] = __ldg(src + np2 * e);
       }
       grid.sync();
+      long long c1 = A.phase ? clock64() : 0;
       for (int mt = blockIdx.x; mt < ntiles; mt += nblk)
         col_dmma_tile<true>(np2, A.K, A.r, A.V, A.Y, mt * 16LL, t == 0 ? 1 : 0, w, A.z, tpart, tred);
       grid.sync();
+      if (A.phase && blockIdx.x == 0 && tid == 0) {
+        A.phase[0] += static_cast<unsigned long long>(c1 - c0);
+        A.phase[1] += static_cast<unsigned long long>(clock64() - c1);
+      }
     }
+    long long c2 = A.phase ? clock64() : 0;
     // downdate (chol_step_dev_kernel's arithmetic): rows in passes of kTC_ROWS, kCholParts partial sums each
     const double piv = sqrt(s_dm);
     double lm = -INFINITY;
@@ -946,7 +954,13 @@ __global__ void __launch_bounds__(kCD2_THREADS, 3) tei_chol_coop_kernel(TeiCoopA
     cl = __syncthreads_or(cl);
     block_argmax(lm, li, sv, si);
     if (tid == 0) A.part[buf * nblk + blockIdx.x] = make_double4(lm, static_cast<double>(li), 0.0, 2.0 * bad + cl);
+    long long c3 = A.phase ? clock64() : 0;
     grid.sync();
+    if (A.phase && blockIdx.x == 0 && tid == 0) {
+      A.phase[2] += static_cast<unsigned long long>(c3 - c2);
+      A.phase[3] += static_cast<unsigned long long>(clock64() - c3);
+      A.phase[4] += 1;
+    }
     if (tid < 32) {
       double dm, ds;
       int p, fl;
@@ -1521,6 +1535,12 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
       a.neg_tol = 1e-10;  // tei.cpp:202
       a.part = static_cast<double4*>(ctx->ws_misc3.get(static_cast<size_t>(2 * nblk) * sizeof(double4)));
       a.st = st;
+      a.phase = nullptr;
+      static thread_local DevBuf phbuf;
+      if (getenv("TGB_PHASE_CLK")) {
+        a.phase = static_cast<unsigned long long*>(phbuf.get(8 * sizeof(unsigned long long)));
+        TGB_CUDA(cudaMemsetAsync(a.phase, 0, 8 * sizeof(unsigned long long), ctx->stream));
+      }
       void* args[] = {&a};
       TGB_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(tei_chol_coop_kernel), dim3(nblk),
                                            dim3(kCD2_THREADS), args, 0, ctx->stream));
@@ -1528,6 +1548,13 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
       CholState hs{};
       TGB_CUDA(cudaMemcpyAsync(&hs, st, sizeof(CholState), cudaMemcpyDeviceToHost, ctx->stream));
       TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (a.phase) {  // analysis only
+        unsigned long long h[8];
+        TGB_CUDA(cudaMemcpy(h, a.phase, sizeof(h), cudaMemcpyDeviceToHost));
+        const double ns = static_cast<double>(h[4] ? h[4] : 1);
+        fprintf(stderr, "tei coop cycles/step (CTA 0): gather+barrier %.0f column+barrier %.0f downdate %.0f "
+                "barrier+reduce wait %.0f (steps %llu)\n", h[0] / ns, h[1] / ns, h[2] / ns, h[3] / ns, h[4]);
+      }
       if (hs.flags[1])
         throw Error(TGB_NUMERICAL_ERROR, "pivoted_cholesky: negative diagonal beyond tolerance; matrix not PSD");
       f.RB = hs.rank;
