@@ -158,3 +158,14 @@ def test_tei_cholesky_cooperative_matches_graph_loop(ctx, monkeypatch, contracte
     assert out[0][0] == out[1][0] > 1
     assert out[0][1] == out[1][1]
     assert np.array_equal(out[0][2], out[1][2])
+
+
+def test_tei_many_kernel_terms(ctx):
+    # K = 2M+1 = 51 > 48 kernel columns: the column falls back to the SIMT kernel inside the
+    # graph-replayed step (the DMMA tile and the cooperative grid cover K <= 48)
+    rng = Rng(16)
+    cents = rng.uniform(6, -1.0, 1.0).reshape(2, 3)
+    bs = make_basis(48, 6.0, cents, ("s",), rng)
+    kern = tg.kernel_tensor(bs.grid, tg.make_expsum(25, 0.9), False)
+    assert kern.rank() == 51
+    run_case(ctx, bs, kern)
