@@ -232,7 +232,8 @@ def add(a: CanonicalTensor3, b: CanonicalTensor3) -> CanonicalTensor3:
     a.check_valid(), b.check_valid()
     if a.extents() != b.extents():
         raise InvalidArgument("add: extent mismatch")
-    return CanonicalTensor3([np.hstack([a.factor[ax], b.factor[ax]]) for ax in range(3)],
+    # Fortran-order result straight from the row stacks of the transposes (no C-order detour)
+    return CanonicalTensor3([np.concatenate([a.factor[ax].T, b.factor[ax].T], axis=0).T for ax in range(3)],
                             np.concatenate([a.weight, b.weight]))
 
 
