@@ -1,4 +1,4 @@
-# A/B of an env knob on the config-2 pair kernel: usage bash tools/ab_env.sh "TGB_NO_TWL=1"
+# A/B of an env knob on the config-2 pair kernel: usage bash tools/ab_env.sh "TGB_NO_FUSED=1"
 ALT="$1"
 timeout 600 python -m pytest tests -x -q -m gpu -k "conv or golden" 2>&1 | tail -1
 env $ALT timeout 600 python -m pytest tests -x -q -m gpu -k "conv or golden" 2>&1 | tail -1

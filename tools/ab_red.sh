@@ -1,4 +1,4 @@
-# A/B of an env knob on the rank reduction / TEI fit: usage bash tools/ab_red.sh "TGB_CHOL_V1=1"
+# A/B of an env knob on the rank reduction / TEI fit: usage bash tools/ab_red.sh "TGB_NO_SPLITK=1"
 ALT="$1"
 timeout 600 python -m pytest tests -x -q -m gpu -k "reduc or linalg or tei or hf or scf or golden" 2>&1 | tail -1
 env $ALT timeout 600 python -m pytest tests -x -q -m gpu -k "reduc or linalg or tei or hf or scf or golden" 2>&1 | tail -1
