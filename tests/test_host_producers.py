@@ -28,3 +28,25 @@ def test_reciprocal_expsum_bit_identical():
         assert (t.value, k.value) == (int(terms), int(ok)) and a.value == ach
         assert np.array_equal(r[:t.value], G[f"recip_{idx}_rates"]) and np.array_equal(w[:t.value],
                                                                                     G[f"recip_{idx}_weights"])
+
+
+def test_flatten_basis_and_add_layouts():
+    # host-side CP concatenations: Fortran-order factors, column order = function order
+    from paper_1504_06289_b200.inputs import basis_case
+    from paper_1504_06289_b200.tengrid import flatten_basis
+
+    bs, _ = basis_case(1, n=33)
+    disc = tg.discretize_basis(bs)
+    flat, offs = flatten_basis(disc)
+    for ax in range(3):
+        ref = np.hstack([d.factor[ax] for d in disc])
+        assert flat.factor[ax].flags["F_CONTIGUOUS"] and np.array_equal(flat.factor[ax], ref)
+    assert np.array_equal(flat.weight, np.concatenate([d.weight for d in disc]))
+    assert list(offs) == [0] + list(np.cumsum([d.rank() for d in disc]))
+    s = tg.add(disc[0], disc[1])
+    assert s.rank() == disc[0].rank() + disc[1].rank()
+    for ax in range(3):
+        assert s.factor[ax].flags["F_CONTIGUOUS"]
+        assert np.array_equal(s.factor[ax], np.hstack([disc[0].factor[ax], disc[1].factor[ax]]))
+    z = tg.add(tg.CanonicalTensor3.zero(disc[0].extents()), disc[0])
+    assert z.rank() == disc[0].rank()
