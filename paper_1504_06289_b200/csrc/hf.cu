@@ -416,11 +416,26 @@ void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_of
       for (int64_t m = m0; m <= m1; ++m) seg[m - m0] = RN * c0[m] - r0;
       const int64_t* dseg = upload(ctx, sseg, seg);
       double* T[3];
+      // the three axis GEMMs are independent: axis 2 runs on the aux stream so its wave tail
+      // overlaps axes 0-1 (only without split-K, whose workspace is shared)
+      const bool fork = ((rows + 63) / 64) * ((Gc + 63) / 64) >= ctx->num_sms && !getenv("TGB_EXCHANGE_SERIAL");
+      if (fork) {
+        TGB_CUDA(cudaEventRecord(ctx->aux_in, ctx->stream));
+        TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
+      }
       for (int ax = 0; ax < 3; ++ax) {
         T[ax] = st.p + ax * rows * Gc;
+        const bool on_aux = fork && ax == 2;
+        cudaStream_t main_stream = ctx->stream;
+        if (on_aux) ctx->stream = ctx->aux_stream;
         // T_ax (rows x Gc) = Y_ax(:, r0 : r0 + rows)^T GP_ax(:, 0 : Gc)
         dgemm(ctx, true, false, rows, Gc, basis.n[ax], 1.0, y[ax] + r0 * basis.n[ax], basis.n[ax], gp[ax],
               basis.n[ax], 0.0, T[ax], rows);
+        ctx->stream = main_stream;
+      }
+      if (fork) {
+        TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
+        TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
       }
       seg_triple_dot_kernel<<<dim3(static_cast<unsigned>(Gc), static_cast<unsigned>(m1 - m0)), 256, 0, ctx->stream>>>(
           rows, static_cast<int>(Gc), T[0], T[1], T[2], dwy + r0, dseg, ss.p);
