@@ -266,9 +266,23 @@ std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* co
     double* parts = work + off + 3 * static_cast<size_t>(chunk) * P;
     for (int c = 0; c < nch; ++c) {
       const int q0 = c * chunk, nq = std::min(chunk, RB - q0);
-      for (int ax = 0; ax < 3; ++ax)  // T_ax (nq x P) = B_ax(:, q0:q0+nq)^T L_ax
+      // axis 2 on the aux stream: its wave tail overlaps axes 0-1 (no split-K, whose workspace is shared)
+      const bool fork = ((nq + 63) / 64) * ((P + 63) / 64) >= ctx->num_sms;
+      if (fork) {
+        TGB_CUDA(cudaEventRecord(ctx->aux_in, ctx->stream));
+        TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
+      }
+      for (int ax = 0; ax < 3; ++ax) {  // T_ax (nq x P) = B_ax(:, q0:q0+nq)^T L_ax
+        cudaStream_t main_stream = ctx->stream;
+        if (fork && ax == 2) ctx->stream = ctx->aux_stream;
         dgemm(ctx, true, false, nq, P, n[ax], 1.0, B[ax] + static_cast<int64_t>(q0) * n[ax], n[ax], Lh[ax], n[ax], 0.0,
               T[ax], nq);
+        ctx->stream = main_stream;
+      }
+      if (fork) {
+        TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
+        TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
+      }
       triple_dot_kernel<<<dim3(static_cast<unsigned>(P), 1), 256, 0, ctx->stream>>>(nq, P, T[0], T[1], T[2], wb + q0,
                                                                                     parts + static_cast<size_t>(c) * P);
       TGB_LAUNCHED(ctx);
