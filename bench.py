@@ -7,12 +7,15 @@ FP64 convolutions of length 16385 per step.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One process per GPU (torchrun for N > 1).  The path partitions by rank pair
-with no data-path collective (output factors stay on their devices), so by
-default every rank convolves its own R_f = 500 density columns (a rank-specific
-shard of an N x 500-column seeded density): weak scaling, per-GPU work fixed.
-`--strong` instead shards the fixed 500 columns of config 2 across the ranks
-(the north star's 20,500 rank pairs split over 1/2/4/8 GPUs).  Rank 0 prints ONE
-JSON line.  The timed region is bracketed by a barrier and
+with no data-path collective (output factors stay on their devices).  By
+default config 2's fixed 500 density columns are sharded across the ranks
+(strong scaling: the north star's 20,500 rank pairs per axis split over
+1/2/4/8 GPUs, its 85 %-at-8 target); `--weak` instead gives every rank its own
+500 columns (a rank-specific shard of an N x 500-column seeded density).
+Rank 0 prints ONE JSON line.  The run fails (exit 3) if V_H at the 10^4
+seeded sample points differs from the reference's values
+(tests/golden/reference_cfg2_vh_samples.npz, computed by oracle/_ref over all
+61,500 convolutions) by more than 1e-10 relative max-norm.  The timed region is bracketed by a barrier and
 torch.cuda.synchronize() on both sides, timed with CUDA events on the libtgb
 context stream, max over ranks.
 
@@ -117,51 +120,106 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------- CPU reference arm
 
-def cpu_reference_sample(budget_s: float = 12.0, threads: int | None = None) -> dict:
-    """Time the reference's conv_central_many (proj/src/fft.cpp:97-122, the
-    per-column kernel of tg::convolve) on a bounded sample of the config-2
-    workload: one axis, `cols` density columns against kernel columns in
-    turn, all host threads.  Returns units/s (one unit = one windowed length-n
-    convolution, as in the GPU metric)."""
+def reference_inputs():
+    """Config 2's inputs built WITHOUT libtgb: the seeded density with numpy
+    (paper_1504_06289_b200.inputs.gaussian_density, pure Python), the Newton
+    kernel with the reference's own kernel_tensor (oracle/_ref, kernel.cpp:
+    182-203), so the reference arm loads only the reference's code."""
     import ctypes as C
 
     from oracle import oracle as O
-    from paper_1504_06289_b200.inputs import hartree_case
+    from paper_1504_06289_b200.inputs import KERNEL_C0, KERNEL_M, SEED_BASE, Rng, gaussian_density
+    from paper_1504_06289_b200.tengrid import Grid3
+
+    R = O.rlib()
+    n, b = N_GRID, 10.0
+    hh = 2.0 * b / float(n + 1)  # grid.cpp mesh size
+    grid = Grid3((n, n, n), (b, b, b), (hh, hh, hh))
+    theta, *_ = gaussian_density(grid, Rng(SEED_BASE + CFG), R_F, 0.05, 500.0)
+    if R is None:
+        return None, grid, theta, None
+    kt = O.OCP(lib=R)
+    bb = np.array([b, b, b])
+    rc = R.ref_kernel_tensor(C.c_void_p(bb.ctypes.data), (C.c_longlong * 3)(n, n, n), C.c_longlong(KERNEL_M[CFG]),
+                             C.c_double(KERNEL_C0[CFG]), C.c_int(0), kt.h)
+    if rc:
+        raise RuntimeError(R.ref_last_error().decode())
+    return R, grid, theta, kt.factors()[0]
+
+
+_REF_CACHE = {}
+
+
+def cpu_reference_sample(budget_s: float = 12.0, threads: int | None = None) -> dict:
+    """Time the reference's own CPU path for config 2 (oracle/_ref: fft.cpp
+    conv_central_many inside tg::convolve's loop, tensor.cpp:189-195): each
+    call convolves ALL 500 density columns with one kernel column (one kernel
+    FFT reused across the 500 columns, as in the reference), times h.  With
+    T threads the kernel-column loop is split across std::threads (SURVEY
+    §8d), one kernel column per thread per round; the sample is whole rounds
+    of axis 0 until the budget is spent.  A one-thread figure (one call)
+    is reported beside it.  Units = windowed length-n convolutions."""
+    import ctypes as C
 
     threads = threads or os.cpu_count() or 1
-    case = hartree_case(CFG, nsamples=1)
-    U = np.asfortranarray(case.theta.factor[0])
-    K = case.kernel.tensor.factor[0]
-    R = O.rlib()
-    kind = "reference" if R is not None else "port"
+    if "inputs" not in _REF_CACHE:
+        _REF_CACHE["inputs"] = reference_inputs()
+    R, grid, theta, K = _REF_CACHE["inputs"]
     n = N_GRID
-    cols = min(R_F, max(threads, 16))
-    out = np.zeros((n, cols), order="F")
-    Usub = np.asfortranarray(U[:, :cols])
+    U = np.asfortranarray(theta.factor[0])
+    ra = U.shape[1]
+    if R is None:  # restatement (port) fallback: one column loop on the oracle
+        from oracle import oracle as O
+        from paper_1504_06289_b200.inputs import KERNEL_C0, KERNEL_M
 
-    def run_one(j):
-        v = np.ascontiguousarray(K[:, j])
-        if R is not None:
-            rc = R.ref_conv_central_many(C.c_longlong(n), C.c_longlong(cols), C.c_void_p(Usub.ctypes.data),
-                                         C.c_void_p(v.ctypes.data), C.c_void_p(out.ctypes.data), C.c_int(threads))
-            if rc:
-                raise RuntimeError(R.ref_last_error().decode())
-        else:
-            out[:] = O.conv_central_many(Usub, v)
+        nodes, w, _, _ = O.make_expsum(KERNEL_M[CFG], KERNEL_C0[CFG])
+        K = O.kernel_tensor(grid.b_half, n, nodes, w, False).factors()[0]
+        t0 = time.perf_counter()
+        units, j = 0, 0
+        while time.perf_counter() - t0 < budget_s:
+            O.conv_central_many(U, K[:, j % K.shape[1]])
+            units += ra
+            j += 1
+        el = time.perf_counter() - t0
+        return {"value": units / el, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": f"axis 0 of config 2 on the restatement: {j} kernel columns x {ra} density columns"}
+    K = np.asfortranarray(K)
+    rb = K.shape[1]
+    h = grid.h[0]
+
+    def run(js, nthreads):
+        jsa = np.ascontiguousarray(np.asarray(js, dtype=np.int64))
+        chk = C.c_double()
+        t0 = time.perf_counter()
+        rc = R.ref_convolve_axis_sample(C.c_longlong(n), C.c_longlong(ra), C.c_void_p(U.ctypes.data),
+                                        C.c_void_p(K.ctypes.data), C.c_void_p(jsa.ctypes.data),
+                                        C.c_longlong(len(js)), C.c_double(h), C.c_int(nthreads), C.byref(chk))
+        if rc:
+            raise RuntimeError(R.ref_last_error().decode())
+        return time.perf_counter() - t0
 
     t0 = time.perf_counter()
-    units = 0
-    j = 0
+    units, rounds, j0 = 0, 0, 0
     while True:
-        run_one(j % K.shape[1])
-        units += cols
-        j += 1
+        js = [(j0 + k) % rb for k in range(threads)]
+        run(js, threads)
+        j0 += threads
+        units += ra * len(js)
+        rounds += 1
         el = time.perf_counter() - t0
         if el >= budget_s:
             break
-    return {"value": units / el, "unit": UNIT, "cores": threads, "kind": kind,
-            "sample": f"axis 0 of config 2: {cols} density columns x {j} kernel columns "
-                      f"(n={n}, reference radix-2 FFT length 65536), {units} convolutions in {el:.1f} s"}
+    out = {"value": units / el, "unit": UNIT, "cores": threads, "kind": "reference",
+           "sample": f"axis 0 of config 2: {rounds} round(s) x {threads} kernel columns (one per thread), each "
+                     f"conv_central_many over all {ra} density columns (n={n}, the reference's radix-2 FFT of "
+                     f"length 65536; one kernel FFT per call as in tensor.cpp:191-195): {units} convolutions "
+                     f"in {el:.1f} s"}
+    if "one_thread" not in _REF_CACHE:
+        t1 = run([0], 1)
+        _REF_CACHE["one_thread"] = {"value": ra / t1, "cores": 1,
+                                    "sample": f"one conv_central_many call: {ra} convolutions in {t1:.1f} s"}
+    out["one_thread"] = _REF_CACHE["one_thread"]
+    return out
 
 
 def run_reference_arm(args, rank: int, world: int) -> None:
@@ -169,7 +227,7 @@ def run_reference_arm(args, rank: int, world: int) -> None:
         return
     results = []
     for _ in range(args.warmup):
-        cpu_reference_sample(budget_s=1.0)
+        cpu_reference_sample(budget_s=0.5)
     for _ in range(args.steps):
         results.append(cpu_reference_sample(budget_s=max(2.0, 60.0 / max(args.steps, 1))))
     vals = [r["value"] for r in results]
@@ -182,7 +240,8 @@ def run_reference_arm(args, rank: int, world: int) -> None:
         "warmup": args.warmup, "ms_per_step": per_step_ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config 2: Hartree convolution n=16385, R_f=500, R_N=41 (M=20)", "n": N_GRID,
-                   "R_f": R_F, "R_N": 41, "parallelism": "host threads", "steps_are": "bounded samples"},
+                   "R_f": R_F, "R_N": 41, "parallelism": "host threads",
+                   "steps_are": "bounded samples (whole rounds of one kernel column per thread)"},
         "cpu_baseline": base,
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -200,7 +259,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--strong", action="store_true", help="shard config 2's fixed 500 density columns")
+    ap.add_argument("--weak", action="store_true", help="every rank convolves its own 500 density columns")
+    ap.add_argument("--strong", action="store_true", help="(default) shard config 2's fixed 500 density columns")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -224,7 +284,7 @@ def main():
     import paper_1504_06289_b200 as tg
     from paper_1504_06289_b200.inputs import hartree_case
 
-    strong = args.strong or world == 1
+    strong = not args.weak or world == 1
     total_f = R_F if strong else R_F * world
     case = hartree_case(CFG, rank=total_f, nsamples=10_000)
     # shard the density columns (rank pairs i + R_f j with i in this rank's block)
@@ -293,6 +353,16 @@ def main():
     if world > 1:
         dist.all_reduce(part)
     samples_vh = part.cpu().numpy()
+    parity = {"checked": False}
+    gold = ROOT / "tests" / "golden" / "reference_cfg2_vh_samples.npz"
+    if strong and gold.exists():
+        g = np.load(gold)
+        if np.array_equal(g["samples"], case.samples):
+            ref = g["vh"]
+            err = float(np.abs(samples_vh - ref).max() / np.abs(ref).max())
+            parity = {"checked": True, "max_rel_err": err, "tol": 1e-10, "ok": err <= 1e-10,
+                      "against": "tests/golden/reference_cfg2_vh_samples.npz (oracle/_ref over all 61,500 "
+                                 "convolutions, tools/make_golden_cfg2.py)"}
 
     # ---- roofline of the dominant kernel (pair convolution kernel, one launch = one axis)
     hbm_peak, peak_kind = peaks()
@@ -362,7 +432,7 @@ def main():
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if args.strong else "weak",
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": "config 2: Hartree convolution (tg::hartree_potential) n=16385, R_f=500, "
                                "R_N=41 (M=20), 61,500 windowed FP64 1D convolutions per step",
@@ -383,11 +453,14 @@ def main():
         "e2e": e2e,
         "cpu_baseline": cpu,
         "validation": {"sample_points": int(len(samples_vh)), "vh_sample_checksum": float(np.sum(samples_vh)),
-                       "allreduce": "nccl" if world > 1 else "none (single rank)"},
+                       "allreduce": "nccl" if world > 1 else "none (single rank)", "parity": parity},
     }
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+    if parity.get("checked") and not parity["ok"]:
+        log(f"PARITY FAILURE: V_H samples differ from the reference by {parity['max_rel_err']:.3e} > 1e-10")
+        sys.exit(3)
 
 
 if __name__ == "__main__":

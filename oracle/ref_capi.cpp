@@ -3,6 +3,7 @@
 // place from /root/reference/proj/src against oracle/eigen_shim) so tests can
 // pin the restatement and generate golden fixtures, and bench.py can time the
 // reference's CPU path (`--impl reference`).
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -136,6 +137,85 @@ int ref_conv_central_many(long long n, long long c, const double* U, const doubl
       });
     }
     for (auto& t : ts) t.join();
+  });
+}
+// CPU baseline shaped like tg::convolve's own loop (tensor.cpp:189-195): for
+// each kernel column js[k], conv_central_many over ALL ra density columns
+// (one kernel FFT per call, reused across the columns), times h.  `threads`
+// std::threads split the k loop (the function is pure); each
+// thread owns its result matrix.  checksum = sum over k of out(0, 0) (keeps
+// the work observable).
+int ref_convolve_axis_sample(long long n, long long ra, const double* U, const double* K, const long long* js,
+                             long long njs, double h, int threads, double* checksum) {
+  return guard([&] {
+    const Eigen::MatrixXd Um = mat(U, n, ra);
+    std::vector<double> first(static_cast<size_t>(njs), 0.0);
+    auto work = [&](long long k0, long long k1) {
+      for (long long k = k0; k < k1; ++k) {
+        Eigen::VectorXd v(static_cast<Eigen::Index>(n));
+        std::memcpy(v.data(), K + js[k] * n, sizeof(double) * n);
+        Eigen::MatrixXd cols = h * tg::conv_central_many(Um, v);
+        first[static_cast<size_t>(k)] = cols.size() ? cols(0, 0) : 0.0;
+      }
+    };
+    if (threads <= 1 || njs < 2) {
+      work(0, njs);
+    } else {
+      std::vector<std::thread> ts;
+      for (int t = 0; t < threads; ++t) {
+        const long long lo = njs * t / threads, hi = njs * (t + 1) / threads;
+        if (lo < hi) ts.emplace_back(work, lo, hi);
+      }
+      for (auto& t : ts) t.join();
+    }
+    double s = 0.0;
+    for (double x : first) s += x;
+    *checksum = s;
+  });
+}
+
+// Fixture generator (tools/make_golden_cfg2.py): V_H = hartree_potential(theta,
+// kernel, h) (hf.cpp:131-138 -> convolve, tensor.cpp:179-198) evaluated at
+// npts grid points (value_at, tensor.hpp:135-140) WITHOUT materialising the
+// ra*rb-column factors: for each kernel column j, the three axes'
+// conv_central_many(theta.factor[ax], kernel.factor[ax].col(j)) (the
+// reference's own code), h-scaled as in convolve, then
+// sum_i w_i w_j prod_ax F_ax(idx_ax, i) per point; per-j partials summed in j
+// order, terms within a j in i order.
+int ref_hartree_samples(void* theta_h, void* kernel_h, const double* h, long long npts, const long long* ijk,
+                        int threads, double* out) {
+  return guard([&] {
+    const auto& th = *static_cast<tg::CanonicalTensor3*>(theta_h);
+    const auto& kt = *static_cast<tg::CanonicalTensor3*>(kernel_h);
+    const double inv_vol = 1.0 / (h[0] * h[1] * h[2]);
+    const tg::CanonicalTensor3 ks = tg::scale(kt, inv_vol);
+    const long long ra = th.rank(), rb = ks.rank();
+    std::vector<std::vector<double>> part(static_cast<size_t>(rb), std::vector<double>(static_cast<size_t>(npts), 0.0));
+    auto work = [&](long long j0, long long j1) {
+      for (long long j = j0; j < j1; ++j) {
+        Eigen::MatrixXd F[3];
+        for (int ax = 0; ax < 3; ++ax) F[ax] = h[ax] * tg::conv_central_many(th.factor[ax], ks.factor[ax].col(j));
+        auto& pj = part[static_cast<size_t>(j)];
+        for (long long p = 0; p < npts; ++p) {
+          double s = 0.0;
+          for (long long i = 0; i < ra; ++i)
+            s += (th.weight[i] * ks.weight[j]) * F[0](ijk[3 * p], i) * F[1](ijk[3 * p + 1], i) * F[2](ijk[3 * p + 2], i);
+          pj[static_cast<size_t>(p)] = s;
+        }
+      }
+    };
+    std::vector<std::thread> ts;
+    const int nt = std::max(1, threads);
+    for (int t = 0; t < nt; ++t) {
+      const long long lo = rb * t / nt, hi = rb * (t + 1) / nt;
+      if (lo < hi) ts.emplace_back(work, lo, hi);
+    }
+    for (auto& t : ts) t.join();
+    for (long long p = 0; p < npts; ++p) {
+      double s = 0.0;
+      for (long long j = 0; j < rb; ++j) s += part[static_cast<size_t>(j)][static_cast<size_t>(p)];
+      out[p] = s;
+    }
   });
 }
 int ref_convolve(void* a, void* b, const double* h, void* out) {

@@ -158,3 +158,65 @@ def test_hartree_config2_columns(ctx):
     of = ovh.factors()
     for ax in range(3):
         assert relmax(vh.factor[ax], of[ax]) <= TOL
+
+
+GOLDEN_CFG2 = __import__("pathlib").Path(__file__).parent / "golden" / "reference_cfg2_vh_samples.npz"
+
+
+def test_hartree_config2_full_benchmarked_path(ctx):
+    """The benchmarked configuration itself (bench.py): all 500 density columns
+    x 41 kernel columns x 3 axes through the device-resident path, i.e. the
+    persistent pair kernel with ~71 pairs per CTA, density-column switches
+    inside a CTA's run and shared/tensor memory reused across pairs.
+    * 64 complete output columns per axis against the reference's own
+      conv_central_many (oracle/_ref, proj/src/fft.cpp:97-122) times h, as
+      tg::convolve forms them (tensor.cpp:191-195); the density columns are
+      chosen so that their pairs sit mid-run in CTAs that switched density
+      column before them (work list: i-major, 21 distinct kernel columns per i,
+      CTA b takes entries [10500 b / 148, 10500 (b + 1) / 148)).
+    * V_H at the 10^4 seeded sample points against the fixture the reference
+      computed over all 61,500 convolutions (tools/make_golden_cfg2.py)."""
+    import ctypes as C
+
+    import torch
+
+    R = O.rlib()
+    if R is None:
+        pytest.skip("oracle/_ref not built")
+    g = np.load(GOLDEN_CFG2)
+    case = hartree_case(2, nsamples=int(g["samples"].shape[0]))
+    assert np.array_equal(case.samples, g["samples"])
+    ra, rb = case.theta.rank(), case.kernel.rank()
+    n = case.grid.n[0]
+    d_theta = DeviceCP.from_host(case.theta)
+    d_kern = DeviceCP.from_host(case.kernel.tensor)
+    d_out = DeviceCP.empty([n, n, n], ra * rb)
+    hartree_potential(d_theta, d_kern, case.grid.h, ctx, out=d_out)
+    ctx.synchronize()
+    # V_H at the sample points vs the reference over all 61,500 convolutions
+    got_t = value_at_points(d_out, torch.as_tensor(case.samples).cuda(), ctx)
+    ctx.synchronize()
+    got = got_t.cpu().numpy()
+    assert relmax(got, g["vh"]) <= TOL, relmax(got, g["vh"])
+    # complete output columns vs the reference's conv_central_many
+    ii = [0, 3, 4, 70, 71, 250, 251, 499]
+    jj = [0, 40, 5, 35, 13, 20, 27, 39]
+    kf = case.kernel.tensor.factor
+    for ax in range(3):
+        U = np.asfortranarray(case.theta.factor[ax][:, ii])
+        cols = torch.as_tensor([i + ra * j for j in jj for i in ii], device=d_out.factor[ax].device)
+        sel = d_out.factor[ax].index_select(0, cols)
+        torch.cuda.synchronize()
+        mine = sel.cpu().numpy().T  # n x 64
+        for jx, j in enumerate(jj):
+            v = np.ascontiguousarray(kf[ax][:, j])
+            ref = np.zeros((n, len(ii)), order="F")
+            rc = R.ref_conv_central_many(C.c_longlong(n), C.c_longlong(len(ii)), C.c_void_p(U.ctypes.data),
+                                         C.c_void_p(v.ctypes.data), C.c_void_p(ref.ctypes.data), C.c_int(8))
+            assert rc == 0
+            ref *= case.grid.h[ax]
+            blk = mine[:, jx * len(ii):(jx + 1) * len(ii)]
+            for c in range(len(ii)):
+                assert relmax(blk[:, c], ref[:, c]) <= TOL, (ax, ii[c], j, relmax(blk[:, c], ref[:, c]))
+    del d_out
+    torch.cuda.empty_cache()
