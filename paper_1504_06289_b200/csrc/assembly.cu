@@ -273,11 +273,9 @@ std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* co
         TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
       }
       for (int ax = 0; ax < 3; ++ax) {  // T_ax (nq x P) = B_ax(:, q0:q0+nq)^T L_ax
-        cudaStream_t main_stream = ctx->stream;
-        if (fork && ax == 2) ctx->stream = ctx->aux_stream;
+        StreamSwap on_aux(ctx, fork && ax == 2, ctx->aux_stream);  // restored on every exit path
         dgemm(ctx, true, false, nq, P, n[ax], 1.0, B[ax] + static_cast<int64_t>(q0) * n[ax], n[ax], Lh[ax], n[ax], 0.0,
               T[ax], nq);
-        ctx->stream = main_stream;
       }
       if (fork) {
         TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));

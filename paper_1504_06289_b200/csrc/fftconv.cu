@@ -1791,11 +1791,11 @@ static int busy_width(const ConvPlan& pl, Kern kern, bool pair) {
 template <int R0, bool BREAL>
 static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
                         const PairEntry* dwork, const int* winfo, double* out) {
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kTgbMaxDevices] = {};  // per device
+  if (!attr[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel<R0, BREAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin)));
-    attr = true;
+    attr[ctx->device] = true;
   }
   int& tt = pl.pair_threads[BREAL ? 1 : 0];
   if (!tt) tt = busy_width(pl, pair_kernel<R0, BREAL>, true);
@@ -1820,8 +1820,8 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
   if constexpr (R0 == 16) {
     if (fused_ok && kern == pair_kernel_tmem<R0, R1, R2, R3, TT, BREAL>) kern = pair_kernel_fused<R0, R1, R2, R3, TT, BREAL>;
   }
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kTgbMaxDevices] = {};  // per device
+  if (!attr[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel_static<R0, R1, R2, R3, TT, BREAL>,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
     cudaFuncAttributes fa{};
@@ -1835,7 +1835,7 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
     }
-    attr = true;
+    attr[ctx->device] = true;
   }
   int per_sm = 1;
   TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TT, pl.smem));
@@ -1885,19 +1885,19 @@ static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA
 static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, int nA, void* specA, const double* B,
                             const int* colidx, int nB, void* specB, void* specB2, int modeB, int64_t ldx, double h) {
   if (nA + nB == 0) return;
-  static bool attr_set = false;
-  if (!attr_set) {
+  static bool attr_set[kTgbMaxDevices] = {};  // per device
+  if (!attr_set[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin)));
-    attr_set = true;
+    attr_set[ctx->device] = true;
   }
   const PlanArgs& a = pl.a;
   if (a.P == 4 && a.r[0] == 16 && a.r[1] == 10 && a.r[2] == 10 && a.r[3] == 8 && !getenv("TGB_NO_STATIC")) {
-    static bool attr2 = false;
-    if (!attr2) {
+    static bool attr2[kTgbMaxDevices] = {};  // per device
+    if (!attr2[ctx->device]) {
       TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel_static<16, 10, 10, 8, 320>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
-      attr2 = true;
+      attr2[ctx->device] = true;
     }
     spectrum_kernel_static<16, 10, 10, 8, 320><<<nA + nB, 320, pl.smem, ctx->stream>>>(
         pl.a, A, nA, specA, B, colidx, nB, specB, specB2, modeB, ldx, h);

@@ -425,13 +425,10 @@ void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_of
       }
       for (int ax = 0; ax < 3; ++ax) {
         T[ax] = st.p + ax * rows * Gc;
-        const bool on_aux = fork && ax == 2;
-        cudaStream_t main_stream = ctx->stream;
-        if (on_aux) ctx->stream = ctx->aux_stream;
+        StreamSwap on_aux(ctx, fork && ax == 2, ctx->aux_stream);  // restored on every exit path
         // T_ax (rows x Gc) = Y_ax(:, r0 : r0 + rows)^T GP_ax(:, 0 : Gc)
         dgemm(ctx, true, false, rows, Gc, basis.n[ax], 1.0, y[ax] + r0 * basis.n[ax], basis.n[ax], gp[ax],
               basis.n[ax], 0.0, T[ax], rows);
-        ctx->stream = main_stream;
       }
       if (fork) {
         TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
@@ -625,13 +622,13 @@ void generalized_eigensolve_dev(tgb_ctx* ctx, int64_t nb, const double* F, const
   const bool staged = nb <= kGenMax;
   Scratch sl(ctx, nb * nb), sb(ctx, nb * nb), ss(ctx, nb + 2), sw(ctx, staged ? 1 : 2 * nb * nb);
   const size_t smem = staged ? 2 * static_cast<size_t>(nb * nb) * sizeof(double) : 0;
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kTgbMaxDevices] = {};  // per device
+  if (!attr[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(gen_eig_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(2 * kGenMax * kGenMax * sizeof(double))));
     TGB_CUDA(cudaFuncSetAttribute(gen_eig_finish_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(kGenMax * kGenMax * sizeof(double))));
-    attr = true;
+    attr[ctx->device] = true;
   }
   double* sigma = ss.p + nb;
   int* fail = reinterpret_cast<int*>(ss.p + nb + 1);

@@ -653,20 +653,20 @@ void cholqr2(tgb_ctx* ctx, int64_t d, int p, double* X, Dev& tmp) {
     const size_t l_bytes = static_cast<size_t>(p) * p * sizeof(double);
     if (p <= kCholSmem && 2 * l_bytes <= static_cast<size_t>(kCholSmemBytes)) {
       // L and L^{-1} both in shared memory: the row-at-a-time kernel (96 vs 101 us at config 1's blocks)
-      static bool cattr = false;
-      if (!cattr) {
+      static bool cattr[kTgbMaxDevices] = {};  // per device
+      if (!cattr[ctx->device]) {
         TGB_CUDA(cudaFuncSetAttribute(chol_inv_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kCholSmemBytes));
-        cattr = true;
+        cattr[ctx->device] = true;
       }
       chol_inv_smem_kernel<<<1, p > 64 ? 1024 : 512, 2 * l_bytes, ctx->stream>>>(p, H);
     } else if (p <= kCF_ROWS) {
       // in-place inverse (0.21 vs 0.38 ms at p = 110-128, the TEI fit's ranks)
-      static bool fattr = false;
-      if (!fattr) {
+      static bool fattr[kTgbMaxDevices] = {};  // per device
+      if (!fattr[ctx->device]) {
         TGB_CUDA(cudaFuncSetAttribute(chol_inv_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       kCF_ROWS * kCF_ROWS * static_cast<int>(sizeof(double))));
-        fattr = true;
+        fattr[ctx->device] = true;
       }
       chol_inv_fast_kernel<<<1, kCF_ROWS * kCF_GRP, l_bytes, ctx->stream>>>(p, H);
     } else {
@@ -709,11 +709,11 @@ void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg);
 static void launch_jacobi_onesided(tgb_ctx* ctx, int64_t m, int64_t p, double* X, double* V, double* sg, int* perm) {
   const size_t sm = static_cast<size_t>(p) * sizeof(double);
   if (sm + 1024 > ctx->smem_optin) throw Error(TGB_INVALID_ARGUMENT, "one-sided Jacobi: too many columns");
-  static bool attr = false;
-  if (!attr) {
+  static bool attr[kTgbMaxDevices] = {};  // per device
+  if (!attr[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(jacobi_onesided_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin - 1024)));
-    attr = true;
+    attr[ctx->device] = true;
   }
   jacobi_onesided_kernel<<<1, 1024, sm, ctx->stream>>>(m, static_cast<int>(p), X, V, sg, perm);
   TGB_LAUNCHED(ctx);
@@ -786,13 +786,13 @@ void jacobi_svd_dev(tgb_ctx* ctx, int p, double* S, double* sg) {
     return;
   }
   const size_t jsm = static_cast<size_t>(p) * (p + (p & 1)) * sizeof(double);
-  static bool jattr = false;
-  if (!jattr) {
+  static bool jattr[kTgbMaxDevices] = {};  // per device
+  if (!jattr[ctx->device]) {
     cudaFuncAttributes fa{};
     TGB_CUDA(cudaFuncGetAttributes(&fa, jacobi_svd_kernel));
     TGB_CUDA(cudaFuncSetAttribute(jacobi_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
-    jattr = true;
+    jattr[ctx->device] = true;
   }
   jacobi_svd_kernel<<<1, kJacThreads, jsm, ctx->stream>>>(p, S, sg);
   TGB_LAUNCHED(ctx);
@@ -985,6 +985,10 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
           fprintf(stderr, "[tgb]   it=%d p=%d conv=%d r_est=%lld s0=%.3e s_last=%.3e\n", it, p, conv,
                   static_cast<long long>(r_est), sg[0], sg[p - 1]);
         if (r_est + 4 > p && p < dmin) {
+          if (p >= kMaxBlock)  // the block cannot grow past kMaxBlock columns: fail instead of looping
+            throw Error(TGB_NUMERICAL_ERROR,
+                        "reduce: more than " + std::to_string(kMaxBlock - 4) +
+                            " singular vectors needed in one mode (device subspace block limit)");
           grow = true;
           break;
         }
@@ -1001,6 +1005,9 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
       TGB_LAUNCHED(ctx);
       cholqr2(ctx, k, p, Y.p, tmp);
     }
+    if (!done && !grow && !getenv("TGB_QUIET"))
+      fprintf(stderr, "[tgb] warning: reduce: subspace iteration hit its 400-iteration cap (n=%lld k=%lld p=%d); "
+                      "rank taken from the unconverged block\n", static_cast<long long>(n), static_cast<long long>(k), p);
     if (done || !grow) break;
     // grow the block: keep X, double p
     const int pn = static_cast<int>(std::min<int64_t>(std::min<int64_t>(dmin, 2 * p), kMaxBlock));

@@ -1107,7 +1107,10 @@ void tei_fit(tgb_ctx* ctx, TEI& f, const tgb_cp& basis_dev, const int64_t* fn_of
   const int64_t np = f.np, np2 = np * np;
   // phase 1: per axis G (n x np^2, column p + np q = g_p .* g_q) and its Gram GG^T as the elementwise
   // square of F F^T (n x n x np instead of n x n x np^2 flops; tei.cpp:118-124)
-  static thread_local std::array<DevBuf, 3> gbuf, grambuf, lbuf, smallbuf;
+  std::array<DevBuf, 3>& gbuf = ctx_buf3(ctx, "tei1110.gbuf");
+  std::array<DevBuf, 3>& grambuf = ctx_buf3(ctx, "tei1110.grambuf");
+  std::array<DevBuf, 3>& lbuf = ctx_buf3(ctx, "tei1110.lbuf");
+  std::array<DevBuf, 3>& smallbuf = ctx_buf3(ctx, "tei1110.smallbuf");  // per context
   std::array<double*, 3> G{}, gram{}, Lw{}, dg{}, resid{};
   std::array<int*, 3> piv{}, info{};
   std::array<int64_t, 3> cap{};
@@ -1262,7 +1265,7 @@ void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
   const int nc = static_cast<int>(nb * nb);
   TGB_CUDA(cudaMemsetAsync(diag, 0, nc * sizeof(double), ctx->stream));
   std::array<double*, 3> Y{};
-  static thread_local std::array<DevBuf, 3> ybuf;
+  std::array<DevBuf, 3>& ybuf = ctx_buf3(ctx, "tei1265.ybuf");  // per context
   // keep every V M_k^T for the Cholesky columns when it fits a modest budget (config 3: 0.8 GB)
   size_t pk_bytes = 0;
   for (int ax = 0; ax < 3; ++ax) pk_bytes += static_cast<size_t>(np2) * f.R[ax] * f.K * sizeof(double);
@@ -1280,7 +1283,7 @@ void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
       dgemm(ctx, false, true, np2, r * f.K, r, 1.0, dptr(f.V[ax]), np2, dptr(f.Mst[ax]), r * f.K, 0.0,
             dptr(f.Pk[ax]), np2);
     }
-    static thread_local DevBuf sbuf;
+    DevBuf& sbuf = ctx_buf(ctx, "tei1283.sbuf");  // per context
     auto* sk = static_cast<double*>(sbuf.get(std::max<size_t>(8, static_cast<size_t>(f.K) * nc * sizeof(double))));
     tei_diag_terms_kernel<<<dim3((nc + 127) / 128, static_cast<unsigned>(f.K)), 128, 0, ctx->stream>>>(
         nc, static_cast<const int*>(f.d_cstart.p), static_cast<const int*>(f.d_cpairs.p),
@@ -1310,7 +1313,9 @@ void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
 // primitive-level column b_prim_column(j) (np^2, device) via three GEMMs + combine
 static void b_prim_column_dev(tgb_ctx* ctx, TEI& f, int64_t j, double* col) {
   const int64_t np2 = f.np * f.np, K = f.K;
-  static thread_local std::array<DevBuf, 3> wbuf, ybuf, vrow;
+  std::array<DevBuf, 3>& wbuf = ctx_buf3(ctx, "tei1313.wbuf");
+  std::array<DevBuf, 3>& ybuf = ctx_buf3(ctx, "tei1313.ybuf");
+  std::array<DevBuf, 3>& vrow = ctx_buf3(ctx, "tei1313.vrow");  // per context
   std::array<double*, 3> W{};
   for (int ax = 0; ax < 3; ++ax) {
     const int64_t r = f.R[ax];
@@ -1340,7 +1345,8 @@ void tei_column_dev(tgb_ctx* ctx, TEI& f, int64_t pair, double* out) {
   ensure_contraction_tables(ctx, f);
   const int64_t nb = f.nb, np = f.np, np2 = np * np;
   const int64_t kappa = pair % nb, lambda = pair / nb;
-  static thread_local DevBuf zbuf, cbuf;
+  DevBuf& zbuf = ctx_buf(ctx, "tei1343.zbuf");
+  DevBuf& cbuf = ctx_buf(ctx, "tei1343.cbuf");  // per context
   auto* z = static_cast<double*>(zbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
   auto* c = static_cast<double*>(cbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
   // z = sum over primitive pairs (p, q) of (kappa, lambda) of w_p w_q b_prim_column(p + np q)
@@ -1367,8 +1373,13 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
   tei_diagonal_dev(ctx, f, dg);
   f.L.get(std::max<int64_t>(1, nb2 * nb2) * sizeof(double));
   double* L = dptr(f.L);
-  static thread_local DevBuf zbuf, cbuf, stbuf, pivbuf;
-  static thread_local std::array<DevBuf, 3> wbuf, ybuf, vrow;
+  DevBuf& zbuf = ctx_buf(ctx, "tei1370.zbuf");
+  DevBuf& cbuf = ctx_buf(ctx, "tei1370.cbuf");
+  DevBuf& stbuf = ctx_buf(ctx, "tei1370.stbuf");
+  DevBuf& pivbuf = ctx_buf(ctx, "tei1370.pivbuf");  // per context
+  std::array<DevBuf, 3>& wbuf = ctx_buf3(ctx, "tei1371.wbuf");
+  std::array<DevBuf, 3>& ybuf = ctx_buf3(ctx, "tei1371.ybuf");
+  std::array<DevBuf, 3>& vrow = ctx_buf3(ctx, "tei1371.vrow");  // per context
   auto* z = static_cast<double*>(zbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
   auto* cc = static_cast<double*>(cbuf.get(std::max<int64_t>(1, np2) * sizeof(double)));
   auto* st = static_cast<CholState*>(stbuf.get(sizeof(CholState)));
@@ -1401,7 +1412,7 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
   CholState h0{};
   TGB_CUDA(cudaMemcpyAsync(st, &h0, sizeof(CholState), cudaMemcpyHostToDevice, ctx->stream));
   // fused column path: the three y_ax (r_ax x K) and a rows x K product tile in shared memory
-  static thread_local DevBuf ptrbuf;
+  DevBuf& ptrbuf = ctx_buf(ctx, "tei1404.ptrbuf");  // per context
   const int64_t rmax = std::max({f.R[0], f.R[1], f.R[2], int64_t(1)});
   int col_rows = static_cast<int>(std::min<int64_t>(96, std::max<int64_t>(8, (np2 + ctx->num_sms - 1) / ctx->num_sms)));
   const int col_groups = std::max(1, std::min(8, 1024 / col_rows));
@@ -1418,11 +1429,11 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
   const int* dr = nullptr;
   const double* const* dPk = nullptr;
   if (fused_col) {
-    static bool attr = false;
-    if (!attr) {
+    static bool attr[kTgbMaxDevices] = {};  // per device
+    if (!attr[ctx->device]) {
       TGB_CUDA(cudaFuncSetAttribute(chol_col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(ctx->smem_optin - 1024)));
-      attr = true;
+      attr[ctx->device] = true;
     }
     struct Ptrs {
       const double* V[3];
@@ -1536,7 +1547,7 @@ void tei_cholesky(tgb_ctx* ctx, TEI& f, double eps_chol) {
       a.part = static_cast<double4*>(ctx->ws_misc3.get(static_cast<size_t>(2 * nblk) * sizeof(double4)));
       a.st = st;
       a.phase = nullptr;
-      static thread_local DevBuf phbuf;
+      DevBuf& phbuf = ctx_buf(ctx, "tei1539.phbuf");  // per context
       if (getenv("TGB_PHASE_CLK")) {
         a.phase = static_cast<unsigned long long*>(phbuf.get(8 * sizeof(unsigned long long)));
         TGB_CUDA(cudaMemsetAsync(a.phase, 0, 8 * sizeof(unsigned long long), ctx->stream));
@@ -1622,7 +1633,7 @@ int64_t pivoted_cholesky_dev(tgb_ctx* ctx, int64_t n, const double* A, double to
                              int64_t max_rank, double neg_tol, double* L, int64_t* pivots_host, double* residual,
                              bool* clamped) {
   const int64_t cap = std::min(n, max_rank);
-  static thread_local DevBuf wbuf;
+  DevBuf& wbuf = ctx_buf(ctx, "tei1625.wbuf");  // per context
   auto* w = static_cast<double*>(wbuf.get((n + 64 + std::max<int64_t>(cap, 1)) * sizeof(double)));
   double* dg = w;
   int* piv = reinterpret_cast<int*>(w + n + 8);
@@ -1719,7 +1730,7 @@ int tgb_tei_diagonal(tgb_ctx* ctx, tgb_tei* t, double* out, int mem) {
   return tgb::guarded_call([&] {
     tgb::DevStreamScope scope(ctx);
     const int64_t nb2 = t->t.nb * t->t.nb;
-    static thread_local tgb::DevBuf buf;
+    tgb::DevBuf& buf = tgb::ctx_buf(ctx, "tei1722.buf");  // per context
     auto* d = static_cast<double*>(buf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
     tgb::tei_diagonal_dev(ctx, t->t, d);
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1732,7 +1743,7 @@ int tgb_tei_column(tgb_ctx* ctx, tgb_tei* t, int64_t pair, double* out, int mem)
     tgb::DevStreamScope scope(ctx);
     tgb::require(pair >= 0 && pair < t->t.nb * t->t.nb, "tei_column: index out of range");
     const int64_t nb2 = t->t.nb * t->t.nb;
-    static thread_local tgb::DevBuf buf;
+    tgb::DevBuf& buf = tgb::ctx_buf(ctx, "tei1735.buf");  // per context
     auto* d = static_cast<double*>(buf.get(std::max<int64_t>(1, nb2) * sizeof(double)));
     tgb::tei_column_dev(ctx, t->t, pair, d);
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -13,6 +14,9 @@
 #include "tgb.h"
 
 namespace tgb {
+
+// cudaFuncSetAttribute is per device: one-time flags are kept per device id
+constexpr int kTgbMaxDevices = 64;
 
 // Exceptions carry the C-ABI return code (tgb.h) and map 1:1 to the
 // reference's exception types (common.hpp:11-25).
@@ -121,9 +125,30 @@ struct tgb_ctx {
   std::multimap<size_t, void*> scratch_free;  // cached Dev blocks (reduction.cu)
   void* stage_pin[2] = {nullptr, nullptr};     // pinned chunks for pageable host copies (hostcopy.cpp)
   cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  // per-context named device workspaces of the TEI / HF drivers (device
+  // pointers are never shared across contexts or devices)
+  std::map<std::string, tgb::DevBuf> named;
+  std::map<std::string, std::array<tgb::DevBuf, 3>> named3;
+  void* nccl_comm = nullptr;  // ncclComm_t (tgb_ctx_set_comm), owned by the caller
+  int comm_rank = 0, comm_size = 1;
 };
 
 namespace tgb {
+// a named per-context workspace (replaces function-static buffers)
+inline DevBuf& ctx_buf(tgb_ctx* ctx, const std::string& name) { return ctx->named[name]; }
+inline std::array<DevBuf, 3>& ctx_buf3(tgb_ctx* ctx, const std::string& name) { return ctx->named3[name]; }
+
+// Runs a section of work on another stream of the context and restores
+// ctx->stream on every exit path (exceptions included).
+struct StreamSwap {
+  tgb_ctx* ctx;
+  cudaStream_t saved;
+  StreamSwap(tgb_ctx* c, bool on, cudaStream_t s) : ctx(c), saved(c->stream) {
+    if (on) ctx->stream = s;
+  }
+  ~StreamSwap() { ctx->stream = saved; }
+};
+
 // bracket a hot-kernel launch with timing events when profiling is enabled
 inline void prof_begin(tgb_ctx* ctx) {
   if (!ctx->profiling) return;
