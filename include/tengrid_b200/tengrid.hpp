@@ -8,8 +8,20 @@
 // calls into this header
 // (INTEGRATION.md).  It is templated on the matrix type so it works with
 // Eigen::MatrixXd / Eigen::VectorXd (column-major, data()/rows()/cols()/
-// size()) without including Eigen here.  Errors are rethrown as the
-// reference's exception classes (proj/include/tengrid/common.hpp:11-25).
+// size()) without including Eigen here.
+//
+// Errors are rethrown as the reference's own exception classes
+// (proj/include/tengrid/common.hpp:11-25): std::invalid_argument,
+// std::domain_error, tg::SnapError, tg::NumericalError.  The two tg:: types
+// are taken from the including translation unit:
+//   * a reference build has proj/include on its include path, so
+//     <tengrid/common.hpp> is found and tg::SnapError / tg::NumericalError
+//     are thrown directly;
+//   * or the includer names them before including this header:
+//       #define TGB_SNAP_ERROR_T tg::SnapError
+//       #define TGB_NUMERICAL_ERROR_T tg::NumericalError
+//   * otherwise (standalone use) the tgb_cpp fallbacks below are thrown.
+// Both types must be constructible from a std::string, as the reference's are.
 #pragma once
 
 #include <array>
@@ -18,9 +30,19 @@
 #include <vector>
 
 #include "tgb.h"
+#include "tgb_host.h"
+
+#if !defined(TGB_SNAP_ERROR_T) && !defined(TGB_NUMERICAL_ERROR_T) && defined(__has_include)
+#if __has_include(<tengrid/common.hpp>)
+#include <tengrid/common.hpp>
+#define TGB_SNAP_ERROR_T ::tg::SnapError
+#define TGB_NUMERICAL_ERROR_T ::tg::NumericalError
+#endif
+#endif
 
 namespace tgb_cpp {
 
+// standalone fallbacks (used only when the reference's classes are not visible)
 struct SnapError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
@@ -31,16 +53,34 @@ struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
 
-inline void check(int rc) {
-  if (rc == TGB_OK) return;
-  const std::string msg = tgb_last_error();
+#ifdef TGB_SNAP_ERROR_T
+using snap_error_t = TGB_SNAP_ERROR_T;
+#else
+using snap_error_t = SnapError;
+#endif
+#ifdef TGB_NUMERICAL_ERROR_T
+using numerical_error_t = TGB_NUMERICAL_ERROR_T;
+#else
+using numerical_error_t = NumericalError;
+#endif
+
+inline void throw_code(int rc, const std::string& msg) {
   switch (rc) {
     case TGB_INVALID_ARGUMENT: throw std::invalid_argument(msg);
     case TGB_DOMAIN_ERROR: throw std::domain_error(msg);
-    case TGB_SNAP_ERROR: throw SnapError(msg);
-    case TGB_NUMERICAL_ERROR: throw NumericalError(msg);
+    case TGB_SNAP_ERROR: throw snap_error_t(msg);
+    case TGB_NUMERICAL_ERROR: throw numerical_error_t(msg);
     default: throw CudaError(msg);
   }
+}
+
+// device entry points (tgb.h): message from tgb_last_error()
+inline void check(int rc) {
+  if (rc != TGB_OK) throw_code(rc, tgb_last_error());
+}
+// host input producers (tgb_host.h): message from tgb_host_last_error()
+inline void check_host(int rc) {
+  if (rc != TGB_OK) throw_code(rc, tgb_host_last_error());
 }
 
 // One context per thread per device (contexts are not shared across threads).
@@ -206,6 +246,115 @@ void generalized_eigensolve(const Matrix& f, const Matrix& s, Matrix& c, Vector&
   c = Matrix(f.rows(), f.rows());
   e = Vector(f.rows());
   check(tgb_generalized_eigensolve(context(), f.rows(), f.data(), s.data(), c.data(), e.data(), TGB_MEM_HOST));
+}
+
+// ---- host input producers (tgb_host.h) ------------------------------------
+
+// tg::snap_to_node (grid.cpp:23-30): std::domain_error outside the box,
+// the reference's SnapError farther than h/2 from every node.
+template <class Grid>
+int64_t snap_to_node(const Grid& g, int axis, double x) {
+  int64_t node = 0;
+  check_host(tgb_snap_to_node(g.b_half[axis], static_cast<int64_t>(g.n[axis]), x, &node));
+  return node;
+}
+
+// tg::expsum_for_interval (kernel.cpp:131-165): the Newton quadrature (M, C0)
+// meeting eps on [r_min, r_max]; the reference's NumericalError when m_cap
+// is exceeded.
+struct ExpSumChoice {
+  int64_t m;
+  double c0;
+};
+inline ExpSumChoice expsum_for_interval(double r_min, double r_max, double eps, int64_t m_cap = 2048) {
+  ExpSumChoice c{0, 0.0};
+  check_host(tgb_expsum_for_interval(r_min, r_max, eps, m_cap, &c.m, &c.c0));
+  return c;
+}
+
+// ---- SCF / MP2 (tgb.h) ------------------------------------------------------
+
+// tg::scf_solve (hf.cpp:201-270) for a reference-shaped Molecule / BasisSet /
+// SCFConfig (members as in basis.hpp:10-52 and hf.hpp:54-64).  Returns the
+// scalar results and the orbital energies / density (column-major nb x nb).
+struct ScfResult {
+  double energy = 0.0, nuclear_energy = 0.0;
+  bool converged = false;
+  int iterations = 0, n_occupied = 0;
+  int64_t tei_rank_b = 0;
+  std::vector<double> orbital_energies, density;
+};
+template <class Mol, class Basis, class Cfg>
+ScfResult scf_solve(const Mol& mol, const Basis& bs, const Cfg& cfg) {
+  std::vector<double> centers, exps, coefs, charges, ncent;
+  std::vector<int> degs;
+  std::vector<int64_t> off(1, 0);
+  for (const auto& f : bs.functions) {
+    for (int ax = 0; ax < 3; ++ax) {
+      centers.push_back(f.center[ax]);
+      degs.push_back(f.degree[ax]);
+    }
+    for (const auto& p : f.primitives) {
+      exps.push_back(p.exponent);
+      coefs.push_back(p.coeff);
+    }
+    off.push_back(static_cast<int64_t>(exps.size()));
+  }
+  for (const auto& nu : mol.nuclei) {
+    charges.push_back(nu.charge);
+    for (int ax = 0; ax < 3; ++ax) ncent.push_back(nu.center[ax]);
+  }
+  tgb_basis_spec spec{};
+  for (int ax = 0; ax < 3; ++ax) {
+    spec.b_half[ax] = bs.grid.b_half[ax];
+    spec.n[ax] = static_cast<int64_t>(bs.grid.n[ax]);
+  }
+  spec.nfn = static_cast<int64_t>(bs.functions.size());
+  spec.centers = centers.data();
+  spec.degrees = degs.data();
+  spec.prim_offset = off.data();
+  spec.exponents = exps.data();
+  spec.coeffs = coefs.data();
+  tgb_molecule m{static_cast<int64_t>(mol.nuclei.size()), charges.data(), ncent.data(),
+                 static_cast<int64_t>(mol.n_electrons)};
+  tgb_scf_config c{};
+  c.max_iterations = cfg.max_iterations;
+  c.energy_tol = cfg.energy_tol;
+  c.mixing = cfg.mixing;
+  c.eps_fit = cfg.eps_fit;
+  c.eps_chol = cfg.eps_chol;
+  c.kernel_eps = cfg.kernel_eps;
+  c.kernel_r_max = cfg.kernel_r_max;
+  c.density_reduce_eps = cfg.density_reduce_eps;
+  c.exact_mass_kinetic = cfg.exact_mass_kinetic ? 1 : 0;
+  ScfResult r;
+  const size_t nb = bs.functions.size();
+  r.orbital_energies.assign(nb, 0.0);
+  r.density.assign(nb * nb, 0.0);
+  tgb_scf_state st{};
+  st.orbital_energies = r.orbital_energies.data();
+  st.density = r.density.data();
+  check(tgb_scf_solve(context(), &m, &spec, &c, &st));
+  r.energy = st.energy;
+  r.nuclear_energy = st.nuclear_energy;
+  r.converged = st.converged != 0;
+  r.iterations = st.iterations;
+  r.n_occupied = st.n_occupied;
+  r.tei_rank_b = st.tei_rank_b;
+  return r;
+}
+
+// tg::mp2_energy (mp2.cpp:60-105): mode 0 = MP2Mode::oracle, 1 = factorized.
+// factor is the MOCholesky factor (N_ov x R_B, column-major); energies the
+// MOSpace orbital energies (ascending).  The reference's NumericalError for a
+// non-positive denominator gap.
+template <class Matrix, class Vector>
+double mp2_energy(const Matrix& factor, int64_t n_occ, int64_t n_vir, const Vector& energies, int mode = 0,
+                  double expsum_eps = 1e-9) {
+  double e = 0.0;
+  check(tgb_mp2_energy(context(), n_occ, n_vir, static_cast<int64_t>(factor.cols()), factor.data(), energies.data(),
+                       mode, expsum_eps, &e, TGB_MEM_HOST));
+  return e;
 }
 
 }  // namespace tgb_cpp

@@ -10,19 +10,42 @@ ROOT = Path(__file__).resolve().parent.parent
 EXE = ROOT / "tests" / "cpp" / "test_cpp_api.bin"
 
 
-def build_exe():
+REF_INCLUDE = Path("/root/reference/proj/include")
+
+
+def build_exe(exe=EXE, extra=()):
     src = ROOT / "tests" / "cpp" / "test_cpp_api.cpp"
-    if EXE.exists() and EXE.stat().st_mtime > max(src.stat().st_mtime,
-                                                   (ROOT / "paper_1504_06289_b200" / "libtgb.so").stat().st_mtime):
+    hdr = ROOT / "include" / "tengrid_b200" / "tengrid.hpp"
+    if exe.exists() and exe.stat().st_mtime > max(src.stat().st_mtime, hdr.stat().st_mtime,
+                                                  (ROOT / "paper_1504_06289_b200" / "libtgb.so").stat().st_mtime):
         return
-    subprocess.run(["g++", "-std=c++17", "-O1", "-I", str(ROOT / "include"), "-I", str(ROOT / "oracle" / "eigen_shim"),
+    subprocess.run(["g++", "-std=c++17", "-O1", *extra, "-I", str(ROOT / "include"),
+                    "-I", str(ROOT / "oracle" / "eigen_shim"),
                     str(src), "-L", str(ROOT / "paper_1504_06289_b200"), "-ltgb",
-                    f"-Wl,-rpath,{ROOT / 'paper_1504_06289_b200'}", "-o", str(EXE)], check=True)
+                    f"-Wl,-rpath,{ROOT / 'paper_1504_06289_b200'}", "-o", str(exe)], check=True)
 
 
 def test_cpp_header_compiles_and_links():
     build_exe()
     assert EXE.exists()
+
+
+def test_cpp_header_maps_host_errors_to_reference_types():
+    # expsum_for_interval -> tg::NumericalError (test_kernel.cpp:88); snap_to_node
+    # -> std::domain_error / tg::SnapError (test_grid.cpp:100-106); no GPU needed
+    build_exe()
+    r = subprocess.run([str(EXE), "--host-only"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+@pytest.mark.skipif(not REF_INCLUDE.exists(), reason="reference include tree only in the build container")
+def test_cpp_header_finds_reference_exception_classes():
+    # a reference build (proj/include on the include path) gets tg::SnapError /
+    # tg::NumericalError from <tengrid/common.hpp> itself, no macros
+    exe = ROOT / "tests" / "cpp" / "test_cpp_api_refhdr.bin"
+    build_exe(exe, ("-DTGB_TEST_REFERENCE_HEADERS", "-I", str(REF_INCLUDE)))
+    r = subprocess.run([str(exe), "--host-only"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 @pytest.mark.gpu
