@@ -40,7 +40,7 @@ def build_lib(force: bool = False) -> Path:
     from concurrent.futures import ThreadPoolExecutor
 
     srcs = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
-    hdrs = sorted(CSRC.glob("*.hpp")) + [ROOT / "include" / "tgb.h"]
+    hdrs = sorted(CSRC.glob("*.hpp")) + sorted(CSRC.glob("*.cuh")) + [ROOT / "include" / "tgb.h"]
     hdrs += sorted((ROOT / "include" / "tengrid_b200").glob("*.hpp"))
     objdir = ROOT / "build" / "libtgb"
     objdir.mkdir(parents=True, exist_ok=True)

@@ -1,0 +1,491 @@
+// Config-2 plan of the mode convolutions (n = 16385, BASELINE.json configs[2]):
+// circular length m = 24576 = 2 N, N = 12288 = 16 * 16 * 3 * 16 — the
+// reference's tg::conv_central_many (proj/src/fft.cpp:97-122) for the odd
+// extents whose cheapest plan is this N.
+//
+//  * m is ONE below the alias-free minimum at n = 16385: exactly one full-
+//    convolution term aliases into each end of the window (index 0 picks up
+//    full[2n-2] = f[n-1] p[n-1], index n-1 picks up full[0] = f[0] p[0]); the
+//    pair kernel subtracts those two products, so the result equals the
+//    reference's window up to roundoff (tools/proto_n12k.py models the whole
+//    index scheme in numpy).  12288 is 3-smooth: radix-16 stages instead of
+//    the 16 * 10 * 10 * 8 plan of fftconv.cu, 4 % fewer points.
+//  * Natural-order spectra, decimation in frequency from the high digit:
+//    k = kk + 768 s0 (stage 1, radix 16), kk = k1 + 48 s1 (stage 2, radix 16),
+//    k1 = k2 + 16 s2 (stage 3, radix 3), k2 = s3 (stage 4, radix 16); the
+//    output index t = t0 + 16 t1 + 256 t2 + 768 t3 comes out in natural order
+//    in stage 4, which writes the window straight to HBM.
+//  * 384 threads = 12 warps (3 per SM sub-partition).  Stage 1 is one block
+//    pair (kk, 768 - kk) per thread: the real-signal split needs P[k] and
+//    P[N - k] together, and k = kk + 768 s0 mirrors into block 768 - kk, so the
+//    383 regular pairs plus the two self-mirror blocks (0, 384; thread 383)
+//    fill the CTA exactly.  Stages 2 and 4: two radix-16 butterflies per
+//    thread; stage 3: 10.67 radix-3 butterflies per thread.
+//  * The density spectrum A_i of a CTA's i-major run is held in tensor memory
+//    (384 of 512 columns: thread t's 32 stage-1 values in its own lane), the
+//    kernel spectrum B_j (real for mirror-symmetric kernel columns) comes
+//    from L2 in natural order, coalesced.
+//  * Shared memory: 16 segments (t0) of 817 slots (16 rows of 51: 48 data +
+//    3 pad, then 1 pad) = 209 KB; every stage's accesses are bank-conflict
+//    free within a quarter warp (see slot()).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+
+#include "fft_common.cuh"
+#include "tgb_internal.hpp"
+
+namespace tgb {
+namespace k12 {
+
+constexpr int N = 12288, M = 24576, NB = 768, TT = 384;
+constexpr int S0 = 817, SLOTS = 16 * S0;
+constexpr size_t kSmem = static_cast<size_t>(SLOTS) * sizeof(double2);
+
+__device__ __forceinline__ int slot(int t0, int a, int r) { return t0 * S0 + a * 51 + r; }
+__device__ __forceinline__ int slot_kk(int t0, int kk) { return slot(t0, kk / 48, kk % 48); }
+
+// e^{2 pi i e / L}
+__device__ __forceinline__ double2 root(int64_t e, int64_t L) {
+  double s, c;
+  sincospi(2.0 * static_cast<double>(e % L) / static_cast<double>(L), &s, &c);
+  return make_double2(c, s);
+}
+
+// powers w^q, q = 0..R-1, by a log-depth product tree
+template <int R>
+__device__ __forceinline__ void powers(double2 w, double2* wp) {
+  wp[0] = make_double2(1.0, 0.0);
+  wp[1] = w;
+#pragma unroll
+  for (int q = 2; q < R; ++q) wp[q] = (q & 1) ? cmul(wp[q - 1], w) : cmul(wp[q >> 1], wp[q >> 1]);
+}
+
+__device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -a.y); }
+
+// e^{2 pi i u / 32}, u in [0, 16) (a constant after unrolling)
+__device__ __forceinline__ double2 cs32(int u) {
+  constexpr double C[9] = {1.0, 0.98078528040323044913, 0.92387953251128675613, 0.83146961230254523708,
+                           0.70710678118654752440, 0.55557023301960222474, 0.38268343236508977173,
+                           0.19509032201612826785, 0.0};
+  return u <= 8 ? make_double2(C[u], C[8 - u]) : make_double2(-C[16 - u], C[u - 8]);
+}
+
+// Z[k], Z[N-k] from P[k], P[N-k] and w_m^k (the inverse real-signal split):
+// Z[k] = (P[k] + conj P[N-k]) + i w^k (P[k] - conj P[N-k]),  Z[N-k] = conj(sum - i w^k dif)
+__device__ __forceinline__ void zsplit2(double2 p, double2 q, double2 w, double2& zp, double2& zq) {
+  const double2 sum = make_double2(p.x + q.x, p.y - q.y);
+  const double2 dif = make_double2(p.x - q.x, p.y + q.y);
+  const double2 wd = cmul(w, dif);
+  zp = make_double2(sum.x - wd.y, sum.y + wd.x);
+  zq = make_double2(sum.x + wd.y, wd.x - sum.y);
+}
+
+// ---------------------------------------------------------------- stages 2, 3 (in place, shared memory)
+
+template <int S>
+__device__ __forceinline__ void stage2(double2* sm, int tid, double2 w2base) {
+  const int k1 = tid % 48, t0a = tid / 48;
+  double2 w2[16];  // formed per call: keeping 15 powers live across the pair loop costs 60 registers
+  powers<16>(w2base, w2);
+#pragma unroll 1
+  for (int h = 0; h < 2; ++h) {
+    const int t0 = t0a + 8 * h;
+    double2* p = sm + slot(t0, 0, k1);
+    double2 v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = p[51 * s];
+    dft<16, S>(v);
+#pragma unroll
+    for (int t = 1; t < 16; ++t) v[t] = cmul(v[t], w2[t]);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) p[51 * t] = v[t];
+  }
+}
+
+template <int S>
+__device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double2 w32) {
+  const int k2 = tid & 15;
+#pragma unroll 2
+  for (int b = tid; b < 4096; b += TT) {
+    const int t1 = (b >> 4) & 15, t0 = b >> 8;
+    double2* p = sm + slot(t0, t1, k2);
+    double2 v0 = p[0], v1 = p[16], v2 = p[32];
+    dft3<S>(v0, v1, v2);
+    p[0] = v0;
+    p[16] = cmul(v1, w31);
+    p[32] = cmul(v2, w32);
+  }
+}
+
+// ---------------------------------------------------------------- forward spectra
+
+// One CTA per column: columns [0, nB) are kernel columns (modeB: 1 real form
+// hm Re(X e^{2 pi i k ofs/m}), 2 complex form hm X e^{2 pi i k ofs/m}, 3 both),
+// columns [nB, nB + nA) density columns (complex X).  Spectra: N + 1
+// natural-order entries per column.
+__global__ void __launch_bounds__(TT, 1)
+    k12_spectrum_kernel(int n, const double* __restrict__ XA, int nA, double2* __restrict__ specA,
+                        const double* __restrict__ XB, int nB, double* __restrict__ specBr,
+                        double2* __restrict__ specBc, int modeB, int64_t ldx, double h) {
+  extern __shared__ double2 sm[];
+  double2* zlo = sm + SLOTS;   // w_m^{-i}, i < 64
+  double2* zhi = zlo + 64;     // w_m^{-64 j}, j < M / 64
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 64 + M / 64; i += TT) {
+    const double2 w = i < 64 ? root(i, M) : root(64LL * (i - 64), M);
+    (i < 64 ? zlo[i] : zhi[i - 64]) = cconj(w);
+  }
+  const bool isB = static_cast<int>(blockIdx.x) < nB;
+  const int c = isB ? blockIdx.x : blockIdx.x - nB;
+  const double* x = (isB ? XB : XA) + static_cast<int64_t>(c) * ldx;
+  // stage 1: blocks tt = tid, tid + 384: inputs z[tt + 768 s0], z[t] = x[2t] + i x[2t+1]
+#pragma unroll 1
+  for (int hb = 0; hb < 2; ++hb) {
+    const int tt = tid + TT * hb;
+    double2 v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int i0 = 2 * (tt + NB * s);
+      v[s].x = i0 < n ? __ldg(x + i0) : 0.0;
+      v[s].y = i0 + 1 < n ? __ldg(x + i0 + 1) : 0.0;
+    }
+    dft<16, -1>(v);
+    double2 wp[16];
+    powers<16>(cconj(root(tt, N)), wp);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) sm[slot_kk(t, tt)] = t ? cmul(v[t], wp[t]) : v[t];
+  }
+  __syncthreads();
+  stage2<-1>(sm, tid, cconj(root(tid % 48, 768)));
+  __syncthreads();
+  {
+    const double2 w31 = cconj(root(tid & 15, 48));
+    stage3<-1>(sm, tid, w31, cmul(w31, w31));
+  }
+  __syncthreads();
+  // stage 4: natural-order Z[u + 768 k3]; held in registers until every thread has read its inputs
+  double2 za[16], zb[16];
+#pragma unroll
+  for (int hb = 0; hb < 2; ++hb) {
+    const int u = tid + TT * hb;
+    const double2* p = sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8));
+    double2* v = hb ? zb : za;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = p[s];
+    dft<16, -1>(v);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int hb = 0; hb < 2; ++hb) {
+    const int u = tid + TT * hb;
+    const double2* v = hb ? zb : za;
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      const int k = u + NB * t;
+      sm[k + (k >> 4)] = v[t];
+    }
+  }
+  __syncthreads();
+  // real post-processing: X[k] = (Z_k + conj Z_{N-k})/2 - i w^-k (Z_k - conj Z_{N-k})/2, k = 0..N
+  const double hm = h / M;
+  const int64_t base = static_cast<int64_t>(c) * (N + 1);
+  const int64_t ofs = (n - 1) / 2;
+  for (int k = tid; k <= N; k += TT) {
+    const int ka = k == N ? 0 : k, kb = ka == 0 ? 0 : N - ka;  // Z_N = Z_0
+    const double2 zk = sm[ka + (ka >> 4)];
+    double2 zm = sm[kb + (kb >> 4)];
+    zm.y = -zm.y;
+    const double2 sum = cadd(zk, zm), dif = csub(zk, zm);
+    const double2 wd = cmul(cmul(zlo[k & 63], zhi[k >> 6]), dif);
+    double2 X = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
+    if (k == 0 || k == N) X.y = 0.0;  // DC and Nyquist of a real signal
+    if (!isB) {
+      specA[base + k] = X;
+    } else {
+      const int64_t e = (static_cast<int64_t>(k) * ofs) % M;
+      const double2 ph = cconj(cmul(zlo[e & 63], zhi[e >> 6]));  // e^{+2 pi i k ofs/m}
+      const double2 y = cmul(X, ph);
+      if (modeB & 1) specBr[base + k] = hm * y.x;
+      if (modeB & 2) specBc[base + k] = cscale(y, hm);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- pair kernel
+
+// Stage-1 item of thread tid.  Regular (tid < 383): block kk = tid + 1 and its
+// mirror 768 - kk from the 16 split pairs (k, N - k), k = kk + 768 u.
+// Self (tid == 383): blocks 0 and 384; pair u < 8: k = 768 u (u = 0: N - k = N,
+// the Nyquist term), u >= 8: k = 384 + 768 (u - 8); plus Z[6144] (the centre of
+// block 0) from one extra split.
+__device__ __forceinline__ int item_ka(int tid, int u) {
+  return tid < TT - 1 ? tid + 1 + NB * u : (u < 8 ? NB * u : 384 + NB * (u - 8));
+}
+
+template <bool BREAL>
+__device__ __forceinline__ double2 bmul(double2 a, const void* B, int k) {
+  if constexpr (BREAL)
+    return cscale(a, __ldg(static_cast<const double*>(B) + k));
+  else
+    return cmul(a, ld2(static_cast<const double2*>(B) + k));
+}
+
+template <bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    k12_pair_kernel(const double2* __restrict__ specA, const void* __restrict__ specB,
+                    const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out,
+                    const double* __restrict__ U, int64_t ldu, const double* __restrict__ V, int64_t ldv, double h,
+                    int n, int alias) {
+  if ((winfo[1] != 0) != BREAL) return;
+  const int nwork = winfo[0];
+  __shared__ uint32_t tmem_base_sh;
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) {
+    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base_sh));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tbase = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
+                         static_cast<uint32_t>((warp >> 2) * 128);
+  const bool self = tid == TT - 1;
+  const int kk = tid + 1;
+  // per-thread constants: split twiddle base w_m^kk in registers; the stage-2/3
+  // twiddle bases in a per-thread shared-memory table (registers are the limit)
+  const double2 wkk = self ? make_double2(1.0, 0.0) : root(kk, M);
+  double2* cst = sm + SLOTS + 3 * tid;
+  cst[0] = root(tid % 48, 768);
+  cst[1] = root(tid & 15, 48);
+  cst[2] = cmul(cst[1], cst[1]);
+  const int nz = (n + 1) >> 1;
+  const bool odd_n = n & 1;
+  const int kX = self ? 0 : kk, kY = self ? 384 : NB - kk;
+  const int u_last = (nz - 1) % NB;  // stage-4 butterfly holding x[n-1]
+
+  const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
+  const int w1 = static_cast<int>((static_cast<int64_t>(nwork) * (blockIdx.x + 1)) / gridDim.x);
+  int ia_cur = -1;
+  for (int w = w0; w < w1; ++w) {
+    const PairEntry e = work[w];
+    const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
+    // alias corrections at the window ends, loaded early: x[0] -= h f[n-1] p[n-1], x[n-1] -= h f[0] p[0]
+    double corr0 = 0.0, corr1 = 0.0;
+    if (alias && tid == 0) corr0 = h * __ldg(U + e.ia * ldu + n - 1) * __ldg(V + e.jb * ldv + n - 1);
+    if (alias && tid == u_last % TT) corr1 = h * __ldg(U + e.ia * ldu) * __ldg(V + e.jb * ldv);
+    if (e.ia != ia_cur) {  // CTA-uniform: a new density column -> tensor memory
+      ia_cur = e.ia;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {  // chunk c: u = 8 (c & 1) + [0, 8); c < 2: P[k], else P[N - k]
+        uint32_t r[32];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int u = 8 * (c & 1) + q;
+          const int ka = item_ka(tid, u);
+          const double2 v = ld2(a + (c < 2 ? ka : N - ka));
+          r[4 * q + 0] = __double2loint(v.x);
+          r[4 * q + 1] = __double2hiint(v.x);
+          r[4 * q + 2] = __double2loint(v.y);
+          r[4 * q + 3] = __double2hiint(v.y);
+        }
+        tmem_st32(tbase + 32 * c, r);
+      }
+      tmem_wait_st();
+    }
+    // ---- stage 1: products, real split, two radix-16 blocks per thread.  Z[k] stays in
+    // registers (block X), Z[N-k] goes to this thread's own block-Y slots in natural order;
+    // the warp holding the self thread stashes both (its routing differs per lane).
+    {
+      const bool w11 = warp == TT / 32 - 1;
+      const double2 wkh = self ? make_double2(0.99518472667219688624, 0.09801714032956060199) : wkk;  // w_m^384
+      double2 x[16];
+#pragma unroll
+      for (int hf = 0; hf < 4; ++hf) {
+        uint32_t ra[16], rb[16];
+        tmem_ld16(tbase + 16 * hf, ra);
+        tmem_ld16(tbase + 64 + 16 * hf, rb);
+        tmem_wait_ld();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int u = 4 * hf + q;
+          const int ka = item_ka(tid, u);
+          const double2 av = make_double2(__hiloint2double(ra[4 * q + 1], ra[4 * q + 0]),
+                                          __hiloint2double(ra[4 * q + 3], ra[4 * q + 2]));
+          const double2 an = make_double2(__hiloint2double(rb[4 * q + 1], rb[4 * q + 0]),
+                                          __hiloint2double(rb[4 * q + 3], rb[4 * q + 2]));
+          const double2 pk = bmul<BREAL>(av, b, ka), pn = bmul<BREAL>(an, b, N - ka);
+          // w_m^ka = w_m^kk e^{2 pi i u / 32} (regular); self: e^{2 pi i u / 32}, then w_m^384 e^{2 pi i (u-8) / 32}
+          const double2 wk = cmul(u < 8 ? wkk : wkh, self && u >= 8 ? cs32(u - 8) : cs32(u));
+          double2 zq;
+          zsplit2(pk, pn, wk, x[u], zq);
+          if (!w11) {
+            sm[slot_kk(15 - u, kY)] = zq;  // Z[N - k] = Z[kY + 768 (15 - u)]
+          } else if (!self) {
+            sm[slot_kk(15 - u, kY)] = zq;
+            sm[slot_kk(u, kX)] = x[u];
+          } else {  // blocks 0 and 384 in natural order
+            if (u < 8) {
+              sm[slot_kk(u, 0)] = x[u];
+              if (u > 0) sm[slot_kk(16 - u, 0)] = zq;
+            } else {
+              sm[slot_kk(u - 8, 384)] = x[u];
+              sm[slot_kk(23 - u, 384)] = zq;
+            }
+          }
+        }
+      }
+      if (w11) {
+        if (self) {  // centre of block 0: Z[N/2]
+          const double2 pc = bmul<BREAL>(ld2(a + N / 2), b, N / 2);
+          double2 zc, dummy;
+          zsplit2(pc, pc, make_double2(0.0, 1.0), zc, dummy);  // w_m^{N/2} = i
+          sm[slot_kk(8, 0)] = zc;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < 16; ++s) x[s] = sm[slot_kk(s, kX)];
+      }
+      // block X: DFT, twiddles w_N^{kX t} by recurrence, store
+      const double2 wX = self ? make_double2(1.0, 0.0) : cmul(wkk, wkk);  // w_N^kk = w_m^{2 kk}
+      dft<16, 1>(x);
+      {
+        double2 wt = wX;
+        sm[slot_kk(0, kX)] = x[0];
+#pragma unroll
+        for (int t = 1; t < 16; ++t) {
+          sm[slot_kk(t, kX)] = cmul(x[t], wt);
+          wt = cmul(wt, wX);
+        }
+      }
+      // block Y: natural-order stash, loaded rotated by one (absorbs e^{2 pi i t/16}); twiddles
+      // conj(w_N^{(768 - kY) t}) = w_N^{kY t} e^{-2 pi i t/16}
+      double2 y[16];
+#pragma unroll
+      for (int s = 0; s < 16; ++s) y[s] = sm[slot_kk((s + 15) & 15, kY)];
+      dft<16, 1>(y);
+      {
+        const double2 wY = cconj(self ? cs32(1) : wX);  // w_N^{384} = e^{2 pi i / 32}
+        double2 wt = wY;
+        sm[slot_kk(0, kY)] = y[0];
+#pragma unroll
+        for (int t = 1; t < 16; ++t) {
+          sm[slot_kk(t, kY)] = cmul(y[t], wt);
+          wt = cmul(wt, wY);
+        }
+      }
+    }
+    __syncthreads();
+    stage2<1>(sm, tid, cst[0]);
+    __syncthreads();
+    stage3<1>(sm, tid, cst[1], cst[2]);
+    __syncthreads();
+    // ---- stage 4: radix 16, window straight to HBM
+    {
+      double* o0 = out + e.out0;
+      double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+      const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
+#pragma unroll 1
+      for (int hb = 0; hb < 2; ++hb) {
+        const int u = tid + TT * hb;
+        const double2* p = sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8));
+        double2 v[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s) v[s] = p[s];
+        dft<16, 1>(v);
+#pragma unroll
+        for (int t3 = 0; t3 < 16; ++t3) {
+          const int t = u + NB * t3;
+          if (t >= nz) break;
+          if (alias) {
+            if (t == 0) v[t3].x -= corr0;
+            if (t == nz - 1) v[t3].x -= corr1;
+          }
+          const bool full = !(odd_n && t == nz - 1);
+          if (aligned && full) {
+            __stcs(reinterpret_cast<double2*>(o0 + 2 * t), v[t3]);
+            if (o1) __stcs(reinterpret_cast<double2*>(o1 + 2 * t), v[t3]);
+          } else {
+            __stcs(o0 + 2 * t, v[t3].x);
+            if (full) __stcs(o0 + 2 * t + 1, v[t3].y);
+            if (o1) {
+              __stcs(o1 + 2 * t, v[t3].x);
+              if (full) __stcs(o1 + 2 * t + 1, v[t3].y);
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh) : "memory");
+}
+
+}  // namespace k12
+
+// ---------------------------------------------------------------- host side
+
+// Applicable: odd n whose window fits m = 24576 with at most the one-term
+// correction at each end, when the generic plan would not pick a smaller N.
+bool k12_applicable(int64_t n, int64_t generic_N) {
+  if (getenv("TGB_NO_K12")) return false;
+  if (n % 2 == 0 || n < 3) return false;
+  const int64_t need = (3 * n - 3) / 2;  // m must be >= need (== need: one aliased term per end)
+  return need <= k12::M && generic_N >= k12::N;
+}
+
+bool k12_alias(int64_t n) { return (3 * n - 3) / 2 == k12::M; }
+
+void k12_spectra(tgb_ctx* ctx, int64_t n, const double* A, int nA, double2* specA, const double* B, int nB,
+                 double* specBr, double2* specBc, int modeB, int64_t ldx, double h) {
+  if (nA + nB == 0) return;
+  static bool attr[kTgbMaxDevices] = {};
+  const size_t smem = k12::kSmem + (64 + k12::M / 64) * sizeof(double2);
+  if (!attr[ctx->device]) {
+    TGB_CUDA(cudaFuncSetAttribute(k12::k12_spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    attr[ctx->device] = true;
+  }
+  k12::k12_spectrum_kernel<<<nA + nB, k12::TT, smem, ctx->stream>>>(static_cast<int>(n), A, nA, specA, B, nB, specBr,
+                                                                     specBc, modeB, ldx, h);
+  TGB_LAUNCHED(ctx);
+}
+
+constexpr size_t kPairSmem = k12::kSmem + 3 * k12::TT * sizeof(double2);  // + per-thread twiddle bases
+
+template <bool BREAL>
+static void k12_pairs_t(tgb_ctx* ctx, int64_t n, const double2* specA, const void* specB, const PairEntry* work,
+                        const int* winfo, double* out, const double* U, int64_t ldu, const double* V, int64_t ldv,
+                        double h) {
+  static bool attr[kTgbMaxDevices] = {};
+  if (!attr[ctx->device]) {
+    cudaFuncAttributes fa{};
+    TGB_CUDA(cudaFuncGetAttributes(&fa, k12::k12_pair_kernel<BREAL>));
+    TGB_CUDA(cudaFuncSetAttribute(k12::k12_pair_kernel<BREAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kPairSmem)));
+    attr[ctx->device] = true;
+  }
+  prof_begin(ctx);
+  k12::k12_pair_kernel<BREAL><<<ctx->num_sms, k12::TT, kPairSmem, ctx->stream>>>(
+      specA, specB, work, winfo, out, U, ldu, V, ldv, h, static_cast<int>(n), k12_alias(n) ? 1 : 0);
+  TGB_LAUNCHED(ctx);
+  prof_end(ctx);
+}
+
+void k12_pairs(tgb_ctx* ctx, int64_t n, const double2* specA, const double* specBr, const double2* specBc,
+               const PairEntry* work, const int* winfo, double* out, const double* U, int64_t ldu, const double* V,
+               int64_t ldv, double h) {
+  // both forms; the one that disagrees with the device-side symmetry flag returns at once
+  k12_pairs_t<true>(ctx, n, specA, specBr, work, winfo, out, U, ldu, V, ldv, h);
+  k12_pairs_t<false>(ctx, n, specA, specBc, work, winfo, out, U, ldu, V, ldv, h);
+}
+
+}  // namespace tgb

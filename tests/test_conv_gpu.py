@@ -27,7 +27,7 @@ def window_np(u, v):
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 16, 17, 31, 64, 65, 100, 127, 128, 129, 200, 513, 1000, 1025, 2048,
-                               2049, 4097, 8193])
+                               2049, 4097, 8193, 16383, 16385])
 @pytest.mark.parametrize("force_fft", [False, True])
 def test_conv_central_many_matches_oracle(ctx, n, force_fft):
     rng = Rng(1000 + n)
@@ -55,6 +55,35 @@ def test_conv_large_n_gaussians(ctx):
     got = conv_central_many(U, v, ctx)
     ref = O.conv_central_many(U, v)
     assert relmax(got, ref) <= TOL
+
+
+def test_k12_plan_many_pairs_per_cta(ctx):
+    """The N = 12288 plan (fftconv12k.cu: m = 24576, one aliased term per window end
+    at n = 16385, subtracted exactly) with ~6 pairs per persistent CTA, density-column
+    switches inside a CTA's run, duplicate kernel columns (one result, two output
+    columns), the real-spectrum path (axis 0: every kernel column mirror-symmetric)
+    and the complex path (axes 1, 2: one non-symmetric column).  Sampled output
+    columns against the oracle's conv_central_many (proj/src/fft.cpp:97-122) x h."""
+    dims = (16385, 16383, 16385)
+    ra = 300
+    rng = Rng(4242)
+    fa = [np.asfortranarray(rng.normal(d * ra).reshape(d, ra, order="F")) for d in dims]
+    a = CanonicalTensor3(fa, rng.normal(ra))
+    fb = []
+    for ax, d in enumerate(dims):
+        x = np.arange(d) - 0.5 * (d - 1)
+        g = np.exp(-(x / 900.0) ** 2)
+        c2 = np.exp(-((x / 300.0) ** 2)) if ax == 0 else rng.normal(d)
+        fb.append(np.asfortranarray(np.stack([g, g.copy(), c2], axis=1)))
+    b = CanonicalTensor3(fb, np.ones(3))
+    h = (0.011, 0.013, 0.017)
+    c = convolve(a, b, h, ctx)
+    for ax, d in enumerate(dims):
+        for i in (0, 1, 149, 150, 151, 298, 299):
+            for j in range(3):
+                ref = O.conv_central_many(np.asfortranarray(fa[ax][:, [i]]), np.ascontiguousarray(fb[ax][:, j]))[:, 0]
+                assert relmax(c.factor[ax][:, i + ra * j], h[ax] * ref) <= TOL, (ax, i, j)
+        assert np.array_equal(c.factor[ax][:, 0:ra], c.factor[ax][:, ra:2 * ra])
 
 
 def test_convolve_delta_identity(ctx):
