@@ -32,6 +32,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "fft_common.cuh"
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(TT, 1)
     k12_pair_kernel(const double2* __restrict__ specA, const void* __restrict__ specB,
                     const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out,
                     const double* __restrict__ U, int64_t ldu, const double* __restrict__ V, int64_t ldv, double h,
-                    int n, int alias) {
+                    int n, int alias, unsigned long long* __restrict__ phase) {
   if ((winfo[1] != 0) != BREAL) return;
   const int nwork = winfo[0];
   __shared__ uint32_t tmem_base_sh;
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(TT, 1)
   int ia_cur = -1;
   for (int w = w0; w < w1; ++w) {
     const PairEntry e = work[w];
+    const long long c0 = phase ? clock64() : 0;
     const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
     const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
                           : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
@@ -382,10 +384,13 @@ __global__ void __launch_bounds__(TT, 1)
       }
     }
     __syncthreads();
+    const long long c1 = phase ? clock64() : 0;
     stage2<1>(sm, tid, cst[0]);
     __syncthreads();
+    const long long c2 = phase ? clock64() : 0;
     stage3<1>(sm, tid, cst[1], cst[2]);
     __syncthreads();
+    const long long c3 = phase ? clock64() : 0;
     // ---- stage 4: radix 16, window straight to HBM
     {
       double* o0 = out + e.out0;
@@ -423,6 +428,14 @@ __global__ void __launch_bounds__(TT, 1)
       }
     }
     __syncthreads();
+    if (phase && tid == 0) {
+      const long long c4 = clock64();
+      atomicAdd(phase + 0, static_cast<unsigned long long>(c1 - c0));
+      atomicAdd(phase + 1, static_cast<unsigned long long>(c2 - c1));
+      atomicAdd(phase + 2, static_cast<unsigned long long>(c3 - c2));
+      atomicAdd(phase + 3, static_cast<unsigned long long>(c4 - c3));
+      atomicAdd(phase + 4, 1ULL);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -474,10 +487,24 @@ static void k12_pairs_t(tgb_ctx* ctx, int64_t n, const double2* specA, const voi
     attr[ctx->device] = true;
   }
   prof_begin(ctx);
+  static DevBuf phase_buf;
+  unsigned long long* phase = nullptr;
+  if (getenv("TGB_PHASE_CLK")) {  // analysis only: per-stage SM cycles per pair
+    phase = static_cast<unsigned long long*>(phase_buf.get(8 * sizeof(unsigned long long)));
+    TGB_CUDA(cudaMemsetAsync(phase, 0, 8 * sizeof(unsigned long long), ctx->stream));
+  }
   k12::k12_pair_kernel<BREAL><<<ctx->num_sms, k12::TT, kPairSmem, ctx->stream>>>(
-      specA, specB, work, winfo, out, U, ldu, V, ldv, h, static_cast<int>(n), k12_alias(n) ? 1 : 0);
+      specA, specB, work, winfo, out, U, ldu, V, ldv, h, static_cast<int>(n), k12_alias(n) ? 1 : 0, phase);
   TGB_LAUNCHED(ctx);
   prof_end(ctx);
+  if (phase) {
+    unsigned long long hb[8];
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    TGB_CUDA(cudaMemcpy(hb, phase, sizeof(hb), cudaMemcpyDeviceToHost));
+    if (hb[4])
+      fprintf(stderr, "k12 cycles/pair: stage1 %.0f stage2 %.0f stage3 %.0f stage4 %.0f (pairs %llu)\n",
+              double(hb[0]) / hb[4], double(hb[1]) / hb[4], double(hb[2]) / hb[4], double(hb[3]) / hb[4], hb[4]);
+  }
 }
 
 void k12_pairs(tgb_ctx* ctx, int64_t n, const double2* specA, const double* specBr, const double2* specBc,
