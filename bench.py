@@ -284,28 +284,39 @@ def main():
     import paper_1504_06289_b200 as tg
     from paper_1504_06289_b200.inputs import hartree_case
 
+    from paper_1504_06289_b200 import shard
+
     strong = not args.weak or world == 1
     total_f = R_F if strong else R_F * world
     case = hartree_case(CFG, rank=total_f, nsamples=10_000)
-    # shard the density columns (rank pairs i + R_f j with i in this rank's block)
-    lo = rank * total_f // world
-    hi = (rank + 1) * total_f // world
-    theta = tg.CanonicalTensor3([f[:, lo:hi] for f in case.theta.factor], case.theta.weight[lo:hi])
+    stream = torch.cuda.Stream(device=dev)
+    ctx = tg.Context(local, stream=stream.cuda_stream)
+    if world > 1:  # libtgb-owned NCCL communicator; the id travels over torch.distributed
+        shard.init_nccl_from_torch(ctx)
+    # density columns: strong — the whole density on every rank, libtgb convolves this
+    # rank's block (tgb_hartree_potential_shard, tgb_shard_range); weak — a rank-specific
+    # 500-column block of an N x 500-column density
+    lo, hi = shard.shard_range(total_f, rank, world)
+    theta = (case.theta if strong else
+             tg.CanonicalTensor3([f[:, lo:hi] for f in case.theta.factor], case.theta.weight[lo:hi]))
     kern = case.kernel.tensor
-    ra, rb = theta.rank(), kern.rank()
+    ra, rb = hi - lo, kern.rank()
     n = N_GRID
     units_local = 3 * ra * rb
     units_total = 3 * total_f * rb
 
-    stream = torch.cuda.Stream(device=dev)
-    ctx = tg.Context(local, stream=stream.cuda_stream)
     d_theta = tg.DeviceCP.from_host(theta, device=dev)
     d_kern = tg.DeviceCP.from_host(kern, device=dev)
     d_out = tg.DeviceCP.empty([n, n, n], ra * rb, device=dev)
     h = case.grid.h
+    if not strong:
+        shard.set_comm(ctx, None)  # weak: every rank runs an unsharded hartree_potential on its own block
 
     def step():
-        tg.hartree_potential(d_theta, d_kern, h, ctx, out=d_out)
+        if strong:
+            shard.hartree_potential_shard(d_theta, d_kern, h, ctx, out=d_out)
+        else:
+            tg.hartree_potential(d_theta, d_kern, h, ctx, out=d_out)
 
     def barrier():
         if world > 1:
@@ -347,12 +358,12 @@ def main():
     # ---- validation outside the timed region: V_H at 10^4 sample points, one
     # NCCL allreduce of the per-rank partial sums (the path's only exchange).
     pts = torch.as_tensor(case.samples, device=dev)
-    part = tg.value_at_points(d_out, pts, ctx)
-    wt = d_out.weight  # weights already in place
+    if strong:
+        vh_pts = shard.value_at_allreduce(d_out, pts, ctx)  # libtgb: value_at + one NCCL all-reduce
+    else:
+        vh_pts = tg.value_at_points(d_out, pts, ctx)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.all_reduce(part)
-    samples_vh = part.cpu().numpy()
+    samples_vh = vh_pts.cpu().numpy()
     parity = {"checked": False}
     gold = ROOT / "tests" / "golden" / "reference_cfg2_vh_samples.npz"
     if strong and gold.exists():
@@ -381,8 +392,8 @@ def main():
             traffic = json.loads(tj.read_text()).get("pair_kernel_dram_bytes_per_launch")
         except Exception:
             traffic = None
-    # FP64 work actually issued per launch (inverse FFT length m = 2N = 25600)
-    m = 25600
+    # FP64 work actually issued per launch (config-2 plan: inverse FFT length m = 2N = 24576, fftconv12k.cu)
+    m = 24576
     N = m // 2
     flops_pair = 5.0 * N * np.log2(N) + 16.0 * N  # complex FFT + split + product (nominal)
     fp64_tflops = ra * nd * flops_pair / (avg_launch_ms / 1e3) / 1e12
@@ -390,10 +401,12 @@ def main():
     # ---- e2e through the C-ABI with pinned HOST buffers (copies inside the timed region)
     e2e = None
     if not args.no_e2e:
+        # this rank's density block [lo, hi) in pinned host memory
+        wl = np.ascontiguousarray(theta.weight[lo:hi] if strong else theta.weight)
         th = tg.CanonicalTensor3([torch.empty((ra, n), dtype=torch.float64).pin_memory().numpy().T for _ in range(3)],
-                                 theta.weight)
+                                 wl)
         for ax in range(3):
-            th.factor[ax][:] = theta.factor[ax]
+            th.factor[ax][:] = theta.factor[ax][:, lo:hi] if strong else theta.factor[ax]
         kh = tg.CanonicalTensor3([torch.empty((rb, n), dtype=torch.float64).pin_memory().numpy().T for _ in range(3)],
                                  kern.weight)
         for ax in range(3):
@@ -442,12 +455,12 @@ def main():
                    "l2": "no flush needed: each step writes 8.06 GB of factors (> 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "pair_kernel (inverse FFT + window + store, one launch per axis)",
+                     "kernel": "k12_pair_kernel (product, real split, inverse FFT N=12288, window stores; one launch per axis)",
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_launch_ms,
                      "launch_share_of_step": pair_ms / ms_local if ms_local else None,
                      "fp64": {"achieved_tflops_nominal": fp64_tflops, "peak_tflops": FP64_TFLOPS,
                               "frac": fp64_tflops / FP64_TFLOPS,
-                              "note": "nominal 5 N log2 N + 16 N flops per inverse transform, N = 12800"}},
+                              "note": "nominal 5 N log2 N + 16 N flops per inverse transform, N = 12288"}},
         "gpu_launches": int(launches),
         "clocks": clk,
         "e2e": e2e,

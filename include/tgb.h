@@ -49,6 +49,18 @@ typedef struct tgb_cp {
   double* weight;    /* R */
 } tgb_cp;
 
+/* A communicator for the multi-GPU path (one process per GPU):
+ * allreduce_sum sums `count` doubles in place over all ranks (device memory on
+ * the cudaStream_t `stream` when on_device, else host memory) and returns 0 on
+ * success.  libtgb also owns an NCCL communicator itself (tgb_ctx_init_nccl);
+ * a tgb_comm lets any other backend (MPI, torch.distributed, gloo) stand in. */
+typedef struct tgb_comm {
+  int rank;
+  int world;
+  int (*allreduce_sum)(double* buf, int64_t count, int on_device, void* stream, void* user);
+  void* user;
+} tgb_comm;
+
 /* ---- context -------------------------------------------------------------
  * One CUDA stream per context (`stream` = a cudaStream_t, or NULL for a
  * context-owned stream).  Calls are reentrant across contexts. */
@@ -71,6 +83,27 @@ int tgb_ctx_profile_read(tgb_ctx* ctx, double* total_ms, int64_t* launches);
  * 0 forces the FFT path wherever it exists. */
 int tgb_ctx_set_direct_max(tgb_ctx* ctx, int64_t direct_max);
 
+/* ---- multi-GPU ---------------------------------------------------------------
+ * No reference counterpart (the reference is one CPU process).  The mode
+ * convolutions shard by density column: rank r owns columns [lo, hi) of
+ * tgb_shard_range(theta.rank, r, world) and produces its (hi - lo) * R_b output
+ * columns with no exchange.  Sums over all pairs (V_H at points, J) take ONE
+ * all-reduce over the context's communicator; the TEI convolution matrices
+ * (by kernel term) and diagonal (by pair row) likewise.
+ * tgb_ctx_init_nccl: rank 0 calls tgb_nccl_get_unique_id and distributes the
+ * 128 bytes; every rank then creates the libtgb-owned NCCL communicator.
+ * tgb_ctx_set_comm: a caller-provided communicator (NULL detaches). */
+int tgb_shard_range(int64_t total, int rank, int world, int64_t* lo, int64_t* hi);
+int tgb_nccl_get_unique_id(unsigned char id[128]);
+int tgb_ctx_init_nccl(tgb_ctx* ctx, int rank, int world, const unsigned char id[128]);
+int tgb_ctx_set_comm(tgb_ctx* ctx, const tgb_comm* comm);
+int tgb_ctx_comm_info(tgb_ctx* ctx, int* rank, int* world);
+/* Context-free helpers (host buffers): the sum, and the sum followed by the
+ * exact mirror of the upper triangle that keeps J symmetric (hf.cpp:145-149)
+ * whatever order the all-reduce summed J_km and J_mk in. */
+int tgb_comm_allreduce_host(const tgb_comm* comm, double* buf, int64_t count);
+int tgb_symmetric_allreduce_host(const tgb_comm* comm, double* J, int64_t nb);
+
 /* ---- mode convolutions -----------------------------------------------------
  * replaces tg::conv_central_many (proj/include/tengrid/fft.hpp:30,
  * proj/src/fft.cpp:97-122): out(:, c) = central_window(conv_full(U(:, c), v)). */
@@ -88,10 +121,23 @@ int tgb_convolve(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double h[
 int tgb_hartree_potential(tgb_ctx* ctx, const tgb_cp* theta, const tgb_cp* kernel, const double h[3], tgb_cp* out,
                           int mem);
 
+/* Multi-GPU tg::hartree_potential: this rank's density-column block [lo, hi)
+ * (tgb_shard_range over theta->rank with the context's rank / world) convolved
+ * with the whole kernel; `out` has rank (hi - lo) * kernel->rank, column
+ * (i - lo) + (hi - lo) j.  No communication; a single process gets the full
+ * result (identical to tgb_hartree_potential). */
+int tgb_hartree_potential_shard(tgb_ctx* ctx, const tgb_cp* theta, const tgb_cp* kernel, const double h[3],
+                                tgb_cp* out, int mem);
+
 /* replaces CanonicalTensor3::value_at (tensor.hpp:135-140) for a batch of
  * grid points: out[p] = sum_k w_k f0(i_p,k) f1(j_p,k) f2(l_p,k); ijk is
  * npts x 3 (row-major triples), both in the space given by `mem`. */
 int tgb_value_at(tgb_ctx* ctx, const tgb_cp* t, int64_t npts, const int64_t* ijk, double* out, int mem);
+
+/* value_at of a sharded tensor: each rank evaluates its own columns, then one
+ * all-reduce (the sum over all rank pairs) leaves the full values on every rank. */
+int tgb_value_at_allreduce(tgb_ctx* ctx, const tgb_cp* t_shard, int64_t npts, const int64_t* ijk, double* out,
+                           int mem);
 
 /* ---- assembly --------------------------------------------------------------
  * replaces tg::scalar_product(CanonicalTensor3, CanonicalTensor3)
@@ -106,6 +152,10 @@ int tgb_scalar_product(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, double* r
  * (nb + 1 entries, host memory).  J is nb x nb (space given by `mem`). */
 int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
                        const double h[3], double* J, int mem);
+/* Multi-GPU coulomb_matrix: the partial J over this rank's V_H columns, one
+ * all-reduce of the N_b x N_b partials, then the exact mirror. */
+int tgb_coulomb_matrix_allreduce(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
+                                 const tgb_cp* vh_shard, const double h[3], double* J, int mem);
 
 /* ---- Hartree-Fock operators on the same path -------------------
  * replaces tg::nuclear_potential_tensor (hf.hpp:29-30, hf.cpp:89-101):

@@ -50,6 +50,13 @@ class tgb_cp(C.Structure):
     _fields_ = [("n", C.c_int64 * 3), ("rank", C.c_int64), ("factor", C.c_void_p * 3), ("weight", C.c_void_p)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_int, C.c_void_p, C.c_void_p)
+
+
+class tgb_comm(C.Structure):
+    _fields_ = [("rank", C.c_int), ("world", C.c_int), ("allreduce_sum", ALLREDUCE_FN), ("user", C.c_void_p)]
+
+
 class tgb_scf_config(C.Structure):
     _fields_ = [("max_iterations", C.c_int), ("energy_tol", C.c_double), ("mixing", C.c_double),
                 ("eps_fit", C.c_double), ("eps_chol", C.c_double), ("kernel_eps", C.c_double),
@@ -96,6 +103,16 @@ def lib() -> C.CDLL:
             "tgb_ctx_set_direct_max": (I, [P, I64]),
             "tgb_ctx_set_profiling": (I, [P, I]),
             "tgb_ctx_profile_read": (I, [P, C.POINTER(D), C.POINTER(I64)]),
+            "tgb_shard_range": (I, [I64, I, I, C.POINTER(I64), C.POINTER(I64)]),
+            "tgb_nccl_get_unique_id": (I, [P]),
+            "tgb_ctx_init_nccl": (I, [P, I, I, P]),
+            "tgb_ctx_set_comm": (I, [P, C.POINTER(tgb_comm)]),
+            "tgb_ctx_comm_info": (I, [P, C.POINTER(I), C.POINTER(I)]),
+            "tgb_comm_allreduce_host": (I, [C.POINTER(tgb_comm), P, I64]),
+            "tgb_symmetric_allreduce_host": (I, [C.POINTER(tgb_comm), P, I64]),
+            "tgb_hartree_potential_shard": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),
+            "tgb_value_at_allreduce": (I, [P, C.POINTER(tgb_cp), I64, P, P, I]),
+            "tgb_coulomb_matrix_allreduce": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, P, I]),
             "tgb_conv_central_many": (I, [P, I64, I64, P, P, P, I]),
             "tgb_convolve": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),
             "tgb_hartree_potential": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),

@@ -204,6 +204,7 @@ int tgb_ctx_destroy(tgb_ctx* ctx) {
     cudaStreamDestroy(ctx->copy_stream);
     cudaStreamDestroy(ctx->aux_stream);
     if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    tgb::comm_release(ctx);
     delete ctx;
   });
 }
@@ -282,6 +283,29 @@ int tgb_hartree_potential(tgb_ctx* ctx, const tgb_cp* theta, const tgb_cp* kerne
   });
 }
 
+int tgb_hartree_potential_shard(tgb_ctx* ctx, const tgb_cp* theta, const tgb_cp* kernel, const double h[3],
+                                tgb_cp* out, int mem) {
+  return guarded([&] {
+    tgb::require(ctx != nullptr, "hartree_potential_shard: null context");
+    check_cp(theta, "hartree_potential_shard");
+    tgb::require(h && h[0] > 0.0 && h[1] > 0.0 && h[2] > 0.0, "convolve: mesh size must be positive");
+    int64_t lo = 0, hi = 0;
+    tgb::shard_range(theta->rank, ctx->comm_rank, ctx->comm_size, &lo, &hi);
+    tgb_cp part = *theta;  // columns [lo, hi): column-major factors, zero-copy
+    part.rank = hi - lo;
+    for (int ax = 0; ax < 3; ++ax) part.factor[ax] = theta->factor[ax] ? theta->factor[ax] + lo * theta->n[ax] : nullptr;
+    part.weight = theta->weight ? theta->weight + lo : nullptr;
+    convolve_impl(ctx, &part, kernel, h, out, mem, 1.0 / (h[0] * h[1] * h[2]));  // hf.cpp:136
+  });
+}
+
+int tgb_value_at_allreduce(tgb_ctx* ctx, const tgb_cp* t_shard, int64_t npts, const int64_t* ijk, double* out,
+                           int mem) {
+  const int rc = tgb_value_at(ctx, t_shard, npts, ijk, out, mem);
+  if (rc != TGB_OK) return rc;
+  return guarded([&] { tgb::comm_allreduce(ctx, out, npts, mem == TGB_MEM_DEVICE); });
+}
+
 int tgb_value_at(tgb_ctx* ctx, const tgb_cp* t, int64_t npts, const int64_t* ijk, double* out, int mem) {
   return guarded([&] {
     check_cp(t, "value_at");
@@ -314,23 +338,46 @@ int tgb_scalar_product(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, double* r
   });
 }
 
+namespace {
+// J (host vector) from basis / V_H in the space given by `mem`
+void coulomb_to_host(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
+                     const double h[3], int mem, std::vector<double>& hj) {
+  check_cp(basis, "coulomb_matrix");
+  check_cp(vh, "coulomb_matrix");
+  check_extents(basis, vh, "coulomb_matrix");
+  tgb::require(nb >= 0 && fn_offset && fn_offset[0] == 0 && fn_offset[nb] == basis->rank,
+               "coulomb_matrix: bad basis function offsets");
+  for (int64_t k = 0; k < nb; ++k) tgb::require(fn_offset[k + 1] > fn_offset[k], "coulomb_matrix: empty function");
+  TGB_CUDA(cudaSetDevice(ctx->device));
+  DevCP db(basis, mem == TGB_MEM_DEVICE), dv(vh, mem == TGB_MEM_DEVICE);
+  hj.assign(nb * nb, 0.0);
+  tgb::coulomb_matrix_dev(ctx, db.t, fn_offset, nb, dv.t, h[0] * h[1] * h[2], hj.data());
+}
+
+void put_matrix(const std::vector<double>& hj, double* J, int mem) {
+  if (mem == TGB_MEM_DEVICE)
+    TGB_CUDA(cudaMemcpy(J, hj.data(), hj.size() * sizeof(double), cudaMemcpyHostToDevice));
+  else
+    std::memcpy(J, hj.data(), hj.size() * sizeof(double));
+}
+}  // namespace
+
 int tgb_coulomb_matrix(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb, const tgb_cp* vh,
                        const double h[3], double* J, int mem) {
   return guarded([&] {
-    check_cp(basis, "coulomb_matrix");
-    check_cp(vh, "coulomb_matrix");
-    check_extents(basis, vh, "coulomb_matrix");
-    tgb::require(nb >= 0 && fn_offset && fn_offset[0] == 0 && fn_offset[nb] == basis->rank,
-                 "coulomb_matrix: bad basis function offsets");
-    for (int64_t k = 0; k < nb; ++k) tgb::require(fn_offset[k + 1] > fn_offset[k], "coulomb_matrix: empty function");
-    TGB_CUDA(cudaSetDevice(ctx->device));
-    DevCP db(basis, mem == TGB_MEM_DEVICE), dv(vh, mem == TGB_MEM_DEVICE);
-    std::vector<double> hj(nb * nb);
-    tgb::coulomb_matrix_dev(ctx, db.t, fn_offset, nb, dv.t, h[0] * h[1] * h[2], hj.data());
-    if (mem == TGB_MEM_DEVICE)
-      TGB_CUDA(cudaMemcpy(J, hj.data(), hj.size() * sizeof(double), cudaMemcpyHostToDevice));
-    else
-      std::memcpy(J, hj.data(), hj.size() * sizeof(double));
+    std::vector<double> hj;
+    coulomb_to_host(ctx, basis, fn_offset, nb, vh, h, mem, hj);
+    put_matrix(hj, J, mem);
+  });
+}
+
+int tgb_coulomb_matrix_allreduce(tgb_ctx* ctx, const tgb_cp* basis, const int64_t* fn_offset, int64_t nb,
+                                 const tgb_cp* vh_shard, const double h[3], double* J, int mem) {
+  return guarded([&] {
+    std::vector<double> hj;
+    coulomb_to_host(ctx, basis, fn_offset, nb, vh_shard, h, mem, hj);
+    tgb::symmetric_allreduce_host(nullptr, ctx, hj.data(), nb);
+    put_matrix(hj, J, mem);
   });
 }
 

@@ -129,11 +129,19 @@ struct tgb_ctx {
   // pointers are never shared across contexts or devices)
   std::map<std::string, tgb::DevBuf> named;
   std::map<std::string, std::array<tgb::DevBuf, 3>> named3;
-  void* nccl_comm = nullptr;  // ncclComm_t (tgb_ctx_set_comm), owned by the caller
+  // multi-GPU (comm.cpp): a libtgb-owned NCCL communicator or a caller's tgb_comm
+  void* nccl_comm = nullptr;  // ncclComm_t (tgb_ctx_init_nccl)
+  bool own_nccl = false;
+  tgb_comm user_comm{};
   int comm_rank = 0, comm_size = 1;
 };
 
 namespace tgb {
+// comm.cpp: sums over the context's ranks (no-ops on a single process)
+void comm_allreduce(tgb_ctx* ctx, double* buf, int64_t count, bool on_device);
+void symmetric_allreduce_host(const tgb_comm* c, tgb_ctx* ctx, double* J, int64_t nb);
+void shard_range(int64_t total, int rank, int world, int64_t* lo, int64_t* hi);
+void comm_release(tgb_ctx* ctx);
 // a named per-context workspace (replaces function-static buffers)
 inline DevBuf& ctx_buf(tgb_ctx* ctx, const std::string& name) { return ctx->named[name]; }
 inline std::array<DevBuf, 3>& ctx_buf3(tgb_ctx* ctx, const std::string& name) { return ctx->named3[name]; }

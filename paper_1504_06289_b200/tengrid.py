@@ -63,6 +63,14 @@ class Context:
         check(lib().tgb_ctx_profile_read(self._h, C.byref(ms), C.byref(cnt)))
         return ms.value, cnt.value
 
+    def torch_stream(self):
+        """This context's stream as a torch ExternalStream (cached)."""
+        import torch
+
+        if getattr(self, "_tstream", None) is None:
+            self._tstream = torch.cuda.ExternalStream(self.stream, device=torch.device("cuda", self.device))
+        return self._tstream
+
     def close(self) -> None:
         if self._h:
             check(lib().tgb_ctx_destroy(self._h))
@@ -195,6 +203,34 @@ class DeviceCP:
         return s
 
 
+def _stream_order(ctx: "Context", *objs) -> None:
+    """Device calls run asynchronously on the context's stream: order torch's
+    current stream after the call, so torch ops reading the results see them
+    and memory the caching allocator hands out again on that stream (a freed
+    input, say) is not overwritten while the call still reads it.  The calls
+    themselves first wait for torch's current stream (_stream_enter)."""
+    import torch
+
+    if not any(isinstance(o, (DeviceCP, torch.Tensor)) for o in objs):
+        return
+    dev = torch.device("cuda", ctx.device)
+    cur = torch.cuda.current_stream(dev)
+    s = ctx.torch_stream()
+    if cur.cuda_stream != s.cuda_stream:
+        cur.wait_stream(s)
+
+
+def _stream_enter(ctx: "Context") -> None:
+    """The context's stream waits for torch's current stream (inputs produced there are ready)."""
+    import torch
+
+    dev = torch.device("cuda", ctx.device)
+    cur = torch.cuda.current_stream(dev)
+    s = ctx.torch_stream()
+    if cur.cuda_stream != s.cuda_stream:
+        s.wait_stream(cur)
+
+
 def _mem(*ts) -> int:
     dev = [isinstance(t, DeviceCP) for t in ts]
     if all(dev):
@@ -274,7 +310,11 @@ def convolve(a, b, h, ctx: Context | None = None, out=None):
     if out is None:
         out = _out_like(a, a.rank() * b.rank(), mem)
     ca, cb, co = a._cstruct(), b._cstruct(), out._cstruct()
+    if mem == MEM_DEVICE:
+        _stream_enter(ctx)
     check(lib().tgb_convolve(ctx.handle, C.byref(ca), C.byref(cb), hh.ctypes.data, C.byref(co), mem))
+    if mem == MEM_DEVICE:
+        _stream_order(ctx, a, b, out)
     return out
 
 
@@ -290,7 +330,11 @@ def hartree_potential(theta, kernel, h, ctx: Context | None = None, out=None):
     if out is None:
         out = _out_like(theta, theta.rank() * kernel.rank(), mem)
     ct, ck, co = theta._cstruct(), kernel._cstruct(), out._cstruct()
+    if mem == MEM_DEVICE:
+        _stream_enter(ctx)
     check(lib().tgb_hartree_potential(ctx.handle, C.byref(ct), C.byref(ck), hh.ctypes.data, C.byref(co), mem))
+    if mem == MEM_DEVICE:
+        _stream_order(ctx, theta, kernel, out)
     return out
 
 
@@ -305,7 +349,9 @@ def value_at_points(t, ijk, ctx: Context | None = None):
         pts = ijk if isinstance(ijk, torch.Tensor) else torch.as_tensor(np.asarray(ijk, dtype=np.int64))
         pts = pts.to(device=t.weight.device, dtype=torch.int64).contiguous()
         out = torch.empty(pts.shape[0], dtype=torch.float64, device=t.weight.device)
+        _stream_enter(ctx)
         check(lib().tgb_value_at(ctx.handle, C.byref(ct), pts.shape[0], pts.data_ptr(), out.data_ptr(), mem))
+        _stream_order(ctx, t, pts, out)
         return out
     pts = np.ascontiguousarray(np.asarray(ijk, dtype=np.int64).reshape(-1, 3))
     out = np.zeros(pts.shape[0])

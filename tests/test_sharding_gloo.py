@@ -35,13 +35,14 @@ def _worker(rank, world, port, q):
     try:
         from oracle import oracle as O
         from paper_1504_06289_b200.inputs import hartree_case
-        from paper_1504_06289_b200.shard import allreduce_sum, shard_canonical
+        from paper_1504_06289_b200.shard import allreduce_sum, shard_canonical, torch_comm
 
+        comm = torch_comm()
         case = hartree_case(0, n=65, rank=7, nsamples=40)
         theta_r, (lo, hi) = shard_canonical(case.theta, rank, world)
         vh = O.hartree_potential(O.OCP.from_cp(theta_r), O.OCP.from_cp(case.kernel.tensor), case.grid.h)
         part = O.value_at(vh, case.samples) if theta_r.rank() else np.zeros(len(case.samples))
-        total = allreduce_sum(np.ascontiguousarray(part))
+        total = allreduce_sum(np.ascontiguousarray(part), comm)  # libtgb tgb_comm_allreduce_host
         if rank == 0:
             full = O.hartree_potential(O.OCP.from_cp(case.theta), O.OCP.from_cp(case.kernel.tensor), case.grid.h)
             ref = O.value_at(full, case.samples)
@@ -124,3 +125,58 @@ def test_sharded_coulomb_allreduce_gloo():
         assert p.exitcode == 0
     err, sym = q.get(timeout=10)
     assert err <= 1e-12 and sym
+
+
+def _worker_sym(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1504_06289_b200.shard import symmetric_allreduce, torch_comm
+
+        nb = 9
+        rng = np.random.default_rng(100 + rank)
+        part = rng.standard_normal((nb, nb))
+        part = np.asfortranarray(part + part.T)
+        J = symmetric_allreduce(part, torch_comm())
+        if rank == 0:
+            parts = []
+            for r in range(world):
+                p = np.random.default_rng(100 + r).standard_normal((nb, nb))
+                parts.append(p + p.T)
+            ref = np.sum(parts, axis=0)
+            q.put((float(np.abs(J - ref).max()), bool(np.array_equal(J, J.T))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_symmetric_allreduce_gloo_world3():
+    """libtgb's tgb_symmetric_allreduce_host over a torch.distributed (gloo)
+    tgb_comm at world size 3: the sum of the partial J blocks, exactly
+    symmetric whatever order the backend summed J_km and J_mk in."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_sym, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    err, sym = q.get(timeout=10)
+    assert err <= 1e-13 and sym
+
+
+def test_shard_range_is_libtgb():
+    """shard_range comes from the C-ABI (tgb_shard_range) and rejects bad ranks."""
+    from paper_1504_06289_b200 import InvalidArgument
+
+    assert shard_range(500, 7, 8) == (437, 500)
+    with pytest.raises(InvalidArgument):
+        shard_range(10, 2, 2)
