@@ -440,13 +440,16 @@ __global__ void tei_diag_term_kernel(int nc, const int* __restrict__ cstart, con
 // All kernel terms at once when every Y_k = V M_k^T is stored (Pk): grid.y = k,
 // s[k nc + c] = tei_diag_term_kernel's per-term sum; tei_diag_sum_kernel then
 // adds the terms in k order, so diag is bit-identical to the per-term launches.
-__global__ void tei_diag_terms_kernel(int nc, const int* __restrict__ cstart, const int* __restrict__ cpairs,
-                                      const double* __restrict__ cw, int64_t np2, const double* __restrict__ V0,
-                                      const double* __restrict__ V1, const double* __restrict__ V2, int r0, int r1,
-                                      int r2, const double* __restrict__ P0, const double* __restrict__ P1,
+// Rows c in [c0, c1) (all of them on one process; a rank's pair-row block
+// under a communicator).
+__global__ void tei_diag_terms_kernel(int nc, int c0, int c1, const int* __restrict__ cstart,
+                                      const int* __restrict__ cpairs, const double* __restrict__ cw, int64_t np2,
+                                      const double* __restrict__ V0, const double* __restrict__ V1,
+                                      const double* __restrict__ V2, int r0, int r1, int r2,
+                                      const double* __restrict__ P0, const double* __restrict__ P1,
                                       const double* __restrict__ P2, double* __restrict__ s_out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nc) return;
+  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
   const int64_t k = blockIdx.y;
   const double* Y0 = P0 + np2 * r0 * k;
   const double* Y1 = P1 + np2 * r1 * k;
@@ -464,9 +467,10 @@ __global__ void tei_diag_terms_kernel(int nc, const int* __restrict__ cstart, co
   s_out[k * nc + c] = s;
 }
 
-__global__ void tei_diag_sum_kernel(int nc, int K, const double* __restrict__ s_in, double* __restrict__ acc) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= nc) return;
+__global__ void tei_diag_sum_kernel(int nc, int c0, int c1, int K, const double* __restrict__ s_in,
+                                    double* __restrict__ acc) {
+  const int c = c0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= c1) return;
   double v = acc[c];
   for (int k = 0; k < K; ++k) v += s_in[static_cast<int64_t>(k) * nc + c];
   acc[c] = v;
@@ -1214,9 +1218,40 @@ void tei_conv(tgb_ctx* ctx, TEI& f, const tgb_cp& kernel_dev) {
     if (r == 0 || K == 0) continue;
     // conv columns: column i + r k = h * window(conv(U_i, p_k))   (tei.cpp:153-154)
     auto* co = static_cast<double*>(ctx->ws_out.get(static_cast<size_t>(n) * r * K * sizeof(double)));
-    convolve_axis(ctx, n, r, dptr(f.U[ax]), K, kernel_dev.factor[ax], f.h[ax], co);
+    if (ctx->comm_size > 1) {
+      // multi-GPU: this rank convolves its block of kernel-term PAIRS {j, K-1-j} (the +-t
+      // sinc nodes stay together, so duplicates are still convolved once); the other
+      // terms' columns are zero, the full-size GEMM below then gives this rank's M_k
+      // blocks bit-identical to one process and zeros elsewhere, and one all-reduce of
+      // M completes it
+      const int64_t npair = (K + 1) / 2;
+      int64_t p0 = 0, p1 = 0;
+      shard_range(npair, ctx->comm_rank, ctx->comm_size, &p0, &p1);
+      std::vector<int64_t> ks;
+      for (int64_t j = p0; j < p1; ++j) {
+        ks.push_back(j);
+        if (K - 1 - j != j) ks.push_back(K - 1 - j);
+      }
+      std::sort(ks.begin(), ks.end());
+      TGB_CUDA(cudaMemsetAsync(co, 0, static_cast<size_t>(n) * r * K * sizeof(double), ctx->stream));
+      if (!ks.empty()) {
+        const int64_t S = static_cast<int64_t>(ks.size());
+        auto* ksub = static_cast<double*>(ctx_buf(ctx, "tei.conv.ksub").get(static_cast<size_t>(n) * S * sizeof(double)));
+        auto* csub = static_cast<double*>(ctx_buf(ctx, "tei.conv.csub").get(static_cast<size_t>(n) * r * S * sizeof(double)));
+        for (int64_t s2 = 0; s2 < S; ++s2)
+          TGB_CUDA(cudaMemcpyAsync(ksub + n * s2, kernel_dev.factor[ax] + n * ks[s2], n * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+        convolve_axis(ctx, n, r, dptr(f.U[ax]), S, ksub, f.h[ax], csub);
+        for (int64_t s2 = 0; s2 < S; ++s2)
+          TGB_CUDA(cudaMemcpyAsync(co + n * r * ks[s2], csub + n * r * s2, static_cast<size_t>(n) * r * sizeof(double),
+                                   cudaMemcpyDeviceToDevice, ctx->stream));
+      }
+    } else {
+      convolve_axis(ctx, n, r, dptr(f.U[ax]), K, kernel_dev.factor[ax], f.h[ax], co);
+    }
     // [M_0 | ... | M_{K-1}] = U^T [conv_0 | ...]   (tei.cpp:155)
     dgemm(ctx, true, false, r, r * K, n, 1.0, dptr(f.U[ax]), n, co, n, 0.0, dptr(f.M[ax]), r);
+    if (ctx->comm_size > 1) comm_allreduce(ctx, dptr(f.M[ax]), r * r * K, true);
     f.Mst[ax].get(std::max<int64_t>(1, r * r * K) * sizeof(double));
     stack_kernel<<<static_cast<unsigned>((r * r * K + 255) / 256), 256, 0, ctx->stream>>>(
         static_cast<int>(r), static_cast<int>(K), dptr(f.M[ax]), dptr(f.Mst[ax]));
@@ -1285,14 +1320,24 @@ void tei_diagonal_dev(tgb_ctx* ctx, TEI& f, double* diag) {
     }
     DevBuf& sbuf = ctx_buf(ctx, "tei1283.sbuf");  // per context
     auto* sk = static_cast<double*>(sbuf.get(std::max<size_t>(8, static_cast<size_t>(f.K) * nc * sizeof(double))));
-    tei_diag_terms_kernel<<<dim3((nc + 127) / 128, static_cast<unsigned>(f.K)), 128, 0, ctx->stream>>>(
-        nc, static_cast<const int*>(f.d_cstart.p), static_cast<const int*>(f.d_cpairs.p),
-        static_cast<const double*>(f.d_cw.p), np2, dptr(f.V[0]), dptr(f.V[1]), dptr(f.V[2]),
-        static_cast<int>(f.R[0]), static_cast<int>(f.R[1]), static_cast<int>(f.R[2]), dptr(f.Pk[0]), dptr(f.Pk[1]),
-        dptr(f.Pk[2]), sk);
-    TGB_LAUNCHED(ctx);
-    tei_diag_sum_kernel<<<(nc + 255) / 256, 256, 0, ctx->stream>>>(nc, static_cast<int>(f.K), sk, diag);
-    TGB_LAUNCHED(ctx);
+    // multi-GPU: this rank's block of pair rows, zeros elsewhere, one all-reduce (x + 0 is exact,
+    // so the diagonal is bit-identical to the single-process one); Pk stays replicated (the
+    // Cholesky column engine reads every row of it)
+    int64_t c0 = 0, c1 = nc;
+    if (ctx->comm_size > 1) shard_range(nc, ctx->comm_rank, ctx->comm_size, &c0, &c1);
+    const int nrow = static_cast<int>(c1 - c0);
+    if (nrow > 0) {
+      tei_diag_terms_kernel<<<dim3((nrow + 127) / 128, static_cast<unsigned>(f.K)), 128, 0, ctx->stream>>>(
+          nc, static_cast<int>(c0), static_cast<int>(c1), static_cast<const int*>(f.d_cstart.p),
+          static_cast<const int*>(f.d_cpairs.p), static_cast<const double*>(f.d_cw.p), np2, dptr(f.V[0]),
+          dptr(f.V[1]), dptr(f.V[2]), static_cast<int>(f.R[0]), static_cast<int>(f.R[1]), static_cast<int>(f.R[2]),
+          dptr(f.Pk[0]), dptr(f.Pk[1]), dptr(f.Pk[2]), sk);
+      TGB_LAUNCHED(ctx);
+      tei_diag_sum_kernel<<<(nrow + 255) / 256, 256, 0, ctx->stream>>>(
+          nc, static_cast<int>(c0), static_cast<int>(c1), static_cast<int>(f.K), sk, diag);
+      TGB_LAUNCHED(ctx);
+    }
+    if (ctx->comm_size > 1) comm_allreduce(ctx, diag, nc, true);
     return;
   }
   for (int64_t k = 0; k < f.K; ++k) {

@@ -115,3 +115,70 @@ def test_nccl_single_rank_context(ctx):
     ref = tg.value_at_points(out, torch.as_tensor(case.samples).cuda(), ctx)
     assert torch.equal(v, ref)
     shard.set_comm(ctx, None)
+
+
+def _worker_tei(rank, world, port, q):
+    import sys
+    from pathlib import Path
+
+    here = Path(__file__).resolve().parent
+    sys.path.insert(0, str(here.parent))
+    sys.path.insert(0, str(here))
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1504_06289_b200 as tg
+        from paper_1504_06289_b200 import shard
+        from paper_1504_06289_b200.inputs import Rng
+        from test_tei_gpu import make_basis
+
+        rng = Rng(12)
+        cents = rng.uniform(6, -1.5, 1.5).reshape(2, 3)
+        bs = make_basis(65, 7.0, cents, ("s", "p"), rng)
+        kern = tg.kernel_tensor(bs.grid, tg.make_expsum(10, 0.9), False)
+        disc = tg.discretize_basis(bs)
+
+        def run(ctx):
+            fac = tg.TEIFactorization(ctx)
+            tg.tei_density_fitting(fac, bs, disc, 1e-6)
+            tg.tei_convolution_matrices(fac, kern)
+            conv = [fac.conv(k, ax) for k in range(kern.rank()) for ax in range(3)]
+            d = tg.tei_diagonal(fac)
+            tg.tei_cholesky(fac, 1e-8)
+            return fac.fit_ranks(), conv, d, fac.rank_b(), list(fac.pivots), np.array(fac.chol)
+
+        ctx = tg.Context(0)
+        comm = shard.torch_comm()
+        shard.set_comm(ctx, comm)
+        got = run(ctx)
+        shard.set_comm(ctx, None)
+        if rank == 0:
+            ref = run(tg.Context(0))
+            same = (got[0] == ref[0] and all(np.array_equal(a, b) for a, b in zip(got[1], ref[1]))
+                    and np.array_equal(got[2], ref[2]) and got[3] == ref[3] and got[4] == ref[4]
+                    and np.array_equal(got[5], ref[5]))
+            q.put((bool(same), got[3]))
+        ctx.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_tei_two_processes_bit_identical():
+    """TEI sharded per SURVEY §8e over a gloo tgb_comm: convolution matrices by
+    kernel-term pair, the diagonal by pair rows, one all-reduce each; the
+    pivoted Cholesky replicated.  Fit ranks, every M_k, the diagonal, R_B, the
+    pivot sequence and L are bit-identical to one process."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_tei, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=600)
+        assert p.exitcode == 0
+    same, rb = q.get(timeout=10)
+    assert same and rb > 1
