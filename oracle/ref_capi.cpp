@@ -502,4 +502,81 @@ int ref_reciprocal_expsum(double lo, double hi, double eps, long long* terms, do
     *ok = rs.ok;
   });
 }
+// ---- full-size config fixtures (tools/make_golden_configs.py) -------------------
+// density_tensor (hf.cpp:118-129) with reduce_rank split into its two steps
+// (reduction.cpp:271-273) so the Tucker ranks can be reported.
+// info = {r0, r1, r2, reduced canonical rank, unreduced rank}
+int ref_density_tucker(TG_BASIS_ARGS, long long nocc, const double* c_occ, double eps, long long* info, void* out) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    const auto disc = tg::discretize_basis(bs);
+    const tg::CanonicalTensor3 theta = tg::density_tensor(disc, mat(c_occ, nfn, nocc), 0.0);  // unreduced
+    const tg::TuckerResult tr = tg::canonical_to_tucker(theta, tg::ReductionConfig::tolerance(eps));
+    const auto rk = tr.tucker.ranks();
+    for (int ax = 0; ax < 3; ++ax) info[ax] = rk[ax];
+    tg::CanonicalTensor3 red = tg::tucker_to_canonical(tr.tucker);
+    info[3] = red.rank();
+    info[4] = theta.rank();
+    *static_cast<tg::CanonicalTensor3*>(out) = std::move(red);
+  });
+}
+// coulomb_matrix(bs, disc, hartree_potential(theta, kernel, h)) (hf.cpp:131-151) with
+// V_H split by kernel column j (J is linear in V_H's columns): threads take blocks of
+// j, each materialises only its V_H^(j); the partial J^(j) are summed in j order.
+int ref_coulomb_from_theta(TG_BASIS_ARGS, void* theta_h, long long m, double c0, int threads, double* J) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    const auto disc = tg::discretize_basis(bs);
+    const auto& th = *static_cast<tg::CanonicalTensor3*>(theta_h);
+    const tg::KernelTensor kern = tg::kernel_tensor(bs.grid, tg::make_expsum(m, c0), false);
+    const long long rb = kern.rank();
+    std::vector<Eigen::MatrixXd> part(static_cast<size_t>(rb));
+    auto work = [&](long long j0, long long j1) {
+      for (long long j = j0; j < j1; ++j) {
+        tg::KernelTensor kj = kern;
+        for (int ax = 0; ax < 3; ++ax) kj.tensor.factor[ax] = Eigen::MatrixXd(kern.tensor.factor[ax].col(j));
+        kj.tensor.weight = Eigen::VectorXd::Constant(1, kern.tensor.weight[j]);
+        const tg::CanonicalTensor3 vh = tg::hartree_potential(th, kj, bs.grid.h);
+        part[static_cast<size_t>(j)] = tg::coulomb_matrix(bs, disc, vh);
+      }
+    };
+    std::vector<std::thread> ts;
+    const int nt = std::max(1, threads);
+    for (int t = 0; t < nt; ++t) {
+      const long long lo = rb * t / nt, hi = rb * (t + 1) / nt;
+      if (lo < hi) ts.emplace_back(work, lo, hi);
+    }
+    for (auto& t : ts) t.join();
+    Eigen::MatrixXd acc = part[0];
+    for (long long j = 1; j < rb; ++j) acc = acc + part[static_cast<size_t>(j)];
+    put(acc, J);
+  });
+}
+// build_tei (tei.cpp:206-213) with the pivot sequence of its Cholesky kept:
+// tei_density_fitting + tei_convolution_matrices, then pivoted_cholesky with
+// tei_cholesky's arguments (tei.cpp:198-204).  info = {R_l[3], R_B, clamped}
+int ref_build_tei_pivots(TG_BASIS_ARGS, long long m, double c0, double eps_fit, double eps_chol, long long* info,
+                         double* fit_residual, long long* pivots, void** handle) {
+  return guard([&] {
+    const tg::BasisSet bs = basis_set(TG_BASIS);
+    const tg::KernelTensor kern = tg::kernel_tensor(bs.grid, tg::make_expsum(m, c0), false);
+    auto* fac = new tg::TEIFactorization();
+    tg::tei_density_fitting(*fac, bs, tg::discretize_basis(bs), eps_fit);
+    tg::tei_convolution_matrices(*fac, kern);
+    fac->eps_chol = eps_chol;
+    const tg::PivotedCholesky pc = tg::pivoted_cholesky([&](tg::index_t j) { return tg::tei_column(*fac, j); },
+                                                        tg::tei_diagonal(*fac), eps_chol, tg::CholeskyStop::max_diagonal,
+                                                        fac->n_b * fac->n_b, 1e-10);
+    fac->chol = pc.factor;
+    for (int ax = 0; ax < 3; ++ax) {
+      info[ax] = fac->fit_ranks()[ax];
+      fit_residual[ax] = fac->fit_residual[ax];
+    }
+    info[3] = fac->rank_b();
+    info[4] = fac->fit_clamped_negative ? 1 : 0;
+    for (size_t r = 0; r < pc.pivots.size(); ++r) pivots[r] = pc.pivots[r];
+    *handle = fac;
+  });
+}
+
 }  // extern "C"

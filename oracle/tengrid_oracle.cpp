@@ -84,6 +84,11 @@ void sym_eigen(const Mat& a_in, Vec& ev, Mat& z) {
   ev.assign(n, 0.0);
   Vec e(n, 0.0);
   if (n == 0) return;
+  // matrix scale for the deflation test below (max |a_ij|, as the eigensolver the
+  // reference links scales its input before tridiagonalising)
+  double amax = 0.0;
+  for (idx j = 0; j < n; ++j)
+    for (idx i = 0; i < n; ++i) amax = std::max(amax, std::fabs(a_in(i, j)));
   // tridiagonalise (row i of the lower triangle eliminated from the bottom)
   for (idx i = n - 1; i > 0; --i) {
     const idx l = i - 1;
@@ -147,7 +152,14 @@ void sym_eigen(const Mat& a_in, Vec& ev, Mat& z) {
     do {
       for (m = l; m < n - 1; ++m) {
         const double dd = std::fabs(ev[m]) + std::fabs(ev[m + 1]);
-        if (std::fabs(e[m]) <= 1e-300 || std::fabs(e[m]) <= 2.220446049250313e-16 * dd) break;
+        const double em = std::fabs(e[m]);
+        // relative test, or |e|^2 <= eps^2 amax (|d_m| + |d_m+1|): deflates the
+        // near-null block of a rank-deficient Gram matrix (RHOSVD's wide branch),
+        // where both neighbouring diagonals are ~eps amax and the purely relative
+        // test never fires
+        if (em <= 1e-300 || em <= 2.220446049250313e-16 * dd ||
+            (em / 2.220446049250313e-16) * (em / 2.220446049250313e-16) <= amax * dd)
+          break;
       }
       if (m != l) {
         if (++iter > 200) throw numerical_error("sym_eigen: QL did not converge");
