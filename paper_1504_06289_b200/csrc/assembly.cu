@@ -11,8 +11,12 @@
 //  * batched value_at probes (tensor.hpp:135-140).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
+#include <utility>
 #include <vector>
 
 #include "tgb_internal.hpp"
@@ -216,6 +220,112 @@ __global__ void __launch_bounds__(256) triple_dot_kernel(int nq, int P, const do
   if (threadIdx.x == 0) part[blockIdx.y * static_cast<int64_t>(P) + p] = sh[0];
 }
 
+// Duplicate right columns.  V_H = convolve(theta, kernel) repeats every column
+// block of a kernel column's bitwise twin (the +-t sinc nodes, kernel.cpp:194):
+// config 1 has 108,650 V_H columns of which 55,650 are distinct.  Two 64-bit
+// hashes per column (order-independent sums of mixed (position, bits) words
+// over all three axes) group candidates on the host; every candidate is then
+// compared bitwise on the device before its weight is merged into its
+// representative's, so a hash collision can never merge different columns.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void col_hash_kernel(int64_t n0, int64_t n1, int64_t n2, const double* __restrict__ B0,
+                                const double* __restrict__ B1, const double* __restrict__ B2,
+                                unsigned long long* __restrict__ h, unsigned long long* __restrict__ key,
+                                int* __restrict__ val) {
+  const int64_t q = blockIdx.x;
+  uint64_t a = 0, b = 0;
+  const int64_t ns[3] = {n0, n1, n2};
+  const double* Bs[3] = {B0, B1, B2};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const uint64_t* col = reinterpret_cast<const uint64_t*>(Bs[ax] + q * ns[ax]);
+    for (int64_t k = threadIdx.x; k < ns[ax]; k += blockDim.x) {
+      const uint64_t v = col[k];
+      const uint64_t pos = static_cast<uint64_t>(k) + (static_cast<uint64_t>(ax) << 40);
+      a += mix64(v ^ (pos * 0x9E3779B97F4A7C15ull));
+      b += mix64(v + pos * 0xD1B54A32D192ED03ull + 0x632BE59BD9B4E019ull);
+    }
+  }
+  __shared__ uint64_t sa[256], sb[256];
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int st = blockDim.x / 2; st; st >>= 1) {
+    if (threadIdx.x < st) {
+      sa[threadIdx.x] += sa[threadIdx.x + st];
+      sb[threadIdx.x] += sb[threadIdx.x + st];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    h[2 * q] = sa[0];
+    h[2 * q + 1] = sb[0];
+    key[q] = sa[0];
+    val[q] = static_cast<int>(q);
+  }
+}
+
+// Over the hash-sorted columns (stable: ascending index within a run of equal
+// first hashes): one CTA per sorted position t; a run member is merged into
+// the run start r when the second hashes match AND its three columns are
+// bitwise equal to r's (coalesced compare).  rep[q] = r, or -1.
+__global__ void dedup_verify_kernel(int RB, int64_t n0, int64_t n1, int64_t n2, const double* __restrict__ B0,
+                                    const double* __restrict__ B1, const double* __restrict__ B2,
+                                    const unsigned long long* __restrict__ h, const unsigned long long* __restrict__ key,
+                                    const int* __restrict__ val, int* __restrict__ rep) {
+  const int t = blockIdx.x;
+  const int q = val[t];
+  if (t == 0 || key[t - 1] != key[t]) {
+    if (threadIdx.x == 0) rep[q] = -1;
+    return;
+  }
+  __shared__ int s_r;
+  if (threadIdx.x == 0) {
+    int s = t - 1;
+    while (s > 0 && key[s - 1] == key[t]) --s;
+    s_r = val[s];
+  }
+  __syncthreads();
+  const int r = s_r;
+  int eq = h[2 * q + 1] == h[2 * r + 1];
+  const int64_t ns[3] = {n0, n1, n2};
+  const double* Bs[3] = {B0, B1, B2};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    const uint64_t* x = reinterpret_cast<const uint64_t*>(Bs[ax] + q * ns[ax]);
+    const uint64_t* y = reinterpret_cast<const uint64_t*>(Bs[ax] + static_cast<int64_t>(r) * ns[ax]);
+    for (int64_t k = threadIdx.x; k < ns[ax]; k += blockDim.x) eq &= (x[k] == y[k]);
+  }
+  eq = __syncthreads_and(eq);
+  if (threadIdx.x == 0) rep[q] = eq ? r : -1;
+}
+
+// Merged weights: a run start sums its merged members' weights in ascending
+// column order (deterministic); merged columns get keep = 0.
+__global__ void dedup_weights_kernel(int RB, const unsigned long long* __restrict__ key, const int* __restrict__ val,
+                                     const int* __restrict__ rep, const double* __restrict__ w,
+                                     unsigned char* __restrict__ keep, double* __restrict__ wout) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= RB) return;
+  const int q = val[t];
+  if (rep[q] >= 0) {
+    keep[q] = 0;
+    wout[q] = 0.0;
+    return;
+  }
+  keep[q] = 1;
+  double acc = w[q];
+  if (t == 0 || key[t - 1] != key[t])
+    for (int u = t + 1; u < RB && key[u] == key[t]; ++u)
+      if (rep[val[u]] == q) acc += w[val[u]];
+  wout[q] = acc;
+}
+
 // s[p] = sum_q wb[q] prod_ax <left_p^ax, B_q^ax>, returned to the host.
 std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* const F[3], const double* const B[3],
                               const double* wb, int RB, const std::vector<int>& i0, const std::vector<int>& i1) {
@@ -264,8 +374,56 @@ std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* co
     }
     double* T[3] = {work + off, work + off + static_cast<size_t>(chunk) * P, work + off + 2 * static_cast<size_t>(chunk) * P};
     double* parts = work + off + 3 * static_cast<size_t>(chunk) * P;
-    for (int c = 0; c < nch; ++c) {
-      const int q0 = c * chunk, nq = std::min(chunk, RB - q0);
+    // duplicate right columns: merged weights and the kept column ranges
+    const double* wq = wb;
+    std::vector<std::pair<int, int>> chunks;  // (q0, nq)
+    {
+      std::vector<char> keep(RB, 1);
+      if (RB >= 1024 && !getenv("TGB_NO_DEDUP")) {
+        DevBuf& db = ctx_buf(ctx, "sep.dedup");
+        // layout: hash pairs (2 RB u64), sorted keys + values, keep flags, merged weights, CUB temp
+        size_t cub_bytes = 0;
+        cub::DeviceRadixSort::SortPairs(nullptr, cub_bytes, static_cast<const unsigned long long*>(nullptr),
+                                        static_cast<unsigned long long*>(nullptr), static_cast<const int*>(nullptr),
+                                        static_cast<int*>(nullptr), RB, 0, 64, ctx->stream);
+        const size_t o_h = 0, o_k0 = o_h + 16 * size_t(RB), o_k1 = o_k0 + 8 * size_t(RB), o_v0 = o_k1 + 8 * size_t(RB),
+                     o_v1 = o_v0 + 4 * size_t(RB), o_keep = o_v1 + 4 * size_t(RB),
+                     o_w = (o_keep + size_t(RB) + 15) & ~size_t(15), o_tmp = o_w + 8 * size_t(RB);
+        char* base = static_cast<char*>(db.get(o_tmp + cub_bytes + 256));
+        auto* hh = reinterpret_cast<unsigned long long*>(base + o_h);
+        auto* k0 = reinterpret_cast<unsigned long long*>(base + o_k0);
+        auto* k1 = reinterpret_cast<unsigned long long*>(base + o_k1);
+        auto* v0 = reinterpret_cast<int*>(base + o_v0);
+        auto* v1 = reinterpret_cast<int*>(base + o_v1);
+        auto* dkeep = reinterpret_cast<unsigned char*>(base + o_keep);
+        auto* dw = reinterpret_cast<double*>(base + o_w);
+        col_hash_kernel<<<RB, 256, 0, ctx->stream>>>(n[0], n[1], n[2], B[0], B[1], B[2], hh, k0, v0);
+        TGB_LAUNCHED(ctx);
+        // stable sort by the first hash: equal columns end up in runs, ascending index within a run
+        TGB_CUDA(cub::DeviceRadixSort::SortPairs(base + o_tmp, cub_bytes, k0, k1, v0, v1, RB, 0, 64, ctx->stream));
+        dedup_verify_kernel<<<RB, 128, 0, ctx->stream>>>(RB, n[0], n[1], n[2], B[0], B[1], B[2], hh, k1, v1, v0);
+        TGB_LAUNCHED(ctx);  // v0 (free after the sort) holds rep[]
+        dedup_weights_kernel<<<(RB + 127) / 128, 128, 0, ctx->stream>>>(RB, k1, v1, v0, wb, dkeep, dw);
+        TGB_LAUNCHED(ctx);
+        TGB_CUDA(cudaMemcpyAsync(keep.data(), dkeep, RB, cudaMemcpyDeviceToHost, ctx->stream));
+        TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        wq = dw;
+      }
+      for (int q = 0; q < RB;) {  // kept ranges, split into chunks
+        if (!keep[q]) {
+          ++q;
+          continue;
+        }
+        int e = q;
+        while (e < RB && keep[e] && e - q < chunk) ++e;
+        chunks.push_back({q, e - q});
+        q = e;
+      }
+    }
+    const int nchk = static_cast<int>(chunks.size());
+    if (nchk > nch) parts = static_cast<double*>(ctx_buf(ctx, "sep.parts").get(static_cast<size_t>(nchk) * P * sizeof(double)));
+    for (int c = 0; c < nchk; ++c) {
+      const int q0 = chunks[c].first, nq = chunks[c].second;
       // axis 2 on the aux stream: its wave tail overlaps axes 0-1 (no split-K, whose workspace is shared)
       const bool fork = ((nq + 63) / 64) * ((P + 63) / 64) >= ctx->num_sms;
       if (fork) {
@@ -281,11 +439,12 @@ std::vector<double> sep_inner(tgb_ctx* ctx, const int64_t n[3], const double* co
         TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
         TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
       }
-      triple_dot_kernel<<<dim3(static_cast<unsigned>(P), 1), 256, 0, ctx->stream>>>(nq, P, T[0], T[1], T[2], wb + q0,
+      triple_dot_kernel<<<dim3(static_cast<unsigned>(P), 1), 256, 0, ctx->stream>>>(nq, P, T[0], T[1], T[2], wq + q0,
                                                                                     parts + static_cast<size_t>(c) * P);
       TGB_LAUNCHED(ctx);
     }
-    reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(parts, nch, P, dsum);
+    if (nchk == 0) TGB_CUDA(cudaMemsetAsync(parts, 0, P * sizeof(double), ctx->stream));
+    reduce_tiles_kernel<<<(P + 127) / 128, 128, 0, ctx->stream>>>(parts, std::max(nchk, 1), P, dsum);
     TGB_LAUNCHED(ctx);
   } else {
     dim3 grid((P + TP - 1) / TP, ntq);

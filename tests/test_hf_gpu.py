@@ -242,3 +242,29 @@ def test_tei_config3_structure_vs_reference_binary(g, ctx):
     assert fac.fit_clamped_negative == bool(g["tei3s_clamped"][0])
     L, oL = fac.chol, g["tei3s_chol"]
     assert relmax(L @ L.T, oL @ oL.T) <= TOL
+
+
+def test_coulomb_duplicate_columns_merged(g, case, ctx, monkeypatch):
+    """V_H's bitwise-twin columns (+-t sinc nodes) are merged before the J GEMMs
+    (hash + device bitwise check, assembly.cu): J agrees with the unmerged
+    route to roundoff and stays exactly symmetric; a V_H whose twins are
+    perturbed in one bit is not merged."""
+    bs, disc, _, _ = case
+    theta = tg.CanonicalTensor3([g[f"theta_f{ax}"] for ax in range(3)], g["theta_w"])
+    kern = tg.kernel_tensor(bs.grid, tg.make_expsum(20, 0.76), False)  # 41 terms: R_V >= 1024
+    vh = tg.hartree_potential(theta, kern, bs.grid.h, ctx)
+    assert vh.rank() >= 1024
+    J = tg.coulomb_matrix(bs, disc, vh, ctx)
+    monkeypatch.setenv("TGB_NO_DEDUP", "1")
+    J0 = tg.coulomb_matrix(bs, disc, vh, ctx)
+    monkeypatch.delenv("TGB_NO_DEDUP")
+    assert relmax(J, J0) <= 1e-13 and np.array_equal(J, J.T)
+    # break one twin by one ulp: the hash groups differ, nothing merges wrongly
+    f0 = vh.factor[0].copy(order="F")
+    r = theta.rank()
+    f0[5, 40 * r] = np.nextafter(f0[5, 40 * r], np.inf)
+    vh2 = tg.CanonicalTensor3([f0, vh.factor[1], vh.factor[2]], vh.weight)
+    J2 = tg.coulomb_matrix(bs, disc, vh2, ctx)
+    monkeypatch.setenv("TGB_NO_DEDUP", "1")
+    J2b = tg.coulomb_matrix(bs, disc, vh2, ctx)
+    assert relmax(J2, J2b) <= 1e-13
