@@ -86,6 +86,7 @@ struct ConvPlan {
   bool direct = false;
   int threads = 0;
   mutable int pair_threads[2] = {0, 0};  // generic pair kernel, per kernel-spectrum form (chosen at first launch)
+  mutable int pair_per_sm[2] = {0, 0};   // and its resident CTAs per SM (host overhead matters at small n)
   mutable int spec_threads = 0;          // generic spectrum kernel
   size_t smem = 0;
   DevBuf perm, inv, leader, tw, twpost, ph1, ph2, phase, spos, kf;
@@ -740,10 +741,33 @@ __device__ __forceinline__ double2* load_tables(double2* sm, const PlanArgs& pa)
 // One launch covers the density columns (CTAs [0, nA): mode 0 into specA)
 // and the distinct kernel columns (CTAs [nA, ...): colidx, modeB into specB),
 // so the few, latency-bound kernel transforms overlap the density ones.
+// Per-axis operands of the generic kernels: blockIdx.y selects the axis, so one
+// launch covers every axis that shares a plan (small problems are launch-bound).
+struct SpecAxes {
+  const double* XA[3];
+  void* specA[3];
+  const double* XB[3];
+  void* specB[3];
+  void* specB2[3];
+  double h[3];
+};
+struct PairAxes {
+  const double2* specA[3];
+  const void* specB[3];
+  const PairEntry* work[3];
+  const int* winfo[3];
+  double* out[3];
+};
+
 __global__ void __launch_bounds__(kMaxThreads, 1)
-    spectrum_kernel(PlanArgs pa, const double* __restrict__ XA, int nA, void* __restrict__ specA,
-                    const double* __restrict__ XB, const int* __restrict__ colidx, int nB, void* __restrict__ specB,
-                    void* __restrict__ specB2, int modeB, int64_t ldx, double h) {
+    spectrum_kernel(PlanArgs pa, SpecAxes sx, int nA, const int* __restrict__ colidx, int nB, int modeB, int64_t ldx) {
+  const int axis = blockIdx.y;
+  const double* __restrict__ XA = sx.XA[axis];
+  void* __restrict__ specA = sx.specA[axis];
+  const double* __restrict__ XB = sx.XB[axis];
+  void* __restrict__ specB = sx.specB[axis];
+  void* __restrict__ specB2 = sx.specB2[axis];
+  const double h = sx.h[axis];
   extern __shared__ double2 sm[];
   const double2* tws = load_tables(sm, pa);
   const bool isA = static_cast<int>(blockIdx.x) >= nB;  // kernel columns first (they carry the extra work)
@@ -874,11 +898,11 @@ __device__ __forceinline__ void pair_body(const PlanArgs& pa, const double2* __r
 // work list (build_work_kernel), so no host round trip sits between the
 // grouping and this launch.
 template <int R0, bool BREAL>
-__global__ void __launch_bounds__(kMaxThreads, 1)
-    pair_kernel(PlanArgs pa, const double2* __restrict__ specA, const void* __restrict__ specB,
-                const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out) {
+__global__ void __launch_bounds__(kMaxThreads, 1) pair_kernel(PlanArgs pa, PairAxes px) {
+  const int axis = blockIdx.y;
+  const int* winfo = px.winfo[axis];
   if ((winfo[1] != 0) != BREAL) return;
-  pair_body<R0, BREAL>(pa, specA, specB, work, winfo[0], out);
+  pair_body<R0, BREAL>(pa, px.specA[axis], px.specB[axis], px.work[axis], winfo[0], px.out[axis]);
 }
 
 // ---- compile-time plans: every span L and stride is a constant, so the
@@ -1439,7 +1463,18 @@ __global__ void direct_conv_kernel(int n, int ofs, int even, const double* __res
 
 // flags[j * rb + j2] = 1 iff columns j and j2 (j < j2) of B are bitwise equal;
 // flags[j * rb + j] = 1 iff column j is mirror-symmetric (b[i] == b[n-1-i]).
-__global__ void dup_columns_kernel(const double* __restrict__ B, int64_t n, int rb, unsigned char* flags) {
+struct ColAxes {  // per-axis operands of the grouping kernels (blockIdx.y = axis)
+  const double* B[3];
+  int64_t n[3];
+  unsigned char* flags[3];
+  PairEntry* work[3];
+  int* winfo[3];
+};
+
+__global__ void dup_columns_kernel(ColAxes ca, int rb) {
+  const double* __restrict__ B = ca.B[blockIdx.y];
+  const int64_t n = ca.n[blockIdx.y];
+  unsigned char* flags = ca.flags[blockIdx.y];
   const int p = blockIdx.x;
   int j, j2;
   if (p < rb) {
@@ -1469,9 +1504,11 @@ __global__ void dup_columns_kernel(const double* __restrict__ B, int64_t n, int 
 // dup/symmetry flags, and the i-major pair work list: for each density
 // column i, one entry per pair of identical kernel columns (the entry's
 // result is stored to both).  winfo = {entries, all columns symmetric}.
-__global__ void build_work_kernel(const unsigned char* __restrict__ f, int rb, int64_t ra, int64_t n,
-                                  PairEntry* __restrict__ w, int* __restrict__ winfo, int flags_in_smem,
-                                  const int64_t* __restrict__ cmap) {
+__global__ void build_work_kernel(ColAxes ca, int rb, int64_t ra, int flags_in_smem, const int64_t* __restrict__ cmap) {
+  const unsigned char* __restrict__ f = ca.flags[blockIdx.y];
+  const int64_t n = ca.n[blockIdx.y];
+  PairEntry* __restrict__ w = ca.work[blockIdx.y];
+  int* __restrict__ winfo = ca.winfo[blockIdx.y];
   // Grouping in parallel (bitwise identity is an equivalence): rep[j] = the
   // smallest j' <= j identical to j; a member's rank in its group = the number
   // of earlier members; groups are ordered by representative.  Every CTA
@@ -1606,8 +1643,7 @@ static int busy_width(const ConvPlan& pl, Kern kern, bool pair) {
 }
 
 template <int R0, bool BREAL>
-static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
-                        const PairEntry* dwork, const int* winfo, double* out) {
+static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const PairAxes& px, int naxes) {
   static bool attr[kTgbMaxDevices] = {};  // per device
   if (!attr[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(pair_kernel<R0, BREAL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1616,11 +1652,11 @@ static void launch_pair(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, 
   }
   int& tt = pl.pair_threads[BREAL ? 1 : 0];
   if (!tt) tt = busy_width(pl, pair_kernel<R0, BREAL>, true);
-  int per_sm = 1;
-  TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel<R0, BREAL>, tt, pl.smem));
-  const int grid = std::max(1, per_sm) * ctx->num_sms;
+  int& per_sm = pl.pair_per_sm[BREAL ? 1 : 0];
+  if (!per_sm) TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pair_kernel<R0, BREAL>, tt, pl.smem));
+  const int grid = std::max(1, std::max(1, per_sm) * ctx->num_sms / naxes);
   prof_begin(ctx);
-  pair_kernel<R0, BREAL><<<grid, tt, pl.smem, ctx->stream>>>(pl.a, specA, specB, dwork, winfo, out);
+  pair_kernel<R0, BREAL><<<dim3(grid, naxes), tt, pl.smem, ctx->stream>>>(pl.a, px);
   TGB_LAUNCHED(ctx);
   prof_end(ctx);
 }
@@ -1680,21 +1716,56 @@ static bool try_static(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, c
 }
 
 template <bool BREAL>
-static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
-                          const PairEntry* dwork, const int* winfo, double* out) {
-  // compile-time plans (config 2: n = 16385 -> N = 12800)
-  if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
+static void launch_pair_generic(tgb_ctx* ctx, const ConvPlan& pl, const PairAxes& px, int naxes) {
   switch (pl.a.r[0]) {
-    case 2: launch_pair<2, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
-    case 3: launch_pair<3, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
-    case 4: launch_pair<4, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
-    case 5: launch_pair<5, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
-    case 6: launch_pair<6, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
-    case 8: launch_pair<8, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
-    case 10: launch_pair<10, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
-    case 16: launch_pair<16, BREAL>(ctx, pl, specA, specB, dwork, winfo, out); break;
+    case 2: launch_pair<2, BREAL>(ctx, pl, px, naxes); break;
+    case 3: launch_pair<3, BREAL>(ctx, pl, px, naxes); break;
+    case 4: launch_pair<4, BREAL>(ctx, pl, px, naxes); break;
+    case 5: launch_pair<5, BREAL>(ctx, pl, px, naxes); break;
+    case 6: launch_pair<6, BREAL>(ctx, pl, px, naxes); break;
+    case 8: launch_pair<8, BREAL>(ctx, pl, px, naxes); break;
+    case 10: launch_pair<10, BREAL>(ctx, pl, px, naxes); break;
+    case 16: launch_pair<16, BREAL>(ctx, pl, px, naxes); break;
     default: throw Error(TGB_CUDA_ERROR, "fftconv: unsupported first radix");
   }
+}
+
+static bool static_plan(const ConvPlan& pl) {
+  const PlanArgs& a = pl.a;
+  return a.P == 4 && a.r[0] == 16 && a.r[1] == 10 && a.r[2] == 10 && a.r[3] == 8 && !getenv("TGB_NO_STATIC");
+}
+
+template <bool BREAL>
+static void launch_pair_r(tgb_ctx* ctx, const ConvPlan& pl, const double2* specA, const void* specB,
+                          const PairEntry* dwork, const int* winfo, double* out) {
+  // compile-time plans (n = 16385 -> N = 12800 when the N = 12288 plan does not apply)
+  if (try_static<16, 10, 10, 8, 320, BREAL>(ctx, pl, specA, specB, dwork, winfo, out)) return;
+  PairAxes px{};
+  px.specA[0] = specA;
+  px.specB[0] = specB;
+  px.work[0] = dwork;
+  px.winfo[0] = winfo;
+  px.out[0] = out;
+  launch_pair_generic<BREAL>(ctx, pl, px, 1);
+}
+
+// generic spectra of `naxes` axes sharing one plan, one launch (grid.y = axis)
+static void launch_spectrum_axes(tgb_ctx* ctx, const ConvPlan& pl, const SpecAxes& sx, int naxes, int nA,
+                                 const int* colidx, int nB, int modeB, int64_t ldx) {
+  static bool attr_set[kTgbMaxDevices] = {};  // per device
+  if (!attr_set[ctx->device]) {
+    TGB_CUDA(cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(ctx->smem_optin)));
+    attr_set[ctx->device] = true;
+  }
+  if (!pl.spec_threads) {
+    pl.spec_threads = busy_width(pl, spectrum_kernel, false);
+    const char* f = getenv("TGB_SPEC_THREADS");  // A/B override
+    if (f && atoi(f) > 0) pl.spec_threads = atoi(f);
+  }
+  spectrum_kernel<<<dim3(nA + nB, naxes), pl.spec_threads, pl.smem, ctx->stream>>>(pl.a, sx, nA, colidx, nB, modeB,
+                                                                                   ldx);
+  TGB_LAUNCHED(ctx);
 }
 
 // One launch: nB kernel columns (CTAs [0, nB), mode modeB; colidx == nullptr:
@@ -1730,10 +1801,14 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
     }
     return;
   }
-  if (!pl.spec_threads) pl.spec_threads = busy_width(pl, spectrum_kernel, false);
-  spectrum_kernel<<<nA + nB, pl.spec_threads, pl.smem, ctx->stream>>>(pl.a, A, nA, specA, B, colidx, nB, specB,
-                                                                       specB2, modeB, ldx, h);
-  TGB_LAUNCHED(ctx);
+  SpecAxes sx{};
+  sx.XA[0] = A;
+  sx.specA[0] = specA;
+  sx.XB[0] = B;
+  sx.specB[0] = specB;
+  sx.specB2[0] = specB2;
+  sx.h[0] = h;
+  launch_spectrum_axes(ctx, pl, sx, 1, nA, colidx, nB, modeB, ldx);
 }
 
 // config-2 plan (fftconv12k.cu)
@@ -1771,20 +1846,60 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
   const int flags_in_smem = wsmem + static_cast<size_t>(rb * rb) <= 48 * 1024;
   if (flags_in_smem) wsmem += static_cast<size_t>(rb * rb);
   std::vector<PairEntry*> dwork(naxes);
+  ColAxes ca{};
   for (int ax = 0; ax < naxes; ++ax) {
-    unsigned char* f = flags + ax * rb * rb;
     dwork[ax] = reinterpret_cast<PairEntry*>(wlist + ax * (wentries * sizeof(PairEntry) + 256));
-    dup_columns_kernel<<<static_cast<unsigned>(nblocks), 256, 0, ctx->aux_stream>>>(B[ax], n[ax],
-                                                                                   static_cast<int>(rb), f);
-    TGB_LAUNCHED(ctx);
-    const unsigned wblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ra / 4, 2 * ctx->num_sms)));
-    build_work_kernel<<<wblocks, 128, wsmem, ctx->aux_stream>>>(f, static_cast<int>(rb), ra, n[ax], dwork[ax],
-                                                               winfo + 2 * ax, flags_in_smem, colmap);
-    TGB_LAUNCHED(ctx);
+    ca.B[ax] = B[ax];
+    ca.n[ax] = n[ax];
+    ca.flags[ax] = flags + ax * rb * rb;
+    ca.work[ax] = dwork[ax];
+    ca.winfo[ax] = winfo + 2 * ax;
   }
+  // every axis in one launch each (grid.y = axis)
+  dup_columns_kernel<<<dim3(static_cast<unsigned>(nblocks), naxes), 256, 0, ctx->aux_stream>>>(ca, static_cast<int>(rb));
+  TGB_LAUNCHED(ctx);
+  const unsigned wblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ra / 4, 2 * ctx->num_sms)));
+  build_work_kernel<<<dim3(wblocks, naxes), 128, wsmem, ctx->aux_stream>>>(ca, static_cast<int>(rb), ra,
+                                                                          flags_in_smem, colmap);
+  TGB_LAUNCHED(ctx);
   TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
   // ---- main stream: spectra (independent of the grouping), then the pairs
   bool joined = false;
+  bool same_n = true;
+  for (int ax = 1; ax < naxes; ++ax) same_n = same_n && n[ax] == n[0];
+  const ConvPlan& p0 = *plans[0];
+  if (naxes > 1 && same_n && !p0.direct && !k12_applicable(n[0], p0.a.N) && !static_plan(p0)) {
+    // every axis shares one generic plan: one spectrum launch and one pair launch per
+    // spectrum form for all axes (config 0 is launch-bound: 16 -> 6 launches)
+    const size_t N1 = static_cast<size_t>(p0.a.N) + 1;
+    const size_t a_bytes = (static_cast<size_t>(ra) * N1 * sizeof(double2) + 255) & ~size_t(255);
+    auto* sa = static_cast<char*>(ctx->ws_spec_a.get(naxes * a_bytes));
+    const size_t real_bytes = (static_cast<size_t>(rb) * N1 * sizeof(double) + 255) & ~size_t(255);
+    const size_t b_bytes = real_bytes + static_cast<size_t>(rb) * N1 * sizeof(double2);
+    auto* sb = static_cast<char*>(ctx->ws_spec_b.get(naxes * b_bytes));
+    SpecAxes sx{};
+    PairAxes pr{}, pc{};
+    for (int ax = 0; ax < naxes; ++ax) {
+      char* b0 = sb + ax * b_bytes;
+      sx.XA[ax] = A[ax];
+      sx.specA[ax] = sa + ax * a_bytes;
+      sx.XB[ax] = B[ax];
+      sx.specB[ax] = b0;
+      sx.specB2[ax] = b0 + real_bytes;
+      sx.h[ax] = h[ax];
+      pr.specA[ax] = pc.specA[ax] = reinterpret_cast<const double2*>(sa + ax * a_bytes);
+      pr.specB[ax] = b0;
+      pc.specB[ax] = b0 + real_bytes;
+      pr.work[ax] = pc.work[ax] = dwork[ax];
+      pr.winfo[ax] = pc.winfo[ax] = winfo + 2 * ax;
+      pr.out[ax] = pc.out[ax] = out[ax];
+    }
+    launch_spectrum_axes(ctx, p0, sx, naxes, static_cast<int>(ra), nullptr, static_cast<int>(rb), 3, n[0]);
+    TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
+    launch_pair_generic<true>(ctx, p0, pr, naxes);
+    launch_pair_generic<false>(ctx, p0, pc, naxes);
+    return;
+  }
   for (int ax = 0; ax < naxes; ++ax) {
     const ConvPlan& pl = *plans[ax];
     if (pl.direct) {

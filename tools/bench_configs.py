@@ -49,6 +49,19 @@ def cfg0(ctx):
     dt, dk = tg.DeviceCP.from_host(case.theta), tg.DeviceCP.from_host(case.kernel.tensor)
     out = tg.DeviceCP.empty([1025] * 3, dt.rank() * dk.rank())
     t, _ = timed(lambda: tg.hartree_potential(dt, dk, case.grid.h, ctx, out=out), reps=20, sync=torch.cuda.synchronize)
+    # device time per call (CUDA events on the context stream around 100 back-to-back calls)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.ExternalStream(ctx.stream)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(100):
+        tg.hartree_potential(dt, dk, case.grid.h, ctx, out=out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    t_dev = e0.elapsed_time(e1) / 100 / 1e3
+    ctx.reset_launch_count()
+    tg.hartree_potential(dt, dk, case.grid.h, ctx, out=out)
+    launches = ctx.launch_count()
     units = 3 * 50 * 31
     byts = 8.0 * 3 * 1025 * (50 * 31 + 50 + 31)
     vh = out.to_host()
@@ -63,6 +76,7 @@ def cfg0(ctx):
 
     ana = analytic_potential(xyz, case.a, case.centres, case.c)
     return {"config": 0, "what": "hartree_potential n=1025 R_f=50 R_N=31", "ms": t * 1e3, "convs_per_s": units / t,
+            "device_ms_per_call": t_dev * 1e3, "launches_per_call": launches,
             "hbm_frac": byts / t / 1e9 / HBM, "parity_factor_relmax": err,
             "parity_samples_relmax": float(np.abs(got - ref).max() / np.abs(ref).max()),
             "analytic_relmax_200pts": float(np.abs(got[:200] - ana).max() / np.abs(ana).max())}
@@ -245,7 +259,9 @@ def main():
 
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
     which = sys.argv[2].split(",") if len(sys.argv) > 2 else ["0", "1", "3", "4"]
-    ctx = tg.Context(0)
+    import torch
+
+    ctx = tg.Context(0, stream=torch.cuda.current_stream().cuda_stream)  # torch's stream: no cross-stream ordering
     out = []
     for w in which:
         fn = {"0": cfg0, "1": cfg1, "3": cfg3, "4": cfg4, "hf": cfg_hf}[w]
