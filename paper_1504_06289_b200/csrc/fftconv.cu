@@ -39,6 +39,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <mutex>
+#include <set>
 #include <tuple>
 #include <vector>
 
@@ -1819,6 +1821,11 @@ void k12_pairs(tgb_ctx* ctx, int64_t n, const double2* specA, const double* spec
                const PairEntry* work, const int* winfo, double* out, const double* U, int64_t ldu, const double* V,
                int64_t ldv, double h);
 
+// large-n plan (fftconv12k.cu): N = S * 12288 split into S sub-transforms
+int kS_split(int64_t n);
+void kS_convolve_axis(tgb_ctx* ctx, int64_t n, int S, int64_t ra, const double* A, int64_t rb, const double* B,
+                      double h, double* out, const PairEntry* work, const int* winfo, cudaEvent_t join);
+
 // out[ax] (n x ra*rb, column i + ra*j) = h[ax] * window(conv(A_i, B_j)) for
 // naxes axes; device pointers, stream-ordered, no host synchronisation.
 // The kernel columns' duplicate/symmetry flags and the pair work lists are
@@ -1902,7 +1909,20 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
   }
   for (int ax = 0; ax < naxes; ++ax) {
     const ConvPlan& pl = *plans[ax];
+    if (const int S = n[ax] > ctx->direct_max ? kS_split(n[ax]) : 0) {  // beyond one CTA: split transform
+      kS_convolve_axis(ctx, n[ax], S, ra, A[ax], rb, B[ax], h[ax], out[ax], dwork[ax], winfo + 2 * ax, ctx->aux_done);
+      joined = true;
+      continue;
+    }
     if (pl.direct) {
+      if (n[ax] > 4096 && !getenv("TGB_QUIET")) {  // no FFT plan here: O(n^2) per column, say so once
+        static std::set<int64_t> warned;
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lk(mu);
+        if (warned.insert(n[ax]).second)
+          fprintf(stderr, "[tgb] convolve: n = %lld has no FFT plan (even n > 16385 or n > 65537): direct O(n^2) "
+                          "summation\n", static_cast<long long>(n[ax]));
+      }
       if (!joined) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
       joined = true;
       const int th = static_cast<int>(std::min<int64_t>(256, ((n[ax] + 31) / 32) * 32));

@@ -33,6 +33,7 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 
 #include "fft_common.cuh"
@@ -442,6 +443,309 @@ __global__ void __launch_bounds__(TT, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh) : "memory");
 }
 
+
+// ---------------------------------------------------------------- large n: N = S * 12288 (S = 2..8)
+// Beyond one CTA's shared memory (n > 16385) the length-N transform is split
+// into S independent sub-transforms of H = 12288, each one CTA, on the same
+// 4-stage machinery (tools/proto_n12k.py's index scheme at H):
+//  forward  Z[S k' + g] = sum_t' w_H^{-k't'} [ w_N^{-g t'} sum_q z[t' + q H] e^{-2 pi i g q/S} ]
+//  inverse  z[S t + g]  = sum_k  w_H^{k t}  [ sum_q Z[k + q H] w_N^{(k + q H) g} ]
+// (decimation of the transform's output / of the inverse's output index by S).
+// The forward sub-spectra land interleaved in a scratch and one O(N) pass forms
+// the half spectra; the inverse writes its window elements interleaved (stride
+// S).  m = 2N is the alias-free minimum, or one below it with the two boundary
+// products subtracted as in the N = 12288 plan (n = 32769 -> S = 2,
+// n = 65537 -> S = 4).
+constexpr int kMaxS = 8;
+
+__global__ void __launch_bounds__(TT, 1)
+    kS_spectrum_kernel(int n, int S, const double* __restrict__ XA, int nA, const double* __restrict__ XB, int nB,
+                       int64_t ldx, double2* __restrict__ Zout) {
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x;
+  const int col = blockIdx.x, g = blockIdx.y;
+  const bool isB = col < nB;
+  const double* x = isB ? XB + static_cast<int64_t>(col) * ldx : XA + static_cast<int64_t>(col - nB) * ldx;
+  const int64_t NN = static_cast<int64_t>(S) * N;
+  double2* eq = sm + SLOTS;  // e^{-2 pi i g q / S}
+  if (tid < S) eq[tid] = cconj(root(static_cast<int64_t>(g) * tid, S));
+  __syncthreads();
+#pragma unroll 1
+  for (int hb = 0; hb < 2; ++hb) {
+    const int tt = tid + TT * hb;
+    double2 v[16];
+    double2 wt = cconj(root(static_cast<int64_t>(g) * tt, NN));  // w_N^{-g t'}, t' = tt + 768 s0
+    const double2 wst = cconj(root(static_cast<int64_t>(g) * NB, NN));
+#pragma unroll
+    for (int s0 = 0; s0 < 16; ++s0) {
+      double2 acc = make_double2(0.0, 0.0);
+      const int64_t tp = tt + NB * s0;
+      for (int q = 0; q < S; ++q) {
+        const int64_t i0 = 2 * (tp + static_cast<int64_t>(q) * N);
+        const double2 z = make_double2(i0 < n ? __ldg(x + i0) : 0.0, i0 + 1 < n ? __ldg(x + i0 + 1) : 0.0);
+        acc = cadd(acc, cmul(z, eq[q]));
+      }
+      v[s0] = cmul(acc, wt);
+      wt = cmul(wt, wst);
+    }
+    dft<16, -1>(v);
+    double2 wp[16];
+    powers<16>(cconj(root(tt, N)), wp);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) sm[slot_kk(t, tt)] = t ? cmul(v[t], wp[t]) : v[t];
+  }
+  __syncthreads();
+  stage2<-1>(sm, tid, cconj(root(tid % 48, 768)));
+  __syncthreads();
+  {
+    const double2 w31 = cconj(root(tid & 15, 48));
+    stage3<-1>(sm, tid, w31, cmul(w31, w31));
+  }
+  __syncthreads();
+  double2* zc = Zout + static_cast<int64_t>(col) * NN;
+#pragma unroll 1
+  for (int hb = 0; hb < 2; ++hb) {
+    const int u = tid + TT * hb;
+    const double2* pp = sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8));
+    double2 v[16];
+#pragma unroll
+    for (int s2 = 0; s2 < 16; ++s2) v[s2] = pp[s2];
+    dft<16, -1>(v);
+#pragma unroll
+    for (int t = 0; t < 16; ++t) zc[static_cast<int64_t>(S) * (u + NB * t) + g] = v[t];
+  }
+}
+
+// half spectra from the interleaved full Z: X[K] = (Z_K + conj Z_{N-K})/2 - i w^-K (Z_K - conj Z_{N-K})/2
+__global__ void kS_post_kernel(int n, int S, const double2* __restrict__ Z, int nA, int nB,
+                               double2* __restrict__ specA, double* __restrict__ specBr, double2* __restrict__ specBc,
+                               int modeB, double h) {
+  const int64_t NN = static_cast<int64_t>(S) * N, m = 2 * NN;
+  const int col = blockIdx.y;
+  const bool isB = col < nB;
+  const double2* zc = Z + static_cast<int64_t>(col) * NN;
+  const int64_t ofs = (n - 1) / 2;
+  const double hm = h / static_cast<double>(m);
+  for (int64_t K = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; K <= NN;
+       K += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t ka = K == NN ? 0 : K, kb = ka == 0 ? 0 : NN - ka;
+    const double2 zk = zc[ka];
+    const double2 zm = cconj(zc[kb]);
+    const double2 sum = cadd(zk, zm), dif = csub(zk, zm);
+    const double2 wd = cmul(cconj(root(K, m)), dif);
+    double2 X = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
+    if (K == 0 || K == NN) X.y = 0.0;
+    if (!isB) {
+      specA[static_cast<int64_t>(col - nB) * (NN + 1) + K] = X;
+    } else {
+      const double2 y = cmul(X, root((K * ofs) % m, m));  // e^{+2 pi i K ofs/m}
+      const int64_t o = static_cast<int64_t>(col) * (NN + 1) + K;
+      if (modeB & 1) specBr[o] = hm * y.x;
+      if (modeB & 2) specBc[o] = cscale(y, hm);
+    }
+  }
+}
+
+// stage 1 of an inverse sub-transform g: Y_g[k] = sum_q Z[k + qH] w_N^{(k + qH) g}
+// (Z from the split of P = A B, zsplit2), two radix-16 blocks per thread, into
+// shared memory in the slot layout.
+template <bool BREAL>
+__device__ __forceinline__ void ks_stage1(double2* sm, int tid, int S, int g, int64_t NN, const double2* __restrict__ a,
+                                          const void* __restrict__ b, const double2* cq, const double2* dq) {
+  const int64_t m = 2 * NN;
+#pragma unroll 1
+    for (int hb = 0; hb < 2; ++hb) {
+      const int kk = tid + TT * hb;
+      double2 x[16];
+      double2 wk = root(kk, m), vk = root(static_cast<int64_t>(kk) * g, NN);  // w_m^k, w_N^{k g}
+      const double2 wst = root(NB, m), vst = root(static_cast<int64_t>(NB) * g, NN);
+#pragma unroll
+      for (int s0 = 0; s0 < 16; ++s0) {
+        double2 acc = make_double2(0.0, 0.0);
+        for (int q = 0; q < S; ++q) {
+          const int64_t K = kk + static_cast<int64_t>(NB) * s0 + static_cast<int64_t>(q) * N;
+          const double2 pk = bmul<BREAL>(ld2(a + K), b, static_cast<int>(K));
+          const double2 pn = bmul<BREAL>(ld2(a + NN - K), b, static_cast<int>(NN - K));
+          double2 zp, zq;
+          zsplit2(pk, pn, cmul(wk, cq[q]), zp, zq);
+          acc = cadd(acc, cmul(zp, cmul(vk, dq[q])));
+        }
+        x[s0] = acc;
+        wk = cmul(wk, wst);
+        vk = cmul(vk, vst);
+      }
+      dft<16, 1>(x);
+      double2 wp[16];
+      powers<16>(root(kk, N), wp);
+#pragma unroll
+      for (int t = 0; t < 16; ++t) sm[slot_kk(t, kk)] = t ? cmul(x[t], wp[t]) : x[t];
+    }
+}
+
+template <bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    kS_pair_kernel(int n, int S, const double2* __restrict__ specA, const void* __restrict__ specB,
+                   const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out,
+                   const double* __restrict__ U, int64_t ldu, const double* __restrict__ V, int64_t ldv, double h,
+                   int alias) {
+  if ((winfo[1] != 0) != BREAL) return;
+  const int64_t nitems = static_cast<int64_t>(winfo[0]) * S;
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x;
+  const int64_t NN = static_cast<int64_t>(S) * N, m = 2 * NN;
+  double2* cq = sm + SLOTS;          // w_m^{qH} = e^{i pi q / S}
+  double2* dq = cq + kMaxS;          // w_N^{q H g} = e^{2 pi i q g / S}   (per item)
+  double2* cst = dq + kMaxS;         // per-thread stage-2/3 bases
+  cst[3 * tid] = root(tid % 48, 768);
+  cst[3 * tid + 1] = root(tid & 15, 48);
+  cst[3 * tid + 2] = cmul(cst[3 * tid + 1], cst[3 * tid + 1]);
+  if (tid < S) cq[tid] = root(tid, 2 * S);
+  const int nz = (n + 1) >> 1;
+  const bool odd_n = n & 1;
+  const int64_t i0 = nitems * blockIdx.x / gridDim.x, i1 = nitems * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t it = i0; it < i1; ++it) {
+    const PairEntry e = work[it / S];
+    const int g = static_cast<int>(it % S);
+    if (tid < S) dq[tid] = root(static_cast<int64_t>(tid) * g, S);
+    __syncthreads();
+    const double2* a = specA + static_cast<int64_t>(e.ia) * (NN + 1);
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (NN + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (NN + 1));
+    // x[0] -= h f[n-1] p[n-1] (z index 0: thread 0 of sub-transform 0); x[n-1] -= h f[0] p[0]
+    // (z index nz-1: the thread whose stage-4 butterfly stores it, when it belongs to this g)
+    double corr0 = 0.0, corr1 = 0.0;
+    if (alias && g == 0 && tid == 0) corr0 = h * __ldg(U + e.ia * ldu + n - 1) * __ldg(V + e.jb * ldv + n - 1);
+    if (alias && (nz - 1 - g) % S == 0 && ((nz - 1 - g) / S) % NB % TT == tid)
+      corr1 = h * __ldg(U + e.ia * ldu) * __ldg(V + e.jb * ldv);
+    ks_stage1<BREAL>(sm, tid, S, g, NN, a, b, cq, dq);
+    __syncthreads();
+    stage2<1>(sm, tid, cst[3 * tid]);
+    __syncthreads();
+    stage3<1>(sm, tid, cst[3 * tid + 1], cst[3 * tid + 2]);
+    __syncthreads();
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+#pragma unroll 1
+    for (int hb = 0; hb < 2; ++hb) {
+      const int u = tid + TT * hb;
+      const double2* pp = sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8));
+      double2 v[16];
+#pragma unroll
+      for (int s2 = 0; s2 < 16; ++s2) v[s2] = pp[s2];
+      dft<16, 1>(v);
+#pragma unroll
+      for (int t3 = 0; t3 < 16; ++t3) {
+        const int64_t j = static_cast<int64_t>(S) * (u + NB * t3) + g;  // z index
+        if (j >= nz) continue;
+        double2 val = v[t3];
+        if (alias) {
+          if (j == 0) val.x -= corr0;
+          if (j == nz - 1) val.x -= corr1;
+        }
+        const bool full = !(odd_n && j == nz - 1);
+        __stcs(o0 + 2 * j, val.x);
+        if (full) __stcs(o0 + 2 * j + 1, val.y);
+        if (o1) {
+          __stcs(o1 + 2 * j, val.x);
+          if (full) __stcs(o1 + 2 * j + 1, val.y);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// S = 2 (16385 < n <= 32769): one CTA computes BOTH sub-transforms of a pair,
+// so the window leaves as contiguous 8-byte stores across the warp (the
+// interleaved z[2t + g] stores of one sub-transform per CTA run at a fraction
+// of the store rate, tools/probe/store_probe.cu).  Sub-transform 0's outputs
+// y0[t] go to a per-CTA scratch in t order (coalesced, L2-resident); sub-
+// transform 1's stay in shared memory (in-place stage 4); one pass then
+// writes x[p] = (p/2 even ? y0 : y1)[p/4].(p%2) for consecutive p.
+template <bool BREAL>
+__global__ void __launch_bounds__(TT, 1)
+    kS2_pair_kernel(int n, const double2* __restrict__ specA, const void* __restrict__ specB,
+                    const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out,
+                    const double* __restrict__ U, int64_t ldu, const double* __restrict__ V, int64_t ldv, double h,
+                    int alias, double2* __restrict__ scratch) {
+  if ((winfo[1] != 0) != BREAL) return;
+  constexpr int S = 2;
+  const int nwork = winfo[0];
+  extern __shared__ double2 sm[];
+  const int tid = threadIdx.x;
+  const int64_t NN = static_cast<int64_t>(S) * N;
+  double2* cq = sm + SLOTS;
+  double2* dq0 = cq + kMaxS;
+  double2* dq1 = dq0 + kMaxS;
+  double2* cst = dq1 + kMaxS;
+  cst[3 * tid] = root(tid % 48, 768);
+  cst[3 * tid + 1] = root(tid & 15, 48);
+  cst[3 * tid + 2] = cmul(cst[3 * tid + 1], cst[3 * tid + 1]);
+  if (tid < S) {
+    cq[tid] = root(tid, 2 * S);
+    dq0[tid] = make_double2(1.0, 0.0);
+    dq1[tid] = root(tid, S);
+  }
+  double2* y0 = scratch + static_cast<int64_t>(blockIdx.x) * N;
+  const int nz = (n + 1) >> 1;
+  const int w0 = static_cast<int>(static_cast<int64_t>(nwork) * blockIdx.x / gridDim.x);
+  const int w1 = static_cast<int>(static_cast<int64_t>(nwork) * (blockIdx.x + 1) / gridDim.x);
+  __syncthreads();
+  for (int w = w0; w < w1; ++w) {
+    const PairEntry e = work[w];
+    const double2* a = specA + static_cast<int64_t>(e.ia) * (NN + 1);
+    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (NN + 1))
+                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (NN + 1));
+#pragma unroll 1
+    for (int g = 0; g < S; ++g) {
+      ks_stage1<BREAL>(sm, tid, S, g, NN, a, b, cq, g ? dq1 : dq0);
+      __syncthreads();
+      stage2<1>(sm, tid, cst[3 * tid]);
+      __syncthreads();
+      stage3<1>(sm, tid, cst[3 * tid + 1], cst[3 * tid + 2]);
+      __syncthreads();
+#pragma unroll 1
+      for (int hb = 0; hb < 2; ++hb) {
+        const int u = tid + TT * hb;
+        double2* pp = sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8));
+        double2 v[16];
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) v[s2] = pp[s2];
+        dft<16, 1>(v);
+        if (g == 0) {
+#pragma unroll
+          for (int t3 = 0; t3 < 16; ++t3) __stcg(y0 + u + NB * t3, v[t3]);  // y0[t], t = u + 768 t3
+        } else {
+#pragma unroll
+          for (int t3 = 0; t3 < 16; ++t3) pp[t3] = v[t3];  // in place: y1[t] in the slot of input t3
+        }
+      }
+      __syncthreads();
+    }
+    // window out: x[p], p < n, z index j = p / 2 (sub-transform j % 2, t = j / 2)
+    double* o0 = out + e.out0;
+    double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
+    double c0 = 0.0, c1 = 0.0;
+    if (alias) {
+      c0 = h * __ldg(U + e.ia * ldu + n - 1) * __ldg(V + e.jb * ldv + n - 1);
+      c1 = h * __ldg(U + e.ia * ldu) * __ldg(V + e.jb * ldv);
+    }
+    for (int p = tid; p < n; p += TT) {
+      const int j = p >> 1, t = j >> 1;
+      const int u = t % NB, t3 = t / NB;
+      const double2 z = (j & 1) ? sm[slot(u & 15, (u >> 4) & 15, 16 * (u >> 8) + t3)] : __ldcg(y0 + t);
+      double val = (p & 1) ? z.y : z.x;
+      if (alias) {
+        if (p == 0) val -= c0;
+        if (p == n - 1) val -= c1;
+      }
+      __stcs(o0 + p, val);
+      if (o1) __stcs(o1 + p, val);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace k12
 
 // ---------------------------------------------------------------- host side
@@ -513,6 +817,81 @@ void k12_pairs(tgb_ctx* ctx, int64_t n, const double2* specA, const double* spec
   // both forms; the one that disagrees with the device-side symmetry flag returns at once
   k12_pairs_t<true>(ctx, n, specA, specBr, work, winfo, out, U, ldu, V, ldv, h);
   k12_pairs_t<false>(ctx, n, specA, specBc, work, winfo, out, U, ldu, V, ldv, h);
+}
+
+}  // namespace tgb
+
+namespace tgb {
+
+// Large-n plan: odd n > 16385 with m = 2 S 12288 >= (3n - 3)/2 (S <= 8, n <= 65537);
+// 0 when not applicable (even n or larger n keep the direct summation).
+int kS_split(int64_t n) {
+  if (n % 2 == 0 || n <= 16385 || getenv("TGB_NO_KS")) return 0;
+  const int64_t need = (3 * n - 3) / 2;
+  const int64_t S = (need + 2 * k12::N - 1) / (2 * k12::N);
+  return S <= k12::kMaxS ? static_cast<int>(S) : 0;
+}
+
+void kS_convolve_axis(tgb_ctx* ctx, int64_t n, int S, int64_t ra, const double* A, int64_t rb, const double* B,
+                      double h, double* out, const PairEntry* work, const int* winfo, cudaEvent_t join) {
+  const int64_t NN = static_cast<int64_t>(S) * k12::N;
+  const bool alias = (3 * n - 3) / 2 == 2 * NN;
+  auto* Zs = static_cast<double2*>(ctx_buf(ctx, "kS.Z").get(static_cast<size_t>(ra + rb) * NN * sizeof(double2)));
+  auto* specA = static_cast<double2*>(ctx->ws_spec_a.get(static_cast<size_t>(ra) * (NN + 1) * sizeof(double2)));
+  const size_t real_bytes = (static_cast<size_t>(rb) * (NN + 1) * sizeof(double) + 255) & ~size_t(255);
+  char* sb = static_cast<char*>(ctx->ws_spec_b.get(real_bytes + static_cast<size_t>(rb) * (NN + 1) * sizeof(double2)));
+  auto* specBr = reinterpret_cast<double*>(sb);
+  auto* specBc = reinterpret_cast<double2*>(sb + real_bytes);
+  const size_t smem_spec = k12::kSmem + k12::kMaxS * sizeof(double2);
+  const size_t smem_pair = k12::kSmem + (2 * k12::kMaxS + 3 * k12::TT) * sizeof(double2);
+  static bool attr[kTgbMaxDevices] = {};
+  if (!attr[ctx->device]) {
+    TGB_CUDA(cudaFuncSetAttribute(k12::kS_spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_spec)));
+    TGB_CUDA(cudaFuncSetAttribute(k12::kS_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_pair)));
+    TGB_CUDA(cudaFuncSetAttribute(k12::kS_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem_pair)));
+    attr[ctx->device] = true;
+  }
+  k12::kS_spectrum_kernel<<<dim3(static_cast<unsigned>(ra + rb), S), k12::TT, smem_spec, ctx->stream>>>(
+      static_cast<int>(n), S, A, static_cast<int>(ra), B, static_cast<int>(rb), n, Zs);
+  TGB_LAUNCHED(ctx);
+  const unsigned pblocks = static_cast<unsigned>(std::min<int64_t>((NN + 256) / 256, 64));
+  k12::kS_post_kernel<<<dim3(pblocks, static_cast<unsigned>(ra + rb)), 256, 0, ctx->stream>>>(
+      static_cast<int>(n), S, Zs, static_cast<int>(ra), static_cast<int>(rb), specA, specBr, specBc, 3, h);
+  TGB_LAUNCHED(ctx);
+  TGB_CUDA(cudaStreamWaitEvent(ctx->stream, join, 0));
+  if (S == 2 && !getenv("TGB_KS_INTERLEAVED")) {
+    const size_t smem2 = k12::kSmem + (3 * k12::kMaxS + 3 * k12::TT) * sizeof(double2);
+    static bool attr2[kTgbMaxDevices] = {};
+    if (!attr2[ctx->device]) {
+      TGB_CUDA(cudaFuncSetAttribute(k12::kS2_pair_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem2)));
+      TGB_CUDA(cudaFuncSetAttribute(k12::kS2_pair_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(smem2)));
+      attr2[ctx->device] = true;
+    }
+    auto* scr = static_cast<double2*>(ctx_buf(ctx, "kS.y0").get(static_cast<size_t>(ctx->num_sms) * k12::N *
+                                                                  sizeof(double2)));
+    prof_begin(ctx);
+    k12::kS2_pair_kernel<true><<<ctx->num_sms, k12::TT, smem2, ctx->stream>>>(
+        static_cast<int>(n), specA, specBr, work, winfo, out, A, n, B, n, h, alias ? 1 : 0, scr);
+    TGB_LAUNCHED(ctx);
+    prof_end(ctx);
+    k12::kS2_pair_kernel<false><<<ctx->num_sms, k12::TT, smem2, ctx->stream>>>(
+        static_cast<int>(n), specA, specBc, work, winfo, out, A, n, B, n, h, alias ? 1 : 0, scr);
+    TGB_LAUNCHED(ctx);
+    return;
+  }
+  prof_begin(ctx);
+  k12::kS_pair_kernel<true><<<ctx->num_sms, k12::TT, smem_pair, ctx->stream>>>(
+      static_cast<int>(n), S, specA, specBr, work, winfo, out, A, n, B, n, h, alias ? 1 : 0);
+  TGB_LAUNCHED(ctx);
+  prof_end(ctx);
+  k12::kS_pair_kernel<false><<<ctx->num_sms, k12::TT, smem_pair, ctx->stream>>>(
+      static_cast<int>(n), S, specA, specBc, work, winfo, out, A, n, B, n, h, alias ? 1 : 0);
+  TGB_LAUNCHED(ctx);
 }
 
 }  // namespace tgb

@@ -860,6 +860,10 @@ struct RedState {
   bool rank_clamped = false, fallback = false;
   std::vector<double> sweep_fits;
   std::array<std::vector<double>, 3> sigma;
+  // rank-selection margins of the initializing SVDs (tgb_tucker_margins)
+  std::array<double, 3> total{};  // sum of ALL squared singular values of the mode's side matrix
+  bool use_eps = false;
+  double eps = 0.0;
 };
 
 // select_rank (reduction.cpp:34-59) on the leading singular values sg (descending);
@@ -904,7 +908,7 @@ static int64_t select_rank_host(const std::vector<double>& sg, double total, int
 // the Cholesky-QR so the blocks stay well conditioned.
 static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a, const RedCfgC* cfg, int mode,
                              int64_t sel, bool* clamped, Dev& Zout, std::vector<double>* sigma_out,
-                             const double* warm = nullptr, int64_t warm_cols = 0) {
+                             const double* warm = nullptr, int64_t warm_cols = 0, double* total_out = nullptr) {
   if (n == 0 || k == 0) {
     if (sigma_out) sigma_out->clear();
     return 0;
@@ -1030,6 +1034,7 @@ static int64_t left_subspace(tgb_ctx* ctx, int64_t n, int64_t k, const double* a
     r = select_rank_host(sg, total, dmin, *cfg, mode, clamped, &more);
   }
   if (sigma_out) *sigma_out = sg;
+  if (total_out) *total_out = total;
   Zout.resize(std::max<int64_t>(1, n * r));
   if (r > 0)
     TGB_CUDA(cudaMemcpyAsync(Zout.p, X.p, static_cast<size_t>(n) * r * sizeof(double), cudaMemcpyDeviceToDevice,
@@ -1097,7 +1102,10 @@ void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, Red
       scale_cols_kernel<<<static_cast<unsigned>((n * R + 255) / 256), 256, 0, ctx->stream>>>(n, R, st.f[mode], st.w, W.p);
       TGB_LAUNCHED(ctx);
     }
-    st.r[mode] = left_subspace(ctx, n, R, W.p, &cfg, mode, -1, &st.rank_clamped, st.Z[mode], &st.sigma[mode]);
+    st.r[mode] = left_subspace(ctx, n, R, W.p, &cfg, mode, -1, &st.rank_clamped, st.Z[mode], &st.sigma[mode],
+                               nullptr, 0, &st.total[mode]);
+    st.use_eps = cfg.use_eps;
+    st.eps = cfg.eps;
     tm.mark("rhosvd left subspace");
   }
   project_core(ctx, st);
@@ -1267,6 +1275,34 @@ int tgb_tucker_sigma(tgb_tucker* t, int axis, int64_t* count, double* sigma) {
     *count = static_cast<int64_t>(s.size());
     if (sigma)
       for (size_t i = 0; i < s.size(); ++i) sigma[i] = s[i];
+  });
+}
+
+// Rank-selection margins of mode `axis` (the RHOSVD initializing SVD,
+// select_rank reduction.cpp:34-59), for judging whether a rank is robust:
+// out = {r, sigma_{r-1} (last kept), sigma_r (first dropped; -1 if not formed),
+//        sigma_{r-1} / sigma_r, tail(r-1) / budget (> 1), tail(r) / budget (<= 1)}
+// with tail(j) = sum_{i >= j} sigma_i^2 and budget = eps^2 * total (eps mode;
+// the two tail ratios are -1 in fixed-rank mode).
+int tgb_tucker_margins(tgb_tucker* t, int axis, double* out) {
+  return tgb::guarded_call([&] {
+    tgb::require(t && out && axis >= 0 && axis < 3, "tucker_margins: bad argument");
+    const auto& st = t->st;
+    const auto& sg = st.sigma[axis];
+    const int64_t r = st.r[axis];
+    out[0] = static_cast<double>(r);
+    out[1] = r >= 1 && r - 1 < static_cast<int64_t>(sg.size()) ? sg[r - 1] : -1.0;
+    out[2] = r < static_cast<int64_t>(sg.size()) ? sg[r] : -1.0;
+    out[3] = out[1] > 0 && out[2] > 0 ? out[1] / out[2] : -1.0;
+    out[4] = out[5] = -1.0;
+    if (st.use_eps && st.total[axis] > 0.0) {
+      const double budget = st.eps * st.eps * st.total[axis];
+      double tail = st.total[axis];
+      for (int64_t i = 0; i + 1 < r && i < static_cast<int64_t>(sg.size()); ++i) tail -= sg[i] * sg[i];
+      out[4] = tail / budget;  // before dropping sigma_{r-1}
+      if (r >= 1 && r - 1 < static_cast<int64_t>(sg.size())) tail -= sg[r - 1] * sg[r - 1];
+      out[5] = tail / budget;
+    }
   });
 }
 

@@ -27,7 +27,7 @@ def window_np(u, v):
 
 
 @pytest.mark.parametrize("n", [1, 2, 3, 5, 16, 17, 31, 64, 65, 100, 127, 128, 129, 200, 513, 1000, 1025, 2048,
-                               2049, 4097, 8193, 16383, 16385])
+                               2049, 4097, 8193, 16383, 16385, 16387, 20001, 32769, 32771, 65537])
 @pytest.mark.parametrize("force_fft", [False, True])
 def test_conv_central_many_matches_oracle(ctx, n, force_fft):
     rng = Rng(1000 + n)

@@ -19,6 +19,20 @@ __global__ void store_kernel(double* out, long long per_cta, int mode, int iters
       for (long long i = threadIdx.x; i < per_cta / 2; i += T) __stcs(p + i, v);
     } else if (mode == 1) {  // 8 B coalesced
       for (long long i = threadIdx.x; i < per_cta; i += T) __stcs(base + i, v.x);
+    } else if (mode == 3) {  // one lane writes 32 B as two back-to-back 16 B stores (lanes at 32 B stride)
+      double2* p = reinterpret_cast<double2*>(base);
+      for (long long i = threadIdx.x; 2 * i + 1 < per_cta / 2; i += T) {
+        __stcs(p + 2 * i, v);
+        __stcs(p + 2 * i + 1, v);
+      }
+    } else if (mode == 4) {  // one lane writes 32 B as four 8 B stores, column base 8 B (not 16 B) aligned
+      double* q = base + 1;
+      for (long long i = threadIdx.x; 4 * i + 3 < per_cta - 1; i += T) {
+        __stcs(q + 4 * i, v.x);
+        __stcs(q + 4 * i + 1, v.y);
+        __stcs(q + 4 * i + 2, v.x);
+        __stcs(q + 4 * i + 3, v.y);
+      }
     } else {  // 16 B at 32 B stride; warps 2w and 2w+1 fill the two halves of each sector
       double2* p = reinterpret_cast<double2*>(base);
       const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, half = w & 1, wp = w >> 1, nwp = T / 64;
@@ -71,10 +85,11 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  const char* names[3] = {"16B coalesced", "8B coalesced", "16B @32B stride, 2 warps/sector"};
-  for (int mode = 0; mode < 3; ++mode) {
-    for (int g : {sms, sms / 2, sms / 4, sms / 8, 8}) {
-      for (int threads : {320, 1024}) {
+  const char* names[5] = {"16B coalesced", "8B coalesced", "16B @32B stride, 2 warps/sector",
+                          "32B/lane as 2x16B (same warp)", "32B/lane as 4x8B, 8B-aligned base"};
+  for (int mode : {0, 2, 3, 4}) {
+    for (int g : {sms, sms / 4}) {
+      for (int threads : {384}) {
         store_kernel<<<g, threads>>>(out, per_cta, mode, 1);
         cudaEventRecord(e0);
         store_kernel<<<g, threads>>>(out, per_cta, mode, 2);
@@ -93,7 +108,7 @@ int main() {
   // mixed FP64 pipes: 8 warps per CTA, 4 CTAs/SM-equivalent grid
   double* o2;
   cudaMalloc(&o2, sizeof(double) * sms * 8 * 256);
-  for (int dw : {0, 8, 4, 2}) {
+  for (int dw : {0}) {
     const int iters = 2000;
     mixed_fp64<<<sms * 8, 256>>>(o2, iters, dw);
     cudaEventRecord(e0);
