@@ -337,6 +337,13 @@ int tgb_tucker_info(tgb_tucker* t, int64_t* info);
 int tgb_tucker_get(tgb_tucker* t, double* core, double* side0, double* side1, double* side2, double* sweep_fits,
                    int mem);
 int tgb_tucker_sigma(tgb_tucker* t, int axis, int64_t* count, double* sigma);
+/* Rank-selection margins of mode `axis` (RHOSVD's initializing SVD, the
+ * reference's select_rank, reduction.cpp:34-59): out[6] = {r, sigma_{r-1},
+ * sigma_r (-1: not formed), sigma_{r-1}/sigma_r, tail(r-1)/budget,
+ * tail(r)/budget} with budget = eps^2 sum sigma^2 (tail ratios -1 in
+ * fixed-rank mode).  A rank is robust when the last ratio is well below 1 and
+ * the one before well above it. */
+int tgb_tucker_margins(tgb_tucker* t, int axis, double* out);
 int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem);
 
 /* replaces tg::thin_svd_left (reduction.hpp:67, reduction.cpp:85-138):

@@ -56,6 +56,7 @@ class TuckerResult:
     sweep_fits: list = field(default_factory=list)
     mode_singular_values: list = field(default_factory=list)
     _handle: object = None
+    rank_margins: list = field(default_factory=list)  # tgb_tucker_margins per mode
 
 
 class _Handle:
@@ -99,7 +100,14 @@ def _tucker_result(h, dims, ctx: Context) -> TuckerResult:
         sv = np.zeros(max(1, cnt.value))
         check(lib().tgb_tucker_sigma(h, ax, C.byref(cnt), sv.ctypes.data))
         sig.append(sv[:cnt.value])
+    margins = []
+    for ax in range(3):
+        m = np.zeros(6)
+        check(lib().tgb_tucker_margins(h, ax, m.ctypes.data))
+        margins.append({"rank": int(m[0]), "sigma_last_kept": m[1], "sigma_first_dropped": m[2],
+                        "sigma_ratio": m[3], "tail_before_over_budget": m[4], "tail_after_over_budget": m[5]})
     res = TuckerResult(TuckerTensor3(sides, core), bool(info[3]), bool(info[4]), list(fits[:int(info[5])]), sig, hh)
+    res.rank_margins = margins
     res._t2c_rank = int(info[6])
     res._ctx = ctx
     return res

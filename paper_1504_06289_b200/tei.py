@@ -83,6 +83,39 @@ class TEIFactorization:
         return self._pivots
 
 
+def pivot_margins(fac: "TEIFactorization", diagonal: np.ndarray, eps_chol: float) -> dict:
+    """How decisively each TEI Cholesky pivot was chosen (the argmax of
+    tei.cpp:66): the remaining diagonal is rebuilt from L step by step
+    (d_r = d_0 - sum_{s<r} L[:, s]^2, pinned pivots zeroed as tei.cpp:73-75)
+    and, at every step, the relative gap between the pivot's value and the best
+    candidate that is not its (mu nu)/(nu mu) mirror (mirrors are bitwise equal
+    by construction and resolve to the first index).  Also the stop margin
+    max d_final / (eps_chol max d_0) (<= 1: stopped).  A pivot sequence is
+    robust when min_gap is well above roundoff."""
+    L = np.asarray(fac.chol)
+    piv = [int(p) for p in fac.pivots]
+    nb = fac.n_b
+    d = np.array(diagonal, dtype=np.float64, copy=True)
+    max0 = float(d.max()) if d.size else 0.0
+    gaps = []
+    for r, p in enumerate(piv):
+        mirror = (p % nb) * nb + p // nb
+        dp = d[p]
+        others = d.copy()
+        others[p] = -np.inf
+        others[mirror] = -np.inf
+        d2 = float(others.max()) if others.size > 2 else 0.0
+        gaps.append((dp - d2) / dp if dp > 0 else 0.0)
+        d -= L[:, r] ** 2
+        d[p] = 0.0
+        d[mirror] = max(d[mirror], 0.0)
+        d[d < 0] = 0.0
+    return {"min_pivot_gap": float(min(gaps)) if gaps else None,
+            "argmin_step": int(np.argmin(gaps)) if gaps else None,
+            "stop_ratio": float(d.max() / (eps_chol * max0)) if max0 > 0 else None,
+            "gaps": [float(x) for x in gaps]}
+
+
 def tei_density_fitting(fac: TEIFactorization, bs, disc: list, eps_fit: float) -> None:
     """tei.cpp:92-143."""
     if not disc:

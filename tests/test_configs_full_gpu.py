@@ -3,9 +3,15 @@ reference's own code computed (tools/make_golden_configs.py on oracle/_ref).
 
 * config 4 (lattice_sum_canonical, L=32, n=32769): every factor matrix
   bit-identical (SHA-256), window_ops = 3L, value_at at 10^5 points <= 1e-13.
-* config 3 (build_tei, N_b=80, n=4097, eps 1e-6): fit ranks, R_B and the whole
-  pivot sequence identical; the TEI diagonal, L L^T at 4096 probes and four B
-  columns within 1e-10 (relative max-norm).
+* config 3 (build_tei, N_b=80, n=4097, eps 1e-6): fit ranks and R_B identical;
+  L L^T at 4096 probes within 1e-10; the pivot sequence identical up to the
+  first near-tie (a step whose argmax margin is below 1e-9 relative); the TEI
+  diagonal and four B columns within 1e-8.  That bound is set by the
+  reference's OWN reproducibility at this size: moving every primitive
+  exponent by one ulp changes its diagonal by 1.3e-9 and its pivot sequence
+  (profiles/r02_tei_reference_sensitivity.json, tools/tei_sensitivity.py) —
+  the fit basis is the QR of a pivoted Cholesky factor stopped at a 1e-12
+  trace residual, conditioned ~1e6.
 * config 1 (density_tensor -> V_H -> J, n=2049, N_b=40): Tucker and canonical
   ranks identical.  The reduced density is an eps = 1e-6 approximation whose
   factors two correct implementations choose differently (the reference's Gram
@@ -26,6 +32,7 @@ from paper_1504_06289_b200.inputs import (KERNEL_C0, KERNEL_M, Rng, basis_case, 
 
 pytestmark = pytest.mark.gpu
 GOLD = Path(__file__).resolve().parent / "golden"
+TOL3 = 1e-8  # the reference's own 1-ulp sensitivity is 1.3e-9 (see above)
 
 
 def _sha(a):
@@ -63,16 +70,27 @@ def test_config3_tei_full(ctx):
     assert fac.fit_ranks() == tuple(int(x) for x in g["fit_ranks"])
     tg.tei_convolution_matrices(fac, kern)
     d = tg.tei_diagonal(fac)
-    assert relmax(d, g["diagonal"]) <= 1e-10
-    for c, j in enumerate(g["b_cols"]):
-        assert relmax(tg.tei_column(fac, int(j)), g["B"][:, c]) <= 1e-10
+    e_diag = relmax(d, g["diagonal"])
+    e_cols = max(relmax(tg.tei_column(fac, int(j)), g["B"][:, c]) for c, j in enumerate(g["b_cols"]))
     tg.tei_cholesky(fac, 1e-6)
-    assert fac.rank_b() == int(g["rank_b"])
-    assert list(fac.pivots) == [int(p) for p in g["pivots"]]
+    from paper_1504_06289_b200.tei import pivot_margins
+
     L = np.asarray(fac.chol)
     pr = g["probes"]
-    llt = np.einsum("ij,ij->i", L[pr[:, 0]], L[pr[:, 1]])
-    assert np.abs(llt - g["llt"]).max() <= 1e-10 * np.abs(g["diagonal"]).max()
+    same_rb = fac.rank_b() == int(g["rank_b"])
+    piv = list(fac.pivots)
+    first_diff = next((i for i, (a, b) in enumerate(zip(piv, g["pivots"])) if a != b), None)
+    e_llt = (np.abs(np.einsum("ij,ij->i", L[pr[:, 0]], L[pr[:, 1]]) - g["llt"]).max() / np.abs(g["diagonal"]).max()
+             if same_rb else None)
+    mg = pivot_margins(fac, d, 1e-6)
+    gaps = mg.pop("gaps")
+    k0 = next((i for i, x in enumerate(gaps) if x < 1e-9), len(gaps))  # first near-tie
+    print(f"config 3: diag {e_diag:.3e} B cols {e_cols:.3e} LLt {e_llt} R_B {fac.rank_b()}/{int(g['rank_b'])} "
+          f"first pivot difference at {first_diff}, first near-tie at {k0}; margins {mg}")
+    assert same_rb and len(piv) == len(g["pivots"])
+    assert first_diff is None or first_diff >= k0
+    assert e_llt <= 1e-10
+    assert e_diag <= TOL3 and e_cols <= TOL3
 
 
 def test_config1_density_vh_j_full(ctx):
@@ -87,6 +105,7 @@ def test_config1_density_vh_j_full(ctx):
         theta = tg.add(theta, tg.scale(tg.hadamard(phi, phi), 2.0))
     assert theta.rank() == int(g["unreduced_rank"])
     res = tg.canonical_to_tucker(theta, tg.ReductionConfig.tolerance(1e-6), ctx)
+    print("config 1 rank margins:", res.rank_margins)
     assert list(res.tucker.ranks()) == [int(x) for x in g["tucker_ranks"]]
     red = tg.density_tensor(disc, c_occ, 1e-6, ctx)
     assert red.rank() == int(g["canonical_rank"])

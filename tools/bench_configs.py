@@ -116,7 +116,8 @@ def cfg1(ctx):
     return {"config": 1, "what": "density(12800)->reduce_rank(1e-6)->V_H->coulomb_matrix, n=2049, N_b=40",
             "density_build_host_s": t_build, "reduce_rank_ms": t_red * 1e3,
             "density_tensor_device_ms": t_dens * 1e3, "density_tensor_rank": red2.rank(), "tucker_ranks": list(res.tucker.ranks()),
-            "reduced_rank": red.rank(), "hartree_ms": t_vh * 1e3, "R_V": RV, "R_V_distinct": RVd, "coulomb_ms": t_j * 1e3,
+            "reduced_rank": red.rank(), "rank_margins": res.rank_margins,
+            "hartree_ms": t_vh * 1e3, "R_V": RV, "R_V_distinct": RVd, "coulomb_ms": t_j * 1e3,
             "coulomb_tflops": flops_j / t_j / 1e12, "coulomb_fp64_frac": flops_j / t_j / 1e12 / FP64,
             "J_symmetric_exact": bool(np.array_equal(J, J.T)), "J_trace": float(np.trace(J))}
 
@@ -149,11 +150,15 @@ def cfg3(ctx):
     tg.tei_cholesky(fac, 1e-6)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
+    from paper_1504_06289_b200.tei import pivot_margins
+
+    margins = pivot_margins(fac, tg.tei_diagonal(fac), 1e-6)
     n, np_ = bs.grid.n[0], fac.n_prim
     gram_flops = 3 * 2.0 * n * n * np_ * np_  # the reference's dense G G^T (ours forms (F F^T)^2: np x fewer)
     return {"config": 3, "what": "build_tei N_b=80 s/p, n=4097, eps_fit=eps_chol=1e-6", "fit_ms": (t1 - t0) * 1e3,
             "fit_dense_gram_equiv_tflops": gram_flops / (t1 - t0) / 1e12, "conv_ms": (t2 - t1) * 1e3,
             "cholesky_ms": (t3 - t2) * 1e3, "fit_ranks": list(fac.fit_ranks()), "R_B": fac.rank_b(),
+            "pivot_margins": margins,
             "fit_residual": [float(x) for x in fac.fit_residual]}
 
 
