@@ -111,3 +111,15 @@ def test_mode_rank_beyond_shared_memory_jacobi(ctx):
     o1 = O.reduce(O.OCP.from_cp(a), eps=1e-10, mode=1)
     assert c2t.tucker.ranks() == o1["ranks"] == (30, 6, 5)
     assert relmax(c2t.tucker.to_dense(), a.to_dense()) <= 1e-10
+
+
+@pytest.mark.timeout(300)
+def test_rank_beyond_subspace_block_fails_not_hangs(ctx):
+    """a fixed rank above the subspace-iteration block (1020 columns)
+    with min(n, R) > 1024 must raise NumericalError, not loop."""
+    rng = Rng(31)
+    n, R = 1100, 1100
+    f = [np.asfortranarray(rng.normal(n * R).reshape(n, R, order="F")) for _ in range(3)]
+    a = tg.CanonicalTensor3(f, np.ones(R))
+    with pytest.raises(tg.NumericalError):
+        tg.canonical_to_tucker(a, tg.ReductionConfig.fixed(1030, 4, 4), ctx)
