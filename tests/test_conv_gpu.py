@@ -249,3 +249,24 @@ def test_hartree_config2_full_benchmarked_path(ctx):
                 assert relmax(blk[:, c], ref[:, c]) <= TOL, (ax, ii[c], j, relmax(blk[:, c], ref[:, c]))
     del d_out
     torch.cuda.empty_cache()
+
+
+def test_pair_kernels_deterministic(ctx):
+    """Race evidence in lieu of compute-sanitizer (closed on this pool): the
+    config-2 plan with several pairs per CTA, density-column switches and
+    twin columns, and the split plan (n = 32769), run twice on the same inputs,
+    give bit-identical factors."""
+    rng = Rng(99)
+    for n, ra in ((16385, 300), (32769, 40)):
+        dims = (n, n, n)
+        fa = [np.asfortranarray(rng.normal(n * ra).reshape(n, ra, order="F")) for _ in dims]
+        x = np.arange(n) - 0.5 * (n - 1)
+        g = np.exp(-(x / 700.0) ** 2)
+        fb = [np.asfortranarray(np.stack([g, g], axis=1)) for _ in dims]
+        a = DeviceCP.from_host(CanonicalTensor3(fa, np.ones(ra)))
+        b = DeviceCP.from_host(CanonicalTensor3(fb, np.ones(2)))
+        c1 = convolve(a, b, 0.01, ctx)
+        c2 = convolve(a, b, 0.01, ctx)
+        ctx.synchronize()
+        for ax in range(3):
+            assert bool((c1.factor[ax] == c2.factor[ax]).all()), (n, ax)
