@@ -592,7 +592,7 @@ __global__ void __launch_bounds__(TT, 1)
   const int64_t nitems = static_cast<int64_t>(winfo[0]) * S;
   extern __shared__ double2 sm[];
   const int tid = threadIdx.x;
-  const int64_t NN = static_cast<int64_t>(S) * N, m = 2 * NN;
+  const int64_t NN = static_cast<int64_t>(S) * N;
   double2* cq = sm + SLOTS;          // w_m^{qH} = e^{i pi q / S}
   double2* dq = cq + kMaxS;          // w_N^{q H g} = e^{2 pi i q g / S}   (per item)
   double2* cst = dq + kMaxS;         // per-thread stage-2/3 bases
@@ -687,7 +687,6 @@ __global__ void __launch_bounds__(TT, 1)
     dq1[tid] = root(tid, S);
   }
   double2* y0 = scratch + static_cast<int64_t>(blockIdx.x) * N;
-  const int nz = (n + 1) >> 1;
   const int w0 = static_cast<int>(static_cast<int64_t>(nwork) * blockIdx.x / gridDim.x);
   const int w1 = static_cast<int>(static_cast<int64_t>(nwork) * (blockIdx.x + 1) / gridDim.x);
   __syncthreads();
