@@ -13,6 +13,7 @@ ctx = tg.Context(0, stream=stream.cuda_stream)
 shapes = [  # (ta, tb, M, N, K)
     (0, 0, 2049, 96, 12800), (1, 0, 12800, 96, 2049), (1, 0, 96, 96, 2049), (0, 0, 2049, 2950, 12800),
     (1, 0, 53, 12800, 2049), (0, 1, 53, 2950, 12800), (1, 0, 50, 2950, 2049), (0, 0, 4097, 4097, 4097),
+    (1, 0, 32768, 820, 2049), (1, 0, 22882, 820, 2049),
 ]
 for ta, tb, M, N, K in shapes:
     A = torch.randn((K, M) if ta else (M, K), dtype=torch.float64, device="cuda").t().contiguous().t()
