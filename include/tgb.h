@@ -139,6 +139,15 @@ int tgb_value_at(tgb_ctx* ctx, const tgb_cp* t, int64_t npts, const int64_t* ijk
 int tgb_value_at_allreduce(tgb_ctx* ctx, const tgb_cp* t_shard, int64_t npts, const int64_t* ijk, double* out,
                            int mem);
 
+/* ---- canonical-tensor algebra (tensor.hpp:173-177, tensor.cpp:141-177) -------
+ * replaces tg::hadamard: out rank a.rank * b.rank, column i + a.rank j =
+ * a_i .* b_j per axis, weight a.w[i] b.w[j];  tg::add: out rank a.rank + b.rank,
+ * [a | b];  tg::scale: weights times alpha.  `out` caller-allocated; all
+ * element-wise, bit-identical to the reference. */
+int tgb_hadamard(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, tgb_cp* out, int mem);
+int tgb_add(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, tgb_cp* out, int mem);
+int tgb_scale(tgb_ctx* ctx, const tgb_cp* a, double alpha, tgb_cp* out, int mem);
+
 /* ---- assembly --------------------------------------------------------------
  * replaces tg::scalar_product(CanonicalTensor3, CanonicalTensor3)
  * (tensor.hpp:173, tensor.cpp:88-98).  Result written to *result (host). */

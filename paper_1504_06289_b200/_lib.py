@@ -118,6 +118,9 @@ def lib() -> C.CDLL:
             "tgb_hartree_potential": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), P, C.POINTER(tgb_cp), I]),
             "tgb_value_at": (I, [P, C.POINTER(tgb_cp), I64, P, P, I]),
             "tgb_scalar_product": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), C.POINTER(D), I]),
+            "tgb_hadamard": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), C.POINTER(tgb_cp), I]),
+            "tgb_add": (I, [P, C.POINTER(tgb_cp), C.POINTER(tgb_cp), C.POINTER(tgb_cp), I]),
+            "tgb_scale": (I, [P, C.POINTER(tgb_cp), D, C.POINTER(tgb_cp), I]),
             "tgb_coulomb_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, P, I]),
             "tgb_lattice_assemble_axis": (I, [P, I64, I64, P, P, I64, P, I]),
             "tgb_nuclear_potential_tensor": (I, [P, C.POINTER(tgb_cp), P, P, I64, C.POINTER(tgb_cp), I]),

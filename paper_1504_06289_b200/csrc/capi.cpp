@@ -141,10 +141,48 @@ struct DevCP {
   }
 };
 
+// device staging of a host output CP (host-memory calls): compute into it, then finish()
+struct DevOutCP {
+  tgb_cp t{};
+  const tgb_cp* host;
+  std::vector<double*> bufs;
+  explicit DevOutCP(const tgb_cp* h) : host(h) {
+    t = *h;
+    for (int ax = 0; ax < 3; ++ax) {
+      double* p = nullptr;
+      const size_t bytes = h->n[ax] * h->rank * sizeof(double);
+      if (bytes) TGB_CUDA(cudaMalloc(&p, bytes));
+      t.factor[ax] = p;
+      bufs.push_back(p);
+    }
+    double* w = nullptr;
+    if (h->rank) TGB_CUDA(cudaMalloc(&w, h->rank * sizeof(double)));
+    t.weight = w;
+    bufs.push_back(w);
+  }
+  void finish(tgb_ctx* ctx) {
+    for (int ax = 0; ax < 3; ++ax)
+      if (host->n[ax] * host->rank)
+        TGB_CUDA(cudaMemcpyAsync(host->factor[ax], t.factor[ax], host->n[ax] * host->rank * sizeof(double),
+                                 cudaMemcpyDeviceToHost, ctx->stream));
+    if (host->rank)
+      TGB_CUDA(cudaMemcpyAsync(host->weight, t.weight, host->rank * sizeof(double), cudaMemcpyDeviceToHost,
+                               ctx->stream));
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  ~DevOutCP() {
+    for (double* p : bufs)
+      if (p) cudaFree(p);
+  }
+};
+
 }  // namespace
 
 namespace tgb {
 void set_last_error(const std::string& msg) { g_last_error = msg; }
+void hadamard_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b, const tgb_cp& out);
+void add_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b, const tgb_cp& out);
+void scale_dev(tgb_ctx* ctx, const tgb_cp& a, double alpha, const tgb_cp& out);
 }  // namespace tgb
 
 extern "C" {
@@ -324,6 +362,65 @@ int tgb_value_at(tgb_ctx* ctx, const tgb_cp* t, int64_t npts, const int64_t* ijk
     tgb::value_at_dev(ctx, d.t, npts, dijk, dout);
     TGB_CUDA(cudaMemcpyAsync(out, dout, npts * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// CP algebra (tensor.cpp:141-177): out is caller-allocated with the result's rank
+int tgb_hadamard(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, tgb_cp* out, int mem) {
+  return guarded([&] {
+    check_cp(a, "hadamard");
+    check_cp(b, "hadamard");
+    check_extents(a, b, "hadamard");
+    check_cp(out, "hadamard");
+    check_extents(a, out, "hadamard");
+    tgb::require(out->rank == a->rank * b->rank, "hadamard: output rank must be a.rank * b.rank");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCP da(a, mem == TGB_MEM_DEVICE), db(b, mem == TGB_MEM_DEVICE);
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::hadamard_dev(ctx, da.t, db.t, *out);
+      return;
+    }
+    DevOutCP o(out);
+    tgb::hadamard_dev(ctx, da.t, db.t, o.t);
+    o.finish(ctx);
+  });
+}
+
+int tgb_add(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, tgb_cp* out, int mem) {
+  return guarded([&] {
+    check_cp(a, "add");
+    check_cp(b, "add");
+    check_extents(a, b, "add");
+    check_cp(out, "add");
+    check_extents(a, out, "add");
+    tgb::require(out->rank == a->rank + b->rank, "add: output rank must be a.rank + b.rank");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCP da(a, mem == TGB_MEM_DEVICE), db(b, mem == TGB_MEM_DEVICE);
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::add_dev(ctx, da.t, db.t, *out);
+      return;
+    }
+    DevOutCP o(out);
+    tgb::add_dev(ctx, da.t, db.t, o.t);
+    o.finish(ctx);
+  });
+}
+
+int tgb_scale(tgb_ctx* ctx, const tgb_cp* a, double alpha, tgb_cp* out, int mem) {
+  return guarded([&] {
+    check_cp(a, "scale");
+    check_cp(out, "scale");
+    check_extents(a, out, "scale");
+    tgb::require(out->rank == a->rank, "scale: output rank must equal a.rank");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    DevCP da(a, mem == TGB_MEM_DEVICE);
+    if (mem == TGB_MEM_DEVICE) {
+      tgb::scale_dev(ctx, da.t, alpha, *out);
+      return;
+    }
+    DevOutCP o(out);
+    tgb::scale_dev(ctx, da.t, alpha, o.t);
+    o.finish(ctx);
   });
 }
 

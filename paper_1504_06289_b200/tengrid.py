@@ -249,8 +249,28 @@ def _h3(h) -> np.ndarray:
 # --------------------------------------------------------------------------- algebra (host, 1D complexity)
 
 
-def hadamard(a: CanonicalTensor3, b: CanonicalTensor3) -> CanonicalTensor3:
-    """tensor.cpp:141-157 (column i + Ra*j)."""
+def _cp_algebra(fn: str, a, b, rank: int, ctx, alpha: float | None = None):
+    """Device-resident CP algebra through the C-ABI (tgb_hadamard / tgb_add / tgb_scale)."""
+    ctx = ctx or default_context()
+    out = DeviceCP.empty([a.extent(ax) for ax in range(3)], rank, device=a.weight.device)
+    ca, co = a._cstruct(), out._cstruct()
+    _stream_enter(ctx)
+    if fn == "tgb_scale":
+        check(lib().tgb_scale(ctx.handle, C.byref(ca), float(alpha), C.byref(co), MEM_DEVICE))
+    else:
+        cb = b._cstruct()
+        check(getattr(lib(), fn)(ctx.handle, C.byref(ca), C.byref(cb), C.byref(co), MEM_DEVICE))
+    _stream_order(ctx, a, b, out)
+    return out
+
+
+def hadamard(a, b, ctx: "Context | None" = None):
+    """tensor.cpp:141-157 (column i + Ra*j).  Device tensors go through tgb_hadamard."""
+    if isinstance(a, DeviceCP) or isinstance(b, DeviceCP):
+        _mem(a, b)
+        if [a.extent(ax) for ax in range(3)] != [b.extent(ax) for ax in range(3)]:
+            raise InvalidArgument("hadamard: extent mismatch")
+        return _cp_algebra("tgb_hadamard", a, b, a.rank() * b.rank(), ctx)
     a.check_valid(), b.check_valid()
     if a.extents() != b.extents():
         raise InvalidArgument("hadamard: extent mismatch")
@@ -263,8 +283,13 @@ def hadamard(a: CanonicalTensor3, b: CanonicalTensor3) -> CanonicalTensor3:
     return CanonicalTensor3(f, w)
 
 
-def add(a: CanonicalTensor3, b: CanonicalTensor3) -> CanonicalTensor3:
-    """tensor.cpp:159-171 (concatenation)."""
+def add(a, b, ctx: "Context | None" = None):
+    """tensor.cpp:159-171 (concatenation).  Device tensors go through tgb_add."""
+    if isinstance(a, DeviceCP) or isinstance(b, DeviceCP):
+        _mem(a, b)
+        if [a.extent(ax) for ax in range(3)] != [b.extent(ax) for ax in range(3)]:
+            raise InvalidArgument("add: extent mismatch")
+        return _cp_algebra("tgb_add", a, b, a.rank() + b.rank(), ctx)
     a.check_valid(), b.check_valid()
     if a.extents() != b.extents():
         raise InvalidArgument("add: extent mismatch")
@@ -273,8 +298,10 @@ def add(a: CanonicalTensor3, b: CanonicalTensor3) -> CanonicalTensor3:
                             np.concatenate([a.weight, b.weight]))
 
 
-def scale(a: CanonicalTensor3, alpha: float) -> CanonicalTensor3:
-    """tensor.cpp:173-177 (weights only)."""
+def scale(a, alpha: float, ctx: "Context | None" = None):
+    """tensor.cpp:173-177 (weights only).  Device tensors go through tgb_scale."""
+    if isinstance(a, DeviceCP):
+        return _cp_algebra("tgb_scale", a, None, a.rank(), ctx, alpha)
     return CanonicalTensor3([f.copy(order="F") for f in a.factor], a.weight * alpha)
 
 

@@ -270,3 +270,27 @@ def test_pair_kernels_deterministic(ctx):
         ctx.synchronize()
         for ax in range(3):
             assert bool((c1.factor[ax] == c2.factor[ax]).all()), (n, ax)
+
+
+def test_cp_algebra_device_bitwise(ctx):
+    """tgb_hadamard / tgb_add / tgb_scale (tensor.cpp:141-177) on device tensors are
+    bit-identical to the element-wise host definitions (the reference's), with
+    column order i + R_a j and rank-0 operands."""
+    rng = Rng(5150)
+    dims = (17, 9, 23)
+    a = random_canonical(rng, dims, 3)
+    b = random_canonical(rng, dims, 4)
+    z = random_canonical(rng, dims, 0)
+    from paper_1504_06289_b200 import add, hadamard, scale
+
+    da, db, dz = DeviceCP.from_host(a), DeviceCP.from_host(b), DeviceCP.from_host(z)
+    for got, ref in ((hadamard(da, db, ctx), hadamard(a, b)), (add(da, db, ctx), add(a, b)),
+                     (scale(da, -0.37, ctx), scale(a, -0.37)), (hadamard(da, dz, ctx), hadamard(a, z)),
+                     (add(dz, db, ctx), add(z, b))):
+        h = got.to_host()
+        assert h.rank() == ref.rank()
+        assert np.array_equal(h.weight, ref.weight)
+        for ax in range(3):
+            assert np.array_equal(h.factor[ax], ref.factor[ax])
+    with pytest.raises(InvalidArgument):
+        hadamard(da, DeviceCP.from_host(random_canonical(rng, (17, 9, 22), 2)), ctx)
