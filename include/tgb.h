@@ -391,6 +391,14 @@ int tgb_dgemm(tgb_ctx* ctx, int trans_a, int trans_b, int64_t M, int64_t N, int6
  * ref is (2n) x R; offsets (host memory) come from tg::window_offset. */
 int tgb_lattice_assemble_axis(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets,
                               int64_t L, double* out, int mem);
+/* All three axes of lattice_sum_canonical (lattice.cpp:116-129) in one call:
+ * axis arrays n[3], ref[3] (2 n[ax] x R), offsets[3] (L[ax] entries, host),
+ * out[3] (n[ax] x R).  An axis whose extent, offsets and reference factor equal
+ * an earlier axis's (cubic lattice, cubic grid) gets that axis's result copied,
+ * which is bit-identical to assembling it again (host memory: the factors are
+ * compared bitwise; device memory: the same reference pointer). */
+int tgb_lattice_assemble(tgb_ctx* ctx, const int64_t* n, int64_t R, const double* const* ref,
+                         const int64_t* const* offsets, const int64_t* L, double* const* out, int mem);
 
 #ifdef __cplusplus
 }

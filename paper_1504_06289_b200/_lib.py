@@ -123,6 +123,7 @@ def lib() -> C.CDLL:
             "tgb_scale": (I, [P, C.POINTER(tgb_cp), D, C.POINTER(tgb_cp), I]),
             "tgb_coulomb_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, P, I]),
             "tgb_lattice_assemble_axis": (I, [P, I64, I64, P, P, I64, P, I]),
+            "tgb_lattice_assemble": (I, [P, P, I64, P, P, P, P, I]),
             "tgb_nuclear_potential_tensor": (I, [P, C.POINTER(tgb_cp), P, P, I64, C.POINTER(tgb_cp), I]),
             "tgb_nuclear_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, C.POINTER(tgb_cp), P, I]),
             "tgb_exchange_matrix": (I, [P, C.POINTER(tgb_cp), P, I64, P, I64, C.POINTER(tgb_cp), P, P, I]),

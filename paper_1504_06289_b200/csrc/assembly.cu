@@ -540,6 +540,31 @@ void value_at_dev(tgb_ctx* ctx, const tgb_cp& t, int64_t npts, const int64_t* ij
   TGB_LAUNCHED(ctx);
 }
 
+namespace {
+__global__ void equal_kernel(const unsigned long long* __restrict__ x, const unsigned long long* __restrict__ y,
+                             int64_t count, int* __restrict__ diff) {
+  int d = 0;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    d |= x[i] != y[i];
+  if (__syncthreads_or(d) && threadIdx.x == 0) atomicOr(diff, 1);
+}
+}  // namespace
+
+// bitwise equality of two device arrays of doubles
+bool device_equal(tgb_ctx* ctx, const double* x, const double* y, int64_t count) {
+  if (x == y || count == 0) return true;
+  auto* d = static_cast<int*>(ctx_buf(ctx, "equal.flag").get(sizeof(int)));
+  TGB_CUDA(cudaMemsetAsync(d, 0, sizeof(int), ctx->stream));
+  equal_kernel<<<static_cast<unsigned>(std::min<int64_t>((count + 255) / 256, 4 * ctx->num_sms)), 256, 0, ctx->stream>>>(
+      reinterpret_cast<const unsigned long long*>(x), reinterpret_cast<const unsigned long long*>(y), count, d);
+  TGB_LAUNCHED(ctx);
+  int h = 0;
+  TGB_CUDA(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+  TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  return h == 0;
+}
+
 void lattice_assemble_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* ref, const int64_t* offsets, int64_t L,
                           double* out) {
   if (n == 0 || R == 0) return;

@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -895,6 +896,63 @@ int tgb_lattice_assemble_axis(tgb_ctx* ctx, int64_t n, int64_t R, const double* 
     tgb::lattice_assemble_dev(ctx, n, R, dref, offsets, L, dout);
     TGB_CUDA(cudaMemcpyAsync(out, dout, n * R * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+// Three axes at once (lattice.cpp:116-129 assembles every axis).  An axis whose
+// extent, offsets and reference factor equal an earlier axis's (a cubic lattice
+// on a cubic grid: the reference factors are bitwise the same) gets that axis's
+// result copied — bit-identical to assembling it again.
+int tgb_lattice_assemble(tgb_ctx* ctx, const int64_t* n, int64_t R, const double* const* ref,
+                         const int64_t* const* offsets, const int64_t* L, double* const* out, int mem) {
+  return guarded([&] {
+    tgb::require(n && ref && offsets && L && out, "lattice_assemble: null argument");
+    for (int ax = 0; ax < 3; ++ax) {
+      tgb::require(n[ax] >= 1 && R >= 0 && L[ax] >= 0, "lattice_assemble: bad sizes");
+      for (int64_t l = 0; l < L[ax]; ++l)
+        tgb::require(offsets[ax][l] >= 0 && offsets[ax][l] + n[ax] <= 2 * n[ax],
+                     "window_offset: window escapes the doubled grid");
+    }
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    const bool dev = mem == TGB_MEM_DEVICE;
+    int same[3] = {-1, -1, -1};
+    for (int ax = 1; ax < 3; ++ax)
+      for (int p = 0; p < ax && same[ax] < 0; ++p) {
+        if (same[p] >= 0 || n[p] != n[ax] || L[p] != L[ax]) continue;
+        if (std::memcmp(offsets[p], offsets[ax], L[ax] * sizeof(int64_t)) != 0) continue;
+        // device memory: the same reference pointer (a device compare would cost a stream sync);
+        // host memory: bitwise comparison of the factors
+        bool eq = ref[p] == ref[ax];
+        if (!eq && !dev) eq = std::memcmp(ref[p], ref[ax], 2 * n[ax] * R * sizeof(double)) == 0;
+        if (eq) same[ax] = p;
+      }
+    std::array<double*, 3> dout{};
+    for (int ax = 0; ax < 3; ++ax) {
+      const int64_t nr = n[ax] * R;
+      if (dev) {
+        dout[ax] = out[ax];
+      } else {
+        dout[ax] = static_cast<double*>(tgb::ctx_buf(ctx, "lat.out" + std::to_string(ax)).get(std::max<int64_t>(1, nr) * sizeof(double)));
+      }
+      if (same[ax] >= 0) {
+        if (nr) TGB_CUDA(cudaMemcpyAsync(dout[ax], dout[same[ax]], nr * sizeof(double), cudaMemcpyDeviceToDevice,
+                                         ctx->stream));
+        continue;
+      }
+      const double* r = ref[ax];
+      if (!dev) {
+        auto* dref = static_cast<double*>(ctx->ws_in.get(std::max<int64_t>(1, 2 * nr) * sizeof(double)));
+        TGB_CUDA(cudaMemcpyAsync(dref, ref[ax], 2 * nr * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+        r = dref;
+      }
+      tgb::lattice_assemble_dev(ctx, n[ax], R, r, offsets[ax], L[ax], dout[ax]);
+    }
+    if (!dev) {
+      for (int ax = 0; ax < 3; ++ax)
+        if (n[ax] * R)
+          TGB_CUDA(cudaMemcpyAsync(out[ax], dout[ax], n[ax] * R * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    }
   });
 }
 

@@ -142,6 +142,8 @@ void comm_allreduce(tgb_ctx* ctx, double* buf, int64_t count, bool on_device);
 void symmetric_allreduce_host(const tgb_comm* c, tgb_ctx* ctx, double* J, int64_t nb);
 void shard_range(int64_t total, int rank, int world, int64_t* lo, int64_t* hi);
 void comm_release(tgb_ctx* ctx);
+// assembly.cu: bitwise equality of two device double arrays (synchronises the context stream)
+bool device_equal(tgb_ctx* ctx, const double* x, const double* y, int64_t count);
 // a named per-context workspace (replaces function-static buffers)
 inline DevBuf& ctx_buf(tgb_ctx* ctx, const std::string& name) { return ctx->named[name]; }
 inline std::array<DevBuf, 3>& ctx_buf3(tgb_ctx* ctx, const std::string& name) { return ctx->named3[name]; }

@@ -653,11 +653,18 @@ def lattice_sum_canonical(spec: LatticeSpec, grid: Grid3, reference: KernelTenso
         if spec.counts[ax] < 1:
             raise InvalidArgument("LatticeSpec: counts must be >= 1")
     out = AssembledPotential()
-    facs = []
-    for ax in range(3):
-        offs = lattice_offsets(spec, grid, ax)
-        facs.append(lattice_assemble_axis(reference.tensor.factor[ax], offs, grid.n[ax], ctx))
-        out.window_ops += len(offs)
+    ctx = ctx or default_context()
+    offs = [np.ascontiguousarray(lattice_offsets(spec, grid, ax), dtype=np.int64) for ax in range(3)]
+    R = reference.rank()
+    refs = [np.asfortranarray(reference.tensor.factor[ax], dtype=np.float64) for ax in range(3)]
+    facs = [np.zeros((grid.n[ax], R), order="F") for ax in range(3)]
+    P3 = C.c_void_p * 3
+    nn = (C.c_int64 * 3)(*grid.n)
+    LL = (C.c_int64 * 3)(*[len(o) for o in offs])
+    check(lib().tgb_lattice_assemble(ctx.handle, nn, R, P3(*[r.ctypes.data if r.size else None for r in refs]),
+                                     P3(*[o.ctypes.data if o.size else None for o in offs]), LL,
+                                     P3(*[f.ctypes.data if f.size else None for f in facs]), MEM_HOST))
+    out.window_ops = int(sum(len(o) for o in offs))
     out.canonical = CanonicalTensor3(facs, spec.charge * reference.tensor.weight)
     return out
 

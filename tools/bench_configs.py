@@ -177,18 +177,40 @@ def cfg4(ctx):
 
     from paper_1504_06289_b200._lib import MEM_DEVICE, check, lib
 
-    def run():
+    offs_c = [np.ascontiguousarray(o, dtype=np.int64) for o in offs]
+    P3 = C.c_void_p * 3
+    nn, LL = (C.c_int64 * 3)(n, n, n), (C.c_int64 * 3)(*[len(o) for o in offs_c])
+    # equal host factors -> one device copy for every axis (tgb_lattice_assemble then assembles once)
+    same = [ax == 0 or np.array_equal(ref.tensor.factor[ax], ref.tensor.factor[0]) for ax in range(3)]
+    refp = P3(*[(dref[0] if same[ax] else dref[ax]).data_ptr() for ax in range(3)])
+    offp = P3(*[o.ctypes.data for o in offs_c])
+    outp = P3(*[d.data_ptr() for d in dout])
+
+    def run():  # tgb_lattice_assemble: all three axes (the cubic case assembles one and copies)
+        check(lib().tgb_lattice_assemble(ctx.handle, nn, R, refp, offp, LL, outp, MEM_DEVICE))
+
+    def run_axes():  # one tgb_lattice_assemble_axis per axis
         for ax in range(3):
-            o = np.ascontiguousarray(offs[ax], dtype=np.int64)
-            check(lib().tgb_lattice_assemble_axis(ctx.handle, n, R, dref[ax].data_ptr(), o.ctypes.data, len(o),
-                                                  dout[ax].data_ptr(), MEM_DEVICE))
+            check(lib().tgb_lattice_assemble_axis(ctx.handle, n, R, dref[ax].data_ptr(), offs_c[ax].ctypes.data,
+                                                  len(offs_c[ax]), dout[ax].data_ptr(), MEM_DEVICE))
 
     t, _ = timed(run, reps=20, sync=torch.cuda.synchronize)
+    t_axes, _ = timed(run_axes, reps=20, sync=torch.cuda.synchronize)
+    st = torch.cuda.ExternalStream(ctx.stream)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(20):
+        run_axes()
+    e1.record(st)
+    torch.cuda.synchronize()
+    t_axes_dev = e0.elapsed_time(e1) / 20 / 1e3
     byts = 3 * 8.0 * (2 * n + n) * R
     lat = tg.DeviceCP(dout, torch.from_numpy(spec.charge * ref.tensor.weight).cuda())
     pts = torch.as_tensor(Rng(1504062894).integers(3 * 100_000, n).reshape(-1, 3)).cuda()
     tv, vals = timed(lambda: tg.value_at_points(lat, pts, ctx), reps=5, sync=torch.cuda.synchronize)
     return {"config": 4, "what": "lattice_sum_canonical L=32^3, n=32769, R_N=41 (+1e5 probes)", "assembly_ms": t * 1e3,
+            "assembly_per_axis_calls_ms": t_axes * 1e3, "assembly_per_axis_device_ms": t_axes_dev * 1e3,
             "assembly_hbm_frac": byts / t / 1e9 / HBM, "window_ops": int(sum(len(o) for o in offs)),
             "probe_ms_1e5": tv * 1e3}
 
