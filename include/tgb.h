@@ -78,6 +78,10 @@ void tgb_ctx_reset_launch_count(tgb_ctx* ctx);
  * (ms) and launch count since the last read, and resets them. */
 int tgb_ctx_set_profiling(tgb_ctx* ctx, int enabled);
 int tgb_ctx_profile_read(tgb_ctx* ctx, double* total_ms, int64_t* launches);
+/* Bytes host-memory calls moved host->device and device->host since the last
+ * read (then reset).  Bitwise-twin output blocks of tgb_convolve /
+ * tgb_hartree_potential cross PCIe once and are replicated on the host. */
+int tgb_ctx_transfer_bytes(tgb_ctx* ctx, int64_t* h2d, int64_t* d2h);
 /* Tuning / testing knob: 1D convolutions with n <= direct_max use direct
  * summation (reference: kFftConvThreshold = 128, fft.hpp:13).  Default 64;
  * 0 forces the FFT path wherever it exists. */

@@ -101,6 +101,7 @@ def lib() -> C.CDLL:
             "tgb_ctx_launch_count": (I64, [P]),
             "tgb_ctx_reset_launch_count": (None, [P]),
             "tgb_ctx_set_direct_max": (I, [P, I64]),
+            "tgb_ctx_transfer_bytes": (I, [P, C.POINTER(I64), C.POINTER(I64)]),
             "tgb_ctx_set_profiling": (I, [P, I]),
             "tgb_ctx_profile_read": (I, [P, C.POINTER(D), C.POINTER(I64)]),
             "tgb_shard_range": (I, [I64, I, I, C.POINTER(I64), C.POINTER(I64)]),

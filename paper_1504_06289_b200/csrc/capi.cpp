@@ -97,15 +97,57 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
     dout_ax[ax] = dout + ooff;
     ooff += a->n[ax] * r;
   }
+  // Bitwise-twin kernel columns (the +-t sinc nodes, kernel.cpp:194) give bitwise-equal output
+  // column blocks (i + R_a j, i < R_a): only the representative blocks cross PCIe, the twins are
+  // filled by host threads while the next axis transfers (pinned outputs; pageable outputs keep
+  // the staged whole-factor copy).
+  std::array<std::vector<int64_t>, 3> rep;
   for (int ax = 0; ax < 3; ++ax) {
+    const int64_t n = a->n[ax];
+    rep[ax].resize(rb);
+    for (int64_t j = 0; j < rb; ++j) {
+      rep[ax][j] = j;
+      for (int64_t jp = 0; jp < j; ++jp)
+        if (rep[ax][jp] == jp && std::memcmp(b->factor[ax] + n * jp, b->factor[ax] + n * j, n * sizeof(double)) == 0) {
+          rep[ax][j] = jp;
+          break;
+        }
+    }
+  }
+  bool pinned[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    pinned[ax] = !tgb::is_pageable(out->factor[ax]);
     tgb::h2d(ctx, da[ax], a->factor[ax], a->n[ax] * ra * sizeof(double), ctx->stream);
     tgb::h2d(ctx, db[ax], b->factor[ax], a->n[ax] * rb * sizeof(double), ctx->stream);
     tgb::convolve_axis(ctx, a->n[ax], ra, da[ax], rb, db[ax], h[ax], dout_ax[ax]);
     cudaEvent_t ev = ctx_event(ctx, ax);
     TGB_CUDA(cudaEventRecord(ev, ctx->stream));
     TGB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev, 0));
-    TGB_CUDA(cudaMemcpyAsync(out->factor[ax], dout_ax[ax], a->n[ax] * r * sizeof(double), cudaMemcpyDeviceToHost,
-                             ctx->copy_stream));
+    const size_t blk = static_cast<size_t>(a->n[ax]) * ra;  // doubles per kernel-column block
+    if (pinned[ax]) {  // one event per representative block: its twins are copied as soon as it lands
+      for (int64_t j = 0; j < rb; ++j)
+        if (rep[ax][j] == j) {
+          TGB_CUDA(cudaMemcpyAsync(out->factor[ax] + blk * j, dout_ax[ax] + blk * j, blk * sizeof(double),
+                                   cudaMemcpyDeviceToHost, ctx->copy_stream));
+          TGB_CUDA(cudaEventRecord(ctx_event(ctx, 3 + ax * rb + j), ctx->copy_stream));
+          ctx->bytes_d2h += static_cast<int64_t>(blk * sizeof(double));
+        }
+    }
+  }
+  for (int ax = 0; ax < 3; ++ax) {
+    const size_t blk = static_cast<size_t>(a->n[ax]) * ra;
+    if (!pinned[ax]) {  // staged copy of the whole factor (pageable destination)
+      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+      tgb::d2h(ctx, out->factor[ax], dout_ax[ax], blk * rb * sizeof(double), ctx->copy_stream);
+      continue;
+    }
+    for (int64_t j = 0; j < rb; ++j) {
+      if (rep[ax][j] != j) continue;
+      TGB_CUDA(cudaEventSynchronize(ctx_event(ctx, 3 + ax * rb + j)));
+      for (int64_t jt = j + 1; jt < rb; ++jt)
+        if (rep[ax][jt] == j)
+          tgb::par_memcpy(out->factor[ax] + blk * jt, out->factor[ax] + blk * j, blk * sizeof(double));
+    }
   }
   TGB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   TGB_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -278,6 +320,15 @@ int tgb_ctx_profile_read(tgb_ctx* ctx, double* total_ms, int64_t* launches) {
     *total_ms = tot;
     *launches = static_cast<int64_t>(ctx->prof_used);
     ctx->prof_used = 0;
+  });
+}
+
+int tgb_ctx_transfer_bytes(tgb_ctx* ctx, int64_t* h2d, int64_t* d2h) {
+  return guarded([&] {
+    tgb::require(ctx && h2d && d2h, "ctx_transfer_bytes: null argument");
+    *h2d = ctx->bytes_h2d;
+    *d2h = ctx->bytes_d2h;
+    ctx->bytes_h2d = ctx->bytes_d2h = 0;
   });
 }
 

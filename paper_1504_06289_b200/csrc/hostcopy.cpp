@@ -9,6 +9,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <cstdint>
+#include <mutex>
 #include <cstring>
 #include <thread>
 #include <vector>
@@ -22,6 +25,8 @@ namespace {
 constexpr size_t kChunk = 64u << 20;  // bytes per staging chunk
 constexpr size_t kDirect = 8u << 20;  // below this the driver's pageable path is fine
 
+}  // namespace
+
 bool is_pageable(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -31,22 +36,89 @@ bool is_pageable(const void* p) {
   return a.type == cudaMemoryTypeUnregistered;
 }
 
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const size_t nt = std::min<size_t>({static_cast<size_t>(hw), 8, std::max<size_t>(1, bytes >> 22)});
-  if (nt <= 1) {
-    std::memcpy(dst, src, bytes);
-    return;
+// A persistent pool of host copy threads (spawning threads per call cost more than the
+// copies when the output's twin blocks are replicated block by block).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool pool;
+    return pool;
   }
-  std::vector<std::thread> th;
-  const size_t part = (bytes + nt - 1) / nt;
-  for (size_t t = 0; t < nt; ++t) {
-    const size_t b0 = t * part, b1 = std::min(bytes, b0 + part);
-    if (b0 >= b1) break;
-    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b0, static_cast<const char*>(src) + b0, b1 - b0); });
+  void copy(void* dst, const void* src, size_t bytes) {
+    const size_t nt = std::min<size_t>(workers_.size() + 1, std::max<size_t>(1, bytes >> 22));
+    if (nt <= 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    std::lock_guard<std::mutex> call(call_mu_);  // one parallel copy at a time
+    const size_t part = (bytes + nt - 1) / nt;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      bytes_ = bytes;
+      part_ = part;
+      nparts_ = nt;
+      next_ = 1;  // part 0 is the caller's
+      done_ = 0;
+      ++gen_;
+    }
+    cv_.notify_all();
+    run_part(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return done_ == nparts_ - 1; });
   }
-  for (auto& x : th) x.join();
-}
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned n = std::min(hw, 16u) - 1;
+    for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void run_part(size_t p) {
+    const size_t b0 = p * part_, b1 = std::min(bytes_, b0 + part_);
+    if (b0 < b1) std::memcpy(dst_ + b0, src_ + b0, b1 - b0);
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      size_t p;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || (gen_ != seen && next_ < nparts_); });
+        if (stop_) return;
+        p = next_++;
+        if (next_ >= nparts_) seen = gen_;
+      }
+      run_part(p);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        ++done_;
+      }
+      done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, call_mu_;
+  std::condition_variable cv_, done_cv_;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0, part_ = 0, nparts_ = 0, next_ = 0, done_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
+void par_memcpy(void* dst, const void* src, size_t bytes) { CopyPool::get().copy(dst, src, bytes); }
+
+namespace {
 
 void ensure_stage(tgb_ctx* ctx) {
   for (int i = 0; i < 2; ++i) {
@@ -59,6 +131,7 @@ void ensure_stage(tgb_ctx* ctx) {
 
 void h2d(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t stream) {
   if (!bytes) return;
+  ctx->bytes_h2d += static_cast<int64_t>(bytes);
   if (bytes < kDirect || !is_pageable(src)) {
     TGB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream));
     return;
@@ -77,6 +150,7 @@ void h2d(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st
 
 void d2h(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t stream) {
   if (!bytes) return;
+  ctx->bytes_d2h += static_cast<int64_t>(bytes);
   if (bytes < kDirect || !is_pageable(dst)) {
     TGB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream));
     TGB_CUDA(cudaStreamSynchronize(stream));

@@ -80,6 +80,8 @@ void* scratch_alloc(tgb_ctx* ctx, size_t bytes, size_t* got);
 // host <-> device copies; pageable host memory is staged through pinned chunks (hostcopy.cpp)
 void h2d(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t stream);
 void d2h(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t stream);
+bool is_pageable(const void* p);
+void par_memcpy(void* dst, const void* src, size_t bytes);  // host threads
 void scratch_free(tgb_ctx* ctx, void* p, size_t bytes);
 
 // Run f, mapping exceptions to the C-ABI return codes (tgb.h).
@@ -134,6 +136,8 @@ struct tgb_ctx {
   bool own_nccl = false;
   tgb_comm user_comm{};
   int comm_rank = 0, comm_size = 1;
+  // bytes moved between host and device by host-memory calls (tgb_ctx_transfer_bytes)
+  int64_t bytes_h2d = 0, bytes_d2h = 0;
 };
 
 namespace tgb {

@@ -54,6 +54,12 @@ class Context:
     def set_direct_max(self, n: int) -> None:
         check(lib().tgb_ctx_set_direct_max(self._h, n))
 
+    def transfer_bytes(self) -> tuple[int, int]:
+        """(H2D, D2H) bytes moved by host-memory calls since the last read (tgb_ctx_transfer_bytes)."""
+        h, d = C.c_int64(), C.c_int64()
+        check(lib().tgb_ctx_transfer_bytes(self._h, C.byref(h), C.byref(d)))
+        return h.value, d.value
+
     def set_profiling(self, enabled: bool) -> None:
         check(lib().tgb_ctx_set_profiling(self._h, int(enabled)))
 

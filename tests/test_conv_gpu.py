@@ -294,3 +294,25 @@ def test_cp_algebra_device_bitwise(ctx):
             assert np.array_equal(h.factor[ax], ref.factor[ax])
     with pytest.raises(InvalidArgument):
         hadamard(da, DeviceCP.from_host(random_canonical(rng, (17, 9, 22), 2)), ctx)
+
+
+def test_host_path_pinned_twin_replication(ctx):
+    """Host-memory hartree_potential into PINNED output buffers: only the
+    representative kernel-column blocks cross PCIe (twins replicated on the
+    host, tgb_ctx_transfer_bytes counts it) and the result is bit-identical to
+    the pageable path's whole-factor copy."""
+    import torch
+
+    case = hartree_case(0, n=1025, rank=12)
+    ra, rb = case.theta.rank(), case.kernel.rank()
+    ref = hartree_potential(case.theta, case.kernel, case.grid.h, ctx)  # pageable output
+    oh = CanonicalTensor3([torch.empty((ra * rb, 1025), dtype=torch.float64).pin_memory().numpy().T
+                           for _ in range(3)], np.zeros(ra * rb))
+    ctx.transfer_bytes()
+    hartree_potential(case.theta, case.kernel, case.grid.h, ctx, out=oh)
+    h2d, d2h = ctx.transfer_bytes()
+    distinct = len({case.kernel.tensor.factor[0][:, j].tobytes() for j in range(rb)})
+    assert d2h == 3 * 1025 * ra * distinct * 8 < 3 * 1025 * ra * rb * 8
+    for ax in range(3):
+        assert np.array_equal(oh.factor[ax], ref.factor[ax])
+    assert np.array_equal(oh.weight, ref.weight)
