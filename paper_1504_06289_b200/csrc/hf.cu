@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cstring>
 #include <vector>
 
@@ -333,10 +334,13 @@ void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_of
   // <g_c, g_c' * p> = <g_c', g_c * p>: only the blocks k <= m of K are formed and the
   // other triangle is their mirror (the reference forms both and averages, hf.cpp:169).
   bool sym_kernel = RN > 0 && !getenv("TGB_EXCHANGE_FULL");
-  for (int ax = 0; ax < 3 && sym_kernel; ++ax) {
+  std::array<std::vector<double>, 3> kfh;
+  for (int ax = 0; ax < 3; ++ax) {
     const int64_t n = kernel.n[ax];
-    std::vector<double> kf(n * RN);
-    TGB_CUDA(cudaMemcpy(kf.data(), kernel.factor[ax], kf.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    kfh[ax].resize(n * RN);
+    if (n * RN)
+      TGB_CUDA(cudaMemcpy(kfh[ax].data(), kernel.factor[ax], kfh[ax].size() * sizeof(double), cudaMemcpyDeviceToHost));
+    const std::vector<double>& kf = kfh[ax];
     for (int64_t q = 0; q < RN && sym_kernel; ++q)
       for (int64_t i = 0; i < n / 2; ++i)
         if (kf[i + n * q] != kf[n - 1 - i + n * q]) {
@@ -344,7 +348,45 @@ void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_of
           break;
         }
   }
-  for (int64_t a = 0; a < nocc && RN > 0; ++a) {
+  // Bitwise-twin kernel columns (the +-t sinc nodes, kernel.cpp:194) produce identical convolved
+  // columns, and K is linear in the kernel's weighted columns: convolve with the distinct columns
+  // only, each weighted by the sum of its twins' weights (config-1 basis: 41 -> 21 columns, the
+  // GEMM rows halve).
+  std::vector<int64_t> reps;
+  std::vector<double> wrep;
+  for (int64_t q = 0; q < RN; ++q) {
+    int64_t r = -1;
+    for (size_t i = 0; i < reps.size() && r < 0; ++i) {
+      bool eq = true;
+      for (int ax = 0; ax < 3 && eq; ++ax) {
+        const int64_t n = kernel.n[ax];
+        eq = std::memcmp(kfh[ax].data() + n * reps[i], kfh[ax].data() + n * q, n * sizeof(double)) == 0;
+      }
+      if (eq) r = static_cast<int64_t>(i);
+    }
+    if (r < 0 || getenv("TGB_EXCHANGE_NO_DEDUP")) {
+      reps.push_back(q);
+      wrep.push_back(wk[q]);
+    } else {
+      wrep[r] += wk[q];
+    }
+  }
+  const int64_t RD = static_cast<int64_t>(reps.size());
+  Scratch skd(ctx, (kernel.n[0] + kernel.n[1] + kernel.n[2]) * std::max<int64_t>(RD, 1));
+  const double* kfd[3];
+  {
+    int64_t off = 0;
+    for (int ax = 0; ax < 3; ++ax) {
+      double* dst = skd.p + off * RD;
+      for (int64_t i = 0; i < RD; ++i)
+        TGB_CUDA(cudaMemcpyAsync(dst + kernel.n[ax] * i, kernel.factor[ax] + kernel.n[ax] * reps[i],
+                                 kernel.n[ax] * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+      kfd[ax] = dst;
+      off += kernel.n[ax];
+    }
+  }
+  wk = wrep;
+  for (int64_t a = 0; a < nocc && RD > 0; ++a) {
     // phi_a = sum_k c_ka G_k (orbital_tensor, hf.cpp:39-46): columns = primitives of G_k, c_k != 0
     std::vector<int> phic;
     std::vector<double> wphi;
@@ -372,48 +414,47 @@ void exchange_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_of
           gi[c] = static_cast<int>(fn_offset[m] + i);
           gj[c] = phic[j];
           wg[c] = wprim[fn_offset[m] + i] * wphi[j];
-          cmap[c] = RN * c0[m] + (c - c0[m]);  // v_m columns [RN c0[m], RN c0[m+1]), local col + s_m q
+          cmap[c] = RD * c0[m] + (c - c0[m]);  // v_m columns [RD c0[m], RD c0[m+1]), local col + s_m q
           cmap[G + c] = npm * rphi;
         }
     }
     c0[nb] = G;
-    std::vector<double> wy(G * RN);  // weights of the convolved columns: w_g * (w_q / h^3)
+    std::vector<double> wy(G * RD);  // weights of the convolved columns: w_g * (w_q / h^3)
     for (int64_t c = 0; c < G; ++c)
-      for (int64_t q = 0; q < RN; ++q) wy[cmap[c] + cmap[G + c] * q] = wg[c] * (wk[q] * inv_vol);
-    Scratch sgi(ctx, (G + 1) / 2), sgj(ctx, (G + 1) / 2), smap(ctx, 2 * G), swy(ctx, G * RN);
+      for (int64_t q = 0; q < RD; ++q) wy[cmap[c] + cmap[G + c] * q] = wg[c] * (wk[q] * inv_vol);
+    Scratch sgi(ctx, (G + 1) / 2), sgj(ctx, (G + 1) / 2), smap(ctx, 2 * G), swy(ctx, G * RD);
     const int* dgi = upload(ctx, sgi, gi);
     const int* dgj = upload(ctx, sgj, gj);
     const int64_t* dmap = upload(ctx, smap, cmap);
     const double* dwy = upload(ctx, swy, wy);
     Scratch sgp(ctx, (basis.n[0] + basis.n[1] + basis.n[2]) * G);
-    Scratch sy(ctx, (basis.n[0] + basis.n[1] + basis.n[2]) * G * RN);
+    Scratch sy(ctx, (basis.n[0] + basis.n[1] + basis.n[2]) * G * RD);
     double *gp[3], *y[3];
     int64_t off = 0;
     for (int ax = 0; ax < 3; ++ax) {
       gp[ax] = sgp.p + off * G;
-      y[ax] = sy.p + off * G * RN;
+      y[ax] = sy.p + off * G * RD;
       off += basis.n[ax];
       hadamard_pairs_kernel<<<col_grid(basis.n[ax], G), 256, 0, ctx->stream>>>(basis.n[ax], basis.factor[ax], dgi,
                                                                                dgj, G, gp[ax]);
       TGB_LAUNCHED(ctx);
     }
     const double* gpc[3] = {gp[0], gp[1], gp[2]};
-    const double* kf[3] = {kernel.factor[0], kernel.factor[1], kernel.factor[2]};
-    convolve_axes(ctx, 3, basis.n, G, gpc, RN, kf, h, y, dmap);
+    convolve_axes(ctx, 3, basis.n, G, gpc, RD, kfd, h, y, dmap);
     // groups of consecutive blocks m -> one GEMM per axis + the segmented reduction
     // symmetric kernel: small groups keep the GEMM width c0[m1] (blocks k <= m) tight
-    const int64_t row_cap = sym_kernel ? std::max<int64_t>(2048, RN * (c0[nb] / std::max<int64_t>(nb, 1)) * 4)
+    const int64_t row_cap = sym_kernel ? std::max<int64_t>(2048, RD * (c0[nb] / std::max<int64_t>(nb, 1)) * 4)
                                        : std::max<int64_t>(8192, (int64_t(1) << 26) / std::max<int64_t>(G, 1));
     std::vector<double> s_all(nb * G);
     int64_t m0 = 0;
     while (m0 < nb) {
       int64_t m1 = m0 + 1;
-      while (m1 < nb && RN * (c0[m1 + 1] - c0[m0]) <= row_cap) ++m1;
-      const int64_t r0 = RN * c0[m0], rows = RN * (c0[m1] - c0[m0]);
+      while (m1 < nb && RD * (c0[m1 + 1] - c0[m0]) <= row_cap) ++m1;
+      const int64_t r0 = RD * c0[m0], rows = RD * (c0[m1] - c0[m0]);
       const int64_t Gc = sym_kernel ? c0[m1] : G;  // left columns needed: blocks k <= m (symmetric) or all
       Scratch st(ctx, 3 * rows * Gc), sseg(ctx, m1 - m0 + 1), ss(ctx, (m1 - m0) * Gc);
       std::vector<int64_t> seg(m1 - m0 + 1);
-      for (int64_t m = m0; m <= m1; ++m) seg[m - m0] = RN * c0[m] - r0;
+      for (int64_t m = m0; m <= m1; ++m) seg[m - m0] = RD * c0[m] - r0;
       const int64_t* dseg = upload(ctx, sseg, seg);
       double* T[3];
       // the three axis GEMMs are independent: axis 2 runs on the aux stream so its wave tail
