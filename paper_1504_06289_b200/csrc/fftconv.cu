@@ -559,6 +559,47 @@ __device__ __forceinline__ void stage_product(double2* sm, int N, const double2*
   }
 }
 
+// Static-size staging: all ceil((N+1)/TT) loads of A and B in flight at once,
+// the Nyquist product included (slot pidx(N)).
+template <int N, int TT, bool BREAL>
+__device__ __forceinline__ void stage_product_static(double2* sm, const double2* __restrict__ A,
+                                                     const void* __restrict__ Bv) {
+  constexpr int K = (N + 1 + TT - 1) / TT;
+  constexpr bool kWhole = (N + 1) % TT == 0;
+  double2 a[K];
+  if constexpr (BREAL) {
+    double b[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int pos = threadIdx.x + k * TT;
+      if (kWhole || pos <= N) {
+        a[k] = ld2(A + pos);
+        b[k] = __ldg(static_cast<const double*>(Bv) + pos);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int pos = threadIdx.x + k * TT;
+      if (kWhole || pos <= N) sm[pidx(pos)] = cscale(a[k], b[k]);
+    }
+  } else {
+    double2 b[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int pos = threadIdx.x + k * TT;
+      if (kWhole || pos <= N) {
+        a[k] = ld2(A + pos);
+        b[k] = ld2(static_cast<const double2*>(Bv) + pos);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int pos = threadIdx.x + k * TT;
+      if (kWhole || pos <= N) sm[pidx(pos)] = cmul(a[k], b[k]);
+    }
+  }
+}
+
 // First inverse pass on the staged product: real split, radix-R butterflies
 // on the paired blocks g (frequencies kk + s N/R) and g2 (the mirrors N - k),
 // in place in shared memory.  Twiddles w_m^{kk} from the two-level table.
@@ -584,16 +625,19 @@ __device__ __forceinline__ void scale_block(double2* v, const void* __restrict__
   }
 }
 
-template <int R, bool MULB = false, bool BREAL = true>
-__device__ __forceinline__ void first_item(double2* sm, const double2* tws, const PlanArgs& pa,
-                                           const double2* __restrict__ A, const void* __restrict__ B, bool breal,
-                                           int q) {
+// LOWREG: the regular (g, g2) case keeps only block g in registers — the
+// split halves of block g2 go back to its own shared-memory slots and are
+// reloaded for its butterfly (same arithmetic, half the live registers).
+// NYQ: the Nyquist product P[N] is already staged at shared slot pidx(N).
+template <int R, bool MULB = false, bool BREAL = true, bool LOWREG = false, bool NYQ = false>
+__device__ __forceinline__ void first_item_gg(double2* sm, const double2* tws, const PlanArgs& pa,
+                                              const double2* __restrict__ A, const void* __restrict__ B, bool breal,
+                                              int4 gg) {
   const int N = pa.N;
   const double2* cs = tws + pa.off_cs;
   const double2* zlo = tws + pa.off_zlo;
   const double2* zhi = tws + pa.off_zhi;
   {
-    const int4 gg = __ldg(pa.leader + q);
     const int g = gg.x, g2 = gg.y;
     double2 a[R];
 #pragma unroll
@@ -601,9 +645,14 @@ __device__ __forceinline__ void first_item(double2* sm, const double2* tws, cons
     scale_block<R, MULB, BREAL>(a, B, g * R);
     if (g == 0) {
       // natural frequencies s*N/R; mirror of s is R-s (s = 0 mirrors to the Nyquist term N)
-      const double2 an = MULB ? sm[pidx(N)] : ld2(A + N);
-      const double2 pn = breal ? cscale(an, __ldg(static_cast<const double*>(B) + N))
-                               : cmul(an, ld2(static_cast<const double2*>(B) + N));
+      double2 pn;
+      if constexpr (NYQ) {
+        pn = sm[pidx(N)];
+      } else {
+        const double2 an = MULB ? sm[pidx(N)] : ld2(A + N);
+        pn = breal ? cscale(an, __ldg(static_cast<const double*>(B) + N))
+                   : cmul(an, ld2(static_cast<const double2*>(B) + N));
+      }
       const double2 z0 = zsplit(a[0], pn, make_double2(1.0, 0.0));
 #pragma unroll
       for (int s = 1; 2 * s <= R; ++s) {
@@ -636,6 +685,23 @@ __device__ __forceinline__ void first_item(double2* sm, const double2* tws, cons
       dft<R, 1>(a);
 #pragma unroll
       for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
+    } else if constexpr (LOWREG && !MULB) {
+      const double2 wk = cmul(zlo[gg.z & 63], zhi[gg.z >> 6]);
+#pragma unroll
+      for (int s = 0; s < R; ++s) {
+        double2 za, zb;
+        zsplit_pair(a[s], sm[pidx(g2 * R + R - 1 - s)], cmul(wk, cs[s]), za, zb);
+        a[s] = za;
+        sm[pidx(g2 * R + R - 1 - s)] = zb;
+      }
+      dft<R, 1>(a);
+#pragma unroll
+      for (int s = 0; s < R; ++s) sm[pidx(g * R + s)] = a[s];
+#pragma unroll
+      for (int s = 0; s < R; ++s) a[s] = sm[pidx(g2 * R + s)];
+      dft<R, 1>(a);
+#pragma unroll
+      for (int s = 0; s < R; ++s) sm[pidx(g2 * R + s)] = a[s];
     } else {
       const double2 wk = cmul(zlo[gg.z & 63], zhi[gg.z >> 6]);
       double2 b[R];
@@ -660,11 +726,19 @@ __device__ __forceinline__ void first_item(double2* sm, const double2* tws, cons
   }
 }
 
-template <int R, bool MULB = false, bool BREAL = true>
+template <int R, bool MULB = false, bool BREAL = true, bool LOWREG = false>
+__device__ __forceinline__ void first_item(double2* sm, const double2* tws, const PlanArgs& pa,
+                                           const double2* __restrict__ A, const void* __restrict__ B, bool breal,
+                                           int q) {
+  first_item_gg<R, MULB, BREAL, LOWREG>(sm, tws, pa, A, B, breal, __ldg(pa.leader + q));
+}
+
+template <int R, bool MULB = false, bool BREAL = true, bool LOWREG = false>
 __device__ __forceinline__ void first_pass_inv(double2* sm, const double2* tws, const PlanArgs& pa,
                                                const double2* __restrict__ A, const void* __restrict__ B,
                                                bool breal) {
-  for (int q = threadIdx.x; q < pa.npl; q += blockDim.x) first_item<R, MULB, BREAL>(sm, tws, pa, A, B, breal, q);
+  for (int q = threadIdx.x; q < pa.npl; q += blockDim.x)
+    first_item<R, MULB, BREAL, LOWREG>(sm, tws, pa, A, B, breal, q);
 }
 
 // First pass with TT threads when TT < npl <= 2 TT: one full round, then the
@@ -993,7 +1067,8 @@ __device__ __forceinline__ void static_last(const double2* sm, const double2* lo
   }
 }
 
-template <int R0, int R1, int R2, int R3, int TT, bool BREAL>
+// R3 == 1: a three-pass plan (R0, R1, R2).
+template <int R0, int R1, int R2, int R3, int TT, bool BREAL, bool HALF = false>
 __device__ __forceinline__ void pair_body_static(const PlanArgs& pa, const double2* __restrict__ specA,
                                                  const void* __restrict__ specB, const PairEntry* __restrict__ work,
                                                  int nwork, double* __restrict__ out) {
@@ -1003,39 +1078,94 @@ __device__ __forceinline__ void pair_body_static(const PlanArgs& pa, const doubl
   const double2* tws = load_tables(sm, pa);
   const int nz = (pa.n + 1) >> 1;
   const bool odd_n = pa.n & 1;
+  // this thread's first-pass item (the same for every pair of the launch).  HALF:
+  // threads 2u, 2u+1 share regular block pair u (one block each), then one
+  // thread per single (self-mirror) block — the pass-0 critical path halves
+  const int nreg = pa.npl - pa.nsp;
+  const int tid = threadIdx.x;
+  const int lq = !HALF ? tid : (tid < 2 * nreg ? tid >> 1 : tid - nreg);
+  const int4 lead = lq < pa.npl && (!HALF || tid < 2 * nreg + pa.nsp) ? __ldg(pa.leader + lq) : make_int4(0, 0, 0, 0);
+  PairEntry nxt;
+  if (static_cast<int>(blockIdx.x) < nwork) nxt = work[blockIdx.x];
   for (int w = blockIdx.x; w < nwork; w += gridDim.x) {
-    const PairEntry e = work[w];
+    const PairEntry e = nxt;
+    if (w + static_cast<int>(gridDim.x) < nwork) nxt = work[w + gridDim.x];  // next entry in flight
     const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
     const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
                           : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
     long long t0 = pa.phase ? clock64() : 0;
-    stage_product<BREAL>(sm, N, a, b);
+    __syncthreads();  // the previous pair's last pass has read shared memory
+    stage_product_static<N, TT, BREAL>(sm, a, b);
     __syncthreads();
     long long t1 = pa.phase ? clock64() : 0;
-    first_pass_inv<R0>(sm, tws, pa, a, b, BREAL);
+    if constexpr (HALF) {
+      const unsigned halfmask = __ballot_sync(0xffffffffu, tid < 2 * nreg);
+      if (tid < 2 * nreg) {
+        const int h = tid & 1;
+        const int gx = h ? lead.y : lead.x, gy = h ? lead.x : lead.y, kx = h ? lead.w : lead.z;
+        const double2* cs = tws + pa.off_cs;
+        const double2 wk = cmul(tws[pa.off_zlo + (kx & 63)], tws[pa.off_zhi + (kx >> 6)]);
+        double2 x[R0];
+#pragma unroll
+        for (int q = 0; q < R0; ++q)
+          x[q] = zsplit(sm[pidx(gx * R0 + q)], sm[pidx(gy * R0 + R0 - 1 - q)], cmul(wk, cs[q]));
+        dft<R0, 1>(x);
+        __syncwarp(halfmask);  // the partner lane has read this block too
+#pragma unroll
+        for (int q = 0; q < R0; ++q) sm[pidx(gx * R0 + q)] = x[q];
+      } else if (tid < 2 * nreg + pa.nsp) {
+        first_item_gg<R0, false, BREAL, true, true>(sm, tws, pa, a, b, BREAL, lead);
+      }
+    } else {
+      if (tid < pa.npl) first_item_gg<R0, false, BREAL, true, true>(sm, tws, pa, a, b, BREAL, lead);
+      for (int q = tid + TT; q < pa.npl; q += TT)
+        first_item_gg<R0, false, BREAL, true, true>(sm, tws, pa, a, b, BREAL, __ldg(pa.leader + q));
+    }
     __syncthreads();
     long long t2 = pa.phase ? clock64() : 0;
-    static_pass<R1, L1, N, 1>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
+    static_pass_t<R1, L1, N, 1, TT>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
     __syncthreads();
     long long t3 = pa.phase ? clock64() : 0;
-    static_pass<R2, L2, N, 1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
-    __syncthreads();
-    long long t4 = pa.phase ? clock64() : 0;
     double* o0 = out + e.out0;
     double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
-    static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
-    __syncthreads();
-    if (pa.phase && threadIdx.x == 0) {
-      const long long t5 = clock64();
-      atomicAdd(pa.phase + 0, static_cast<unsigned long long>(t1 - t0));
-      atomicAdd(pa.phase + 1, static_cast<unsigned long long>(t2 - t1));
-      atomicAdd(pa.phase + 2, static_cast<unsigned long long>(t3 - t2));
-      atomicAdd(pa.phase + 3, static_cast<unsigned long long>(t4 - t3));
-      atomicAdd(pa.phase + 4, static_cast<unsigned long long>(t5 - t4));
-      atomicAdd(pa.phase + 5, 1ULL);
+    if constexpr (R3 > 1) {
+      static_pass_t<R2, L2, N, 1, TT>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+      __syncthreads();
+      static_last<R3, L3, N>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3], nz, odd_n, o0, o1, aligned);
+    } else {
+      static_last<R2, L2, N>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2], nz, odd_n, o0, o1, aligned);
+    }
+    long long t4 = t3;
+    if (pa.phase) {
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const long long t5 = clock64();
+        atomicAdd(pa.phase + 0, static_cast<unsigned long long>(t1 - t0));
+        atomicAdd(pa.phase + 1, static_cast<unsigned long long>(t2 - t1));
+        atomicAdd(pa.phase + 2, static_cast<unsigned long long>(t3 - t2));
+        atomicAdd(pa.phase + 3, static_cast<unsigned long long>(t4 - t3));
+        atomicAdd(pa.phase + 4, static_cast<unsigned long long>(t5 - t4));
+        atomicAdd(pa.phase + 5, 1ULL);
+      }
     }
   }
+}
+
+// Small compile-time plans: one launch covers every axis (blockIdx.y) and both
+// kernel-spectrum forms (the device-side symmetry flag picks one per axis).
+template <int R0, int R1, int R2, int R3, int TT, int MINB>
+__global__ void __launch_bounds__(TT, MINB)
+    pair_kernel_small(const __grid_constant__ PlanArgs pa, const __grid_constant__ PairAxes pr,
+                      const __grid_constant__ PairAxes pc) {
+  const int axis = blockIdx.y;
+  const int* winfo = pr.winfo[axis];
+  if (winfo[1])
+    pair_body_static<R0, R1, R2, R3, TT, true, true>(pa, pr.specA[axis], pr.specB[axis], pr.work[axis], winfo[0],
+                                                     pr.out[axis]);
+  else
+    pair_body_static<R0, R1, R2, R3, TT, false, true>(pa, pc.specA[axis], pc.specB[axis], pc.work[axis], winfo[0],
+                                                      pc.out[axis]);
 }
 
 // Launched once per form of the kernel-column spectra; the instance whose
@@ -1189,34 +1319,40 @@ __global__ void __launch_bounds__(TT, 1)
 // from per-plan tables instead of sincospi.
 template <int R0, int R1, int R2, int R3, int TT>
 __global__ void __launch_bounds__(TT, 1)
-    spectrum_kernel_static(PlanArgs pa, const double* __restrict__ XA, int nA, void* __restrict__ specA,
-                           const double* __restrict__ XB, const int* __restrict__ colidx, int nB,
-                           void* __restrict__ specB, void* __restrict__ specB2, int modeB, int64_t ldx, double h) {
+    spectrum_kernel_static(PlanArgs pa, SpecAxes sx, int nA, const int* __restrict__ colidx, int nB, int modeB,
+                           int64_t ldx) {
   constexpr int N = R0 * R1 * R2 * R3;
   constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
   extern __shared__ double2 sm[];
   const double2* tws = load_tables(sm, pa);
+  const int axis = blockIdx.y;
   const bool isA = static_cast<int>(blockIdx.x) >= nB;  // kernel columns first (they carry the extra work)
   const int c = isA ? blockIdx.x - nB : blockIdx.x;
   const int mode = isA ? 0 : modeB;
-  const double* x = isA ? XA + c * ldx : XB + (colidx ? colidx[c] : c) * ldx;
+  const double* x = isA ? sx.XA[axis] + c * ldx : sx.XB[axis] + (colidx ? colidx[c] : c) * ldx;
+  void* __restrict__ specA = sx.specA[axis];
+  void* __restrict__ specB = sx.specB[axis];
+  void* __restrict__ specB2 = sx.specB2[axis];
+  const double h = sx.h[axis];
   const int n = pa.n;
   long long c0 = pa.phase ? clock64() : 0;
   constexpr int UB = 8;  // loads in flight per thread (20 measured no faster)
-  static_assert(N % (UB * TT) == 0, "whole batches");
+  constexpr bool kWhole = N % (UB * TT) == 0;
 #pragma unroll 1
   for (int k0 = threadIdx.x; k0 < N; k0 += UB * TT) {
     double2 v[UB];
     int p[UB];
 #pragma unroll
     for (int u = 0; u < UB; ++u) {
-      const int i0 = 2 * (k0 + u * TT);
+      const int k = k0 + u * TT;
+      const int i0 = 2 * k;
       v[u].x = i0 < n ? __ldg(x + i0) : 0.0;
       v[u].y = i0 + 1 < n ? __ldg(x + i0 + 1) : 0.0;
-      p[u] = __ldg(pa.inv + k0 + u * TT);
+      p[u] = (kWhole || k < N) ? __ldg(pa.inv + k) : -1;
     }
 #pragma unroll
-    for (int u = 0; u < UB; ++u) sm[pidx(p[u])] = v[u];
+    for (int u = 0; u < UB; ++u)
+      if (kWhole || p[u] >= 0) sm[pidx(p[u])] = v[u];
   }
   __syncthreads();
   long long c1 = pa.phase ? clock64() : 0;
@@ -1224,9 +1360,13 @@ __global__ void __launch_bounds__(TT, 1)
   __syncthreads();
   static_pass_t<R1, L1, N, -1, TT>(sm, tws + pa.off_lo[1], tws + pa.off_hi[1]);
   __syncthreads();
-  static_pass_t<R2, L2, N, -1, TT>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
-  __syncthreads();
-  static_pass<R3, L3, N, -1>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3]);
+  if constexpr (R3 > 1) {
+    static_pass_t<R2, L2, N, -1, TT>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+    __syncthreads();
+    static_pass<R3, L3, N, -1>(sm, tws + pa.off_lo[3], tws + pa.off_hi[3]);
+  } else {
+    static_pass<R2, L2, N, -1>(sm, tws + pa.off_lo[2], tws + pa.off_hi[2]);
+  }
   __syncthreads();
   long long c2 = pa.phase ? clock64() : 0;
   const double hm = h / pa.m;
@@ -1237,7 +1377,7 @@ __global__ void __launch_bounds__(TT, 1)
   const int* order = pa.fused ? pa.kf : pa.perm;
   const double2* zlo = tws + pa.off_zlo;
   const double2* zhi2 = tws + pa.off_zhi2;
-  static_assert(N % (8 * TT) == 0, "whole batches");
+  constexpr bool kWholeP = N % (8 * TT) == 0;
   auto post = [&](int pos, int k) {
     const int kk = k == N ? 0 : k;
     const double2 zk = sm[pidx(kk)];
@@ -1266,9 +1406,10 @@ __global__ void __launch_bounds__(TT, 1)
   for (int p0 = threadIdx.x; p0 < N; p0 += 8 * TT) {
     int kb[8];
 #pragma unroll
-    for (int u = 0; u < 8; ++u) kb[u] = __ldg(order + p0 + u * TT);
+    for (int u = 0; u < 8; ++u) kb[u] = (kWholeP || p0 + u * TT < N) ? __ldg(order + p0 + u * TT) : -1;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) post(p0 + u * TT, kb[u]);
+    for (int u = 0; u < 8; ++u)
+      if (kWholeP || kb[u] >= 0) post(p0 + u * TT, kb[u]);
   }
   if (threadIdx.x == 0) post(N, N);
   if (pa.phase) {
@@ -1463,95 +1604,187 @@ __global__ void direct_conv_kernel(int n, int ofs, int even, const double* __res
   }
 }
 
-// flags[j * rb + j2] = 1 iff columns j and j2 (j < j2) of B are bitwise equal;
-// flags[j * rb + j] = 1 iff column j is mirror-symmetric (b[i] == b[n-1-i]).
-struct ColAxes {  // per-axis operands of the grouping kernels (blockIdx.y = axis)
+// Kernel-column grouping and the pair work lists, all axes, three short
+// launches on the aux stream (they overlap the spectra):
+//  (1) per (column, chunk of kChunk elements): an order-dependent 64-bit hash
+//      (sum of mixed words, combined with atomicAdd) and the mirror-symmetry
+//      flag (b[i] == b[n-1-i], atomicAnd);
+//  (2) per (column, chunk): the candidate representative = the smallest
+//      earlier column with the same hash; the chunk is compared bitwise and a
+//      mismatch (a hash collision) marks the column;
+//  (3) every CTA: representatives in shared memory (a marked column re-searches
+//      with full bitwise verification), group ranks / sizes / partners by warp
+//      ballots, then its share of the i-major work list: for each density
+//      column i, one entry per pair of identical kernel columns (the entry's
+//      result is stored to both).  winfo = {entries, all columns symmetric}.
+// Bitwise identity is an equivalence, so rep[j] = the smallest identical
+// j' <= j names the group; groups are ordered by representative.
+struct ColAxes {  // per-axis operands (blockIdx.y-free: the grid strides over axis x column)
   const double* B[3];
   int64_t n[3];
-  unsigned char* flags[3];
+  unsigned long long* sig;  // naxes * rb hashes (zeroed before the launch)
+  int* asym;                // naxes * rb: column not mirror-symmetric (zeroed)
+  int* rep;                 // naxes * rb candidate representatives
+  int* bad;                 // naxes * rb: candidate failed verification (zeroed)
   PairEntry* work[3];
   int* winfo[3];
 };
 
-__global__ void dup_columns_kernel(ColAxes ca, int rb) {
-  const double* __restrict__ B = ca.B[blockIdx.y];
-  const int64_t n = ca.n[blockIdx.y];
-  unsigned char* flags = ca.flags[blockIdx.y];
-  const int p = blockIdx.x;
-  int j, j2;
-  if (p < rb) {
-    j = j2 = p;
-  } else {
-    int rem = p - rb;
-    j = 0;
-    while (rem >= rb - 1 - j) {
-      rem -= rb - 1 - j;
-      ++j;
-    }
-    j2 = j + 1 + rem;
-  }
-  const unsigned long long* x = reinterpret_cast<const unsigned long long*>(B + j * n);
-  const unsigned long long* y = reinterpret_cast<const unsigned long long*>(B + j2 * n);
-  int same = 1;
-  if (j == j2) {
-    for (int64_t i = threadIdx.x; i < n / 2; i += blockDim.x) same &= (x[i] == x[n - 1 - i]);
-  } else {
-    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) same &= (x[i] == y[i]);
-  }
-  same = __syncthreads_and(same);
-  if (threadIdx.x == 0) flags[j * rb + j2] = static_cast<unsigned char>(same);
+constexpr int kChunk = 1024;  // elements of one column per warp item in phases (1)-(2)
+
+__device__ __forceinline__ unsigned long long mix64c(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
 }
 
-// Device-side grouping of the kernel columns (per axis) from the
-// dup/symmetry flags, and the i-major pair work list: for each density
-// column i, one entry per pair of identical kernel columns (the entry's
-// result is stored to both).  winfo = {entries, all columns symmetric}.
-__global__ void build_work_kernel(ColAxes ca, int rb, int64_t ra, int flags_in_smem, const int64_t* __restrict__ cmap) {
-  const unsigned char* __restrict__ f = ca.flags[blockIdx.y];
-  const int64_t n = ca.n[blockIdx.y];
-  PairEntry* __restrict__ w = ca.work[blockIdx.y];
-  int* __restrict__ winfo = ca.winfo[blockIdx.y];
-  // Grouping in parallel (bitwise identity is an equivalence): rep[j] = the
-  // smallest j' <= j identical to j; a member's rank in its group = the number
-  // of earlier members; groups are ordered by representative.  Every CTA
-  // repeats this O(rb^2 / threads) step and writes its share of the density
-  // columns i.
-  extern __shared__ int wsh[];  // rep[rb], rank[rb], goff[rb] (pair offset of group rep j), then flags
-  int* rep = wsh;
-  int* rnk = rep + rb;
-  int* goff = rnk + rb;
-  unsigned char* fs = reinterpret_cast<unsigned char*>(goff + rb);
-  __shared__ int s_np, s_sym;
-  if (flags_in_smem) {
-    for (int i = threadIdx.x; i < rb * rb; i += blockDim.x) fs[i] = f[i];
-    __syncthreads();
-    f = fs;
+// Position-salted word hash, summed over a column (one 64-bit multiply per
+// word; the sums are mixed once at the end).  Only a filter: every match is
+// verified bitwise.
+__device__ __forceinline__ unsigned long long col_word_hash(unsigned long long v, int64_t i) {
+  return (v ^ (static_cast<unsigned long long>(i) * 0x9E3779B97F4A7C15ull)) * 0xD6E8FEB86659FD93ull;
+}
+
+__device__ __forceinline__ bool cols_equal_warp(const unsigned long long* x, const unsigned long long* y, int64_t n,
+                                                int lane) {
+  int same = 1;
+  for (int64_t i0 = lane; i0 < n; i0 += 32 * 8) {  // 16 loads in flight per lane
+    unsigned long long p[8], q[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t i = i0 + 32 * u;
+      p[u] = i < n ? x[i] : 0;
+      q[u] = i < n ? y[i] : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) same &= p[u] == q[u];
   }
-  if (threadIdx.x == 0) s_sym = 1;
-  __syncthreads();
-  for (int j = threadIdx.x; j < rb; j += blockDim.x) {
+  return __all_sync(0xffffffffu, same);
+}
+
+struct ColItems {  // (column, chunk) items of phases (1)-(2), all axes
+  int64_t nch[3] = {0, 0, 0};
+  int64_t items = 0;
+  __device__ ColItems(const ColAxes& ca, int naxes, int rb) {
+    for (int ax = 0; ax < naxes; ++ax) {
+      nch[ax] = (ca.n[ax] + kChunk - 1) / kChunk;
+      items += nch[ax] * rb;
+    }
+  }
+  __device__ void decode(const ColAxes& ca, int rb, int64_t it, int& ax, int& j, int64_t& lo, int64_t& hi) const {
+    ax = 0;
+    while (it >= nch[ax] * rb) it -= nch[ax++] * rb;
+    j = static_cast<int>(it / nch[ax]);
+    lo = (it % nch[ax]) * kChunk;
+    hi = min(lo + kChunk, ca.n[ax]);
+  }
+};
+
+__global__ void __launch_bounds__(256) col_hash_kernel(const __grid_constant__ ColAxes ca, int naxes, int rb, int weak) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * nw + warp, GW = static_cast<int64_t>(gridDim.x) * nw;
+  const ColItems ci(ca, naxes, rb);
+  // (1) hashes and mirror symmetry
+  for (int64_t it = gw; it < ci.items; it += GW) {
+    int ax, j;
+    int64_t lo, hi;
+    ci.decode(ca, rb, it, ax, j, lo, hi);
+    const int64_t n = ca.n[ax];
+    const auto* x = reinterpret_cast<const unsigned long long*>(ca.B[ax] + j * n);
+    unsigned long long h = 0;
+    int sym = 1;
+    for (int64_t i0 = lo + lane; i0 < hi; i0 += 32 * 8) {  // 16 loads in flight per lane
+      unsigned long long v[8], m[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = i0 + 32 * u;
+        v[u] = i < hi ? x[i] : 0;
+        m[u] = i < hi && i < n / 2 ? x[n - 1 - i] : v[u];
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t i = i0 + 32 * u;
+        if (i < hi) h += col_word_hash(v[u], i);
+        sym &= v[u] == m[u];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    sym = __all_sync(0xffffffffu, sym);
+    if (lane == 0) {
+      atomicAdd(ca.sig + ax * rb + j, weak ? 0ull : mix64c(h));
+      if (!sym) atomicOr(ca.asym + ax * rb + j, 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) col_verify_kernel(const __grid_constant__ ColAxes ca, int naxes, int rb) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t gw = static_cast<int64_t>(blockIdx.x) * nw + warp, GW = static_cast<int64_t>(gridDim.x) * nw;
+  const ColItems ci(ca, naxes, rb);
+  // (2) candidate representative by hash, verified chunk by chunk
+  for (int64_t it = gw; it < ci.items; it += GW) {
+    int ax, j;
+    int64_t lo, hi;
+    ci.decode(ca, rb, it, ax, j, lo, hi);
+    const unsigned long long* sg = ca.sig + ax * rb;
+    const unsigned long long sj = sg[j];
     int r = j;
-    for (int jp = 0; jp < j; ++jp)
-      if (f[jp * rb + j]) {
-        r = jp;
-        break;
+    for (int c0 = 0; c0 < j && r == j; c0 += 32) {
+      const unsigned m = __ballot_sync(0xffffffffu, c0 + lane < j && sg[c0 + lane] == sj);
+      if (m) r = c0 + __ffs(m) - 1;
+    }
+    if (lo == 0 && lane == 0) ca.rep[ax * rb + j] = r;
+    if (r != j) {
+      const int64_t n = ca.n[ax];
+      const auto* x = reinterpret_cast<const unsigned long long*>(ca.B[ax] + j * n);
+      const auto* y = reinterpret_cast<const unsigned long long*>(ca.B[ax] + r * n);
+      int same = 1;
+      for (int64_t i0 = lo + lane; i0 < hi; i0 += 32 * 8) {
+        unsigned long long p[8], q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int64_t i = i0 + 32 * u;
+          p[u] = i < hi ? x[i] : 0;
+          q[u] = i < hi ? y[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) same &= p[u] == q[u];
       }
-    rep[j] = r;
-    if (!f[j * rb + j]) atomicAnd(&s_sym, 0);
+      if (!__all_sync(0xffffffffu, same) && lane == 0) atomicOr(ca.bad + ax * rb + j, 1);
+    }
+  }
+}
+
+// (3) for one axis, from the representatives in shared memory: group ranks,
+// sizes and partners by warp ballots, the pair offsets of the groups, and the
+// work-list rows [i0, i1).  `rep`, `rnk`, `goff`, `part`: rb ints of shared
+// memory each; rep[] is final on entry.
+__device__ void groups_and_work(const ColAxes& ca, int ax, int rb, int64_t ra, const int64_t* __restrict__ cmap,
+                                int* rep, int* rnk, int* goff, int* part, int sym, int64_t i0, int64_t i1,
+                                bool write_info) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ int s_np;
+  for (int j = warp; j < rb; j += nw) {
+    const int r = rep[j];
+    int k = 0, size = 0, partner = -1;
+    for (int c0 = 0; c0 < rb; c0 += 32) {
+      const int jp = c0 + lane;
+      const unsigned m = __ballot_sync(0xffffffffu, jp < rb && rep[jp] == r);
+      const unsigned below = j >= c0 + 32 ? 0xffffffffu : (j <= c0 ? 0u : ((1u << (j - c0)) - 1u));
+      const unsigned above = ~below & ~(j >= c0 && j < c0 + 32 ? (1u << (j - c0)) : 0u);
+      size += __popc(m);
+      k += __popc(m & below);
+      if (partner < 0 && (m & above)) partner = c0 + __ffs(m & above) - 1;
+    }
+    if (lane == 0) {
+      rnk[j] = k;
+      goff[j] = (size + 1) / 2;  // pairs of this group (read at the representative)
+      part[j] = partner;
+    }
   }
   __syncthreads();
-  for (int j = threadIdx.x; j < rb; j += blockDim.x) {
-    int k = 0, size = 0;
-    for (int jp = 0; jp < rb; ++jp)
-      if (rep[jp] == rep[j]) {
-        k += jp < j;
-        ++size;
-      }
-    rnk[j] = k;
-    goff[j] = (size + 1) / 2;  // pairs of this group (read at the representative)
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {  // exclusive prefix over representatives in index order (rb steps)
+  if (threadIdx.x == 0) {  // exclusive prefix over representatives in index order
     int acc = 0;
     for (int j = 0; j < rb; ++j)
       if (rep[j] == j) {
@@ -1560,35 +1793,153 @@ __global__ void build_work_kernel(ColAxes ca, int rb, int64_t ra, int flags_in_s
         acc += c;
       }
     s_np = acc;
-    if (blockIdx.x == 0) {
-      winfo[0] = static_cast<int>(ra * acc);
-      winfo[1] = s_sym;
+    if (write_info) {
+      ca.winfo[ax][0] = static_cast<int>(ra * acc);
+      ca.winfo[ax][1] = sym;
     }
   }
   __syncthreads();
   const int np = s_np;
-  const int64_t i0 = ra * blockIdx.x / gridDim.x, i1 = ra * (blockIdx.x + 1) / gridDim.x;
-  for (int j = threadIdx.x; j < rb; j += blockDim.x) {  // j = the member stored to out0 of its pair
+  const int64_t n = ca.n[ax];
+  PairEntry* __restrict__ w = ca.work[ax];
+  // one thread per (row, pair member j stored to out0)
+  const int64_t tot = (i1 - i0) * rb;
+  for (int64_t t = threadIdx.x; t < tot; t += blockDim.x) {
+    const int j = static_cast<int>(t % rb);
+    const int64_t i = i0 + t / rb;
     if (rnk[j] & 1) continue;
     const int r = rep[j];
-    const int slot = goff[r] + rnk[j] / 2;
-    int partner = -1;  // next member of the group
-    for (int jp = j + 1; jp < rb; ++jp)
-      if (rep[jp] == r) {
-        partner = jp;
-        break;
-      }
-    for (int64_t i = i0; i < i1; ++i) {
-      PairEntry e;
-      e.ia = static_cast<int>(i);
-      e.jb = r;
-      // output column i + ra j, or base[i] + stride[i] j under a column map
-      const int64_t cb = cmap ? cmap[i] : i, cs = cmap ? cmap[ra + i] : ra;
-      e.out0 = (cb + cs * j) * n;
-      e.out1 = partner >= 0 ? (cb + cs * partner) * n : -1;
-      w[i * np + slot] = e;
+    const int partner = part[j];  // the next member of the group
+    PairEntry e;
+    e.ia = static_cast<int>(i);
+    e.jb = r;
+    // output column i + ra j, or base[i] + stride[i] j under a column map
+    const int64_t cb = cmap ? cmap[i] : i, cs = cmap ? cmap[ra + i] : ra;
+    e.out0 = (cb + cs * j) * n;
+    e.out1 = partner >= 0 ? (cb + cs * partner) * n : -1;
+    w[i * np + goff[r] + rnk[j] / 2] = e;
+  }
+}
+
+// A hash collision left column j's candidate unverified: search again with full
+// bitwise comparison, ascending, so rep is the smallest identical earlier column.
+__device__ int rep_search_warp(const ColAxes& ca, int ax, int rb, int j, const unsigned long long* sig, int lane) {
+  const int64_t n = ca.n[ax];
+  const auto* x = reinterpret_cast<const unsigned long long*>(ca.B[ax] + j * n);
+  for (int jp = 0; jp < j; ++jp)
+    if (sig[jp] == sig[j] &&
+        cols_equal_warp(reinterpret_cast<const unsigned long long*>(ca.B[ax] + jp * n), x, n, lane))
+      return jp;
+  return j;
+}
+
+// (3) over the grid: blockIdx.y = axis; every CTA rebuilds the axis' grouping
+// from the verified representatives and writes its rows of the work list.
+__global__ void __launch_bounds__(256) col_work_kernel(const __grid_constant__ ColAxes ca, int rb, int64_t ra,
+                                                       const int64_t* __restrict__ cmap) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ax = blockIdx.y;
+  extern __shared__ int wsh[];  // rep, rank, goff, partner (rb each), then the hashes (rb u64)
+  int* rep = wsh;
+  int* rnk = rep + rb;
+  int* goff = rnk + rb;
+  int* part = goff + rb;
+  auto* sg = reinterpret_cast<unsigned long long*>(part + rb);  // 16 rb bytes in: 8-byte aligned
+  int sym = 1, anybad = 0;
+  for (int j = threadIdx.x; j < rb; j += blockDim.x) {  // one parallel sweep of the per-column results
+    rep[j] = ca.rep[ax * rb + j];
+    rnk[j] = ca.bad[ax * rb + j];
+    sg[j] = ca.sig[ax * rb + j];
+    sym &= !ca.asym[ax * rb + j];
+    anybad |= rnk[j];
+  }
+  sym = __syncthreads_and(sym);
+  if (__syncthreads_or(anybad)) {
+    for (int j = warp; j < rb; j += nw) {
+      if (!rnk[j]) continue;
+      const int r = rep_search_warp(ca, ax, rb, j, sg, lane);
+      if (lane == 0) rep[j] = r;
+    }
+    __syncthreads();
+  }
+  const int64_t i0 = ra * blockIdx.x / gridDim.x, i1 = ra * (blockIdx.x + 1) / gridDim.x;
+  groups_and_work(ca, ax, rb, ra, cmap, rep, rnk, goff, part, sym, i0, i1, blockIdx.x == 0);
+}
+
+// Small problems (rb * n <= kColCtaMax): ONE launch.  The grid (blockIdx.y =
+// axis) hashes (column, chunk) items as col_hash_kernel does; the last CTA to
+// finish an axis (threadfence + ticket) verifies the candidates, groups the
+// columns and writes that axis' whole work list.
+constexpr int64_t kColCtaMax = 1 << 17;
+constexpr int kSmallChunk = 256;  // elements per warp item: one batch of loads per lane
+
+__global__ void __launch_bounds__(256) col_groups_small_kernel(const __grid_constant__ ColAxes ca, int rb, int64_t ra,
+                                                               const int64_t* __restrict__ cmap, int weak,
+                                                               unsigned* __restrict__ ticket) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int ax = blockIdx.y;
+  const int64_t n = ca.n[ax];
+  const int64_t nch = (n + kSmallChunk - 1) / kSmallChunk;
+  for (int64_t it = static_cast<int64_t>(blockIdx.x) * nw + warp; it < nch * rb; it += static_cast<int64_t>(gridDim.x) * nw) {
+    const int j = static_cast<int>(it / nch);
+    const int64_t lo = (it % nch) * kSmallChunk, hi = min(lo + kSmallChunk, n);
+    const auto* x = reinterpret_cast<const unsigned long long*>(ca.B[ax] + j * n);
+    unsigned long long v[kSmallChunk / 32], m[kSmallChunk / 32];
+#pragma unroll
+    for (int u = 0; u < kSmallChunk / 32; ++u) {
+      const int64_t i = lo + lane + 32 * u;
+      v[u] = i < hi ? x[i] : 0;
+      m[u] = i < hi && i < n / 2 ? x[n - 1 - i] : v[u];
+    }
+    unsigned long long h = 0;
+    int sym = 1;
+#pragma unroll
+    for (int u = 0; u < kSmallChunk / 32; ++u) {
+      const int64_t i = lo + lane + 32 * u;
+      if (i < hi) h += col_word_hash(v[u], i);
+      sym &= v[u] == m[u];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    sym = __all_sync(0xffffffffu, sym);
+    if (lane == 0) {
+      atomicAdd(ca.sig + ax * rb + j, weak ? 0ull : mix64c(h));
+      if (!sym) atomicOr(ca.asym + ax * rb + j, 1);
     }
   }
+  // the last CTA of this axis carries on
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket + ax, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  extern __shared__ int wsh[];
+  int* rep = wsh;
+  int* rnk = rep + rb;
+  int* goff = rnk + rb;
+  int* part = goff + rb;
+  auto* sg = reinterpret_cast<unsigned long long*>(part + rb);  // 16 rb bytes in: 8-byte aligned
+  int sym = 1;
+  for (int j = threadIdx.x; j < rb; j += blockDim.x) {
+    sg[j] = __ldcg(ca.sig + ax * rb + j);  // L2: written by other CTAs of this launch
+    sym &= !__ldcg(ca.asym + ax * rb + j);
+  }
+  sym = __syncthreads_and(sym);
+  for (int j = warp; j < rb; j += nw) {  // representatives: smallest identical earlier column
+    int r = j;
+    for (int c0 = 0; c0 < j && r == j; c0 += 32) {
+      const unsigned m = __ballot_sync(0xffffffffu, c0 + lane < j && sg[c0 + lane] == sg[j]);
+      if (m) r = c0 + __ffs(m) - 1;
+    }
+    if (r != j && !cols_equal_warp(reinterpret_cast<const unsigned long long*>(ca.B[ax] + r * n),
+                                   reinterpret_cast<const unsigned long long*>(ca.B[ax] + j * n), n, lane))
+      r = rep_search_warp(ca, ax, rb, j, sg, lane);
+    if (lane == 0) rep[j] = r;
+  }
+  __syncthreads();
+  groups_and_work(ca, ax, rb, ra, cmap, rep, rnk, goff, part, sym, 0, ra, true);
 }
 
 __global__ void weights_outer_kernel(int64_t ra, const double* __restrict__ wa, int64_t rb,
@@ -1789,8 +2140,15 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
       attr2[ctx->device] = true;
     }
-    spectrum_kernel_static<16, 10, 10, 8, 320><<<nA + nB, 320, pl.smem, ctx->stream>>>(
-        pl.a, A, nA, specA, B, colidx, nB, specB, specB2, modeB, ldx, h);
+    SpecAxes sx{};
+    sx.XA[0] = A;
+    sx.specA[0] = specA;
+    sx.XB[0] = B;
+    sx.specB[0] = specB;
+    sx.specB2[0] = specB2;
+    sx.h[0] = h;
+    spectrum_kernel_static<16, 10, 10, 8, 320><<<nA + nB, 320, pl.smem, ctx->stream>>>(pl.a, sx, nA, colidx, nB,
+                                                                                        modeB, ldx);
     TGB_LAUNCHED(ctx);
     if (a.phase) {
       unsigned long long hb[16];
@@ -1811,6 +2169,61 @@ static void launch_spectrum(tgb_ctx* ctx, const ConvPlan& pl, const double* A, i
   sx.specB2[0] = specB2;
   sx.h[0] = h;
   launch_spectrum_axes(ctx, pl, sx, 1, nA, colidx, nB, modeB, ldx);
+}
+
+// Compile-time small plan (config 0: n = 1025 -> N = 16*10*5): the spectra of
+// every axis in one launch, then every axis' pairs in ONE launch that also
+// picks the kernel-spectrum form on the device.  The
+// runtime-generic kernels carry every radix (8k SASS instructions, 168
+// registers, a stack for the per-pass tables) and ran these sizes at a few %
+// of the HBM bound.
+template <int R0, int R1, int R2, int R3, int TT, int MINB, int STT>
+static bool try_small(tgb_ctx* ctx, const ConvPlan& pl, const SpecAxes& sx, const PairAxes& pr, const PairAxes& pc,
+                      int naxes, int nA, int nB, int64_t ldx) {
+  const PlanArgs& a = pl.a;
+  constexpr int P = R3 > 1 ? 4 : 3;
+  if (a.P != P || a.r[0] != R0 || a.r[1] != R1 || a.r[2] != R2 || (P == 4 && a.r[3] != R3) || a.fused ||
+      2 * (a.npl - a.nsp) + a.nsp > TT || getenv("TGB_NO_SMALL"))
+    return false;
+  auto pk = pair_kernel_small<R0, R1, R2, R3, TT, MINB>;
+  auto sk = spectrum_kernel_static<R0, R1, R2, R3, STT>;
+  static bool attr[kTgbMaxDevices] = {};
+  static int per_sm[kTgbMaxDevices] = {};
+  if (!attr[ctx->device]) {
+    TGB_CUDA(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+    TGB_CUDA(cudaFuncSetAttribute(sk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ctx->smem_optin)));
+    attr[ctx->device] = true;
+  }
+  sk<<<dim3(nA + nB, naxes), STT, pl.smem, ctx->stream>>>(pl.a, sx, nA, nullptr, nB, 3, ldx);
+  TGB_LAUNCHED(ctx);
+  TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
+  if (!per_sm[ctx->device]) TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ctx->device], pk, TT, pl.smem));
+  const int grid = std::max(1, std::max(1, per_sm[ctx->device]) * ctx->num_sms / naxes);
+  prof_begin(ctx);
+  pk<<<dim3(grid, naxes), TT, pl.smem, ctx->stream>>>(pl.a, pr, pc);
+  TGB_LAUNCHED(ctx);
+  prof_end(ctx);
+  if (a.phase) {  // analysis only (TGB_PHASE_CLK): cycles per pair by phase, summed over CTAs
+    unsigned long long hb[8];
+    TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+    TGB_CUDA(cudaMemcpy(hb, a.phase, sizeof(hb), cudaMemcpyDeviceToHost));
+    const double np = static_cast<double>(hb[5] ? hb[5] : 1);
+    fprintf(stderr, "small pair cycles/pair: stage %.0f pass0 %.0f pass1 %.0f last %.0f (pairs %llu)\n", hb[0] / np,
+            hb[1] / np, hb[2] / np, hb[4] / np, hb[5]);
+    TGB_CUDA(cudaMemset(a.phase, 0, sizeof(hb)));
+  }
+  return true;
+}
+
+static bool small_plan(const ConvPlan& pl) {
+  const PlanArgs& a = pl.a;
+  return a.P == 3 && !a.fused && a.r[0] == 16 && a.r[1] == 10 && a.r[2] == 5 && !getenv("TGB_NO_SMALL");
+}
+
+// (n = 2049 -> 16*10*10 measured slower here than the generic kernels: 2.93 vs 2.79 ms for config 1's V_H)
+static bool launch_small(tgb_ctx* ctx, const ConvPlan& pl, const SpecAxes& sx, const PairAxes& pr,
+                         const PairAxes& pc, int naxes, int nA, int nB, int64_t ldx) {
+  return try_small<16, 10, 5, 1, 160, 3, 160>(ctx, pl, sx, pr, pc, naxes, nA, nB, ldx);
 }
 
 // config-2 plan (fftconv12k.cu)
@@ -1837,45 +2250,80 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
   if (ra == 0 || rb == 0 || naxes == 0) return;
   std::vector<std::shared_ptr<ConvPlan>> plans(naxes);
   for (int ax = 0; ax < naxes; ++ax) plans[ax] = get_plan(ctx, n[ax]);
-  // ---- aux stream: flags -> groups -> work lists
-  const int64_t nblocks = rb + rb * (rb - 1) / 2;
-  const size_t fbytes = (static_cast<size_t>(naxes * rb * rb) + 255) & ~size_t(255);
+  // ---- aux stream: hashes -> verified representatives -> groups and work lists
+  const size_t cbytes = (static_cast<size_t>(naxes * rb) * (sizeof(unsigned long long) + 3 * sizeof(int)) + 16 + 255) &
+                        ~size_t(255);
   const size_t wentries = static_cast<size_t>(ra * rb);
-  char* wsp = static_cast<char*>(
-      ctx->ws_pairs.get(fbytes + naxes * (wentries * sizeof(PairEntry) + 256) + 256));
-  auto* flags = reinterpret_cast<unsigned char*>(wsp);
-  auto* winfo = reinterpret_cast<int*>(wsp + fbytes);  // 2 ints per axis
-  char* wlist = wsp + fbytes + 256;
+  char* wsp = static_cast<char*>(ctx->ws_pairs.get(cbytes + naxes * (wentries * sizeof(PairEntry) + 256) + 256));
+  auto* sig = reinterpret_cast<unsigned long long*>(wsp);
+  auto* asym = reinterpret_cast<int*>(sig + naxes * rb);
+  auto* bad = asym + naxes * rb;
+  auto* ticket = reinterpret_cast<unsigned*>(bad + naxes * rb);  // 4 per-axis counters
+  auto* rep = bad + naxes * rb + 4;
+  const size_t zbytes = static_cast<size_t>(naxes * rb) * (sizeof(unsigned long long) + 2 * sizeof(int)) + 16;
+  auto* winfo = reinterpret_cast<int*>(wsp + cbytes);  // 2 ints per axis
+  char* wlist = wsp + cbytes + 256;
   TGB_CUDA(cudaEventRecord(ctx->aux_in, ctx->stream));  // B is ready in stream order
   TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
-  size_t wsmem = static_cast<size_t>(3 * rb) * sizeof(int);
-  if (wsmem > 48 * 1024) throw Error(TGB_INVALID_ARGUMENT, "convolve: kernel rank too large for the work builder");
-  const int flags_in_smem = wsmem + static_cast<size_t>(rb * rb) <= 48 * 1024;
-  if (flags_in_smem) wsmem += static_cast<size_t>(rb * rb);
+  const size_t wsmem = static_cast<size_t>(4 * rb) * sizeof(int) + static_cast<size_t>(rb) * 8;
+  if (wsmem + 1024 > ctx->smem_optin)
+    throw Error(TGB_INVALID_ARGUMENT, "convolve: kernel rank too large for the work builder");
   std::vector<PairEntry*> dwork(naxes);
   ColAxes ca{};
+  ca.sig = sig;
+  ca.asym = asym;
+  ca.bad = bad;
+  ca.rep = rep;
   for (int ax = 0; ax < naxes; ++ax) {
     dwork[ax] = reinterpret_cast<PairEntry*>(wlist + ax * (wentries * sizeof(PairEntry) + 256));
     ca.B[ax] = B[ax];
     ca.n[ax] = n[ax];
-    ca.flags[ax] = flags + ax * rb * rb;
     ca.work[ax] = dwork[ax];
     ca.winfo[ax] = winfo + 2 * ax;
   }
-  // every axis in one launch each (grid.y = axis)
-  dup_columns_kernel<<<dim3(static_cast<unsigned>(nblocks), naxes), 256, 0, ctx->aux_stream>>>(ca, static_cast<int>(rb));
-  TGB_LAUNCHED(ctx);
-  const unsigned wblocks = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(ra / 4, 2 * ctx->num_sms)));
-  build_work_kernel<<<dim3(wblocks, naxes), 128, wsmem, ctx->aux_stream>>>(ca, static_cast<int>(rb), ra,
-                                                                          flags_in_smem, colmap);
-  TGB_LAUNCHED(ctx);
+  {
+    int64_t maxcol = 0, items = 0;
+    for (int ax = 0; ax < naxes; ++ax) {
+      maxcol = std::max(maxcol, n[ax]);
+      items += rb * ((n[ax] + kChunk - 1) / kChunk);
+    }
+    const int irb = static_cast<int>(rb);
+    // test hook: every hash 0, so every candidate goes through the collision path
+    const int weak = getenv("TGB_COLHASH_WEAK") ? 1 : 0;
+    static size_t attr_smem[2][kTgbMaxDevices] = {};
+    const bool one_cta = rb * maxcol <= kColCtaMax;
+    const void* fn = one_cta ? reinterpret_cast<const void*>(col_groups_small_kernel)
+                             : reinterpret_cast<const void*>(col_work_kernel);
+    if (wsmem > 48 * 1024 && wsmem > attr_smem[one_cta][ctx->device]) {
+      TGB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsmem)));
+      attr_smem[one_cta][ctx->device] = wsmem;
+    }
+    if (one_cta) {
+      TGB_CUDA(cudaMemsetAsync(sig, 0, zbytes, ctx->aux_stream));
+      const int64_t per_axis = rb * ((maxcol + kSmallChunk - 1) / kSmallChunk);
+      const unsigned gs = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((per_axis + 7) / 8, ctx->num_sms)));
+      col_groups_small_kernel<<<dim3(gs, naxes), 256, wsmem, ctx->aux_stream>>>(ca, irb, ra, colmap, weak, ticket);
+      TGB_LAUNCHED(ctx);
+    } else {
+      TGB_CUDA(cudaMemsetAsync(sig, 0, zbytes, ctx->aux_stream));
+      const unsigned gi = static_cast<unsigned>(std::min<int64_t>((items + 7) / 8, 4 * ctx->num_sms));
+      col_hash_kernel<<<gi, 256, 0, ctx->aux_stream>>>(ca, naxes, irb, weak);
+      TGB_LAUNCHED(ctx);
+      col_verify_kernel<<<gi, 256, 0, ctx->aux_stream>>>(ca, naxes, irb);
+      TGB_LAUNCHED(ctx);
+      const unsigned gw = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((ra + 15) / 16, ctx->num_sms)));
+      col_work_kernel<<<dim3(gw, naxes), 256, wsmem, ctx->aux_stream>>>(ca, irb, ra, colmap);
+      TGB_LAUNCHED(ctx);
+    }
+  }
   TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
   // ---- main stream: spectra (independent of the grouping), then the pairs
   bool joined = false;
   bool same_n = true;
   for (int ax = 1; ax < naxes; ++ax) same_n = same_n && n[ax] == n[0];
   const ConvPlan& p0 = *plans[0];
-  if (naxes > 1 && same_n && !p0.direct && !k12_applicable(n[0], p0.a.N) && !static_plan(p0)) {
+  if ((naxes > 1 || small_plan(p0)) && same_n && !p0.direct && !k12_applicable(n[0], p0.a.N) && !static_plan(p0) &&
+      !(n[0] > ctx->direct_max && kS_split(n[0]))) {
     // every axis shares one generic plan: one spectrum launch and one pair launch per
     // spectrum form for all axes (config 0 is launch-bound: 16 -> 6 launches)
     const size_t N1 = static_cast<size_t>(p0.a.N) + 1;
@@ -1901,6 +2349,7 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
       pr.winfo[ax] = pc.winfo[ax] = winfo + 2 * ax;
       pr.out[ax] = pc.out[ax] = out[ax];
     }
+    if (launch_small(ctx, p0, sx, pr, pc, naxes, static_cast<int>(ra), static_cast<int>(rb), n[0])) return;
     launch_spectrum_axes(ctx, p0, sx, naxes, static_cast<int>(ra), nullptr, static_cast<int>(rb), 3, n[0]);
     TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
     launch_pair_generic<true>(ctx, p0, pr, naxes);

@@ -316,3 +316,39 @@ def test_host_path_pinned_twin_replication(ctx):
     for ax in range(3):
         assert np.array_equal(oh.factor[ax], ref.factor[ax])
     assert np.array_equal(oh.weight, ref.weight)
+
+
+def _grouping_case(rng, n, sym):
+    """Kernel-side tensor whose columns form groups of bitwise-identical columns
+    {1, 5, 7}, {2, 6} and singletons (optionally all mirror-symmetric)."""
+    rb, ra = 9, 3
+    fac = []
+    for _ in range(3):
+        f = rng.normal(n * rb).reshape(n, rb, order="F")
+        if sym:
+            f = 0.5 * (f + f[::-1])
+        f[:, 5] = f[:, 1]
+        f[:, 7] = f[:, 1]
+        f[:, 6] = f[:, 2]
+        fac.append(np.asfortranarray(f))
+    b = CanonicalTensor3(fac, rng.uniform(rb) + 0.5)
+    a = random_canonical(rng, (n, n, n), ra)
+    return a, b
+
+
+@pytest.mark.parametrize("n", [257, 16385])  # one-CTA grouping (rb*n small) / hash + verify + work kernels
+@pytest.mark.parametrize("sym", [True, False])
+@pytest.mark.parametrize("weak", [False, True])  # weak: every hash collides -> the verified re-search path
+def test_kernel_column_grouping_paths(ctx, monkeypatch, n, sym, weak):
+    if weak:
+        monkeypatch.setenv("TGB_COLHASH_WEAK", "1")
+    rng = Rng(424242 + n + 2 * sym)
+    a, b = _grouping_case(rng, n, sym)
+    h = (0.3, 0.25, 0.2)
+    c = convolve(a, b, h, ctx)
+    oc = O.convolve(O.OCP.from_cp(a), O.OCP.from_cp(b), h)
+    ra = a.rank()
+    for ax in range(3):
+        assert relmax(c.factor[ax], oc.factors()[ax]) <= TOL
+        blk = lambda j: c.factor[ax][:, j * ra:(j + 1) * ra]  # noqa: E731
+        assert np.array_equal(blk(1), blk(5)) and np.array_equal(blk(1), blk(7)) and np.array_equal(blk(2), blk(6))
