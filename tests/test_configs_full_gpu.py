@@ -13,12 +13,11 @@ reference's own code computed (tools/make_golden_configs.py on oracle/_ref).
   the fit basis is the QR of a pivoted Cholesky factor stopped at a 1e-12
   trace residual, conditioned ~1e6.
 * config 1 (density_tensor -> V_H -> J, n=2049, N_b=40): Tucker and canonical
-  ranks identical.  The reduced density is an eps = 1e-6 approximation whose
-  factors two correct implementations choose differently (the reference's Gram
-  branch vs the device subspace iteration, both within eps of Theta; DESIGN.md
-  §2), so V_H and J are compared at the accuracy the reduction defines
-  (<= 10 eps relative); the J assembly itself is pinned at 1e-10 on the
-  reference's own fixture (test_hf_gpu.py::test_coulomb_matrix_vs_reference_binary)."""
+  ranks identical; V_H at 10^4 seeded points and J within 1e-10 (measured
+  3.4e-13 and 2.9e-13).  The reduced factors themselves are not compared: the
+  reference's Gram branch and the device subspace iteration pick different
+  bases of the same truncated subspaces, and the reduced TENSOR
+  is what V_H and J see."""
 import hashlib
 from pathlib import Path
 
@@ -117,5 +116,5 @@ def test_config1_density_vh_j_full(ctx):
     J = tg.coulomb_matrix(bs, disc, vh, ctx)
     ej = relmax(J, g["J"])
     print(f"config 1: V_H samples rel err {ev:.3e}, J rel err {ej:.3e}")
-    assert ev <= 1e-5 and ej <= 1e-5
+    assert ev <= 1e-10 and ej <= 1e-10
     assert np.array_equal(J, J.T)
