@@ -340,7 +340,9 @@ int tgb_tei_get_cholesky(tgb_tei* t, double* L, int64_t* pivots, int mem); /* nb
  * max_sweeps.  The result (TuckerResult) stays on the device; read it with
  * tgb_tucker_info / _get / _sigma, or convert it with tgb_tucker_to_canonical
  * (tucker_to_canonical, reduction.cpp:238-269; reduce_rank = mode 1 + T2C).
- * Singular values are the leading ones the rank rule needed (Gram spectrum). */
+ * Singular values are the leading ones the rank rule needed; mode + 2 also
+ * computes each RHOSVD mode matrix's FULL spectrum (TuckerResult::
+ * mode_singular_values, reduction.hpp:42), which tgb_tucker_sigma then returns. */
 typedef struct tgb_tucker tgb_tucker;
 int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, const int64_t* ranks, int max_sweeps,
                       int mode, int mem, tgb_tucker** out);
@@ -358,6 +360,16 @@ int tgb_tucker_sigma(tgb_tucker* t, int axis, int64_t* count, double* sigma);
  * the one before well above it. */
 int tgb_tucker_margins(tgb_tucker* t, int axis, double* out);
 int tgb_tucker_to_canonical(tgb_ctx* ctx, tgb_tucker* t, tgb_cp* out, int mem);
+
+/* TuckerResult::mode_singular_values of rhosvd(a) for one mode (reduction.hpp:42,
+ * reduction.cpp:172-190 with thin_svd_left's branches, :85-138): the singular
+ * values of W = f_axis diag(w) of normalize(a), descending; min(n_axis, rank)
+ * of them, except the tall Gram branch (n >= 4 R, R >= 8), which keeps
+ * lambda > lambda_max 1e-24.  sigma: min(n_axis, rank) doubles, host; *count =
+ * values written.  Device Gram + Householder tridiagonalisation (one
+ * cooperative grid) + bisection; sigma_i carries ~eps m sigma_0^2 / sigma_i
+ * absolute error (Gram spectrum).  a in space `mem`. */
+int tgb_mode_spectrum(tgb_ctx* ctx, const tgb_cp* a, int axis, int mem, int64_t* count, double* sigma);
 
 /* replaces tg::thin_svd_left (reduction.hpp:67, reduction.cpp:85-138):
  * left singular pairs of a rows x cols matrix A (column-major, space `mem`),

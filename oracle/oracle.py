@@ -532,6 +532,20 @@ def ref_reduce(a: OCP, eps: float | None = None, ranks=None, sweeps: int = 3, mo
             "sweeps": info[5], "canonical_rank": info[6]}, out
 
 
+def ref_mode_sigma(a: OCP, axis: int, eps: float | None = 1e-6, ranks=None, mode: int = 0) -> np.ndarray:
+    """The reference's TuckerResult::mode_singular_values[axis] (rhosvd: mode 0)."""
+    R = rlib()
+    rk = (C.c_longlong * 3)(*(ranks or (0, 0, 0)))
+    cap = max(1, min(a.rank(), max(a.factors()[axis].shape[0], 1)))
+    out = np.zeros(cap)
+    cnt = C.c_longlong()
+    rc = R.ref_mode_sigma(a.h, C.c_int(eps is not None), C.c_double(eps or 0.0), rk, C.c_int(mode), C.c_int(axis),
+                          C.c_longlong(cap), C.byref(cnt), _p(out))
+    if rc:
+        raise OracleError(rc, R.ref_last_error().decode())
+    return out[:cnt.value]
+
+
 def ref_expsum_for_interval(r_min: float, r_max: float, eps: float):
     R = rlib()
     m, c0 = C.c_longlong(), C.c_double()

@@ -415,6 +415,21 @@ int ref_reduce(void* a, int use_eps, double eps, const long long* ranks, int swe
   });
 }
 
+// TuckerResult::mode_singular_values[axis] of rhosvd (mode 0) / canonical_to_tucker (mode 1)
+// (reduction.cpp:172-190); *count values into sigma (capacity cap).
+int ref_mode_sigma(void* a, int use_eps, double eps, const long long* ranks, int mode, int axis, long long cap,
+                   long long* count, double* sigma) {
+  return guard([&] {
+    const auto& t = *static_cast<tg::CanonicalTensor3*>(a);
+    const tg::ReductionConfig cfg = use_eps ? tg::ReductionConfig::tolerance(eps)
+                                            : tg::ReductionConfig::fixed(ranks[0], ranks[1], ranks[2]);
+    const tg::TuckerResult r = mode == 0 ? tg::rhosvd(t, cfg) : tg::canonical_to_tucker(t, cfg);
+    const auto& sv = r.mode_singular_values[axis];
+    *count = static_cast<long long>(sv.size());
+    for (size_t i = 0; i < sv.size() && static_cast<long long>(i) < cap; ++i) sigma[i] = sv[i];
+  });
+}
+
 // kernel.cpp:131-165
 int ref_expsum_for_interval(double r_min, double r_max, double eps, long long* m, double* c0) {
   return guard([&] {

@@ -20,7 +20,7 @@ from .hf import (Molecule, Nucleus, SCFConfig, SCFState, generalized_eigensolve,
                  fock_from_factors, kinetic_matrix, nuclear_matrix, nuclear_potential_tensor, overlap_matrix,
                  window_for_center)
 
-from .reduction import (ReductionConfig, TuckerResult, TuckerTensor3, canonical_to_tucker, reduce_rank, rhosvd,
-                        thin_svd_left)
+from .reduction import (ReductionConfig, TuckerResult, TuckerTensor3, canonical_to_tucker, mode_spectrum, reduce_rank,
+                        rhosvd, thin_svd_left)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

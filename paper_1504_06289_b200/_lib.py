@@ -163,6 +163,7 @@ def lib() -> C.CDLL:
             "tgb_tucker_get": (I, [P, P, P, P, P, P, I]),
             "tgb_tucker_sigma": (I, [P, I, C.POINTER(I64), P]),
             "tgb_tucker_margins": (I, [P, I, P]),
+            "tgb_mode_spectrum": (I, [P, C.POINTER(tgb_cp), I, I, P, P]),
             "tgb_tucker_to_canonical": (I, [P, P, C.POINTER(tgb_cp), I]),
             "tgb_dgemm": (I, [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64]),
             "tgb_host_last_error": (C.c_char_p, []),

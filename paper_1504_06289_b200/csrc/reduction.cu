@@ -845,6 +845,7 @@ struct RedCfgC {
   double eps;
   int64_t ranks[3];
   int max_sweeps;
+  bool full_spectra = false;  // also the whole spectrum of each RHOSVD mode matrix (spectrum.cu)
 };
 
 struct RedState {
@@ -860,6 +861,8 @@ struct RedState {
   bool rank_clamped = false, fallback = false;
   std::vector<double> sweep_fits;
   std::array<std::vector<double>, 3> sigma;
+  std::array<std::vector<double>, 3> sigma_full;  // mode_singular_values when requested
+  bool has_full = false;
   // rank-selection margins of the initializing SVDs (tgb_tucker_margins)
   std::array<double, 3> total{};  // sum of ALL squared singular values of the mode's side matrix
   bool use_eps = false;
@@ -1104,6 +1107,10 @@ void reduce_dev(tgb_ctx* ctx, const tgb_cp& a, const RedCfgC& cfg, bool als, Red
     }
     st.r[mode] = left_subspace(ctx, n, R, W.p, &cfg, mode, -1, &st.rank_clamped, st.Z[mode], &st.sigma[mode],
                                nullptr, 0, &st.total[mode]);
+    if (cfg.full_spectra) {
+      st.sigma_full[mode] = mode_spectrum_dev(ctx, n, R, W.p);
+      st.has_full = true;
+    }
     st.use_eps = cfg.use_eps;
     st.eps = cfg.eps;
     tm.mark("rhosvd left subspace");
@@ -1198,7 +1205,8 @@ struct tgb_tucker {
 
 extern "C" {
 
-// mode: 0 rhosvd, 1 canonical_to_tucker (RHOSVD + ALS).  a: device or host (mem).
+// mode: 0 rhosvd, 1 canonical_to_tucker (RHOSVD + ALS); + 2: also the full
+// spectra of the RHOSVD mode matrices (mode_singular_values).  a: device or host (mem).
 int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, const int64_t* ranks, int max_sweeps,
                       int mode, int mem, tgb_tucker** out) {
   return tgb::guarded_call([&] {
@@ -1210,7 +1218,8 @@ int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, co
     TGB_CUDA(cudaSetDevice(ctx->device));
     tgb::DevStreamScope scope(ctx);
     tgb::StageTimer tm(ctx);
-    tgb::RedCfgC cfg{use_eps != 0, eps, {0, 0, 0}, max_sweeps};
+    tgb::require(mode >= 0 && mode <= 3, "reduce: bad mode");
+    tgb::RedCfgC cfg{use_eps != 0, eps, {0, 0, 0}, max_sweeps, (mode & 2) != 0};
     if (!use_eps)
       for (int i = 0; i < 3; ++i) cfg.ranks[i] = ranks[i];
     tgb_cp dev = *a;
@@ -1228,7 +1237,7 @@ int tgb_reduce_tucker(tgb_ctx* ctx, const tgb_cp* a, int use_eps, double eps, co
     tm.mark("input to device");
     auto* t = new tgb_tucker();
     try {
-      tgb::reduce_dev(ctx, dev, cfg, mode == 1, t->st);
+      tgb::reduce_dev(ctx, dev, cfg, (mode & 1) != 0, t->st);
       TGB_CUDA(cudaStreamSynchronize(ctx->stream));
     } catch (...) {
       delete t;
@@ -1271,7 +1280,8 @@ int tgb_tucker_get(tgb_tucker* t, double* core, double* side0, double* side1, do
 
 int tgb_tucker_sigma(tgb_tucker* t, int axis, int64_t* count, double* sigma) {
   return tgb::guarded_call([&] {
-    const auto& s = t->st.sigma[axis];
+    tgb::require(t && count && axis >= 0 && axis < 3, "tucker_sigma: bad argument");
+    const auto& s = t->st.has_full ? t->st.sigma_full[axis] : t->st.sigma[axis];
     *count = static_cast<int64_t>(s.size());
     if (sigma)
       for (size_t i = 0; i < s.size(); ++i) sigma[i] = s[i];

@@ -191,6 +191,10 @@ void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const
 double scalar_product_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b);
 void coulomb_matrix_dev(tgb_ctx* ctx, const tgb_cp& basis, const int64_t* fn_offset, int64_t nb, const tgb_cp& vh,
                         double vol, double* J);
+// spectrum.cu: full spectra of RHOSVD mode matrices (mode_singular_values)
+void sym_eigvals_dev(tgb_ctx* ctx, int64_t m, double* G, double* lam);
+std::vector<double> mode_spectrum_dev(tgb_ctx* ctx, int64_t n, int64_t R, const double* W);
+std::vector<double> cp_mode_spectrum(tgb_ctx* ctx, const tgb_cp& a, int axis);
 void dgemm(tgb_ctx* ctx, bool ta, bool tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
            int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
 void orthonormalize_columns(tgb_ctx* ctx, int64_t d, int p, double* X);

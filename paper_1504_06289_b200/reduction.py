@@ -7,7 +7,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import MEM_HOST, InvalidArgument, check, lib
+from ._lib import MEM_DEVICE, MEM_HOST, InvalidArgument, check, lib
 from .tengrid import CanonicalTensor3, Context, default_context
 
 
@@ -18,6 +18,9 @@ class ReductionConfig:
     ranks: tuple | None = None
     epsilon: float | None = None
     max_sweeps: int = 3
+    # also fill TuckerResult.mode_singular_values with the FULL spectra (reduction.hpp:42);
+    # off by default: the rank rule only needs the leading values
+    full_spectra: bool = False
 
     @staticmethod
     def fixed(r1, r2, r3, sweeps=3):
@@ -78,7 +81,8 @@ def _run(a: CanonicalTensor3, cfg: ReductionConfig, mode: int, ctx: Context | No
     ca = a._cstruct()
     ranks = np.asarray(cfg.ranks if cfg.ranks is not None else (0, 0, 0), dtype=np.int64)
     check(lib().tgb_reduce_tucker(ctx.handle, C.byref(ca), int(cfg.epsilon is not None), cfg.epsilon or 0.0,
-                                  ranks.ctypes.data, cfg.max_sweeps, mode, MEM_HOST, C.byref(h)))
+                                  ranks.ctypes.data, cfg.max_sweeps, mode + (2 if cfg.full_spectra else 0), MEM_HOST,
+                                  C.byref(h)))
     return _tucker_result(h, a.extents(), ctx)
 
 
@@ -111,6 +115,24 @@ def _tucker_result(h, dims, ctx: Context) -> TuckerResult:
     res._t2c_rank = int(info[6])
     res._ctx = ctx
     return res
+
+
+def mode_spectrum(a, axis: int, ctx: Context | None = None) -> np.ndarray:
+    """tgb_mode_spectrum: the full singular-value spectrum rhosvd reports for mode `axis`
+    (TuckerResult::mode_singular_values, reduction.hpp:42; reduction.cpp:172-190), device-computed.
+    `a`: CanonicalTensor3 (host) or DeviceCP."""
+    from .tengrid import DeviceCP
+
+    ctx = ctx or default_context()
+    if not 0 <= axis < 3:
+        raise InvalidArgument("mode_spectrum: axis must be 0, 1 or 2")
+    mem = MEM_DEVICE if isinstance(a, DeviceCP) else MEM_HOST
+    ca = a._cstruct()
+    cnt = C.c_int64()
+    n_ax = a.extent(axis) if isinstance(a, DeviceCP) else a.extents()[axis]
+    out = np.zeros(max(1, min(n_ax, a.rank())))
+    check(lib().tgb_mode_spectrum(ctx.handle, C.byref(ca), axis, mem, C.byref(cnt), out.ctypes.data))
+    return out[:cnt.value].copy()
 
 
 def rhosvd(a: CanonicalTensor3, cfg: ReductionConfig, ctx: Context | None = None) -> TuckerResult:

@@ -103,6 +103,10 @@ def cfg1(ctx):
     # the drop-in density_tensor: Theta built on the device from the basis, reduced there
     t_dens, red2 = timed(lambda: tg.density_tensor(disc, c_occ, 1e-6, ctx), reps=1, sync=torch.cuda.synchronize)
     res = tg.canonical_to_tucker(theta_full, cfgr, ctx)
+    # opt-in full mode_singular_values (csrc/spectrum.cu): the three 2049-point spectra of Theta's mode matrices
+    dth = tg.DeviceCP.from_host(theta_full)
+    t_spec, spec = timed(lambda: [tg.mode_spectrum(dth, ax, ctx) for ax in range(3)], reps=1,
+                         sync=torch.cuda.synchronize)
     kern = tg.kernel_tensor(bs.grid, tg.make_expsum(KERNEL_M[1], KERNEL_C0[1]), False)
     dt, dk = tg.DeviceCP.from_host(red), tg.DeviceCP.from_host(kern.tensor)
     vh = tg.DeviceCP.empty(list(bs.grid.n), dt.rank() * dk.rank())
@@ -117,6 +121,7 @@ def cfg1(ctx):
             "density_build_host_s": t_build, "reduce_rank_ms": t_red * 1e3,
             "density_tensor_device_ms": t_dens * 1e3, "density_tensor_rank": red2.rank(), "tucker_ranks": list(res.tucker.ranks()),
             "reduced_rank": red.rank(), "rank_margins": res.rank_margins,
+            "mode_spectra_ms": t_spec * 1e3, "mode_spectra_counts": [len(x) for x in spec],
             "hartree_ms": t_vh * 1e3, "R_V": RV, "R_V_distinct": RVd, "coulomb_ms": t_j * 1e3,
             "coulomb_tflops": flops_j / t_j / 1e12, "coulomb_fp64_frac": flops_j / t_j / 1e12 / FP64,
             "J_symmetric_exact": bool(np.array_equal(J, J.T)), "J_trace": float(np.trace(J))}
