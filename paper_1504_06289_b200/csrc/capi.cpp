@@ -67,10 +67,10 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
   for (int ax = 0; ax < 3; ++ax) tgb::require(out->n[ax] == a->n[ax], "convolve: output extent mismatch");
   TGB_CUDA(cudaSetDevice(ctx->device));
   if (mem == TGB_MEM_DEVICE) {
-    tgb::weights_outer(ctx, ra, a->weight, rb, b->weight, bscale, out->weight);
     const double* fa[3] = {a->factor[0], a->factor[1], a->factor[2]};
     const double* fb[3] = {b->factor[0], b->factor[1], b->factor[2]};
-    tgb::convolve_axes(ctx, 3, a->n, ra, fa, rb, fb, h, out->factor);
+    tgb::convolve_axes(ctx, 3, a->n, ra, fa, rb, fb, h, out->factor, nullptr, a->weight, b->weight, bscale,
+                       out->weight);
     return;
   }
   tgb::require(mem == TGB_MEM_HOST, "convolve: bad memory space");

@@ -559,43 +559,34 @@ __device__ __forceinline__ void stage_product(double2* sm, int N, const double2*
   }
 }
 
-// Static-size staging: all ceil((N+1)/TT) loads of A and B in flight at once,
-// the Nyquist product included (slot pidx(N)).
+// Static-size staging: the ceil((N+1)/TT) loads of A and B per thread in
+// batches of up to 6 in flight (one batch at TT >= 160), the Nyquist product
+// included (slot pidx(N)).
 template <int N, int TT, bool BREAL>
 __device__ __forceinline__ void stage_product_static(double2* sm, const double2* __restrict__ A,
                                                      const void* __restrict__ Bv) {
   constexpr int K = (N + 1 + TT - 1) / TT;
-  constexpr bool kWhole = (N + 1) % TT == 0;
-  double2 a[K];
-  if constexpr (BREAL) {
-    double b[K];
+  constexpr int KB = K < 6 ? K : 6;
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int pos = threadIdx.x + k * TT;
-      if (kWhole || pos <= N) {
-        a[k] = ld2(A + pos);
-        b[k] = __ldg(static_cast<const double*>(Bv) + pos);
+  for (int k0 = 0; k0 < K; k0 += KB) {
+    double2 a[KB];
+    double2 bc[KB];
+    double br[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+      const int pos = threadIdx.x + (k0 + q) * TT;
+      if (k0 + q < K && pos <= N) {
+        a[q] = ld2(A + pos);
+        if constexpr (BREAL)
+          br[q] = __ldg(static_cast<const double*>(Bv) + pos);
+        else
+          bc[q] = ld2(static_cast<const double2*>(Bv) + pos);
       }
     }
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int pos = threadIdx.x + k * TT;
-      if (kWhole || pos <= N) sm[pidx(pos)] = cscale(a[k], b[k]);
-    }
-  } else {
-    double2 b[K];
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int pos = threadIdx.x + k * TT;
-      if (kWhole || pos <= N) {
-        a[k] = ld2(A + pos);
-        b[k] = ld2(static_cast<const double2*>(Bv) + pos);
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int pos = threadIdx.x + k * TT;
-      if (kWhole || pos <= N) sm[pidx(pos)] = cmul(a[k], b[k]);
+    for (int q = 0; q < KB; ++q) {
+      const int pos = threadIdx.x + (k0 + q) * TT;
+      if (k0 + q < K && pos <= N) sm[pidx(pos)] = BREAL ? cscale(a[q], br[q]) : cmul(a[q], bc[q]);
     }
   }
 }
@@ -1318,9 +1309,8 @@ __global__ void __launch_bounds__(TT, 1)
 // so the spectrum stores are coalesced; the phase factors of modes 1/2 come
 // from per-plan tables instead of sincospi.
 template <int R0, int R1, int R2, int R3, int TT>
-__global__ void __launch_bounds__(TT, 1)
-    spectrum_kernel_static(PlanArgs pa, SpecAxes sx, int nA, const int* __restrict__ colidx, int nB, int modeB,
-                           int64_t ldx) {
+__device__ __forceinline__ void spectrum_body_static(const PlanArgs& pa, const SpecAxes& sx, int nA,
+                                                     const int* __restrict__ colidx, int nB, int modeB, int64_t ldx) {
   constexpr int N = R0 * R1 * R2 * R3;
   constexpr int L1 = R0, L2 = R0 * R1, L3 = R0 * R1 * R2;
   extern __shared__ double2 sm[];
@@ -1422,6 +1412,13 @@ __global__ void __launch_bounds__(TT, 1)
       atomicAdd(pa.phase + 11, 1ULL);
     }
   }
+}
+
+template <int R0, int R1, int R2, int R3, int TT>
+__global__ void __launch_bounds__(TT, 1)
+    spectrum_kernel_static(const __grid_constant__ PlanArgs pa, const __grid_constant__ SpecAxes sx, int nA,
+                           const int* __restrict__ colidx, int nB, int modeB, int64_t ldx) {
+  spectrum_body_static<R0, R1, R2, R3, TT>(pa, sx, nA, colidx, nB, modeB, ldx);
 }
 
 // ---- Fused first pass.  Leaders 0..TT-1 (regular block pairs, one per
@@ -1942,6 +1939,119 @@ __global__ void __launch_bounds__(256) col_groups_small_kernel(const __grid_cons
   groups_and_work(ca, ax, rb, ra, cmap, rep, rnk, goff, part, sym, 0, ra, true);
 }
 
+struct WeightArgs {  // out[i + ra j] = wa[i] * (use_scale ? wb[j] * scale : wb[j]) (weights_outer)
+  const double* wa = nullptr;
+  const double* wb = nullptr;
+  double scale = 1.0;
+  int use_scale = 0;
+  double* out = nullptr;
+};
+
+// Config-0 fusion: the small plan's spectra, the kernel-column grouping and
+// the output weights in ONE launch.  Kernel-column CTAs also hash their column
+// and test its mirror symmetry (L1/L2-resident: just loaded for the
+// transform); the last CTA of each axis (ticket) verifies the hash matches,
+// groups the columns and writes the whole work list, so the pair kernel
+// follows in stream order with no aux-stream round trip.  The output weights
+// are a grid-stride loop of the axis-0 CTAs.
+template <int R0, int R1, int R2, int R3, int TT>
+__global__ void __launch_bounds__(TT, 1)
+    spectrum_group_kernel(const __grid_constant__ PlanArgs pa, const __grid_constant__ SpecAxes sx, int nA, int nB,
+                          int64_t ldx, const __grid_constant__ ColAxes ca, int64_t ra, const int64_t* __restrict__ cmap,
+                          int weak, unsigned* __restrict__ ticket, const __grid_constant__ WeightArgs wt) {
+  spectrum_body_static<R0, R1, R2, R3, TT>(pa, sx, nA, nullptr, nB, 3, ldx);
+  const int ax = blockIdx.y, rb = nB;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (wt.out && ax == 0)
+    for (int64_t idx = blockIdx.x * static_cast<int64_t>(TT) + threadIdx.x; idx < ra * rb;
+         idx += static_cast<int64_t>(gridDim.x) * TT) {
+      const int64_t i = idx % ra, j = idx / ra;
+      const double bj = wt.use_scale ? wt.wb[j] * wt.scale : wt.wb[j];
+      wt.out[idx] = wt.wa[i] * bj;
+    }
+  if (static_cast<int>(blockIdx.x) >= nB) return;  // density columns are done
+  extern __shared__ double2 smx[];
+  __syncthreads();  // the spectrum's shared memory is free from here on
+  auto* red = reinterpret_cast<unsigned long long*>(smx);
+  const int64_t n = ca.n[ax];
+  {  // (1) this kernel column's hash and mirror symmetry
+    // also: bitwise equal to the index-mirrored column rb-1-j?  (the +-t sinc twins of a kernel
+    // tensor sit there, kernel.cpp:194) — the grouping then needs no second pass over them
+    const int j = blockIdx.x, jm = rb - 1 - j;
+    const auto* x = reinterpret_cast<const unsigned long long*>(ca.B[ax] + j * n);
+    const auto* y = reinterpret_cast<const unsigned long long*>(ca.B[ax] + jm * n);
+    unsigned long long h = 0;
+    int sym = 1, mir = 1;
+    for (int64_t i0 = threadIdx.x; i0 < n; i0 += static_cast<int64_t>(TT) * 4) {
+      unsigned long long v[4], m[4], z[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(TT) * u;
+        v[u] = i < n ? x[i] : 0;
+        m[u] = i < n / 2 ? x[n - 1 - i] : v[u];
+        z[u] = i < n ? y[i] : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t i = i0 + static_cast<int64_t>(TT) * u;
+        if (i < n) h += col_word_hash(v[u], i);
+        sym &= v[u] == m[u];
+        mir &= v[u] == z[u];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if (lane == 0) red[warp] = h;
+    sym = __syncthreads_and(sym);
+    mir = __syncthreads_and(mir);
+    if (threadIdx.x == 0) {
+      unsigned long long hs = 0;
+      for (int q = 0; q < nw; ++q) hs += red[q];
+      ca.sig[ax * rb + j] = weak ? 0ull : mix64c(hs);
+      ca.asym[ax * rb + j] = !sym;
+      ca.bad[ax * rb + j] = mir;  // here: "equals column rb-1-j"
+    }
+  }
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  // kernel columns are CTAs [0, nB): dispatched first, so the last of them runs the grouping
+  // while the density-column CTAs are still transforming
+  if (threadIdx.x == 0) s_last = atomicAdd(ticket + ax, 1u) == static_cast<unsigned>(nB) - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // (2)-(3) the last CTA of this axis: representatives, groups, the whole work list
+  int* rep = reinterpret_cast<int*>(smx);
+  int* rnk = rep + rb;
+  int* goff = rnk + rb;
+  int* part = goff + rb;
+  auto* sg = reinterpret_cast<unsigned long long*>(part + rb);  // 16 rb bytes in: 8-byte aligned
+  int sym = 1;
+  for (int j = threadIdx.x; j < rb; j += blockDim.x) {
+    sg[j] = __ldcg(ca.sig + ax * rb + j);
+    sym &= !__ldcg(ca.asym + ax * rb + j);
+    rnk[j] = __ldcg(ca.bad + ax * rb + j);  // equals its index mirror (scratch until groups_and_work)
+  }
+  sym = __syncthreads_and(sym);
+  if (threadIdx.x == 0) ticket[ax] = 0;  // self-resetting for the next call
+  for (int j = warp; j < rb; j += nw) {
+    int r = j;
+    for (int c0 = 0; c0 < j && r == j; c0 += 32) {
+      const unsigned m = __ballot_sync(0xffffffffu, c0 + lane < j && sg[c0 + lane] == sg[j]);
+      if (m) r = c0 + __ffs(m) - 1;
+    }
+    const bool known = r == rb - 1 - j && rnk[j];  // already compared bitwise by CTA j
+    if (r != j && !known &&
+        !cols_equal_warp(reinterpret_cast<const unsigned long long*>(ca.B[ax] + r * n),
+                         reinterpret_cast<const unsigned long long*>(ca.B[ax] + j * n), n, lane))
+      r = rep_search_warp(ca, ax, rb, j, sg, lane);
+    if (lane == 0) rep[j] = r;
+  }
+  __syncthreads();
+  groups_and_work(ca, ax, rb, ra, cmap, rep, rnk, goff, part, sym, 0, ra, true);
+}
+
 __global__ void weights_outer_kernel(int64_t ra, const double* __restrict__ wa, int64_t rb,
                                      const double* __restrict__ wb, double scale, int use_scale, double* out) {
   const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
@@ -2223,7 +2333,46 @@ static bool small_plan(const ConvPlan& pl) {
 // (n = 2049 -> 16*10*10 measured slower here than the generic kernels: 2.93 vs 2.79 ms for config 1's V_H)
 static bool launch_small(tgb_ctx* ctx, const ConvPlan& pl, const SpecAxes& sx, const PairAxes& pr,
                          const PairAxes& pc, int naxes, int nA, int nB, int64_t ldx) {
+  const char* f = getenv("TGB_SMALL_TT");  // A/B: CTA width vs resident CTAs per SM (128 registers each)
+  const int tt = f ? atoi(f) : 160;
+  if (tt == 64) return try_small<16, 10, 5, 1, 64, 8, 160>(ctx, pl, sx, pr, pc, naxes, nA, nB, ldx);
+  if (tt == 96) return try_small<16, 10, 5, 1, 96, 5, 160>(ctx, pl, sx, pr, pc, naxes, nA, nB, ldx);
+  if (tt == 128) return try_small<16, 10, 5, 1, 128, 4, 160>(ctx, pl, sx, pr, pc, naxes, nA, nB, ldx);
   return try_small<16, 10, 5, 1, 160, 3, 160>(ctx, pl, sx, pr, pc, naxes, nA, nB, ldx);
+}
+
+// Config-0 fusion (spectrum_group_kernel): the grouping's shared memory
+// (24 rb bytes) must fit the spectrum launch, the split first pass its width.
+static bool small_fusable(const ConvPlan& pl, int64_t rb) {
+  const PlanArgs& a = pl.a;
+  return small_plan(pl) && static_cast<size_t>(24 * rb) <= pl.smem && 2 * (a.npl - a.nsp) + a.nsp <= 160 &&
+         !getenv("TGB_NO_FUSE");
+}
+
+static void launch_small_fused(tgb_ctx* ctx, const ConvPlan& pl, const SpecAxes& sx, const PairAxes& pr,
+                               const PairAxes& pc, int naxes, int nA, int nB, int64_t ldx, const ColAxes& ca,
+                               const int64_t* cmap, int weak, unsigned* ticket, const WeightArgs& wt) {
+  auto sk = spectrum_group_kernel<16, 10, 5, 1, 160>;
+  auto pk = pair_kernel_small<16, 10, 5, 1, 160, 3>;
+  static bool attr[kTgbMaxDevices] = {};
+  static int per_sm[kTgbMaxDevices] = {};
+  if (!attr[ctx->device]) {
+    for (const void* f : {reinterpret_cast<const void*>(sk), reinterpret_cast<const void*>(pk)}) {
+      cudaFuncAttributes fa{};
+      TGB_CUDA(cudaFuncGetAttributes(&fa, f));
+      TGB_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(ctx->smem_optin - fa.sharedSizeBytes)));
+    }
+    TGB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ctx->device], pk, 160, pl.smem));
+    attr[ctx->device] = true;
+  }
+  sk<<<dim3(nA + nB, naxes), 160, pl.smem, ctx->stream>>>(pl.a, sx, nA, nB, ldx, ca, nA, cmap, weak, ticket, wt);
+  TGB_LAUNCHED(ctx);
+  const int grid = std::max(1, std::max(1, per_sm[ctx->device]) * ctx->num_sms / naxes);
+  prof_begin(ctx);
+  pk<<<dim3(grid, naxes), 160, pl.smem, ctx->stream>>>(pl.a, pr, pc);
+  TGB_LAUNCHED(ctx);
+  prof_end(ctx);
 }
 
 // config-2 plan (fftconv12k.cu)
@@ -2246,10 +2395,23 @@ void kS_convolve_axis(tgb_ctx* ctx, int64_t n, int S, int64_t ra, const double* 
 // kernel column's spectrum is formed in both the real and the complex form,
 // and each pair kernel picks one from the device-side symmetry flag.
 void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const double* const* A, int64_t rb,
-                   const double* const* B, const double* h, double* const* out, const int64_t* colmap) {
-  if (ra == 0 || rb == 0 || naxes == 0) return;
+                   const double* const* B, const double* h, double* const* out, const int64_t* colmap,
+                   const double* wa, const double* wb, double wscale, double* wout) {
+  if (wout && ra * rb == 0) return;
+  if (ra == 0 || rb == 0 || naxes == 0) {
+    if (wout) weights_outer(ctx, ra, wa, rb, wb, wscale, wout);
+    return;
+  }
   std::vector<std::shared_ptr<ConvPlan>> plans(naxes);
   for (int ax = 0; ax < naxes; ++ax) plans[ax] = get_plan(ctx, n[ax]);
+  bool same_n = true;
+  for (int ax = 1; ax < naxes; ++ax) same_n = same_n && n[ax] == n[0];
+  const ConvPlan& p0 = *plans[0];
+  const bool batched = (naxes > 1 || small_plan(p0)) && same_n && !p0.direct && !k12_applicable(n[0], p0.a.N) &&
+                       !static_plan(p0) && !(n[0] > ctx->direct_max && kS_split(n[0]));
+  // the config-0 small plan fuses the grouping (and the weights) into its spectrum launch
+  const bool fused = batched && small_fusable(p0, rb);
+  if (wout && !fused) weights_outer(ctx, ra, wa, rb, wb, wscale, wout);
   // ---- aux stream: hashes -> verified representatives -> groups and work lists
   const size_t cbytes = (static_cast<size_t>(naxes * rb) * (sizeof(unsigned long long) + 3 * sizeof(int)) + 16 + 255) &
                         ~size_t(255);
@@ -2263,8 +2425,6 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
   const size_t zbytes = static_cast<size_t>(naxes * rb) * (sizeof(unsigned long long) + 2 * sizeof(int)) + 16;
   auto* winfo = reinterpret_cast<int*>(wsp + cbytes);  // 2 ints per axis
   char* wlist = wsp + cbytes + 256;
-  TGB_CUDA(cudaEventRecord(ctx->aux_in, ctx->stream));  // B is ready in stream order
-  TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
   const size_t wsmem = static_cast<size_t>(4 * rb) * sizeof(int) + static_cast<size_t>(rb) * 8;
   if (wsmem + 1024 > ctx->smem_optin)
     throw Error(TGB_INVALID_ARGUMENT, "convolve: kernel rank too large for the work builder");
@@ -2281,15 +2441,17 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
     ca.work[ax] = dwork[ax];
     ca.winfo[ax] = winfo + 2 * ax;
   }
-  {
+  // test hook: every hash 0, so every candidate goes through the collision path
+  const int weak = getenv("TGB_COLHASH_WEAK") ? 1 : 0;
+  if (!fused) {
+    TGB_CUDA(cudaEventRecord(ctx->aux_in, ctx->stream));  // B is ready in stream order
+    TGB_CUDA(cudaStreamWaitEvent(ctx->aux_stream, ctx->aux_in, 0));
     int64_t maxcol = 0, items = 0;
     for (int ax = 0; ax < naxes; ++ax) {
       maxcol = std::max(maxcol, n[ax]);
       items += rb * ((n[ax] + kChunk - 1) / kChunk);
     }
     const int irb = static_cast<int>(rb);
-    // test hook: every hash 0, so every candidate goes through the collision path
-    const int weak = getenv("TGB_COLHASH_WEAK") ? 1 : 0;
     static size_t attr_smem[2][kTgbMaxDevices] = {};
     const bool one_cta = rb * maxcol <= kColCtaMax;
     const void* fn = one_cta ? reinterpret_cast<const void*>(col_groups_small_kernel)
@@ -2315,15 +2477,11 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
       col_work_kernel<<<dim3(gw, naxes), 256, wsmem, ctx->aux_stream>>>(ca, irb, ra, colmap);
       TGB_LAUNCHED(ctx);
     }
+    TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
   }
-  TGB_CUDA(cudaEventRecord(ctx->aux_done, ctx->aux_stream));
   // ---- main stream: spectra (independent of the grouping), then the pairs
   bool joined = false;
-  bool same_n = true;
-  for (int ax = 1; ax < naxes; ++ax) same_n = same_n && n[ax] == n[0];
-  const ConvPlan& p0 = *plans[0];
-  if ((naxes > 1 || small_plan(p0)) && same_n && !p0.direct && !k12_applicable(n[0], p0.a.N) && !static_plan(p0) &&
-      !(n[0] > ctx->direct_max && kS_split(n[0]))) {
+  if (batched) {
     // every axis shares one generic plan: one spectrum launch and one pair launch per
     // spectrum form for all axes (config 0 is launch-bound: 16 -> 6 launches)
     const size_t N1 = static_cast<size_t>(p0.a.N) + 1;
@@ -2348,6 +2506,19 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
       pr.work[ax] = pc.work[ax] = dwork[ax];
       pr.winfo[ax] = pc.winfo[ax] = winfo + 2 * ax;
       pr.out[ax] = pc.out[ax] = out[ax];
+    }
+    if (fused) {
+      DevBuf& tk = ctx_buf(ctx, "colgrp.ticket");  // self-resetting per-axis counters, zeroed once
+      if (!tk.bytes) TGB_CUDA(cudaMemsetAsync(tk.get(16), 0, 16, ctx->stream));
+      WeightArgs wt;
+      wt.wa = wa;
+      wt.wb = wb;
+      wt.scale = wscale;
+      wt.use_scale = wscale != 1.0;
+      wt.out = wout;
+      launch_small_fused(ctx, p0, sx, pr, pc, naxes, static_cast<int>(ra), static_cast<int>(rb), n[0], ca, colmap, weak,
+                         static_cast<unsigned*>(tk.get(16)), wt);
+      return;
     }
     if (launch_small(ctx, p0, sx, pr, pc, naxes, static_cast<int>(ra), static_cast<int>(rb), n[0])) return;
     launch_spectrum_axes(ctx, p0, sx, naxes, static_cast<int>(ra), nullptr, static_cast<int>(rb), 3, n[0]);

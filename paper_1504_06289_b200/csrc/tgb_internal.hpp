@@ -184,8 +184,12 @@ void convolve_axis(tgb_ctx* ctx, int64_t n, int64_t ra, const double* A, int64_t
 // colmap (device, optional): 2 ra entries; density column i's result for
 // kernel column j goes to output column colmap[i] + colmap[ra + i] * j
 // instead of i + ra * j.
+// wout (optional): the output weights wout[i + ra j] = wa[i] * (wscale != 1 ? wb[j] * wscale : wb[j]),
+// as weights_outer, computed inside the first launch where the small plan fuses it.
 void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const double* const* A, int64_t rb,
-                   const double* const* B, const double* h, double* const* out, const int64_t* colmap = nullptr);
+                   const double* const* B, const double* h, double* const* out, const int64_t* colmap = nullptr,
+                   const double* wa = nullptr, const double* wb = nullptr, double wscale = 1.0,
+                   double* wout = nullptr);
 void conv_central_many_dev(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U, const double* v, double* out);
 void weights_outer(tgb_ctx* ctx, int64_t ra, const double* wa, int64_t rb, const double* wb, double scale, double* out);
 double scalar_product_dev(tgb_ctx* ctx, const tgb_cp& a, const tgb_cp& b);

@@ -336,7 +336,7 @@ def _grouping_case(rng, n, sym):
     return a, b
 
 
-@pytest.mark.parametrize("n", [257, 16385])  # one-CTA grouping (rb*n small) / hash + verify + work kernels
+@pytest.mark.parametrize("n", [257, 1025, 16385])  # one-launch grouping / fused into the N = 800 spectra / 3 kernels
 @pytest.mark.parametrize("sym", [True, False])
 @pytest.mark.parametrize("weak", [False, True])  # weak: every hash collides -> the verified re-search path
 def test_kernel_column_grouping_paths(ctx, monkeypatch, n, sym, weak):
