@@ -6,6 +6,9 @@
 
 #include <algorithm>
 #include <array>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -74,6 +77,7 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
     return;
   }
   tgb::require(mem == TGB_MEM_HOST, "convolve: bad memory space");
+  const auto t_call0 = std::chrono::steady_clock::now();
   for (int64_t j = 0; j < rb; ++j) {
     const double bj = bscale != 1.0 ? b->weight[j] * bscale : b->weight[j];
     for (int64_t i = 0; i < ra; ++i) out->weight[i + ra * j] = a->weight[i] * bj;
@@ -101,14 +105,24 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
   // column blocks (i + R_a j, i < R_a): only the representative blocks cross PCIe, the twins are
   // filled by host threads while the next axis transfers (pinned outputs; pageable outputs keep
   // the staged whole-factor copy).
+  // (column hashes first: kernel columns share long runs of underflowed zeros, so an all-pairs
+  // memcmp scans most of every column; only hash-equal pairs are compared)
   std::array<std::vector<int64_t>, 3> rep;
   for (int ax = 0; ax < 3; ++ax) {
     const int64_t n = a->n[ax];
+    std::vector<uint64_t> hv(rb);
+    for (int64_t j = 0; j < rb; ++j) {
+      const auto* x = reinterpret_cast<const uint64_t*>(b->factor[ax] + n * j);
+      uint64_t hh = 0x9E3779B97F4A7C15ull;
+      for (int64_t i = 0; i < n; ++i) hh = (hh ^ x[i]) * 0x100000001B3ull + static_cast<uint64_t>(i);
+      hv[j] = hh;
+    }
     rep[ax].resize(rb);
     for (int64_t j = 0; j < rb; ++j) {
       rep[ax][j] = j;
       for (int64_t jp = 0; jp < j; ++jp)
-        if (rep[ax][jp] == jp && std::memcmp(b->factor[ax] + n * jp, b->factor[ax] + n * j, n * sizeof(double)) == 0) {
+        if (rep[ax][jp] == jp && hv[jp] == hv[j] &&
+            std::memcmp(b->factor[ax] + n * jp, b->factor[ax] + n * j, n * sizeof(double)) == 0) {
           rep[ax][j] = jp;
           break;
         }
@@ -134,6 +148,12 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
         }
     }
   }
+  const bool trace = getenv("TGB_E2E_TRACE") != nullptr;  // analysis: host-side phases of this call
+  const auto tr0 = std::chrono::steady_clock::now();
+  double t_wait = 0.0, t_copy = 0.0;
+  auto since = [](std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+  };
   for (int ax = 0; ax < 3; ++ax) {
     const size_t blk = static_cast<size_t>(a->n[ax]) * ra;
     if (!pinned[ax]) {  // staged copy of the whole factor (pageable destination)
@@ -143,14 +163,21 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
     }
     for (int64_t j = 0; j < rb; ++j) {
       if (rep[ax][j] != j) continue;
+      auto tw = std::chrono::steady_clock::now();
       TGB_CUDA(cudaEventSynchronize(ctx_event(ctx, 3 + ax * rb + j)));
+      t_wait += since(tw);
+      tw = std::chrono::steady_clock::now();
       for (int64_t jt = j + 1; jt < rb; ++jt)
         if (rep[ax][jt] == j)
           tgb::par_memcpy(out->factor[ax] + blk * jt, out->factor[ax] + blk * j, blk * sizeof(double));
+      t_copy += since(tw);
     }
   }
   TGB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (trace)
+    fprintf(stderr, "[tgb-e2e] setup %.1f ms, waiting on D2H %.1f ms, twin copies %.1f ms, total %.1f ms\n",
+            std::chrono::duration<double, std::milli>(tr0 - t_call0).count(), t_wait, t_copy, since(t_call0));
 }
 
 // Device copy of a CP tensor (host mode helper); returns device view.

@@ -13,6 +13,7 @@
 #include <cstdint>
 #include <mutex>
 #include <cstring>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
@@ -72,7 +73,9 @@ class CopyPool {
  private:
   CopyPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned n = std::min(hw, 16u) - 1;
+    unsigned nt = std::min(hw, 16u);
+    if (const char* e = getenv("TGB_COPY_THREADS")) nt = std::max(1, std::min(64, atoi(e)));
+    const unsigned n = nt - 1;
     for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this] { loop(); });
   }
   ~CopyPool() {
