@@ -2377,11 +2377,12 @@ static void launch_small_fused(tgb_ctx* ctx, const ConvPlan& pl, const SpecAxes&
 
 // config-2 plan (fftconv12k.cu)
 bool k12_applicable(int64_t n, int64_t generic_N);
+bool k12_use_bulk(int64_t n, int64_t ra, const double* out, bool colmap);
 void k12_spectra(tgb_ctx* ctx, int64_t n, const double* A, int nA, double2* specA, const double* B, int nB,
-                 double* specBr, double2* specBc, int modeB, int64_t ldx, double h);
+                 double* specBr, double2* specBc, int modeB, int64_t ldx, double h, bool shiftA);
 void k12_pairs(tgb_ctx* ctx, int64_t n, const double2* specA, const double* specBr, const double2* specBc,
                const PairEntry* work, const int* winfo, double* out, const double* U, int64_t ldu, const double* V,
-               int64_t ldv, double h);
+               int64_t ldv, double h, bool bulk);
 
 // large-n plan (fftconv12k.cu): N = S * 12288 split into S sub-transforms
 int kS_split(int64_t n);
@@ -2559,12 +2560,13 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
       char* sb = static_cast<char*>(ctx->ws_spec_b.get(real_bytes + static_cast<size_t>(rb) * N1 * sizeof(double2)));
       auto* specBr = reinterpret_cast<double*>(sb);
       auto* specBc = reinterpret_cast<double2*>(sb + real_bytes);
+      const bool bulk = k12_use_bulk(n[ax], ra, out[ax], colmap != nullptr);
       k12_spectra(ctx, n[ax], A[ax], static_cast<int>(ra), specA, B[ax], static_cast<int>(rb), specBr, specBc, 3,
-                  n[ax], h[ax]);
+                  n[ax], h[ax], bulk);
       if (!joined) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
       joined = true;
       k12_pairs(ctx, n[ax], specA, specBr, specBc, dwork[ax], winfo + 2 * ax, out[ax], A[ax], n[ax], B[ax], n[ax],
-                h[ax]);
+                h[ax], bulk);
       continue;
     }
     const size_t N1 = static_cast<size_t>(pl.a.N) + 1;
