@@ -378,12 +378,11 @@ def main():
     # ---- roofline of the dominant kernel (pair convolution kernel, one launch = one axis)
     hbm_peak, peak_kind = peaks()
     nd = 21  # distinct kernel columns (M + 1)
-    bytes_launch = 8.0 * n * ra * rb + 8.0 * n * (ra + rb)
-    # each axis launches the pair kernel once per spectrum form (real / complex);
-    # the form that disagrees with the device-side symmetry flag exits at once,
-    # so the working launches are 3 per step (its ~4 us is kept in pair_ms)
-    work_launches = 3 * args.steps
-    avg_launch_ms = pair_ms / max(min(pair_launches, work_launches), 1)
+    # ONE persistent launch per step covers the three axes (fftconv12k.cu k12_pair_kernel);
+    # per axis: the output window columns plus the input factor columns
+    axes_per_launch = 3
+    bytes_launch = axes_per_launch * (8.0 * n * ra * rb + 8.0 * n * (ra + rb))
+    avg_launch_ms = pair_ms / max(pair_launches, 1)
     achieved = bytes_launch / (avg_launch_ms / 1e3) / 1e9
     traffic = None
     tj = ROOT / "profiles" / "ncu_traffic.json"
@@ -396,7 +395,7 @@ def main():
     m = 24576
     N = m // 2
     flops_pair = 5.0 * N * np.log2(N) + 16.0 * N  # complex FFT + split + product (nominal)
-    fp64_tflops = ra * nd * flops_pair / (avg_launch_ms / 1e3) / 1e12
+    fp64_tflops = axes_per_launch * ra * nd * flops_pair / (avg_launch_ms / 1e3) / 1e12
 
     # ---- e2e through the C-ABI with pinned HOST buffers (copies inside the timed region)
     e2e = None
@@ -460,7 +459,8 @@ def main():
                    "l2": "no flush needed: each step writes 8.06 GB of factors (> 126 MB L2)"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k12_pair_kernel (product, real split, inverse FFT N=12288, window stores; one launch per axis)",
+                     "kernel": "k12_pair_kernel (product, real split, inverse FFT N=12288, window stores; one launch per step = 3 axes)",
+                     "axes_per_launch": axes_per_launch,
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_launch_ms,
                      "launch_share_of_step": pair_ms / ms_local if ms_local else None,
                      "fp64": {"achieved_tflops_nominal": fp64_tflops, "peak_tflops": FP64_TFLOPS,

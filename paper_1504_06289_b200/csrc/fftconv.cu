@@ -2377,12 +2377,13 @@ static void launch_small_fused(tgb_ctx* ctx, const ConvPlan& pl, const SpecAxes&
 
 // config-2 plan (fftconv12k.cu)
 bool k12_applicable(int64_t n, int64_t generic_N);
-bool k12_use_bulk(int64_t n, int64_t ra, const double* out, bool colmap);
-void k12_spectra(tgb_ctx* ctx, int64_t n, const double* A, int nA, double2* specA, const double* B, int nB,
-                 double* specBr, double2* specBc, int modeB, int64_t ldx, double h, bool shiftA);
-void k12_pairs(tgb_ctx* ctx, int64_t n, const double2* specA, const double* specBr, const double2* specBc,
-               const PairEntry* work, const int* winfo, double* out, const double* U, int64_t ldu, const double* V,
-               int64_t ldv, double h, bool bulk);
+bool k12_use_shift(int64_t n, int64_t ra, const double* out, bool colmap);
+void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int nA, double2* const* specA,
+                 const double* const* B, int nB, double* const* specBr, double2* const* specBc, int modeB,
+                 int64_t ldx, const double* h, bool shiftA);
+void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double* const* specBr,
+               double2* const* specBc, PairEntry* const* work, const int* winfo0, double* const* out,
+               const double* const* U, const double* const* V, const double* h, bool shifted);
 
 // large-n plan (fftconv12k.cu): N = S * 12288 split into S sub-transforms
 int kS_split(int64_t n);
@@ -2528,6 +2529,11 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
     launch_pair_generic<false>(ctx, p0, pc, naxes);
     return;
   }
+  int k12_first = -1, k12_count = 0;  // the batch of axes whose N = 12288 spectra are already formed
+  bool k12_shift = false;
+  double2* k12_specA[3] = {};
+  double* k12_specBr[3] = {};
+  double2* k12_specBc[3] = {};
   for (int ax = 0; ax < naxes; ++ax) {
     const ConvPlan& pl = *plans[ax];
     if (const int S = n[ax] > ctx->direct_max ? kS_split(n[ax]) : 0) {  // beyond one CTA: split transform
@@ -2555,18 +2561,43 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
     }
     if (k12_applicable(n[ax], pl.a.N)) {  // N = 12288 natural-order plan (config 2)
       const size_t N1 = 12288 + 1;
-      auto* specA = static_cast<double2*>(ctx->ws_spec_a.get(static_cast<size_t>(ra) * N1 * sizeof(double2)));
+      const size_t a_bytes = (static_cast<size_t>(ra) * N1 * sizeof(double2) + 255) & ~size_t(255);
       const size_t real_bytes = (static_cast<size_t>(rb) * N1 * sizeof(double) + 255) & ~size_t(255);
-      char* sb = static_cast<char*>(ctx->ws_spec_b.get(real_bytes + static_cast<size_t>(rb) * N1 * sizeof(double2)));
-      auto* specBr = reinterpret_cast<double*>(sb);
-      auto* specBc = reinterpret_cast<double2*>(sb + real_bytes);
-      const bool bulk = k12_use_bulk(n[ax], ra, out[ax], colmap != nullptr);
-      k12_spectra(ctx, n[ax], A[ax], static_cast<int>(ra), specA, B[ax], static_cast<int>(rb), specBr, specBc, 3,
-                  n[ax], h[ax], bulk);
-      if (!joined) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
-      joined = true;
-      k12_pairs(ctx, n[ax], specA, specBr, specBc, dwork[ax], winfo + 2 * ax, out[ax], A[ax], n[ax], B[ax], n[ax],
-                h[ax], bulk);
+      const size_t b_bytes = real_bytes + ((static_cast<size_t>(rb) * N1 * sizeof(double2) + 255) & ~size_t(255));
+      // axes of this extent and the same output form share one spectrum launch (whole waves)
+      int nb = 0;  // batch [ax, ax + nb)
+      if (k12_first < 0 || ax >= k12_first + k12_count) {
+        const bool sh0 = k12_use_shift(n[ax], ra, out[ax], colmap != nullptr);
+        nb = 1;
+        while (ax + nb < naxes && nb < 3 && n[ax + nb] == n[ax] &&
+               k12_use_shift(n[ax + nb], ra, out[ax + nb], colmap != nullptr) == sh0)
+          ++nb;
+        k12_first = ax;
+        k12_count = nb;
+        k12_shift = sh0;
+        auto* sa = static_cast<char*>(ctx->ws_spec_a.get(nb * a_bytes));
+        auto* sbb = static_cast<char*>(ctx->ws_spec_b.get(nb * b_bytes));
+        const double* Ab[3];
+        const double* Bb[3];
+        double2* sAb[3];
+        double* sBr[3];
+        double2* sBc[3];
+        for (int i = 0; i < nb; ++i) {
+          Ab[i] = A[ax + i];
+          Bb[i] = B[ax + i];
+          sAb[i] = k12_specA[i] = reinterpret_cast<double2*>(sa + i * a_bytes);
+          sBr[i] = k12_specBr[i] = reinterpret_cast<double*>(sbb + i * b_bytes);
+          sBc[i] = k12_specBc[i] = reinterpret_cast<double2*>(sbb + i * b_bytes + real_bytes);
+        }
+        k12_spectra(ctx, n[ax], nb, Ab, static_cast<int>(ra), sAb, Bb, static_cast<int>(rb), sBr, sBc, 3, n[ax],
+                    h + ax, k12_shift);
+      }
+      if (nb) {  // first axis of its batch: one pair launch for the whole batch
+        if (!joined) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
+        joined = true;
+        k12_pairs(ctx, n[ax], nb, k12_specA, k12_specBr, k12_specBc, dwork.data() + ax, winfo + 2 * ax, out + ax,
+                  A + ax, B + ax, h + ax, k12_shift);
+      }
       continue;
     }
     const size_t N1 = static_cast<size_t>(pl.a.N) + 1;

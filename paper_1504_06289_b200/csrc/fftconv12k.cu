@@ -122,49 +122,31 @@ __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double
   }
 }
 
-// Round-wise forms (pair kernel, two-round schedule): after stage 1 the 16 segments t0 are
-// independent 768-point transforms; round r covers the segments t0 in [8 r, 8 r + 8).
-template <int S>
-__device__ __forceinline__ void stage2_round(double2* sm, int tid, double2 w2base, int r) {
-  const int k1 = tid % 48, t0 = tid / 48 + 8 * r;
-  double2 w2[16];
-  powers<16>(w2base, w2);
-  double2* p = sm + slot(t0, 0, k1);
-  double2 v[16];
-#pragma unroll
-  for (int s = 0; s < 16; ++s) v[s] = p[51 * s];
-  dft<16, S>(v);
-#pragma unroll
-  for (int t = 1; t < 16; ++t) v[t] = cmul(v[t], w2[t]);
-#pragma unroll
-  for (int t = 0; t < 16; ++t) p[51 * t] = v[t];
-}
-
-template <int S>
-__device__ __forceinline__ void stage3_round(double2* sm, int tid, double2 w31, double2 w32, int r) {
-  const int k2 = tid & 15;
-#pragma unroll 2
-  for (int b = tid; b < 2048; b += TT) {
-    const int t1 = (b >> 4) & 15, t0 = 8 * r + (b >> 8);
-    double2* p = sm + slot(t0, t1, k2);
-    double2 v0 = p[0], v1 = p[16], v2 = p[32];
-    dft3<S>(v0, v1, v2);
-    p[0] = v0;
-    p[16] = cmul(v1, w31);
-    p[32] = cmul(v2, w32);
-  }
-}
-
 // ---------------------------------------------------------------- forward spectra
 
 // One CTA per column: columns [0, nB) are kernel columns (modeB: 1 real form
 // hm Re(X e^{2 pi i k ofs/m}), 2 complex form hm X e^{2 pi i k ofs/m}, 3 both),
 // columns [nB, nB + nA) density columns (complex X).  Spectra: N + 1
 // natural-order entries per column.
+// blockIdx.y: axis (axes of one extent share a launch: 3 x 541 columns fill whole waves of the
+// one-CTA-per-SM grid, 541 leave a 0.35-wave tail per axis)
+struct SpecAxes12 {
+  const double* XA[3];
+  const double* XB[3];
+  double2* specA[3];
+  double* specBr[3];
+  double2* specBc[3];
+  double h[3];
+};
+
 __global__ void __launch_bounds__(TT, 1)
-    k12_spectrum_kernel(int n, const double* __restrict__ XA, int nA, double2* __restrict__ specA,
-                        const double* __restrict__ XB, int nB, double* __restrict__ specBr,
-                        double2* __restrict__ specBc, int modeB, int64_t ldx, double h, int shiftA) {
+    k12_spectrum_kernel(int n, SpecAxes12 axs, int nA, int nB, int modeB, int64_t ldx, int shiftA) {
+  const double* __restrict__ XA = axs.XA[blockIdx.y];
+  const double* __restrict__ XB = axs.XB[blockIdx.y];
+  double2* __restrict__ specA = axs.specA[blockIdx.y];
+  double* __restrict__ specBr = axs.specBr[blockIdx.y];
+  double2* __restrict__ specBc = axs.specBc[blockIdx.y];
+  const double h = axs.h[blockIdx.y];
   extern __shared__ double2 sm[];
   double2* zlo = sm + SLOTS;   // w_m^{-i}, i < 64
   double2* zhi = zlo + 64;     // w_m^{-64 j}, j < M / 64
@@ -271,49 +253,23 @@ __device__ __forceinline__ double2 bmul(double2 a, const void* B, int k) {
     return cmul(a, ld2(static_cast<const double2*>(B) + k));
 }
 
-// VAR 0: stages 2-4 each over the whole transform (four CTA barriers per pair).
-// VAR 1: two rounds of eight segments, the rounds skewed by one stage so that round 0's window
-//        stores drain while round 1's stage 3 runs: [2 r0] [3 r0, 2 r1] [4 r0, 3 r1] [4 r1].
-// VAR 2: two rounds back to back: [2 r0] [3 r0] [4 r0, 2 r1] [3 r1] [4 r1].
-template <bool BREAL, int VAR>
-__global__ void __launch_bounds__(TT, 1)
-    k12_pair_kernel(const double2* __restrict__ specA, const void* __restrict__ specB,
-                    const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out,
-                    const double* __restrict__ U, int64_t ldu, const double* __restrict__ V, int64_t ldv, double h,
-                    int n, int alias, unsigned long long* __restrict__ phase, int shifted) {
-  if ((winfo[1] != 0) != BREAL) return;
-  const int nwork = winfo[0];
-  __shared__ uint32_t tmem_base_sh;
-  extern __shared__ double2 sm[];
+// One CTA's pairs [w0, w1) of one axis (spectrum form BREAL), inside k12_pair_kernel.
+template <bool BREAL>
+__device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const double2* __restrict__ specA,
+                                             const void* __restrict__ specB, const PairEntry* __restrict__ work,
+                                             int w0, int w1, double* __restrict__ out, const double* __restrict__ U,
+                                             int64_t ldu, const double* __restrict__ V, int64_t ldv, double h, int n,
+                                             int alias, unsigned long long* __restrict__ phase, int shifted,
+                                             double2 wkk) {
   const int tid = threadIdx.x, warp = tid >> 5;
-  if (warp == 0) {
-    const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base_sh));
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tbase = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
-                         static_cast<uint32_t>((warp >> 2) * 128);
   const bool self = tid == TT - 1;
   const int kk = tid + 1;
-  // per-thread constants: split twiddle base w_m^kk in registers; the stage-2/3
-  // twiddle bases in a per-thread shared-memory table (registers are the limit)
-  const double2 wkk = self ? make_double2(1.0, 0.0) : root(kk, M);
   double2* cst = sm + SLOTS + 3 * tid;
-  cst[0] = root(tid % 48, 768);
-  cst[1] = root(tid & 15, 48);
-  cst[2] = cmul(cst[1], cst[1]);
   const int nz = (n + 1) >> 1;
   const bool odd_n = n & 1;
   const int kX = self ? 0 : kk, kY = self ? 384 : NB - kk;
   const int u_last = (nz - 1) % NB;  // stage-4 butterfly holding x[n-1]
-  // its thread: u = tid + 384 hb (VAR 0); u = t0 + 16 a + 256 c at tid = (t0 & 7) + 8 a + 128 c (rounds)
-  const int tid_last = VAR == 0 ? u_last % TT : (u_last & 7) + 8 * ((u_last >> 4) & 15) + 128 * (u_last >> 8);
-
-  const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
-  const int w1 = static_cast<int>((static_cast<int64_t>(nwork) * (blockIdx.x + 1)) / gridDim.x);
+  const int tid_last = u_last % TT;  // its thread: u = tid + 384 hb
   int ia_cur = -1;
   for (int w = w0; w < w1; ++w) {
     const PairEntry e = work[w];
@@ -455,6 +411,10 @@ __global__ void __launch_bounds__(TT, 1)
             if (t == nf) (sh ? v[t3].y : v[t3].x) -= corr1;
           }
           if (t >= lo && t < hi) {
+            if (shifted & 2) {  // timing probe (TGB_K12_NOSTORE): keep the arithmetic live, store nothing
+              if (v[t3].x == 1.2345e300) __stcs(q0, v[t3].y);
+              continue;
+            }
             __stcs(reinterpret_cast<double2*>(q0 + 2 * t), v[t3]);
             if (q1) __stcs(reinterpret_cast<double2*>(q1 + 2 * t), v[t3]);
           } else if (t == tsp) {
@@ -486,45 +446,16 @@ __global__ void __launch_bounds__(TT, 1)
         }
       }
     };
-    if constexpr (VAR == 0) {
-      stage2<1>(sm, tid, cst[0]);
-      __syncthreads();
-      c2 = phase ? clock64() : 0;
-      stage3<1>(sm, tid, cst[1], cst[2]);
-      __syncthreads();
-      c3 = phase ? clock64() : 0;
+    stage2<1>(sm, tid, cst[0]);
+    __syncthreads();
+    c2 = phase ? clock64() : 0;
+    stage3<1>(sm, tid, cst[1], cst[2]);
+    __syncthreads();
+    c3 = phase ? clock64() : 0;
 #pragma unroll 1
-      for (int hb = 0; hb < 2; ++hb) {
-        const int u = tid + TT * hb;
-        stage4_store(sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8)), u);
-      }
-    } else {
-      // round r, thread tid: segment t0 = 8 r + (tid & 7), row a = (tid >> 3) & 15, third c = tid >> 7
-      const int t0l = tid & 7, a4 = (tid >> 3) & 15, c4i = tid >> 7;
-      const int u0 = t0l + 16 * a4 + 256 * c4i;
-      const double2* p0 = sm + slot(t0l, a4, 16 * c4i);
-      stage2_round<1>(sm, tid, cst[0], 0);
-      __syncthreads();
-      c2 = phase ? clock64() : 0;
-      if constexpr (VAR == 1) {
-        stage3_round<1>(sm, tid, cst[1], cst[2], 0);
-        stage2_round<1>(sm, tid, cst[0], 1);
-        __syncthreads();
-        c3 = phase ? clock64() : 0;
-        stage4_store(p0, u0);
-        stage3_round<1>(sm, tid, cst[1], cst[2], 1);
-        __syncthreads();
-      } else {
-        stage3_round<1>(sm, tid, cst[1], cst[2], 0);
-        __syncthreads();
-        stage4_store(p0, u0);
-        stage2_round<1>(sm, tid, cst[0], 1);
-        __syncthreads();
-        c3 = phase ? clock64() : 0;
-        stage3_round<1>(sm, tid, cst[1], cst[2], 1);
-        __syncthreads();
-      }
-      stage4_store(p0 + 8 * S0, u0 + 8);
+    for (int hb = 0; hb < 2; ++hb) {
+      const int u = tid + TT * hb;
+      stage4_store(sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8)), u);
     }
     __syncthreads();
     if (phase && tid == 0) {
@@ -536,69 +467,30 @@ __global__ void __launch_bounds__(TT, 1)
       atomicAdd(phase + 4, 1ULL);
     }
   }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh) : "memory");
 }
 
+// The pairs of up to three axes of one extent in ONE persistent launch (one CTA per SM): the
+// concatenated per-axis work lists are split evenly over the CTAs, each CTA walking a contiguous
+// i-major run (consecutive pairs share the density spectrum held in tensor memory); per axis the
+// kernel-spectrum form (real for mirror-symmetric kernel columns) comes from the device-side flag.
+struct PairAxes12 {
+  const double2* specA[3];
+  const double* specBr[3];
+  const double2* specBc[3];
+  const PairEntry* work[3];
+  const int* winfo[3];
+  double* out[3];
+  const double* U[3];
+  const double* V[3];
+  double h[3];
+  int naxes;
+};
 
-// ---------------------------------------------------------------- pair kernel, bulk-store form
-// Same transform as k12_pair_kernel, with the window leaving through the bulk-copy engine
-// (cp.async.bulk shared -> global) instead of the load/store unit, whose store queue
-// otherwise stalls every other memory instruction of the SM while 262 KB per pair drain
-// at ~32 B/clk:
-//  * after stage 2 the 256 rows (t0, a) of 48 are independent for stages 3-4; round 0 is the
-//    rows a < 8, round 1 the rows a >= 8.  Stage 4 of a round is in place within each warp's
-//    32 butterflies: output (lane, t3) goes to the 16-slot run of butterfly 2 t3 + (lane >> 4)
-//    at position lane & 15, so every run holds 16 consecutive window elements (256 B) and its
-//    lane posts one bulk store per destination column.
-//  * round 0's stores drain under round 1's stages 3-4; round 1's under the next pair's
-//    stage 1: there the thread keeps its mirror block (768 - kk: rows a >= 8) in registers and
-//    stashes its own block (kk < 384: rows a < 8, already drained), and only after the mirror
-//    block's butterfly waits for round 1's bulk reads (one extra CTA barrier).
-//  * requires 16-byte-aligned complex window elements in every output column: the odd
-//    columns' density spectra are formed delayed by one sample (k12_spectrum_kernel shiftA),
-//    which needs an even density rank and a 16-byte-aligned output (host side checks).
-__device__ __forceinline__ void bulk_store(double* dst, const double2* src, uint32_t bytes, uint64_t pol) {
-  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(src));
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(
-                   __cvta_generic_to_global(dst)),
-               "r"(sa), "r"(bytes), "l"(pol)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int K>
-__device__ __forceinline__ void bulk_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(K) : "memory");
-}
-
-// stage 3 over the rows a in [8 r, 8 r + 8) of every segment
-template <int S>
-__device__ __forceinline__ void stage3_rows(double2* sm, int tid, double2 w31, double2 w32, int r) {
-  const int k2 = tid & 15;
-#pragma unroll 2
-  for (int b = tid; b < 2048; b += TT) {
-    const int t1 = 8 * r + ((b >> 4) & 7), t0 = b >> 7;
-    double2* p = sm + slot(t0, t1, k2);
-    double2 v0 = p[0], v1 = p[16], v2 = p[32];
-    dft3<S>(v0, v1, v2);
-    p[0] = v0;
-    p[16] = cmul(v1, w31);
-    p[32] = cmul(v2, w32);
-  }
-}
-
-template <bool BREAL>
 __global__ void __launch_bounds__(TT, 1)
-    k12_pair_kernel_bulk(const double2* __restrict__ specA, const void* __restrict__ specB,
-                         const PairEntry* __restrict__ work, const int* __restrict__ winfo, double* __restrict__ out,
-                         const double* __restrict__ U, int64_t ldu, const double* __restrict__ V, int64_t ldv, double h,
-                         int n, int alias, unsigned long long* __restrict__ phase, int mode) {
-  if ((winfo[1] != 0) != BREAL) return;
-  const int nwork = winfo[0];
+    k12_pair_kernel(PairAxes12 ax, int n, int alias, unsigned long long* __restrict__ phase, int shifted) {
   __shared__ uint32_t tmem_base_sh;
   extern __shared__ double2 sm[];
-  const int tid = threadIdx.x, warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
+  const int tid = threadIdx.x, warp = tid >> 5;
   if (warp == 0) {
     const uint32_t dst = static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base_sh));
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(dst) : "memory");
@@ -609,224 +501,35 @@ __global__ void __launch_bounds__(TT, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tbase = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                          static_cast<uint32_t>((warp >> 2) * 128);
-  uint64_t pol;
-  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  const bool self = tid == TT - 1;
-  const int kk = tid + 1;
-  const double2 wkk = self ? make_double2(1.0, 0.0) : root(kk, M);
+  // per-thread constants: split twiddle base w_m^kk in registers; the stage-2/3
+  // twiddle bases in a per-thread shared-memory table (registers are the limit)
+  const double2 wkk = tid == TT - 1 ? make_double2(1.0, 0.0) : root(tid + 1, M);
   double2* cst = sm + SLOTS + 3 * tid;
   cst[0] = root(tid % 48, 768);
   cst[1] = root(tid & 15, 48);
   cst[2] = cmul(cst[1], cst[1]);
-  const int nf = (n - 1) >> 1;  // n = 2 nf + 1
-  const int kX = self ? 0 : kk, kY = self ? 384 : NB - kk;
-  // stage-4 geometry: warp -> third c, row pair; lane -> segment t0 and row within the pair
-  const int cth = warp >> 2, ap = 2 * (warp & 3);
-  // thread of the butterfly u = (nf % 768) holding window element nf (round (a >> 3))
-  const int ul = nf % NB;
-  const int tid_last = (ul & 15) + 16 * ((ul >> 4) & 1) + 32 * (4 * (ul >> 8) + (((ul >> 4) & 7) >> 1));
-
-  const int w0 = static_cast<int>((static_cast<int64_t>(nwork) * blockIdx.x) / gridDim.x);
-  const int w1 = static_cast<int>((static_cast<int64_t>(nwork) * (blockIdx.x + 1)) / gridDim.x);
-  int ia_cur = -1;
-  for (int w = w0; w < w1; ++w) {
-    const PairEntry e = work[w];
-    const long long c0 = phase ? clock64() : 0;
-    const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
-    const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
-                          : static_cast<const void*>(static_cast<const double2*>(specB) + static_cast<int64_t>(e.jb) * (N + 1));
-    const int sh = e.ia & 1;  // this density column's spectrum is delayed by one sample
-    // alias corrections: result[0] -= h f[n-1] p[n-1], result[n-1] -= h f[0] p[0]
-    double corr0 = 0.0, corr1 = 0.0;
-    if (alias && tid == 0) corr0 = h * __ldg(U + e.ia * ldu + n - 1) * __ldg(V + e.jb * ldv + n - 1);
-    if (alias && tid == tid_last) corr1 = h * __ldg(U + e.ia * ldu) * __ldg(V + e.jb * ldv);
-    if (e.ia != ia_cur) {  // CTA-uniform: a new density column -> tensor memory
-      ia_cur = e.ia;
+  int64_t total = 0;
+  for (int i = 0; i < ax.naxes; ++i) total += ax.winfo[i][0];
+  const int64_t g0 = total * blockIdx.x / gridDim.x, g1 = total * (blockIdx.x + 1) / gridDim.x;
+  int64_t off = 0;
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t r[32];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const int u = 8 * (c & 1) + q;
-          const int ka = item_ka(tid, u);
-          const double2 v = ld2(a + (c < 2 ? ka : N - ka));
-          r[4 * q + 0] = __double2loint(v.x);
-          r[4 * q + 1] = __double2hiint(v.x);
-          r[4 * q + 2] = __double2loint(v.y);
-          r[4 * q + 3] = __double2hiint(v.y);
-        }
-        tmem_st32(tbase + 32 * c, r);
-      }
-      tmem_wait_st();
-    }
-    // ---- stage 1a: products and real split; Z[N - k] (block Y, rows a >= 8) stays in registers in
-    // natural order, Z[k] (block X, rows a < 8: drained) is stashed in its own slots
-    double2 y[16];
-    {
-      const double2 wkh = self ? make_double2(0.99518472667219688624, 0.09801714032956060199) : wkk;  // w_m^384
-#pragma unroll
-      for (int hf = 0; hf < 4; ++hf) {
-        uint32_t ra[16], rb[16];
-        tmem_ld16(tbase + 16 * hf, ra);
-        tmem_ld16(tbase + 64 + 16 * hf, rb);
-        tmem_wait_ld();
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int u = 4 * hf + q;
-          const int ka = item_ka(tid, u);
-          const double2 av = make_double2(__hiloint2double(ra[4 * q + 1], ra[4 * q + 0]),
-                                          __hiloint2double(ra[4 * q + 3], ra[4 * q + 2]));
-          const double2 an = make_double2(__hiloint2double(rb[4 * q + 1], rb[4 * q + 0]),
-                                          __hiloint2double(rb[4 * q + 3], rb[4 * q + 2]));
-          const double2 pk = bmul<BREAL>(av, b, ka), pn = bmul<BREAL>(an, b, N - ka);
-          const double2 wk = cmul(u < 8 ? wkk : wkh, self && u >= 8 ? cs32(u - 8) : cs32(u));
-          double2 zp, zq;
-          zsplit2(pk, pn, wk, zp, zq);
-          if (!self) {
-            sm[slot_kk(u, kX)] = zp;  // Z[kk + 768 u]
-            y[15 - u] = zq;           // Z[N - k] = Z[kY + 768 (15 - u)]
-          } else if (u < 8) {         // block 0: Z[768 u], Z[768 (16 - u)]
-            sm[slot_kk(u, 0)] = zp;
-            if (u > 0) sm[slot_kk(16 - u, 0)] = zq;
-          } else {                    // block 384: Z[384 + 768 (u - 8)], Z[384 + 768 (23 - u)]
-            y[u - 8] = zp;
-            y[23 - u] = zq;
-          }
-        }
-      }
-      if (self) {  // centre of block 0: Z[N/2]
-        const double2 pc = bmul<BREAL>(ld2(a + N / 2), b, N / 2);
-        double2 zc, dummy;
-        zsplit2(pc, pc, make_double2(0.0, 1.0), zc, dummy);  // w_m^{N/2} = i
-        sm[slot_kk(8, 0)] = zc;
-      }
-    }
-    const double2 wX = self ? make_double2(1.0, 0.0) : cmul(wkk, wkk);  // w_N^kk = w_m^{2 kk}
-    // block Y: inputs rotated by one (absorbs e^{2 pi i t/16}); twiddles conj(w_N^{(768 - kY) t})
-    double2 v[16];
-#pragma unroll
-    for (int s = 0; s < 16; ++s) v[s] = y[(s + 15) & 15];
-    dft<16, 1>(v);
-    {
-      const double2 wY = cconj(self ? cs32(1) : wX);  // w_N^{384} = e^{2 pi i / 32}
-      double2 wt = wY;
-#pragma unroll
-      for (int t = 1; t < 16; ++t) {
-        v[t] = cmul(v[t], wt);
-        wt = cmul(wt, wY);
-      }
-    }
-    bulk_wait_read<0>();  // this thread's round-1 stores of the previous pair have left shared memory
-    __syncthreads();
-    const long long c1 = phase ? clock64() : 0;
-    // ---- stage 1b: block Y out, block X from its stash
-#pragma unroll
-    for (int t = 0; t < 16; ++t) sm[slot_kk(t, kY)] = v[t];
-#pragma unroll
-    for (int s = 0; s < 16; ++s) v[s] = sm[slot_kk(s, kX)];
-    dft<16, 1>(v);
-    {
-      double2 wt = wX;
-      sm[slot_kk(0, kX)] = v[0];
-#pragma unroll
-      for (int t = 1; t < 16; ++t) {
-        sm[slot_kk(t, kX)] = cmul(v[t], wt);
-        wt = cmul(wt, wX);
-      }
-    }
-    __syncthreads();
-    const long long c2 = phase ? clock64() : 0;
-    stage2<1>(sm, tid, cst[0]);
-    __syncthreads();
-    const long long c3 = phase ? clock64() : 0;
-    stage3_rows<1>(sm, tid, cst[1], cst[2], 0);
-    __syncthreads();
-    const long long c4 = phase ? clock64() : 0;
-    // ---- stage 4 of a round: radix 16 into registers; once every butterfly of the round has read
-    // its inputs the round's rows are free, and the window elements are staged there as 33 runs
-    // of 128 consecutive elements (2 KB: run q = 11 c + t3 in segment q / 3 at 128 (q % 3)), which
-    // one lane per warp posts as bulk stores
-    double* o0 = out + e.out0 - sh;
-    double* o1 = e.out1 >= 0 ? out + e.out1 - sh : nullptr;
-    const int lo = sh, hi = nf + sh;        // bulk range of window elements; the other end is a scalar
-    const int tsp = sh ? 0 : nf;            // the half element: result[0] = z[0].y / result[n-1] = z[nf].x
-    const int ul = 16 * ap + lane;          // u = ul + 128 r + 256 c
-    const bool lsu0 = (mode & 1) && o1;     // first column through the load/store unit, its twin as bulk stores
-    double2 z[16];
-    auto read4 = [&](int r) {
-      const double2* p = sm + slot(lane & 15, 8 * r + ap + (lane >> 4), 16 * cth);
-#pragma unroll
-      for (int s = 0; s < 16; ++s) z[s] = p[s];
-      dft<16, 1>(z);
-    };
-    auto stage_out = [&](int r) {
-      const int u = ul + 128 * r + 256 * cth;
-      double2* st = sm + 8 * r * 51 + ul;
-#pragma unroll
-      for (int t3 = 0; t3 < 11; ++t3) {     // window elements t = u + 768 t3 <= nf <= 8192
-        const int t = u + NB * t3;
-        if (alias) {
-          if (t == 0) (sh ? z[t3].y : z[t3].x) -= corr0;
-          if (t == nf) (sh ? z[t3].y : z[t3].x) -= corr1;
-        }
-        const int q = 11 * cth + t3;
-        if (t >= lo && t < hi) {
-          st[S0 * (q / 3) + 128 * (q % 3)] = z[t3];
-          if (lsu0) __stcs(reinterpret_cast<double2*>(o0 + 2 * t), z[t3]);
-        }
-        if (t == tsp) {
-          __stcs(o0 + sh + (sh ? 0 : n - 1), sh ? z[t3].y : z[t3].x);
-          if (o1) __stcs(o1 + sh + (sh ? 0 : n - 1), sh ? z[t3].y : z[t3].x);
-        }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    };
-    auto issue = [&](int r) {
-      if (lane == 0) {
-#pragma unroll 1
-        for (int q = warp; q < 33; q += TT / 32) {
-          const int ts = 128 * r + 256 * (q / 11) + NB * (q % 11);
-          const int s0 = max(ts, lo), s1 = min(ts + 128, hi);
-          if (s0 < s1) {
-            const double2* src = sm + 8 * r * 51 + S0 * (q / 3) + 128 * (q % 3) + (s0 - ts);
-            const uint32_t bytes = static_cast<uint32_t>(16 * (s1 - s0));
-            if (!lsu0) bulk_store(o0 + 2 * s0, src, bytes, pol);
-            if (o1) bulk_store(o1 + 2 * s0, src, bytes, pol);
-          }
-        }
-      }
-      bulk_commit();
-    };
-    read4(0);
-    stage3_rows<1>(sm, tid, cst[1], cst[2], 1);
-    __syncthreads();
-    stage_out(0);
-    __syncthreads();
-    const long long c5 = phase ? clock64() : 0;
-    issue(0);
-    read4(1);
-    __syncthreads();
-    stage_out(1);
-    __syncthreads();
-    issue(1);
-    bulk_wait_read<1>();  // round 0's staging rows (a < 8) are free for the next pair's stash
-    __syncthreads();
-    if (phase && tid == 0) {
-      const long long c6 = clock64();
-      atomicAdd(phase + 0, static_cast<unsigned long long>(c1 - c0));
-      atomicAdd(phase + 1, static_cast<unsigned long long>(c2 - c1));
-      atomicAdd(phase + 2, static_cast<unsigned long long>(c3 - c2));
-      atomicAdd(phase + 3, static_cast<unsigned long long>(c4 - c3));
-      atomicAdd(phase + 4, 1ULL);
-      atomicAdd(phase + 5, static_cast<unsigned long long>(c5 - c4));
-      atomicAdd(phase + 6, static_cast<unsigned long long>(c6 - c5));
-    }
+  for (int i = 0; i < ax.naxes; ++i) {
+    const int nw = ax.winfo[i][0];
+    const int w0 = static_cast<int>(max(g0, off) - off), w1 = static_cast<int>(min(g1, off + nw) - off);
+    off += nw;
+    if (w0 >= w1) continue;
+    if (ax.winfo[i][1])
+      k12_pair_run<true>(sm, tbase, ax.specA[i], ax.specBr[i], ax.work[i], w0, w1, ax.out[i], ax.U[i], n, ax.V[i], n,
+                         ax.h[i], n, alias, phase, shifted, wkk);
+    else
+      k12_pair_run<false>(sm, tbase, ax.specA[i], ax.specBc[i], ax.work[i], w0, w1, ax.out[i], ax.U[i], n, ax.V[i], n,
+                          ax.h[i], n, alias, phase, shifted, wkk);
   }
-  bulk_wait_read<0>();
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base_sh) : "memory");
 }
+
 
 // ---------------------------------------------------------------- large n: N = S * 12288 (S = 2..8)
 // Beyond one CTA's shared memory (n > 16385) the length-N transform is split
@@ -1144,9 +847,11 @@ bool k12_applicable(int64_t n, int64_t generic_N) {
 
 bool k12_alias(int64_t n) { return (3 * n - 3) / 2 == k12::M; }
 
-void k12_spectra(tgb_ctx* ctx, int64_t n, const double* A, int nA, double2* specA, const double* B, int nB,
-                 double* specBr, double2* specBc, int modeB, int64_t ldx, double h, bool shiftA) {
-  if (nA + nB == 0) return;
+// spectra of naxes axes of one extent n in one launch (per-axis inputs and spectrum buffers)
+void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int nA, double2* const* specA,
+                 const double* const* B, int nB, double* const* specBr, double2* const* specBc, int modeB,
+                 int64_t ldx, const double* h, bool shiftA) {
+  if (nA + nB == 0 || naxes == 0) return;
   static bool attr[kTgbMaxDevices] = {};
   const size_t smem = k12::kSmem + (64 + k12::M / 64) * sizeof(double2);
   if (!attr[ctx->device]) {
@@ -1154,30 +859,44 @@ void k12_spectra(tgb_ctx* ctx, int64_t n, const double* A, int nA, double2* spec
                                   static_cast<int>(smem)));
     attr[ctx->device] = true;
   }
-  k12::k12_spectrum_kernel<<<nA + nB, k12::TT, smem, ctx->stream>>>(static_cast<int>(n), A, nA, specA, B, nB, specBr,
-                                                                     specBc, modeB, ldx, h, shiftA ? 1 : 0);
+  k12::SpecAxes12 axs{};
+  for (int ax = 0; ax < naxes; ++ax) {
+    axs.XA[ax] = A[ax];
+    axs.XB[ax] = B[ax];
+    axs.specA[ax] = specA[ax];
+    axs.specBr[ax] = specBr[ax];
+    axs.specBc[ax] = specBc[ax];
+    axs.h[ax] = h[ax];
+  }
+  k12::k12_spectrum_kernel<<<dim3(nA + nB, naxes), k12::TT, smem, ctx->stream>>>(static_cast<int>(n), axs, nA, nB,
+                                                                                 modeB, ldx, shiftA ? 1 : 0);
   TGB_LAUNCHED(ctx);
 }
 
 constexpr size_t kPairSmem = k12::kSmem + 3 * k12::TT * sizeof(double2);  // + per-thread twiddle bases
 
-// KIND 0: k12_pair_kernel<BREAL, 0> (load/store-unit window stores, any alignment);
-// KIND 1: k12_pair_kernel_bulk<BREAL> (shifted odd columns, bulk-copy window stores);
-// KIND 2, 3: the two-round A/B schedules of k12_pair_kernel (TGB_K12_VAR, analysis only)
-template <bool BREAL, int KIND>
-static void k12_pairs_t(tgb_ctx* ctx, int64_t n, const double2* specA, const void* specB, const PairEntry* work,
-                        const int* winfo, double* out, const double* U, int64_t ldu, const double* V, int64_t ldv,
-                        double h, bool shifted) {
-  auto kernel = [] {
-    if constexpr (KIND == 1)
-      return k12::k12_pair_kernel_bulk<BREAL>;
-    else
-      return k12::k12_pair_kernel<BREAL, KIND == 0 ? 0 : KIND - 1>;
-  }();
+// pairs of naxes (<= 3) axes of one extent: one launch
+void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double* const* specBr,
+               double2* const* specBc, PairEntry* const* work, const int* winfo0, double* const* out,
+               const double* const* U, const double* const* V, const double* h, bool shifted) {
   static bool attr[kTgbMaxDevices] = {};
   if (!attr[ctx->device]) {
-    TGB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kPairSmem)));
+    TGB_CUDA(cudaFuncSetAttribute(k12::k12_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kPairSmem)));
     attr[ctx->device] = true;
+  }
+  k12::PairAxes12 ax{};
+  ax.naxes = naxes;
+  for (int i = 0; i < naxes; ++i) {
+    ax.specA[i] = specA[i];
+    ax.specBr[i] = specBr[i];
+    ax.specBc[i] = specBc[i];
+    ax.work[i] = work[i];
+    ax.winfo[i] = winfo0 + 2 * i;
+    ax.out[i] = out[i];
+    ax.U[i] = U[i];
+    ax.V[i] = V[i];
+    ax.h[i] = h[i];
   }
   prof_begin(ctx);
   static DevBuf phase_buf;
@@ -1186,59 +905,28 @@ static void k12_pairs_t(tgb_ctx* ctx, int64_t n, const double2* specA, const voi
     phase = static_cast<unsigned long long*>(phase_buf.get(8 * sizeof(unsigned long long)));
     TGB_CUDA(cudaMemsetAsync(phase, 0, 8 * sizeof(unsigned long long), ctx->stream));
   }
-  if constexpr (KIND == 1) {
-    static const int mode = getenv("TGB_K12_MODE") ? atoi(getenv("TGB_K12_MODE")) : 0;
-    kernel<<<ctx->num_sms, k12::TT, kPairSmem, ctx->stream>>>(specA, specB, work, winfo, out, U, ldu, V, ldv, h,
-                                                              static_cast<int>(n), k12_alias(n) ? 1 : 0, phase, mode);
-  } else {
-    kernel<<<ctx->num_sms, k12::TT, kPairSmem, ctx->stream>>>(specA, specB, work, winfo, out, U, ldu, V, ldv, h,
-                                                              static_cast<int>(n), k12_alias(n) ? 1 : 0, phase,
-                                                              shifted ? 1 : 0);
-  }
+  // TGB_K12_NOSTORE: timing probe only (the window stores are skipped, results are wrong)
+  const int smode = shifted ? (getenv("TGB_K12_NOSTORE") ? 3 : 1) : 0;
+  k12::k12_pair_kernel<<<ctx->num_sms, k12::TT, kPairSmem, ctx->stream>>>(ax, static_cast<int>(n),
+                                                                         k12_alias(n) ? 1 : 0, phase, smode);
   TGB_LAUNCHED(ctx);
   prof_end(ctx);
   if (phase) {
     unsigned long long hb[8];
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
     TGB_CUDA(cudaMemcpy(hb, phase, sizeof(hb), cudaMemcpyDeviceToHost));
-    if (hb[4] && KIND == 1)
-      fprintf(stderr, "k12 bulk cycles/pair: stage1a+wait %.0f stage1b %.0f stage2 %.0f stage3r0 %.0f "
-                      "stage4r0+3r1 %.0f stage4r1+wait %.0f (pairs %llu)\n",
-              double(hb[0]) / hb[4], double(hb[1]) / hb[4], double(hb[2]) / hb[4], double(hb[3]) / hb[4],
-              double(hb[5]) / hb[4], double(hb[6]) / hb[4], hb[4]);
-    else if (hb[4])
+    if (hb[4])
       fprintf(stderr, "k12 cycles/pair: stage1 %.0f stage2 %.0f stage3 %.0f stage4 %.0f (pairs %llu)\n",
               double(hb[0]) / hb[4], double(hb[1]) / hb[4], double(hb[2]) / hb[4], double(hb[3]) / hb[4], hb[4]);
   }
 }
 
-// The bulk-store form needs every complex window element 16-byte aligned: odd n, an even
-// density rank, the plain column order and an aligned output; the odd density columns'
-// spectra are then formed delayed by one sample (k12_spectra shiftA).
-bool k12_use_bulk(int64_t n, int64_t ra, const double* out, bool colmap) {
+// Shifted form: every complex window element 16-byte aligned in every output column.  Needs odd
+// n, an even density rank, the plain column order and an aligned output; the odd density
+// columns' spectra are then formed delayed by one sample (k12_spectra shiftA).
+bool k12_use_shift(int64_t n, int64_t ra, const double* out, bool colmap) {
   if (getenv("TGB_K12_NO_SHIFT")) return false;
   return (n & 1) && ra % 2 == 0 && !colmap && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-}
-
-void k12_pairs(tgb_ctx* ctx, int64_t n, const double2* specA, const double* specBr, const double2* specBc,
-               const PairEntry* work, const int* winfo, double* out, const double* U, int64_t ldu, const double* V,
-               int64_t ldv, double h, bool bulk) {
-  // both forms; the one that disagrees with the device-side symmetry flag returns at once
-  static const int var = getenv("TGB_K12_VAR") ? atoi(getenv("TGB_K12_VAR")) : 0;  // A/B: stage schedule
-  static const bool use_bulk_kernel = getenv("TGB_K12_BULK") != nullptr;
-  if (bulk && use_bulk_kernel) {
-    k12_pairs_t<true, 1>(ctx, n, specA, specBr, work, winfo, out, U, ldu, V, ldv, h, bulk);
-    k12_pairs_t<false, 1>(ctx, n, specA, specBc, work, winfo, out, U, ldu, V, ldv, h, bulk);
-  } else if (var == 1) {
-    k12_pairs_t<true, 2>(ctx, n, specA, specBr, work, winfo, out, U, ldu, V, ldv, h, bulk);
-    k12_pairs_t<false, 2>(ctx, n, specA, specBc, work, winfo, out, U, ldu, V, ldv, h, bulk);
-  } else if (var == 2) {
-    k12_pairs_t<true, 3>(ctx, n, specA, specBr, work, winfo, out, U, ldu, V, ldv, h, bulk);
-    k12_pairs_t<false, 3>(ctx, n, specA, specBc, work, winfo, out, U, ldu, V, ldv, h, bulk);
-  } else {
-    k12_pairs_t<true, 0>(ctx, n, specA, specBr, work, winfo, out, U, ldu, V, ldv, h, bulk);
-    k12_pairs_t<false, 0>(ctx, n, specA, specBc, work, winfo, out, U, ldu, V, ldv, h, bulk);
-  }
 }
 
 }  // namespace tgb
