@@ -394,36 +394,36 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
     // aligned; the half element is result[0] = z[0].y (sh) or result[n-1] = z[nf].x
     const int sh = shifted ? (e.ia & 1) : 0;
     const int nf = (n - 1) >> 1;
+    // shifted window stores of one butterfly's outputs v (elements t = u + 768 t3)
+    auto store_shifted = [&](double2* v, int u) {
+      double* q0 = o0 - sh;
+      double* q1 = o1 ? o1 - sh : nullptr;
+      const int lo = sh, hi = nf + sh, tsp = sh ? 0 : nf;
+#pragma unroll
+      for (int t3 = 0; t3 < 11; ++t3) {
+        const int t = u + NB * t3;
+        if (alias) {
+          if (t == 0) (sh ? v[t3].y : v[t3].x) -= corr0;
+          if (t == nf) (sh ? v[t3].y : v[t3].x) -= corr1;
+        }
+        if (t >= lo && t < hi) {
+          if (shifted & 2) {  // timing probe (TGB_K12_NOSTORE): keep the arithmetic live, store nothing
+            if (v[t3].x == 1.2345e300) __stcs(q0, v[t3].y);
+            continue;
+          }
+          __stcs(reinterpret_cast<double2*>(q0 + 2 * t), v[t3]);
+          if (q1) __stcs(reinterpret_cast<double2*>(q1 + 2 * t), v[t3]);
+        } else if (t == tsp) {
+          __stcs(o0 + (sh ? 0 : n - 1), sh ? v[t3].y : v[t3].x);
+          if (o1) __stcs(o1 + (sh ? 0 : n - 1), sh ? v[t3].y : v[t3].x);
+        }
+      }
+    };
     auto stage4_store = [&](const double2* p, int u) {
       double2 v[16];
 #pragma unroll
       for (int s = 0; s < 16; ++s) v[s] = p[s];
       dft<16, 1>(v);
-      if (shifted) {
-        double* q0 = o0 - sh;
-        double* q1 = o1 ? o1 - sh : nullptr;
-        const int lo = sh, hi = nf + sh, tsp = sh ? 0 : nf;
-#pragma unroll
-        for (int t3 = 0; t3 < 11; ++t3) {
-          const int t = u + NB * t3;
-          if (alias) {
-            if (t == 0) (sh ? v[t3].y : v[t3].x) -= corr0;
-            if (t == nf) (sh ? v[t3].y : v[t3].x) -= corr1;
-          }
-          if (t >= lo && t < hi) {
-            if (shifted & 2) {  // timing probe (TGB_K12_NOSTORE): keep the arithmetic live, store nothing
-              if (v[t3].x == 1.2345e300) __stcs(q0, v[t3].y);
-              continue;
-            }
-            __stcs(reinterpret_cast<double2*>(q0 + 2 * t), v[t3]);
-            if (q1) __stcs(reinterpret_cast<double2*>(q1 + 2 * t), v[t3]);
-          } else if (t == tsp) {
-            __stcs(o0 + (sh ? 0 : n - 1), sh ? v[t3].y : v[t3].x);
-            if (o1) __stcs(o1 + (sh ? 0 : n - 1), sh ? v[t3].y : v[t3].x);
-          }
-        }
-        return;
-      }
 #pragma unroll
       for (int t3 = 0; t3 < 16; ++t3) {
         const int t = u + NB * t3;
@@ -452,10 +452,28 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
     stage3<1>(sm, tid, cst[1], cst[2]);
     __syncthreads();
     c3 = phase ? clock64() : 0;
+    if (shifted) {
+      // the second butterfly's inputs are read before the first one's stores enter the load/store
+      // unit (whose queue they would wait behind), and its arithmetic runs while those drain
+      const int ub = tid + TT;
+      const double2* pa = sm + slot(tid & 15, (tid >> 4) & 15, 16 * (tid >> 8));
+      const double2* pb = sm + slot(ub & 15, (ub >> 4) & 15, 16 * (ub >> 8));
+      double2 va[16], vb[16];
+#pragma unroll
+      for (int s = 0; s < 16; ++s) va[s] = pa[s];
+      dft<16, 1>(va);
+#pragma unroll
+      for (int s = 0; s < 16; ++s) vb[s] = pb[s];
+      asm volatile("" ::: "memory");
+      store_shifted(va, tid);
+      dft<16, 1>(vb);
+      store_shifted(vb, ub);
+    } else {
 #pragma unroll 1
-    for (int hb = 0; hb < 2; ++hb) {
-      const int u = tid + TT * hb;
-      stage4_store(sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8)), u);
+      for (int hb = 0; hb < 2; ++hb) {
+        const int u = tid + TT * hb;
+        stage4_store(sm + slot(u & 15, (u >> 4) & 15, 16 * (u >> 8)), u);
+      }
     }
     __syncthreads();
     if (phase && tid == 0) {
