@@ -107,6 +107,41 @@ __device__ __forceinline__ void stage2(double2* sm, int tid, double2 w2base) {
   }
 }
 
+// Pair-kernel form of stage 2: both butterflies' inputs are loaded up front (the second one's
+// shared-memory latency hides under the first one's arithmetic); the twiddles w^t come from a
+// running product instead of a 15-entry table, which is what frees the registers for that.
+template <int S>
+__device__ __forceinline__ void stage2_dual(double2* sm, int tid, double2 w) {
+  const int k1 = tid % 48, t0a = tid / 48;
+  double2* pa = sm + slot(t0a, 0, k1);
+  double2* pb = sm + slot(t0a + 8, 0, k1);
+  double2 va[16], vb[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) va[s] = pa[51 * s];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) vb[s] = pb[51 * s];
+  dft<16, S>(va);
+  {
+    double2 wt = w;
+    pa[0] = va[0];
+#pragma unroll
+    for (int t = 1; t < 16; ++t) {
+      pa[51 * t] = cmul(va[t], wt);
+      wt = cmul(wt, w);
+    }
+  }
+  dft<16, S>(vb);
+  {
+    double2 wt = w;
+    pb[0] = vb[0];
+#pragma unroll
+    for (int t = 1; t < 16; ++t) {
+      pb[51 * t] = cmul(vb[t], wt);
+      wt = cmul(wt, w);
+    }
+  }
+}
+
 template <int S>
 __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double2 w32) {
   const int k2 = tid & 15;
@@ -392,7 +427,7 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
     // shifted: the odd density columns' spectra are delayed by one sample (k12_spectrum_kernel
     // shiftA), so every complex window element (result[2t - sh], result[2t - sh + 1]) is 16-byte
     // aligned; the half element is result[0] = z[0].y (sh) or result[n-1] = z[nf].x
-    const int sh = shifted ? (e.ia & 1) : 0;
+    const int sh = (shifted & 1) ? (e.ia & 1) : 0;
     const int nf = (n - 1) >> 1;
     // shifted window stores of one butterfly's outputs v (elements t = u + 768 t3)
     auto store_shifted = [&](double2* v, int u) {
@@ -446,13 +481,13 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
         }
       }
     };
-    stage2<1>(sm, tid, cst[0]);
+    stage2_dual<1>(sm, tid, cst[0]);
     __syncthreads();
     c2 = phase ? clock64() : 0;
     stage3<1>(sm, tid, cst[1], cst[2]);
     __syncthreads();
     c3 = phase ? clock64() : 0;
-    if (shifted) {
+    if (shifted & 1) {
       // the second butterfly's inputs are read before the first one's stores enter the load/store
       // unit (whose queue they would wait behind), and its arithmetic runs while those drain
       const int ub = tid + TT;
