@@ -306,7 +306,7 @@ def main():
     units_total = 3 * total_f * rb
 
     d_theta = tg.DeviceCP.from_host(theta, device=dev)
-    d_kern = tg.DeviceCP.from_host(kern, device=dev)
+    d_kern = tg.DeviceCP.from_host(kern, device=dev, share_equal_axes=True)  # cubic grid: one kernel factor matrix
     d_out = tg.DeviceCP.empty([n, n, n], ra * rb, device=dev)
     h = case.grid.h
     if not strong:

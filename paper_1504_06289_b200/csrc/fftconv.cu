@@ -2586,8 +2586,14 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
           Ab[i] = A[ax + i];
           Bb[i] = B[ax + i];
           sAb[i] = k12_specA[i] = reinterpret_cast<double2*>(sa + i * a_bytes);
-          sBr[i] = k12_specBr[i] = reinterpret_cast<double*>(sbb + i * b_bytes);
-          sBc[i] = k12_specBc[i] = reinterpret_cast<double2*>(sbb + i * b_bytes + real_bytes);
+          int src = i;  // an axis given the same kernel factor matrix and step as an earlier one shares its spectra
+          for (int j = 0; j < i; ++j)
+            if (B[ax + j] == B[ax + i] && h[ax + j] == h[ax + i]) {
+              src = j;
+              break;
+            }
+          sBr[i] = k12_specBr[i] = reinterpret_cast<double*>(sbb + src * b_bytes);
+          sBc[i] = k12_specBc[i] = reinterpret_cast<double2*>(sbb + src * b_bytes + real_bytes);
         }
         k12_spectra(ctx, n[ax], nb, Ab, static_cast<int>(ra), sAb, Bb, static_cast<int>(rb), sBr, sBc, 3, n[ax],
                     h + ax, k12_shift);

@@ -172,10 +172,12 @@ struct SpecAxes12 {
   double* specBr[3];
   double2* specBc[3];
   double h[3];
+  int bsrc[3];  // axis whose kernel spectra this axis shares (the same factor matrix and h), else itself
 };
 
 __global__ void __launch_bounds__(TT, 1)
     k12_spectrum_kernel(int n, SpecAxes12 axs, int nA, int nB, int modeB, int64_t ldx, int shiftA) {
+  if (static_cast<int>(blockIdx.x) < nB && axs.bsrc[blockIdx.y] != static_cast<int>(blockIdx.y)) return;
   const double* __restrict__ XA = axs.XA[blockIdx.y];
   const double* __restrict__ XB = axs.XB[blockIdx.y];
   double2* __restrict__ specA = axs.specA[blockIdx.y];
@@ -920,6 +922,12 @@ void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int
     axs.specBr[ax] = specBr[ax];
     axs.specBc[ax] = specBc[ax];
     axs.h[ax] = h[ax];
+    axs.bsrc[ax] = ax;
+    for (int j = 0; j < ax; ++j)
+      if (specBr[j] == specBr[ax]) {  // the caller pointed this axis at an earlier axis's kernel spectra
+        axs.bsrc[ax] = j;
+        break;
+      }
   }
   k12::k12_spectrum_kernel<<<dim3(nA + nB, naxes), k12::TT, smem, ctx->stream>>>(static_cast<int>(n), axs, nA, nB,
                                                                                  modeB, ldx, shiftA ? 1 : 0);

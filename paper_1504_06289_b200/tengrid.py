@@ -176,10 +176,17 @@ class DeviceCP:
         self.weight = weight
 
     @staticmethod
-    def from_host(t: CanonicalTensor3, device="cuda") -> "DeviceCP":
+    def from_host(t: CanonicalTensor3, device="cuda", share_equal_axes: bool = False) -> "DeviceCP":
+        """share_equal_axes: axes whose factor matrices are bitwise equal (the Newton kernel on a
+        cubic grid) share ONE device matrix; libtgb then forms that matrix's spectra once.  Only for
+        tensors that are not modified in place afterwards."""
         import torch
 
-        f = [torch.from_numpy(np.ascontiguousarray(x.T)).to(device) for x in t.factor]
+        f = []
+        for ax, x in enumerate(t.factor):
+            src = next((j for j in range(ax) if share_equal_axes and t.factor[j].shape == x.shape
+                        and np.array_equal(t.factor[j], x)), None)
+            f.append(f[src] if src is not None else torch.from_numpy(np.ascontiguousarray(x.T)).to(device))
         return DeviceCP(f, torch.from_numpy(t.weight.copy()).to(device))
 
     @staticmethod

@@ -176,6 +176,24 @@ def test_hartree_device_resident_matches_host(ctx):
     assert relmax(got, value_at_points(host, case.samples[:500], ctx)) <= 1e-13
 
 
+def test_k12_shared_kernel_axes_bitwise(ctx):
+    """Config-2 extent: the Newton kernel's three factor matrices are bitwise equal on a cubic
+    grid; given as ONE device matrix (DeviceCP.from_host share_equal_axes) libtgb forms its
+    spectra once (fftconv12k.cu k12_spectrum_kernel bsrc) - the result must not change by a bit.
+    Even density rank (shifted odd columns) and odd rank (unshifted stores) both."""
+    for rank in (6, 5):
+        case = hartree_case(2, rank=rank, nsamples=1)
+        dt = DeviceCP.from_host(case.theta)
+        sep = hartree_potential(dt, DeviceCP.from_host(case.kernel.tensor), case.grid.h, ctx)
+        dks = DeviceCP.from_host(case.kernel.tensor, share_equal_axes=True)
+        assert dks.factor[1] is dks.factor[0] and dks.factor[2] is dks.factor[0]
+        shared = hartree_potential(dt, dks, case.grid.h, ctx)
+        ctx.synchronize()
+        a, b = sep.to_host(), shared.to_host()
+        for ax in range(3):
+            assert np.array_equal(a.factor[ax], b.factor[ax])
+
+
 def test_hartree_config2_columns(ctx):
     # n = 16385 (config 2 extent) with a slice of the density: every kernel
     # column, a few density columns, all three axes against the oracle.

@@ -11,7 +11,7 @@ from paper_1504_06289_b200.inputs import hartree_case
 case = hartree_case(2, rank=500, nsamples=1)
 stream = torch.cuda.Stream()
 ctx = tg.Context(0, stream=stream.cuda_stream)
-dk = tg.DeviceCP.from_host(case.kernel.tensor)
+dk = tg.DeviceCP.from_host(case.kernel.tensor, share_equal_axes=True)
 res = {}
 for world, cols in ((1, 500), (2, 250), (4, 125), (8, 63), (8, 62)):
     th = tg.CanonicalTensor3([f[:, :cols] for f in case.theta.factor], case.theta.weight[:cols])
