@@ -145,7 +145,7 @@ __device__ __forceinline__ void stage2_dual(double2* sm, int tid, double2 w) {
 template <int S>
 __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double2 w32) {
   const int k2 = tid & 15;
-#pragma unroll 2
+#pragma unroll 4
   for (int b = tid; b < 4096; b += TT) {
     const int t1 = (b >> 4) & 15, t0 = b >> 8;
     double2* p = sm + slot(t0, t1, k2);
