@@ -3,6 +3,7 @@
 // class; host-memory calls stage through the context workspace with
 // per-axis copy/compute overlap.
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <algorithm>
 #include <array>
@@ -128,6 +129,13 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
         }
     }
   }
+  // D2H piece size: small enough that the replication reads a piece while the DMA's lines are
+  // still cached, large enough for the copy engine (tools/probe/e2e_chunk_probe.cu: 4-8 MB)
+  static const size_t piece = [] {
+    const char* e = getenv("TGB_E2E_PIECE_KB");
+    return static_cast<size_t>(e ? std::max(64, atoi(e)) : 4096) << 10;
+  }();
+  size_t nev = 3;  // events 0..2: per-axis "convolved"; then one per D2H piece in issue order
   bool pinned[3];
   for (int ax = 0; ax < 3; ++ax) {
     pinned[ax] = !tgb::is_pageable(out->factor[ax]);
@@ -138,13 +146,18 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
     TGB_CUDA(cudaEventRecord(ev, ctx->stream));
     TGB_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ev, 0));
     const size_t blk = static_cast<size_t>(a->n[ax]) * ra;  // doubles per kernel-column block
-    if (pinned[ax]) {  // one event per representative block: its twins are copied as soon as it lands
+    if (pinned[ax]) {  // representative blocks leave in pieces, one event each: the twins are filled piece by piece
       for (int64_t j = 0; j < rb; ++j)
         if (rep[ax][j] == j) {
-          TGB_CUDA(cudaMemcpyAsync(out->factor[ax] + blk * j, dout_ax[ax] + blk * j, blk * sizeof(double),
-                                   cudaMemcpyDeviceToHost, ctx->copy_stream));
-          TGB_CUDA(cudaEventRecord(ctx_event(ctx, 3 + ax * rb + j), ctx->copy_stream));
-          ctx->bytes_d2h += static_cast<int64_t>(blk * sizeof(double));
+          const size_t bytes = blk * sizeof(double);
+          for (size_t o = 0; o < bytes; o += piece) {
+            const size_t len = std::min(piece, bytes - o);
+            TGB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(out->factor[ax] + blk * j) + o,
+                                     reinterpret_cast<const char*>(dout_ax[ax] + blk * j) + o, len,
+                                     cudaMemcpyDeviceToHost, ctx->copy_stream));
+            TGB_CUDA(cudaEventRecord(ctx_event(ctx, nev++), ctx->copy_stream));
+          }
+          ctx->bytes_d2h += static_cast<int64_t>(bytes);
         }
     }
   }
@@ -154,6 +167,8 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
   auto since = [](std::chrono::steady_clock::time_point t) {
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
   };
+  size_t iev = 3;
+  bool spinning = false;
   for (int ax = 0; ax < 3; ++ax) {
     const size_t blk = static_cast<size_t>(a->n[ax]) * ra;
     if (!pinned[ax]) {  // staged copy of the whole factor (pageable destination)
@@ -161,18 +176,34 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
       tgb::d2h(ctx, out->factor[ax], dout_ax[ax], blk * rb * sizeof(double), ctx->copy_stream);
       continue;
     }
+    if (!spinning) {
+      tgb::stream_copy_begin();
+      spinning = true;
+    }
     for (int64_t j = 0; j < rb; ++j) {
       if (rep[ax][j] != j) continue;
-      auto tw = std::chrono::steady_clock::now();
-      TGB_CUDA(cudaEventSynchronize(ctx_event(ctx, 3 + ax * rb + j)));
-      t_wait += since(tw);
-      tw = std::chrono::steady_clock::now();
-      for (int64_t jt = j + 1; jt < rb; ++jt)
-        if (rep[ax][jt] == j)
-          tgb::par_memcpy(out->factor[ax] + blk * jt, out->factor[ax] + blk * j, blk * sizeof(double));
-      t_copy += since(tw);
+      const size_t bytes = blk * sizeof(double);
+      for (size_t o = 0; o < bytes; o += piece) {
+        const size_t len = std::min(piece, bytes - o);
+        auto tw = std::chrono::steady_clock::now();
+        cudaError_t st;
+        while ((st = cudaEventQuery(ctx_event(ctx, iev))) == cudaErrorNotReady) _mm_pause();
+        ++iev;
+        if (st != cudaSuccess) {
+          tgb::stream_copy_end();
+          TGB_CUDA(st);
+        }
+        t_wait += since(tw);
+        tw = std::chrono::steady_clock::now();
+        for (int64_t jt = j + 1; jt < rb; ++jt)
+          if (rep[ax][jt] == j)
+            tgb::stream_copy(reinterpret_cast<char*>(out->factor[ax] + blk * jt) + o,
+                             reinterpret_cast<const char*>(out->factor[ax] + blk * j) + o, len);
+        t_copy += since(tw);
+      }
     }
   }
+  if (spinning) tgb::stream_copy_end();
   TGB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   TGB_CUDA(cudaStreamSynchronize(ctx->stream));
   if (trace)

@@ -7,8 +7,10 @@
 // single-threaded pageable path (~6 GB/s measured on the bench host for the
 // 630 MB density of config 1).
 #include <cuda_runtime.h>
+#include <emmintrin.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <mutex>
@@ -120,6 +122,122 @@ class CopyPool {
 };
 
 void par_memcpy(void* dst, const void* src, size_t bytes) { CopyPool::get().copy(dst, src, bytes); }
+
+// ---- streaming replication of D2H pieces (the bitwise-twin output blocks of the host-memory
+// convolve).  Pieces of a few MB are replicated the moment their DMA lands, by all threads at
+// once: the threads spin between pieces (a condition-variable wake-up costs more than a piece)
+// and write with non-temporal stores (no read-for-ownership of the destination lines).
+// Measured on the bench host (tools/probe/e2e_chunk_probe.cu): 4 GB D2H + 4 GB replicated takes
+// 113-119 ms with memcpy on 65 MB blocks, 91-98 ms with 4-8 MB pieces and non-temporal stores.
+namespace {
+
+void nt_copy(char* dst, const char* src, size_t n) {
+  size_t i = 0;
+  while (i < n && (reinterpret_cast<uintptr_t>(dst + i) & 15)) {
+    dst[i] = src[i];
+    ++i;
+  }
+  for (; i + 64 <= n; i += 64) {
+    const __m128i a = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i));
+    const __m128i b = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 16));
+    const __m128i c = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 32));
+    const __m128i d = _mm_loadu_si128(reinterpret_cast<const __m128i*>(src + i + 48));
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i), a);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 16), b);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 32), c);
+    _mm_stream_si128(reinterpret_cast<__m128i*>(dst + i + 48), d);
+  }
+  for (; i < n; ++i) dst[i] = src[i];
+  _mm_sfence();
+}
+
+class SpinCopyPool {
+ public:
+  static SpinCopyPool& get() {
+    static SpinCopyPool pool;
+    return pool;
+  }
+  // between begin() and end() the workers spin; one user at a time
+  void begin() {
+    user_.lock();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      active_ = true;
+    }
+    cv_.notify_all();
+  }
+  void end() {
+    active_.store(false, std::memory_order_release);
+    user_.unlock();
+  }
+  void copy(void* dst, const void* src, size_t bytes) {
+    dst_ = static_cast<char*>(dst);
+    src_ = static_cast<const char*>(src);
+    bytes_ = bytes;
+    done_.store(0, std::memory_order_relaxed);
+    gen_.fetch_add(1, std::memory_order_release);
+    part(0);
+    while (done_.load(std::memory_order_acquire) != nt_ - 1) _mm_pause();
+  }
+
+ private:
+  SpinCopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    nt_ = static_cast<int>(std::min(hw, 16u));
+    if (const char* e = getenv("TGB_COPY_THREADS")) nt_ = std::max(1, std::min(64, atoi(e)));
+    for (int t = 1; t < nt_; ++t) workers_.emplace_back([this, t] { loop(t); });
+  }
+  ~SpinCopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& w : workers_) w.join();
+  }
+  void part(int t) {
+    const size_t lo = (bytes_ * t / nt_) & ~size_t(63);
+    const size_t hi = t + 1 == nt_ ? bytes_ : (bytes_ * (t + 1) / nt_) & ~size_t(63);
+    if (lo < hi) nt_copy(dst_ + lo, src_ + lo, hi - lo);
+  }
+  void loop(int t) {
+    uint64_t seen = 0;  // every copy posted since construction is this thread's to join, however late it starts
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return stop_ || active_.load(std::memory_order_acquire); });
+        if (stop_) return;
+      }
+      while (active_.load(std::memory_order_acquire)) {
+        const uint64_t g = gen_.load(std::memory_order_acquire);
+        if (g == seen) {
+          _mm_pause();
+          continue;
+        }
+        seen = g;
+        part(t);
+        done_.fetch_add(1, std::memory_order_release);
+      }
+    }
+  }
+  int nt_ = 1;
+  std::vector<std::thread> workers_;
+  std::mutex mu_, user_;
+  std::condition_variable cv_;
+  std::atomic<bool> active_{false};
+  bool stop_ = false;
+  std::atomic<uint64_t> gen_{0};
+  std::atomic<int> done_{0};
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+}  // namespace
+
+void stream_copy_begin() { SpinCopyPool::get().begin(); }
+void stream_copy(void* dst, const void* src, size_t bytes) { SpinCopyPool::get().copy(dst, src, bytes); }
+void stream_copy_end() { SpinCopyPool::get().end(); }
 
 namespace {
 

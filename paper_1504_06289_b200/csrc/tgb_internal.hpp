@@ -82,6 +82,10 @@ void h2d(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st
 void d2h(tgb_ctx* ctx, void* dst, const void* src, size_t bytes, cudaStream_t stream);
 bool is_pageable(const void* p);
 void par_memcpy(void* dst, const void* src, size_t bytes);  // host threads
+// replication of freshly landed D2H pieces: spinning threads, non-temporal stores (hostcopy.cpp)
+void stream_copy_begin();
+void stream_copy(void* dst, const void* src, size_t bytes);
+void stream_copy_end();
 void scratch_free(tgb_ctx* ctx, void* p, size_t bytes);
 
 // Run f, mapping exceptions to the C-ABI return codes (tgb.h).
