@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(TT, 1)
     for (int t = 0; t < 16; ++t) sm[slot_kk(t, tt)] = t ? cmul(v[t], wp[t]) : v[t];
   }
   __syncthreads();
-  stage2<-1>(sm, tid, cconj(root(tid % 48, 768)));
+  stage2_dual<-1>(sm, tid, cconj(root(tid % 48, 768)));
   __syncthreads();
   {
     const double2 w31 = cconj(root(tid & 15, 48));
@@ -250,6 +250,24 @@ __global__ void __launch_bounds__(TT, 1)
   const double hm = h / M;
   const int64_t base = static_cast<int64_t>(c) * (N + 1);
   const int64_t ofs = (n - 1) / 2;
+  if (!isB) {
+    // density columns: X[k] and X[N-k] from one pair (Z_k, Z_{N-k}) and one twiddle:
+    // w^-(N-k) (Z_{N-k} - conj Z_k) = conj(w^-k (Z_k - conj Z_{N-k}))
+    for (int k = tid; k <= N / 2; k += TT) {
+      const int kb = k == 0 ? 0 : N - k;  // Z_N = Z_0
+      const double2 zk = sm[k + (k >> 4)];
+      double2 zm = sm[kb + (kb >> 4)];
+      zm.y = -zm.y;
+      const double2 sum = cadd(zk, zm), dif = csub(zk, zm);
+      const double2 wd = cmul(cmul(zlo[k & 63], zhi[k >> 6]), dif);
+      double2 X = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
+      double2 Y = make_double2(0.5 * (sum.x - wd.y), -0.5 * (sum.y + wd.x));
+      if (k == 0) X.y = Y.y = 0.0;  // DC and Nyquist of a real signal
+      specA[base + k] = X;
+      if (2 * k != N) specA[base + N - k] = Y;
+    }
+    return;
+  }
   for (int k = tid; k <= N; k += TT) {
     const int ka = k == N ? 0 : k, kb = ka == 0 ? 0 : N - ka;  // Z_N = Z_0
     const double2 zk = sm[ka + (ka >> 4)];
