@@ -116,7 +116,9 @@ int tgb_conv_central_many(tgb_ctx* ctx, int64_t n, int64_t cols, const double* U
 
 /* replaces tg::convolve(a, b, h) (tensor.hpp:185-186, tensor.cpp:179-198).
  * `out` must have rank a.rank * b.rank; column i + a.rank * j of every factor
- * is h[ax] * conv_central(a_i, b_j); weight = a.w[i] * b.w[j]. */
+ * is h[ax] * conv_central(a_i, b_j); weight = a.w[i] * b.w[j].
+ * Device memory: axes of b that point at the SAME factor matrix (the Newton kernel on a cubic
+ * grid) with the same h share one set of kernel spectra. */
 int tgb_convolve(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double h[3], tgb_cp* out, int mem);
 
 /* replaces tg::hartree_potential (hf.hpp:34-39, hf.cpp:131-138):
