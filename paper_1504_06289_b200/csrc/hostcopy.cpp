@@ -8,6 +8,7 @@
 // 630 MB density of config 1).
 #include <cuda_runtime.h>
 #include <emmintrin.h>
+#include <sched.h>
 
 #include <algorithm>
 #include <atomic>
@@ -177,12 +178,23 @@ class SpinCopyPool {
     done_.store(0, std::memory_order_relaxed);
     gen_.fetch_add(1, std::memory_order_release);
     part(0);
-    while (done_.load(std::memory_order_acquire) != nt_ - 1) _mm_pause();
+    unsigned idle = 0;
+    while (done_.load(std::memory_order_acquire) != nt_ - 1) {
+      if (++idle > 4096) {
+        std::this_thread::yield();
+        idle = 0;
+      } else {
+        _mm_pause();
+      }
+    }
   }
 
  private:
   SpinCopyPool() {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    // spinning threads must each own a core: count the CPUs this process may run on
+    unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) hw = std::max(1, std::min<int>(hw, CPU_COUNT(&set)));
     nt_ = static_cast<int>(std::min(hw, 16u));
     if (const char* e = getenv("TGB_COPY_THREADS")) nt_ = std::max(1, std::min(64, atoi(e)));
     for (int t = 1; t < nt_; ++t) workers_.emplace_back([this, t] { loop(t); });
@@ -202,6 +214,7 @@ class SpinCopyPool {
   }
   void loop(int t) {
     uint64_t seen = 0;  // every copy posted since construction is this thread's to join, however late it starts
+    unsigned idle = 0;
     for (;;) {
       {
         std::unique_lock<std::mutex> lk(mu_);
@@ -211,9 +224,15 @@ class SpinCopyPool {
       while (active_.load(std::memory_order_acquire)) {
         const uint64_t g = gen_.load(std::memory_order_acquire);
         if (g == seen) {
-          _mm_pause();
+          if (++idle > 4096) {  // a long gap (the next piece is still in flight): let others run
+            std::this_thread::yield();
+            idle = 0;
+          } else {
+            _mm_pause();
+          }
           continue;
         }
+        idle = 0;
         seen = g;
         part(t);
         done_.fetch_add(1, std::memory_order_release);
