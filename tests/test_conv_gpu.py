@@ -336,6 +336,49 @@ def test_host_path_pinned_twin_replication(ctx):
     assert np.array_equal(oh.weight, ref.weight)
 
 
+def test_host_path_pinned_pieces_and_mixed_extents(ctx):
+    """Host-memory convolve into PINNED outputs at the config-2 extent: a representative block
+    (n * ra * 8 = 5.2 MB) leaves the device in 4 MB pieces (capi.cpp) and each piece's twin is
+    written as it lands (hostcopy.cpp SpinCopyPool, non-temporal stores) - bit-identical to the
+    pageable path's whole-factor copy.  Extents (16385, 16385, 16383): device-resident, the
+    first two axes share one spectrum launch and one pair launch of the N = 12288 plan and the
+    third runs alone; the host path convolves axis by axis - the same bits either way."""
+    import torch
+
+    dims = (16385, 16385, 16383)
+    ra = 40
+    rng = Rng(777)
+    a = CanonicalTensor3([np.asfortranarray(rng.normal(d * ra).reshape(d, ra, order="F")) for d in dims],
+                         rng.normal(ra))
+    fb = []
+    for d in dims:
+        x = np.arange(d) - 0.5 * (d - 1)
+        g = np.exp(-(x / 700.0) ** 2)
+        fb.append(np.asfortranarray(np.stack([g, np.exp(-(x / 200.0) ** 2), g.copy()], axis=1)))  # columns 0 and 2: twins
+    b = CanonicalTensor3(fb, np.ones(3))
+    h = (0.011, 0.013, 0.017)
+    ref = convolve(a, b, h, ctx)  # pageable output
+    oh = CanonicalTensor3([torch.empty((ra * 3, d), dtype=torch.float64).pin_memory().numpy().T for d in dims],
+                          np.zeros(ra * 3))
+    for f in oh.factor:
+        f[:] = np.nan
+    ctx.transfer_bytes()
+    convolve(a, b, h, ctx, out=oh)
+    _, d2h = ctx.transfer_bytes()
+    assert d2h == sum(d * ra * 2 * 8 for d in dims)  # two distinct kernel columns per axis cross PCIe
+    for ax, d in enumerate(dims):
+        assert np.array_equal(oh.factor[ax], ref.factor[ax])
+        assert np.array_equal(oh.factor[ax][:, :ra], oh.factor[ax][:, 2 * ra:])
+        for i, j in ((0, 0), (1, 1), (ra - 1, 2)):
+            want = O.conv_central_many(np.asfortranarray(a.factor[ax][:, [i]]), np.ascontiguousarray(fb[ax][:, j]))[:, 0]
+            assert relmax(oh.factor[ax][:, i + ra * j], h[ax] * want) <= TOL, (ax, i, j)
+    dv = convolve(DeviceCP.from_host(a), DeviceCP.from_host(b), h, ctx)
+    ctx.synchronize()
+    back = dv.to_host()
+    for ax in range(3):
+        assert np.array_equal(back.factor[ax], ref.factor[ax])
+
+
 def _grouping_case(rng, n, sym):
     """Kernel-side tensor whose columns form groups of bitwise-identical columns
     {1, 5, 7}, {2, 6} and singletons (optionally all mirror-symmetric)."""
