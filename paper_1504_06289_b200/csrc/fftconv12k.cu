@@ -28,6 +28,20 @@
 //  * Shared memory: 16 segments (t0) of 817 slots (16 rows of 51: 48 data +
 //    3 pad, then 1 pad) = 209 KB; every stage's accesses are bank-conflict
 //    free within a quarter warp (see slot()).
+//  * One spectrum launch and ONE persistent pair launch serve every axis of
+//    this extent (k12_spectra / k12_pairs take up to three axes): the axes'
+//    work lists are concatenated and split evenly over the CTAs, and each axis
+//    picks its kernel-spectrum form on the device.
+//  * Window stores: n is odd, so the odd output columns sit 8 bytes off a
+//    16-byte boundary.  With an even density rank and an aligned output the
+//    odd density columns' spectra are formed delayed by one sample (shiftA),
+//    which makes every complex window element of every column one 16-byte
+//    store; other shapes keep 8-byte stores on the odd columns.
+//  * The load/store unit is in order and a window store waits for the SM's
+//    32 B/clk egress, so each stage issues its shared-memory loads before its
+//    stores (two butterflies in flight in stages 2 and 4, four in stage 3).
+//    profiles/r02_ncu_k12_final.txt has the per-stage cycles and the variants
+//    that were measured and dropped (bulk-copy stores, two-round schedules).
 #include <cuda_runtime.h>
 
 #include <cmath>
