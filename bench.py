@@ -272,6 +272,12 @@ def main():
         run_reference_arm(args, rank, world)
         return
 
+    # one process per GPU on one host: libtgb's host copy threads (host-memory calls) spin while a
+    # call runs, so the ranks share the cores instead of each taking all of them
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    if local_world > 1:
+        os.environ.setdefault("TGB_COPY_THREADS", str(max(1, (os.cpu_count() or 1) // local_world)))
+
     import torch
     import torch.distributed as dist
 
