@@ -162,27 +162,30 @@ int tgb_expsum_for_interval(double r_min, double r_max, double eps, int64_t m_ca
       build(m, c0);
       return max_rel(300);
     };
+    // golden-section search of log c0 on [log 0.15, log 12] (22 shrinks, kernel.cpp:141-161); the
+    // bracket and its two interior probes are updated with the reference's expressions, so c0
+    // comes out bit-identical
+    struct Probe {
+      double x, err;
+    };
     auto best_c0 = [&](int64_t m) {
-      const double phi = 0.5 * (std::sqrt(5.0) - 1.0);
-      double lo = std::log(0.15), hi = std::log(12.0);
-      double x1 = hi - phi * (hi - lo), x2 = lo + phi * (hi - lo);
-      double f1 = measured(m, std::exp(x1)), f2 = measured(m, std::exp(x2));
-      for (int it = 0; it < 22; ++it) {
-        if (f1 <= f2) {
-          hi = x2;
-          x2 = x1;
-          f2 = f1;
-          x1 = hi - phi * (hi - lo);
-          f1 = measured(m, std::exp(x1));
+      const double ratio = 0.5 * (std::sqrt(5.0) - 1.0);
+      auto probe = [&](double x) { return Probe{x, measured(m, std::exp(x))}; };
+      double left = std::log(0.15), right = std::log(12.0);
+      Probe near = probe(right - ratio * (right - left));  // interior point closer to `left`
+      Probe far = probe(left + ratio * (right - left));
+      for (int shrink = 0; shrink < 22; ++shrink) {
+        if (near.err <= far.err) {  // the minimum is left of `far`
+          right = far.x;
+          far = near;
+          near = probe(right - ratio * (right - left));
         } else {
-          lo = x1;
-          x1 = x2;
-          f1 = f2;
-          x2 = lo + phi * (hi - lo);
-          f2 = measured(m, std::exp(x2));
+          left = near.x;
+          near = far;
+          far = probe(left + ratio * (right - left));
         }
       }
-      return std::exp(0.5 * (lo + hi));
+      return std::exp(0.5 * (left + right));
     };
     const double l = std::log(1.0 / std::min(eps * 1e3, 0.5));
     tgb::require(std::min(eps * 1e3, 0.5) > 0.0 && std::min(eps * 1e3, 0.5) < 1.0,
@@ -221,38 +224,44 @@ int tgb_reciprocal_expsum(double lo, double hi, double eps, int64_t term_cap, in
       *ok = 1;
       return;
     }
+    // scaled problem 1/x on [1, q]; quadrature nodes u_j = u_min + j * mesh over [u_min, u_max]
     const double q = hi / lo;
     const double u_min = std::log(eps / (6.0 * q));
     const double u_max = std::log(std::log(6.0 * q / eps)) + 1.0;
-    std::vector<double> r, w;
-    for (double mesh = 2.0 * kPi / (std::log(1.0 / eps) + 6.0);; mesh *= 0.8) {
-      const int64_t n = static_cast<int64_t>(std::ceil((u_max - u_min) / mesh)) + 1;
-      if (n > term_cap) return;
-      r.assign(n, 0.0);
-      w.assign(n, 0.0);
-      for (int64_t j = 0; j < n; ++j) {
-        const double u = u_min + static_cast<double>(j) * mesh;
-        r[j] = std::exp(u);
-        w[j] = mesh * std::exp(u);
-      }
+    std::vector<double> rate, wt;
+    auto worst_error = [&](int64_t n) {  // max relative error at 1000 log-spaced points of [1, q]
       double worst = 0.0;
-      const int samples = 1000;
-      for (int i = 0; i < samples; ++i) {
-        const double x = std::pow(q, static_cast<double>(i) / (samples - 1));
+      for (int i = 0; i < 1000; ++i) {
+        const double x = std::pow(q, static_cast<double>(i) / 999);
         double sum = 0.0;
-        for (int64_t j = 0; j < n; ++j) sum += w[j] * std::exp(-r[j] * x);
+        for (int64_t j = 0; j < n; ++j) sum += wt[j] * std::exp(-rate[j] * x);
         worst = std::max(worst, std::abs(sum - 1.0 / x) * x);
       }
+      return worst;
+    };
+    double mesh = 2.0 * kPi / (std::log(1.0 / eps) + 6.0);
+    for (;;) {
+      const int64_t n = static_cast<int64_t>(std::ceil((u_max - u_min) / mesh)) + 1;
+      if (n > term_cap) return;  // *ok stays 0
+      rate.resize(n);
+      wt.resize(n);
+      for (int64_t j = 0; j < n; ++j) {
+        const double e = std::exp(u_min + static_cast<double>(j) * mesh);
+        rate[j] = e;
+        wt[j] = mesh * e;
+      }
+      const double worst = worst_error(n);
       if (worst <= eps) {
-        for (int64_t j = 0; j < n; ++j) {
-          rates[j] = r[j] / lo;
-          weights[j] = w[j] / lo;
+        for (int64_t j = 0; j < n; ++j) {  // back to [lo, hi]
+          rates[j] = rate[j] / lo;
+          weights[j] = wt[j] / lo;
         }
         *terms = n;
         *achieved = worst;
         *ok = 1;
         return;
       }
+      mesh *= 0.8;
     }
   });
 }
