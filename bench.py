@@ -402,6 +402,10 @@ def main():
     N = m // 2
     flops_pair = 5.0 * N * np.log2(N) + 16.0 * N  # complex FFT + split + product (nominal)
     fp64_tflops = axes_per_launch * ra * nd * flops_pair / (avg_launch_ms / 1e3) / 1e12
+    try:  # FP64 issue rate of this box, measured now (libtgb's DFMA probe)
+        fp64_peak, fp64_peak_kind = ctx.probe_fp64_peak(), "measured in this run (tgb_probe_fp64_peak, DFMA chains)"
+    except Exception:
+        fp64_peak, fp64_peak_kind = FP64_TFLOPS, "fallback: profiles/r01_box_probe.txt"
 
     # ---- e2e through the C-ABI with pinned HOST buffers (copies inside the timed region)
     e2e = None
@@ -469,8 +473,8 @@ def main():
                      "axes_per_launch": axes_per_launch,
                      "bytes_per_launch": bytes_launch, "avg_launch_ms": avg_launch_ms,
                      "launch_share_of_step": pair_ms / ms_local if ms_local else None,
-                     "fp64": {"achieved_tflops_nominal": fp64_tflops, "peak_tflops": FP64_TFLOPS,
-                              "frac": fp64_tflops / FP64_TFLOPS,
+                     "fp64": {"achieved_tflops_nominal": fp64_tflops, "peak_tflops": fp64_peak,
+                              "peak_kind": fp64_peak_kind, "frac": fp64_tflops / fp64_peak,
                               "note": "nominal 5 N log2 N + 16 N flops per inverse transform, N = 12288"}},
         "gpu_launches": int(launches),
         "clocks": clk,

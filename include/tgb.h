@@ -400,6 +400,9 @@ int tgb_pivoted_cholesky(tgb_ctx* ctx, int64_t n, const double* A, double tol, i
  * it; exported for tests and callers that hold device matrices. */
 int tgb_dgemm(tgb_ctx* ctx, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, double alpha, const double* A,
               int64_t lda, const double* B, int64_t ldb, double beta, double* C, int64_t ldc);
+/* Measured FP64 issue rate of this device (independent DFMA chains on every SM, best of three
+ * ~5 ms runs): the FP64 roofline denominator bench.py reports against, taken in the same run. */
+int tgb_probe_fp64_peak(tgb_ctx* ctx, double* tflops);
 
 /* ---- lattice sums ------------------------------------------------------------
  * replaces the per-axis assembly of tg::lattice_sum_canonical / _tucker /

@@ -166,6 +166,7 @@ def lib() -> C.CDLL:
             "tgb_mode_spectrum": (I, [P, C.POINTER(tgb_cp), I, I, P, P]),
             "tgb_tucker_to_canonical": (I, [P, P, C.POINTER(tgb_cp), I]),
             "tgb_dgemm": (I, [P, I, I, I64, I64, I64, D, P, I64, P, I64, D, P, I64]),
+            "tgb_probe_fp64_peak": (I, [P, C.POINTER(D)]),
             "tgb_host_last_error": (C.c_char_p, []),
             "tgb_mesh_size": (D, [D, I64]),
             "tgb_snap_to_node": (I, [D, I64, D, C.POINTER(I64)]),

@@ -218,3 +218,55 @@ extern "C" int tgb_dgemm(tgb_ctx* ctx, int trans_a, int trans_b, int64_t M, int6
     tgb::dgemm(ctx, trans_a != 0, trans_b != 0, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc);
   });
 }
+
+// ---- FP64 issue-rate probe (bench.py's FP64 roofline denominator, measured in the same run).
+// Every thread runs eight independent DFMA chains; all SMs filled.
+namespace tgb {
+namespace {
+__global__ void __launch_bounds__(256) fp64_probe_kernel(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      x0 = fma(x0, a, b);
+      x1 = fma(x1, a, b);
+      x2 = fma(x2, a, b);
+      x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b);
+      x5 = fma(x5, a, b);
+      x6 = fma(x6, a, b);
+      x7 = fma(x7, a, b);
+    }
+  }
+  const double s = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (s == 1.2345e300) out[0] = s;  // keeps the chains live
+}
+}  // namespace
+}  // namespace tgb
+
+extern "C" int tgb_probe_fp64_peak(tgb_ctx* ctx, double* tflops) {
+  return tgb::guarded_call([&] {
+    tgb::require(tflops != nullptr, "probe_fp64_peak: null output");
+    TGB_CUDA(cudaSetDevice(ctx->device));
+    double* dummy = static_cast<double*>(tgb::ctx_buf(ctx, "probe.fp64").get(sizeof(double)));
+    const int iters = 1024, ctas = 8 * ctx->num_sms, threads = 256;
+    cudaEvent_t e0, e1;
+    TGB_CUDA(cudaEventCreate(&e0));
+    TGB_CUDA(cudaEventCreate(&e1));
+    double best = 0.0;
+    for (int rep = 0; rep < 4; ++rep) {  // first repetition warms up; best of the rest
+      TGB_CUDA(cudaEventRecord(e0, ctx->stream));
+      tgb::fp64_probe_kernel<<<ctas, threads, 0, ctx->stream>>>(dummy, iters, 1.0000001, 1e-9);
+      TGB_LAUNCHED(ctx);
+      TGB_CUDA(cudaEventRecord(e1, ctx->stream));
+      TGB_CUDA(cudaEventSynchronize(e1));
+      float ms = 0.f;
+      TGB_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+      const double flops = 2.0 * 256.0 * iters * static_cast<double>(ctas) * threads;
+      if (rep) best = std::max(best, flops / (ms * 1e-3) / 1e12);
+    }
+    TGB_CUDA(cudaEventDestroy(e0));
+    TGB_CUDA(cudaEventDestroy(e1));
+    *tflops = best;
+  });
+}

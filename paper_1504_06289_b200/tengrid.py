@@ -60,6 +60,12 @@ class Context:
         check(lib().tgb_ctx_transfer_bytes(self._h, C.byref(h), C.byref(d)))
         return h.value, d.value
 
+    def probe_fp64_peak(self) -> float:
+        """Measured FP64 DFMA rate of the device in TFLOP/s (tgb_probe_fp64_peak)."""
+        t = C.c_double()
+        check(lib().tgb_probe_fp64_peak(self._h, C.byref(t)))
+        return t.value
+
     def set_profiling(self, enabled: bool) -> None:
         check(lib().tgb_ctx_set_profiling(self._h, int(enabled)))
 

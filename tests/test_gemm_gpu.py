@@ -31,3 +31,10 @@ def test_dgemm_vs_numpy(ctx, ta, tb, M, N, K):
     got = dC.cpu().numpy().T
     ref = 0.5 * ((A.T if ta else A) @ (B.T if tb else B)) - 2.0 * C0
     assert np.abs(got - ref).max() <= 1e-13 * max(1.0, np.abs(ref).max()) * np.sqrt(K)
+
+
+def test_fp64_peak_probe(ctx):
+    """tgb_probe_fp64_peak: the FP64 roofline denominator bench.py takes in the same run (DFMA chains
+    on every SM); a B200 sustains 30-38 TFLOP/s."""
+    tf = ctx.probe_fp64_peak()
+    assert 20.0 < tf < 45.0, tf
