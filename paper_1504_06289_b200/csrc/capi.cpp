@@ -168,42 +168,46 @@ void convolve_impl(tgb_ctx* ctx, const tgb_cp* a, const tgb_cp* b, const double 
     return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
   };
   size_t iev = 3;
-  bool spinning = false;
-  for (int ax = 0; ax < 3; ++ax) {
-    const size_t blk = static_cast<size_t>(a->n[ax]) * ra;
-    if (!pinned[ax]) {  // staged copy of the whole factor (pageable destination)
-      TGB_CUDA(cudaStreamSynchronize(ctx->stream));
-      tgb::d2h(ctx, out->factor[ax], dout_ax[ax], blk * rb * sizeof(double), ctx->copy_stream);
-      continue;
-    }
-    if (!spinning) {
-      tgb::stream_copy_begin();
-      spinning = true;
-    }
-    for (int64_t j = 0; j < rb; ++j) {
-      if (rep[ax][j] != j) continue;
-      const size_t bytes = blk * sizeof(double);
-      for (size_t o = 0; o < bytes; o += piece) {
-        const size_t len = std::min(piece, bytes - o);
-        auto tw = std::chrono::steady_clock::now();
-        cudaError_t st;
-        while ((st = cudaEventQuery(ctx_event(ctx, iev))) == cudaErrorNotReady) _mm_pause();
-        ++iev;
-        if (st != cudaSuccess) {
-          tgb::stream_copy_end();
+  {
+    struct SpinScope {  // the copy threads spin only while pieces are being consumed, also on an error path
+      bool on = false;
+      void begin() {
+        if (!on) tgb::stream_copy_begin();
+        on = true;
+      }
+      ~SpinScope() {
+        if (on) tgb::stream_copy_end();
+      }
+    } spin;
+    for (int ax = 0; ax < 3; ++ax) {
+      const size_t blk = static_cast<size_t>(a->n[ax]) * ra;
+      if (!pinned[ax]) {  // staged copy of the whole factor (pageable destination)
+        TGB_CUDA(cudaStreamSynchronize(ctx->stream));
+        tgb::d2h(ctx, out->factor[ax], dout_ax[ax], blk * rb * sizeof(double), ctx->copy_stream);
+        continue;
+      }
+      spin.begin();
+      for (int64_t j = 0; j < rb; ++j) {
+        if (rep[ax][j] != j) continue;
+        const size_t bytes = blk * sizeof(double);
+        for (size_t o = 0; o < bytes; o += piece) {
+          const size_t len = std::min(piece, bytes - o);
+          auto tw = std::chrono::steady_clock::now();
+          cudaError_t st;
+          while ((st = cudaEventQuery(ctx_event(ctx, iev))) == cudaErrorNotReady) _mm_pause();
+          ++iev;
           TGB_CUDA(st);
+          t_wait += since(tw);
+          tw = std::chrono::steady_clock::now();
+          for (int64_t jt = j + 1; jt < rb; ++jt)
+            if (rep[ax][jt] == j)
+              tgb::stream_copy(reinterpret_cast<char*>(out->factor[ax] + blk * jt) + o,
+                               reinterpret_cast<const char*>(out->factor[ax] + blk * j) + o, len);
+          t_copy += since(tw);
         }
-        t_wait += since(tw);
-        tw = std::chrono::steady_clock::now();
-        for (int64_t jt = j + 1; jt < rb; ++jt)
-          if (rep[ax][jt] == j)
-            tgb::stream_copy(reinterpret_cast<char*>(out->factor[ax] + blk * jt) + o,
-                             reinterpret_cast<const char*>(out->factor[ax] + blk * j) + o, len);
-        t_copy += since(tw);
       }
     }
   }
-  if (spinning) tgb::stream_copy_end();
   TGB_CUDA(cudaStreamSynchronize(ctx->copy_stream));
   TGB_CUDA(cudaStreamSynchronize(ctx->stream));
   if (trace)
