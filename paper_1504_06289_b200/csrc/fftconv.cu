@@ -2383,7 +2383,7 @@ void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int
                  int64_t ldx, const double* h, bool shiftA);
 void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double* const* specBr,
                double2* const* specBc, PairEntry* const* work, const int* winfo0, double* const* out,
-               const double* const* U, const double* const* V, const double* h, bool shifted);
+               const double* const* U, const double* const* V, const double* h, bool shifted, int nB);
 
 // large-n plan (fftconv12k.cu): N = S * 12288 split into S sub-transforms
 int kS_split(int64_t n);
@@ -2563,7 +2563,9 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
       const size_t N1 = 12288 + 1;
       const size_t a_bytes = (static_cast<size_t>(ra) * N1 * sizeof(double2) + 255) & ~size_t(255);
       const size_t real_bytes = (static_cast<size_t>(rb) * N1 * sizeof(double) + 255) & ~size_t(255);
-      const size_t b_bytes = real_bytes + ((static_cast<size_t>(rb) * N1 * sizeof(double2) + 255) & ~size_t(255));
+      // real spectra | complex spectra | per-column band limits (k12_band_of)
+      const size_t b_bytes = real_bytes + ((static_cast<size_t>(rb) * N1 * sizeof(double2) + 255) & ~size_t(255)) +
+                             ((static_cast<size_t>(rb) * sizeof(int) + 255) & ~size_t(255));
       // axes of this extent and the same output form share one spectrum launch (whole waves)
       int nb = 0;  // batch [ax, ax + nb)
       if (k12_first < 0 || ax >= k12_first + k12_count) {
@@ -2602,7 +2604,7 @@ void convolve_axes(tgb_ctx* ctx, int naxes, const int64_t* n, int64_t ra, const 
         if (!joined) TGB_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->aux_done, 0));
         joined = true;
         k12_pairs(ctx, n[ax], nb, k12_specA, k12_specBr, k12_specBc, dwork.data() + ax, winfo + 2 * ax, out + ax,
-                  A + ax, B + ax, h + ax, k12_shift);
+                  A + ax, B + ax, h + ax, k12_shift, static_cast<int>(rb));
       }
       continue;
     }

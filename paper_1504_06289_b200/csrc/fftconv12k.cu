@@ -171,6 +171,53 @@ __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double
   }
 }
 
+// Pruned form of stage 2 for a band-limited pair (kBand): after the pruned stage 1 only the
+// blocks kk < 144 and kk >= 624 are populated, i.e. the inputs s1 in {0, 1, 2, 13, 14, 15} of
+// every stage-2 butterfly (kk = k1 + 48 s1); the other ten are zero and are neither read nor
+// multiplied (the compiler folds them out of the radix-16 butterfly).
+constexpr int kBand = 144;
+template <int S>
+__device__ __forceinline__ void stage2_dual_pruned(double2* sm, int tid, double2 w) {
+  const int k1 = tid % 48, t0a = tid / 48;
+  double2* pa = sm + slot(t0a, 0, k1);
+  double2* pb = sm + slot(t0a + 8, 0, k1);
+  double2 va[16], vb[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const bool live = s < 3 || s > 12;
+    va[s] = live ? pa[51 * s] : make_double2(0.0, 0.0);
+    vb[s] = live ? pb[51 * s] : make_double2(0.0, 0.0);
+  }
+  dft<16, S>(va);
+  {
+    double2 wt = w;
+    pa[0] = va[0];
+#pragma unroll
+    for (int t = 1; t < 16; ++t) {
+      pa[51 * t] = cmul(va[t], wt);
+      wt = cmul(wt, w);
+    }
+  }
+  dft<16, S>(vb);
+  {
+    double2 wt = w;
+    pb[0] = vb[0];
+#pragma unroll
+    for (int t = 1; t < 16; ++t) {
+      pb[51 * t] = cmul(vb[t], wt);
+      wt = cmul(wt, w);
+    }
+  }
+}
+
+// one complex double = 4 columns of this thread's lane
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* r) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr)
+               : "memory");
+}
+
 // ---------------------------------------------------------------- forward spectra
 
 // One CTA per column: columns [0, nB) are kernel columns (modeB: 1 real form
@@ -187,7 +234,15 @@ struct SpecAxes12 {
   double2* specBc[3];
   double h[3];
   int bsrc[3];  // axis whose kernel spectra this axis shares (the same factor matrix and h), else itself
+  int* band[3];  // per kernel column: band limit of its spectrum (see kBandTol), N + 1 = none
 };
+
+// A kernel column's spectrum is band-limited at K when every |B[k]|, k >= K, is below 2^-46 of
+// its largest entry - below the roundoff floor of the transform that produced it (sampled smooth
+// kernels: the Newton kernel's Gaussian terms on config 2's grid stop at K = 30..123 of 12289;
+// columns cut off by the box edge decay like 1/k and keep the full band).  The pair kernel skips
+// the arithmetic on those entries (k12_pair_run, pruned form).
+constexpr double kBandTol2 = 0x1p-92;  // (2^-46)^2, on |B|^2
 
 __global__ void __launch_bounds__(TT, 1)
     k12_spectrum_kernel(int n, SpecAxes12 axs, int nA, int nB, int modeB, int64_t ldx, int shiftA) {
@@ -282,7 +337,9 @@ __global__ void __launch_bounds__(TT, 1)
     }
     return;
   }
-  for (int k = tid; k <= N; k += TT) {
+  // kernel columns: spectrum with the window phase, and its band limit (two sweeps: largest
+  // |y|^2, then the last k above kBandTol2 of it)
+  auto bval = [&](int k) {
     const int ka = k == N ? 0 : k, kb = ka == 0 ? 0 : N - ka;  // Z_N = Z_0
     const double2 zk = sm[ka + (ka >> 4)];
     double2 zm = sm[kb + (kb >> 4)];
@@ -291,16 +348,41 @@ __global__ void __launch_bounds__(TT, 1)
     const double2 wd = cmul(cmul(zlo[k & 63], zhi[k >> 6]), dif);
     double2 X = make_double2(0.5 * (sum.x + wd.y), 0.5 * (sum.y - wd.x));
     if (k == 0 || k == N) X.y = 0.0;  // DC and Nyquist of a real signal
-    if (!isB) {
-      specA[base + k] = X;
-    } else {
-      const int64_t e = (static_cast<int64_t>(k) * ofs) % M;
-      const double2 ph = cconj(cmul(zlo[e & 63], zhi[e >> 6]));  // e^{+2 pi i k ofs/m}
-      const double2 y = cmul(X, ph);
-      if (modeB & 1) specBr[base + k] = hm * y.x;
-      if (modeB & 2) specBc[base + k] = cscale(y, hm);
-    }
+    const int64_t e = (static_cast<int64_t>(k) * ofs) % M;
+    const double2 ph = cconj(cmul(zlo[e & 63], zhi[e >> 6]));  // e^{+2 pi i k ofs/m}
+    return cmul(X, ph);
+  };
+  double vmax = 0.0;
+  for (int k = tid; k <= N; k += TT) {
+    const double2 y = bval(k);
+    if (modeB & 1) specBr[base + k] = hm * y.x;
+    if (modeB & 2) specBc[base + k] = cscale(y, hm);
+    vmax = fmax(vmax, y.x * y.x + y.y * y.y);
   }
+  double* red = reinterpret_cast<double*>(zhi + M / 64);  // past the twiddle tables (not used beyond this point)
+  __syncthreads();
+  red[tid] = vmax;
+  __syncthreads();
+  for (int st = 256; st > 0; st >>= 1) {
+    if (tid < st && tid + st < TT) red[tid] = fmax(red[tid], red[tid + st]);
+    __syncthreads();
+  }
+  const double thr = red[0] * kBandTol2;
+  __syncthreads();
+  int last = -1;
+  for (int k = tid; k <= N; k += TT) {
+    const double2 y = bval(k);
+    if (!(y.x * y.x + y.y * y.y <= thr)) last = k;  // a NaN entry counts as data
+  }
+  if (!(thr < INFINITY)) last = N;  // non-finite spectrum: no pruning, the pair kernel propagates it
+  int* ired = reinterpret_cast<int*>(red);
+  ired[tid] = last;
+  __syncthreads();
+  for (int st = 256; st > 0; st >>= 1) {
+    if (tid < st && tid + st < TT) ired[tid] = max(ired[tid], ired[tid + st]);
+    __syncthreads();
+  }
+  if (tid == 0) axs.band[blockIdx.y][c] = ired[0] + 1;
 }
 
 // ---------------------------------------------------------------- pair kernel
@@ -329,7 +411,7 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
                                              int w0, int w1, double* __restrict__ out, const double* __restrict__ U,
                                              int64_t ldu, const double* __restrict__ V, int64_t ldv, double h, int n,
                                              int alias, unsigned long long* __restrict__ phase, int shifted,
-                                             double2 wkk) {
+                                             double2 wkk, const int* __restrict__ band) {
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool self = tid == TT - 1;
   const int kk = tid + 1;
@@ -369,6 +451,42 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
       }
       tmem_wait_st();
     }
+    // Band-limited kernel column (B[k] below the roundoff floor for k >= kBand, k12_spectrum_kernel):
+    // only the split pairs (k, N - k), k < kBand, carry data - one per block pair kk = k < kBand,
+    // so each of those threads holds ONE nonzero input per radix-16 block and the butterfly is a
+    // broadcast: block kk gets Z[k] w_N^{kk t}, its mirror block conj-twiddled Z[N - k].
+    const bool pruned = band[e.jb] <= kBand && !(shifted & 8);
+    if (pruned) {
+      if (warp <= (kBand - 1) / 32 || warp == TT / 32 - 1) {  // warp-uniform: tensor-memory loads are warp-wide
+        uint32_t r4[4];
+        tmem_ld4(tbase, r4);  // A[ka], u = 0
+        tmem_wait_ld();
+        if (tid < kBand - 1 || self) {
+          const double2 av = make_double2(__hiloint2double(r4[1], r4[0]), __hiloint2double(r4[3], r4[2]));
+          const double2 pk = bmul<BREAL>(av, b, self ? 0 : kk);
+          double2 zp, zq;
+          zsplit2(pk, make_double2(0.0, 0.0), wkk, zp, zq);  // self: w = 1
+          if (self) {  // block 0: only Z[0]; every output of the butterfly equals it (twiddle 1)
+#pragma unroll
+            for (int t = 0; t < 16; ++t) sm[slot_kk(t, 0)] = zp;
+          } else {
+            const double2 wX = cmul(wkk, wkk);  // w_N^kk
+            double2 wt = wX;
+            sm[slot_kk(0, kX)] = zp;
+            sm[slot_kk(0, kY)] = zq;
+#pragma unroll
+            for (int t = 1; t < 16; ++t) {
+              sm[slot_kk(t, kX)] = cmul(zp, wt);
+              sm[slot_kk(t, kY)] = cmul(zq, cconj(wt));  // conj(w_N^{(768 - kY) t}) with the rotation absorbed
+              wt = cmul(wt, wX);
+            }
+          }
+        } else if (tid == kBand - 1) {  // block 768 - kBand: read by stage 2 (s1 = 13, k1 = 0), holds no data
+#pragma unroll
+          for (int t = 0; t < 16; ++t) sm[slot_kk(t, NB - kBand)] = make_double2(0.0, 0.0);
+        }
+      }
+    } else
     // ---- stage 1: products, real split, two radix-16 blocks per thread.  Z[k] stays in
     // registers (block X), Z[N-k] goes to this thread's own block-Y slots in natural order;
     // the warp holding the self thread stashes both (its routing differs per lane).
@@ -515,7 +633,10 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
         }
       }
     };
-    stage2_dual<1>(sm, tid, cst[0]);
+    if (pruned)
+      stage2_dual_pruned<1>(sm, tid, cst[0]);
+    else
+      stage2_dual<1>(sm, tid, cst[0]);
     __syncthreads();
     c2 = phase ? clock64() : 0;
     stage3<1>(sm, tid, cst[1], cst[2]);
@@ -569,6 +690,7 @@ struct PairAxes12 {
   double* out[3];
   const double* U[3];
   const double* V[3];
+  const int* band[3];  // kernel columns' spectral band limits (k12_spectrum_kernel)
   double h[3];
   int naxes;
 };
@@ -607,10 +729,10 @@ __global__ void __launch_bounds__(TT, 1)
     if (w0 >= w1) continue;
     if (ax.winfo[i][1])
       k12_pair_run<true>(sm, tbase, ax.specA[i], ax.specBr[i], ax.work[i], w0, w1, ax.out[i], ax.U[i], n, ax.V[i], n,
-                         ax.h[i], n, alias, phase, shifted, wkk);
+                         ax.h[i], n, alias, phase, shifted, wkk, ax.band[i]);
     else
       k12_pair_run<false>(sm, tbase, ax.specA[i], ax.specBc[i], ax.work[i], w0, w1, ax.out[i], ax.U[i], n, ax.V[i], n,
-                          ax.h[i], n, alias, phase, shifted, wkk);
+                          ax.h[i], n, alias, phase, shifted, wkk, ax.band[i]);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -934,13 +1056,20 @@ bool k12_applicable(int64_t n, int64_t generic_N) {
 
 bool k12_alias(int64_t n) { return (3 * n - 3) / 2 == k12::M; }
 
+// The band limits of an axis's nB kernel columns sit behind its complex kernel spectra (256-byte
+// aligned; convolve_axes sizes the block for them), so axes sharing spectra share them too.
+static int* k12_band_of(double2* specBc, int nB) {
+  const size_t cbytes = (static_cast<size_t>(nB) * (k12::N + 1) * sizeof(double2) + 255) & ~size_t(255);
+  return reinterpret_cast<int*>(reinterpret_cast<char*>(specBc) + cbytes);
+}
+
 // spectra of naxes axes of one extent n in one launch (per-axis inputs and spectrum buffers)
 void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int nA, double2* const* specA,
                  const double* const* B, int nB, double* const* specBr, double2* const* specBc, int modeB,
                  int64_t ldx, const double* h, bool shiftA) {
   if (nA + nB == 0 || naxes == 0) return;
   static bool attr[kTgbMaxDevices] = {};
-  const size_t smem = k12::kSmem + (64 + k12::M / 64) * sizeof(double2);
+  const size_t smem = k12::kSmem + (64 + k12::M / 64) * sizeof(double2) + k12::TT * sizeof(double);
   if (!attr[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(k12::k12_spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   static_cast<int>(smem)));
@@ -954,6 +1083,7 @@ void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int
     axs.specBr[ax] = specBr[ax];
     axs.specBc[ax] = specBc[ax];
     axs.h[ax] = h[ax];
+    axs.band[ax] = k12_band_of(specBc[ax], nB);
     axs.bsrc[ax] = ax;
     for (int j = 0; j < ax; ++j)
       if (specBr[j] == specBr[ax]) {  // the caller pointed this axis at an earlier axis's kernel spectra
@@ -971,7 +1101,7 @@ constexpr size_t kPairSmem = k12::kSmem + 3 * k12::TT * sizeof(double2);  // + p
 // pairs of naxes (<= 3) axes of one extent: one launch
 void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double* const* specBr,
                double2* const* specBc, PairEntry* const* work, const int* winfo0, double* const* out,
-               const double* const* U, const double* const* V, const double* h, bool shifted) {
+               const double* const* U, const double* const* V, const double* h, bool shifted, int nB) {
   static bool attr[kTgbMaxDevices] = {};
   if (!attr[ctx->device]) {
     TGB_CUDA(cudaFuncSetAttribute(k12::k12_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -990,6 +1120,7 @@ void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double
     ax.U[i] = U[i];
     ax.V[i] = V[i];
     ax.h[i] = h[i];
+    ax.band[i] = k12_band_of(specBc[i], nB);
   }
   prof_begin(ctx);
   static DevBuf phase_buf;
@@ -999,7 +1130,8 @@ void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double
     TGB_CUDA(cudaMemsetAsync(phase, 0, 8 * sizeof(unsigned long long), ctx->stream));
   }
   // TGB_K12_NOSTORE: timing probe only (the window stores are skipped, results are wrong)
-  const int smode = shifted ? (getenv("TGB_K12_NOSTORE") ? 3 : 1) : 0;
+  // TGB_K12_NO_PRUNE: A/B switch, band-limited kernel columns take the full stages 1-2 too
+  const int smode = (shifted ? (getenv("TGB_K12_NOSTORE") ? 3 : 1) : 0) | (getenv("TGB_K12_NO_PRUNE") ? 8 : 0);
   k12::k12_pair_kernel<<<ctx->num_sms, k12::TT, kPairSmem, ctx->stream>>>(ax, static_cast<int>(n),
                                                                          k12_alias(n) ? 1 : 0, phase, smode);
   TGB_LAUNCHED(ctx);
