@@ -176,6 +176,8 @@ __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double
 // every stage-2 butterfly (kk = k1 + 48 s1); the other ten are zero and are neither read nor
 // multiplied (the compiler folds them out of the radix-16 butterfly).
 constexpr int kBand = 144;
+constexpr int kChunk = 192;            // work entries staged in shared memory at a time (k12_pair_run)
+constexpr int kPrunedBit = 1 << 30;  // in a staged entry's jb: band-limited kernel column
 template <int S>
 __device__ __forceinline__ void stage2_dual_pruned(double2* sm, int tid, double2 w) {
   const int k1 = tid % 48, t0a = tid / 48;
@@ -422,8 +424,23 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
   const int u_last = (nz - 1) % NB;  // stage-4 butterfly holding x[n-1]
   const int tid_last = u_last % TT;  // its thread: u = tid + 384 hb
   int ia_cur = -1;
+  // The run's work entries come through shared memory, kChunk at a time, each with its kernel
+  // column's band-limit flag folded into jb: the pair loop starts from one shared-memory read
+  // instead of two dependent L2 reads (entry, then band limit) in front of its first load.
+  PairEntry* tab = reinterpret_cast<PairEntry*>(sm + SLOTS + 3 * TT);
   for (int w = w0; w < w1; ++w) {
-    const PairEntry e = work[w];
+    const int wi = (w - w0) % kChunk;
+    if (wi == 0) {  // (the previous pair ended on a CTA barrier: nobody still reads the table)
+      if (tid < min(kChunk, w1 - w)) {
+        PairEntry t = work[w + tid];
+        if (band[t.jb] <= kBand && !(shifted & 8)) t.jb |= kPrunedBit;
+        tab[tid] = t;
+      }
+      __syncthreads();
+    }
+    PairEntry e = tab[wi];
+    const bool pruned = e.jb & kPrunedBit;
+    e.jb &= ~kPrunedBit;
     const long long c0 = phase ? clock64() : 0;
     const double2* a = specA + static_cast<int64_t>(e.ia) * (N + 1);
     const void* b = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + static_cast<int64_t>(e.jb) * (N + 1))
@@ -455,7 +472,6 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
     // only the split pairs (k, N - k), k < kBand, carry data - one per block pair kk = k < kBand,
     // so each of those threads holds ONE nonzero input per radix-16 block and the butterfly is a
     // broadcast: block kk gets Z[k] w_N^{kk t}, its mirror block conj-twiddled Z[N - k].
-    const bool pruned = band[e.jb] <= kBand && !(shifted & 8);
     if (pruned) {
       if (warp <= (kBand - 1) / 32 || warp == TT / 32 - 1) {  // warp-uniform: tensor-memory loads are warp-wide
         uint32_t r4[4];
@@ -639,6 +655,16 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
       stage2_dual<1>(sm, tid, cst[0]);
     __syncthreads();
     c2 = phase ? clock64() : 0;
+    // the next pair, if band-limited, starts from kBand kernel-spectrum entries: bring their lines into L1 now
+    if (w + 1 < w1 && wi + 1 < kChunk && tid < kBand) {
+      const PairEntry en = tab[wi + 1];
+      if (en.jb & kPrunedBit) {
+        const int64_t o = static_cast<int64_t>(en.jb & ~kPrunedBit) * (N + 1) + (tid == kBand - 1 ? 0 : tid + 1);
+        const void* pb = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + o)
+                               : static_cast<const void*>(static_cast<const double2*>(specB) + o);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(pb));
+      }
+    }
     stage3<1>(sm, tid, cst[1], cst[2]);
     __syncthreads();
     c3 = phase ? clock64() : 0;
@@ -1096,7 +1122,8 @@ void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int
   TGB_LAUNCHED(ctx);
 }
 
-constexpr size_t kPairSmem = k12::kSmem + 3 * k12::TT * sizeof(double2);  // + per-thread twiddle bases
+// + per-thread twiddle bases + the staged work entries
+constexpr size_t kPairSmem = k12::kSmem + 3 * k12::TT * sizeof(double2) + k12::kChunk * sizeof(PairEntry);
 
 // pairs of naxes (<= 3) axes of one extent: one launch
 void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double* const* specBr,
