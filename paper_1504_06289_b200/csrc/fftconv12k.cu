@@ -171,45 +171,58 @@ __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double
   }
 }
 
-// Pruned form of stage 2 for a band-limited pair (kBand): after the pruned stage 1 only the
-// blocks kk < 144 and kk >= 624 are populated, i.e. the inputs s1 in {0, 1, 2, 13, 14, 15} of
-// every stage-2 butterfly (kk = k1 + 48 s1); the other ten are zero and are neither read nor
-// multiplied (the compiler folds them out of the radix-16 butterfly).
+// ---------------------------------------------------------------- band-limited pairs
+// A kernel column whose spectrum is below the roundoff floor for k >= kBand (k12_spectrum_kernel)
+// leaves only the 2 kBand - 1 entries Zs[f], |f| < kBand, of the packed spectrum nonzero
+// (Zs[f] = Z[f], Zs[-j] = Z[N - j]).  Those pairs replace stages 1-3 by (tools/proto_k12_pruned.py):
+//  T  the table Zs[f] = P[f] (1 + i w_m^f), Zs[-f] = conj(P[f] (1 - i w_m^f)), P = A B, in shared memory;
+//  M  one thread per (t0, k2): its 18 stage-1 values y[c] = Zs[k2 + 16 c] w_N^{(k2 + 16 c) t0},
+//     c = -9..8 (the only live inputs of the 48-point transform over kk = k2 + 16 c), parked in
+//     the thread's tensor-memory lane, then for t2 = 0, 1, 2 the outputs tau = t2 + 3 t1 as ONE
+//     dense radix-16 butterfly over s1 (c = s1 + 16 s2: s2 = 0 for c >= 0, s2 = 2 for c < 0):
+//       g[s1] = w_48^{s1 t2} y[s1] + w_48^{(s1 + 32) t2} y[s1 - 16],   X[tau] = w_768^{k2 tau} dft16(g)[t1]
+//     written where stage 4 expects them.  No shared-memory reads of transform data, one pass of
+//     writes, two CTA barriers fewer than the full stages 1-3.
 constexpr int kBand = 144;
 constexpr int kChunk = 192;            // work entries staged in shared memory at a time (k12_pair_run)
 constexpr int kPrunedBit = 1 << 30;  // in a staged entry's jb: band-limited kernel column
-template <int S>
-__device__ __forceinline__ void stage2_dual_pruned(double2* sm, int tid, double2 w) {
-  const int k1 = tid % 48, t0a = tid / 48;
-  double2* pa = sm + slot(t0a, 0, k1);
-  double2* pb = sm + slot(t0a + 8, 0, k1);
-  double2 va[16], vb[16];
-#pragma unroll
-  for (int s = 0; s < 16; ++s) {
-    const bool live = s < 3 || s > 12;
-    va[s] = live ? pa[51 * s] : make_double2(0.0, 0.0);
-    vb[s] = live ? pb[51 * s] : make_double2(0.0, 0.0);
+// shared memory behind the transform slots, in double2 units (k12_pair_kernel fills the tables)
+constexpr int kExt768 = 0;     // w_768^r, r < 48
+constexpr int kExt48 = 48;     // w_48^r, r < 16
+constexpr int kExt48sq = 64;   // w_48^{2r}
+constexpr int kExtBase = 80;   // w_N^{k2 t0} of the M-stage thread (t0, k2) = (tid >> 4, tid & 15), tid < 256
+constexpr int kZsLen = 292;    // one Zs table: [f] for f >= 0, [kBand + j] for f = -j (289 entries)
+constexpr int kExtZs = 336;    // two Zs tables (this pair's, the next band-limited pair's)
+constexpr int kExtWm = kExtZs + 2 * kZsLen;  // w_m^f, f < kBand
+constexpr int kExtTab = kExtWm + kBand;      // staged work entries
+constexpr int kExtEnd = kExtTab + (kChunk * 24 + 15) / 16;
+
+// v e^{2 pi i e / 48} (e a constant after unrolling)
+__device__ __forceinline__ double2 mulw48(double2 v, int e) {
+  constexpr double C[13] = {1.0,
+                            0.991444861373810411145,
+                            0.96592582628906828675,
+                            0.923879532511286756128,
+                            0.866025403784438646764,
+                            0.79335334029123516458,
+                            0.707106781186547524401,
+                            0.608761429008720639416,
+                            0.5,
+                            0.382683432365089771728,
+                            0.258819045102520762349,
+                            0.130526192220051591548,
+                            0.0};
+  e %= 48;
+  const int q = e / 12, r = e % 12;
+  if (r == 0) {
+    if (q == 0) return v;
+    if (q == 1) return make_double2(-v.y, v.x);
+    if (q == 2) return make_double2(-v.x, -v.y);
+    return make_double2(v.y, -v.x);
   }
-  dft<16, S>(va);
-  {
-    double2 wt = w;
-    pa[0] = va[0];
-#pragma unroll
-    for (int t = 1; t < 16; ++t) {
-      pa[51 * t] = cmul(va[t], wt);
-      wt = cmul(wt, w);
-    }
-  }
-  dft<16, S>(vb);
-  {
-    double2 wt = w;
-    pb[0] = vb[0];
-#pragma unroll
-    for (int t = 1; t < 16; ++t) {
-      pb[51 * t] = cmul(vb[t], wt);
-      wt = cmul(wt, w);
-    }
-  }
+  const double c = q == 0 ? C[r] : q == 1 ? -C[12 - r] : q == 2 ? -C[r] : C[12 - r];
+  const double sn = q == 0 ? C[12 - r] : q == 1 ? C[r] : q == 2 ? -C[12 - r] : -C[r];
+  return cmul(v, make_double2(c, sn));
 }
 
 // one complex double = 4 columns of this thread's lane
@@ -218,6 +231,18 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t* r) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(taddr)
                : "memory");
+}
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, double2 v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr),
+               "r"(__double2loint(v.x)), "r"(__double2hiint(v.x)), "r"(__double2loint(v.y)), "r"(__double2hiint(v.y))
+               : "memory");
+}
+__device__ __forceinline__ double2 tmem_ld_c(uint32_t taddr) {
+  uint32_t r[4];
+  tmem_ld4(taddr, r);
+  tmem_wait_ld();
+  return make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
 }
 
 // ---------------------------------------------------------------- forward spectra
@@ -389,6 +414,25 @@ __global__ void __launch_bounds__(TT, 1)
 
 // ---------------------------------------------------------------- pair kernel
 
+// T-stage job f < kBand of a band-limited pair (density spectrum a, kernel spectrum b): both
+// table entries of the split pair (f, N - f), whose N - f half is zero.
+template <bool BREAL>
+__device__ __forceinline__ void zs_job(int f, const double2* __restrict__ a, const void* __restrict__ b,
+                                       const double2* __restrict__ wM, double2* __restrict__ zs) {
+  double2 pk = ld2(a + f);
+  if constexpr (BREAL)
+    pk = cscale(pk, __ldg(static_cast<const double*>(b) + f));
+  else
+    pk = cmul(pk, ld2(static_cast<const double2*>(b) + f));
+  double2 zp, zq;
+  zsplit2(pk, make_double2(0.0, 0.0), wM[f], zp, zq);
+  zs[f] = zp;
+  if (f > 0)
+    zs[kBand + f] = zq;
+  else
+    zs[2 * kBand] = make_double2(0.0, 0.0);  // f = -kBand: read by (k2 = 0, c = -9), holds no data
+}
+
 // Stage-1 item of thread tid.  Regular (tid < 383): block kk = tid + 1 and its
 // mirror 768 - kk from the 16 split pairs (k, N - k), k = kk + 768 u.
 // Self (tid == 383): blocks 0 and 384; pair u < 8: k = 768 u (u = 0: N - k = N,
@@ -417,7 +461,10 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
   const int tid = threadIdx.x, warp = tid >> 5;
   const bool self = tid == TT - 1;
   const int kk = tid + 1;
-  double2* cst = sm + SLOTS + 3 * tid;
+  const double2* ext = sm + SLOTS;
+  double2* zs = sm + SLOTS + kExtZs;  // two tables: the pair's and the next band-limited pair's
+  const double2* wM = ext + kExtWm;
+  bool zs_ready = false;  // CTA-uniform: the previous pair's idle warps formed this pair's table
   const int nz = (n + 1) >> 1;
   const bool odd_n = n & 1;
   const int kX = self ? 0 : kk, kY = self ? 384 : NB - kk;
@@ -427,7 +474,7 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
   // The run's work entries come through shared memory, kChunk at a time, each with its kernel
   // column's band-limit flag folded into jb: the pair loop starts from one shared-memory read
   // instead of two dependent L2 reads (entry, then band limit) in front of its first load.
-  PairEntry* tab = reinterpret_cast<PairEntry*>(sm + SLOTS + 3 * TT);
+  PairEntry* tab = reinterpret_cast<PairEntry*>(sm + SLOTS + kExtTab);
   for (int w = w0; w < w1; ++w) {
     const int wi = (w - w0) % kChunk;
     if (wi == 0) {  // (the previous pair ended on a CTA barrier: nobody still reads the table)
@@ -449,7 +496,7 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
     double corr0 = 0.0, corr1 = 0.0;
     if (alias && tid == 0) corr0 = h * __ldg(U + e.ia * ldu + n - 1) * __ldg(V + e.jb * ldv + n - 1);
     if (alias && tid == tid_last) corr1 = h * __ldg(U + e.ia * ldu) * __ldg(V + e.jb * ldv);
-    if (e.ia != ia_cur) {  // CTA-uniform: a new density column -> tensor memory
+    if (!pruned && e.ia != ia_cur) {  // CTA-uniform: a new density column -> tensor memory
       ia_cur = e.ia;
 #pragma unroll 1
       for (int c = 0; c < 4; ++c) {  // chunk c: u = 8 (c & 1) + [0, 8); c < 2: P[k], else P[N - k]
@@ -468,41 +515,120 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
       }
       tmem_wait_st();
     }
-    // Band-limited kernel column (B[k] below the roundoff floor for k >= kBand, k12_spectrum_kernel):
-    // only the split pairs (k, N - k), k < kBand, carry data - one per block pair kk = k < kBand,
-    // so each of those threads holds ONE nonzero input per radix-16 block and the butterfly is a
-    // broadcast: block kk gets Z[k] w_N^{kk t}, its mirror block conj-twiddled Z[N - k].
+    long long c1 = 0, c2 = 0, c3 = 0;
     if (pruned) {
-      if (warp <= (kBand - 1) / 32 || warp == TT / 32 - 1) {  // warp-uniform: tensor-memory loads are warp-wide
-        uint32_t r4[4];
-        tmem_ld4(tbase, r4);  // A[ka], u = 0
-        tmem_wait_ld();
-        if (tid < kBand - 1 || self) {
-          const double2 av = make_double2(__hiloint2double(r4[1], r4[0]), __hiloint2double(r4[3], r4[2]));
-          const double2 pk = bmul<BREAL>(av, b, self ? 0 : kk);
-          double2 zp, zq;
-          zsplit2(pk, make_double2(0.0, 0.0), wkk, zp, zq);  // self: w = 1
-          if (self) {  // block 0: only Z[0]; every output of the butterfly equals it (twiddle 1)
+      // ---- T: the 2 kBand - 1 live entries of the packed spectrum (the density spectrum's
+      // entries come straight from L2: a band-limited pair does not need it in tensor memory).
+      // Normally formed by warps 8-11 during the PREVIOUS pair's M stage; here only for the
+      // first band-limited pair after a full one or a refill of the entry table.
+      double2* zsc = zs + kZsLen * (wi & 1);
+      // y[c] = Zs[k2 + 16 c] w_N^{(k2 + 16 c) t0} of the thread's (t0, k2) -> tensor-memory columns 4 (c + 9)
+      auto park_y = [&](const double2* zt) {
+        const int k2 = tid & 15, t0 = tid >> 4;
+        const double2 base = ext[kExtBase + tid], step = ext[kExt768 + t0];
+        double2 tw = base;
 #pragma unroll
-            for (int t = 0; t < 16; ++t) sm[slot_kk(t, 0)] = zp;
-          } else {
-            const double2 wX = cmul(wkk, wkk);  // w_N^kk
-            double2 wt = wX;
-            sm[slot_kk(0, kX)] = zp;
-            sm[slot_kk(0, kY)] = zq;
-#pragma unroll
-            for (int t = 1; t < 16; ++t) {
-              sm[slot_kk(t, kX)] = cmul(zp, wt);
-              sm[slot_kk(t, kY)] = cmul(zq, cconj(wt));  // conj(w_N^{(768 - kY) t}) with the rotation absorbed
-              wt = cmul(wt, wX);
-            }
-          }
-        } else if (tid == kBand - 1) {  // block 768 - kBand: read by stage 2 (s1 = 13, k1 = 0), holds no data
-#pragma unroll
-          for (int t = 0; t < 16; ++t) sm[slot_kk(t, NB - kBand)] = make_double2(0.0, 0.0);
+        for (int c = 0; c < 9; ++c) {
+          tmem_st4(tbase + 4 * (c + 9), cmul(zt[k2 + 16 * c], tw));
+          tw = cmul(tw, step);
         }
+        const double2 sc = cconj(step);
+        tw = cmul(base, sc);
+#pragma unroll
+        for (int m = 1; m <= 9; ++m) {
+          tmem_st4(tbase + 4 * (9 - m), cmul(zt[kBand + 16 * m - k2], tw));
+          tw = cmul(tw, sc);
+        }
+        tmem_wait_st();
+      };
+      if (!zs_ready) {
+        if (tid < kBand) zs_job<BREAL>(tid, a, b, wM, zsc);
+        __syncthreads();
+        if (tid < 256) park_y(zsc);
       }
-    } else
+      c1 = phase ? clock64() : 0;
+      const bool has_next = w + 1 < w1 && wi + 1 < kChunk;
+      int next_jb = 0, next_ia = 0;
+      if (has_next) {
+        next_jb = tab[wi + 1].jb;
+        next_ia = tab[wi + 1].ia;
+      }
+      zs_ready = has_next && (next_jb & kPrunedBit);
+      // ---- M (warps 0-7): the 48-point transforms over kk = k2 + 16 c of the thread's (t0, k2)
+      if (tid < 256) {
+        const int k2 = tid & 15, t0 = tid >> 4;
+        const double2 u1 = ext[kExt768 + k2];                // w_768^{k2}
+        const double2 u2 = cmul(u1, u1), u3 = cmul(u2, u1);  // u3 = w_256^{k2}: tau advances by 3
+#pragma unroll
+        for (int t2 = 0; t2 < 3; ++t2) {
+          double2 g[16];
+          auto take = [&](int idx, const uint32_t* r) {  // idx = c + 9
+            const double2 y = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+            if (idx < 9) {  // c < 0: s2 = 2, s1 = c + 16
+              const int s1 = idx + 7;
+              g[s1] = mulw48(y, (s1 + 32) * t2);
+            } else {  // c >= 0: s2 = 0, s1 = c
+              const int s1 = idx - 9;
+              const double2 v = mulw48(y, s1 * t2);
+              if (s1 >= 7) {
+                g[s1].x += v.x;
+                g[s1].y += v.y;
+              } else {
+                g[s1] = v;
+              }
+            }
+          };
+          {
+            uint32_t ra[16], rb[16];
+            tmem_ld16(tbase, ra);
+            tmem_ld16(tbase + 16, rb);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) take(q, ra + 4 * q);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) take(4 + q, rb + 4 * q);
+            tmem_ld16(tbase + 32, ra);
+            tmem_ld16(tbase + 48, rb);
+            tmem_wait_ld();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) take(8 + q, ra + 4 * q);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) take(12 + q, rb + 4 * q);
+            tmem_ld4(tbase + 64, ra);
+            tmem_ld4(tbase + 68, ra + 4);
+            tmem_wait_ld();
+            take(16, ra);
+            take(17, ra + 4);
+          }
+          dft<16, 1>(g);
+          double2 tw = t2 == 0 ? make_double2(1.0, 0.0) : t2 == 1 ? u1 : u2;
+#pragma unroll
+          for (int t1 = 0; t1 < 16; ++t1) {
+            const int tau = t2 + 3 * t1;
+            sm[slot(t0, tau & 15, 16 * (tau >> 4) + k2)] = (t2 == 0 && t1 == 0) ? g[0] : cmul(g[t1], tw);
+            tw = cmul(tw, u3);
+          }
+        }
+      } else if (zs_ready) {  // warps 8-11: the next band-limited pair's table
+        const double2* an = specA + static_cast<int64_t>(next_ia) * (N + 1);
+        const int64_t ob = static_cast<int64_t>(next_jb & ~kPrunedBit) * (N + 1);
+        const void* bn = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + ob)
+                               : static_cast<const void*>(static_cast<const double2*>(specB) + ob);
+        double2* zsn = zs + kZsLen * ((wi + 1) & 1);
+        zs_job<BREAL>(tid - 256, an, bn, wM, zsn);
+        if (tid - 256 + 128 < kBand) zs_job<BREAL>(tid - 256 + 128, an, bn, wM, zsn);
+      }
+      ia_cur = -1;  // the parked values overwrote the density spectrum's columns
+      if (zs_ready) {
+        // the next pair's y values are parked BEFORE this pair's window stores enter the
+        // load/store unit: its M stage then starts from tensor memory and FP64 arithmetic alone
+        // while those stores wait for the egress
+        __syncthreads();
+        c2 = phase ? clock64() : 0;
+        if (tid < 256) park_y(zs + kZsLen * ((wi + 1) & 1));
+      }
+    } else {
+      zs_ready = false;
     // ---- stage 1: products, real split, two radix-16 blocks per thread.  Z[k] stays in
     // registers (block X), Z[N-k] goes to this thread's own block-Y slots in natural order;
     // the warp holding the self thread stashes both (its routing differs per lane).
@@ -585,9 +711,9 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
         }
       }
     }
-    __syncthreads();
-    const long long c1 = phase ? clock64() : 0;
-    long long c2 = 0, c3 = 0;
+      __syncthreads();
+      c1 = phase ? clock64() : 0;
+    }
     double* o0 = out + e.out0;
     double* o1 = e.out1 >= 0 ? out + e.out1 : nullptr;
     const bool aligned = (reinterpret_cast<uintptr_t>(o0) & 15) == 0 && (!o1 || (reinterpret_cast<uintptr_t>(o1) & 15) == 0);
@@ -649,25 +775,30 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
         }
       }
     };
-    if (pruned)
-      stage2_dual_pruned<1>(sm, tid, cst[0]);
-    else
-      stage2_dual<1>(sm, tid, cst[0]);
-    __syncthreads();
-    c2 = phase ? clock64() : 0;
-    // the next pair, if band-limited, starts from kBand kernel-spectrum entries: bring their lines into L1 now
-    if (w + 1 < w1 && wi + 1 < kChunk && tid < kBand) {
-      const PairEntry en = tab[wi + 1];
-      if (en.jb & kPrunedBit) {
-        const int64_t o = static_cast<int64_t>(en.jb & ~kPrunedBit) * (N + 1) + (tid == kBand - 1 ? 0 : tid + 1);
-        const void* pb = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + o)
-                               : static_cast<const void*>(static_cast<const double2*>(specB) + o);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(pb));
+    if (!pruned) {
+      stage2_dual<1>(sm, tid, ext[kExt768 + tid % 48]);
+      __syncthreads();
+      c2 = phase ? clock64() : 0;
+    }
+    // the band-limited pair whose table is formed next (during the next pair's M stage after a
+    // band-limited pair, else at the next pair's start): bring its spectrum lines into L1 now
+    {
+      const int ahead = pruned ? 2 : 1;
+      if (w + ahead < w1 && wi + ahead < kChunk && tid < kBand) {
+        const PairEntry en = tab[wi + ahead];
+        if (en.jb & kPrunedBit) {
+          const int64_t o = static_cast<int64_t>(en.jb & ~kPrunedBit) * (N + 1) + tid;
+          const void* pb = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + o)
+                                 : static_cast<const void*>(static_cast<const double2*>(specB) + o);
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(pb));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(specA + static_cast<int64_t>(en.ia) * (N + 1) + tid));
+        }
       }
     }
-    stage3<1>(sm, tid, cst[1], cst[2]);
-    __syncthreads();
+    if (!pruned) stage3<1>(sm, tid, ext[kExt48 + (tid & 15)], ext[kExt48sq + (tid & 15)]);
+    if (!(pruned && zs_ready)) __syncthreads();  // (that path met at the barrier behind its M stage)
     c3 = phase ? clock64() : 0;
+    if (pruned && !zs_ready) c2 = c3;
     if (shifted & 1) {
       // the second butterfly's inputs are read before the first one's stores enter the load/store
       // unit (whose queue they would wait behind), and its arithmetic runs while those drain
@@ -737,12 +868,20 @@ __global__ void __launch_bounds__(TT, 1)
   const uint32_t tbase = tmem_base_sh + (static_cast<uint32_t>(32 * (warp & 3)) << 16) +
                          static_cast<uint32_t>((warp >> 2) * 128);
   // per-thread constants: split twiddle base w_m^kk in registers; the stage-2/3
-  // twiddle bases in a per-thread shared-memory table (registers are the limit)
+  // twiddle bases in small shared-memory tables (registers are the limit)
   const double2 wkk = tid == TT - 1 ? make_double2(1.0, 0.0) : root(tid + 1, M);
-  double2* cst = sm + SLOTS + 3 * tid;
-  cst[0] = root(tid % 48, 768);
-  cst[1] = root(tid & 15, 48);
-  cst[2] = cmul(cst[1], cst[1]);
+  {
+    double2* ext = sm + SLOTS;
+    if (tid < 48) ext[kExt768 + tid] = root(tid, 768);
+    if (tid < 16) {
+      const double2 r = root(tid, 48);
+      ext[kExt48 + tid] = r;
+      ext[kExt48sq + tid] = cmul(r, r);
+    }
+    if (tid < 256) ext[kExtBase + tid] = root((tid & 15) * (tid >> 4), N);
+    if (tid >= 240) ext[kExtWm + tid - 240] = root(tid - 240, M);
+  }
+  __syncthreads();
   int64_t total = 0;
   for (int i = 0; i < ax.naxes; ++i) total += ax.winfo[i][0];
   const int64_t g0 = total * blockIdx.x / gridDim.x, g1 = total * (blockIdx.x + 1) / gridDim.x;
@@ -1122,8 +1261,9 @@ void k12_spectra(tgb_ctx* ctx, int64_t n, int naxes, const double* const* A, int
   TGB_LAUNCHED(ctx);
 }
 
-// + per-thread twiddle bases + the staged work entries
-constexpr size_t kPairSmem = k12::kSmem + 3 * k12::TT * sizeof(double2) + k12::kChunk * sizeof(PairEntry);
+// + twiddle tables, the band-limited pairs' Zs table, the staged work entries (kExt*)
+constexpr size_t kPairSmem = k12::kSmem + k12::kExtEnd * sizeof(double2);
+static_assert(sizeof(PairEntry) == 24, "kExtEnd assumes 24-byte work entries");
 
 // pairs of naxes (<= 3) axes of one extent: one launch
 void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double* const* specBr,
