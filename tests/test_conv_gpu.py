@@ -86,6 +86,66 @@ def test_k12_plan_many_pairs_per_cta(ctx):
         assert np.array_equal(c.factor[ax][:, 0:ra], c.factor[ax][:, ra:2 * ra])
 
 
+def test_k12_band_limited_pairs(ctx, monkeypatch):
+    """Band-limited kernel columns (spectrum below 2^-46 of its peak beyond k = 144: smooth
+    Gaussians, the Newton kernel's mid-range terms) take the pruned path of k12_pair_kernel
+    (Zs table + merged 48-point stage, fftconv12k.cu); the others the full stages 1-3.  Kernel
+    columns ordered so that a CTA's run switches between the two forms in both directions and
+    runs several band-limited pairs back to back (table and y values formed one pair ahead):
+    off-centre Gaussians (non-symmetric: complex spectra on axis 0), centred ones (real spectra
+    on axis 1), a box-truncated wide Gaussian, a spike, a zero column.  Against the oracle
+    (proj/src/fft.cpp:97-122) and against the same call with the pruning switched off."""
+    n, ra = 16385, 64
+    rng = Rng(777)
+    fa = [np.asfortranarray(rng.normal(n * ra).reshape(n, ra, order="F")) for _ in range(3)]
+    a = CanonicalTensor3(fa, rng.normal(ra))
+    x = np.arange(n) - 0.5 * (n - 1)
+    gauss = lambda s, c=0.0: np.exp(-(((x - c) / s) ** 2))
+    spike = np.zeros(n)
+    spike[n // 2 - 3:n // 2 + 4] = [1, -2, 3, 5, 3, -2, 1]
+    cols0 = [gauss(700, 40.5), gauss(400, -300), gauss(9000), gauss(900, 123), gauss(350, 7), spike,
+             np.zeros(n), gauss(1200, -77), gauss(500, 2000)]
+    cols1 = [gauss(700), gauss(400), gauss(9000), gauss(900), gauss(350), spike, np.zeros(n), gauss(1200), gauss(320)]
+    fb = [np.asfortranarray(np.stack(c, axis=1)) for c in (cols0, cols1, cols0[::-1])]
+    rb = len(cols0)
+    b = CanonicalTensor3(fb, np.ones(rb))
+    h = (0.011, 0.013, 0.017)
+    c = convolve(a, b, h, ctx)
+    monkeypatch.setenv("TGB_K12_NO_PRUNE", "1")
+    cfull = convolve(a, b, h, ctx)
+    monkeypatch.delenv("TGB_K12_NO_PRUNE")
+    for ax in range(3):
+        assert relmax(c.factor[ax], cfull.factor[ax]) <= 1e-12, ax
+        for j in range(rb):
+            blk = c.factor[ax][:, ra * j:ra * (j + 1)]
+            scale = np.abs(cfull.factor[ax][:, ra * j:ra * (j + 1)]).max()
+            assert np.abs(blk - cfull.factor[ax][:, ra * j:ra * (j + 1)]).max() <= 1e-12 * max(scale, 1e-300), (ax, j)
+        for i in (0, 1, 31, 62, 63):
+            for j in range(rb):
+                ref = O.conv_central_many(np.asfortranarray(fa[ax][:, [i]]), np.ascontiguousarray(fb[ax][:, j]))[:, 0]
+                assert relmax(c.factor[ax][:, i + ra * j], h[ax] * ref) <= TOL, (ax, i, j)
+
+
+def test_k12_non_finite_kernel_column_not_pruned(ctx):
+    """A kernel column holding a NaN has a NaN spectrum: it must not be classed as band-limited
+    (its NaNs would be dropped with the pruned entries); every window element is NaN as in the
+    reference's FFT (fft.cpp:97-122), and the finite columns beside it are untouched."""
+    n, ra = 16385, 6
+    rng = Rng(778)
+    fa = [np.asfortranarray(rng.normal(n * ra).reshape(n, ra, order="F")) for _ in range(3)]
+    a = CanonicalTensor3(fa, np.ones(ra))
+    x = np.arange(n) - 0.5 * (n - 1)
+    g = np.exp(-((x / 800.0) ** 2))
+    bad = g.copy()
+    bad[5] = np.nan
+    fb = [np.asfortranarray(np.stack([g, bad], axis=1)) for _ in range(3)]
+    c = convolve(a, CanonicalTensor3(fb, np.ones(2)), (1.0, 1.0, 1.0), ctx)
+    for ax in range(3):
+        assert np.isnan(c.factor[ax][:, ra:]).all()
+        ref = O.conv_central_many(fa[ax], g)
+        assert relmax(c.factor[ax][:, :ra], ref) <= TOL
+
+
 def test_convolve_delta_identity(ctx):
     # test_tensor.cpp:122-135 — delta kernel with h-scaling removed
     n, h = 17, 0.25
