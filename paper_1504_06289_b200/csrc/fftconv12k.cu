@@ -37,6 +37,13 @@
 //    odd density columns' spectra are formed delayed by one sample (shiftA),
 //    which makes every complex window element of every column one 16-byte
 //    store; other shapes keep 8-byte stores on the odd columns.
+//  * Band-limited kernel columns (|B[k]| below 2^-46 of the column's peak for k >= 144, found per
+//    column by the spectrum kernel: the Newton kernel's Gaussians that neither reach the box
+//    edge nor fall under the mesh width, 32 of config 2's 41 columns) leave 287 nonzero entries
+//    in the packed spectrum; their pairs replace stages 1-3 by a table of those entries and ONE
+//    merged 48-point stage per (t0, k2) thread (see "band-limited pairs" below,
+//    tools/proto_k12_pruned.py).  Everything else (random, box-truncated, non-finite columns)
+//    keeps the full path; TGB_K12_NO_PRUNE forces it.
 //  * The load/store unit is in order and a window store waits for the SM's
 //    32 B/clk egress, so each stage issues its shared-memory loads before its
 //    stores (two butterflies in flight in stages 2 and 4, four in stage 3).
