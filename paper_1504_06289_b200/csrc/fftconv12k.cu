@@ -52,6 +52,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <type_traits>
 #include <cstdint>
 #include <cstdio>
 #include <algorithm>
@@ -530,7 +531,7 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
       // first band-limited pair after a full one or a refill of the entry table.
       double2* zsc = zs + kZsLen * (wi & 1);
       // y[c] = Zs[k2 + 16 c] w_N^{(k2 + 16 c) t0} of the thread's (t0, k2) -> tensor-memory columns 4 (c + 9)
-      auto park_y = [&](const double2* zt) {
+      auto park_y = [&](const double2* zt) {  // warps 0-7
         const int k2 = tid & 15, t0 = tid >> 4;
         const double2 base = ext[kExtBase + tid], step = ext[kExt768 + t0];
         double2 tw = base;
@@ -547,12 +548,15 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
           tw = cmul(tw, sc);
         }
         tmem_wait_st();
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       };
       if (!zs_ready) {
         if (tid < kBand) zs_job<BREAL>(tid, a, b, wM, zsc);
         __syncthreads();
         if (tid < 256) park_y(zsc);
+        __syncthreads();  // (warps 8-11 read the parked values of the lanes they share)
       }
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       c1 = phase ? clock64() : 0;
       const bool has_next = w + 1 < w1 && wi + 1 < kChunk;
       int next_jb = 0, next_ia = 0;
@@ -561,69 +565,76 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
         next_ia = tab[wi + 1].ia;
       }
       zs_ready = has_next && (next_jb & kPrunedBit);
-      // ---- M (warps 0-7): the 48-point transforms over kk = k2 + 16 c of the thread's (t0, k2)
-      if (tid < 256) {
-        const int k2 = tid & 15, t0 = tid >> 4;
+      // ---- M: the 48-point transforms over kk = k2 + 16 c of the M thread tm = (t0, k2); pass t2
+      // gives the outputs tau = t2 + 3 t1 from the y values parked at tensor-memory column ycol
+      auto m_pass = [&](auto T2, int tm, uint32_t ycol) {
+        constexpr int t2 = decltype(T2)::value;
+        const int k2 = tm & 15, t0 = tm >> 4;
+        double2 g[16];
+        auto take = [&](int idx, const uint32_t* r) {  // idx = c + 9
+          const double2 y = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+          if (idx < 9) {  // c < 0: s2 = 2, s1 = c + 16
+            const int s1 = idx + 7;
+            g[s1] = mulw48(y, (s1 + 32) * t2);
+          } else {  // c >= 0: s2 = 0, s1 = c
+            const int s1 = idx - 9;
+            const double2 v = mulw48(y, s1 * t2);
+            if (s1 >= 7) {
+              g[s1].x += v.x;
+              g[s1].y += v.y;
+            } else {
+              g[s1] = v;
+            }
+          }
+        };
+        {
+          uint32_t ra[16], rb[16];
+          tmem_ld16(ycol, ra);
+          tmem_ld16(ycol + 16, rb);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) take(q, ra + 4 * q);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) take(4 + q, rb + 4 * q);
+          tmem_ld16(ycol + 32, ra);
+          tmem_ld16(ycol + 48, rb);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q) take(8 + q, ra + 4 * q);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) take(12 + q, rb + 4 * q);
+          tmem_ld4(ycol + 64, ra);
+          tmem_ld4(ycol + 68, ra + 4);
+          tmem_wait_ld();
+          take(16, ra);
+          take(17, ra + 4);
+        }
+        dft<16, 1>(g);
         const double2 u1 = ext[kExt768 + k2];                // w_768^{k2}
         const double2 u2 = cmul(u1, u1), u3 = cmul(u2, u1);  // u3 = w_256^{k2}: tau advances by 3
+        double2 tw = t2 == 0 ? make_double2(1.0, 0.0) : t2 == 1 ? u1 : u2;
 #pragma unroll
-        for (int t2 = 0; t2 < 3; ++t2) {
-          double2 g[16];
-          auto take = [&](int idx, const uint32_t* r) {  // idx = c + 9
-            const double2 y = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
-            if (idx < 9) {  // c < 0: s2 = 2, s1 = c + 16
-              const int s1 = idx + 7;
-              g[s1] = mulw48(y, (s1 + 32) * t2);
-            } else {  // c >= 0: s2 = 0, s1 = c
-              const int s1 = idx - 9;
-              const double2 v = mulw48(y, s1 * t2);
-              if (s1 >= 7) {
-                g[s1].x += v.x;
-                g[s1].y += v.y;
-              } else {
-                g[s1] = v;
-              }
-            }
-          };
-          {
-            uint32_t ra[16], rb[16];
-            tmem_ld16(tbase, ra);
-            tmem_ld16(tbase + 16, rb);
-            tmem_wait_ld();
-#pragma unroll
-            for (int q = 0; q < 4; ++q) take(q, ra + 4 * q);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) take(4 + q, rb + 4 * q);
-            tmem_ld16(tbase + 32, ra);
-            tmem_ld16(tbase + 48, rb);
-            tmem_wait_ld();
-#pragma unroll
-            for (int q = 0; q < 4; ++q) take(8 + q, ra + 4 * q);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) take(12 + q, rb + 4 * q);
-            tmem_ld4(tbase + 64, ra);
-            tmem_ld4(tbase + 68, ra + 4);
-            tmem_wait_ld();
-            take(16, ra);
-            take(17, ra + 4);
-          }
-          dft<16, 1>(g);
-          double2 tw = t2 == 0 ? make_double2(1.0, 0.0) : t2 == 1 ? u1 : u2;
-#pragma unroll
-          for (int t1 = 0; t1 < 16; ++t1) {
-            const int tau = t2 + 3 * t1;
-            sm[slot(t0, tau & 15, 16 * (tau >> 4) + k2)] = (t2 == 0 && t1 == 0) ? g[0] : cmul(g[t1], tw);
-            tw = cmul(tw, u3);
-          }
+        for (int t1 = 0; t1 < 16; ++t1) {
+          const int tau = t2 + 3 * t1;
+          sm[slot(t0, tau & 15, 16 * (tau >> 4) + k2)] = (t2 == 0 && t1 == 0) ? g[0] : cmul(g[t1], tw);
+          tw = cmul(tw, u3);
         }
-      } else if (zs_ready) {  // warps 8-11: the next band-limited pair's table
-        const double2* an = specA + static_cast<int64_t>(next_ia) * (N + 1);
-        const int64_t ob = static_cast<int64_t>(next_jb & ~kPrunedBit) * (N + 1);
-        const void* bn = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + ob)
-                               : static_cast<const void*>(static_cast<const double2*>(specB) + ob);
-        double2* zsn = zs + kZsLen * ((wi + 1) & 1);
-        zs_job<BREAL>(tid - 256, an, bn, wM, zsn);
-        if (tid - 256 + 128 < kBand) zs_job<BREAL>(tid - 256 + 128, an, bn, wM, zsn);
+      };
+      if (tid < 256) {  // warps 0-7: passes 0 and 1 of their own (t0, k2)
+        m_pass(std::integral_constant<int, 0>{}, tid, tbase);
+        m_pass(std::integral_constant<int, 1>{}, tid, tbase);
+      } else {  // warps 8-11: the next band-limited pair's table, then pass 2 of the two M threads in this lane
+        if (zs_ready) {
+          const double2* an = specA + static_cast<int64_t>(next_ia) * (N + 1);
+          const int64_t ob = static_cast<int64_t>(next_jb & ~kPrunedBit) * (N + 1);
+          const void* bn = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + ob)
+                                 : static_cast<const void*>(static_cast<const double2*>(specB) + ob);
+          double2* zsn = zs + kZsLen * ((wi + 1) & 1);
+          zs_job<BREAL>(tid - 256, an, bn, wM, zsn);
+          if (tid - 256 + 128 < kBand) zs_job<BREAL>(tid - 256 + 128, an, bn, wM, zsn);
+        }
+        m_pass(std::integral_constant<int, 2>{}, tid - 256, tbase - 256);
+        m_pass(std::integral_constant<int, 2>{}, tid - 128, tbase - 128);
       }
       ia_cur = -1;  // the parked values overwrote the density spectrum's columns
       if (zs_ready) {
