@@ -567,18 +567,36 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
       zs_ready = has_next && (next_jb & kPrunedBit);
       // ---- M: the 48-point transforms over kk = k2 + 16 c of the M thread tm = (t0, k2); pass t2
       // gives the outputs tau = t2 + 3 t1 from the y values parked at tensor-memory column ycol
-      auto m_pass = [&](auto T2, int tm, uint32_t ycol) {
+      // (tensor memory reads at 64 B/clk per SM: the 18 values are read ONCE per thread and serve
+      // both of its passes from registers)
+      auto load_y = [&](uint32_t ycol, double2* y) {
+        uint32_t r[16];
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          tmem_ld16(ycol + 16 * ch, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            y[4 * ch + q] = make_double2(__hiloint2double(r[4 * q + 1], r[4 * q]), __hiloint2double(r[4 * q + 3], r[4 * q + 2]));
+        }
+        tmem_ld4(ycol + 64, r);
+        tmem_ld4(ycol + 68, r + 4);
+        tmem_wait_ld();
+        y[16] = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+        y[17] = make_double2(__hiloint2double(r[5], r[4]), __hiloint2double(r[7], r[6]));
+      };
+      auto m_pass = [&](auto T2, int tm, const double2* y) {
         constexpr int t2 = decltype(T2)::value;
         const int k2 = tm & 15, t0 = tm >> 4;
         double2 g[16];
-        auto take = [&](int idx, const uint32_t* r) {  // idx = c + 9
-          const double2 y = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+#pragma unroll
+        for (int idx = 0; idx < 18; ++idx) {  // idx = c + 9
           if (idx < 9) {  // c < 0: s2 = 2, s1 = c + 16
             const int s1 = idx + 7;
-            g[s1] = mulw48(y, (s1 + 32) * t2);
+            g[s1] = mulw48(y[idx], (s1 + 32) * t2);
           } else {  // c >= 0: s2 = 0, s1 = c
             const int s1 = idx - 9;
-            const double2 v = mulw48(y, s1 * t2);
+            const double2 v = mulw48(y[idx], s1 * t2);
             if (s1 >= 7) {
               g[s1].x += v.x;
               g[s1].y += v.y;
@@ -586,28 +604,6 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
               g[s1] = v;
             }
           }
-        };
-        {
-          uint32_t ra[16], rb[16];
-          tmem_ld16(ycol, ra);
-          tmem_ld16(ycol + 16, rb);
-          tmem_wait_ld();
-#pragma unroll
-          for (int q = 0; q < 4; ++q) take(q, ra + 4 * q);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) take(4 + q, rb + 4 * q);
-          tmem_ld16(ycol + 32, ra);
-          tmem_ld16(ycol + 48, rb);
-          tmem_wait_ld();
-#pragma unroll
-          for (int q = 0; q < 4; ++q) take(8 + q, ra + 4 * q);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) take(12 + q, rb + 4 * q);
-          tmem_ld4(ycol + 64, ra);
-          tmem_ld4(ycol + 68, ra + 4);
-          tmem_wait_ld();
-          take(16, ra);
-          take(17, ra + 4);
         }
         dft<16, 1>(g);
         const double2 u1 = ext[kExt768 + k2];                // w_768^{k2}
@@ -621,8 +617,10 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
         }
       };
       if (tid < 256) {  // warps 0-7: passes 0 and 1 of their own (t0, k2)
-        m_pass(std::integral_constant<int, 0>{}, tid, tbase);
-        m_pass(std::integral_constant<int, 1>{}, tid, tbase);
+        double2 y[18];
+        load_y(tbase, y);
+        m_pass(std::integral_constant<int, 0>{}, tid, y);
+        m_pass(std::integral_constant<int, 1>{}, tid, y);
       } else {  // warps 8-11: the next band-limited pair's table, then pass 2 of the two M threads in this lane
         if (zs_ready) {
           const double2* an = specA + static_cast<int64_t>(next_ia) * (N + 1);
@@ -633,8 +631,11 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
           zs_job<BREAL>(tid - 256, an, bn, wM, zsn);
           if (tid - 256 + 128 < kBand) zs_job<BREAL>(tid - 256 + 128, an, bn, wM, zsn);
         }
-        m_pass(std::integral_constant<int, 2>{}, tid - 256, tbase - 256);
-        m_pass(std::integral_constant<int, 2>{}, tid - 128, tbase - 128);
+        double2 y[18];
+        load_y(tbase - 256, y);
+        m_pass(std::integral_constant<int, 2>{}, tid - 256, y);
+        load_y(tbase - 128, y);
+        m_pass(std::integral_constant<int, 2>{}, tid - 128, y);
       }
       ia_cur = -1;  // the parked values overwrote the density spectrum's columns
       if (zs_ready) {
@@ -644,6 +645,10 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
         __syncthreads();
         c2 = phase ? clock64() : 0;
         if (tid < 256) park_y(zs + kZsLen * ((wi + 1) & 1));
+        if (phase && tid == 0) {  // (analysis: the parking alone, and the band-limited pairs' count)
+          atomicAdd(phase + 5, static_cast<unsigned long long>(clock64() - c2));
+          atomicAdd(phase + 6, 1ULL);
+        }
       }
     } else {
       zs_ready = false;
@@ -1325,6 +1330,7 @@ void k12_pairs(tgb_ctx* ctx, int64_t n, int naxes, double2* const* specA, double
     unsigned long long hb[8];
     TGB_CUDA(cudaStreamSynchronize(ctx->stream));
     TGB_CUDA(cudaMemcpy(hb, phase, sizeof(hb), cudaMemcpyDeviceToHost));
+    if (hb[6]) fprintf(stderr, "k12 band-limited pairs with a successor: %llu, y parking %.0f cycles\n", hb[6], double(hb[5]) / hb[6]);
     if (hb[4])
       fprintf(stderr, "k12 cycles/pair: stage1 %.0f stage2 %.0f stage3 %.0f stage4 %.0f (pairs %llu)\n",
               double(hb[0]) / hb[4], double(hb[1]) / hb[4], double(hb[2]) / hb[4], double(hb[3]) / hb[4], hb[4]);

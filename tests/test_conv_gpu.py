@@ -86,7 +86,8 @@ def test_k12_plan_many_pairs_per_cta(ctx):
         assert np.array_equal(c.factor[ax][:, 0:ra], c.factor[ax][:, ra:2 * ra])
 
 
-def test_k12_band_limited_pairs(ctx, monkeypatch):
+@pytest.mark.parametrize("ra", [64, 7])
+def test_k12_band_limited_pairs(ctx, monkeypatch, ra):
     """Band-limited kernel columns (spectrum below 2^-46 of its peak beyond k = 144: smooth
     Gaussians, the Newton kernel's mid-range terms) take the pruned path of k12_pair_kernel
     (Zs table + merged 48-point stage, fftconv12k.cu); the others the full stages 1-3.  Kernel
@@ -94,8 +95,9 @@ def test_k12_band_limited_pairs(ctx, monkeypatch):
     runs several band-limited pairs back to back (table and y values formed one pair ahead):
     off-centre Gaussians (non-symmetric: complex spectra on axis 0), centred ones (real spectra
     on axis 1), a box-truncated wide Gaussian, a spike, a zero column.  Against the oracle
-    (proj/src/fft.cpp:97-122) and against the same call with the pruning switched off."""
-    n, ra = 16385, 64
+    (proj/src/fft.cpp:97-122) and against the same call with the pruning switched off.
+    ra = 64: aligned (one-sample-delayed) window stores; ra = 7: the unshifted store path."""
+    n = 16385
     rng = Rng(777)
     fa = [np.asfortranarray(rng.normal(n * ra).reshape(n, ra, order="F")) for _ in range(3)]
     a = CanonicalTensor3(fa, rng.normal(ra))
@@ -120,7 +122,7 @@ def test_k12_band_limited_pairs(ctx, monkeypatch):
             blk = c.factor[ax][:, ra * j:ra * (j + 1)]
             scale = np.abs(cfull.factor[ax][:, ra * j:ra * (j + 1)]).max()
             assert np.abs(blk - cfull.factor[ax][:, ra * j:ra * (j + 1)]).max() <= 1e-12 * max(scale, 1e-300), (ax, j)
-        for i in (0, 1, 31, 62, 63):
+        for i in sorted({0, 1, ra // 2, ra - 2, ra - 1}):
             for j in range(rb):
                 ref = O.conv_central_many(np.asfortranarray(fa[ax][:, [i]]), np.ascontiguousarray(fb[ax][:, j]))[:, 0]
                 assert relmax(c.factor[ax][:, i + ra * j], h[ax] * ref) <= TOL, (ax, i, j)
