@@ -191,6 +191,17 @@ __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double
 //       g[s1] = w_48^{s1 t2} y[s1] + w_48^{(s1 + 32) t2} y[s1 - 16],   X[tau] = w_768^{k2 tau} dft16(g)[t1]
 //     written where stage 4 expects them.  No shared-memory reads of transform data, one pass of
 //     writes, two CTA barriers fewer than the full stages 1-3.
+// Schedule of a run of such pairs: the table and the y values of pair w + 1 are formed during pair
+// w - the table by warps 8-11 at the head of the M stage, the y values by the M threads (warps
+// 0-7) between the M stage and stage 4, i.e. BEFORE pair w's window stores enter the load/store
+// unit, so that pair w + 1 starts from tensor memory and FP64 arithmetic while those stores wait
+// for the egress.  The three passes are spread over all 12 warps: an M thread runs t2 = 0, 1 for
+// its own (t0, k2), and the thread of warps 8-11 in the same tensor-memory lane quarter runs
+// t2 = 2 for the two M threads (warp q and warp 4 + q) whose parked values it can read.  The first
+// band-limited pair after a full pair (or a refill of the entry table) forms both in line.
+// A band-limited pair overwrites the density spectrum's tensor-memory columns and does not need
+// them (its 144 entries come from L2), so the fill happens at the first FULL pair of a density
+// column (the work lists are i-major: one fill per column either way).
 constexpr int kBand = 144;
 constexpr int kChunk = 192;            // work entries staged in shared memory at a time (k12_pair_run)
 constexpr int kPrunedBit = 1 << 30;  // in a staged entry's jb: band-limited kernel column
