@@ -202,7 +202,8 @@ __device__ __forceinline__ void stage3(double2* sm, int tid, double2 w31, double
 // A band-limited pair overwrites the density spectrum's tensor-memory columns and does not need
 // them (its 144 entries come from L2), so the fill happens at the first FULL pair of a density
 // column (the work lists are i-major: one fill per column either way).
-constexpr int kBand = 144;
+constexpr int kBand = 144;       // a multiple of 16, <= 144 (kZsLen; M-stage value count 2 kC <= 18); 128 measured alike
+constexpr int kC = kBand / 16;   // live values c = -kC..kC-1 of the 48-point transform
 constexpr int kChunk = 192;            // work entries staged in shared memory at a time (k12_pair_run)
 constexpr int kPrunedBit = 1 << 30;  // in a staged entry's jb: band-limited kernel column
 // shared memory behind the transform slots, in double2 units (k12_pair_kernel fills the tables)
@@ -449,7 +450,7 @@ __device__ __forceinline__ void zs_job(int f, const double2* __restrict__ a, con
   if (f > 0)
     zs[kBand + f] = zq;
   else
-    zs[2 * kBand] = make_double2(0.0, 0.0);  // f = -kBand: read by (k2 = 0, c = -9), holds no data
+    zs[2 * kBand] = make_double2(0.0, 0.0);  // f = -kBand: read by (k2 = 0, c = -kC), holds no data
 }
 
 // Stage-1 item of thread tid.  Regular (tid < 383): block kk = tid + 1 and its
@@ -541,21 +542,21 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
       // Normally formed by warps 8-11 during the PREVIOUS pair's M stage; here only for the
       // first band-limited pair after a full one or a refill of the entry table.
       double2* zsc = zs + kZsLen * (wi & 1);
-      // y[c] = Zs[k2 + 16 c] w_N^{(k2 + 16 c) t0} of the thread's (t0, k2) -> tensor-memory columns 4 (c + 9)
+      // y[c] = Zs[k2 + 16 c] w_N^{(k2 + 16 c) t0} of the thread's (t0, k2) -> tensor-memory columns 4 (c + kC)
       auto park_y = [&](const double2* zt) {  // warps 0-7
         const int k2 = tid & 15, t0 = tid >> 4;
         const double2 base = ext[kExtBase + tid], step = ext[kExt768 + t0];
         double2 tw = base;
 #pragma unroll
-        for (int c = 0; c < 9; ++c) {
-          tmem_st4(tbase + 4 * (c + 9), cmul(zt[k2 + 16 * c], tw));
+        for (int c = 0; c < kC; ++c) {
+          tmem_st4(tbase + 4 * (c + kC), cmul(zt[k2 + 16 * c], tw));
           tw = cmul(tw, step);
         }
         const double2 sc = cconj(step);
         tw = cmul(base, sc);
 #pragma unroll
-        for (int m = 1; m <= 9; ++m) {
-          tmem_st4(tbase + 4 * (9 - m), cmul(zt[kBand + 16 * m - k2], tw));
+        for (int m = 1; m <= kC; ++m) {
+          tmem_st4(tbase + 4 * (kC - m), cmul(zt[kBand + 16 * m - k2], tw));
           tw = cmul(tw, sc);
         }
         tmem_wait_st();
@@ -590,25 +591,27 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
           for (int q = 0; q < 4; ++q)
             y[4 * ch + q] = make_double2(__hiloint2double(r[4 * q + 1], r[4 * q]), __hiloint2double(r[4 * q + 3], r[4 * q + 2]));
         }
-        tmem_ld4(ycol + 64, r);
-        tmem_ld4(ycol + 68, r + 4);
-        tmem_wait_ld();
-        y[16] = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
-        y[17] = make_double2(__hiloint2double(r[5], r[4]), __hiloint2double(r[7], r[6]));
+        if (kC == 9) {
+          tmem_ld4(ycol + 64, r);
+          tmem_ld4(ycol + 68, r + 4);
+          tmem_wait_ld();
+          y[16] = make_double2(__hiloint2double(r[1], r[0]), __hiloint2double(r[3], r[2]));
+          y[17] = make_double2(__hiloint2double(r[5], r[4]), __hiloint2double(r[7], r[6]));
+        }
       };
       auto m_pass = [&](auto T2, int tm, const double2* y) {
         constexpr int t2 = decltype(T2)::value;
         const int k2 = tm & 15, t0 = tm >> 4;
         double2 g[16];
 #pragma unroll
-        for (int idx = 0; idx < 18; ++idx) {  // idx = c + 9
-          if (idx < 9) {  // c < 0: s2 = 2, s1 = c + 16
-            const int s1 = idx + 7;
+        for (int idx = 0; idx < 2 * kC; ++idx) {  // idx = c + kC
+          if (idx < kC) {  // c < 0: s2 = 2, s1 = c + 16
+            const int s1 = idx - kC + 16;
             g[s1] = mulw48(y[idx], (s1 + 32) * t2);
           } else {  // c >= 0: s2 = 0, s1 = c
-            const int s1 = idx - 9;
+            const int s1 = idx - kC;
             const double2 v = mulw48(y[idx], s1 * t2);
-            if (s1 >= 7) {
+            if (s1 >= 16 - kC) {  // (kC = 9 only: s1 = 7, 8 carry a value of either sign of c)
               g[s1].x += v.x;
               g[s1].y += v.y;
             } else {
