@@ -817,21 +817,6 @@ __device__ __forceinline__ void k12_pair_run(double2* sm, uint32_t tbase, const 
       __syncthreads();
       c2 = phase ? clock64() : 0;
     }
-    // the band-limited pair whose table is formed next (during the next pair's M stage after a
-    // band-limited pair, else at the next pair's start): bring its spectrum lines into L1 now
-    {
-      const int ahead = pruned ? 2 : 1;
-      if (w + ahead < w1 && wi + ahead < kChunk && tid < kBand) {
-        const PairEntry en = tab[wi + ahead];
-        if (en.jb & kPrunedBit) {
-          const int64_t o = static_cast<int64_t>(en.jb & ~kPrunedBit) * (N + 1) + tid;
-          const void* pb = BREAL ? static_cast<const void*>(static_cast<const double*>(specB) + o)
-                                 : static_cast<const void*>(static_cast<const double2*>(specB) + o);
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(pb));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(specA + static_cast<int64_t>(en.ia) * (N + 1) + tid));
-        }
-      }
-    }
     if (!pruned) stage3<1>(sm, tid, ext[kExt48 + (tid & 15)], ext[kExt48sq + (tid & 15)]);
     if (!(pruned && zs_ready)) __syncthreads();  // (that path met at the barrier behind its M stage)
     c3 = phase ? clock64() : 0;
